@@ -1,0 +1,217 @@
+/*
+ * nexel_b200.h — C-ABI of the B200 (sm_100a) Nexel render path.
+ *
+ * This is the drop-in boundary for the reference's render hot path
+ * (reference: /root/reference/proj/core, namespace nexel):
+ *
+ *   reference C++ entry point                         C-ABI replacement
+ *   ------------------------------------------------  -------------------------------------
+ *   collection_pass(Scene, Camera, RenderResult&)      nx_collection_pass
+ *       include/nexel/renderer.hpp:22, src/renderer.cpp:115-171
+ *   texturing_pass(Scene, Camera, FrameBuffers&)       nx_texturing_pass
+ *       include/nexel/renderer.hpp:26, src/renderer.cpp:207-237
+ *   render(Scene, Camera) -> RenderResult              nx_render (+ nx_frame_download)
+ *       include/nexel/renderer.hpp:28, src/renderer.cpp:239-244
+ *   Scene / RenderSettings / TextureField (scene.hpp:10-32,
+ *       texture_field.hpp:16-25, hash_grid.hpp:39-66, mlp.hpp:11-33)
+ *                                                      nx_scene_create (device-resident copy)
+ *   FrameBuffers / RenderResult (framebuffers.hpp:61-86,
+ *       renderer.hpp:11-16)                            nx_frame_* (device-resident buffers)
+ *   nexel::Error{code,msg} (error.hpp:10-22)           int status codes + nx_ctx_last_error
+ *       "bad-settings"  renderer.cpp:13-21  -> NX_BAD_SETTINGS
+ *       "bad-camera"    camera.cpp:8-31     -> NX_BAD_CAMERA
+ *       "bad-primitive" primitive.cpp:47-63 -> NX_BAD_PRIMITIVE
+ *
+ * Conventions: every function returns NX_OK (0) or an NX_* code; on failure the
+ * message is available from nx_ctx_last_error(). Exceptions never cross this
+ * boundary. Host arrays use the reference's in-memory layouts (doubles, row-major
+ * [out][in] MLP weights, [level][row][feature] hash table, 60 doubles per Nexel in
+ * field order). `stream` arguments are cudaStream_t passed as void* (NULL = the
+ * context's own stream). A context is bound to one device and one host thread.
+ */
+#ifndef NEXEL_B200_H
+#define NEXEL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NX_OK 0
+#define NX_BAD_SETTINGS 1    /* "bad-settings"  (renderer.cpp:13-21) */
+#define NX_BAD_CAMERA 2      /* "bad-camera"    (camera.cpp:8-31)    */
+#define NX_BAD_PRIMITIVE 3   /* "bad-primitive" (primitive.cpp:47-63) */
+#define NX_INVALID_ARGUMENT 10
+#define NX_UNSUPPORTED 11
+#define NX_OUT_OF_MEMORY 12
+#define NX_CUDA_ERROR 13
+#define NX_NO_DEVICE 14
+
+#define NX_MAX_TOP_K 8          /* kMaxTopK, scene.hpp:23 */
+#define NX_PARAMS_PER_NEXEL 60  /* kParamsPerPrimitive, primitive.hpp:14 */
+#define NX_SH_VALUES 48         /* kShValues, primitive.hpp:12 */
+
+typedef struct nx_ctx nx_ctx;
+typedef struct nx_scene nx_scene;
+typedef struct nx_frame nx_frame;
+
+/* RenderSettings (scene.hpp:10-21). Booleans are 0/1. */
+typedef struct nx_settings {
+    int32_t top_k;              /* 0..8; 0 disables the texture pass */
+    int32_t tile;               /* >= 1; the CUDA path supports tile <= 32 */
+    double background[3];
+    double near_eps;            /* default 1e-3 */
+    double alpha_max;           /* default 0.999 */
+    double min_transmittance;   /* default 1e-4 */
+    int32_t no_gamma;
+    int32_t no_prim_sh;
+    int32_t no_downweight;
+    int32_t reserved;
+} nx_settings;
+
+/* HashGridConfig (hash_grid.hpp:39-56) + TextureMlp shapes (mlp.hpp:11-33). */
+typedef struct nx_field_desc {
+    int32_t levels;       /* 16 */
+    int32_t log2_table;   /* 20 */
+    int32_t features;     /* 2 */
+    int32_t n_hidden;     /* 64; n_in = levels*features, n_out = 48 */
+    double base_scale;    /* 1/extent */
+    double growth;        /* 32768^(1/(levels-1)) */
+} nx_field_desc;
+
+/* Camera (camera.hpp:17-43): pinhole, OpenCV axes, X_cam = R X_world + t. */
+typedef struct nx_camera {
+    int32_t width, height;
+    double fx, fy, cx, cy;
+    double R[9];   /* row-major */
+    double t[3];
+} nx_camera;
+
+/* Device-resident frame buffers (FrameBuffers, framebuffers.hpp:61-86).
+ * Slot layout is pixel-major, slot-minor like the reference: slot = pix*K + j.
+ * Types: decisions and contributor data stay fp64 (depths, weights); colour
+ * buffers are fp32 (tolerance-checked). */
+typedef struct nx_frame_view {
+    int32_t width, height, top_k, tiles_x, tiles_y;
+    float* base;          /* H*W*3 */
+    int32_t* ids;         /* H*W*K, -1 sentinel */
+    double* depths;       /* H*W*K */
+    double* weights;      /* H*W*K */
+    float* texture;       /* H*W*K*3 */
+    float* final_img;     /* H*W*3 */
+    float* residual;      /* H*W */
+} nx_frame_view;
+
+/* Host destination for nx_frame_download; any pointer may be NULL (skipped). */
+typedef struct nx_host_frame {
+    float* base;
+    int32_t* ids;
+    double* depths;
+    double* weights;
+    float* texture;
+    float* final_img;
+    float* residual;
+} nx_host_frame;
+
+/* Per-frame binning / work statistics (read back with nx_frame_stats). */
+typedef struct nx_frame_stats {
+    int64_t n_nexels;
+    int64_t n_entries;        /* primitives with a binning entry (renderer.cpp:100) */
+    int64_t n_dropped_support;/* ru<=0 or rv<=0 (renderer.cpp:54-56) */
+    int64_t n_behind;         /* fully behind the pinhole (renderer.cpp:77) */
+    int64_t n_offscreen;      /* rect off screen (renderer.cpp:88) */
+    int64_t n_rect;           /* rect-binned */
+    int64_t n_straddlers;     /* all-tile fallback (renderer.cpp:93-98) */
+    int64_t n_straddlers_kept;/* straddlers whose refined work rect is non-empty */
+    int64_t tile_keys;        /* reference tile-key count P (sum of tile-list lengths) */
+    int64_t work_keys;        /* keys materialised and walked by the composite kernel */
+    int64_t n_queries;        /* texture queries Q (non-empty slots) */
+} nx_frame_stats;
+
+/* ---- context ---------------------------------------------------------- */
+const char* nx_version(void);
+const char* nx_status_name(int status);            /* "bad-settings", ... */
+int nx_device_count(int* count);
+int nx_ctx_create(int device, nx_ctx** out);
+void nx_ctx_destroy(nx_ctx* ctx);
+const char* nx_ctx_last_error(const nx_ctx* ctx, int* status);
+void* nx_ctx_stream(nx_ctx* ctx);                  /* the context's own stream */
+int nx_ctx_synchronize(nx_ctx* ctx);
+
+/* Stage timing (CUDA events recorded between the stages of each frame). */
+#define NX_STAGE_PREPROCESS 0
+#define NX_STAGE_DEPTH_SORT 1
+#define NX_STAGE_EMIT 2
+#define NX_STAGE_TILE_SORT 3
+#define NX_STAGE_COMPOSITE 4
+#define NX_STAGE_TEXTURE 5
+#define NX_NUM_STAGES 6
+int nx_ctx_set_profiling(nx_ctx* ctx, int enable);
+int nx_ctx_stage_times(nx_ctx* ctx, float* ms, int n);  /* last frame; synchronises */
+const char* nx_stage_name(int stage);
+
+/* ---- scene (Scene, scene.hpp:25-32) ----------------------------------- */
+/* nexels: n*60 doubles in Nexel field order (primitive.hpp:21-28): mu[3],
+ * quat[4] (w,x,y,z), log_scale[2], opacity_raw, gamma_raw[2], sh[48].
+ * table: levels * 2^log2_table * features doubles; w1 [hidden][levels*features],
+ * w2 [hidden][hidden], w3 [48][hidden]. Validation of the primitives follows
+ * activate() (primitive.cpp:47-63); a failure is recorded and reported by the
+ * render calls (after settings/camera validation, as in collection_pass). */
+int nx_scene_create(nx_ctx* ctx, const nx_settings* settings, int64_t n_nexels,
+                    const double* nexels, const nx_field_desc* field, const double* table,
+                    const double* w1, const double* w2, const double* w3, nx_scene** out);
+int nx_scene_set_settings(nx_ctx* ctx, nx_scene* scene, const nx_settings* settings);
+int nx_scene_get_settings(const nx_scene* scene, nx_settings* out);
+void nx_scene_destroy(nx_scene* scene);
+
+/* ---- frames (FrameBuffers) -------------------------------------------- */
+int nx_frame_create(nx_ctx* ctx, int width, int height, int top_k, nx_frame** out);
+void nx_frame_destroy(nx_frame* frame);
+int nx_frame_view_get(const nx_frame* frame, nx_frame_view* out);
+/* Async device->host copy on `stream`; pinned destinations overlap with compute. */
+int nx_frame_download(nx_ctx* ctx, const nx_frame* frame, const nx_host_frame* dst, void* stream);
+int nx_frame_stats_get(nx_ctx* ctx, const nx_frame* frame, nx_frame_stats* out); /* synchronises */
+
+/* ---- the render path --------------------------------------------------- */
+/* collection_pass: binning, global (depth,id) order, front-to-back compositing with
+ * early termination and top-K (renderer.cpp:115-171). The frame is (re)shaped to
+ * the camera size and settings.top_k like FrameBuffers::allocate. */
+int nx_collection_pass(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam,
+                       nx_frame* frame, void* stream);
+/* texturing_pass: field queries at the buffered crossings + Eq. 7 composite
+ * (renderer.cpp:207-237). Consumes the frame's ids/depths/weights/base. */
+int nx_texturing_pass(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam,
+                      nx_frame* frame, void* stream);
+/* render = collection_pass + texturing_pass (renderer.cpp:239-244). */
+int nx_render(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam, nx_frame* frame,
+              void* stream);
+
+/* ---- parity / debug (not on the timed path) ---------------------------- */
+/* Tile lists for `cam`: reference_lists=1 materialises the reference's lists
+ * (Binning::tile_lists, renderer.cpp:102-110, straddlers in every tile);
+ * reference_lists=0 returns the work lists the composite kernel walks.
+ * offsets: n_tiles+1 host ints; ids: `capacity` host ints; *total = keys. */
+int nx_debug_tile_lists(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam,
+                        int reference_lists, int64_t* offsets, int32_t* ids,
+                        int64_t capacity, int64_t* total, int32_t* tiles_x, int32_t* tiles_y);
+/* Per-pixel contributor sequences (ids of every hit composited, in order, up to
+ * termination) for image rows [y0, y1): hits[(row*W+x)*max_hits + i], counts[...]. */
+int nx_debug_pixel_hits(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam, int y0,
+                        int y1, int max_hits, int32_t* hits, int32_t* counts);
+
+/* ---- synthetic inputs -------------------- */
+/* stump_like(N, c, seed, R_ground): fills nexels (n*60), settings and field desc;
+ * table/w1/w2/w3 may be NULL to query sizes only (field desc is always filled). */
+int nx_synth_stump_like(int64_t n, double coverage, uint64_t seed, double ground_radius,
+                        int32_t log2_table, double grid_init, uint64_t field_seed,
+                        double* nexels, nx_settings* settings, nx_field_desc* field,
+                        double* table, double* w1, double* w2, double* w3);
+int nx_synth_ring_camera(int index, int n_views, int width, int height, nx_camera* out);
+void nx_settings_default(nx_settings* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NEXEL_B200_H */

@@ -1,0 +1,18 @@
+"""B200-native (sm_100a) render path of Nexels (arXiv 2512.13796).
+
+Drop-in for the reference's ``nexel::render`` / ``collection_pass`` /
+``texturing_pass`` (proj/core/include/nexel/renderer.hpp). The compute runs in
+``libnexel_b200.so`` (hand-written CUDA for sm_100a behind the C-ABI in
+``include/nexel_b200.h``); this package is the host-side mirror of the
+reference interface.
+"""
+from .api import (Camera, DeviceFrame, DeviceScene, FrameBuffers, HashGridConfig, NexelError, RenderResult,
+                  RenderSettings, Renderer, Scene, TextureField, collection_pass, render, ring_camera, stump_like,
+                  texturing_pass)
+from . import _abi
+
+__all__ = [
+    "Camera", "DeviceFrame", "DeviceScene", "FrameBuffers", "HashGridConfig", "NexelError", "RenderResult",
+    "RenderSettings", "Renderer", "Scene", "TextureField", "collection_pass", "render", "ring_camera",
+    "stump_like", "texturing_pass", "_abi",
+]

@@ -1,0 +1,472 @@
+"""Python mirror of the reference render interface (nexel::render & co).
+
+Same names, argument meaning and error behaviour as the reference's
+``proj/core/include/nexel/renderer.hpp`` (render / collection_pass /
+texturing_pass), ``scene.hpp`` (RenderSettings, Scene), ``camera.hpp``
+(Camera), ``framebuffers.hpp`` (FrameBuffers) and ``error.hpp`` (Error with a
+machine-readable code). Every call runs on the sm_100a library through the
+C-ABI (include/nexel_b200.h); nothing here computes pixels.
+
+Two layers:
+  * ``Renderer`` — device-resident API: upload a Scene once, render cameras into
+    device frames, download explicitly (what the benchmark times);
+  * ``render`` / ``collection_pass`` / ``texturing_pass`` — the reference's
+    value-semantics API returning host FrameBuffers (fp64 like the reference).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import hashlib
+import math
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+
+
+class NexelError(RuntimeError):
+    """nexel::Error (error.hpp:10-22): ``code`` is "bad-settings", "bad-camera",
+    "bad-primitive", or a boundary code ("cuda-error", "unsupported", ...)."""
+
+    def __init__(self, code: str, message: str):
+        super().__init__(message)
+        self.code = code
+
+    def __str__(self):
+        return f"{self.code}: {self.args[0]}"
+
+
+@dataclasses.dataclass
+class RenderSettings:
+    """RenderSettings (scene.hpp:10-21)."""
+    top_k: int = 2
+    background: Sequence[float] = (0.0, 0.0, 0.0)
+    near_eps: float = 1e-3
+    alpha_max: float = 0.999
+    min_transmittance: float = 1e-4
+    tile: int = 16
+    no_gamma: bool = False
+    no_prim_sh: bool = False
+    no_downweight: bool = False
+
+    def to_c(self) -> _abi.nx_settings:
+        s = _abi.nx_settings()
+        s.top_k = int(self.top_k)
+        s.tile = int(self.tile)
+        for i in range(3):
+            s.background[i] = float(self.background[i])
+        s.near_eps = float(self.near_eps)
+        s.alpha_max = float(self.alpha_max)
+        s.min_transmittance = float(self.min_transmittance)
+        s.no_gamma = int(bool(self.no_gamma))
+        s.no_prim_sh = int(bool(self.no_prim_sh))
+        s.no_downweight = int(bool(self.no_downweight))
+        return s
+
+    @classmethod
+    def from_c(cls, s: _abi.nx_settings) -> "RenderSettings":
+        return cls(top_k=s.top_k, background=tuple(s.background), near_eps=s.near_eps, alpha_max=s.alpha_max,
+                   min_transmittance=s.min_transmittance, tile=s.tile, no_gamma=bool(s.no_gamma),
+                   no_prim_sh=bool(s.no_prim_sh), no_downweight=bool(s.no_downweight))
+
+
+@dataclasses.dataclass
+class HashGridConfig:
+    """HashGridConfig (hash_grid.hpp:39-56)."""
+    levels: int = 16
+    log2_table: int = 20
+    features: int = 2
+    base_scale: float = 1.0
+    growth: float = 2.0
+
+    @classmethod
+    def for_extent(cls, extent: float, levels: int = 16, log2_table: int = 20, features: int = 2):
+        """HashGridConfig::for_extent (hash_grid.cpp:15-24)."""
+        growth = math.pow(32768.0, 1.0 / (levels - 1)) if levels > 1 else 1.0
+        return cls(levels, log2_table, features, 1.0 / extent, growth)
+
+    def table_size(self) -> int:
+        return 1 << self.log2_table
+
+    def param_count(self) -> int:
+        return self.levels * self.table_size() * self.features
+
+
+@dataclasses.dataclass
+class TextureField:
+    """TextureField (texture_field.hpp:16-25): hash grid table [level][row][feature]
+    and the bias-free MLP w1 [hidden][in], w2 [hidden][hidden], w3 [48][hidden]."""
+    grid: HashGridConfig
+    table: np.ndarray
+    w1: np.ndarray
+    w2: np.ndarray
+    w3: np.ndarray
+    n_hidden: int = 64
+
+    def desc(self) -> _abi.nx_field_desc:
+        d = _abi.nx_field_desc()
+        d.levels = self.grid.levels
+        d.log2_table = self.grid.log2_table
+        d.features = self.grid.features
+        d.n_hidden = self.n_hidden
+        d.base_scale = self.grid.base_scale
+        d.growth = self.grid.growth
+        return d
+
+
+@dataclasses.dataclass
+class Scene:
+    """Scene (scene.hpp:25-32): ``nexels`` is (N, 60) float64 in Nexel field order
+    (primitive.hpp:21-28): mu[3], quat[4] (w,x,y,z), log_scale[2], opacity_raw,
+    gamma_raw[2], sh[48]."""
+    nexels: np.ndarray
+    field: TextureField
+    settings: RenderSettings = dataclasses.field(default_factory=RenderSettings)
+    extent: float = 1.0
+
+    def sh_degree(self) -> int:
+        return 0 if self.settings.no_prim_sh else 3
+
+    def fingerprint(self) -> str:
+        h = hashlib.blake2b(digest_size=16)
+        for a in (self.nexels, self.field.table, self.field.w1, self.field.w2, self.field.w3):
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            h.update(str(a.shape).encode())
+            h.update(a.view(np.uint8).data)
+        h.update(repr(dataclasses.astuple(self.field.grid)).encode())
+        h.update(str(self.field.n_hidden).encode())
+        return h.hexdigest()
+
+
+@dataclasses.dataclass
+class Camera:
+    """Camera (camera.hpp:17-43): pinhole, OpenCV axes, X_cam = R X_world + t."""
+    width: int
+    height: int
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    R: np.ndarray
+    t: np.ndarray
+    name: str = ""
+
+    def to_c(self) -> _abi.nx_camera:
+        c = _abi.nx_camera()
+        c.width, c.height = int(self.width), int(self.height)
+        c.fx, c.fy, c.cx, c.cy = float(self.fx), float(self.fy), float(self.cx), float(self.cy)
+        R = np.asarray(self.R, dtype=np.float64).reshape(9)
+        t = np.asarray(self.t, dtype=np.float64).reshape(3)
+        for i in range(9):
+            c.R[i] = float(R[i])
+        for i in range(3):
+            c.t[i] = float(t[i])
+        return c
+
+    @classmethod
+    def from_c(cls, c: _abi.nx_camera, name: str = "") -> "Camera":
+        return cls(c.width, c.height, c.fx, c.fy, c.cx, c.cy, np.array(c.R[:], dtype=np.float64).reshape(3, 3),
+                   np.array(c.t[:], dtype=np.float64), name)
+
+    def position(self) -> np.ndarray:
+        return -(np.asarray(self.R).T @ np.asarray(self.t))
+
+
+@dataclasses.dataclass
+class FrameBuffers:
+    """FrameBuffers (framebuffers.hpp:61-86); slot layout pixel-major, slot-minor."""
+    width: int
+    height: int
+    top_k: int
+    base: np.ndarray
+    ids: np.ndarray
+    depths: np.ndarray
+    weights: np.ndarray
+    texture: np.ndarray
+    final_img: np.ndarray
+    residual: np.ndarray
+
+    def pixel(self, x: int, y: int) -> int:
+        return y * self.width + x
+
+    def slot(self, pix: int, j: int) -> int:
+        return pix * self.top_k + j
+
+
+@dataclasses.dataclass
+class RenderResult:
+    """RenderResult (renderer.hpp:11-16)."""
+    fb: FrameBuffers
+    blended_error: np.ndarray
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(_abi.PD)
+
+
+class DeviceScene:
+    def __init__(self, renderer: "Renderer", handle: C.c_void_p, n: int):
+        self.renderer = renderer
+        self.handle = handle
+        self.n = n
+
+    def set_settings(self, settings: RenderSettings):
+        s = settings.to_c()
+        self.renderer._check(self.renderer.lib.nx_scene_set_settings(self.renderer.ctx, self.handle, C.byref(s)))
+
+    def close(self):
+        if self.handle:
+            self.renderer.lib.nx_scene_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceFrame:
+    def __init__(self, renderer: "Renderer", handle: C.c_void_p):
+        self.renderer = renderer
+        self.handle = handle
+
+    def view(self) -> _abi.nx_frame_view:
+        v = _abi.nx_frame_view()
+        self.renderer.lib.nx_frame_view_get(self.handle, C.byref(v))
+        return v
+
+    def stats(self) -> dict:
+        st = _abi.nx_frame_stats()
+        self.renderer._check(self.renderer.lib.nx_frame_stats_get(self.renderer.ctx, self.handle, C.byref(st)))
+        return st.as_dict()
+
+    def download(self, fields: Optional[Sequence[str]] = None) -> FrameBuffers:
+        """Synchronous download into fresh numpy arrays (device-native dtypes)."""
+        v = self.view()
+        W, H, K = v.width, v.height, v.top_k
+        out = {
+            "base": np.empty((H * W * 3,), np.float32),
+            "ids": np.empty((H * W * K,), np.int32),
+            "depths": np.empty((H * W * K,), np.float64),
+            "weights": np.empty((H * W * K,), np.float64),
+            "texture": np.empty((H * W * K * 3,), np.float32),
+            "final_img": np.empty((H * W * 3,), np.float32),
+            "residual": np.empty((H * W,), np.float32),
+        }
+        want = set(fields) if fields else set(out)
+        hf = _abi.nx_host_frame()
+        for k, arr in out.items():
+            setattr(hf, k, arr.ctypes.data if k in want else None)
+        r = self.renderer
+        r._check(r.lib.nx_frame_download(r.ctx, self.handle, C.byref(hf), None))
+        r._check(r.lib.nx_ctx_synchronize(r.ctx))
+        return FrameBuffers(W, H, K, **out)
+
+    def close(self):
+        if self.handle:
+            self.renderer.lib.nx_frame_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Renderer:
+    """One CUDA context (device + stream) of the sm_100a render path."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _abi.load()
+        self.ctx = C.c_void_p()
+        st = self.lib.nx_ctx_create(int(device), C.byref(self.ctx))
+        if st != _abi.NX_OK:
+            raise NexelError(_abi.STATUS_CODES.get(st, "error"), f"cannot create a context on cuda:{device}")
+        self.device = device
+
+    def _check(self, status: int):
+        if status != _abi.NX_OK:
+            code = C.c_int()
+            msg = self.lib.nx_ctx_last_error(self.ctx, C.byref(code)).decode()
+            raise NexelError(_abi.STATUS_CODES.get(status, "error"), msg)
+
+    @property
+    def stream(self) -> int:
+        return int(self.lib.nx_ctx_stream(self.ctx) or 0)
+
+    def upload(self, scene: Scene) -> DeviceScene:
+        nex = np.ascontiguousarray(scene.nexels, dtype=np.float64).reshape(-1, _abi.NX_PARAMS_PER_NEXEL)
+        f = scene.field
+        tab = np.ascontiguousarray(f.table, dtype=np.float64)
+        w1 = np.ascontiguousarray(f.w1, dtype=np.float64)
+        w2 = np.ascontiguousarray(f.w2, dtype=np.float64)
+        w3 = np.ascontiguousarray(f.w3, dtype=np.float64)
+        if tab.size != f.grid.param_count():
+            raise NexelError("invalid-argument", "hash table size does not match the grid config")
+        nin = f.grid.levels * f.grid.features
+        if w1.size != f.n_hidden * nin or w2.size != f.n_hidden ** 2 or w3.size != 48 * f.n_hidden:
+            raise NexelError("invalid-argument", "MLP weight shapes do not match the field")
+        s = scene.settings.to_c()
+        d = f.desc()
+        h = C.c_void_p()
+        self._check(self.lib.nx_scene_create(self.ctx, C.byref(s), nex.shape[0], _dp(nex), C.byref(d), _dp(tab),
+                                             _dp(w1), _dp(w2), _dp(w3), C.byref(h)))
+        return DeviceScene(self, h, nex.shape[0])
+
+    def frame(self, width: int = 0, height: int = 0, top_k: int = 0) -> DeviceFrame:
+        h = C.c_void_p()
+        self._check(self.lib.nx_frame_create(self.ctx, width, height, top_k, C.byref(h)))
+        return DeviceFrame(self, h)
+
+    def collection_pass(self, dscene: DeviceScene, cam: Camera, frame: DeviceFrame, stream: int = 0):
+        c = cam.to_c()
+        self._check(self.lib.nx_collection_pass(self.ctx, dscene.handle, C.byref(c), frame.handle, stream or None))
+
+    def texturing_pass(self, dscene: DeviceScene, cam: Camera, frame: DeviceFrame, stream: int = 0):
+        c = cam.to_c()
+        self._check(self.lib.nx_texturing_pass(self.ctx, dscene.handle, C.byref(c), frame.handle, stream or None))
+
+    def render(self, dscene: DeviceScene, cam: Camera, frame: DeviceFrame, stream: int = 0):
+        c = cam.to_c()
+        self._check(self.lib.nx_render(self.ctx, dscene.handle, C.byref(c), frame.handle, stream or None))
+
+    def synchronize(self):
+        self._check(self.lib.nx_ctx_synchronize(self.ctx))
+
+    def set_profiling(self, on: bool):
+        self._check(self.lib.nx_ctx_set_profiling(self.ctx, int(on)))
+
+    def stage_times(self) -> dict:
+        ms = (C.c_float * _abi.NX_NUM_STAGES)()
+        self._check(self.lib.nx_ctx_stage_times(self.ctx, ms, _abi.NX_NUM_STAGES))
+        return {name: float(ms[i]) for i, name in enumerate(_abi.STAGE_NAMES)}
+
+    # ---- parity / debug
+    def tile_lists(self, dscene: DeviceScene, cam: Camera, reference_lists: bool = True):
+        c = cam.to_c()
+        total, tx, ty = C.c_int64(), C.c_int32(), C.c_int32()
+        self._check(self.lib.nx_debug_tile_lists(self.ctx, dscene.handle, C.byref(c), int(reference_lists), None,
+                                                 None, 0, C.byref(total), C.byref(tx), C.byref(ty)))
+        n_tiles = tx.value * ty.value
+        offsets = np.empty(n_tiles + 1, np.int64)
+        ids = np.empty(max(total.value, 1), np.int32)
+        self._check(self.lib.nx_debug_tile_lists(self.ctx, dscene.handle, C.byref(c), int(reference_lists),
+                                                 offsets.ctypes.data_as(_abi.PI64), ids.ctypes.data_as(_abi.PI32),
+                                                 total.value, C.byref(total), C.byref(tx), C.byref(ty)))
+        return offsets, ids[: total.value], tx.value, ty.value
+
+    def pixel_hits(self, dscene: DeviceScene, cam: Camera, y0: int, y1: int, max_hits: int = 64):
+        c = cam.to_c()
+        q = (y1 - y0) * cam.width
+        hits = np.full(q * max_hits, -1, np.int32)
+        counts = np.zeros(q, np.int32)
+        self._check(self.lib.nx_debug_pixel_hits(self.ctx, dscene.handle, C.byref(c), y0, y1, max_hits,
+                                                 hits.ctypes.data_as(_abi.PI32), counts.ctypes.data_as(_abi.PI32)))
+        return hits.reshape(q, max_hits), counts
+
+    def close(self):
+        if self.ctx:
+            self.lib.nx_ctx_destroy(self.ctx)
+            self.ctx = None
+
+
+# ---------------------------------------------------------------- reference-style value API
+_default: dict = {}
+
+
+def _renderer(device: int = 0) -> Renderer:
+    r = _default.get(device)
+    if r is None:
+        r = _default[device] = Renderer(device)
+    return r
+
+
+def _device_scene(r: Renderer, scene: Scene) -> DeviceScene:
+    key = scene.fingerprint()
+    cache = _default.setdefault(("scenes", r.device), {})
+    ds = cache.get(key)
+    if ds is None:
+        cache.clear()
+        ds = cache[key] = r.upload(scene)
+    ds.set_settings(scene.settings)
+    return ds
+
+
+def _to_host_fb(fb: FrameBuffers) -> FrameBuffers:
+    """Device-native dtypes -> the reference's fp64 FrameBuffers."""
+    return FrameBuffers(fb.width, fb.height, fb.top_k, fb.base.astype(np.float64), fb.ids.copy(),
+                        fb.depths.astype(np.float64), fb.weights.astype(np.float64), fb.texture.astype(np.float64),
+                        fb.final_img.astype(np.float64), fb.residual.astype(np.float64))
+
+
+def collection_pass(scene: Scene, cam: Camera, out: RenderResult, device: int = 0) -> None:
+    """collection_pass (renderer.hpp:22): fills base/ids/depths/weights/residual."""
+    r = _renderer(device)
+    ds = _device_scene(r, scene)
+    fr = _default.setdefault(("frame", device), r.frame())
+    r.collection_pass(ds, cam, fr)
+    fb = _to_host_fb(fr.download(["base", "ids", "depths", "weights", "residual"]))
+    npix = cam.width * cam.height
+    fb.texture = np.zeros(npix * scene.settings.top_k * 3)
+    fb.final_img = np.zeros(npix * 3)
+    out.fb = fb
+    out.blended_error = np.zeros(scene.nexels.shape[0])
+
+
+def texturing_pass(scene: Scene, cam: Camera, fb: FrameBuffers, device: int = 0) -> None:
+    """texturing_pass (renderer.hpp:26): consumes fb's ids/depths/weights/base."""
+    r = _renderer(device)
+    ds = _device_scene(r, scene)
+    fr = _default.setdefault(("frame", device), r.frame())
+    v = fr.view()
+    if (v.width, v.height, v.top_k) != (fb.width, fb.height, fb.top_k):
+        raise NexelError("invalid-argument", "FrameBuffers do not come from collection_pass on this camera")
+    r.texturing_pass(ds, cam, fr)
+    d = fr.download(["texture", "final_img"])
+    fb.texture = d.texture.astype(np.float64)
+    fb.final_img = d.final_img.astype(np.float64)
+
+
+def render(scene: Scene, cam: Camera, device: int = 0) -> RenderResult:
+    """render (renderer.hpp:28) = collection_pass + texturing_pass."""
+    r = _renderer(device)
+    ds = _device_scene(r, scene)
+    fr = _default.setdefault(("frame", device), r.frame())
+    r.render(ds, cam, fr)
+    fb = _to_host_fb(fr.download())
+    return RenderResult(fb, np.zeros(scene.nexels.shape[0]))
+
+
+# ---------------------------------------------------------------- synthetic inputs
+def stump_like(n: int, coverage: float = 1.0, seed: int = 2512, ground_radius: float = 4.0,
+               log2_table: int = 20, grid_init: float = 1e-4, field_seed: int = 2513) -> Scene:
+    lib = _abi.load()
+    s = _abi.nx_settings()
+    d = _abi.nx_field_desc()
+    nex = np.empty((n, 60), np.float64)
+    lib.nx_synth_stump_like(n, coverage, seed, ground_radius, log2_table, grid_init, field_seed, None, None,
+                            C.byref(d), None, None, None, None)
+    nin = d.levels * d.features
+    table = np.empty(d.levels * (1 << d.log2_table) * d.features, np.float64)
+    w1 = np.empty(d.n_hidden * nin, np.float64)
+    w2 = np.empty(d.n_hidden * d.n_hidden, np.float64)
+    w3 = np.empty(48 * d.n_hidden, np.float64)
+    st = lib.nx_synth_stump_like(n, coverage, seed, ground_radius, log2_table, grid_init, field_seed, _dp(nex),
+                                 C.byref(s), C.byref(d), _dp(table), _dp(w1), _dp(w2), _dp(w3))
+    if st != _abi.NX_OK:
+        raise NexelError("invalid-argument", "stump_like: bad arguments")
+    grid = HashGridConfig(d.levels, d.log2_table, d.features, d.base_scale, d.growth)
+    return Scene(nex, TextureField(grid, table, w1, w2, w3, d.n_hidden), RenderSettings.from_c(s), extent=8.0)
+
+
+def ring_camera(index: int, n_views: int = 256, width: int = 1920, height: int = 1080) -> Camera:
+    lib = _abi.load()
+    c = _abi.nx_camera()
+    st = lib.nx_synth_ring_camera(index, n_views, width, height, C.byref(c))
+    if st != _abi.NX_OK:
+        raise NexelError("invalid-argument", "ring_camera: bad arguments")
+    return Camera.from_c(c, name=f"ring{index}")

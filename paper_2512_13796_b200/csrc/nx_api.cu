@@ -1,0 +1,739 @@
+// C-ABI of the B200 render path (include/nexel_b200.h) and the per-frame
+// orchestration of the stages:
+//
+//   K1 preprocess ........ activation, projection, classification, rects, records
+//   K2 depth sort ......... compaction + stable LSD radix sort of 64-bit depth keys
+//   K3 emit ............... (tile, id) keys in sorted order + per-tile counts
+//   K4 tile sort .......... stable LSD radix sort by tile -> front-to-back tile lists
+//   K5 tile ranges ........ exclusive scan of per-tile counts
+//   K6 composite .......... per-tile compositing, top-K, Eq. 6 base
+//   K7 texture ............ hash grid + MLP + SH at the buffered crossings, Eq. 7
+//
+// Error behaviour follows the reference (renderer.cpp:116-117): settings are
+// validated first (bad-settings), then the camera (bad-camera), then the
+// primitives (bad-primitive, first failing id, as activate_all would throw).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "nx_internal.cuh"
+#include "nx_sort.cuh"
+
+using namespace nx;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(bytes + bytes / 4, 256);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+const char* kStageNames[NX_NUM_STAGES] = {"preprocess", "depth_sort", "emit", "tile_sort", "composite", "texture"};
+
+}  // namespace
+
+struct nx_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    int err_status = NX_OK;
+    // per-frame scratch (grow-only)
+    DevBuf rec, cls, ref_rect, work_rect, key, flag, pos;
+    DevBuf skeys_a, skeys_b, sids_a, sids_b, counts, offsets;
+    DevBuf tkeys_a, tkeys_b, tvals_a, tvals_b, tile_counts, scratch;
+    DevBuf dbg_hits, dbg_counts;
+    int32_t* h_pinned = nullptr;  // small readbacks
+    bool profiling = false;
+    cudaEvent_t ev[NX_NUM_STAGES + 1] = {};
+    bool ev_valid = false;
+};
+
+struct nx_scene {
+    nx_ctx* ctx = nullptr;
+    int64_t n = 0;
+    DevBuf geom, sh, table, w1, w2, w3;
+    nx_field_desc field{};
+    nx_settings st{};
+    int bad_status = NX_OK;
+    std::string bad_msg;
+};
+
+struct nx_frame {
+    nx_ctx* ctx = nullptr;
+    int W = 0, H = 0, K = 0, tiles_x = 0, tiles_y = 0;
+    DevBuf base, ids, depths, weights, texture, final_img, residual;
+    DevBuf tile_offsets;  // n_tiles + 1 (the work lists' ranges of the last collection pass)
+    DevBuf list_ids;
+    FrameStatsD* stats = nullptr;  // device
+    int64_t n_nexels = 0;
+};
+
+namespace {
+
+int set_err(nx_ctx* c, int status, const std::string& msg) {
+    if (c) {
+        c->err_status = status;
+        c->err = msg;
+    }
+    return status;
+}
+
+int cuda_err(nx_ctx* c, cudaError_t e, const char* what) {
+    return set_err(c, NX_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define NX_CUDA(ctx, expr)                                   \
+    do {                                                     \
+        cudaError_t _e = (expr);                             \
+        if (_e != cudaSuccess) return cuda_err(ctx, _e, #expr); \
+    } while (0)
+
+cudaStream_t pick_stream(nx_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) : c->stream; }
+
+// validate_settings (renderer.cpp:13-21)
+int validate_settings(nx_ctx* c, const nx_settings& s) {
+    if (s.top_k < 0 || s.top_k > NX_MAX_TOP_K)
+        return set_err(c, NX_BAD_SETTINGS, "top_k must be in [0, 8], got " + std::to_string(s.top_k));
+    if (!(s.near_eps > 0)) return set_err(c, NX_BAD_SETTINGS, "near_eps must be positive");
+    if (!(s.alpha_max > 0) || s.alpha_max >= 1) return set_err(c, NX_BAD_SETTINGS, "alpha_max must be in (0,1)");
+    if (!(s.min_transmittance >= 0)) return set_err(c, NX_BAD_SETTINGS, "min_transmittance must be >= 0");
+    if (s.tile < 1) return set_err(c, NX_BAD_SETTINGS, "tile must be >= 1");
+    return NX_OK;
+}
+
+// validate_camera (camera.cpp:8-31)
+int validate_camera(nx_ctx* c, const nx_camera& cam) {
+    auto bad = [&](const char* what) { return set_err(c, NX_BAD_CAMERA, std::string("camera: ") + what); };
+    if (cam.width <= 0 || cam.height <= 0) return bad("non-positive image size");
+    if (!(cam.fx > 0) || !(cam.fy > 0)) return bad("non-positive focal length");
+    for (int i = 0; i < 3; ++i) {
+        if (!std::isfinite(cam.t[i])) return bad("non-finite translation");
+        for (int j = 0; j < 3; ++j)
+            if (!std::isfinite(cam.R[i * 3 + j])) return bad("non-finite rotation");
+    }
+    if (!std::isfinite(cam.cx) || !std::isfinite(cam.cy)) return bad("non-finite principal point");
+    const double* R = cam.R;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            const double want = i == j ? 1.0 : 0.0;
+            const double got = R[i * 3] * R[j * 3] + R[i * 3 + 1] * R[j * 3 + 1] + R[i * 3 + 2] * R[j * 3 + 2];
+            if (std::abs(got - want) > 1e-9) return bad("rotation is not orthonormal");
+        }
+    const double cx = R[1] * R[5] - R[2] * R[4], cy = R[2] * R[3] - R[0] * R[5], cz = R[0] * R[4] - R[1] * R[3];
+    if (cx * R[6] + cy * R[7] + cz * R[8] < 0) return bad("rotation is left-handed");
+    return NX_OK;
+}
+
+CamD make_cam(const nx_camera& c) {
+    CamD d;
+    d.W = c.width;
+    d.H = c.height;
+    d.fx = c.fx;
+    d.fy = c.fy;
+    d.cx = c.cx;
+    d.cy = c.cy;
+    for (int k = 0; k < 9; ++k) d.R[k] = c.R[k];
+    for (int k = 0; k < 3; ++k) d.t[k] = c.t[k];
+    // position() = -mul_transposed(R, t) (camera.hpp:24, vec_math.hpp:65-67)
+    for (int k = 0; k < 3; ++k) d.o[k] = -(c.R[k] * c.t[0] + c.R[3 + k] * c.t[1] + c.R[6 + k] * c.t[2]);
+    return d;
+}
+
+// Smallest cosine between a pixel-centre ray and the optical axis (at a corner pixel).
+double min_axis_cosine(const nx_camera& c) {
+    const double ax = std::max(std::abs((0.5 - c.cx) / c.fx), std::abs((c.width - 0.5 - c.cx) / c.fx));
+    const double ay = std::max(std::abs((0.5 - c.cy) / c.fy), std::abs((c.height - 0.5 - c.cy) / c.fy));
+    return 1.0 / std::sqrt(ax * ax + ay * ay + 1.0);
+}
+
+int bits_for(int64_t v) {
+    int b = 0;
+    while (b < 63 && (int64_t(1) << b) < v) ++b;
+    return b;
+}
+
+int frame_shape(nx_ctx* c, nx_frame* f, int W, int H, int K, int tile) {
+    const int64_t npix = static_cast<int64_t>(W) * H;
+    NX_CUDA(c, f->base.ensure(npix * 3 * sizeof(float)));
+    NX_CUDA(c, f->final_img.ensure(npix * 3 * sizeof(float)));
+    NX_CUDA(c, f->residual.ensure(npix * sizeof(float)));
+    const int64_t ns = std::max<int64_t>(npix * K, 1);
+    NX_CUDA(c, f->ids.ensure(ns * sizeof(int32_t)));
+    NX_CUDA(c, f->depths.ensure(ns * sizeof(double)));
+    NX_CUDA(c, f->weights.ensure(ns * sizeof(double)));
+    NX_CUDA(c, f->texture.ensure(ns * 3 * sizeof(float)));
+    f->W = W;
+    f->H = H;
+    f->K = K;
+    f->tiles_x = (W + tile - 1) / tile;
+    f->tiles_y = (H + tile - 1) / tile;
+    return NX_OK;
+}
+
+FrameDev frame_dev(const nx_frame* f) {
+    FrameDev d;
+    d.W = f->W;
+    d.H = f->H;
+    d.K = f->K;
+    d.tiles_x = f->tiles_x;
+    d.tiles_y = f->tiles_y;
+    d.base = f->base.as<float>();
+    d.ids = f->ids.as<int32_t>();
+    d.depths = f->depths.as<double>();
+    d.weights = f->weights.as<double>();
+    d.texture = f->texture.as<float>();
+    d.final_img = f->final_img.as<float>();
+    d.residual = f->residual.as<float>();
+    return d;
+}
+
+SceneDev scene_dev(const nx_scene* s) {
+    SceneDev d;
+    d.n = s->n;
+    d.geom = s->geom.as<double>();
+    d.sh = s->sh.as<float>();
+    d.table = s->table.as<float>();
+    d.w1 = s->w1.as<float>();
+    d.w2 = s->w2.as<float>();
+    d.w3 = s->w3.as<float>();
+    d.field = s->field;
+    return d;
+}
+
+void record(nx_ctx* c, int stage, cudaStream_t s) {
+    if (c->profiling) cudaEventRecord(c->ev[stage], s);
+}
+
+int check_inputs(nx_ctx* c, const nx_scene* scene, const nx_camera* cam) {
+    if (!c || !scene || !cam) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    int st;
+    if ((st = validate_settings(c, scene->st))) return st;
+    if ((st = validate_camera(c, *cam))) return st;
+    if (scene->bad_status) return set_err(c, scene->bad_status, scene->bad_msg);
+    return NX_OK;
+}
+
+// Builds the per-tile lists (work lists, or the reference lists when
+// reference_lists) for `cam` into frame->list_ids / frame->tile_offsets.
+int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame* f, int reference_lists,
+                cudaStream_t s, int64_t* total_keys) {
+    const int64_t n = scene->n;
+    const int64_t n_tiles = static_cast<int64_t>(f->tiles_x) * f->tiles_y;
+    const CamD cd = make_cam(cam);
+    const int64_t nn = std::max<int64_t>(n, 1);
+    NX_CUDA(c, c->rec.ensure(nn * REC_FIELDS * sizeof(double)));
+    NX_CUDA(c, c->cls.ensure(nn * sizeof(int32_t)));
+    NX_CUDA(c, c->ref_rect.ensure(nn * sizeof(int4)));
+    NX_CUDA(c, c->work_rect.ensure(nn * sizeof(int4)));
+    NX_CUDA(c, c->key.ensure(nn * sizeof(uint64_t)));
+    NX_CUDA(c, c->flag.ensure(nn * sizeof(int32_t)));
+    NX_CUDA(c, c->pos.ensure(nn * sizeof(int32_t)));
+    NX_CUDA(c, c->skeys_a.ensure(nn * sizeof(uint64_t)));
+    NX_CUDA(c, c->skeys_b.ensure(nn * sizeof(uint64_t)));
+    NX_CUDA(c, c->sids_a.ensure(nn * sizeof(uint32_t)));
+    NX_CUDA(c, c->sids_b.ensure(nn * sizeof(uint32_t)));
+    NX_CUDA(c, c->counts.ensure(nn * sizeof(int32_t)));
+    NX_CUDA(c, c->offsets.ensure(nn * sizeof(int32_t)));
+    NX_CUDA(c, c->tile_counts.ensure((n_tiles + 1) * sizeof(int32_t)));
+    NX_CUDA(c, f->tile_offsets.ensure((n_tiles + 1) * sizeof(int32_t)));
+    const size_t scratch_ints =
+        std::max({scan_scratch_ints(nn), radix_scratch_ints(nn), scan_scratch_ints(n_tiles + 1)}) + 64;
+    NX_CUDA(c, c->scratch.ensure(scratch_ints * sizeof(int32_t)));
+    NX_CUDA(c, cudaMemsetAsync(f->stats, 0, sizeof(FrameStatsD), s));
+
+    record(c, NX_STAGE_PREPROCESS, s);
+    PreprocessArgs pa;
+    pa.scene = scene_dev(scene);
+    pa.st = scene->st;
+    pa.cam = cd;
+    pa.tiles_x = f->tiles_x;
+    pa.tiles_y = f->tiles_y;
+    pa.zmin_work = 0.5 * scene->st.near_eps * min_axis_cosine(cam);
+    pa.rec = c->rec.as<double>();
+    pa.cls = c->cls.as<int32_t>();
+    pa.ref_rect = c->ref_rect.as<int4>();
+    pa.work_rect = c->work_rect.as<int4>();
+    pa.key = c->key.as<uint64_t>();
+    pa.flag = c->flag.as<int32_t>();
+    pa.reference_lists = reference_lists;
+    pa.stats = f->stats;
+    launch_preprocess(pa, s);
+
+    // K2: compaction of the primitives that own work (id-ascending) + depth sort.
+    int32_t* d_total = c->scratch.as<int32_t>();  // [0] n_sorted, [1] n_keys
+    int32_t* sc = d_total + 64;
+    scan_exclusive(c->flag.as<int32_t>(), c->pos.as<int32_t>(), n, d_total, sc, s);
+    NX_CUDA(c, cudaMemcpyAsync(c->h_pinned, d_total, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    NX_CUDA(c, cudaStreamSynchronize(s));
+    const int64_t n_sorted = n > 0 ? c->h_pinned[0] : 0;
+    record(c, NX_STAGE_DEPTH_SORT, s);
+    launch_compact(c->flag.as<int32_t>(), c->pos.as<int32_t>(), c->key.as<uint64_t>(), n, c->skeys_a.as<uint64_t>(),
+                   c->sids_a.as<uint32_t>(), s);
+    const bool in_b = radix_sort_pairs_u64(c->skeys_a.as<uint64_t>(), c->sids_a.as<uint32_t>(),
+                                           c->skeys_b.as<uint64_t>(), c->sids_b.as<uint32_t>(), n_sorted, 0, 64, sc, s);
+    const uint32_t* sorted_ids = in_b ? c->sids_b.as<uint32_t>() : c->sids_a.as<uint32_t>();
+
+    // K3: emit (tile, id) keys in sorted order.
+    record(c, NX_STAGE_EMIT, s);
+    launch_rect_counts(sorted_ids, n_sorted, c->work_rect.as<int4>(), c->counts.as<int32_t>(), s);
+    scan_exclusive(c->counts.as<int32_t>(), c->offsets.as<int32_t>(), n_sorted, d_total + 1, sc, s);
+    NX_CUDA(c, cudaMemcpyAsync(c->h_pinned + 1, d_total + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    NX_CUDA(c, cudaStreamSynchronize(s));
+    const int64_t n_keys = n_sorted > 0 ? c->h_pinned[1] : 0;
+    if (n_keys < 0) return set_err(c, NX_UNSUPPORTED, "tile-key count exceeds 2^31");
+    const int64_t nk = std::max<int64_t>(n_keys, 1);
+    NX_CUDA(c, c->tkeys_a.ensure(nk * sizeof(uint32_t)));
+    NX_CUDA(c, c->tkeys_b.ensure(nk * sizeof(uint32_t)));
+    NX_CUDA(c, c->tvals_a.ensure(nk * sizeof(uint32_t)));
+    NX_CUDA(c, c->tvals_b.ensure(nk * sizeof(uint32_t)));
+    const size_t need = radix_scratch_ints(nk) + 64;
+    if (need * sizeof(int32_t) > c->scratch.cap) {
+        // grow scratch, preserving nothing (totals already read back)
+        NX_CUDA(c, c->scratch.ensure(need * sizeof(int32_t)));
+        d_total = c->scratch.as<int32_t>();
+        sc = d_total + 64;
+    }
+    NX_CUDA(c, cudaMemsetAsync(c->tile_counts.as<int32_t>(), 0, (n_tiles + 1) * sizeof(int32_t), s));
+    launch_emit(sorted_ids, c->offsets.as<int32_t>(), n_sorted, n_keys, c->work_rect.as<int4>(), f->tiles_x,
+                c->tkeys_a.as<uint32_t>(), c->tvals_a.as<uint32_t>(), c->tile_counts.as<int32_t>(), s);
+
+    // K4: stable sort by tile.
+    record(c, NX_STAGE_TILE_SORT, s);
+    const int tb = std::max(bits_for(n_tiles), 1);
+    const bool t_in_b = radix_sort_pairs_u32(c->tkeys_a.as<uint32_t>(), c->tvals_a.as<uint32_t>(),
+                                             c->tkeys_b.as<uint32_t>(), c->tvals_b.as<uint32_t>(), n_keys, 0, tb, sc, s);
+    // K5: tile ranges.
+    scan_exclusive(c->tile_counts.as<int32_t>(), f->tile_offsets.as<int32_t>(), n_tiles + 1, nullptr, sc, s);
+    f->list_ids.p = t_in_b ? c->tvals_b.p : c->tvals_a.p;  // borrowed (not owned)
+    f->list_ids.cap = 0;
+    *total_keys = n_keys;
+    NX_CUDA(c, cudaGetLastError());
+    return NX_OK;
+}
+
+int collection(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* f, cudaStream_t s,
+               int32_t* dbg_hits, int32_t* dbg_counts, int dbg_y0, int dbg_y1, int dbg_max) {
+    int st;
+    if ((st = check_inputs(c, scene, cam))) return st;
+    if ((st = frame_shape(c, f, cam->width, cam->height, scene->st.top_k, scene->st.tile))) return st;
+    f->n_nexels = scene->n;
+    int64_t total = 0;
+    if ((st = build_lists(c, scene, *cam, f, 0, s, &total))) return st;
+    record(c, NX_STAGE_COMPOSITE, s);
+    CompositeArgs ca;
+    ca.rec = c->rec.as<double>();
+    ca.n = std::max<int64_t>(scene->n, 1);
+    ca.sh = scene->sh.as<float>();
+    ca.list_ids = f->list_ids.as<int32_t>();
+    ca.tile_offsets = f->tile_offsets.as<int32_t>();
+    ca.st = scene->st;
+    ca.cam = make_cam(*cam);
+    ca.fb = frame_dev(f);
+    ca.sh_degree = scene->st.no_prim_sh ? 0 : 3;
+    ca.dbg_hits = dbg_hits;
+    ca.dbg_counts = dbg_counts;
+    ca.dbg_y0 = dbg_y0;
+    ca.dbg_y1 = dbg_y1;
+    ca.dbg_max = dbg_max;
+    launch_composite(ca, s);
+    NX_CUDA(c, cudaGetLastError());
+    return NX_OK;
+}
+
+int texturing(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* f, cudaStream_t s) {
+    if (f->W != cam->width || f->H != cam->height)
+        return set_err(c, NX_INVALID_ARGUMENT, "frame does not match the camera (run collection_pass first)");
+    record(c, NX_STAGE_TEXTURE, s);
+    TextureArgs ta;
+    ta.scene = scene_dev(scene);
+    ta.st = scene->st;
+    ta.cam = make_cam(*cam);
+    ta.fb = frame_dev(f);
+    ta.stats = f->stats;
+    const int st = launch_texture(ta, s);
+    if (st) return set_err(c, st, "texture field shape not supported (n_in <= 64, n_hidden <= 128)");
+    record(c, NX_NUM_STAGES, s);
+    NX_CUDA(c, cudaGetLastError());
+    return NX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nx_version(void) { return "nexel-b200 0.1 (sm_100a)"; }
+
+const char* nx_status_name(int status) {
+    switch (status) {
+        case NX_OK: return "ok";
+        case NX_BAD_SETTINGS: return "bad-settings";
+        case NX_BAD_CAMERA: return "bad-camera";
+        case NX_BAD_PRIMITIVE: return "bad-primitive";
+        case NX_INVALID_ARGUMENT: return "invalid-argument";
+        case NX_UNSUPPORTED: return "unsupported";
+        case NX_OUT_OF_MEMORY: return "out-of-memory";
+        case NX_CUDA_ERROR: return "cuda-error";
+        case NX_NO_DEVICE: return "no-device";
+        default: return "unknown";
+    }
+}
+
+const char* nx_stage_name(int stage) { return stage >= 0 && stage < NX_NUM_STAGES ? kStageNames[stage] : "?"; }
+
+int nx_device_count(int* count) {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    *count = e == cudaSuccess ? n : 0;
+    return e == cudaSuccess ? NX_OK : NX_NO_DEVICE;
+}
+
+int nx_ctx_create(int device, nx_ctx** out) {
+    if (!out) return NX_INVALID_ARGUMENT;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) return NX_NO_DEVICE;
+    if (cudaSetDevice(device) != cudaSuccess) return NX_NO_DEVICE;
+    nx_ctx* c = new (std::nothrow) nx_ctx;
+    if (!c) return NX_OUT_OF_MEMORY;
+    c->device = device;
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMallocHost(&c->h_pinned, 64 * sizeof(int32_t)) != cudaSuccess) {
+        delete c;
+        return NX_CUDA_ERROR;
+    }
+    for (auto& e : c->ev) cudaEventCreate(&e);
+    *out = c;
+    return NX_OK;
+}
+
+void nx_ctx_destroy(nx_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (DevBuf* b : {&c->rec, &c->cls, &c->ref_rect, &c->work_rect, &c->key, &c->flag, &c->pos, &c->skeys_a,
+                      &c->skeys_b, &c->sids_a, &c->sids_b, &c->counts, &c->offsets, &c->tkeys_a, &c->tkeys_b,
+                      &c->tvals_a, &c->tvals_b, &c->tile_counts, &c->scratch, &c->dbg_hits, &c->dbg_counts})
+        b->release();
+    for (auto& e : c->ev) cudaEventDestroy(e);
+    if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char* nx_ctx_last_error(const nx_ctx* c, int* status) {
+    if (!c) return "null context";
+    if (status) *status = c->err_status;
+    return c->err.c_str();
+}
+
+void* nx_ctx_stream(nx_ctx* c) { return c ? c->stream : nullptr; }
+
+int nx_ctx_synchronize(nx_ctx* c) {
+    NX_CUDA(c, cudaStreamSynchronize(c->stream));
+    return NX_OK;
+}
+
+int nx_ctx_set_profiling(nx_ctx* c, int enable) {
+    if (!c) return NX_INVALID_ARGUMENT;
+    c->profiling = enable != 0;
+    return NX_OK;
+}
+
+int nx_ctx_stage_times(nx_ctx* c, float* ms, int n) {
+    if (!c || !ms) return NX_INVALID_ARGUMENT;
+    NX_CUDA(c, cudaDeviceSynchronize());
+    for (int i = 0; i < n && i < NX_NUM_STAGES; ++i) {
+        float v = 0.f;
+        if (cudaEventElapsedTime(&v, c->ev[i], c->ev[i + 1]) != cudaSuccess) v = -1.f;
+        ms[i] = v;
+    }
+    cudaGetLastError();
+    return NX_OK;
+}
+
+int nx_scene_create(nx_ctx* c, const nx_settings* settings, int64_t n, const double* nexels,
+                    const nx_field_desc* field, const double* table, const double* w1, const double* w2,
+                    const double* w3, nx_scene** out) {
+    if (!c || !settings || !field || !out || n < 0 || (n > 0 && !nexels) || !table || !w1 || !w2 || !w3)
+        return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    if (n >= (int64_t(1) << 31)) return set_err(c, NX_UNSUPPORTED, "more than 2^31 primitives");
+    if (field->levels < 1 || field->features < 1 || field->n_hidden < 1 || field->log2_table < 0 ||
+        field->log2_table > 30)
+        return set_err(c, NX_INVALID_ARGUMENT, "bad field description");
+    cudaSetDevice(c->device);
+    nx_scene* s = new (std::nothrow) nx_scene;
+    if (!s) return set_err(c, NX_OUT_OF_MEMORY, "host allocation");
+    s->ctx = c;
+    s->n = n;
+    s->field = *field;
+    s->st = *settings;
+    // Validation exactly as activate() (primitive.cpp:47-63), first failing id.
+    const char* whats[] = {"non-finite position", "non-finite quaternion", "non-finite log scale",
+                           "non-finite kernel exponent", "non-finite opacity", "non-finite sh coefficient",
+                           "degenerate quaternion"};
+    for (int64_t i = 0; i < n && !s->bad_status; ++i) {
+        const double* p = nexels + i * NX_PARAMS_PER_NEXEL;
+        int what = -1;
+        for (int k = 0; k < 3 && what < 0; ++k)
+            if (!std::isfinite(p[k])) what = 0;
+        for (int k = 0; k < 4 && what < 0; ++k)
+            if (!std::isfinite(p[3 + k])) what = 1;
+        for (int k = 0; k < 2 && what < 0; ++k) {
+            if (!std::isfinite(p[7 + k])) what = 2;
+            else if (!std::isfinite(p[10 + k])) what = 3;
+        }
+        if (what < 0 && !std::isfinite(p[9])) what = 4;
+        for (int k = 0; k < NX_SH_VALUES && what < 0; ++k)
+            if (!std::isfinite(p[12 + k])) what = 5;
+        if (what < 0) {
+            const double qn = std::sqrt(p[3] * p[3] + p[4] * p[4] + p[5] * p[5] + p[6] * p[6]);
+            if (!(qn > 1e-12)) what = 6;
+        }
+        if (what >= 0) {
+            s->bad_status = NX_BAD_PRIMITIVE;
+            s->bad_msg = std::string(whats[what]) + " in primitive " + std::to_string(i);
+        }
+    }
+    const int64_t nn = std::max<int64_t>(n, 1);
+    std::vector<double> geom(static_cast<size_t>(kGeomFields * nn), 0.0);
+    std::vector<float> sh(static_cast<size_t>(NX_SH_VALUES * nn), 0.f);
+    for (int64_t i = 0; i < n; ++i) {
+        const double* p = nexels + i * NX_PARAMS_PER_NEXEL;
+        for (int k = 0; k < kGeomFields; ++k) geom[k * nn + i] = p[k];
+        for (int k = 0; k < NX_SH_VALUES; ++k) sh[i * NX_SH_VALUES + k] = static_cast<float>(p[12 + k]);
+    }
+    const size_t n_table = static_cast<size_t>(field->levels) * (size_t(1) << field->log2_table) * field->features;
+    const size_t n_in = static_cast<size_t>(field->levels) * field->features;
+    const size_t nh = field->n_hidden;
+    auto upload_f32 = [&](DevBuf& b, const double* src, size_t count) -> cudaError_t {
+        cudaError_t e = b.ensure(std::max<size_t>(count, 1) * sizeof(float));
+        if (e != cudaSuccess) return e;
+        std::vector<float> tmp(std::min<size_t>(count, size_t(1) << 22));
+        for (size_t at = 0; at < count; at += tmp.size()) {
+            const size_t m = std::min(tmp.size(), count - at);
+            for (size_t k = 0; k < m; ++k) tmp[k] = static_cast<float>(src[at + k]);
+            e = cudaMemcpy(b.as<float>() + at, tmp.data(), m * sizeof(float), cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    };
+    cudaError_t e = s->geom.ensure(geom.size() * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpy(s->geom.p, geom.data(), geom.size() * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = s->sh.ensure(sh.size() * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemcpy(s->sh.p, sh.data(), sh.size() * sizeof(float), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = upload_f32(s->table, table, n_table);
+    if (e == cudaSuccess) e = upload_f32(s->w1, w1, nh * n_in);
+    if (e == cudaSuccess) e = upload_f32(s->w2, w2, nh * nh);
+    if (e == cudaSuccess) e = upload_f32(s->w3, w3, NX_SH_VALUES * nh);
+    if (e != cudaSuccess) {
+        nx_scene_destroy(s);
+        return cuda_err(c, e, "scene upload");
+    }
+    *out = s;
+    return NX_OK;
+}
+
+int nx_scene_set_settings(nx_ctx* c, nx_scene* s, const nx_settings* settings) {
+    if (!s || !settings) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    s->st = *settings;
+    return NX_OK;
+}
+
+int nx_scene_get_settings(const nx_scene* s, nx_settings* out) {
+    if (!s || !out) return NX_INVALID_ARGUMENT;
+    *out = s->st;
+    return NX_OK;
+}
+
+void nx_scene_destroy(nx_scene* s) {
+    if (!s) return;
+    if (s->ctx) cudaSetDevice(s->ctx->device);
+    for (DevBuf* b : {&s->geom, &s->sh, &s->table, &s->w1, &s->w2, &s->w3}) b->release();
+    delete s;
+}
+
+int nx_frame_create(nx_ctx* c, int width, int height, int top_k, nx_frame** out) {
+    if (!c || !out || width < 0 || height < 0 || top_k < 0 || top_k > NX_MAX_TOP_K)
+        return set_err(c, NX_INVALID_ARGUMENT, "bad frame shape");
+    cudaSetDevice(c->device);
+    nx_frame* f = new (std::nothrow) nx_frame;
+    if (!f) return set_err(c, NX_OUT_OF_MEMORY, "host allocation");
+    f->ctx = c;
+    if (cudaMalloc(&f->stats, sizeof(FrameStatsD)) != cudaSuccess) {
+        delete f;
+        return set_err(c, NX_OUT_OF_MEMORY, "frame stats");
+    }
+    cudaMemset(f->stats, 0, sizeof(FrameStatsD));
+    int st = frame_shape(c, f, width, height, top_k, 16);
+    if (st) {
+        nx_frame_destroy(f);
+        return st;
+    }
+    *out = f;
+    return NX_OK;
+}
+
+void nx_frame_destroy(nx_frame* f) {
+    if (!f) return;
+    if (f->ctx) cudaSetDevice(f->ctx->device);
+    for (DevBuf* b : {&f->base, &f->ids, &f->depths, &f->weights, &f->texture, &f->final_img, &f->residual,
+                      &f->tile_offsets})
+        b->release();
+    if (f->stats) cudaFree(f->stats);
+    delete f;
+}
+
+int nx_frame_view_get(const nx_frame* f, nx_frame_view* v) {
+    if (!f || !v) return NX_INVALID_ARGUMENT;
+    v->width = f->W;
+    v->height = f->H;
+    v->top_k = f->K;
+    v->tiles_x = f->tiles_x;
+    v->tiles_y = f->tiles_y;
+    v->base = f->base.as<float>();
+    v->ids = f->ids.as<int32_t>();
+    v->depths = f->depths.as<double>();
+    v->weights = f->weights.as<double>();
+    v->texture = f->texture.as<float>();
+    v->final_img = f->final_img.as<float>();
+    v->residual = f->residual.as<float>();
+    return NX_OK;
+}
+
+int nx_frame_download(nx_ctx* c, const nx_frame* f, const nx_host_frame* dst, void* stream) {
+    if (!c || !f || !dst) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    cudaStream_t s = pick_stream(c, stream);
+    const size_t npix = static_cast<size_t>(f->W) * f->H, ns = npix * f->K;
+    auto cp = [&](void* d, const DevBuf& b, size_t bytes) -> cudaError_t {
+        if (!d || !bytes) return cudaSuccess;
+        return cudaMemcpyAsync(d, b.p, bytes, cudaMemcpyDeviceToHost, s);
+    };
+    NX_CUDA(c, cp(dst->base, f->base, npix * 3 * sizeof(float)));
+    NX_CUDA(c, cp(dst->ids, f->ids, ns * sizeof(int32_t)));
+    NX_CUDA(c, cp(dst->depths, f->depths, ns * sizeof(double)));
+    NX_CUDA(c, cp(dst->weights, f->weights, ns * sizeof(double)));
+    NX_CUDA(c, cp(dst->texture, f->texture, ns * 3 * sizeof(float)));
+    NX_CUDA(c, cp(dst->final_img, f->final_img, npix * 3 * sizeof(float)));
+    NX_CUDA(c, cp(dst->residual, f->residual, npix * sizeof(float)));
+    return NX_OK;
+}
+
+int nx_frame_stats_get(nx_ctx* c, const nx_frame* f, nx_frame_stats* out) {
+    if (!c || !f || !out) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    FrameStatsD h;
+    NX_CUDA(c, cudaStreamSynchronize(c->stream));
+    NX_CUDA(c, cudaDeviceSynchronize());
+    NX_CUDA(c, cudaMemcpy(&h, f->stats, sizeof h, cudaMemcpyDeviceToHost));
+    std::memset(out, 0, sizeof *out);
+    out->n_nexels = f->n_nexels;
+    out->n_dropped_support = static_cast<int64_t>(h.cls[CLS_SUPPORT]);
+    out->n_behind = static_cast<int64_t>(h.cls[CLS_BEHIND]);
+    out->n_offscreen = static_cast<int64_t>(h.cls[CLS_OFFSCREEN]);
+    out->n_rect = static_cast<int64_t>(h.cls[CLS_RECT]);
+    out->n_straddlers = static_cast<int64_t>(h.cls[CLS_STRADDLER]);
+    out->n_entries = out->n_rect + out->n_straddlers;
+    out->n_straddlers_kept = static_cast<int64_t>(h.straddlers_kept);
+    out->tile_keys = static_cast<int64_t>(h.tile_keys);
+    out->work_keys = static_cast<int64_t>(h.work_keys);
+    out->n_queries = static_cast<int64_t>(h.queries);
+    return NX_OK;
+}
+
+int nx_collection_pass(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* f, void* stream) {
+    if (!c || !f) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    return collection(c, scene, cam, f, pick_stream(c, stream), nullptr, nullptr, 0, 0, 0);
+}
+
+int nx_texturing_pass(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* f, void* stream) {
+    if (!c || !f || !scene || !cam) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    return texturing(c, scene, cam, f, pick_stream(c, stream));
+}
+
+int nx_render(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* f, void* stream) {
+    if (!c || !f) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    cudaStream_t s = pick_stream(c, stream);
+    int st = collection(c, scene, cam, f, s, nullptr, nullptr, 0, 0, 0);
+    if (st) return st;
+    return texturing(c, scene, cam, f, s);
+}
+
+int nx_debug_tile_lists(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, int reference_lists,
+                        int64_t* offsets, int32_t* ids, int64_t capacity, int64_t* total, int32_t* tiles_x,
+                        int32_t* tiles_y) {
+    int st;
+    if ((st = check_inputs(c, scene, cam))) return st;
+    nx_frame* f = nullptr;
+    if ((st = nx_frame_create(c, cam->width, cam->height, scene->st.top_k, &f))) return st;
+    st = frame_shape(c, f, cam->width, cam->height, scene->st.top_k, scene->st.tile);
+    int64_t n_keys = 0;
+    cudaStream_t s = c->stream;
+    if (!st) st = build_lists(c, scene, *cam, f, reference_lists, s, &n_keys);
+    if (!st) {
+        const int64_t n_tiles = static_cast<int64_t>(f->tiles_x) * f->tiles_y;
+        std::vector<int32_t> off(static_cast<size_t>(n_tiles + 1));
+        cudaError_t e = cudaMemcpyAsync(off.data(), f->tile_offsets.p, off.size() * sizeof(int32_t),
+                                        cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && ids && n_keys > 0)
+            e = cudaMemcpyAsync(ids, f->list_ids.p, std::min(capacity, n_keys) * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = cuda_err(c, e, "debug download");
+        if (!st && offsets)
+            for (int64_t t = 0; t <= n_tiles; ++t) offsets[t] = off[t];
+        if (total) *total = n_keys;
+        if (tiles_x) *tiles_x = f->tiles_x;
+        if (tiles_y) *tiles_y = f->tiles_y;
+    }
+    nx_frame_destroy(f);
+    return st;
+}
+
+int nx_debug_pixel_hits(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, int y0, int y1, int max_hits,
+                        int32_t* hits, int32_t* counts) {
+    int st;
+    if ((st = check_inputs(c, scene, cam))) return st;
+    if (y0 < 0 || y1 > cam->height || y1 < y0 || max_hits < 1 || !hits || !counts)
+        return set_err(c, NX_INVALID_ARGUMENT, "bad debug row range");
+    const size_t q = static_cast<size_t>(y1 - y0) * cam->width;
+    NX_CUDA(c, c->dbg_hits.ensure(std::max<size_t>(q * max_hits, 1) * sizeof(int32_t)));
+    NX_CUDA(c, c->dbg_counts.ensure(std::max<size_t>(q, 1) * sizeof(int32_t)));
+    nx_frame* f = nullptr;
+    if ((st = nx_frame_create(c, cam->width, cam->height, scene->st.top_k, &f))) return st;
+    cudaStream_t s = c->stream;
+    st = collection(c, scene, cam, f, s, c->dbg_hits.as<int32_t>(), c->dbg_counts.as<int32_t>(), y0, y1, max_hits);
+    if (!st) {
+        cudaError_t e = cudaMemcpyAsync(hits, c->dbg_hits.p, q * max_hits * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(counts, c->dbg_counts.p, q * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = cuda_err(c, e, "debug download");
+    }
+    nx_frame_destroy(f);
+    return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,274 @@
+// K6 composite: per-tile front-to-back alpha compositing with early termination
+// and a top-K buffer (collection_pass, renderer.cpp:115-171).
+//
+// One CTA per screen tile, one thread per pixel. The tile's work list (ids in
+// (depth, id) order) is walked in chunks of kChunk primitives whose intersection
+// records are staged into shared memory (SoA, every thread reads the same
+// primitive at the same time -> broadcast, conflict-free). Every decision is
+// the reference's, in fp64: grazing test, t > near_eps, alpha >= 1/255 (with an
+// exact-preserving early reject on |u| > ru before any transcendental), alpha
+// clamp, transmittance termination, top-K replacement with arrival-order ties.
+// A warp stops testing when all its pixels have terminated; the CTA stops
+// staging when all of its pixels have.
+#include "nx_internal.cuh"
+
+namespace nx {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kChunk = 64;
+
+// eval_sh (sh.hpp:46-57) with fp64 basis (sh_basis, sh.hpp:11-40) and the
+// primitive's fp32 coefficients.
+__device__ __forceinline__ void eval_sh_prim(const float* __restrict__ sh, const double* d, int degree,
+                                             double* rgb) {
+    const double C0 = 0.28209479177387814;
+    double acc0 = 0.5 + static_cast<double>(__ldg(sh + 0)) * C0;
+    double acc1 = 0.5 + static_cast<double>(__ldg(sh + 1)) * C0;
+    double acc2 = 0.5 + static_cast<double>(__ldg(sh + 2)) * C0;
+    if (degree >= 3) {
+        const double C1 = 0.4886025119029199;
+        const double x = d[0], y = d[1], z = d[2];
+        const double xx = x * x, yy = y * y, zz = z * z;
+        double b[16];
+        b[1] = -C1 * y;
+        b[2] = C1 * z;
+        b[3] = -C1 * x;
+        b[4] = 1.0925484305920792 * x * y;
+        b[5] = -1.0925484305920792 * y * z;
+        b[6] = 0.31539156525252005 * (2.0 * zz - xx - yy);
+        b[7] = -1.0925484305920792 * x * z;
+        b[8] = 0.5462742152960396 * (xx - yy);
+        b[9] = -0.5900435899266435 * y * (3.0 * xx - yy);
+        b[10] = 2.890611442640554 * x * y * z;
+        b[11] = -0.4570457994644658 * y * (4.0 * zz - xx - yy);
+        b[12] = 0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+        b[13] = -0.4570457994644658 * x * (4.0 * zz - xx - yy);
+        b[14] = 1.445305721320277 * z * (xx - yy);
+        b[15] = -0.5900435899266435 * x * (xx - 3.0 * yy);
+        const float4* s4 = reinterpret_cast<const float4*>(sh);
+        // coefficients k = 1..15 live at floats 3..47: load 12 float4 and skip the first 3.
+        float c[48];
+#pragma unroll
+        for (int q = 0; q < 12; ++q) {
+            const float4 v = __ldg(s4 + q);
+            c[4 * q + 0] = v.x;
+            c[4 * q + 1] = v.y;
+            c[4 * q + 2] = v.z;
+            c[4 * q + 3] = v.w;
+        }
+#pragma unroll
+        for (int k = 1; k < 16; ++k) {
+            acc0 += static_cast<double>(c[3 * k + 0]) * b[k];
+            acc1 += static_cast<double>(c[3 * k + 1]) * b[k];
+            acc2 += static_cast<double>(c[3 * k + 2]) * b[k];
+        }
+    }
+    rgb[0] = acc0 < 0.0 ? 0.0 : acc0;
+    rgb[1] = acc1 < 0.0 ? 0.0 : acc1;
+    rgb[2] = acc2 < 0.0 ? 0.0 : acc2;
+}
+
+template <int K, bool kDebug>
+__global__ void __launch_bounds__(kThreads) composite_kernel(const CompositeArgs a) {
+    __shared__ double s_rec[REC_FIELDS][kChunk];
+    __shared__ int32_t s_id[kChunk];
+
+    const int tile = a.st.tile;
+    const int t = blockIdx.x;
+    const int tx = t % a.fb.tiles_x, ty = t / a.fb.tiles_x;
+    const int list_begin = a.tile_offsets[t], list_end = a.tile_offsets[t + 1];
+    const int W = a.cam.W, H = a.cam.H;
+    const double near_eps = a.st.near_eps, alpha_max = a.st.alpha_max, min_T = a.st.min_transmittance;
+    const int64_t n = a.n;
+
+    for (int pbase = 0; pbase < tile * tile; pbase += kThreads) {
+        const int lp = pbase + threadIdx.x;
+        const int px = tx * tile + lp % tile, py = ty * tile + lp / tile;
+        const bool in_img = lp < tile * tile && px < W && py < H;
+        double dir[3] = {0.0, 0.0, 1.0};
+        if (in_img) pixel_dir(a.cam, px + 0.5, py + 0.5, dir);
+        const double o0 = a.cam.o[0], o1 = a.cam.o[1], o2 = a.cam.o[2];
+
+        double T = 1.0;
+        double acc[3] = {0.0, 0.0, 0.0};
+        int32_t k_id[K > 0 ? K : 1];
+        double k_w[K > 0 ? K : 1], k_t[K > 0 ? K : 1];
+        uint32_t k_seq[K > 0 ? K : 1];
+#pragma unroll
+        for (int s = 0; s < (K > 0 ? K : 1); ++s) {
+            k_id[s] = -1;
+            k_w[s] = 0.0;
+            k_t[s] = 0.0;
+            k_seq[s] = 0;
+        }
+        int k_size = 0;
+        uint32_t counter = 0;
+        bool active = in_img;
+        int dbg_n = 0;
+        const bool dbg_row = kDebug && in_img && py >= a.dbg_y0 && py < a.dbg_y1;
+        const int64_t dbg_q = kDebug ? (static_cast<int64_t>(py - a.dbg_y0) * W + px) : 0;
+
+        for (int cb = list_begin; cb < list_end; cb += kChunk) {
+            const int cn = min(kChunk, list_end - cb);
+            __syncthreads();
+            for (int e = threadIdx.x; e < cn; e += kThreads) s_id[e] = a.list_ids[cb + e];
+            __syncthreads();
+            for (int e = threadIdx.x; e < REC_FIELDS * cn; e += kThreads) {
+                const int f = e / cn, j = e - f * cn;
+                s_rec[f][j] = __ldg(a.rec + static_cast<int64_t>(f) * n + s_id[j]);
+            }
+            __syncthreads();
+            if (active) {
+                for (int j = 0; j < cn; ++j) {
+                    // intersect (intersect.hpp:23-42)
+                    const double denom = dir[0] * s_rec[REC_NX][j] + dir[1] * s_rec[REC_NY][j] +
+                                         dir[2] * s_rec[REC_NZ][j];
+                    if (fabs(denom) < kMinNormalDot) continue;
+                    const double tt = s_rec[REC_NUM][j] / denom;
+                    if (!(tt > near_eps)) continue;
+                    const double e0 = (o0 + tt * dir[0]) - s_rec[REC_MUX][j];
+                    const double e1 = (o1 + tt * dir[1]) - s_rec[REC_MUY][j];
+                    const double e2 = (o2 + tt * dir[2]) - s_rec[REC_MUZ][j];
+                    const double du = e0 * s_rec[REC_V1X][j] + e1 * s_rec[REC_V1Y][j] + e2 * s_rec[REC_V1Z][j];
+                    if (fabs(du) > s_rec[REC_ULIM][j]) continue;
+                    const double dv = e0 * s_rec[REC_V2X][j] + e1 * s_rec[REC_V2Y][j] + e2 * s_rec[REC_V2Z][j];
+                    if (fabs(dv) > s_rec[REC_VLIM][j]) continue;
+                    const double u = du / s_rec[REC_SX][j];
+                    const double v = dv / s_rec[REC_SY][j];
+                    const double alpha_raw = eval_kernel(u, v, s_rec[REC_OP][j], s_rec[REC_GX][j], s_rec[REC_GY][j]);
+                    if (alpha_raw < kAlphaMin) continue;
+                    // composite (renderer.cpp:146-152)
+                    const int32_t id = s_id[j];
+                    const double alpha = alpha_max < alpha_raw ? alpha_max : alpha_raw;
+                    const double w = alpha * T;
+                    double col[3];
+                    eval_sh_prim(a.sh + static_cast<int64_t>(id) * NX_SH_VALUES, dir, a.sh_degree, col);
+                    acc[0] += w * col[0];
+                    acc[1] += w * col[1];
+                    acc[2] += w * col[2];
+                    if (K > 0) {  // TopKBuffer::insert (framebuffers.hpp:33-48)
+                        const uint32_t seq = counter++;
+                        if (k_size < K) {
+#pragma unroll
+                            for (int s = 0; s < (K > 0 ? K : 1); ++s)
+                                if (s == k_size) {
+                                    k_id[s] = id;
+                                    k_w[s] = w;
+                                    k_t[s] = tt;
+                                    k_seq[s] = seq;
+                                }
+                            ++k_size;
+                        } else {
+                            // last-ranked incumbent: smallest weight, latest arrival among ties
+                            int m = 0;
+                            double wm = k_w[0];
+                            uint32_t qm = k_seq[0];
+#pragma unroll
+                            for (int s = 1; s < (K > 0 ? K : 1); ++s)
+                                if (k_w[s] < wm || (k_w[s] == wm && k_seq[s] > qm)) {
+                                    m = s;
+                                    wm = k_w[s];
+                                    qm = k_seq[s];
+                                }
+#pragma unroll
+                            for (int s = 0; s < (K > 0 ? K : 1); ++s)
+                                if (s == m && w > wm) {
+                                    k_id[s] = id;
+                                    k_w[s] = w;
+                                    k_t[s] = tt;
+                                    k_seq[s] = seq;
+                                }
+                        }
+                    }
+                    if (kDebug && dbg_row) {
+                        if (dbg_n < a.dbg_max) a.dbg_hits[dbg_q * a.dbg_max + dbg_n] = id;
+                        ++dbg_n;
+                    }
+                    T *= 1.0 - alpha;
+                    if (T < min_T) {
+                        active = false;
+                        break;
+                    }
+                }
+            }
+            if (!__syncthreads_or(active)) break;
+        }
+
+        if (in_img) {
+            const int64_t pix = static_cast<int64_t>(py) * W + px;
+            a.fb.residual[pix] = static_cast<float>(T);
+            acc[0] += T * a.st.background[0];
+            acc[1] += T * a.st.background[1];
+            acc[2] += T * a.st.background[2];
+            if (K > 0) {
+                // finalize: weight desc, seq asc (framebuffers.hpp:51-56); slots >= size keep sentinels.
+#pragma unroll
+                for (int i = 0; i < K; ++i)
+#pragma unroll
+                    for (int j = 0; j + 1 < K - i; ++j) {
+                        const bool swap = (j + 1 < k_size) &&
+                                          (k_w[j + 1] > k_w[j] || (k_w[j + 1] == k_w[j] && k_seq[j + 1] < k_seq[j]));
+                        if (swap) {
+                            const int32_t ti = k_id[j];
+                            k_id[j] = k_id[j + 1];
+                            k_id[j + 1] = ti;
+                            const double tw = k_w[j];
+                            k_w[j] = k_w[j + 1];
+                            k_w[j + 1] = tw;
+                            const double td = k_t[j];
+                            k_t[j] = k_t[j + 1];
+                            k_t[j + 1] = td;
+                            const uint32_t ts = k_seq[j];
+                            k_seq[j] = k_seq[j + 1];
+                            k_seq[j + 1] = ts;
+                        }
+                    }
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    const int64_t sl = pix * K + j;
+                    a.fb.ids[sl] = k_id[j];
+                    a.fb.depths[sl] = k_t[j];
+                    a.fb.weights[sl] = k_w[j];
+                    if (j < k_size) {
+                        double col[3];
+                        eval_sh_prim(a.sh + static_cast<int64_t>(k_id[j]) * NX_SH_VALUES, dir, a.sh_degree, col);
+                        acc[0] -= k_w[j] * col[0];
+                        acc[1] -= k_w[j] * col[1];
+                        acc[2] -= k_w[j] * col[2];
+                    }
+                }
+            }
+            a.fb.base[pix * 3 + 0] = static_cast<float>(acc[0]);
+            a.fb.base[pix * 3 + 1] = static_cast<float>(acc[1]);
+            a.fb.base[pix * 3 + 2] = static_cast<float>(acc[2]);
+            if (kDebug && dbg_row) a.dbg_counts[dbg_q] = dbg_n;
+        }
+    }
+}
+
+template <bool kDebug>
+void launch_k(const CompositeArgs& a, cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(a.fb.tiles_x) * a.fb.tiles_y;
+    switch (a.fb.K) {
+        case 0: composite_kernel<0, kDebug><<<grid, kThreads, 0, s>>>(a); break;
+        case 1: composite_kernel<1, kDebug><<<grid, kThreads, 0, s>>>(a); break;
+        case 2: composite_kernel<2, kDebug><<<grid, kThreads, 0, s>>>(a); break;
+        case 3: composite_kernel<3, kDebug><<<grid, kThreads, 0, s>>>(a); break;
+        case 4: composite_kernel<4, kDebug><<<grid, kThreads, 0, s>>>(a); break;
+        case 5: composite_kernel<5, kDebug><<<grid, kThreads, 0, s>>>(a); break;
+        case 6: composite_kernel<6, kDebug><<<grid, kThreads, 0, s>>>(a); break;
+        case 7: composite_kernel<7, kDebug><<<grid, kThreads, 0, s>>>(a); break;
+        default: composite_kernel<8, kDebug><<<grid, kThreads, 0, s>>>(a); break;
+    }
+}
+
+}  // namespace
+
+void launch_composite(const CompositeArgs& a, cudaStream_t s) {
+    if (a.dbg_hits) launch_k<true>(a, s);
+    else launch_k<false>(a, s);
+}
+
+}  // namespace nx

@@ -1,0 +1,210 @@
+// Internal declarations shared by the sm_100a render kernels.
+//
+// Device-side fp64 restatements of the reference math the render path makes
+// decisions with. Every discrete decision of the reference (cull, straddle,
+// tile rect, (depth,id) order, grazing / near-plane / 1/255 tests, alpha clamp,
+// termination, top-K) is taken in fp64 with the reference's formulas, so the
+// discrete outputs (tile lists, contributor lists, ids) are bit-exact.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "../../include/nexel_b200.h"
+
+#define NX_HD __host__ __device__ __forceinline__
+
+namespace nx {
+
+constexpr double kAlphaMin = 1.0 / 255.0;  // kernel.hpp:11
+constexpr double kMinNormalDot = 1e-8;     // intersect.hpp:12
+constexpr double kProjectMinDepth = 1e-9;  // camera.hpp:38
+constexpr int kMaxTopK = NX_MAX_TOP_K;
+constexpr int kGeomFields = 12;            // fp64 geometry params per primitive
+
+// ---------------------------------------------------------------- scalar helpers
+// sigmoid / softplus (vec_math.hpp:69-84)
+NX_HD double sigmoid(double x) {
+    if (x >= 0) {
+        const double e = exp(-x);
+        return 1.0 / (1.0 + e);
+    }
+    const double e = exp(x);
+    return e / (1.0 + e);
+}
+NX_HD double softplus(double x) {
+    if (x > 30.0) return x;
+    if (x < -30.0) return exp(x);
+    return log1p(exp(x));
+}
+// axis_power / eval_kernel / support_radius (kernel.hpp:16-30, 72-76)
+NX_HD double axis_power(double u, double g) {
+    if (u == 0.0) return 0.0;
+    if (g == 1.0) return u * u;
+    const double e = 2.0 * g * log(fabs(u));
+    if (e > 700.0) return INFINITY;
+    return exp(e);
+}
+NX_HD double eval_kernel(double u, double v, double o, double gx, double gy) {
+    const double p = axis_power(u, gx) + axis_power(v, gy);
+    if (isinf(p)) return 0.0;
+    return o * exp(-0.5 * p);
+}
+NX_HD double support_radius(double o, double g) {
+    const double lim = 2.0 * log(o / kAlphaMin);
+    if (lim <= 0.0) return 0.0;
+    return pow(lim, 1.0 / (2.0 * g));
+}
+// static_cast<int>(floor(x)) with x86 cvttsd2si semantics (out-of-range -> INT_MIN),
+// which is what the reference's casts produce on its host (renderer.cpp:84-87).
+NX_HD int x86_to_int(double v) {
+    if (v >= -2147483648.0 && v < 2147483648.0) return static_cast<int>(v);
+    return INT32_MIN;
+}
+NX_HD int clampi(int v, int lo, int hi) { return v < lo ? lo : (hi < v ? hi : v); }
+
+// Orderable 64-bit key for a finite double; -0.0 is canonicalised to +0.0 so
+// that equal depths tie (and fall back to id order, renderer.cpp:102-105).
+NX_HD uint64_t depth_key(double d) {
+    d = d + 0.0;
+#ifdef __CUDA_ARCH__
+    uint64_t b = static_cast<uint64_t>(__double_as_longlong(d));
+#else
+    uint64_t b;
+    memcpy(&b, &d, 8);
+#endif
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// ---------------------------------------------------------------- camera (camera.hpp:17-43)
+struct CamD {
+    int W, H;
+    double fx, fy, cx, cy;
+    double R[9];  // row-major
+    double t[3];
+    double o[3];  // position() = -R^T t
+};
+
+// pixel_ray (camera.hpp:32-35): dir = R^T normalized(((px-cx)/fx, (py-cy)/fy, 1)).
+NX_HD void pixel_dir(const CamD& c, double px, double py, double* dir) {
+    const double d0 = (px - c.cx) / c.fx, d1 = (py - c.cy) / c.fy, d2 = 1.0;
+    const double n = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+    const double n0 = d0 / n, n1 = d1 / n, n2 = d2 / n;
+    dir[0] = c.R[0] * n0 + c.R[3] * n1 + c.R[6] * n2;
+    dir[1] = c.R[1] * n0 + c.R[4] * n1 + c.R[7] * n2;
+    dir[2] = c.R[2] * n0 + c.R[5] * n1 + c.R[8] * n2;
+}
+
+// ---------------------------------------------------------------- per-primitive composite record
+// Staged into shared memory per chunk (SoA, broadcast reads). All fp64.
+enum RecField {
+    REC_NUM = 0,  // dot(mu - origin, n): the per-camera numerator of t (intersect.hpp:29)
+    REC_NX, REC_NY, REC_NZ,
+    REC_V1X, REC_V1Y, REC_V1Z,
+    REC_V2X, REC_V2Y, REC_V2Z,
+    REC_MUX, REC_MUY, REC_MUZ,
+    REC_SX, REC_SY,
+    REC_OP,
+    REC_GX, REC_GY,
+    REC_ULIM, REC_VLIM,  // conservative |dot(delta,v)| bounds for an exact early reject
+    REC_FIELDS
+};
+
+// Classification of a primitive by build_binning (renderer.cpp:52-100).
+enum PrimClass : int32_t {
+    CLS_SUPPORT = 0,    // ru <= 0 || rv <= 0, no entry
+    CLS_BEHIND = 1,     // whole support behind the pinhole, no entry
+    CLS_OFFSCREEN = 2,  // rect entirely off screen, no entry
+    CLS_RECT = 3,       // rect-binned entry
+    CLS_STRADDLER = 4,  // entry in every tile (reference); refined work rect here
+};
+
+struct FrameStatsD {
+    unsigned long long cls[5];
+    unsigned long long straddlers_kept;
+    unsigned long long tile_keys;
+    unsigned long long work_keys;
+    unsigned long long queries;
+};
+
+struct SceneDev {
+    int64_t n;
+    const double* geom;  // kGeomFields x n SoA: mu xyz, quat wxyz, log_scale xy, opacity_raw, gamma_raw xy
+    const float* sh;     // n x 48 (coefficient-major, rgb interleaved), fp32
+    const float* table;  // levels x 2^log2 x features, fp32
+    const float* w1;     // hidden x n_in
+    const float* w2;     // hidden x hidden
+    const float* w3;     // 48 x hidden
+    nx_field_desc field;
+};
+
+struct FrameDev {
+    int W, H, K, tiles_x, tiles_y;
+    float* base;
+    int32_t* ids;
+    double* depths;
+    double* weights;
+    float* texture;
+    float* final_img;
+    float* residual;
+};
+
+// ---------------------------------------------------------------- launchers (nx_kernels.cu)
+struct PreprocessArgs {
+    SceneDev scene;
+    nx_settings st;
+    CamD cam;
+    int tiles_x, tiles_y;
+    double zmin_work;   // conservative camera-z bound of any hit (straddler refinement)
+    double* rec;        // REC_FIELDS x n
+    int32_t* cls;       // n
+    int4* ref_rect;     // n
+    int4* work_rect;    // n
+    uint64_t* key;      // n
+    int32_t* flag;      // n: 1 if the primitive enters the sort (work or reference mode)
+    int reference_lists;
+    FrameStatsD* stats;
+};
+void launch_preprocess(const PreprocessArgs& a, cudaStream_t s);
+
+// Gathers (key, id) of flagged primitives at their scanned positions (id-ascending).
+void launch_compact(const int32_t* flag, const int32_t* pos, const uint64_t* key, int64_t n,
+                    uint64_t* keys_out, uint32_t* ids_out, cudaStream_t s);
+
+// counts[r] = tiles of rect[ids[r]] (work or reference rect).
+void launch_rect_counts(const uint32_t* ids, int64_t n, const int4* rect, int32_t* counts,
+                        cudaStream_t s);
+
+// Emits (tile, id) for every tile of every sorted primitive's rect, in sorted
+// order (row-major tiles, renderer.cpp:106-110), and counts keys per tile.
+void launch_emit(const uint32_t* ids, const int32_t* offsets, int64_t n_sorted, int64_t n_keys,
+                 const int4* rect, int tiles_x, uint32_t* tile_keys, uint32_t* vals,
+                 int32_t* tile_counts, cudaStream_t s);
+
+struct CompositeArgs {
+    const double* rec;
+    int64_t n;
+    const float* sh;
+    const int32_t* list_ids;
+    const int32_t* tile_offsets;
+    nx_settings st;
+    CamD cam;
+    FrameDev fb;
+    int sh_degree;
+    int32_t* dbg_hits;   // optional: per-pixel hit ids (rows [dbg_y0, dbg_y1))
+    int32_t* dbg_counts;
+    int dbg_y0, dbg_y1, dbg_max;
+};
+void launch_composite(const CompositeArgs& a, cudaStream_t s);
+
+struct TextureArgs {
+    SceneDev scene;
+    nx_settings st;
+    CamD cam;
+    FrameDev fb;
+    FrameStatsD* stats;
+};
+int launch_texture(const TextureArgs& a, cudaStream_t s);  // returns NX_OK / NX_UNSUPPORTED
+
+}  // namespace nx

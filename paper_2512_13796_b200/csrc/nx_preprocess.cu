@@ -1,0 +1,289 @@
+// K1 preprocess + binning helpers.
+//
+// One thread per primitive, fp64 throughout. Restates, per primitive, the
+// first half of build_binning (renderer.cpp:52-100): activate (primitive.cpp:
+// 47-76), support radius (kernel.hpp:72-76), the four support corners, the
+// all_behind / all_visible classification, the centre depth and the padded
+// tile rect. It also emits the per-camera composite record and, for the
+// straddlers the reference bins into every tile (renderer.cpp:93-98), a
+// conservative "work rect" that provably contains every pixel whose ray can hit
+// the primitive: the work lists are order-preserving
+// subsequences of the reference lists that drop only provable misses.
+#include "nx_internal.cuh"
+
+namespace nx {
+
+namespace {
+
+struct D3 {
+    double x, y, z;
+};
+
+__device__ __forceinline__ D3 to_camera(const CamD& c, D3 p) {  // camera.hpp:26
+    return {c.R[0] * p.x + c.R[1] * p.y + c.R[2] * p.z + c.t[0],
+            c.R[3] * p.x + c.R[4] * p.y + c.R[5] * p.z + c.t[1],
+            c.R[6] * p.x + c.R[7] * p.y + c.R[8] * p.z + c.t[2]};
+}
+
+__device__ __forceinline__ int4 empty_rect() { return make_int4(1, 0, 1, 0); }
+
+__device__ __forceinline__ int rect_tiles(int4 r) {
+    return (r.y >= r.x && r.w >= r.z) ? (r.y - r.x + 1) * (r.w - r.z + 1) : 0;
+}
+
+// Conservative work rect of a straddler: clip the support rectangle (radii padded
+// by 1e-6) to camera-z >= zmin, project the clipped polygon, take its bounding box
+// padded by 2 px, and convert to tiles. Every hit has t > near_eps, hence
+// camera-z > near_eps * cos(ray, axis) >= 2*zmin, and alpha >= 1/255 implies
+// |u| <= ru, |v| <= rv (kernel.hpp:70-76).
+__device__ int4 straddler_work_rect(const CamD& cam, D3 mu, D3 a1, D3 a2, double zmin, int tile,
+                                    int tiles_x, int tiles_y) {
+    D3 poly[8];
+    const D3 c0 = to_camera(cam, {mu.x + a1.x + a2.x, mu.y + a1.y + a2.y, mu.z + a1.z + a2.z});
+    const D3 c1 = to_camera(cam, {mu.x + a1.x - a2.x, mu.y + a1.y - a2.y, mu.z + a1.z - a2.z});
+    const D3 c2 = to_camera(cam, {mu.x - a1.x - a2.x, mu.y - a1.y - a2.y, mu.z - a1.z - a2.z});
+    const D3 c3 = to_camera(cam, {mu.x - a1.x + a2.x, mu.y - a1.y + a2.y, mu.z - a1.z + a2.z});
+    const D3 in[4] = {c0, c1, c2, c3};
+    int m = 0;
+    for (int k = 0; k < 4; ++k) {  // Sutherland-Hodgman against z >= zmin
+        const D3 a = in[k], b = in[(k + 1) & 3];
+        const bool ia = a.z >= zmin, ib = b.z >= zmin;
+        if (ia) poly[m++] = a;
+        if (ia != ib) {
+            const double s = (zmin - a.z) / (b.z - a.z);
+            poly[m++] = {a.x + s * (b.x - a.x), a.y + s * (b.y - a.y), zmin};
+        }
+    }
+    if (m == 0) return empty_rect();
+    double px0 = 1e300, px1 = -1e300, py0 = 1e300, py1 = -1e300;
+    for (int k = 0; k < m; ++k) {
+        const double z = fmax(poly[k].z, zmin);
+        const double x = cam.fx * poly[k].x / z + cam.cx;
+        const double y = cam.fy * poly[k].y / z + cam.cy;
+        px0 = fmin(px0, x);
+        px1 = fmax(px1, x);
+        py0 = fmin(py0, y);
+        py1 = fmax(py1, y);
+    }
+    // pixel i has its centre at i + 0.5; pad 2 px on each side.
+    px0 = fmax(px0 - 2.5, -1.0);
+    py0 = fmax(py0 - 2.5, -1.0);
+    px1 = fmin(px1 + 1.5, static_cast<double>(cam.W) + 1.0);
+    py1 = fmin(py1 + 1.5, static_cast<double>(cam.H) + 1.0);
+    const int ix0 = static_cast<int>(floor(px0)), ix1 = static_cast<int>(ceil(px1));
+    const int iy0 = static_cast<int>(floor(py0)), iy1 = static_cast<int>(ceil(py1));
+    if (ix1 < 0 || iy1 < 0 || ix0 >= cam.W || iy0 >= cam.H || ix1 < ix0 || iy1 < iy0) return empty_rect();
+    return make_int4(clampi(ix0, 0, cam.W - 1) / tile, clampi(ix1, 0, cam.W - 1) / tile,
+                     clampi(iy0, 0, cam.H - 1) / tile, clampi(iy1, 0, cam.H - 1) / tile);
+}
+
+__global__ void __launch_bounds__(256) preprocess_kernel(const PreprocessArgs a) {
+    __shared__ unsigned long long s_cnt[8];
+    if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t n = a.scene.n;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    int cls = -1, kept = 0;
+    long long ref_keys = 0, work_keys = 0;
+    if (i < n) {
+        const double* g = a.scene.geom;
+        const D3 mu{g[0 * n + i], g[1 * n + i], g[2 * n + i]};
+        const double qw = g[3 * n + i], qx = g[4 * n + i], qy = g[5 * n + i], qz = g[6 * n + i];
+        // activate (primitive.cpp:62-75); inputs were validated at upload.
+        const double qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+        const double inv = 1.0 / qn;
+        const double w = inv * qw, x = inv * qx, y = inv * qy, z = inv * qz;
+        double R[9];  // quat_to_rotation (primitive.cpp:7-20)
+        R[0] = 1 - 2 * (y * y + z * z);
+        R[1] = 2 * (x * y - w * z);
+        R[2] = 2 * (x * z + w * y);
+        R[3] = 2 * (x * y + w * z);
+        R[4] = 1 - 2 * (x * x + z * z);
+        R[5] = 2 * (y * z - w * x);
+        R[6] = 2 * (x * z - w * y);
+        R[7] = 2 * (y * z + w * x);
+        R[8] = 1 - 2 * (x * x + y * y);
+        const double sx = exp(g[7 * n + i]), sy = exp(g[8 * n + i]);
+        const double op = sigmoid(g[9 * n + i]);
+        double gx = 1.0, gy = 1.0;
+        if (!a.st.no_gamma) {
+            gx = 1.0 + softplus(g[10 * n + i]);
+            gy = 1.0 + softplus(g[11 * n + i]);
+        }
+        const double ru = support_radius(op, gx), rv = support_radius(op, gy);
+        int4 ref = empty_rect(), work = empty_rect();
+        double depth = 0.0;
+        if (ru <= 0.0 || rv <= 0.0) {
+            cls = CLS_SUPPORT;
+        } else {
+            const double ku = ru * sx, kv = rv * sy;
+            const D3 du{ku * R[0], ku * R[3], ku * R[6]};
+            const D3 dv{kv * R[1], kv * R[4], kv * R[7]};
+            const D3 corners[4] = {
+                {(mu.x + du.x) + dv.x, (mu.y + du.y) + dv.y, (mu.z + du.z) + dv.z},
+                {(mu.x + du.x) - dv.x, (mu.y + du.y) - dv.y, (mu.z + du.z) - dv.z},
+                {(mu.x - du.x) + dv.x, (mu.y - du.y) + dv.y, (mu.z - du.z) + dv.z},
+                {(mu.x - du.x) - dv.x, (mu.y - du.y) - dv.y, (mu.z - du.z) - dv.z}};
+            const D3 cmu = to_camera(a.cam, mu);
+            bool all_behind = cmu.z < kProjectMinDepth;
+            bool all_visible = true;
+            double px0 = 1e300, px1 = -1e300, py0 = 1e300, py1 = -1e300;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const D3 q = to_camera(a.cam, corners[c]);
+                if (q.z < kProjectMinDepth) {  // camera.hpp:38-42
+                    all_visible = false;
+                    continue;
+                }
+                all_behind = false;
+                const double X = a.cam.fx * q.x / q.z + a.cam.cx;
+                const double Y = a.cam.fy * q.y / q.z + a.cam.cy;
+                px0 = X < px0 ? X : px0;  // std::min / std::max (renderer.cpp:71-74)
+                px1 = px1 < X ? X : px1;
+                py0 = Y < py0 ? Y : py0;
+                py1 = py1 < Y ? Y : py1;
+            }
+            depth = cmu.z;
+            if (all_behind && !all_visible) {
+                cls = CLS_BEHIND;
+            } else if (all_visible) {
+                const int ix0 = x86_to_int(floor(px0 - 1.5)), ix1 = x86_to_int(ceil(px1 + 0.5));
+                const int iy0 = x86_to_int(floor(py0 - 1.5)), iy1 = x86_to_int(ceil(py1 + 0.5));
+                if (ix1 < 0 || iy1 < 0 || ix0 >= a.cam.W || iy0 >= a.cam.H) {
+                    cls = CLS_OFFSCREEN;
+                } else {
+                    cls = CLS_RECT;
+                    const int tile = a.st.tile;
+                    ref = make_int4(clampi(ix0, 0, a.cam.W - 1) / tile, clampi(ix1, 0, a.cam.W - 1) / tile,
+                                    clampi(iy0, 0, a.cam.H - 1) / tile, clampi(iy1, 0, a.cam.H - 1) / tile);
+                    work = ref;
+                }
+            } else {
+                cls = CLS_STRADDLER;
+                ref = make_int4(0, a.tiles_x - 1, 0, a.tiles_y - 1);
+                const double pu = ku * (1.0 + 1e-6), pv = kv * (1.0 + 1e-6);
+                work = straddler_work_rect(a.cam, mu, {pu * R[0], pu * R[3], pu * R[6]},
+                                           {pv * R[1], pv * R[4], pv * R[7]}, a.zmin_work, a.st.tile,
+                                           a.tiles_x, a.tiles_y);
+                // Degenerate near-threshold opacity: keep the reference's all-tile list.
+                if (log(op / kAlphaMin) < 1e-3) work = ref;
+                kept = rect_tiles(work) > 0;
+            }
+        }
+        if (a.reference_lists) work = (cls == CLS_RECT || cls == CLS_STRADDLER) ? ref : empty_rect();
+        a.cls[i] = cls;
+        a.ref_rect[i] = ref;
+        a.work_rect[i] = work;
+        a.key[i] = depth_key(depth);
+        const int wk = rect_tiles(work);
+        a.flag[i] = wk > 0;
+        ref_keys = rect_tiles(ref);
+        work_keys = wk;
+        if (wk > 0) {
+            // Composite record: everything intersect() (intersect.hpp:23-42) needs per primitive.
+            double* r = a.rec;
+            const double nx_ = R[2], ny_ = R[5], nz_ = R[8];
+            r[REC_NUM * n + i] = (mu.x - a.cam.o[0]) * nx_ + (mu.y - a.cam.o[1]) * ny_ + (mu.z - a.cam.o[2]) * nz_;
+            r[REC_NX * n + i] = nx_;
+            r[REC_NY * n + i] = ny_;
+            r[REC_NZ * n + i] = nz_;
+            r[REC_V1X * n + i] = R[0];
+            r[REC_V1Y * n + i] = R[3];
+            r[REC_V1Z * n + i] = R[6];
+            r[REC_V2X * n + i] = R[1];
+            r[REC_V2Y * n + i] = R[4];
+            r[REC_V2Z * n + i] = R[7];
+            r[REC_MUX * n + i] = mu.x;
+            r[REC_MUY * n + i] = mu.y;
+            r[REC_MUZ * n + i] = mu.z;
+            r[REC_SX * n + i] = sx;
+            r[REC_SY * n + i] = sy;
+            r[REC_OP * n + i] = op;
+            r[REC_GX * n + i] = gx;
+            r[REC_GY * n + i] = gy;
+            // |u| > ru implies alpha < 1/255 (margin 1e-6 relative, exact decision kept
+            // for everything inside); disabled when ln(255 o) is tiny.
+            const bool safe = log(op / kAlphaMin) >= 1e-3;
+            r[REC_ULIM * n + i] = safe ? ru * (1.0 + 1e-6) * sx : INFINITY;
+            r[REC_VLIM * n + i] = safe ? rv * (1.0 + 1e-6) * sy : INFINITY;
+        }
+    }
+    // block-aggregated statistics
+    if (cls >= 0) atomicAdd(&s_cnt[cls], 1ull);
+    if (kept) atomicAdd(&s_cnt[5], 1ull);
+    if (ref_keys) atomicAdd(&s_cnt[6], static_cast<unsigned long long>(ref_keys));
+    if (work_keys) atomicAdd(&s_cnt[7], static_cast<unsigned long long>(work_keys));
+    __syncthreads();
+    if (threadIdx.x < 8 && s_cnt[threadIdx.x]) {
+        unsigned long long* dst = threadIdx.x < 5 ? &a.stats->cls[threadIdx.x]
+                                  : threadIdx.x == 5 ? &a.stats->straddlers_kept
+                                  : threadIdx.x == 6 ? &a.stats->tile_keys
+                                                     : &a.stats->work_keys;
+        atomicAdd(dst, s_cnt[threadIdx.x]);
+    }
+}
+
+__global__ void compact_kernel(const int32_t* flag, const int32_t* pos, const uint64_t* key, int64_t n,
+                               uint64_t* keys_out, uint32_t* ids_out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n && flag[i]) {
+        keys_out[pos[i]] = key[i];
+        ids_out[pos[i]] = static_cast<uint32_t>(i);
+    }
+}
+
+__global__ void rect_counts_kernel(const uint32_t* ids, int64_t n, const int4* rect, int32_t* counts) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r < n) counts[r] = rect_tiles(rect[ids[r]]);
+}
+
+// One thread per emitted key: binary search of the owning sorted primitive.
+__global__ void emit_kernel(const uint32_t* ids, const int32_t* offsets, int64_t n_sorted, int64_t n_keys,
+                            const int4* rect, int tiles_x, uint32_t* tile_keys, uint32_t* vals,
+                            int32_t* tile_counts) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n_keys) return;
+    int64_t lo = 0, hi = n_sorted - 1;  // last r with offsets[r] <= k
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (offsets[mid] <= k) lo = mid;
+        else hi = mid - 1;
+    }
+    const uint32_t id = ids[lo];
+    const int4 rc = rect[id];
+    const int j = static_cast<int>(k - offsets[lo]);
+    const int w = rc.y - rc.x + 1;
+    const int tile = (rc.z + j / w) * tiles_x + rc.x + j % w;
+    tile_keys[k] = static_cast<uint32_t>(tile);
+    vals[k] = id;
+    atomicAdd(&tile_counts[tile], 1);
+}
+
+}  // namespace
+
+void launch_preprocess(const PreprocessArgs& a, cudaStream_t s) {
+    if (a.scene.n <= 0) return;
+    const unsigned blocks = static_cast<unsigned>((a.scene.n + 255) / 256);
+    preprocess_kernel<<<blocks, 256, 0, s>>>(a);
+}
+
+void launch_compact(const int32_t* flag, const int32_t* pos, const uint64_t* key, int64_t n,
+                    uint64_t* keys_out, uint32_t* ids_out, cudaStream_t s) {
+    if (n <= 0) return;
+    compact_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(flag, pos, key, n, keys_out, ids_out);
+}
+
+void launch_rect_counts(const uint32_t* ids, int64_t n, const int4* rect, int32_t* counts, cudaStream_t s) {
+    if (n <= 0) return;
+    rect_counts_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(ids, n, rect, counts);
+}
+
+void launch_emit(const uint32_t* ids, const int32_t* offsets, int64_t n_sorted, int64_t n_keys,
+                 const int4* rect, int tiles_x, uint32_t* tile_keys, uint32_t* vals, int32_t* tile_counts,
+                 cudaStream_t s) {
+    if (n_keys <= 0) return;
+    emit_kernel<<<static_cast<unsigned>((n_keys + 255) / 256), 256, 0, s>>>(ids, offsets, n_sorted, n_keys, rect,
+                                                                           tiles_x, tile_keys, vals, tile_counts);
+}
+
+}  // namespace nx

@@ -1,0 +1,33 @@
+// Device scan + stable LSD radix sort used by tile binning.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nx {
+
+constexpr int kScanItems = 4;        // per thread
+constexpr int kScanThreads = 1024;
+constexpr int kScanTile = kScanItems * kScanThreads;
+constexpr int kRadixThreads = 256;
+constexpr int kRadixTile = 4096;     // items per block per pass
+constexpr int kRadixBits = 8;
+constexpr int kRadixBuckets = 1 << kRadixBits;
+
+// Exclusive prefix sum of n int32 values (n <= kScanTile^2). out may alias in.
+// If total != nullptr the grand total is stored there (device).
+// Scratch: scan_scratch_ints(n) ints.
+size_t scan_scratch_ints(int64_t n);
+void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int32_t* total, int32_t* scratch,
+                    cudaStream_t stream);
+
+// Stable LSD radix sort of (key, value) pairs over key bits [begin_bit, end_bit).
+// Ping-pongs between (keys, vals) and (keys_alt, vals_alt); returns true if the
+// sorted result ended in the *_alt buffers. Scratch: radix_scratch_ints(n) ints.
+size_t radix_scratch_ints(int64_t n);
+bool radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,
+                          int64_t n, int begin_bit, int end_bit, int32_t* scratch, cudaStream_t stream);
+bool radix_sort_pairs_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
+                          int64_t n, int begin_bit, int end_bit, int32_t* scratch, cudaStream_t stream);
+
+}  // namespace nx
