@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark of the Nexel render hot path (BASELINE.json metric):
+rendered 1080p frames/sec at 400K nexels on N B200s (+ % HBM roofline).
+
+A step = every rank renders one view (collection_pass + texturing_pass) of the
+400K-nexel stump_like scene at 1920x1080, K=2 (BASELINE.json configs[1]); views
+are dealt round-robin from the 256-view ring (config 3), so per-GPU work is
+fixed as N grows ("scaling": "weak") and there is no collective on the data path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun (N>1) each rank drives its own GPU; timing is CUDA events on the
+render stream, bracketed by a barrier + synchronize, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rendered 1080p frames/sec at 400K nexels (1/2/4/8 B200) + % HBM roofline"
+UNIT = "frames/s"
+N_VIEWS = 256
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--nexels", type=int, default=400_000)
+    p.add_argument("--width", type=int, default=1920)
+    p.add_argument("--height", type=int, default=1080)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU-baseline work")
+    return p.parse_args()
+
+
+def workload(args):
+    return {
+        "workload": f"config 2/3: stump_like {args.nexels} nexels, {args.width}x{args.height}, K=2, "
+                    f"views dealt round-robin from a {N_VIEWS}-view ring",
+        "nexels": args.nexels, "width": args.width, "height": args.height, "top_k": 2,
+        "scene": "stump_like(seed 2512, c=1.0, R_ground=4.0), field grid_init 1e-4 (SURVEY.md §8(d))",
+        "l2": "inputs larger than L2 (scene 115 MB fp64/fp32 + 134 MB hash table), view changes every step",
+    }
+
+
+# ---------------------------------------------------------------- algorithmic bytes
+def frame_bytes(n, P, H, W, K, Q):
+    """B_frame = 240 N + 8 P + (28 + 24 K) H W + 1024 Q + 36,864."""
+    return 240 * n + 8 * P + (28 + 24 * K) * H * W + 1024 * Q + 36_864
+
+
+def stage_bytes(stage, n, P, Pw, H, W, K, Q):
+    """Algorithmic bytes of one launch of a stage."""
+    if stage == "texture":   # gathers 1024/query, reads ids/depth/weight + base, writes texture + final, MLP weights
+        return 1024 * Q + (12 * K + 12) * H * W + (12 * K + 12) * H * W + 36_864
+    if stage == "composite":  # reads the work lists (4/key), writes base 12 + residual 4 + K x (id 4 + depth 4 + weight 4)
+        return 4 * Pw + (16 + 12 * K) * H * W
+    if stage == "preprocess":  # reads 60 params (fp32-counted) per primitive
+        return 240 * n
+    return 8 * P
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join("/tmp", f"nx_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "50", "-i", str(self.device)], stdout=self.fh,
+                                         stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx = max(mx, float(parts[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- distributed plumbing
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local, dist
+
+
+def max_over_ranks(dist, value: float, local: int) -> float:
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# ---------------------------------------------------------------- CPU baseline (the reference on host cores)
+def cpu_reference_sample(scene, view_cam, budget_s: float):
+    """Reference render path (oracle/_ref, compiled in place) on all host cores over a
+    band of rows of the view; frame time = binning + (band - binning) * H / rows."""
+    from oracle.pyoracle import Oracle, Reference
+    import paper_2512_13796_b200 as nx
+    cores = os.cpu_count() or 1
+    os.environ["NEXEL_THREADS"] = str(cores)
+    try:
+        impl, kind = Reference(), "reference"
+    except ImportError:
+        impl, kind = Oracle(), "port"
+        cores = 1
+    H = view_cam.height
+
+    def band_cam(y0, rows):
+        return nx.Camera(view_cam.width, rows, view_cam.fx, view_cam.fy, view_cam.cx, view_cam.cy - y0,
+                         view_cam.R, view_cam.t)
+
+    # binning cost (build_binning over all primitives; independent of the band size)
+    t_bin = 0.0
+    if kind == "reference":
+        t0 = time.perf_counter()
+        impl.tile_lists(scene, view_cam)
+        t_bin = time.perf_counter() - t0
+    rows = 32
+    y0 = (H // 2 // 16) * 16
+    t0 = time.perf_counter()
+    impl.render(scene, band_cam(y0, rows))
+    t_band = time.perf_counter() - t0
+    per_row = max(t_band - t_bin, 1e-3) / rows
+    rows = int(min(max(16, (budget_s / 3 - t_bin) / per_row), H - y0))
+    rows = max(16, (rows // 16) * 16)
+    times = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        impl.render(scene, band_cam(y0, rows))
+        times.append(time.perf_counter() - t0)
+    t_band = statistics.median(times)
+    frame_s = t_bin + max(t_band - t_bin, 0.0) * H / rows
+    sample = (f"rows {y0}-{y0 + rows} of {H} of view 0 (median of 3); frame time = binning {t_bin:.2f}s + "
+              f"(band {t_band:.2f}s - binning) x {H}/{rows}")
+    return {"value": 1.0 / frame_s, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
+            "lib": os.path.basename(getattr(impl, "path", "oracle")), "frame_seconds": frame_s}
+
+
+def run_reference_arm(args):
+    world, rank, local, dist = dist_setup(args)
+    if rank != 0:
+        barrier(dist)
+        return
+    import paper_2512_13796_b200 as nx
+    scene = nx.stump_like(args.nexels)
+    cam = nx.ring_camera(0, N_VIEWS, args.width, args.height)
+    from oracle.pyoracle import Oracle, Reference
+    cores = os.cpu_count() or 1
+    os.environ["NEXEL_THREADS"] = str(cores)
+    try:
+        impl, kind = Reference(), "reference"
+    except ImportError:
+        impl, kind = Oracle(), "port"
+        cores = 1
+    H = cam.height
+    y0 = (H // 2 // 16) * 16
+    rows = 32
+
+    def band(y0, rows):
+        return nx.Camera(cam.width, rows, cam.fx, cam.fy, cam.cx, cam.cy - y0, cam.R, cam.t)
+
+    # size the per-step sample so the whole run stays within a few minutes
+    t0 = time.perf_counter()
+    impl.render(scene, band(y0, rows))
+    dt = time.perf_counter() - t0
+    per_step_budget = max(1.0, 150.0 / max(args.steps + args.warmup, 1))
+    if dt < per_step_budget / 2:
+        rows = int(min(H - y0, max(16, rows * per_step_budget / max(dt, 1e-3) * 0.8)))
+        rows = max(16, rows // 16 * 16)
+    for _ in range(args.warmup):
+        impl.render(scene, band(y0, rows))
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        impl.render(scene, band(y0, rows))
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    fps = (args.steps * rows / H) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload(args),
+        "cpu_baseline": {"value": fps, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"each step renders rows {y0}-{y0 + rows} of {H} of view 0 "
+                                   f"(frame-equivalent = rows/H per step, binning included per step)"},
+        "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    barrier(dist)
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    world, rank, local, dist = dist_setup(args)
+    import torch
+    import paper_2512_13796_b200 as nx
+    from paper_2512_13796_b200 import _abi
+
+    torch.cuda.set_device(local)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+
+    scene = nx.stump_like(args.nexels)
+    r = nx.Renderer(local)
+    ds = r.upload(scene)
+    fr = r.frame()
+    stream = torch.cuda.ExternalStream(r.stream, device=torch.device("cuda", local))
+    n_steps = args.warmup + args.steps
+    views = [(s * world + rank) % N_VIEWS for s in range(n_steps)]
+    cams = {v: nx.ring_camera(v, N_VIEWS, args.width, args.height) for v in set(views)}
+
+    # per-view work statistics (untimed pre-pass): P, work keys, Q
+    vstats = {}
+    for v in sorted(set(views[args.warmup:])):
+        r.render(ds, cams[v], fr)
+        vstats[v] = fr.stats()
+    H, W, K = args.height, args.width, 2
+
+    for s in range(args.warmup):
+        r.render(ds, cams[views[s]], fr)
+    r.synchronize()
+
+    # ---- timed region: device time of K steps (CUDA events on the render stream)
+    r.set_profiling(True)
+    r.stage_times()  # reset accumulators
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = r.lib.nx_launch_count()
+    barrier(dist)
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for s in range(args.warmup, n_steps):
+        r.render(ds, cams[views[s]], fr)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier(dist)
+    launches = int(r.lib.nx_launch_count() - launches0)
+    clk = clocks.stop()
+    ms_local = ev0.elapsed_time(ev1)
+    stage_ms, prof_frames = r.stage_times()
+    r.set_profiling(False)
+    ms = max_over_ranks(dist, ms_local, local)
+    frames_total = args.steps * world
+    fps = frames_total / (ms / 1e3)
+
+    # ---- e2e: the same metric through the public C-ABI with host buffers: camera in,
+    # render, full FrameBuffers read back into pinned host memory, every step.
+    npix = H * W
+    host = {
+        "base": torch.empty(npix * 3, dtype=torch.float32, pin_memory=True),
+        "ids": torch.empty(npix * K, dtype=torch.int32, pin_memory=True),
+        "depths": torch.empty(npix * K, dtype=torch.float64, pin_memory=True),
+        "weights": torch.empty(npix * K, dtype=torch.float64, pin_memory=True),
+        "texture": torch.empty(npix * K * 3, dtype=torch.float32, pin_memory=True),
+        "final_img": torch.empty(npix * 3, dtype=torch.float32, pin_memory=True),
+        "residual": torch.empty(npix, dtype=torch.float32, pin_memory=True),
+    }
+    hf = _abi.nx_host_frame()
+    for k, t in host.items():
+        setattr(hf, k, t.data_ptr())
+    d2h = sum(t.numel() * t.element_size() for t in host.values())
+    h2d = C.sizeof(_abi.nx_camera)
+    barrier(dist)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for s in range(args.warmup, n_steps):
+        r.render(ds, cams[views[s]], fr)
+        r._check(r.lib.nx_frame_download(r.ctx, fr.handle, C.byref(hf), None))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(dist)
+    e2e_ms = max_over_ranks(dist, e0.elapsed_time(e1), local)
+    e2e_fps = frames_total / (e2e_ms / 1e3)
+
+    # ---- roofline of the dominant stage (algorithmic bytes per launch / mean launch time)
+    timed_views = views[args.warmup:]
+    mean = lambda key: sum(vstats[v][key] for v in timed_views) / len(timed_views)
+    P, Pw, Q = mean("tile_keys"), mean("work_keys"), mean("n_queries")
+    dom = max(stage_ms, key=stage_ms.get)
+    dom_bytes = stage_bytes(dom, args.nexels, P, Pw, H, W, K, Q)
+    achieved = dom_bytes / (stage_ms[dom] / 1e3) / 1e9
+    fbytes = frame_bytes(args.nexels, P, H, W, K, Q)
+    frame_gbs = fbytes * (args.steps / (ms_local / 1e3)) / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample(scene, cams[views[0]] if views else nx.ring_camera(0), args.cpu_budget)
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload(args),
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
+                         "bytes_per_launch": dom_bytes, "launch_ms": stage_ms[dom]},
+            "frame_roofline": {"bytes_per_frame": fbytes, "achieved": frame_gbs, "peak": hbm_peak, "unit": "GB/s",
+                               "frac": frame_gbs / hbm_peak, "formula": "240N + 8P + (28+24K)HW + 1024Q + 36864"},
+            "stages_ms": stage_ms, "profiled_frames": prof_frames,
+            "work": {"tile_keys_P": P, "work_keys": Pw, "queries_Q": Q},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "path": "nx_render + nx_frame_download (all FrameBuffers) into pinned host memory"},
+            "gpu_launches": launches, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    fr.close()
+    ds.close()
+    r.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

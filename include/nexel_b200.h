@@ -149,8 +149,12 @@ int nx_ctx_synchronize(nx_ctx* ctx);
 #define NX_STAGE_TEXTURE 5
 #define NX_NUM_STAGES 6
 int nx_ctx_set_profiling(nx_ctx* ctx, int enable);
-int nx_ctx_stage_times(nx_ctx* ctx, float* ms, int n);  /* last frame; synchronises */
+/* Mean per-stage device time (ms per frame) over the profiled frames since the last
+ * call, then resets; synchronises. Stage events bracket each stage on the stream. */
+int nx_ctx_stage_times(nx_ctx* ctx, float* ms, int n, int* frames);
 const char* nx_stage_name(int stage);
+/* Number of kernels this library has launched (all contexts, host-side count). */
+uint64_t nx_launch_count(void);
 
 /* ---- scene (Scene, scene.hpp:25-32) ----------------------------------- */
 /* nexels: n*60 doubles in Nexel field order (primitive.hpp:21-28): mu[3],

@@ -147,8 +147,9 @@ SIGNATURES = [
     ("nx_ctx_stream", P, [P]),
     ("nx_ctx_synchronize", C.c_int, [P]),
     ("nx_ctx_set_profiling", C.c_int, [P, C.c_int]),
-    ("nx_ctx_stage_times", C.c_int, [P, PF, C.c_int]),
+    ("nx_ctx_stage_times", C.c_int, [P, PF, C.c_int, C.POINTER(C.c_int)]),
     ("nx_stage_name", C.c_char_p, [C.c_int]),
+    ("nx_launch_count", C.c_uint64, []),
     ("nx_scene_create", C.c_int,
      [P, C.POINTER(nx_settings), I64, PD, C.POINTER(nx_field_desc), PD, PD, PD, PD, C.POINTER(P)]),
     ("nx_scene_set_settings", C.c_int, [P, P, C.POINTER(nx_settings)]),

@@ -340,10 +340,12 @@ class Renderer:
     def set_profiling(self, on: bool):
         self._check(self.lib.nx_ctx_set_profiling(self.ctx, int(on)))
 
-    def stage_times(self) -> dict:
+    def stage_times(self):
+        """Mean per-stage device ms per frame since the last call (and the frame count)."""
         ms = (C.c_float * _abi.NX_NUM_STAGES)()
-        self._check(self.lib.nx_ctx_stage_times(self.ctx, ms, _abi.NX_NUM_STAGES))
-        return {name: float(ms[i]) for i, name in enumerate(_abi.STAGE_NAMES)}
+        frames = C.c_int(0)
+        self._check(self.lib.nx_ctx_stage_times(self.ctx, ms, _abi.NX_NUM_STAGES, C.byref(frames)))
+        return {name: float(ms[i]) for i, name in enumerate(_abi.STAGE_NAMES)}, frames.value
 
     # ---- parity / debug
     def tile_lists(self, dscene: DeviceScene, cam: Camera, reference_lists: bool = True):

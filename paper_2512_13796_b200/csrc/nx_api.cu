@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -26,6 +27,10 @@
 #include "nx_sort.cuh"
 
 using namespace nx;
+
+namespace nx {
+void count_launch(int n);
+}
 
 namespace {
 
@@ -53,9 +58,13 @@ struct DevBuf {
     }
 };
 
+std::atomic<unsigned long long> g_launches{0};
+
 const char* kStageNames[NX_NUM_STAGES] = {"preprocess", "depth_sort", "emit", "tile_sort", "composite", "texture"};
 
 }  // namespace
+
+void nx::count_launch(int n) { g_launches.fetch_add(static_cast<unsigned long long>(n), std::memory_order_relaxed); }
 
 struct nx_ctx {
     int device = 0;
@@ -70,7 +79,9 @@ struct nx_ctx {
     int32_t* h_pinned = nullptr;  // small readbacks
     bool profiling = false;
     cudaEvent_t ev[NX_NUM_STAGES + 1] = {};
-    bool ev_valid = false;
+    bool ev_pending = false;          // a profiled frame whose events are not folded yet
+    double stage_acc[NX_NUM_STAGES] = {};
+    int stage_frames = 0;
 };
 
 struct nx_scene {
@@ -229,6 +240,19 @@ void record(nx_ctx* c, int stage, cudaStream_t s) {
     if (c->profiling) cudaEventRecord(c->ev[stage], s);
 }
 
+// Folds the previous profiled frame's stage events into the running sums. Called
+// where the stream is already synchronised, so it never adds a sync of its own.
+void fold_stage_times(nx_ctx* c) {
+    if (!c->ev_pending) return;
+    for (int i = 0; i < NX_NUM_STAGES; ++i) {
+        float v = 0.f;
+        if (cudaEventElapsedTime(&v, c->ev[i], c->ev[i + 1]) == cudaSuccess) c->stage_acc[i] += v;
+    }
+    cudaGetLastError();
+    c->stage_frames += 1;
+    c->ev_pending = false;
+}
+
 int check_inputs(nx_ctx* c, const nx_scene* scene, const nx_camera* cam) {
     if (!c || !scene || !cam) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
     int st;
@@ -266,6 +290,8 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
     NX_CUDA(c, c->scratch.ensure(scratch_ints * sizeof(int32_t)));
     NX_CUDA(c, cudaMemsetAsync(f->stats, 0, sizeof(FrameStatsD), s));
 
+    NX_CUDA(c, cudaStreamSynchronize(s));  // the previous frame on this stream is complete
+    fold_stage_times(c);
     record(c, NX_STAGE_PREPROCESS, s);
     PreprocessArgs pa;
     pa.scene = scene_dev(scene);
@@ -291,6 +317,7 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
     NX_CUDA(c, cudaMemcpyAsync(c->h_pinned, d_total, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     NX_CUDA(c, cudaStreamSynchronize(s));
     const int64_t n_sorted = n > 0 ? c->h_pinned[0] : 0;
+    (void)0;
     record(c, NX_STAGE_DEPTH_SORT, s);
     launch_compact(c->flag.as<int32_t>(), c->pos.as<int32_t>(), c->key.as<uint64_t>(), n, c->skeys_a.as<uint64_t>(),
                    c->sids_a.as<uint32_t>(), s);
@@ -378,6 +405,7 @@ int texturing(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* 
     const int st = launch_texture(ta, s);
     if (st) return set_err(c, st, "texture field shape not supported (n_in <= 64, n_hidden <= 128)");
     record(c, NX_NUM_STAGES, s);
+    if (c->profiling) c->ev_pending = true;
     NX_CUDA(c, cudaGetLastError());
     return NX_OK;
 }
@@ -385,6 +413,8 @@ int texturing(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* 
 }  // namespace
 
 extern "C" {
+
+uint64_t nx_launch_count(void) { return g_launches.load(); }
 
 const char* nx_version(void) { return "nexel-b200 0.1 (sm_100a)"; }
 
@@ -464,15 +494,15 @@ int nx_ctx_set_profiling(nx_ctx* c, int enable) {
     return NX_OK;
 }
 
-int nx_ctx_stage_times(nx_ctx* c, float* ms, int n) {
+int nx_ctx_stage_times(nx_ctx* c, float* ms, int n, int* frames) {
     if (!c || !ms) return NX_INVALID_ARGUMENT;
     NX_CUDA(c, cudaDeviceSynchronize());
-    for (int i = 0; i < n && i < NX_NUM_STAGES; ++i) {
-        float v = 0.f;
-        if (cudaEventElapsedTime(&v, c->ev[i], c->ev[i + 1]) != cudaSuccess) v = -1.f;
-        ms[i] = v;
-    }
-    cudaGetLastError();
+    fold_stage_times(c);
+    for (int i = 0; i < n && i < NX_NUM_STAGES; ++i)
+        ms[i] = c->stage_frames ? static_cast<float>(c->stage_acc[i] / c->stage_frames) : 0.f;
+    if (frames) *frames = c->stage_frames;
+    for (double& v : c->stage_acc) v = 0.0;
+    c->stage_frames = 0;
     return NX_OK;
 }
 
@@ -725,6 +755,8 @@ int nx_debug_pixel_hits(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, 
     nx_frame* f = nullptr;
     if ((st = nx_frame_create(c, cam->width, cam->height, scene->st.top_k, &f))) return st;
     cudaStream_t s = c->stream;
+    NX_CUDA(c, cudaMemsetAsync(c->dbg_hits.p, 0xff, q * max_hits * sizeof(int32_t), s));  // -1 = no hit
+    NX_CUDA(c, cudaMemsetAsync(c->dbg_counts.p, 0, q * sizeof(int32_t), s));
     st = collection(c, scene, cam, f, s, c->dbg_hits.as<int32_t>(), c->dbg_counts.as<int32_t>(), y0, y1, max_hits);
     if (!st) {
         cudaError_t e = cudaMemcpyAsync(hits, c->dbg_hits.p, q * max_hits * sizeof(int32_t), cudaMemcpyDeviceToHost, s);

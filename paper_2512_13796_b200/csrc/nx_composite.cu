@@ -267,6 +267,7 @@ void launch_k(const CompositeArgs& a, cudaStream_t s) {
 }  // namespace
 
 void launch_composite(const CompositeArgs& a, cudaStream_t s) {
+    count_launch();
     if (a.dbg_hits) launch_k<true>(a, s);
     else launch_k<false>(a, s);
 }

@@ -150,7 +150,10 @@ struct FrameDev {
     float* residual;
 };
 
-// ---------------------------------------------------------------- launchers (nx_kernels.cu)
+// Host-side count of kernel launches issued by this library (all contexts).
+void count_launch(int n = 1);
+
+// ---------------------------------------------------------------- launchers
 struct PreprocessArgs {
     SceneDev scene;
     nx_settings st;

@@ -264,17 +264,20 @@ __global__ void emit_kernel(const uint32_t* ids, const int32_t* offsets, int64_t
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t s) {
     if (a.scene.n <= 0) return;
     const unsigned blocks = static_cast<unsigned>((a.scene.n + 255) / 256);
+    count_launch();
     preprocess_kernel<<<blocks, 256, 0, s>>>(a);
 }
 
 void launch_compact(const int32_t* flag, const int32_t* pos, const uint64_t* key, int64_t n,
                     uint64_t* keys_out, uint32_t* ids_out, cudaStream_t s) {
     if (n <= 0) return;
+    count_launch();
     compact_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(flag, pos, key, n, keys_out, ids_out);
 }
 
 void launch_rect_counts(const uint32_t* ids, int64_t n, const int4* rect, int32_t* counts, cudaStream_t s) {
     if (n <= 0) return;
+    count_launch();
     rect_counts_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(ids, n, rect, counts);
 }
 
@@ -282,6 +285,7 @@ void launch_emit(const uint32_t* ids, const int32_t* offsets, int64_t n_sorted, 
                  const int4* rect, int tiles_x, uint32_t* tile_keys, uint32_t* vals, int32_t* tile_counts,
                  cudaStream_t s) {
     if (n_keys <= 0) return;
+    count_launch();
     emit_kernel<<<static_cast<unsigned>((n_keys + 255) / 256), 256, 0, s>>>(ids, offsets, n_sorted, n_keys, rect,
                                                                            tiles_x, tile_keys, vals, tile_counts);
 }

@@ -164,6 +164,7 @@ bool radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, i
         uint32_t* vi = in_alt ? vals_alt : vals;
         K* ko = in_alt ? keys : keys_alt;
         uint32_t* vo = in_alt ? vals : vals_alt;
+        count_launch(2);
         radix_hist_kernel<K><<<n_blocks, kRadixThreads, 0, stream>>>(ki, n, bit, hist, n_blocks);
         scan_exclusive(hist, hist, hist_n, nullptr, scan_scratch, stream);
         radix_scatter_kernel<K><<<n_blocks, kRadixThreads, 0, stream>>>(ki, vi, ko, vo, n, bit, hist, n_blocks);
@@ -184,10 +185,12 @@ void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int32_t* total, 
     }
     const int64_t n_blocks = (n + kScanTile - 1) / kScanTile;
     if (n_blocks == 1) {
+        count_launch(1);
         scan_single_kernel<<<1, kScanThreads, 0, stream>>>(in, out, n, total, nullptr);
         return;
     }
     // n_blocks <= kScanTile is required (n <= 16.7M).
+    count_launch(3);
     scan_reduce_kernel<<<static_cast<unsigned>(n_blocks), kScanThreads, 0, stream>>>(in, n, scratch);
     scan_single_kernel<<<1, kScanThreads, 0, stream>>>(scratch, scratch, n_blocks, nullptr, nullptr);
     scan_single_kernel<<<static_cast<unsigned>(n_blocks), kScanThreads, 0, stream>>>(in, out, n, total,

@@ -6,6 +6,8 @@
 
 namespace nx {
 
+void count_launch(int n);
+
 constexpr int kScanItems = 4;        // per thread
 constexpr int kScanThreads = 1024;
 constexpr int kScanTile = kScanItems * kScanThreads;

@@ -231,6 +231,7 @@ void launch_tex(const TextureArgs& a, cudaStream_t s) {
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(texture_kernel<NIN, NH, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
+    count_launch();
     texture_kernel<NIN, NH, F><<<blocks, threads, smem, s>>>(a);
 }
 
@@ -240,7 +241,7 @@ int launch_texture(const TextureArgs& a, cudaStream_t s) {
     const int64_t npix = static_cast<int64_t>(a.cam.W) * a.cam.H;
     if (a.fb.K == 0) {
         if (npix * 3 > 0)
-            copy_base_kernel<<<static_cast<unsigned>((npix * 3 + 255) / 256), 256, 0, s>>>(a.fb.base, a.fb.final_img,
+            count_launch(), copy_base_kernel<<<static_cast<unsigned>((npix * 3 + 255) / 256), 256, 0, s>>>(a.fb.base, a.fb.final_img,
                                                                                          npix * 3);
         return NX_OK;
     }

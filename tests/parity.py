@@ -1,0 +1,48 @@
+"""Shared parity checks: the north-star bar (BASELINE.json) as assertions.
+
+Discrete outputs are bit-exact (ids, tile lists, contributor lists); colour
+outputs are within max-abs 1e-3 with PSNR >= 60 dB against the reference image.
+fp64 contributor data (depths, weights) is checked to 1e-9 relative.
+"""
+import numpy as np
+
+RGB_TOL = 1e-3       # north star: RGB/alpha max-abs 1e-3
+PSNR_MIN = 60.0      # north star: PSNR >= 60 dB vs the reference image
+F64_RTOL = 1e-9      # depths / weights / residual are computed in fp64
+
+
+def psnr(a, b):
+    mse = float(np.mean((np.asarray(a, np.float64) - np.asarray(b, np.float64)) ** 2))
+    return float("inf") if mse == 0 else 10.0 * np.log10(1.0 / mse)
+
+
+def compare_frames(gpu, ref, *, rgb_tol=RGB_TOL, check_psnr=True):
+    """gpu: DeviceFrame download (device dtypes); ref: fp64 FrameBuffers-like."""
+    rep = {}
+    assert gpu.ids.shape == ref.ids.shape
+    mism = int(np.count_nonzero(gpu.ids != ref.ids))
+    rep["ids_mismatch"] = mism
+    assert mism == 0, f"{mism} slot ids differ"
+    occupied = ref.ids >= 0
+    for k in ("depths", "weights"):
+        a, b = getattr(gpu, k), getattr(ref, k)
+        err = np.abs(a - b)
+        rep[k] = float(err.max()) if err.size else 0.0
+        assert np.all(err <= F64_RTOL * np.maximum(np.abs(b), 1e-12) + 1e-15), f"{k} max err {rep[k]}"
+        assert np.all(a[~occupied] == 0.0)
+    r = np.abs(gpu.residual.astype(np.float64) - ref.residual)
+    rep["residual"] = float(r.max()) if r.size else 0.0
+    assert rep["residual"] <= 1e-6
+    for k in ("base", "texture", "final_img"):
+        a, b = getattr(gpu, k).astype(np.float64), getattr(ref, k)
+        rep[k] = float(np.abs(a - b).max()) if a.size else 0.0
+        assert rep[k] <= rgb_tol, f"{k} max-abs {rep[k]} > {rgb_tol}"
+    if check_psnr and gpu.final_img.size:
+        rep["psnr"] = psnr(gpu.final_img, ref.final_img)
+        assert rep["psnr"] >= PSNR_MIN, f"PSNR {rep['psnr']:.1f} dB"
+    return rep
+
+
+def is_subsequence(sub, full):
+    it = iter(full.tolist())
+    return all(x in it for x in sub.tolist())

@@ -1,0 +1,251 @@
+"""GPU parity of the sm_100a render path against the reference (oracle/_ref, the
+reference compiled in place) and the C restatement (oracle/), on the same
+seeded inputs. The cases follow the reference's own render tests
+(proj/tests/test_renderer.cpp, test_oracle.cpp, acceptance.cpp criteria 2-3)
+plus the BASELINE.json configs 1 and 2 (stump_like scenes, ring cameras).
+"""
+import numpy as np
+import pytest
+
+import paper_2512_13796_b200 as nx
+from paper_2512_13796_b200 import NexelError, RenderSettings
+from parity import compare_frames, is_subsequence, psnr
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_render(renderer, scene, cam):
+    ds = renderer.upload(scene)
+    fr = renderer.frame()
+    renderer.render(ds, cam, fr)
+    out = fr.download()
+    out.stats = fr.stats()
+    return out, ds
+
+
+# ---------------------------------------------------------------- config 1 (10K, 256x256)
+@pytest.fixture(scope="module")
+def config1():
+    return nx.stump_like(10_000), nx.ring_camera(0, 256, 256, 256)
+
+
+def test_config1_reference_tile_lists_bit_exact(renderer, reference, config1):
+    scene, cam = config1
+    ds = renderer.upload(scene)
+    g_off, g_ids, tx, ty = renderer.tile_lists(ds, cam, reference_lists=True)
+    r_off, r_ids, rtx, rty = reference.tile_lists(scene, cam)
+    assert (tx, ty) == (rtx, rty) == (16, 16)
+    assert r_off[-1] == 143_383  # SURVEY.md §6 probe value
+    assert np.array_equal(g_off, r_off)
+    assert np.array_equal(g_ids, r_ids)
+
+
+def test_config1_work_lists_are_subsequences(renderer, reference, config1):
+    scene, cam = config1
+    ds = renderer.upload(scene)
+    w_off, w_ids, _, _ = renderer.tile_lists(ds, cam, reference_lists=False)
+    r_off, r_ids, _, _ = reference.tile_lists(scene, cam)
+    assert w_off[-1] < r_off[-1]
+    for t in range(len(r_off) - 1):
+        assert is_subsequence(w_ids[w_off[t]:w_off[t + 1]], r_ids[r_off[t]:r_off[t + 1]]), f"tile {t}"
+
+
+def test_config1_contributor_lists_bit_exact(renderer, reference, config1):
+    scene, cam = config1
+    ds = renderer.upload(scene)
+    g_hits, g_cnt = renderer.pixel_hits(ds, cam, 0, cam.height, 128)
+    r_hits, r_cnt = reference.pixel_hits(scene, cam, 0, cam.height, 128)
+    assert np.array_equal(g_cnt, r_cnt)
+    assert np.array_equal(g_hits, r_hits)
+
+
+def test_config1_render_parity(renderer, reference, config1):
+    scene, cam = config1
+    g, _ = gpu_render(renderer, scene, cam)
+    r = reference.render(scene, cam)
+    rep = compare_frames(g, r)
+    assert g.stats["tile_keys"] == 143_383
+    assert g.stats["n_straddlers"] == 468
+    assert g.stats["n_queries"] == int(np.count_nonzero(r.ids >= 0))
+    assert abs(float(g.final_img.astype(np.float64).sum()) - 92174.708823425) < 0.05
+    assert rep["psnr"] >= 60
+
+
+def test_config1_textured_variant(renderer, reference):
+    """grid_init 1e-1 makes the texture branch non-trivial."""
+    scene = nx.stump_like(10_000, grid_init=1e-1)
+    cam = nx.ring_camera(3, 256, 256, 256)
+    g, _ = gpu_render(renderer, scene, cam)
+    r = reference.render(scene, cam)
+    compare_frames(g, r)
+    assert np.abs(r.texture - 0.5).max() > 1e-2  # the texture really varies
+
+
+@pytest.mark.parametrize("view", [17, 64, 129, 200])
+def test_config3_views(renderer, reference, view):
+    """Several views of the ring (config 3 shape at 256^2)."""
+    scene = nx.stump_like(10_000)
+    cam = nx.ring_camera(view, 256, 256, 256)
+    g, _ = gpu_render(renderer, scene, cam)
+    r = reference.render(scene, cam)
+    compare_frames(g, r)
+
+
+# ---------------------------------------------------------------- reference test shapes
+@pytest.mark.parametrize("seed,k", [(137, 0), (138, 2), (139, 1), (140, 4), (141, 8), (142, 3)])
+def test_random_scenes_match_reference(renderer, reference, seed, k):
+    scene, cam = reference.random_scene(seed, 12, k, 24, 28.0, 2.2)
+    g, _ = gpu_render(renderer, scene, cam)
+    r = reference.render(scene, cam)
+    compare_frames(g, r)
+
+
+@pytest.mark.parametrize("seed", [42000, 42001, 42002])
+def test_thin_scenes_default_termination(renderer, reference, seed):
+    """acceptance.cpp:92-130 shape: many low-opacity primitives."""
+    scene, cam = reference.random_scene(seed, 50, 2, 32, 36.0, 2.4, op_lo=0.02, op_hi=0.13)
+    g, _ = gpu_render(renderer, scene, cam)
+    r = reference.render(scene, cam)
+    compare_frames(g, r)
+    naive = reference.naive_render(scene, cam)
+    assert np.abs(g.final_img - naive).max() <= 1e-3
+
+
+@pytest.mark.parametrize("ablation", ["no_gamma", "no_prim_sh", "no_downweight", "min_t0", "tile8", "tile32",
+                                      "tile5"])
+def test_ablations(renderer, reference, ablation):
+    scene, cam = reference.random_scene(7 + len(ablation), 10, 2, 40, 44.0, 2.2)
+    s = scene.settings
+    if ablation == "min_t0":
+        s.min_transmittance = 0.0
+    elif ablation.startswith("tile"):
+        s.tile = int(ablation[4:])
+    else:
+        setattr(s, ablation, True)
+    g, _ = gpu_render(renderer, scene, cam)
+    r = reference.render(scene, cam)
+    compare_frames(g, r)
+
+
+def test_single_surfel_analytic(renderer, reference):
+    """test_renderer.cpp:80-124: w = 0.6, t = 2, residual 0.4, base = 0.4 bg."""
+    field = reference.field(73, 3, 5, 1e-2, 8)
+    nex = np.zeros((1, 60))
+    nex[0, 3] = 1.0
+    nex[0, 7:9] = np.log(0.5)
+    nex[0, 9] = np.log(0.6 / 0.4)
+    nex[0, 10:12] = -5.0
+    nex[0, 12:15] = (0.25, -0.1, 0.05)
+    scene = nx.Scene(nex, field, RenderSettings(top_k=1, background=(0.2, 0.3, 0.4)))
+    cam = reference.look_at((0, 0, -2), (0, 0, 0), 9, 12.0)
+    g, _ = gpu_render(renderer, scene, cam)
+    pix = 4 * 9 + 4
+    assert g.ids[pix] == 0
+    assert abs(g.weights[pix] - 0.6) < 1e-12
+    assert abs(g.depths[pix] - 2.0) < 1e-12
+    assert abs(g.residual[pix] - 0.4) < 1e-6
+    assert np.allclose(g.base[pix * 3:pix * 3 + 3], 0.4 * np.array([0.2, 0.3, 0.4]), atol=1e-6)
+    compare_frames(g, reference.render(scene, cam))
+
+
+def test_opaque_wall_early_termination(renderer, reference):
+    """test_renderer.cpp:201-239: a primitive behind an opaque wall changes nothing."""
+    field = reference.field(83, 3, 5, 1e-2, 8)
+
+    def wall(n):
+        rows = []
+        for i in range(n):
+            p = np.zeros(60)
+            p[2] = 0.2 * i
+            p[3] = 1.0
+            p[7:9] = np.log(3.0)
+            p[9] = np.log(0.999 / 0.001)
+            p[10:12] = np.log(np.expm1(31.0))
+            p[12] = 0.1 * (i + 1)
+            rows.append(p)
+        return rows
+
+    a_rows = wall(3)
+    b = np.zeros(60)
+    b[2], b[3] = 2.0, 1.0
+    b[7:9] = np.log(3.0)
+    b[9] = np.log(0.8 / 0.2)
+    b[10:12] = -5.0
+    b[12] = 0.7
+    st = RenderSettings(top_k=2, background=(0.9, 0.1, 0.5))
+    sa = nx.Scene(np.array(a_rows), field, st)
+    sb = nx.Scene(np.array(a_rows + [b]), field, st)
+    cam = reference.look_at((0, 0, -2), (0, 0, 1), 8, 8.0)
+    ga, _ = gpu_render(renderer, sa, cam)
+    gb, _ = gpu_render(renderer, sb, cam)
+    for k in ("final_img", "base", "residual", "weights", "ids", "texture"):
+        assert np.array_equal(getattr(ga, k), getattr(gb, k)), k
+    compare_frames(gb, reference.render(sb, cam))
+
+
+def test_empty_scene_is_background(renderer, reference):
+    field = reference.field(127, 3, 5, 1e-2, 8)
+    scene = nx.Scene(np.zeros((0, 60)), field, RenderSettings(top_k=2, background=(0.25, 0.5, 0.75)))
+    cam = reference.look_at((0, 0, -2), (0, 0, 0), 8, 10.0)
+    g, _ = gpu_render(renderer, scene, cam)
+    assert np.allclose(g.final_img.reshape(-1, 3), [0.25, 0.5, 0.75])
+    assert np.all(g.ids == -1)
+
+
+# ---------------------------------------------------------------- errors (nexel::Error codes)
+def test_error_codes(renderer, reference):
+    scene, cam = reference.random_scene(5, 4, 2, 8, 10.0, 2.2)
+    bad = RenderSettings(top_k=9)
+    s2 = nx.Scene(scene.nexels, scene.field, bad)
+    with pytest.raises(NexelError) as e:
+        gpu_render(renderer, s2, cam)
+    assert e.value.code == "bad-settings"
+    cam2 = nx.Camera(cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, np.zeros((3, 3)), cam.t)
+    with pytest.raises(NexelError) as e:
+        gpu_render(renderer, scene, cam2)
+    assert e.value.code == "bad-camera"
+    nex = scene.nexels.copy()
+    nex[2, 0] = np.nan
+    with pytest.raises(NexelError) as e:
+        gpu_render(renderer, nx.Scene(nex, scene.field, scene.settings), cam)
+    assert e.value.code == "bad-primitive" and "primitive 2" in str(e.value)
+
+
+# ---------------------------------------------------------------- config 2 (400K, 1920x1080)
+@pytest.fixture(scope="module")
+def config2():
+    return nx.stump_like(400_000), nx.ring_camera(0, 256, 1920, 1080)
+
+
+def test_config2_binning_counts(renderer, reference, config2):
+    scene, cam = config2
+    g, _ = gpu_render(renderer, scene, cam)
+    st = g.stats
+    assert st["tile_keys"] == 27_511_255  # SURVEY.md §6 probe value (reference P)
+    assert st["n_straddlers"] == 3_268
+    assert st["n_rect"] == 174_828
+    ds = renderer.upload(scene)
+    g_off, g_ids, _, _ = renderer.tile_lists(ds, cam, reference_lists=True)
+    r_off, r_ids, _, _ = reference.tile_lists(scene, cam)
+    assert np.array_equal(g_off, r_off)
+    assert np.array_equal(g_ids, r_ids)
+
+
+@pytest.mark.parametrize("band", [(0, 32), (512, 544), (1048, 1080)])
+def test_config2_contributor_lists_band(renderer, reference, config2, band):
+    scene, cam = config2
+    ds = renderer.upload(scene)
+    g_hits, g_cnt = renderer.pixel_hits(ds, cam, band[0], band[1], 128)
+    r_hits, r_cnt = reference.pixel_hits(scene, cam, band[0], band[1], 128)
+    assert np.array_equal(g_cnt, r_cnt)
+    assert np.array_equal(g_hits, r_hits)
+
+
+@pytest.mark.slow
+def test_config2_full_frame_parity(renderer, reference, config2):
+    scene, cam = config2
+    g, _ = gpu_render(renderer, scene, cam)
+    r = reference.render(scene, cam)
+    rep = compare_frames(g, r)
+    assert abs(float(g.final_img.astype(np.float64).sum()) - 2766856.890023658) < 1.0
+    print("config2 parity", rep)
