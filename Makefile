@@ -14,7 +14,8 @@ REF ?= /root/reference/proj
 
 PKG := paper_2512_13796_b200
 SRC := $(PKG)/csrc
-CU_SRCS := $(SRC)/nx_api.cu $(SRC)/nx_preprocess.cu $(SRC)/nx_sort.cu $(SRC)/nx_composite.cu $(SRC)/nx_texture.cu
+CU_SRCS := $(SRC)/nx_api.cu $(SRC)/nx_preprocess.cu $(SRC)/nx_sort.cu $(SRC)/nx_composite.cu $(SRC)/nx_texture.cu \
+           $(SRC)/nx_texture_tc.cu
 CPP_SRCS := $(SRC)/nx_synth.cpp
 HDRS := include/nexel_b200.h $(SRC)/nx_internal.cuh $(SRC)/nx_sort.cuh
 OBJDIR := build/obj

@@ -211,7 +211,7 @@ class Reference:
             raise OracleError(st, self.lib.ref_last_error().decode())
 
     def _handle(self, scene: Scene):
-        key = id(scene), scene.nexels.ctypes.data, scene.field.table.ctypes.data
+        key = scene.fingerprint()  # content-keyed: ids / buffers of freed scenes get reused
         if self._scene is None or self._scene_key != key:
             self.close()
             nex, d, (tab, w1, w2, w3) = _scene_args(scene)

@@ -72,7 +72,7 @@ struct nx_ctx {
     std::string err;
     int err_status = NX_OK;
     // per-frame scratch (grow-only)
-    DevBuf rec, cls, ref_rect, work_rect, key, flag, pos;
+    DevBuf rec, recf, cls, ref_rect, work_rect, key, flag, pos;
     DevBuf skeys_a, skeys_b, sids_a, sids_b, counts, offsets;
     DevBuf tkeys_a, tkeys_b, tvals_a, tvals_b, tile_counts, scratch;
     DevBuf dbg_hits, dbg_counts;
@@ -271,6 +271,7 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
     const CamD cd = make_cam(cam);
     const int64_t nn = std::max<int64_t>(n, 1);
     NX_CUDA(c, c->rec.ensure(nn * REC_FIELDS * sizeof(double)));
+    NX_CUDA(c, c->recf.ensure(nn * 4 * sizeof(float4)));
     NX_CUDA(c, c->cls.ensure(nn * sizeof(int32_t)));
     NX_CUDA(c, c->ref_rect.ensure(nn * sizeof(int4)));
     NX_CUDA(c, c->work_rect.ensure(nn * sizeof(int4)));
@@ -301,6 +302,7 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
     pa.tiles_y = f->tiles_y;
     pa.zmin_work = 0.5 * scene->st.near_eps * min_axis_cosine(cam);
     pa.rec = c->rec.as<double>();
+    pa.recf = c->recf.as<float4>();
     pa.cls = c->cls.as<int32_t>();
     pa.ref_rect = c->ref_rect.as<int4>();
     pa.work_rect = c->work_rect.as<int4>();
@@ -374,6 +376,7 @@ int collection(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame*
     record(c, NX_STAGE_COMPOSITE, s);
     CompositeArgs ca;
     ca.rec = c->rec.as<double>();
+    ca.recf = c->recf.as<float4>();
     ca.n = std::max<int64_t>(scene->n, 1);
     ca.sh = scene->sh.as<float>();
     ca.list_ids = f->list_ids.as<int32_t>();
@@ -465,7 +468,7 @@ void nx_ctx_destroy(nx_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    for (DevBuf* b : {&c->rec, &c->cls, &c->ref_rect, &c->work_rect, &c->key, &c->flag, &c->pos, &c->skeys_a,
+    for (DevBuf* b : {&c->rec, &c->recf, &c->cls, &c->ref_rect, &c->work_rect, &c->key, &c->flag, &c->pos, &c->skeys_a,
                       &c->skeys_b, &c->sids_a, &c->sids_b, &c->counts, &c->offsets, &c->tkeys_a, &c->tkeys_b,
                       &c->tvals_a, &c->tvals_b, &c->tile_counts, &c->scratch, &c->dbg_hits, &c->dbg_counts})
         b->release();

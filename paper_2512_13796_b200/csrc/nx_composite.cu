@@ -2,12 +2,20 @@
 // and a top-K buffer (collection_pass, renderer.cpp:115-171).
 //
 // One CTA per screen tile, one thread per pixel. The tile's work list (ids in
-// (depth, id) order) is walked in chunks of kChunk primitives whose intersection
-// records are staged into shared memory (SoA, every thread reads the same
-// primitive at the same time -> broadcast, conflict-free). Every decision is
-// the reference's, in fp64: grazing test, t > near_eps, alpha >= 1/255 (with an
-// exact-preserving early reject on |u| > ru before any transcendental), alpha
-// clamp, transmittance termination, top-K replacement with arrival-order ties.
+// (depth, id) order) is walked in chunks of kChunk primitives whose records are
+// staged into shared memory (AoS, every thread reads the same primitive at the
+// same time -> broadcast, conflict-free).
+//
+// Each (pixel, primitive) test runs in two stages:
+//   1. an fp32 conservative prefilter: the plane crossing t and
+//      the in-plane offsets dot(x - mu, v1|v2) are estimated in fp32 with a
+//      rigorous error slack; the test is rejected only if it provably fails the
+//      reference's t > near_eps or |u| <= ru (hence alpha < 1/255) conditions;
+//   2. survivors (and grazing rays, |dot(d,n)| < 1e-2) take the exact fp64 path:
+//      the reference's intersect() formulas (intersect.hpp:23-42), eval_kernel,
+//      the 1/255 test, alpha clamp, top-K insert and transmittance update.
+// So every decision the reference takes is taken here in fp64 with the same
+// formulas; the prefilter only skips provable misses.
 // A warp stops testing when all its pixels have terminated; the CTA stops
 // staging when all of its pixels have.
 #include "nx_internal.cuh"
@@ -17,10 +25,11 @@ namespace nx {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kChunk = 64;
+constexpr int kChunk = 128;
+constexpr int kRecPairs = REC_FIELDS / 2;  // double2 per fp64 record
 
 // eval_sh (sh.hpp:46-57) with fp64 basis (sh_basis, sh.hpp:11-40) and the
-// primitive's fp32 coefficients.
+// primitive's fp32 coefficients (exact copies of the inputs' f32-rounded values).
 __device__ __forceinline__ void eval_sh_prim(const float* __restrict__ sh, const double* d, int degree,
                                              double* rgb) {
     const double C0 = 0.28209479177387814;
@@ -48,7 +57,6 @@ __device__ __forceinline__ void eval_sh_prim(const float* __restrict__ sh, const
         b[14] = 1.445305721320277 * z * (xx - yy);
         b[15] = -0.5900435899266435 * x * (xx - 3.0 * yy);
         const float4* s4 = reinterpret_cast<const float4*>(sh);
-        // coefficients k = 1..15 live at floats 3..47: load 12 float4 and skip the first 3.
         float c[48];
 #pragma unroll
         for (int q = 0; q < 12; ++q) {
@@ -71,8 +79,10 @@ __device__ __forceinline__ void eval_sh_prim(const float* __restrict__ sh, const
 }
 
 template <int K, bool kDebug>
-__global__ void __launch_bounds__(kThreads) composite_kernel(const CompositeArgs a) {
-    __shared__ double s_rec[REC_FIELDS][kChunk];
+__global__ void __launch_bounds__(kThreads, 2) composite_kernel(const CompositeArgs a) {
+    constexpr int KK = K > 0 ? K : 1;
+    __shared__ float4 s_f[kChunk][4];
+    __shared__ double2 s_d[kChunk][kRecPairs];
     __shared__ int32_t s_id[kChunk];
 
     const int tile = a.st.tile;
@@ -81,7 +91,7 @@ __global__ void __launch_bounds__(kThreads) composite_kernel(const CompositeArgs
     const int list_begin = a.tile_offsets[t], list_end = a.tile_offsets[t + 1];
     const int W = a.cam.W, H = a.cam.H;
     const double near_eps = a.st.near_eps, alpha_max = a.st.alpha_max, min_T = a.st.min_transmittance;
-    const int64_t n = a.n;
+    const float near_eps_f = static_cast<float>(near_eps);
 
     for (int pbase = 0; pbase < tile * tile; pbase += kThreads) {
         const int lp = pbase + threadIdx.x;
@@ -89,15 +99,17 @@ __global__ void __launch_bounds__(kThreads) composite_kernel(const CompositeArgs
         const bool in_img = lp < tile * tile && px < W && py < H;
         double dir[3] = {0.0, 0.0, 1.0};
         if (in_img) pixel_dir(a.cam, px + 0.5, py + 0.5, dir);
+        const float dfx = static_cast<float>(dir[0]), dfy = static_cast<float>(dir[1]),
+                    dfz = static_cast<float>(dir[2]);
         const double o0 = a.cam.o[0], o1 = a.cam.o[1], o2 = a.cam.o[2];
 
         double T = 1.0;
         double acc[3] = {0.0, 0.0, 0.0};
-        int32_t k_id[K > 0 ? K : 1];
-        double k_w[K > 0 ? K : 1], k_t[K > 0 ? K : 1];
-        uint32_t k_seq[K > 0 ? K : 1];
+        int32_t k_id[KK];
+        double k_w[KK], k_t[KK];
+        uint32_t k_seq[KK];
 #pragma unroll
-        for (int s = 0; s < (K > 0 ? K : 1); ++s) {
+        for (int s = 0; s < KK; ++s) {
             k_id[s] = -1;
             k_w[s] = 0.0;
             k_t[s] = 0.0;
@@ -113,33 +125,52 @@ __global__ void __launch_bounds__(kThreads) composite_kernel(const CompositeArgs
         for (int cb = list_begin; cb < list_end; cb += kChunk) {
             const int cn = min(kChunk, list_end - cb);
             __syncthreads();
-            for (int e = threadIdx.x; e < cn; e += kThreads) s_id[e] = a.list_ids[cb + e];
-            __syncthreads();
-            for (int e = threadIdx.x; e < REC_FIELDS * cn; e += kThreads) {
-                const int f = e / cn, j = e - f * cn;
-                s_rec[f][j] = __ldg(a.rec + static_cast<int64_t>(f) * n + s_id[j]);
+            for (int e = threadIdx.x; e < cn * 4; e += kThreads) {
+                const int j = e >> 2, q = e & 3;
+                const int32_t id = __ldg(a.list_ids + cb + j);
+                s_f[j][q] = __ldg(a.recf + static_cast<int64_t>(id) * 4 + q);
+                if (q == 0) s_id[j] = id;
+            }
+            for (int e = threadIdx.x; e < cn * kRecPairs; e += kThreads) {
+                const int j = e / kRecPairs, q = e - j * kRecPairs;
+                const int32_t id = __ldg(a.list_ids + cb + j);
+                s_d[j][q] = __ldg(reinterpret_cast<const double2*>(a.rec) + static_cast<int64_t>(id) * kRecPairs + q);
             }
             __syncthreads();
             if (active) {
                 for (int j = 0; j < cn; ++j) {
-                    // intersect (intersect.hpp:23-42)
-                    const double denom = dir[0] * s_rec[REC_NX][j] + dir[1] * s_rec[REC_NY][j] +
-                                         dir[2] * s_rec[REC_NZ][j];
+                    // ---- 1. fp32 conservative prefilter
+                    const float4 f0 = s_f[j][0];
+                    const float denom_f = dfx * f0.x + dfy * f0.y + dfz * f0.z;
+                    if (fabsf(denom_f) >= 1e-2f) {
+                        const float ta = __fdividef(f0.w, denom_f);
+                        if (!(ta * (1.0f + 1e-4f) > near_eps_f)) continue;  // t <= near_eps for sure
+                        const float4 f1 = s_f[j][1], f2 = s_f[j][2], f3 = s_f[j][3];
+                        const float ta1 = ta * (dfx * f1.x + dfy * f1.y + dfz * f1.z);
+                        const float du = ta1 - f1.w;
+                        if (fabsf(du) > f3.x + (1e-4f * (fabsf(ta1) + fabsf(ta) + fabsf(f1.w)) + 1e-7f)) continue;
+                        const float ta2 = ta * (dfx * f2.x + dfy * f2.y + dfz * f2.z);
+                        const float dv = ta2 - f2.w;
+                        if (fabsf(dv) > f3.y + (1e-4f * (fabsf(ta2) + fabsf(ta) + fabsf(f2.w)) + 1e-7f)) continue;
+                    }
+                    // ---- 2. exact fp64 path: intersect (intersect.hpp:23-42)
+                    const double* r = reinterpret_cast<const double*>(&s_d[j][0]);
+                    const double denom = dir[0] * r[REC_NX] + dir[1] * r[REC_NY] + dir[2] * r[REC_NZ];
                     if (fabs(denom) < kMinNormalDot) continue;
-                    const double tt = s_rec[REC_NUM][j] / denom;
+                    const double tt = r[REC_NUM] / denom;
                     if (!(tt > near_eps)) continue;
-                    const double e0 = (o0 + tt * dir[0]) - s_rec[REC_MUX][j];
-                    const double e1 = (o1 + tt * dir[1]) - s_rec[REC_MUY][j];
-                    const double e2 = (o2 + tt * dir[2]) - s_rec[REC_MUZ][j];
-                    const double du = e0 * s_rec[REC_V1X][j] + e1 * s_rec[REC_V1Y][j] + e2 * s_rec[REC_V1Z][j];
-                    if (fabs(du) > s_rec[REC_ULIM][j]) continue;
-                    const double dv = e0 * s_rec[REC_V2X][j] + e1 * s_rec[REC_V2Y][j] + e2 * s_rec[REC_V2Z][j];
-                    if (fabs(dv) > s_rec[REC_VLIM][j]) continue;
-                    const double u = du / s_rec[REC_SX][j];
-                    const double v = dv / s_rec[REC_SY][j];
-                    const double alpha_raw = eval_kernel(u, v, s_rec[REC_OP][j], s_rec[REC_GX][j], s_rec[REC_GY][j]);
+                    const double e0 = (o0 + tt * dir[0]) - r[REC_MUX];
+                    const double e1 = (o1 + tt * dir[1]) - r[REC_MUY];
+                    const double e2 = (o2 + tt * dir[2]) - r[REC_MUZ];
+                    const double du = e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z];
+                    if (fabs(du) > r[REC_ULIM]) continue;
+                    const double dv = e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z];
+                    if (fabs(dv) > r[REC_VLIM]) continue;
+                    const double u = du / r[REC_SX];
+                    const double v = dv / r[REC_SY];
+                    const double alpha_raw = eval_kernel(u, v, r[REC_OP], r[REC_GX], r[REC_GY]);
                     if (alpha_raw < kAlphaMin) continue;
-                    // composite (renderer.cpp:146-152)
+                    // ---- composite (renderer.cpp:146-152)
                     const int32_t id = s_id[j];
                     const double alpha = alpha_max < alpha_raw ? alpha_max : alpha_raw;
                     const double w = alpha * T;
@@ -152,7 +183,7 @@ __global__ void __launch_bounds__(kThreads) composite_kernel(const CompositeArgs
                         const uint32_t seq = counter++;
                         if (k_size < K) {
 #pragma unroll
-                            for (int s = 0; s < (K > 0 ? K : 1); ++s)
+                            for (int s = 0; s < KK; ++s)
                                 if (s == k_size) {
                                     k_id[s] = id;
                                     k_w[s] = w;
@@ -166,14 +197,14 @@ __global__ void __launch_bounds__(kThreads) composite_kernel(const CompositeArgs
                             double wm = k_w[0];
                             uint32_t qm = k_seq[0];
 #pragma unroll
-                            for (int s = 1; s < (K > 0 ? K : 1); ++s)
+                            for (int s = 1; s < KK; ++s)
                                 if (k_w[s] < wm || (k_w[s] == wm && k_seq[s] > qm)) {
                                     m = s;
                                     wm = k_w[s];
                                     qm = k_seq[s];
                                 }
 #pragma unroll
-                            for (int s = 0; s < (K > 0 ? K : 1); ++s)
+                            for (int s = 0; s < KK; ++s)
                                 if (s == m && w > wm) {
                                     k_id[s] = id;
                                     k_w[s] = w;

@@ -97,7 +97,7 @@ NX_HD void pixel_dir(const CamD& c, double px, double py, double* dir) {
 }
 
 // ---------------------------------------------------------------- per-primitive composite record
-// Staged into shared memory per chunk (SoA, broadcast reads). All fp64.
+// AoS, 20 fp64 per primitive, staged into shared memory per chunk (broadcast reads).
 enum RecField {
     REC_NUM = 0,  // dot(mu - origin, n): the per-camera numerator of t (intersect.hpp:29)
     REC_NX, REC_NY, REC_NZ,
@@ -160,7 +160,8 @@ struct PreprocessArgs {
     CamD cam;
     int tiles_x, tiles_y;
     double zmin_work;   // conservative camera-z bound of any hit (straddler refinement)
-    double* rec;        // REC_FIELDS x n
+    double* rec;        // n x REC_FIELDS (AoS, 160 B per primitive)
+    float4* recf;       // n x 4 fp32 prefilter records (64 B per primitive)
     int32_t* cls;       // n
     int4* ref_rect;     // n
     int4* work_rect;    // n
@@ -186,7 +187,8 @@ void launch_emit(const uint32_t* ids, const int32_t* offsets, int64_t n_sorted, 
                  int32_t* tile_counts, cudaStream_t s);
 
 struct CompositeArgs {
-    const double* rec;
+    const double* rec;   // n x REC_FIELDS
+    const float4* recf;  // n x 4
     int64_t n;
     const float* sh;
     const int32_t* list_ids;
@@ -209,5 +211,8 @@ struct TextureArgs {
     FrameStatsD* stats;
 };
 int launch_texture(const TextureArgs& a, cudaStream_t s);  // returns NX_OK / NX_UNSUPPORTED
+// tcgen05 variant for the reference field shape (16 levels x 2 features, 64 hidden).
+bool texture_tc_supported(const nx_field_desc& fd);
+int launch_texture_tc(const TextureArgs& a, cudaStream_t s);
 
 }  // namespace nx

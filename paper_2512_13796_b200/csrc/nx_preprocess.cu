@@ -180,32 +180,45 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const PreprocessArgs a)
         ref_keys = rect_tiles(ref);
         work_keys = wk;
         if (wk > 0) {
-            // Composite record: everything intersect() (intersect.hpp:23-42) needs per primitive.
-            double* r = a.rec;
+            // Composite records: everything intersect() (intersect.hpp:23-42) needs per
+            // primitive (fp64, exact path) + the fp32 prefilter record.
+            double r[REC_FIELDS];
             const double nx_ = R[2], ny_ = R[5], nz_ = R[8];
-            r[REC_NUM * n + i] = (mu.x - a.cam.o[0]) * nx_ + (mu.y - a.cam.o[1]) * ny_ + (mu.z - a.cam.o[2]) * nz_;
-            r[REC_NX * n + i] = nx_;
-            r[REC_NY * n + i] = ny_;
-            r[REC_NZ * n + i] = nz_;
-            r[REC_V1X * n + i] = R[0];
-            r[REC_V1Y * n + i] = R[3];
-            r[REC_V1Z * n + i] = R[6];
-            r[REC_V2X * n + i] = R[1];
-            r[REC_V2Y * n + i] = R[4];
-            r[REC_V2Z * n + i] = R[7];
-            r[REC_MUX * n + i] = mu.x;
-            r[REC_MUY * n + i] = mu.y;
-            r[REC_MUZ * n + i] = mu.z;
-            r[REC_SX * n + i] = sx;
-            r[REC_SY * n + i] = sy;
-            r[REC_OP * n + i] = op;
-            r[REC_GX * n + i] = gx;
-            r[REC_GY * n + i] = gy;
+            const double mx = mu.x - a.cam.o[0], my = mu.y - a.cam.o[1], mz = mu.z - a.cam.o[2];
+            r[REC_NUM] = mx * nx_ + my * ny_ + mz * nz_;  // dot(a.mu - ray.origin, n)
+            r[REC_NX] = nx_;
+            r[REC_NY] = ny_;
+            r[REC_NZ] = nz_;
+            r[REC_V1X] = R[0];
+            r[REC_V1Y] = R[3];
+            r[REC_V1Z] = R[6];
+            r[REC_V2X] = R[1];
+            r[REC_V2Y] = R[4];
+            r[REC_V2Z] = R[7];
+            r[REC_MUX] = mu.x;
+            r[REC_MUY] = mu.y;
+            r[REC_MUZ] = mu.z;
+            r[REC_SX] = sx;
+            r[REC_SY] = sy;
+            r[REC_OP] = op;
+            r[REC_GX] = gx;
+            r[REC_GY] = gy;
             // |u| > ru implies alpha < 1/255 (margin 1e-6 relative, exact decision kept
             // for everything inside); disabled when ln(255 o) is tiny.
             const bool safe = log(op / kAlphaMin) >= 1e-3;
-            r[REC_ULIM * n + i] = safe ? ru * (1.0 + 1e-6) * sx : INFINITY;
-            r[REC_VLIM * n + i] = safe ? rv * (1.0 + 1e-6) * sy : INFINITY;
+            r[REC_ULIM] = safe ? ru * (1.0 + 1e-6) * sx : INFINITY;
+            r[REC_VLIM] = safe ? rv * (1.0 + 1e-6) * sy : INFINITY;
+            double2* dst = reinterpret_cast<double2*>(a.rec + i * REC_FIELDS);
+#pragma unroll
+            for (int q = 0; q < REC_FIELDS / 2; ++q) dst[q] = make_double2(r[2 * q], r[2 * q + 1]);
+            // fp32 prefilter record: n|num, v1|b1, v2|b2, ulim|vlim (rounded up).
+            const double b1 = mx * R[0] + my * R[3] + mz * R[6];
+            const double b2 = mx * R[1] + my * R[4] + mz * R[7];
+            float4* f = a.recf + i * 4;
+            f[0] = make_float4(float(nx_), float(ny_), float(nz_), float(r[REC_NUM]));
+            f[1] = make_float4(float(R[0]), float(R[3]), float(R[6]), float(b1));
+            f[2] = make_float4(float(R[1]), float(R[4]), float(R[7]), float(b2));
+            f[3] = make_float4(__double2float_ru(r[REC_ULIM]), __double2float_ru(r[REC_VLIM]), 0.f, 0.f);
         }
     }
     // block-aggregated statistics

@@ -13,6 +13,9 @@
 //   degree-3 SH colour with the ray direction (eval_sh, sh.hpp:46-57).
 // The CTA then forms final = base + sum_j W[p,j] * texture[p,j] for its pixels
 // (renderer.cpp:219-236) from the slot colours it holds in shared memory.
+#include <cstdlib>
+#include <cstring>
+
 #include "nx_internal.cuh"
 
 namespace nx {
@@ -247,6 +250,12 @@ int launch_texture(const TextureArgs& a, cudaStream_t s) {
     }
     const nx_field_desc& fd = a.scene.field;
     const int nin = fd.levels * fd.features;
+    // NX_TEXTURE_PATH=simt forces the SIMT MLP (validation of the tensor-core path).
+    static const bool force_simt = [] {
+        const char* e = getenv("NX_TEXTURE_PATH");
+        return e && strcmp(e, "simt") == 0;
+    }();
+    if (!force_simt && texture_tc_supported(fd)) return launch_texture_tc(a, s);
     if (nin == 32 && fd.features == 2 && fd.n_hidden == 64) {
         launch_tex<32, 64, 2>(a, s);
         return NX_OK;

@@ -1,0 +1,448 @@
+// K7 texture, tensor-core variant for the reference field shape (16 levels x 2
+// features -> 32 -> 64 -> 64 -> 48): hash-grid gathers on the SIMT pipes, the
+// bias-free ReLU MLP (TextureMlp::forward, mlp.cpp:24-43) on the 5th-gen tensor
+// cores (tcgen05.mma, accumulators in TMEM), SH colour (eval_sh, sh.hpp:46-57)
+// and the Eq. 7 composite (renderer.cpp:219-236) in the epilogue.
+//
+// Persistent CTAs of 256 threads; one tile = 128 top-K slots (pixel-major,
+// slot-minor = the reference's query order, renderer.cpp:177-203) = the M=128
+// rows of every MMA. Per tile:
+//   gather   two threads per row, 8 levels each (grid_lookup, hash_grid.cpp:26-83;
+//            lattice position, floor and hashing in fp64/int64 like the reference,
+//            so the same table rows are read) -> 32 features -> smem (bf16 hi/lo)
+//   layer 1  D1[128x64]  = F[128x32] . W1^T   (TMEM cols   0..63)
+//   layer 2  D2[128x64]  = relu(D1) . W2^T    (TMEM cols  64..127)
+//   layer 3  D3[128x48]  = relu(D2) . W3^T    (TMEM cols 128..175)
+//   epilogue tcgen05.ld D3 rows -> 48 SH coefficients -> rgb, texture, final.
+// fp32-class accuracy from bf16 operands via the 3-term split
+// a.b ~= a_hi.b_hi + a_hi.b_lo + a_lo.b_hi (relative error ~2^-16), accumulated
+// in fp32 in TMEM. Operands use the K-major no-swizzle canonical layout:
+// 8-row x 16-byte core matrices, LBO = 128 B (next K chunk), SBO = 128*K/8 B
+// (next 8-row group).
+#include <cuda_bf16.h>
+
+#include "nx_internal.cuh"
+
+namespace nx {
+
+namespace {
+
+constexpr int kTcThreads = 256;
+constexpr int kRows = 128;
+constexpr int kLevels = 16;
+constexpr int kIn = 32, kHid = 64, kOut = 48;
+constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kColD1 = 0, kColD2 = 64, kColD3 = 128;
+
+// shared-memory carve-up (bytes)
+constexpr int kOffW1h = 0;
+constexpr int kOffW1l = kOffW1h + kHid * kIn * 2;    // 4 KB each
+constexpr int kOffW2h = kOffW1l + kHid * kIn * 2;
+constexpr int kOffW2l = kOffW2h + kHid * kHid * 2;   // 8 KB each
+constexpr int kOffW3h = kOffW2l + kHid * kHid * 2;
+constexpr int kOffW3l = kOffW3h + kOut * kHid * 2;   // 6 KB each
+constexpr int kOffAh = kOffW3l + kOut * kHid * 2;
+constexpr int kOffAl = kOffAh + kRows * kHid * 2;    // 16 KB each
+constexpr int kOffRgb = kOffAl + kRows * kHid * 2;   // float [128][3]
+constexpr int kOffPart = kOffRgb + kRows * 3 * 4;    // float [128][3]
+constexpr int kOffBar = kOffPart + kRows * 3 * 4;    // mbarrier (8 B)
+constexpr int kOffTmem = kOffBar + 8;                // tmem base (4 B)
+constexpr int kSmemUsed = kOffTmem + 8;
+// Request more than needed so that at most two CTAs share an SM (2 x 256 TMEM columns).
+constexpr int kSmemRequest = 100 * 1024;
+static_assert(kSmemUsed <= kSmemRequest, "smem carve-up");
+
+struct TcConst {
+    double level_scale[kLevels];  // HashGridConfig::level_scale by iterated product (hash_grid.cpp:7-13)
+    float inv_level_scale[kLevels];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Byte offset of element (row, k) in a K-major no-swizzle operand with K columns (bf16).
+__device__ __forceinline__ uint32_t kmajor_off(int row, int k, int K) {
+    return static_cast<uint32_t>((row >> 3) * (K / 8) * 128 + (k >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2);
+}
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
+           (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);  // version 1, no swizzle
+}
+
+__host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+           (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);  // .x = a (low half)
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// Writes 8 consecutive K values (one 16-byte core-matrix row) as bf16 hi and lo parts.
+__device__ __forceinline__ void store_split8(uint8_t* smem, int off_hi, int off_lo, uint32_t byte_off, const float* x) {
+    float hi[8], lo[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        hi[i] = __bfloat162float(__float2bfloat16_rn(x[i]));
+        lo[i] = x[i] - hi[i];
+    }
+    const uint4 h = make_uint4(pack_bf16(hi[0], hi[1]), pack_bf16(hi[2], hi[3]), pack_bf16(hi[4], hi[5]),
+                               pack_bf16(hi[6], hi[7]));
+    const uint4 l = make_uint4(pack_bf16(lo[0], lo[1]), pack_bf16(lo[2], lo[3]), pack_bf16(lo[4], lo[5]),
+                               pack_bf16(lo[6], lo[7]));
+    *reinterpret_cast<uint4*>(smem + off_hi + byte_off) = h;
+    *reinterpret_cast<uint4*>(smem + off_lo + byte_off) = l;
+}
+
+__device__ __forceinline__ uint32_t map_positive32(long long x) {  // hash_grid.hpp:12-14
+    return x > 0 ? static_cast<uint32_t>(2 * x - 1) : static_cast<uint32_t>(-2 * x);
+}
+
+__global__ void __launch_bounds__(kTcThreads, 2) texture_tc_kernel(const TextureArgs a, const TcConst cst,
+                                                                   int rows_per_tile, int64_t n_tiles) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t bar = smem_u32(smem + kOffBar);
+
+    // ---- one-time setup: weights -> smem (bf16 hi/lo, K-major core-matrix layout)
+    for (int e = tid; e < kHid * kIn / 8; e += kTcThreads) {  // W1 [64][32]
+        const int n = e / (kIn / 8), c = e % (kIn / 8);
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(a.scene.w1 + n * kIn + c * 8 + i);
+        store_split8(smem, kOffW1h, kOffW1l, kmajor_off(n, c * 8, kIn), x);
+    }
+    for (int e = tid; e < kHid * kHid / 8; e += kTcThreads) {  // W2 [64][64]
+        const int n = e / (kHid / 8), c = e % (kHid / 8);
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(a.scene.w2 + n * kHid + c * 8 + i);
+        store_split8(smem, kOffW2h, kOffW2l, kmajor_off(n, c * 8, kHid), x);
+    }
+    for (int e = tid; e < kOut * kHid / 8; e += kTcThreads) {  // W3 [48][64]
+        const int n = e / (kHid / 8), c = e % (kHid / 8);
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(a.scene.w3 + n * kHid + c * 8 + i);
+        store_split8(smem, kOffW3h, kOffW3l, kmajor_off(n, c * 8, kHid), x);
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem + kOffTmem)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 32) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + kOffTmem);
+    uint32_t phase = 0;
+
+    const int K = a.fb.K;
+    const int W = a.cam.W;
+    const int64_t total = static_cast<int64_t>(a.cam.W) * a.cam.H * K;
+    const int row = tid & (kRows - 1);  // == 32 * (warp % 4) + lane: the TMEM lane this thread reads
+    const int half = tid >> 7;          // gather: levels [8 half, 8 half + 8); epilogue: column half
+    const uint32_t lane_base = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+    const uint32_t T = 1u << a.scene.field.log2_table;
+    const uint32_t mask = T - 1u;
+    const float2* tab = reinterpret_cast<const float2*>(a.scene.table);
+    const float* srgb = reinterpret_cast<const float*>(smem + kOffRgb);
+    float* spart = reinterpret_cast<float*>(smem + kOffPart);
+    constexpr uint32_t kIdesc64 = idesc_bf16_f32(kRows, 64);
+    constexpr uint32_t kIdesc48 = idesc_bf16_f32(kRows, 48);
+    int n_queries = 0;
+
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int64_t slot = tile * rows_per_tile + row;
+        const bool valid = row < rows_per_tile && slot < total && a.fb.ids[slot] >= 0;
+        if (valid && half == 0) ++n_queries;
+        double dir[3] = {0.0, 0.0, 1.0};
+        float feats[16];
+        if (valid) {
+            const int64_t pix = slot / K;
+            const int px = static_cast<int>(pix % W), py = static_cast<int>(pix / W);
+            pixel_dir(a.cam, px + 0.5, py + 0.5, dir);
+            const double t = a.fb.depths[slot];
+            const double x0 = a.cam.o[0] + t * dir[0];
+            const double x1 = a.cam.o[1] + t * dir[1];
+            const double x2 = a.cam.o[2] + t * dir[2];
+            const float ft = static_cast<float>(a.cam.fx / t);
+#pragma unroll
+            for (int li = 0; li < 8; ++li) {
+                const int l = half * 8 + li;
+                const double s = cst.level_scale[l];
+                const double p0 = s * x0, p1 = s * x1, p2 = s * x2;
+                const double fl0 = floor(p0), fl1 = floor(p1), fl2 = floor(p2);
+                const long long b0 = static_cast<long long>(fl0), b1 = static_cast<long long>(fl1),
+                                b2 = static_cast<long long>(fl2);
+                const float fr0 = static_cast<float>(p0 - fl0), fr1 = static_cast<float>(p1 - fl1),
+                            fr2 = static_cast<float>(p2 - fl2);
+                float dw = 1.0f;
+                if (!a.st.no_downweight) {  // downweight (hash_grid.hpp:28-31)
+                    const float r = ft * cst.inv_level_scale[l];
+                    dw = 1.0f - __expf(-r * r * 0.15915494309189535f);
+                }
+                const uint32_t ax0 = map_positive32(b0), ax1 = map_positive32(b0 + 1);
+                const uint32_t by0 = map_positive32(b1) * 2654435761u, by1 = map_positive32(b1 + 1) * 2654435761u;
+                const uint32_t cz0 = map_positive32(b2) * 805459861u, cz1 = map_positive32(b2 + 1) * 805459861u;
+                const size_t slab = static_cast<size_t>(l) * T;
+                float2 v[8];
+#pragma unroll
+                for (int ci = 0; ci < 8; ++ci) {
+                    const uint32_t rowi = ((ci & 1) ? ax1 : ax0) ^ ((ci & 2) ? by1 : by0) ^ ((ci & 4) ? cz1 : cz0);
+                    v[ci] = __ldg(tab + slab + (rowi & mask));
+                }
+                const float wx[2] = {1.0f - fr0, fr0}, wy[2] = {1.0f - fr1, fr1}, wz[2] = {1.0f - fr2, fr2};
+                float g0 = 0.f, g1 = 0.f;
+#pragma unroll
+                for (int ci = 0; ci < 8; ++ci) {
+                    const float w = wx[ci & 1] * wy[(ci >> 1) & 1] * wz[(ci >> 2) & 1];
+                    g0 += w * v[ci].x;
+                    g1 += w * v[ci].y;
+                }
+                feats[2 * li] = g0 * dw;
+                feats[2 * li + 1] = g1 * dw;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) feats[i] = 0.f;
+        }
+        // features k = 16 half + i -> two 8-wide chunks of the layer-1 A operand (K = 32)
+        store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 16 * half, kIn), feats);
+        store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 16 * half + 8, kIn), feats + 8);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+
+        // ---- layer 1: D1 = F . W1^T  (K = 32: 2 k-steps x 3 split terms)
+        if (tid == 0) {
+            tc_fence_after();
+            const uint32_t ah = smem_u32(smem + kOffAh), al = smem_u32(smem + kOffAl);
+            const uint32_t bh = smem_u32(smem + kOffW1h), bl = smem_u32(smem + kOffW1l);
+#pragma unroll
+            for (int s = 0; s < kIn / 16; ++s) {
+                const uint32_t o = s * 256;
+                mma_bf16(tmem + kColD1, smem_desc(ah + o, 128, 512), smem_desc(bh + o, 128, 512), kIdesc64, s > 0);
+                mma_bf16(tmem + kColD1, smem_desc(ah + o, 128, 512), smem_desc(bl + o, 128, 512), kIdesc64, 1);
+                mma_bf16(tmem + kColD1, smem_desc(al + o, 128, 512), smem_desc(bh + o, 128, 512), kIdesc64, 1);
+            }
+            mma_commit(bar);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+
+        // ---- hidden layers: relu(D) -> A (K = 64), then D_next = A . W^T
+#pragma unroll 1
+        for (int layer = 0; layer < 2; ++layer) {
+            const uint32_t dcol = layer == 0 ? kColD1 : kColD2;
+            float v[32];
+            tmem_ld16(tmem + lane_base + dcol + 32 * half, v);
+            tmem_ld16(tmem + lane_base + dcol + 32 * half + 16, v + 16);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 32 * half + 8 * c, kHid), v + 8 * c);
+            fence_async_smem();
+            tc_fence_before();
+            __syncthreads();
+            if (tid == 0) {
+                tc_fence_after();
+                const uint32_t ah = smem_u32(smem + kOffAh), al = smem_u32(smem + kOffAl);
+                const uint32_t bh = smem_u32(smem + (layer == 0 ? kOffW2h : kOffW3h));
+                const uint32_t bl = smem_u32(smem + (layer == 0 ? kOffW2l : kOffW3l));
+                const uint32_t dn = tmem + (layer == 0 ? kColD2 : kColD3);
+                const uint32_t idesc = layer == 0 ? kIdesc64 : kIdesc48;
+#pragma unroll
+                for (int s = 0; s < kHid / 16; ++s) {
+                    const uint32_t o = s * 256;
+                    mma_bf16(dn, smem_desc(ah + o, 128, 1024), smem_desc(bh + o, 128, 1024), idesc, s > 0);
+                    mma_bf16(dn, smem_desc(ah + o, 128, 1024), smem_desc(bl + o, 128, 1024), idesc, 1);
+                    mma_bf16(dn, smem_desc(al + o, 128, 1024), smem_desc(bh + o, 128, 1024), idesc, 1);
+                }
+                mma_commit(bar);
+            }
+            mbar_wait(bar, phase);
+            phase ^= 1;
+            tc_fence_after();
+        }
+
+        // ---- epilogue: D3 (48 SH coefficients, k*3 + c) -> rgb. Column half h holds
+        // coefficients k in [8h, 8h + 8) (24 columns).
+        {
+            float y[24];
+            tmem_ld16(tmem + lane_base + kColD3 + 24 * half, y);
+            tmem_ld8(tmem + lane_base + kColD3 + 24 * half + 16, y + 16);
+            const float x = static_cast<float>(dir[0]), yy_ = static_cast<float>(dir[1]), z = static_cast<float>(dir[2]);
+            const float xx = x * x, yy = yy_ * yy_, zz = z * z;
+            float b[8];
+            if (half == 0) {  // sh_basis (sh.hpp:11-40), k = 0..7
+                b[0] = 0.28209479177387814f;
+                b[1] = -0.4886025119029199f * yy_;
+                b[2] = 0.4886025119029199f * z;
+                b[3] = -0.4886025119029199f * x;
+                b[4] = 1.0925484305920792f * x * yy_;
+                b[5] = -1.0925484305920792f * yy_ * z;
+                b[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+                b[7] = -1.0925484305920792f * x * z;
+            } else {  // k = 8..15
+                b[0] = 0.5462742152960396f * (xx - yy);
+                b[1] = -0.5900435899266435f * yy_ * (3.0f * xx - yy);
+                b[2] = 2.890611442640554f * x * yy_ * z;
+                b[3] = -0.4570457994644658f * yy_ * (4.0f * zz - xx - yy);
+                b[4] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+                b[5] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
+                b[6] = 1.445305721320277f * z * (xx - yy);
+                b[7] = -0.5900435899266435f * x * (xx - 3.0f * yy);
+            }
+            float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                c0 = fmaf(y[3 * k + 0], b[k], c0);
+                c1 = fmaf(y[3 * k + 1], b[k], c1);
+                c2 = fmaf(y[3 * k + 2], b[k], c2);
+            }
+            if (half == 1) {
+                spart[row * 3 + 0] = c0;
+                spart[row * 3 + 1] = c1;
+                spart[row * 3 + 2] = c2;
+            }
+            tc_fence_before();
+            __syncthreads();
+            if (half == 0) {
+                float rgb[3] = {0.f, 0.f, 0.f};
+                if (valid) {
+                    rgb[0] = fmaxf(0.5f + (c0 + spart[row * 3 + 0]), 0.f);
+                    rgb[1] = fmaxf(0.5f + (c1 + spart[row * 3 + 1]), 0.f);
+                    rgb[2] = fmaxf(0.5f + (c2 + spart[row * 3 + 2]), 0.f);
+                }
+                float* dst = reinterpret_cast<float*>(smem + kOffRgb) + row * 3;
+                dst[0] = rgb[0];
+                dst[1] = rgb[1];
+                dst[2] = rgb[2];
+                if (row < rows_per_tile && slot < total) {
+                    a.fb.texture[slot * 3 + 0] = rgb[0];
+                    a.fb.texture[slot * 3 + 1] = rgb[1];
+                    a.fb.texture[slot * 3 + 2] = rgb[2];
+                }
+            }
+            __syncthreads();
+        }
+        // ---- Eq. 7: final = base + sum_j W[p,j] * texture[p,j] for this tile's pixels
+        const int ppt = rows_per_tile / K;
+        if (tid < ppt) {
+            const int64_t pix = tile * ppt + tid;
+            if (pix < static_cast<int64_t>(a.cam.W) * a.cam.H) {
+                double acc0 = a.fb.base[pix * 3 + 0], acc1 = a.fb.base[pix * 3 + 1], acc2 = a.fb.base[pix * 3 + 2];
+                for (int j = 0; j < K; ++j) {
+                    const int64_t sl = pix * K + j;
+                    if (a.fb.ids[sl] < 0) continue;
+                    const double w = a.fb.weights[sl];
+                    const float* tc = srgb + (tid * K + j) * 3;
+                    acc0 += w * tc[0];
+                    acc1 += w * tc[1];
+                    acc2 += w * tc[2];
+                }
+                a.fb.final_img[pix * 3 + 0] = static_cast<float>(acc0);
+                a.fb.final_img[pix * 3 + 1] = static_cast<float>(acc1);
+                a.fb.final_img[pix * 3 + 2] = static_cast<float>(acc2);
+            }
+        }
+        tc_fence_before();
+        __syncthreads();
+    }
+
+    // queries counted by the half-0 threads
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n_queries += __shfl_down_sync(0xffffffffu, n_queries, o);
+    if (lane == 0 && n_queries) atomicAdd(&a.stats->queries, static_cast<unsigned long long>(n_queries));
+    tc_fence_after();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
+}  // namespace
+
+bool texture_tc_supported(const nx_field_desc& fd) {
+    return fd.levels == kLevels && fd.features == 2 && fd.n_hidden == kHid;
+}
+
+int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
+    const int K = a.fb.K;
+    const int rows_per_tile = (kRows / K) * K;
+    const int64_t total = static_cast<int64_t>(a.cam.W) * a.cam.H * K;
+    const int64_t n_tiles = (total + rows_per_tile - 1) / rows_per_tile;
+    if (n_tiles == 0) return NX_OK;
+    TcConst cst;
+    double sc = a.scene.field.base_scale;
+    for (int l = 0; l < kLevels; ++l, sc *= a.scene.field.growth) {
+        cst.level_scale[l] = sc;
+        cst.inv_level_scale[l] = static_cast<float>(1.0 / sc);
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(texture_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemRequest);
+    const int64_t grid = std::min<int64_t>(n_tiles, 2 * static_cast<int64_t>(sms));
+    count_launch();
+    texture_tc_kernel<<<static_cast<unsigned>(grid), kTcThreads, kSmemRequest, s>>>(a, cst, rows_per_tile, n_tiles);
+    return NX_OK;
+}
+
+}  // namespace nx
