@@ -83,6 +83,34 @@ __global__ void __launch_bounds__(kScanThreads) scan_single_kernel(const int32_t
         *total_out = run;
 }
 
+// One block scans n <= kScanLoopMax values in rounds of kScanTile with a carry
+// (one launch instead of three for the radix histogram matrices).
+__global__ void __launch_bounds__(kScanThreads) scan_loop_kernel(const int32_t* in, int32_t* out, int64_t n,
+                                                                 int32_t* total_out) {
+    __shared__ int s_warp[33];
+    int carry = 0;
+    for (int64_t round = 0; round * kScanTile < n; ++round) {
+        const int64_t base = round * kScanTile + threadIdx.x * kScanItems;
+        int vals[kScanItems];
+        int v = 0;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            vals[k] = base + k < n ? in[base + k] : 0;
+            v += vals[k];
+        }
+        int total;
+        int run = block_excl_scan(v, s_warp, &total) + carry;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            if (base + k < n) out[base + k] = run;
+            run += vals[k];
+        }
+        carry += total;
+        __syncthreads();
+    }
+    if (total_out && threadIdx.x == 0) *total_out = carry;
+}
+
 template <typename K>
 __global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(const K* keys, int64_t n, int shift,
                                                                    int32_t* hist, int n_blocks) {
@@ -187,6 +215,11 @@ void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int32_t* total, 
     if (n_blocks == 1) {
         count_launch(1);
         scan_single_kernel<<<1, kScanThreads, 0, stream>>>(in, out, n, total, nullptr);
+        return;
+    }
+    if (n <= kScanLoopMax) {
+        count_launch(1);
+        scan_loop_kernel<<<1, kScanThreads, 0, stream>>>(in, out, n, total);
         return;
     }
     // n_blocks <= kScanTile is required (n <= 16.7M).

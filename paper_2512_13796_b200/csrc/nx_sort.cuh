@@ -11,6 +11,7 @@ void count_launch(int n);
 constexpr int kScanItems = 4;        // per thread
 constexpr int kScanThreads = 1024;
 constexpr int kScanTile = kScanItems * kScanThreads;
+constexpr int64_t kScanLoopMax = 16 * kScanTile;  // single-launch scan up to 64K values
 constexpr int kRadixThreads = 256;
 constexpr int kRadixTile = 4096;     // items per block per pass
 constexpr int kRadixBits = 8;
