@@ -78,8 +78,9 @@ struct nx_ctx {
     DevBuf dbg_hits, dbg_counts;
     int32_t* h_pinned = nullptr;  // small readbacks
     bool profiling = false;
-    cudaEvent_t ev[NX_NUM_STAGES + 1] = {};
-    bool ev_pending = false;          // a profiled frame whose events are not folded yet
+    cudaEvent_t ev[2][NX_NUM_STAGES + 1] = {};
+    int ev_cur = 0;
+    bool ev_pending[2] = {false, false};  // profiled frames whose events are not folded yet
     double stage_acc[NX_NUM_STAGES] = {};
     int stage_frames = 0;
 };
@@ -237,21 +238,24 @@ SceneDev scene_dev(const nx_scene* s) {
 }
 
 void record(nx_ctx* c, int stage, cudaStream_t s) {
-    if (c->profiling) cudaEventRecord(c->ev[stage], s);
+    if (c->profiling) cudaEventRecord(c->ev[c->ev_cur][stage], s);
 }
 
-// Folds the previous profiled frame's stage events into the running sums. Called
-// where the stream is already synchronised, so it never adds a sync of its own.
-void fold_stage_times(nx_ctx* c) {
-    if (!c->ev_pending) return;
+// Folds a completed profiled frame's stage events into the running sums.
+void fold_set(nx_ctx* c, int set) {
+    if (!c->ev_pending[set]) return;
     for (int i = 0; i < NX_NUM_STAGES; ++i) {
         float v = 0.f;
-        if (cudaEventElapsedTime(&v, c->ev[i], c->ev[i + 1]) == cudaSuccess) c->stage_acc[i] += v;
+        if (cudaEventElapsedTime(&v, c->ev[set][i], c->ev[set][i + 1]) == cudaSuccess) c->stage_acc[i] += v;
     }
     cudaGetLastError();
     c->stage_frames += 1;
-    c->ev_pending = false;
+    c->ev_pending[set] = false;
 }
+
+// Event sets alternate between frames, so the previous frame's set is folded at
+// the current frame's (already synchronised) mid-frame point: profiling adds no sync.
+void fold_stage_times(nx_ctx* c) { fold_set(c, c->ev_cur ^ 1); }
 
 int check_inputs(nx_ctx* c, const nx_scene* scene, const nx_camera* cam) {
     if (!c || !scene || !cam) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
@@ -291,8 +295,10 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
     NX_CUDA(c, c->scratch.ensure(scratch_ints * sizeof(int32_t)));
     NX_CUDA(c, cudaMemsetAsync(f->stats, 0, sizeof(FrameStatsD), s));
 
-    NX_CUDA(c, cudaStreamSynchronize(s));  // the previous frame on this stream is complete
-    fold_stage_times(c);
+    if (c->profiling) {
+        c->ev_cur ^= 1;
+        fold_set(c, c->ev_cur);  // only pending if the frame before last was never folded
+    }
     record(c, NX_STAGE_PREPROCESS, s);
     PreprocessArgs pa;
     pa.scene = scene_dev(scene);
@@ -315,24 +321,26 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
     // K2: compaction of the primitives that own work (id-ascending) + depth sort.
     int32_t* d_total = c->scratch.as<int32_t>();  // [0] n_sorted, [1] n_keys
     int32_t* sc = d_total + 64;
+    // The sorted count stays on the device: the sort runs over capacity n with the
+    // device count (no host round trip).
     scan_exclusive(c->flag.as<int32_t>(), c->pos.as<int32_t>(), n, d_total, sc, s);
-    NX_CUDA(c, cudaMemcpyAsync(c->h_pinned, d_total, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    NX_CUDA(c, cudaStreamSynchronize(s));
-    const int64_t n_sorted = n > 0 ? c->h_pinned[0] : 0;
-    (void)0;
     record(c, NX_STAGE_DEPTH_SORT, s);
     launch_compact(c->flag.as<int32_t>(), c->pos.as<int32_t>(), c->key.as<uint64_t>(), n, c->skeys_a.as<uint64_t>(),
                    c->sids_a.as<uint32_t>(), s);
     const bool in_b = radix_sort_pairs_u64(c->skeys_a.as<uint64_t>(), c->sids_a.as<uint32_t>(),
-                                           c->skeys_b.as<uint64_t>(), c->sids_b.as<uint32_t>(), n_sorted, 0, 64, sc, s);
+                                           c->skeys_b.as<uint64_t>(), c->sids_b.as<uint32_t>(), n, d_total, 0, 64, sc,
+                                           s);
     const uint32_t* sorted_ids = in_b ? c->sids_b.as<uint32_t>() : c->sids_a.as<uint32_t>();
 
-    // K3: emit (tile, id) keys in sorted order.
+    // K3: emit (tile, id) keys in sorted order. The one host round trip of the frame:
+    // the key count sizes the key buffers.
     record(c, NX_STAGE_EMIT, s);
-    launch_rect_counts(sorted_ids, n_sorted, c->work_rect.as<int4>(), c->counts.as<int32_t>(), s);
-    scan_exclusive(c->counts.as<int32_t>(), c->offsets.as<int32_t>(), n_sorted, d_total + 1, sc, s);
-    NX_CUDA(c, cudaMemcpyAsync(c->h_pinned + 1, d_total + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    launch_rect_counts(sorted_ids, n, d_total, c->work_rect.as<int4>(), c->counts.as<int32_t>(), s);
+    scan_exclusive(c->counts.as<int32_t>(), c->offsets.as<int32_t>(), n, d_total + 1, sc, s);
+    NX_CUDA(c, cudaMemcpyAsync(c->h_pinned, d_total, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     NX_CUDA(c, cudaStreamSynchronize(s));
+    fold_stage_times(c);  // the previous profiled frame's events are complete
+    const int64_t n_sorted = n > 0 ? c->h_pinned[0] : 0;
     const int64_t n_keys = n_sorted > 0 ? c->h_pinned[1] : 0;
     if (n_keys < 0) return set_err(c, NX_UNSUPPORTED, "tile-key count exceeds 2^31");
     const int64_t nk = std::max<int64_t>(n_keys, 1);
@@ -355,7 +363,8 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
     record(c, NX_STAGE_TILE_SORT, s);
     const int tb = std::max(bits_for(n_tiles), 1);
     const bool t_in_b = radix_sort_pairs_u32(c->tkeys_a.as<uint32_t>(), c->tvals_a.as<uint32_t>(),
-                                             c->tkeys_b.as<uint32_t>(), c->tvals_b.as<uint32_t>(), n_keys, 0, tb, sc, s);
+                                             c->tkeys_b.as<uint32_t>(), c->tvals_b.as<uint32_t>(), n_keys, nullptr, 0,
+                                             tb, sc, s);
     // K5: tile ranges.
     scan_exclusive(c->tile_counts.as<int32_t>(), f->tile_offsets.as<int32_t>(), n_tiles + 1, nullptr, sc, s);
     f->list_ids.p = t_in_b ? c->tvals_b.p : c->tvals_a.p;  // borrowed (not owned)
@@ -408,7 +417,7 @@ int texturing(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* 
     const int st = launch_texture(ta, s);
     if (st) return set_err(c, st, "texture field shape not supported (n_in <= 64, n_hidden <= 128)");
     record(c, NX_NUM_STAGES, s);
-    if (c->profiling) c->ev_pending = true;
+    if (c->profiling) c->ev_pending[c->ev_cur] = true;
     NX_CUDA(c, cudaGetLastError());
     return NX_OK;
 }
@@ -459,7 +468,8 @@ int nx_ctx_create(int device, nx_ctx** out) {
         delete c;
         return NX_CUDA_ERROR;
     }
-    for (auto& e : c->ev) cudaEventCreate(&e);
+    for (auto& set : c->ev)
+        for (auto& e : set) cudaEventCreate(&e);
     *out = c;
     return NX_OK;
 }
@@ -472,7 +482,8 @@ void nx_ctx_destroy(nx_ctx* c) {
                       &c->skeys_b, &c->sids_a, &c->sids_b, &c->counts, &c->offsets, &c->tkeys_a, &c->tkeys_b,
                       &c->tvals_a, &c->tvals_b, &c->tile_counts, &c->scratch, &c->dbg_hits, &c->dbg_counts})
         b->release();
-    for (auto& e : c->ev) cudaEventDestroy(e);
+    for (auto& set : c->ev)
+        for (auto& e : set) cudaEventDestroy(e);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
     cudaStreamDestroy(c->stream);
     delete c;
@@ -500,7 +511,8 @@ int nx_ctx_set_profiling(nx_ctx* c, int enable) {
 int nx_ctx_stage_times(nx_ctx* c, float* ms, int n, int* frames) {
     if (!c || !ms) return NX_INVALID_ARGUMENT;
     NX_CUDA(c, cudaDeviceSynchronize());
-    fold_stage_times(c);
+    fold_set(c, c->ev_cur ^ 1);
+    fold_set(c, c->ev_cur);
     for (int i = 0; i < n && i < NX_NUM_STAGES; ++i)
         ms[i] = c->stage_frames ? static_cast<float>(c->stage_acc[i] / c->stage_frames) : 0.f;
     if (frames) *frames = c->stage_frames;

@@ -176,8 +176,8 @@ void launch_preprocess(const PreprocessArgs& a, cudaStream_t s);
 void launch_compact(const int32_t* flag, const int32_t* pos, const uint64_t* key, int64_t n,
                     uint64_t* keys_out, uint32_t* ids_out, cudaStream_t s);
 
-// counts[r] = tiles of rect[ids[r]] (work or reference rect).
-void launch_rect_counts(const uint32_t* ids, int64_t n, const int4* rect, int32_t* counts,
+// counts[r] = tiles of rect[ids[r]] (work or reference rect) for r < *n_dev, 0 up to n.
+void launch_rect_counts(const uint32_t* ids, int64_t n, const int32_t* n_dev, const int4* rect, int32_t* counts,
                         cudaStream_t s);
 
 // Emits (tile, id) for every tile of every sorted primitive's rect, in sorted

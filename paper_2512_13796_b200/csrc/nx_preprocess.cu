@@ -245,9 +245,13 @@ __global__ void compact_kernel(const int32_t* flag, const int32_t* pos, const ui
     }
 }
 
-__global__ void rect_counts_kernel(const uint32_t* ids, int64_t n, const int4* rect, int32_t* counts) {
+// counts over the capacity n: entries past the device count are zero, so a scan over
+// the whole capacity yields the right offsets and total.
+__global__ void rect_counts_kernel(const uint32_t* ids, int64_t n, const int32_t* n_dev, const int4* rect,
+                                   int32_t* counts) {
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (r < n) counts[r] = rect_tiles(rect[ids[r]]);
+    const int64_t m = n_dev ? min(n, static_cast<int64_t>(*n_dev)) : n;
+    if (r < n) counts[r] = r < m ? rect_tiles(rect[ids[r]]) : 0;
 }
 
 // One thread per emitted key: binary search of the owning sorted primitive.
@@ -288,10 +292,11 @@ void launch_compact(const int32_t* flag, const int32_t* pos, const uint64_t* key
     compact_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(flag, pos, key, n, keys_out, ids_out);
 }
 
-void launch_rect_counts(const uint32_t* ids, int64_t n, const int4* rect, int32_t* counts, cudaStream_t s) {
+void launch_rect_counts(const uint32_t* ids, int64_t n, const int32_t* n_dev, const int4* rect, int32_t* counts,
+                        cudaStream_t s) {
     if (n <= 0) return;
     count_launch();
-    rect_counts_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(ids, n, rect, counts);
+    rect_counts_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(ids, n, n_dev, rect, counts);
 }
 
 void launch_emit(const uint32_t* ids, const int32_t* offsets, int64_t n_sorted, int64_t n_keys,

@@ -111,10 +111,17 @@ __global__ void __launch_bounds__(kScanThreads) scan_loop_kernel(const int32_t* 
     if (total_out && threadIdx.x == 0) *total_out = carry;
 }
 
+// n = device count (capped by the host capacity n_cap) when n_dev != nullptr.
+__device__ __forceinline__ int64_t dev_count(int64_t n_cap, const int32_t* n_dev) {
+    return n_dev ? min(n_cap, static_cast<int64_t>(*n_dev)) : n_cap;
+}
+
 template <typename K>
-__global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(const K* keys, int64_t n, int shift,
+__global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(const K* keys, int64_t n_cap,
+                                                                   const int32_t* n_dev, int shift,
                                                                    int32_t* hist, int n_blocks) {
     __shared__ int s_hist[kRadixBuckets];
+    const int64_t n = dev_count(n_cap, n_dev);
     s_hist[threadIdx.x] = 0;
     __syncthreads();
     const int64_t base = static_cast<int64_t>(blockIdx.x) * kRadixTile;
@@ -131,12 +138,16 @@ __global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(const K* _
                                                                       const uint32_t* __restrict__ vals_in,
                                                                       K* __restrict__ keys_out,
                                                                       uint32_t* __restrict__ vals_out,
-                                                                      int64_t n, int shift,
+                                                                      int64_t n_cap,
+                                                                      const int32_t* __restrict__ n_dev,
+                                                                      int shift,
                                                                       const int32_t* __restrict__ offsets,
                                                                       int n_blocks) {
     constexpr int kWarps = kRadixThreads / 32;
     __shared__ int s_base[kRadixBuckets];
     __shared__ int s_cnt[kWarps][kRadixBuckets];
+    const int64_t n = dev_count(n_cap, n_dev);
+    if (static_cast<int64_t>(blockIdx.x) * kRadixTile >= n) return;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     s_base[tid] = offsets[static_cast<int64_t>(tid) * n_blocks + blockIdx.x];
     const int64_t base = static_cast<int64_t>(blockIdx.x) * kRadixTile;
@@ -179,8 +190,8 @@ __global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(const K* _
 }
 
 template <typename K>
-bool radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n, int begin_bit,
-                     int end_bit, int32_t* scratch, cudaStream_t stream) {
+bool radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n,
+                     const int32_t* n_dev, int begin_bit, int end_bit, int32_t* scratch, cudaStream_t stream) {
     if (n <= 1) return false;
     const int n_blocks = static_cast<int>((n + kRadixTile - 1) / kRadixTile);
     const int64_t hist_n = static_cast<int64_t>(n_blocks) * kRadixBuckets;
@@ -193,9 +204,10 @@ bool radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, i
         K* ko = in_alt ? keys : keys_alt;
         uint32_t* vo = in_alt ? vals : vals_alt;
         count_launch(2);
-        radix_hist_kernel<K><<<n_blocks, kRadixThreads, 0, stream>>>(ki, n, bit, hist, n_blocks);
+        radix_hist_kernel<K><<<n_blocks, kRadixThreads, 0, stream>>>(ki, n, n_dev, bit, hist, n_blocks);
         scan_exclusive(hist, hist, hist_n, nullptr, scan_scratch, stream);
-        radix_scatter_kernel<K><<<n_blocks, kRadixThreads, 0, stream>>>(ki, vi, ko, vo, n, bit, hist, n_blocks);
+        radix_scatter_kernel<K><<<n_blocks, kRadixThreads, 0, stream>>>(ki, vi, ko, vo, n, n_dev, bit, hist,
+                                                                        n_blocks);
         in_alt = !in_alt;
     }
     return in_alt;
@@ -237,13 +249,15 @@ size_t radix_scratch_ints(int64_t n) {
 }
 
 bool radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,
-                          int64_t n, int begin_bit, int end_bit, int32_t* scratch, cudaStream_t stream) {
-    return radix_sort_impl<uint64_t>(keys, vals, keys_alt, vals_alt, n, begin_bit, end_bit, scratch, stream);
+                          int64_t n, const int32_t* n_dev, int begin_bit, int end_bit, int32_t* scratch,
+                          cudaStream_t stream) {
+    return radix_sort_impl<uint64_t>(keys, vals, keys_alt, vals_alt, n, n_dev, begin_bit, end_bit, scratch, stream);
 }
 
 bool radix_sort_pairs_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
-                          int64_t n, int begin_bit, int end_bit, int32_t* scratch, cudaStream_t stream) {
-    return radix_sort_impl<uint32_t>(keys, vals, keys_alt, vals_alt, n, begin_bit, end_bit, scratch, stream);
+                          int64_t n, const int32_t* n_dev, int begin_bit, int end_bit, int32_t* scratch,
+                          cudaStream_t stream) {
+    return radix_sort_impl<uint32_t>(keys, vals, keys_alt, vals_alt, n, n_dev, begin_bit, end_bit, scratch, stream);
 }
 
 }  // namespace nx

@@ -27,10 +27,14 @@ void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int32_t* total, 
 // Stable LSD radix sort of (key, value) pairs over key bits [begin_bit, end_bit).
 // Ping-pongs between (keys, vals) and (keys_alt, vals_alt); returns true if the
 // sorted result ended in the *_alt buffers. Scratch: radix_scratch_ints(n) ints.
+// n is the host-side capacity (grid size); if n_dev != nullptr the actual count is
+// read on the device (no host round trip), capped by n.
 size_t radix_scratch_ints(int64_t n);
 bool radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,
-                          int64_t n, int begin_bit, int end_bit, int32_t* scratch, cudaStream_t stream);
+                          int64_t n, const int32_t* n_dev, int begin_bit, int end_bit, int32_t* scratch,
+                          cudaStream_t stream);
 bool radix_sort_pairs_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
-                          int64_t n, int begin_bit, int end_bit, int32_t* scratch, cudaStream_t stream);
+                          int64_t n, const int32_t* n_dev, int begin_bit, int end_bit, int32_t* scratch,
+                          cudaStream_t stream);
 
 }  // namespace nx

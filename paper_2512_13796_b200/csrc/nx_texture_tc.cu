@@ -31,8 +31,10 @@ constexpr int kTcThreads = 256;
 constexpr int kRows = 128;
 constexpr int kLevels = 16;
 constexpr int kIn = 32, kHid = 64, kOut = 48;
-constexpr uint32_t kTmemCols = 256;
-constexpr uint32_t kColD1 = 0, kColD2 = 64, kColD3 = 128;
+// D1, D2 and D3 share columns 0..63: each is drained (tcgen05.ld + wait + fence +
+// barrier) before the next layer's MMAs overwrite it.
+constexpr uint32_t kTmemCols = 64;
+constexpr uint32_t kColD1 = 0, kColD2 = 0, kColD3 = 0;
 
 // shared-memory carve-up (bytes)
 constexpr int kOffW1h = 0;
@@ -150,7 +152,7 @@ __device__ __forceinline__ uint32_t map_positive32(long long x) {  // hash_grid.
 }
 
 __global__ void __launch_bounds__(kTcThreads, 2) texture_tc_kernel(const TextureArgs a, const TcConst cst,
-                                                                   int rows_per_tile, int64_t n_tiles) {
+                                                                   int bw, int bh, int tiles_x, int64_t n_tiles) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t bar = smem_u32(smem + kOffBar);
@@ -195,7 +197,6 @@ __global__ void __launch_bounds__(kTcThreads, 2) texture_tc_kernel(const Texture
 
     const int K = a.fb.K;
     const int W = a.cam.W;
-    const int64_t total = static_cast<int64_t>(a.cam.W) * a.cam.H * K;
     const int row = tid & (kRows - 1);  // == 32 * (warp % 4) + lane: the TMEM lane this thread reads
     const int half = tid >> 7;          // gather: levels [8 half, 8 half + 8); epilogue: column half
     const uint32_t lane_base = static_cast<uint32_t>(32 * (warp & 3)) << 16;
@@ -208,15 +209,19 @@ __global__ void __launch_bounds__(kTcThreads, 2) texture_tc_kernel(const Texture
     constexpr uint32_t kIdesc48 = idesc_bf16_f32(kRows, 48);
     int n_queries = 0;
 
+    const int ppt = bw * bh;  // pixels per tile; rows = ppt * K <= 128
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int64_t slot = tile * rows_per_tile + row;
-        const bool valid = row < rows_per_tile && slot < total && a.fb.ids[slot] >= 0;
+        // row -> (pixel of the bw x bh block, slot j): neighbouring rows are neighbouring pixels
+        const int tpx = static_cast<int>(tile % tiles_x) * bw, tpy = static_cast<int>(tile / tiles_x) * bh;
+        const int p_in = row / K, j_in = row - (row / K) * K;
+        const int px = tpx + p_in % bw, py = tpy + p_in / bw;
+        const bool in_tile = p_in < ppt && px < W && py < a.cam.H;
+        const int64_t slot = in_tile ? (static_cast<int64_t>(py) * W + px) * K + j_in : 0;
+        const bool valid = in_tile && a.fb.ids[slot] >= 0;
         if (valid && half == 0) ++n_queries;
         double dir[3] = {0.0, 0.0, 1.0};
         float feats[16];
         if (valid) {
-            const int64_t pix = slot / K;
-            const int px = static_cast<int>(pix % W), py = static_cast<int>(pix / W);
             pixel_dir(a.cam, px + 0.5, py + 0.5, dir);
             const double t = a.fb.depths[slot];
             const double x0 = a.cam.o[0] + t * dir[0];
@@ -376,7 +381,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) texture_tc_kernel(const Texture
                 dst[0] = rgb[0];
                 dst[1] = rgb[1];
                 dst[2] = rgb[2];
-                if (row < rows_per_tile && slot < total) {
+                if (in_tile) {
                     a.fb.texture[slot * 3 + 0] = rgb[0];
                     a.fb.texture[slot * 3 + 1] = rgb[1];
                     a.fb.texture[slot * 3 + 2] = rgb[2];
@@ -385,10 +390,10 @@ __global__ void __launch_bounds__(kTcThreads, 2) texture_tc_kernel(const Texture
             __syncthreads();
         }
         // ---- Eq. 7: final = base + sum_j W[p,j] * texture[p,j] for this tile's pixels
-        const int ppt = rows_per_tile / K;
         if (tid < ppt) {
-            const int64_t pix = tile * ppt + tid;
-            if (pix < static_cast<int64_t>(a.cam.W) * a.cam.H) {
+            const int qx = tpx + tid % bw, qy = tpy + tid / bw;
+            if (qx < W && qy < a.cam.H) {
+                const int64_t pix = static_cast<int64_t>(qy) * W + qx;
                 double acc0 = a.fb.base[pix * 3 + 0], acc1 = a.fb.base[pix * 3 + 1], acc2 = a.fb.base[pix * 3 + 2];
                 for (int j = 0; j < K; ++j) {
                     const int64_t sl = pix * K + j;
@@ -425,9 +430,13 @@ bool texture_tc_supported(const nx_field_desc& fd) {
 
 int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
     const int K = a.fb.K;
-    const int rows_per_tile = (kRows / K) * K;
-    const int64_t total = static_cast<int64_t>(a.cam.W) * a.cam.H * K;
-    const int64_t n_tiles = (total + rows_per_tile - 1) / rows_per_tile;
+    // Tiles are pixel blocks (8 wide) so that neighbouring rows query neighbouring
+    // lattice cells; K that do not divide 128 use a one-row block of 128/K pixels.
+    const int ppt = kRows / K;
+    const int bw = (kRows % K == 0 && ppt % 8 == 0) ? 8 : ppt;
+    const int bh = ppt / bw;
+    const int tiles_x = (a.cam.W + bw - 1) / bw;
+    const int64_t n_tiles = static_cast<int64_t>(tiles_x) * ((a.cam.H + bh - 1) / bh);
     if (n_tiles == 0) return NX_OK;
     TcConst cst;
     double sc = a.scene.field.base_scale;
@@ -441,7 +450,7 @@ int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(texture_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemRequest);
     const int64_t grid = std::min<int64_t>(n_tiles, 2 * static_cast<int64_t>(sms));
     count_launch();
-    texture_tc_kernel<<<static_cast<unsigned>(grid), kTcThreads, kSmemRequest, s>>>(a, cst, rows_per_tile, n_tiles);
+    texture_tc_kernel<<<static_cast<unsigned>(grid), kTcThreads, kSmemRequest, s>>>(a, cst, bw, bh, tiles_x, n_tiles);
     return NX_OK;
 }
 
