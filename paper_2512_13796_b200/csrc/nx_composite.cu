@@ -17,6 +17,7 @@
 // longest queue of its pixels instead of the union of all their hits. Every
 // decision is taken in fp64 with the reference formulas; the prefilter only
 // skips provable misses, so contributor lists are bit-exact.
+#include "nx_fp64math.h"
 #include "nx_internal.cuh"
 
 namespace nx {
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(const CompositeA
                         if (fabs(dv) > r[REC_VLIM]) continue;
                         const double u = du / r[REC_SX];
                         const double v = dv / r[REC_SY];
-                        const double alpha_raw = eval_kernel(u, v, r[REC_OP], r[REC_GX], r[REC_GY]);
+                        const double alpha_raw = fm::eval_kernel(u, v, r[REC_OP], r[REC_GX], r[REC_GY]);
                         if (alpha_raw < kAlphaMin) continue;
                         // composite (renderer.cpp:146-152)
                         const int32_t id = s_id[j];
