@@ -2,22 +2,22 @@
 // and a top-K buffer (collection_pass, renderer.cpp:115-171).
 //
 // One CTA per screen tile, one thread per pixel. The tile's work list (ids in
-// (depth, id) order) is walked in chunks of kChunk primitives whose records are
-// staged into shared memory. Per chunk, each pixel
-//   A. runs an fp32 conservative prefilter over every primitive of the chunk
-//      (broadcast smem reads, no divergence) and records the survivors in a
-//      128-bit mask: a test is dropped only if it provably fails the reference's
-//      t > near_eps or |u| <= ru, |v| <= rv conditions (hence alpha < 1/255),
-//      with a rigorous fp32 error slack;
-//   B. walks its own survivors in list order on the exact fp64 path — the
-//      reference's intersect() formulas (intersect.hpp:23-42), eval_kernel, the
-//      1/255 test, alpha clamp, top-K insert, transmittance update and
-//      termination (renderer.cpp:144-153).
-// Lanes walk their own survivor queues in lockstep, so a warp pays for the
-// longest queue of its pixels instead of the union of all their hits. Every
-// decision is taken in fp64 with the reference formulas; the prefilter only
-// skips provable misses, so contributor lists are bit-exact.
-#include "nx_fp64math.h"
+// (depth, id) order) is walked in chunks of kChunk primitives staged into shared
+// memory. Per chunk and per group of kSub primitives, each warp
+//   A. prefilters (fp32, conservative) every (pixel, primitive)
+//      pair: a pair is dropped only if it provably fails the reference's
+//      t > near_eps or |u| <= ru, |v| <= rv conditions (hence alpha < 1/255);
+//   B1. pools the survivors of its 32 pixels and evaluates them with all 32 lanes
+//      busy on the exact fp64 path — the reference's intersect() formulas
+//      (intersect.hpp:23-42) and eval_kernel (kernel.hpp:16-30) — plus the
+//      primitive's SH colour (fp32, colour only);
+//   B2. composites, per pixel and in list order, its own survivors: alpha clamp,
+//      weight, top-K insert, transmittance update and termination
+//      (renderer.cpp:144-153), all fp64.
+// Every decision is the reference's, taken in fp64 with its formulas; the
+// prefilter only skips provable misses, so contributor lists are bit-exact. The
+// pooling keeps the expensive transcendental path at full warp width, whereas a
+// per-pixel walk would run it at the width of the pixels that happen to hit.
 #include "nx_internal.cuh"
 
 namespace nx {
@@ -25,10 +25,28 @@ namespace nx {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kChunk = 128;
-constexpr int kRecPairs = REC_FIELDS / 2;      // double2 per fp64 record (10)
-constexpr int kRecStride = kRecPairs + 1;      // padded to 11 double2 (176 B): lanes reading
-                                               // different records hit different bank groups
+constexpr int kWarps = kThreads / 32;
+constexpr int kChunk = 64;                 // primitives staged per round
+constexpr int kSub = 8;                    // primitives pooled per B1/B2 round (<= 256 entries per warp)
+constexpr int kPool = 32 * kSub;
+constexpr int kRecPairs = REC_FIELDS / 2;  // double2 per fp64 record (10)
+constexpr int kRecStride = kRecPairs + 1;  // padded to 11 double2: different records hit different bank groups
+
+struct PoolEntry {  // one evaluated (pixel, primitive) pair
+    double alpha;   // raw kernel alpha, < 0 for a miss
+    double t;       // plane crossing
+    float rgb[3];   // primitive colour along the ray
+    float pad;
+};
+
+struct SmemLayout {
+    float4 f[kChunk][4];
+    double2 d[kChunk][kRecStride];
+    int32_t id[kChunk];
+    double dir[kThreads][3];
+    uint16_t q[kWarps][kPool];
+    PoolEntry res[kWarps][kPool];
+};
 
 // Primitive SH colour (eval_sh, sh.hpp:46-57) in fp32 from the ray direction:
 // colour outputs are tolerance-checked (max-abs 1e-3), decisions never use it.
@@ -96,17 +114,18 @@ __device__ __forceinline__ bool prefilter(const float4* f, float dfx, float dfy,
 template <int K, bool kDebug>
 __global__ void __launch_bounds__(kThreads, 2) composite_kernel(const CompositeArgs a) {
     constexpr int KK = K > 0 ? K : 1;
-    __shared__ float4 s_f[kChunk][4];
-    __shared__ double2 s_d[kChunk][kRecStride];
-    __shared__ int32_t s_id[kChunk];
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    SmemLayout& sm = *reinterpret_cast<SmemLayout*>(smem_raw);
 
     const int tile = a.st.tile;
     const int t = blockIdx.x;
     const int tx = t % a.fb.tiles_x, ty = t / a.fb.tiles_x;
     const int list_begin = a.tile_offsets[t], list_end = a.tile_offsets[t + 1];
     const int W = a.cam.W, H = a.cam.H;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double near_eps = a.st.near_eps, alpha_max = a.st.alpha_max, min_T = a.st.min_transmittance;
     const float near_eps_f = static_cast<float>(near_eps);
+    const double o0 = a.cam.o[0], o1 = a.cam.o[1], o2 = a.cam.o[2];
 
     for (int pbase = 0; pbase < tile * tile; pbase += kThreads) {
         const int lp = pbase + threadIdx.x;
@@ -114,9 +133,11 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(const CompositeA
         const bool in_img = lp < tile * tile && px < W && py < H;
         double dir[3] = {0.0, 0.0, 1.0};
         if (in_img) pixel_dir(a.cam, px + 0.5, py + 0.5, dir);
+        sm.dir[threadIdx.x][0] = dir[0];
+        sm.dir[threadIdx.x][1] = dir[1];
+        sm.dir[threadIdx.x][2] = dir[2];
         const float dfx = static_cast<float>(dir[0]), dfy = static_cast<float>(dir[1]),
                     dfz = static_cast<float>(dir[2]);
-        const double o0 = a.cam.o[0], o1 = a.cam.o[1], o2 = a.cam.o[2];
 
         double T = 1.0;
         double acc[3] = {0.0, 0.0, 0.0};
@@ -143,60 +164,93 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(const CompositeA
             for (int e = threadIdx.x; e < cn * 4; e += kThreads) {
                 const int j = e >> 2, q = e & 3;
                 const int32_t id = __ldg(a.list_ids + cb + j);
-                s_f[j][q] = __ldg(a.recf + static_cast<int64_t>(id) * 4 + q);
-                if (q == 0) s_id[j] = id;
+                sm.f[j][q] = __ldg(a.recf + static_cast<int64_t>(id) * 4 + q);
+                if (q == 0) sm.id[j] = id;
             }
             for (int e = threadIdx.x; e < cn * kRecPairs; e += kThreads) {
                 const int j = e / kRecPairs, q = e - j * kRecPairs;
                 const int32_t id = __ldg(a.list_ids + cb + j);
-                s_d[j][q] = __ldg(reinterpret_cast<const double2*>(a.rec) + static_cast<int64_t>(id) * kRecPairs + q);
+                sm.d[j][q] = __ldg(reinterpret_cast<const double2*>(a.rec) + static_cast<int64_t>(id) * kRecPairs + q);
             }
             __syncthreads();
-            if (active) {
-                // ---- A. prefilter the whole chunk into a survivor mask
-                uint32_t m[kChunk / 32];
-#pragma unroll
-                for (int w = 0; w < kChunk / 32; ++w) {
-                    uint32_t bits = 0;
-                    const int jn = min(32, cn - 32 * w);
+            if (__any_sync(0xffffffffu, active)) {
+                for (int sb = 0; sb < cn; sb += kSub) {
+                    const int sn = min(kSub, cn - sb);
+                    // ---- A. prefilter this group of primitives
+                    uint32_t mask = 0;
+                    if (active) {
 #pragma unroll 4
-                    for (int b = 0; b < jn; ++b)
-                        if (prefilter(&s_f[32 * w + b][0], dfx, dfy, dfz, near_eps_f)) bits |= 1u << b;
-                    m[w] = bits;
-                }
-                // ---- B. exact fp64 path over this lane's survivors, in list order
+                        for (int b = 0; b < sn; ++b)
+                            if (prefilter(&sm.f[sb + b][0], dfx, dfy, dfz, near_eps_f)) mask |= 1u << b;
+                    }
+                    // warp-wide pool: exclusive offsets of each lane's survivors
+                    const int cnt = __popc(mask);
+                    int incl = cnt;
 #pragma unroll
-                for (int w = 0; w < kChunk / 32; ++w) {
-                    uint32_t bits = m[w];
-                    while (bits && active) {
-                        const int j = 32 * w + (__ffs(bits) - 1);
-                        bits &= bits - 1;
-                        const double* r = reinterpret_cast<const double*>(&s_d[j][0]);
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    const int off = incl - cnt;
+                    const int total = __shfl_sync(0xffffffffu, incl, 31);
+                    if (total == 0) continue;
+                    {
+                        uint32_t m = mask;
+                        int k = off;
+                        while (m) {
+                            const int b = __ffs(m) - 1;
+                            m &= m - 1;
+                            sm.q[warp][k++] = static_cast<uint16_t>((lane << 8) | (sb + b));
+                        }
+                    }
+                    __syncwarp();
+                    // ---- B1. exact fp64 evaluation of the pooled pairs, all lanes busy
+                    for (int e = lane; e < total; e += 32) {
+                        const int ent = sm.q[warp][e];
+                        const int owner = ent >> 8, j = ent & 0xff;
+                        const double* dd = sm.dir[warp * 32 + owner];
+                        const double d0 = dd[0], d1 = dd[1], d2 = dd[2];
+                        const double* r = reinterpret_cast<const double*>(&sm.d[j][0]);
+                        PoolEntry res;
+                        res.alpha = -1.0;
+                        res.t = 0.0;
                         // intersect (intersect.hpp:23-42)
-                        const double denom = dir[0] * r[REC_NX] + dir[1] * r[REC_NY] + dir[2] * r[REC_NZ];
-                        if (fabs(denom) < kMinNormalDot) continue;
-                        const double tt = r[REC_NUM] / denom;
-                        if (!(tt > near_eps)) continue;
-                        const double e0 = (o0 + tt * dir[0]) - r[REC_MUX];
-                        const double e1 = (o1 + tt * dir[1]) - r[REC_MUY];
-                        const double e2 = (o2 + tt * dir[2]) - r[REC_MUZ];
-                        const double du = e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z];
-                        if (fabs(du) > r[REC_ULIM]) continue;
-                        const double dv = e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z];
-                        if (fabs(dv) > r[REC_VLIM]) continue;
-                        const double u = du / r[REC_SX];
-                        const double v = dv / r[REC_SY];
-                        const double alpha_raw = fm::eval_kernel(u, v, r[REC_OP], r[REC_GX], r[REC_GY]);
-                        if (alpha_raw < kAlphaMin) continue;
-                        // composite (renderer.cpp:146-152)
-                        const int32_t id = s_id[j];
-                        const double alpha = alpha_max < alpha_raw ? alpha_max : alpha_raw;
+                        const double denom = d0 * r[REC_NX] + d1 * r[REC_NY] + d2 * r[REC_NZ];
+                        if (fabs(denom) >= kMinNormalDot) {
+                            const double tt = r[REC_NUM] / denom;
+                            if (tt > near_eps) {
+                                const double e0 = (o0 + tt * d0) - r[REC_MUX];
+                                const double e1 = (o1 + tt * d1) - r[REC_MUY];
+                                const double e2 = (o2 + tt * d2) - r[REC_MUZ];
+                                const double du = e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z];
+                                const double dv = e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z];
+                                if (fabs(du) <= r[REC_ULIM] && fabs(dv) <= r[REC_VLIM]) {
+                                    const double u = du / r[REC_SX];
+                                    const double v = dv / r[REC_SY];
+                                    const double al = eval_kernel(u, v, r[REC_OP], r[REC_GX], r[REC_GY]);
+                                    if (al >= kAlphaMin) {
+                                        res.alpha = al;
+                                        res.t = tt;
+                                        eval_sh_f32(a.sh + static_cast<int64_t>(sm.id[j]) * NX_SH_VALUES,
+                                                    static_cast<float>(d0), static_cast<float>(d1),
+                                                    static_cast<float>(d2), a.sh_degree, res.rgb);
+                                    }
+                                }
+                            }
+                        }
+                        sm.res[warp][e] = res;
+                    }
+                    __syncwarp();
+                    // ---- B2. per-pixel compositing of this lane's hits, in list order (renderer.cpp:144-153)
+                    for (int k = off; k < off + cnt && active; ++k) {
+                        const PoolEntry& res = sm.res[warp][k];
+                        if (res.alpha < 0.0) continue;
+                        const int32_t id = sm.id[sm.q[warp][k] & 0xff];
+                        const double alpha = alpha_max < res.alpha ? alpha_max : res.alpha;
                         const double wgt = alpha * T;
-                        float col[3];
-                        eval_sh_f32(a.sh + static_cast<int64_t>(id) * NX_SH_VALUES, dfx, dfy, dfz, a.sh_degree, col);
-                        acc[0] += wgt * col[0];
-                        acc[1] += wgt * col[1];
-                        acc[2] += wgt * col[2];
+                        acc[0] += wgt * res.rgb[0];
+                        acc[1] += wgt * res.rgb[1];
+                        acc[2] += wgt * res.rgb[2];
                         if (K > 0) {  // TopKBuffer::insert (framebuffers.hpp:33-48)
                             const uint32_t seq = counter++;
                             if (k_size < K) {
@@ -205,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(const CompositeA
                                     if (s == k_size) {
                                         k_id[s] = id;
                                         k_w[s] = wgt;
-                                        k_t[s] = tt;
+                                        k_t[s] = res.t;
                                         k_seq[s] = seq;
                                     }
                                 ++k_size;
@@ -226,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(const CompositeA
                                     if (s == mi && wgt > wm) {
                                         k_id[s] = id;
                                         k_w[s] = wgt;
-                                        k_t[s] = tt;
+                                        k_t[s] = res.t;
                                         k_seq[s] = seq;
                                     }
                             }
@@ -238,6 +292,7 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(const CompositeA
                         T *= 1.0 - alpha;
                         if (T < min_T) active = false;
                     }
+                    __syncwarp();
                 }
             }
             if (!__syncthreads_or(active)) break;
@@ -294,22 +349,30 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(const CompositeA
             a.fb.base[pix * 3 + 2] = static_cast<float>(acc[2]);
             if (kDebug && dbg_row) a.dbg_counts[dbg_q] = dbg_n;
         }
+        __syncthreads();  // sm.dir is rewritten by the next pixel pass
     }
+}
+
+template <int K, bool kDebug>
+void launch_one(const CompositeArgs& a, unsigned grid, cudaStream_t s) {
+    const size_t smem = sizeof(SmemLayout);
+    cudaFuncSetAttribute(composite_kernel<K, kDebug>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    composite_kernel<K, kDebug><<<grid, kThreads, smem, s>>>(a);
 }
 
 template <bool kDebug>
 void launch_k(const CompositeArgs& a, cudaStream_t s) {
     const unsigned grid = static_cast<unsigned>(a.fb.tiles_x) * a.fb.tiles_y;
     switch (a.fb.K) {
-        case 0: composite_kernel<0, kDebug><<<grid, kThreads, 0, s>>>(a); break;
-        case 1: composite_kernel<1, kDebug><<<grid, kThreads, 0, s>>>(a); break;
-        case 2: composite_kernel<2, kDebug><<<grid, kThreads, 0, s>>>(a); break;
-        case 3: composite_kernel<3, kDebug><<<grid, kThreads, 0, s>>>(a); break;
-        case 4: composite_kernel<4, kDebug><<<grid, kThreads, 0, s>>>(a); break;
-        case 5: composite_kernel<5, kDebug><<<grid, kThreads, 0, s>>>(a); break;
-        case 6: composite_kernel<6, kDebug><<<grid, kThreads, 0, s>>>(a); break;
-        case 7: composite_kernel<7, kDebug><<<grid, kThreads, 0, s>>>(a); break;
-        default: composite_kernel<8, kDebug><<<grid, kThreads, 0, s>>>(a); break;
+        case 0: launch_one<0, kDebug>(a, grid, s); break;
+        case 1: launch_one<1, kDebug>(a, grid, s); break;
+        case 2: launch_one<2, kDebug>(a, grid, s); break;
+        case 3: launch_one<3, kDebug>(a, grid, s); break;
+        case 4: launch_one<4, kDebug>(a, grid, s); break;
+        case 5: launch_one<5, kDebug>(a, grid, s); break;
+        case 6: launch_one<6, kDebug>(a, grid, s); break;
+        case 7: launch_one<7, kDebug>(a, grid, s); break;
+        default: launch_one<8, kDebug>(a, grid, s); break;
     }
 }
 

@@ -215,7 +215,10 @@ bool radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, i
 
 }  // namespace
 
-size_t scan_scratch_ints(int64_t n) { return static_cast<size_t>((n + kScanTile - 1) / kScanTile) + 8; }
+size_t scan_scratch_ints(int64_t n) {
+    const int64_t n_blocks = (n + kScanTile - 1) / kScanTile;
+    return static_cast<size_t>(n_blocks) + (n_blocks > 1 ? scan_scratch_ints(n_blocks) : 0) + 8;
+}
 
 void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int32_t* total, int32_t* scratch,
                     cudaStream_t stream) {
@@ -234,10 +237,10 @@ void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int32_t* total, 
         scan_loop_kernel<<<1, kScanThreads, 0, stream>>>(in, out, n, total);
         return;
     }
-    // n_blocks <= kScanTile is required (n <= 16.7M).
-    count_launch(3);
+    // reduce per block, scan the block sums (recursively), then scan each block with its offset
+    count_launch(2);
     scan_reduce_kernel<<<static_cast<unsigned>(n_blocks), kScanThreads, 0, stream>>>(in, n, scratch);
-    scan_single_kernel<<<1, kScanThreads, 0, stream>>>(scratch, scratch, n_blocks, nullptr, nullptr);
+    scan_exclusive(scratch, scratch, n_blocks, nullptr, scratch + n_blocks, stream);
     scan_single_kernel<<<static_cast<unsigned>(n_blocks), kScanThreads, 0, stream>>>(in, out, n, total,
                                                                                     scratch);
 }

@@ -13,7 +13,7 @@ constexpr int kScanThreads = 1024;
 constexpr int kScanTile = kScanItems * kScanThreads;
 constexpr int64_t kScanLoopMax = 16 * kScanTile;  // single-launch scan up to 64K values
 constexpr int kRadixThreads = 256;
-constexpr int kRadixTile = 4096;     // items per block per pass
+constexpr int kRadixTile = 1024;     // items per block per pass (>= 1 CTA per SM at ~150K keys)
 constexpr int kRadixBits = 8;
 constexpr int kRadixBuckets = 1 << kRadixBits;
 

@@ -151,6 +151,43 @@ __device__ __forceinline__ uint32_t map_positive32(long long x) {  // hash_grid.
     return x > 0 ? static_cast<uint32_t>(2 * x - 1) : static_cast<uint32_t>(-2 * x);
 }
 
+// One level of grid_lookup (hash_grid.cpp:32-82): lattice cell in fp64/int64 like the
+// reference, the 8 hashed corner rows (hash_cell, hash_grid.hpp:17-23) gathered, the
+// fractional position and the level fade (downweight, hash_grid.hpp:28-31).
+struct LevelFetch {
+    float2 v[8];
+    float fr0, fr1, fr2, dw;
+};
+
+__device__ __forceinline__ LevelFetch fetch_level(int l, double x0, double x1, double x2, const TcConst& cst,
+                                                  const float2* __restrict__ tab, uint32_t T, uint32_t mask, float ft,
+                                                  int no_downweight) {
+    LevelFetch f;
+    const double s = cst.level_scale[l];
+    const double p0 = s * x0, p1 = s * x1, p2 = s * x2;
+    const double fl0 = floor(p0), fl1 = floor(p1), fl2 = floor(p2);
+    const long long b0 = static_cast<long long>(fl0), b1 = static_cast<long long>(fl1),
+                    b2 = static_cast<long long>(fl2);
+    f.fr0 = static_cast<float>(p0 - fl0);
+    f.fr1 = static_cast<float>(p1 - fl1);
+    f.fr2 = static_cast<float>(p2 - fl2);
+    f.dw = 1.0f;
+    if (!no_downweight) {
+        const float r = ft * cst.inv_level_scale[l];
+        f.dw = 1.0f - __expf(-r * r * 0.15915494309189535f);
+    }
+    const uint32_t ax0 = map_positive32(b0), ax1 = map_positive32(b0 + 1);
+    const uint32_t by0 = map_positive32(b1) * 2654435761u, by1 = map_positive32(b1 + 1) * 2654435761u;
+    const uint32_t cz0 = map_positive32(b2) * 805459861u, cz1 = map_positive32(b2 + 1) * 805459861u;
+    const float2* slab = tab + static_cast<size_t>(l) * T;
+#pragma unroll
+    for (int ci = 0; ci < 8; ++ci) {
+        const uint32_t rowi = ((ci & 1) ? ax1 : ax0) ^ ((ci & 2) ? by1 : by0) ^ ((ci & 4) ? cz1 : cz0);
+        f.v[ci] = __ldg(slab + (rowi & mask));
+    }
+    return f;
+}
+
 __global__ void __launch_bounds__(kTcThreads, 2) texture_tc_kernel(const TextureArgs a, const TcConst cst,
                                                                    int bw, int bh, int tiles_x, int64_t n_tiles) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -228,41 +265,25 @@ __global__ void __launch_bounds__(kTcThreads, 2) texture_tc_kernel(const Texture
             const double x1 = a.cam.o[1] + t * dir[1];
             const double x2 = a.cam.o[2] + t * dir[2];
             const float ft = static_cast<float>(a.cam.fx / t);
+            // Two-stage software pipeline over the levels: the 8 corner gathers of level
+            // l+1 are in flight while level l is interpolated.
+            LevelFetch cur = fetch_level(half * 8, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
 #pragma unroll
             for (int li = 0; li < 8; ++li) {
-                const int l = half * 8 + li;
-                const double s = cst.level_scale[l];
-                const double p0 = s * x0, p1 = s * x1, p2 = s * x2;
-                const double fl0 = floor(p0), fl1 = floor(p1), fl2 = floor(p2);
-                const long long b0 = static_cast<long long>(fl0), b1 = static_cast<long long>(fl1),
-                                b2 = static_cast<long long>(fl2);
-                const float fr0 = static_cast<float>(p0 - fl0), fr1 = static_cast<float>(p1 - fl1),
-                            fr2 = static_cast<float>(p2 - fl2);
-                float dw = 1.0f;
-                if (!a.st.no_downweight) {  // downweight (hash_grid.hpp:28-31)
-                    const float r = ft * cst.inv_level_scale[l];
-                    dw = 1.0f - __expf(-r * r * 0.15915494309189535f);
-                }
-                const uint32_t ax0 = map_positive32(b0), ax1 = map_positive32(b0 + 1);
-                const uint32_t by0 = map_positive32(b1) * 2654435761u, by1 = map_positive32(b1 + 1) * 2654435761u;
-                const uint32_t cz0 = map_positive32(b2) * 805459861u, cz1 = map_positive32(b2 + 1) * 805459861u;
-                const size_t slab = static_cast<size_t>(l) * T;
-                float2 v[8];
-#pragma unroll
-                for (int ci = 0; ci < 8; ++ci) {
-                    const uint32_t rowi = ((ci & 1) ? ax1 : ax0) ^ ((ci & 2) ? by1 : by0) ^ ((ci & 4) ? cz1 : cz0);
-                    v[ci] = __ldg(tab + slab + (rowi & mask));
-                }
-                const float wx[2] = {1.0f - fr0, fr0}, wy[2] = {1.0f - fr1, fr1}, wz[2] = {1.0f - fr2, fr2};
+                LevelFetch nxt;
+                if (li < 7) nxt = fetch_level(half * 8 + li + 1, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
+                const float wx[2] = {1.0f - cur.fr0, cur.fr0}, wy[2] = {1.0f - cur.fr1, cur.fr1},
+                            wz[2] = {1.0f - cur.fr2, cur.fr2};
                 float g0 = 0.f, g1 = 0.f;
 #pragma unroll
                 for (int ci = 0; ci < 8; ++ci) {
                     const float w = wx[ci & 1] * wy[(ci >> 1) & 1] * wz[(ci >> 2) & 1];
-                    g0 += w * v[ci].x;
-                    g1 += w * v[ci].y;
+                    g0 += w * cur.v[ci].x;
+                    g1 += w * cur.v[ci].y;
                 }
-                feats[2 * li] = g0 * dw;
-                feats[2 * li + 1] = g1 * dw;
+                feats[2 * li] = g0 * cur.dw;
+                feats[2 * li + 1] = g1 * cur.dw;
+                if (li < 7) cur = nxt;
             }
         } else {
 #pragma unroll
