@@ -26,7 +26,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 64;                 // primitives staged per round
+constexpr int kChunk = 128;                // primitives staged per round (most tiles: one round)
 constexpr int kSub = 8;                    // primitives pooled per B1/B2 round (<= 256 entries per warp)
 constexpr int kPool = 32 * kSub;
 constexpr int kRecPairs = REC_FIELDS / 2;  // double2 per fp64 record (10)
@@ -129,8 +129,17 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(const CompositeA
 
     for (int pbase = 0; pbase < tile * tile; pbase += kThreads) {
         const int lp = pbase + threadIdx.x;
-        const int px = tx * tile + lp % tile, py = ty * tile + lp / tile;
+        // 16x16 tiles: each warp owns an 8x4 pixel block (tighter warp-level culling
+        // than 16x2 rows); other tile sizes: row-major.
+        const int lx = tile == 16 ? (warp & 1) * 8 + (lane & 7) : lp % tile;
+        const int ly = tile == 16 ? (warp >> 1) * 4 + (lane >> 3) : lp / tile;
+        const int px = tx * tile + lx, py = ty * tile + ly;
         const bool in_img = lp < tile * tile && px < W && py < H;
+        // the warp's pixel bounds for the screen-space cull
+        const int wx0 = __reduce_min_sync(0xffffffffu, in_img ? px : 0x7fffffff);
+        const int wx1 = __reduce_max_sync(0xffffffffu, in_img ? px : -1);
+        const int wy0 = __reduce_min_sync(0xffffffffu, in_img ? py : 0x7fffffff);
+        const int wy1 = __reduce_max_sync(0xffffffffu, in_img ? py : -1);
         double dir[3] = {0.0, 0.0, 1.0};
         if (in_img) pixel_dir(a.cam, px + 0.5, py + 0.5, dir);
         sm.dir[threadIdx.x][0] = dir[0];
@@ -178,10 +187,16 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(const CompositeA
                     const int sn = min(kSub, cn - sb);
                     // ---- A. prefilter this group of primitives
                     uint32_t mask = 0;
-                    if (active) {
 #pragma unroll 4
-                        for (int b = 0; b < sn; ++b)
-                            if (prefilter(&sm.f[sb + b][0], dfx, dfy, dfz, near_eps_f)) mask |= 1u << b;
+                    for (int b = 0; b < sn; ++b) {
+                        // screen-space cull: the pixel rect bounds every pixel the primitive can hit
+                        const float4 f3 = sm.f[sb + b][3];
+                        const int rx = __float_as_int(f3.z), ry = __float_as_int(f3.w);
+                        const int x0 = rx & 0xffff, x1 = rx >> 16, y0 = ry & 0xffff, y1 = ry >> 16;
+                        if (x1 < wx0 || x0 > wx1 || y1 < wy0 || y0 > wy1) continue;  // warp-uniform
+                        if (active && px >= x0 && px <= x1 && py >= y0 && py <= y1 &&
+                            prefilter(&sm.f[sb + b][0], dfx, dfy, dfz, near_eps_f))
+                            mask |= 1u << b;
                     }
                     // warp-wide pool: exclusive offsets of each lane's survivors
                     const int cnt = __popc(mask);

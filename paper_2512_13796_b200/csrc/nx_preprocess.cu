@@ -36,8 +36,7 @@ __device__ __forceinline__ int rect_tiles(int4 r) {
 // padded by 2 px, and convert to tiles. Every hit has t > near_eps, hence
 // camera-z > near_eps * cos(ray, axis) >= 2*zmin, and alpha >= 1/255 implies
 // |u| <= ru, |v| <= rv (kernel.hpp:70-76).
-__device__ int4 straddler_work_rect(const CamD& cam, D3 mu, D3 a1, D3 a2, double zmin, int tile,
-                                    int tiles_x, int tiles_y) {
+__device__ int4 straddler_pixel_rect(const CamD& cam, D3 mu, D3 a1, D3 a2, double zmin) {
     D3 poly[8];
     const D3 c0 = to_camera(cam, {mu.x + a1.x + a2.x, mu.y + a1.y + a2.y, mu.z + a1.z + a2.z});
     const D3 c1 = to_camera(cam, {mu.x + a1.x - a2.x, mu.y + a1.y - a2.y, mu.z + a1.z - a2.z});
@@ -73,8 +72,12 @@ __device__ int4 straddler_work_rect(const CamD& cam, D3 mu, D3 a1, D3 a2, double
     const int ix0 = static_cast<int>(floor(px0)), ix1 = static_cast<int>(ceil(px1));
     const int iy0 = static_cast<int>(floor(py0)), iy1 = static_cast<int>(ceil(py1));
     if (ix1 < 0 || iy1 < 0 || ix0 >= cam.W || iy0 >= cam.H || ix1 < ix0 || iy1 < iy0) return empty_rect();
-    return make_int4(clampi(ix0, 0, cam.W - 1) / tile, clampi(ix1, 0, cam.W - 1) / tile,
-                     clampi(iy0, 0, cam.H - 1) / tile, clampi(iy1, 0, cam.H - 1) / tile);
+    return make_int4(clampi(ix0, 0, cam.W - 1), clampi(ix1, 0, cam.W - 1), clampi(iy0, 0, cam.H - 1),
+                     clampi(iy1, 0, cam.H - 1));
+}
+
+__device__ __forceinline__ int4 pixel_to_tiles(int4 p, int tile) {
+    return p.y >= p.x ? make_int4(p.x / tile, p.y / tile, p.z / tile, p.w / tile) : empty_rect();
 }
 
 __global__ void __launch_bounds__(256) preprocess_kernel(const PreprocessArgs a) {
@@ -113,6 +116,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const PreprocessArgs a)
         const double ru = support_radius(op, gx), rv = support_radius(op, gy);
         int4 ref = empty_rect(), work = empty_rect();
         double depth = 0.0;
+        int4 prect = empty_rect();  // pixel rect containing every possible hit (work mode)
         if (ru <= 0.0 || rv <= 0.0) {
             cls = CLS_SUPPORT;
         } else {
@@ -153,24 +157,29 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const PreprocessArgs a)
                     cls = CLS_OFFSCREEN;
                 } else {
                     cls = CLS_RECT;
-                    const int tile = a.st.tile;
-                    ref = make_int4(clampi(ix0, 0, a.cam.W - 1) / tile, clampi(ix1, 0, a.cam.W - 1) / tile,
-                                    clampi(iy0, 0, a.cam.H - 1) / tile, clampi(iy1, 0, a.cam.H - 1) / tile);
+                    // The padded pixel rect contains every pixel centre inside the projected
+                    // support quad (all corners in front: the projection is that quad).
+                    prect = make_int4(clampi(ix0, 0, a.cam.W - 1), clampi(ix1, 0, a.cam.W - 1),
+                                      clampi(iy0, 0, a.cam.H - 1), clampi(iy1, 0, a.cam.H - 1));
+                    ref = pixel_to_tiles(prect, a.st.tile);
                     work = ref;
                 }
             } else {
                 cls = CLS_STRADDLER;
                 ref = make_int4(0, a.tiles_x - 1, 0, a.tiles_y - 1);
                 const double pu = ku * (1.0 + 1e-6), pv = kv * (1.0 + 1e-6);
-                work = straddler_work_rect(a.cam, mu, {pu * R[0], pu * R[3], pu * R[6]},
-                                           {pv * R[1], pv * R[4], pv * R[7]}, a.zmin_work, a.st.tile,
-                                           a.tiles_x, a.tiles_y);
+                prect = straddler_pixel_rect(a.cam, mu, {pu * R[0], pu * R[3], pu * R[6]},
+                                             {pv * R[1], pv * R[4], pv * R[7]}, a.zmin_work);
                 // Degenerate near-threshold opacity: keep the reference's all-tile list.
-                if (log(op / kAlphaMin) < 1e-3) work = ref;
+                if (log(op / kAlphaMin) < 1e-3) prect = make_int4(0, a.cam.W - 1, 0, a.cam.H - 1);
+                work = pixel_to_tiles(prect, a.st.tile);
                 kept = rect_tiles(work) > 0;
             }
         }
-        if (a.reference_lists) work = (cls == CLS_RECT || cls == CLS_STRADDLER) ? ref : empty_rect();
+        if (a.reference_lists) {
+            work = (cls == CLS_RECT || cls == CLS_STRADDLER) ? ref : empty_rect();
+            prect = make_int4(0, a.cam.W - 1, 0, a.cam.H - 1);  // reference walk: no culling
+        }
         a.cls[i] = cls;
         a.ref_rect[i] = ref;
         a.work_rect[i] = work;
@@ -218,7 +227,9 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const PreprocessArgs a)
             f[0] = make_float4(float(nx_), float(ny_), float(nz_), float(r[REC_NUM]));
             f[1] = make_float4(float(R[0]), float(R[3]), float(R[6]), float(b1));
             f[2] = make_float4(float(R[1]), float(R[4]), float(R[7]), float(b2));
-            f[3] = make_float4(__double2float_ru(r[REC_ULIM]), __double2float_ru(r[REC_VLIM]), 0.f, 0.f);
+            // + the pixel rect (x0 | x1 << 16, y0 | y1 << 16) for the composite's warp-level cull
+            f[3] = make_float4(__double2float_ru(r[REC_ULIM]), __double2float_ru(r[REC_VLIM]),
+                               __int_as_float(prect.x | (prect.y << 16)), __int_as_float(prect.z | (prect.w << 16)));
         }
     }
     // block-aggregated statistics
