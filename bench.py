@@ -135,13 +135,20 @@ def dist_setup(args):
     return world, rank, local, dist
 
 
-def max_over_ranks(dist, value: float, local: int) -> float:
+def max_over_ranks(dist, value: float, device) -> float:
+    """Timing is the max over ranks (device: 'cuda:<local>' under NCCL, 'cpu' under gloo)."""
     if dist is None:
         return value
     import torch
-    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def deal_views(n_steps: int, world: int, rank: int, n_views: int = N_VIEWS):
+    """Views of this rank, one per step: step s renders views s*world .. s*world+world-1
+    (mod the ring) across the ranks — disjoint within a step, no data exchange."""
+    return [(s * world + rank) % n_views for s in range(n_steps)]
 
 
 def barrier(dist):
@@ -272,7 +279,7 @@ def run_ours(args):
     fr = r.frame()
     stream = torch.cuda.ExternalStream(r.stream, device=torch.device("cuda", local))
     n_steps = args.warmup + args.steps
-    views = [(s * world + rank) % N_VIEWS for s in range(n_steps)]
+    views = deal_views(n_steps, world, rank)
     cams = {v: nx.ring_camera(v, N_VIEWS, args.width, args.height) for v in set(views)}
 
     # per-view work statistics (untimed pre-pass): P, work keys, Q
@@ -307,7 +314,7 @@ def run_ours(args):
     ms_local = ev0.elapsed_time(ev1)
     stage_ms, prof_frames = r.stage_times()
     r.set_profiling(False)
-    ms = max_over_ranks(dist, ms_local, local)
+    ms = max_over_ranks(dist, ms_local, f"cuda:{local}")
     frames_total = args.steps * world
     fps = frames_total / (ms / 1e3)
 
@@ -339,7 +346,7 @@ def run_ours(args):
     e1.record(stream)
     torch.cuda.synchronize()
     barrier(dist)
-    e2e_ms = max_over_ranks(dist, e0.elapsed_time(e1), local)
+    e2e_ms = max_over_ranks(dist, e0.elapsed_time(e1), f"cuda:{local}")
     e2e_fps = frames_total / (e2e_ms / 1e3)
 
     # ---- roofline of the dominant stage (algorithmic bytes per launch / mean launch time)

@@ -1,0 +1,86 @@
+"""GPU: the sm_100a path against the reference's golden fixtures (no reference
+needed at run time) and against the C oracle on the same inputs."""
+import glob
+import os
+import sys
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(HERE, "golden"))
+from make_golden import load  # noqa: E402
+
+import paper_2512_13796_b200 as nx  # noqa: E402
+from parity import compare_frames  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+CASES = sorted(os.path.splitext(os.path.basename(p))[0] for p in glob.glob(os.path.join(HERE, "golden", "*.npz")))
+INPUT_CASES = [c for c in CASES if c != "config1"]
+
+
+class _Ref:
+    def __init__(self, z):
+        for k in ("ids", "depths", "weights", "residual", "base", "texture", "final_img"):
+            setattr(self, k, z[k].astype(np.float64) if k != "ids" else z[k])
+
+
+def render(renderer, scene, cam):
+    ds = renderer.upload(scene)
+    fr = renderer.frame()
+    renderer.render(ds, cam, fr)
+    return fr.download(), ds
+
+
+@pytest.mark.parametrize("case", INPUT_CASES)
+def test_cuda_matches_reference_golden(renderer, case):
+    z, scene, cam, _ = load(case)
+    g, _ = render(renderer, scene, cam)
+    compare_frames(g, _Ref(z), check_psnr=case not in ("random_k0",))
+    if "naive" in z:
+        assert np.abs(g.final_img - z["naive"]).max() <= 1e-3
+
+
+def test_cuda_tile_lists_match_reference_golden(renderer):
+    z, scene, cam, _ = load("stump_2k")
+    ds = renderer.upload(scene)
+    off, ids, _, _ = renderer.tile_lists(ds, cam, reference_lists=True)
+    assert np.array_equal(off, z["tile_offsets"]) and np.array_equal(ids, z["tile_ids"])
+
+
+def test_cuda_config1_matches_reference_golden(renderer):
+    z, _, cam, _ = load("config1")
+    scene = nx.stump_like(10_000)
+    g, ds = render(renderer, scene, cam)
+    off, ids, _, _ = renderer.tile_lists(ds, cam, reference_lists=True)
+    assert np.array_equal(off, z["tile_offsets"]) and np.array_equal(ids, z["tile_ids"])
+    compare_frames(g, _Ref(z))
+
+
+def test_cuda_matches_c_oracle(renderer, oracle):
+    scene = nx.stump_like(3_000, log2_table=14, grid_init=1e-1, seed=7)
+    for view in (0, 100):
+        cam = nx.ring_camera(view, 256, 96, 80)
+        g, _ = render(renderer, scene, cam)
+        compare_frames(g, oracle.render(scene, cam))
+
+
+def test_texture_paths_agree(renderer):
+    """Tensor-core MLP (tcgen05, bf16 3-term split) vs the fp32 SIMT MLP on the
+    same frame: both within 1e-4 of each other (the SIMT path is forced in a
+    subprocess via NX_TEXTURE_PATH=simt)."""
+    import subprocess
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_2512_13796_b200 as nx; "
+            "s = nx.stump_like(20000, log2_table=16, grid_init=1e-1); c = nx.ring_camera(5, 256, 128, 96); "
+            "r = nx.Renderer(0); d = r.upload(s); f = r.frame(); r.render(d, c, f); "
+            "np.save(sys.argv[1], f.download().texture)") % os.path.dirname(HERE)
+    out = {}
+    for path in ("tc", "simt"):
+        fn = f"/tmp/nx_tex_{path}_{os.getpid()}.npy"
+        env = dict(os.environ)
+        if path == "simt":
+            env["NX_TEXTURE_PATH"] = "simt"
+        subprocess.run([sys.executable, "-c", code, fn], check=True, env=env, timeout=600)
+        out[path] = np.load(fn)
+    assert np.abs(out["tc"] - out["simt"]).max() < 1e-4
