@@ -41,6 +41,45 @@ $(PKG)/libnexel_b200.so: $(CU_OBJS) $(CPP_OBJS)
 oracle:
 	$(MAKE) -C oracle REF=$(REF)
 
+# ---- C++ drop-in: the reference's core library with the forward half of
+# renderer.cpp replaced by host/renderer_b200.cpp (sm_100a via the C-ABI).
+# Reference sources are compiled in place from $(REF) (never copied); the
+# reference's render_backward (next row, CPU) is kept by renaming the forward
+# symbols of its renderer.cpp. Then the reference's own test_oracle.cpp is built
+# unmodified against it (tests/cxx/doctest.h stands in for doctest).
+DROPIN := build/dropin
+DROPIN_TUS := camera primitive hash_grid mlp texture_field threading oracle
+DROPIN_CXX := -std=gnu++20 -O3 -DNDEBUG -fPIC -pthread -march=x86-64-v3 -I$(REF)/core/include
+RENAME_FWD := -Dcollection_pass=nexel_ref_collection_pass -Dtexturing_pass=nexel_ref_texturing_pass \
+              -Drender=nexel_ref_render -Dvalidate_settings=nexel_ref_validate_settings
+
+ifneq ($(wildcard $(REF)/core/src/renderer.cpp),)
+dropin: $(DROPIN)/libnexel_dropin.so $(DROPIN)/test_oracle_dropin
+else
+dropin:
+	@echo "reference sources not present; using the prebuilt $(DROPIN) if any"
+endif
+
+$(DROPIN)/ref_%.o: $(REF)/core/src/%.cpp
+	@mkdir -p $(DROPIN)
+	$(CXX) $(DROPIN_CXX) $(if $(filter mlp,$*),-fassociative-math -fno-signed-zeros -fno-trapping-math -fno-math-errno) -c -o $@ $<
+
+$(DROPIN)/ref_renderer_backward.o: $(REF)/core/src/renderer.cpp
+	@mkdir -p $(DROPIN)
+	$(CXX) $(DROPIN_CXX) $(RENAME_FWD) -c -o $@ $<
+
+$(DROPIN)/renderer_b200.o: $(PKG)/host/renderer_b200.cpp include/nexel_b200.h
+	@mkdir -p $(DROPIN)
+	$(CXX) $(DROPIN_CXX) -c -o $@ $<
+
+$(DROPIN)/libnexel_dropin.so: $(DROPIN)/renderer_b200.o $(DROPIN)/ref_renderer_backward.o \
+                              $(addprefix $(DROPIN)/ref_,$(addsuffix .o,$(DROPIN_TUS))) $(PKG)/libnexel_b200.so
+	$(CXX) -shared -pthread -o $@ $(filter %.o,$^) -L$(PKG) -lnexel_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+
+$(DROPIN)/test_oracle_dropin: $(REF)/tests/test_oracle.cpp tests/cxx/doctest.h $(DROPIN)/libnexel_dropin.so
+	$(CXX) $(DROPIN_CXX) -Itests/cxx -I$(REF)/tests -o $@ $< -L$(DROPIN) -lnexel_dropin -Wl,-rpath,'$$ORIGIN'
+
 clean:
 	rm -rf build $(PKG)/*.so
 	$(MAKE) -C oracle clean

@@ -34,7 +34,7 @@ N_VIEWS = 256
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--nexels", type=int, default=400_000)
@@ -72,6 +72,16 @@ def stage_bytes(stage, n, P, Pw, H, W, K, Q):
     return 8 * P
 
 
+def traffic_of(stage: str):
+    """DRAM bytes per launch of the stage's kernel from the committed ncu capture
+    (profiles/traffic.json), or None if that kernel was not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(stage, {}).get("dram_bytes")
+    except (OSError, ValueError):
+        return None
+
+
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -87,7 +97,7 @@ class ClockSampler:
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "50", "-i", str(self.device)], stdout=self.fh,
+                                          "-lms", "20", "-i", str(self.device)], stdout=self.fh,
                                          stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
@@ -373,7 +383,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload(args),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
+                         "frac": achieved / hbm_peak, "traffic": traffic_of(dom), "peak_source": peak_src,
                          "bytes_per_launch": dom_bytes, "launch_ms": stage_ms[dom]},
             "frame_roofline": {"bytes_per_frame": fbytes, "achieved": frame_gbs, "peak": hbm_peak, "unit": "GB/s",
                                "frac": frame_gbs / hbm_peak, "formula": "240N + 8P + (28+24K)HW + 1024Q + 36864"},

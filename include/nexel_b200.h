@@ -176,6 +176,10 @@ void nx_frame_destroy(nx_frame* frame);
 int nx_frame_view_get(const nx_frame* frame, nx_frame_view* out);
 /* Async device->host copy on `stream`; pinned destinations overlap with compute. */
 int nx_frame_download(nx_ctx* ctx, const nx_frame* frame, const nx_host_frame* dst, void* stream);
+/* Host->device: (re)shapes the frame and copies the given buffers (NULL = skip), e.g.
+ * to run texturing_pass on FrameBuffers that a caller holds on the host. */
+int nx_frame_upload(nx_ctx* ctx, nx_frame* frame, int width, int height, int top_k, const nx_host_frame* src,
+                    void* stream);
 int nx_frame_stats_get(nx_ctx* ctx, const nx_frame* frame, nx_frame_stats* out); /* synchronises */
 
 /* ---- the render path --------------------------------------------------- */

@@ -159,6 +159,7 @@ SIGNATURES = [
     ("nx_frame_destroy", None, [P]),
     ("nx_frame_view_get", C.c_int, [P, C.POINTER(nx_frame_view)]),
     ("nx_frame_download", C.c_int, [P, P, C.POINTER(nx_host_frame), P]),
+    ("nx_frame_upload", C.c_int, [P, P, C.c_int, C.c_int, C.c_int, C.POINTER(nx_host_frame), P]),
     ("nx_frame_stats_get", C.c_int, [P, P, C.POINTER(nx_frame_stats)]),
     ("nx_collection_pass", C.c_int, [P, P, C.POINTER(nx_camera), P, P]),
     ("nx_texturing_pass", C.c_int, [P, P, C.POINTER(nx_camera), P, P]),

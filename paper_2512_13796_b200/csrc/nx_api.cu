@@ -688,6 +688,29 @@ int nx_frame_download(nx_ctx* c, const nx_frame* f, const nx_host_frame* dst, vo
     return NX_OK;
 }
 
+int nx_frame_upload(nx_ctx* c, nx_frame* f, int width, int height, int top_k, const nx_host_frame* src,
+                    void* stream) {
+    if (!c || !f || !src || width < 0 || height < 0 || top_k < 0 || top_k > NX_MAX_TOP_K)
+        return set_err(c, NX_INVALID_ARGUMENT, "bad frame upload");
+    cudaSetDevice(c->device);
+    int st = frame_shape(c, f, width, height, top_k, 16);  // tiles are re-derived by collection_pass
+    if (st) return st;
+    cudaStream_t s = pick_stream(c, stream);
+    const size_t npix = static_cast<size_t>(width) * height, ns = npix * top_k;
+    auto cp = [&](DevBuf& b, const void* h, size_t bytes) -> cudaError_t {
+        if (!h || !bytes) return cudaSuccess;
+        return cudaMemcpyAsync(b.p, h, bytes, cudaMemcpyHostToDevice, s);
+    };
+    NX_CUDA(c, cp(f->base, src->base, npix * 3 * sizeof(float)));
+    NX_CUDA(c, cp(f->ids, src->ids, ns * sizeof(int32_t)));
+    NX_CUDA(c, cp(f->depths, src->depths, ns * sizeof(double)));
+    NX_CUDA(c, cp(f->weights, src->weights, ns * sizeof(double)));
+    NX_CUDA(c, cp(f->texture, src->texture, ns * 3 * sizeof(float)));
+    NX_CUDA(c, cp(f->final_img, src->final_img, npix * 3 * sizeof(float)));
+    NX_CUDA(c, cp(f->residual, src->residual, npix * sizeof(float)));
+    return NX_OK;
+}
+
 int nx_frame_stats_get(nx_ctx* c, const nx_frame* f, nx_frame_stats* out) {
     if (!c || !f || !out) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
     FrameStatsD h;

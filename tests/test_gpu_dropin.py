@@ -1,0 +1,22 @@
+"""GPU: the reference's OWN render tests, compiled unmodified against the C++
+drop-in (paper_2512_13796_b200/host/renderer_b200.cpp over the C-ABI) in place of
+renderer.cpp's forward half: proj/tests/test_oracle.cpp (tiled renderer vs the
+brute-force naive_render <= 1e-6, termination on thin scenes, empty scene,
+k = 0 march). Built by `make dropin` (needs /root/reference at build time)."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "build", "dropin", "test_oracle_dropin")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.skipif(not os.path.exists(BIN), reason="drop-in test binary not built (make dropin)")
+def test_reference_test_oracle_suite_passes_on_the_dropin():
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    print(r.stdout[-2000:], r.stderr[-2000:])
+    assert r.returncode == 0
+    assert "6 test cases, 0 failed" in r.stdout
