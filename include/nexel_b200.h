@@ -198,8 +198,9 @@ int nx_render(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam, nx_frame
 
 /* ---- parity / debug (not on the timed path) ---------------------------- */
 /* Tile lists for `cam`: reference_lists=1 materialises the reference's lists
- * (Binning::tile_lists, renderer.cpp:102-110, straddlers in every tile);
- * reference_lists=0 returns the work lists the composite kernel walks.
+ * (Binning::tile_lists, renderer.cpp:102-110, straddlers in every tile) on
+ * settings.tile tiles; reference_lists=0 returns the work lists the composite
+ * kernel walks (8x8-pixel tiles; *tiles_x/*tiles_y report the list geometry).
  * offsets: n_tiles+1 host ints; ids: `capacity` host ints; *total = keys. */
 int nx_debug_tile_lists(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam,
                         int reference_lists, int64_t* offsets, int32_t* ids,

@@ -97,7 +97,8 @@ struct nx_scene {
 
 struct nx_frame {
     nx_ctx* ctx = nullptr;
-    int W = 0, H = 0, K = 0, tiles_x = 0, tiles_y = 0;
+    int W = 0, H = 0, K = 0, tiles_x = 0, tiles_y = 0;  // reference tiles (settings.tile)
+    int list_tile = kWorkTile, ltiles_x = 0, ltiles_y = 0;  // tiles of the last built lists
     DevBuf base, ids, depths, weights, texture, final_img, residual;
     DevBuf tile_offsets;  // n_tiles + 1 (the work lists' ranges of the last collection pass)
     DevBuf list_ids;
@@ -212,8 +213,8 @@ FrameDev frame_dev(const nx_frame* f) {
     d.W = f->W;
     d.H = f->H;
     d.K = f->K;
-    d.tiles_x = f->tiles_x;
-    d.tiles_y = f->tiles_y;
+    d.tiles_x = f->ltiles_x;  // the composite walks the lists of the last build (work tiles)
+    d.tiles_y = f->ltiles_y;
     d.base = f->base.as<float>();
     d.ids = f->ids.as<int32_t>();
     d.depths = f->depths.as<double>();
@@ -271,7 +272,12 @@ int check_inputs(nx_ctx* c, const nx_scene* scene, const nx_camera* cam) {
 int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame* f, int reference_lists,
                 cudaStream_t s, int64_t* total_keys) {
     const int64_t n = scene->n;
-    const int64_t n_tiles = static_cast<int64_t>(f->tiles_x) * f->tiles_y;
+    // list geometry: reference lists per settings.tile, work lists per kWorkTile
+    const int lt = reference_lists ? scene->st.tile : kWorkTile;
+    f->list_tile = lt;
+    f->ltiles_x = (cam.width + lt - 1) / lt;
+    f->ltiles_y = (cam.height + lt - 1) / lt;
+    const int64_t n_tiles = static_cast<int64_t>(f->ltiles_x) * f->ltiles_y;
     const CamD cd = make_cam(cam);
     const int64_t nn = std::max<int64_t>(n, 1);
     NX_CUDA(c, c->rec.ensure(nn * REC_FIELDS * sizeof(double)));
@@ -306,6 +312,7 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
     pa.cam = cd;
     pa.tiles_x = f->tiles_x;
     pa.tiles_y = f->tiles_y;
+    pa.work_tile = kWorkTile;
     pa.zmin_work = 0.5 * scene->st.near_eps * min_axis_cosine(cam);
     pa.rec = c->rec.as<double>();
     pa.recf = c->recf.as<float4>();
@@ -356,7 +363,7 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
         sc = d_total + 64;
     }
     NX_CUDA(c, cudaMemsetAsync(c->tile_counts.as<int32_t>(), 0, (n_tiles + 1) * sizeof(int32_t), s));
-    launch_emit(sorted_ids, c->offsets.as<int32_t>(), n_sorted, n_keys, c->work_rect.as<int4>(), f->tiles_x,
+    launch_emit(sorted_ids, c->offsets.as<int32_t>(), n_sorted, n_keys, c->work_rect.as<int4>(), f->ltiles_x,
                 c->tkeys_a.as<uint32_t>(), c->tvals_a.as<uint32_t>(), c->tile_counts.as<int32_t>(), s);
 
     // K4: stable sort by tile.
@@ -762,7 +769,7 @@ int nx_debug_tile_lists(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, 
     cudaStream_t s = c->stream;
     if (!st) st = build_lists(c, scene, *cam, f, reference_lists, s, &n_keys);
     if (!st) {
-        const int64_t n_tiles = static_cast<int64_t>(f->tiles_x) * f->tiles_y;
+        const int64_t n_tiles = static_cast<int64_t>(f->ltiles_x) * f->ltiles_y;
         std::vector<int32_t> off(static_cast<size_t>(n_tiles + 1));
         cudaError_t e = cudaMemcpyAsync(off.data(), f->tile_offsets.p, off.size() * sizeof(int32_t),
                                         cudaMemcpyDeviceToHost, s);
@@ -774,8 +781,8 @@ int nx_debug_tile_lists(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, 
         if (!st && offsets)
             for (int64_t t = 0; t <= n_tiles; ++t) offsets[t] = off[t];
         if (total) *total = n_keys;
-        if (tiles_x) *tiles_x = f->tiles_x;
-        if (tiles_y) *tiles_y = f->tiles_y;
+        if (tiles_x) *tiles_x = f->ltiles_x;
+        if (tiles_y) *tiles_y = f->ltiles_y;
     }
     nx_frame_destroy(f);
     return st;

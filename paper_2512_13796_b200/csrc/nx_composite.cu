@@ -1,36 +1,38 @@
 // K6 composite: per-tile front-to-back alpha compositing with early termination
 // and a top-K buffer (collection_pass, renderer.cpp:115-171).
 //
-// One CTA per screen tile, one thread per pixel. The tile's work list (ids in
-// (depth, id) order) is walked in chunks of kChunk primitives staged into shared
-// memory. Per chunk and per group of kSub primitives, each warp
-//   A. prefilters (fp32, conservative) every (pixel, primitive)
-//      pair: a pair is dropped only if it provably fails the reference's
-//      t > near_eps or |u| <= ru, |v| <= rv conditions (hence alpha < 1/255);
-//   B1. pools the survivors of its 32 pixels and evaluates them with all 32 lanes
+// One 64-thread CTA per 8x8-pixel work tile (two warps of 8x4 pixels), one thread
+// per pixel: many small CTAs per SM keep the load balanced across tiles whose hit
+// counts differ a lot. The tile's work list (ids in (depth, id) order) is walked in
+// chunks whose fp32 prefilter records are staged in shared memory (broadcast
+// reads); the fp64 records are read through L1 by the lanes that need them. Per
+// group of kSub primitives each warp
+//   A. culls in screen space (the primitive's padded pixel rect vs the warp's
+//      pixels) and prefilters in fp32 (conservative): a pair is
+//      dropped only if it provably fails the reference's t > near_eps or
+//      |u| <= ru, |v| <= rv conditions (hence alpha < 1/255);
+//   B1. pools the survivors of its 32 pixels and evaluates them with all lanes
 //      busy on the exact fp64 path — the reference's intersect() formulas
 //      (intersect.hpp:23-42) and eval_kernel (kernel.hpp:16-30) — plus the
 //      primitive's SH colour (fp32, colour only);
 //   B2. composites, per pixel and in list order, its own survivors: alpha clamp,
 //      weight, top-K insert, transmittance update and termination
 //      (renderer.cpp:144-153), all fp64.
-// Every decision is the reference's, taken in fp64 with its formulas; the
-// prefilter only skips provable misses, so contributor lists are bit-exact. The
-// pooling keeps the expensive transcendental path at full warp width, whereas a
-// per-pixel walk would run it at the width of the pixels that happen to hit.
+// Every decision is the reference's, taken in fp64 with its formulas; culling and
+// prefilter only skip provable misses, so contributor lists are bit-exact.
 #include "nx_internal.cuh"
 
 namespace nx {
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = kWorkTile * kWorkTile;  // 64: one thread per pixel of the work tile
 constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 128;                // primitives staged per round (most tiles: one round)
-constexpr int kSub = 8;                    // primitives pooled per B1/B2 round (<= 256 entries per warp)
+constexpr int kChunk = 128;                      // primitives staged per round
+constexpr int kSub = 8;                          // primitives pooled per B1/B2 round (<= 256 entries per warp)
 constexpr int kPool = 32 * kSub;
-constexpr int kRecPairs = REC_FIELDS / 2;  // double2 per fp64 record (10)
-constexpr int kRecStride = kRecPairs + 1;  // padded to 11 double2: different records hit different bank groups
+constexpr int kRecPairs = REC_FIELDS / 2;        // double2 per fp64 record (10)
+static_assert(kWorkTile == 8, "warp blocks are 8x4 pixels");
 
 struct PoolEntry {  // one evaluated (pixel, primitive) pair
     double alpha;   // raw kernel alpha, < 0 for a miss
@@ -41,7 +43,6 @@ struct PoolEntry {  // one evaluated (pixel, primitive) pair
 
 struct SmemLayout {
     float4 f[kChunk][4];
-    double2 d[kChunk][kRecStride];
     int32_t id[kChunk];
     double dir[kThreads][3];
     uint16_t q[kWarps][kPool];
@@ -112,12 +113,11 @@ __device__ __forceinline__ bool prefilter(const float4* f, float dfx, float dfy,
 }
 
 template <int K, bool kDebug>
-__global__ void __launch_bounds__(kThreads, 2) composite_kernel(const CompositeArgs a) {
+__global__ void __launch_bounds__(kThreads, 8) composite_kernel(const CompositeArgs a) {
     constexpr int KK = K > 0 ? K : 1;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     SmemLayout& sm = *reinterpret_cast<SmemLayout*>(smem_raw);
 
-    const int tile = a.st.tile;
     const int t = blockIdx.x;
     const int tx = t % a.fb.tiles_x, ty = t / a.fb.tiles_x;
     const int list_begin = a.tile_offsets[t], list_end = a.tile_offsets[t + 1];
@@ -127,244 +127,235 @@ __global__ void __launch_bounds__(kThreads, 2) composite_kernel(const CompositeA
     const float near_eps_f = static_cast<float>(near_eps);
     const double o0 = a.cam.o[0], o1 = a.cam.o[1], o2 = a.cam.o[2];
 
-    for (int pbase = 0; pbase < tile * tile; pbase += kThreads) {
-        const int lp = pbase + threadIdx.x;
-        // 16x16 tiles: each warp owns an 8x4 pixel block (tighter warp-level culling
-        // than 16x2 rows); other tile sizes: row-major.
-        const int lx = tile == 16 ? (warp & 1) * 8 + (lane & 7) : lp % tile;
-        const int ly = tile == 16 ? (warp >> 1) * 4 + (lane >> 3) : lp / tile;
-        const int px = tx * tile + lx, py = ty * tile + ly;
-        const bool in_img = lp < tile * tile && px < W && py < H;
-        // the warp's pixel bounds for the screen-space cull
-        const int wx0 = __reduce_min_sync(0xffffffffu, in_img ? px : 0x7fffffff);
-        const int wx1 = __reduce_max_sync(0xffffffffu, in_img ? px : -1);
-        const int wy0 = __reduce_min_sync(0xffffffffu, in_img ? py : 0x7fffffff);
-        const int wy1 = __reduce_max_sync(0xffffffffu, in_img ? py : -1);
-        double dir[3] = {0.0, 0.0, 1.0};
-        if (in_img) pixel_dir(a.cam, px + 0.5, py + 0.5, dir);
-        sm.dir[threadIdx.x][0] = dir[0];
-        sm.dir[threadIdx.x][1] = dir[1];
-        sm.dir[threadIdx.x][2] = dir[2];
-        const float dfx = static_cast<float>(dir[0]), dfy = static_cast<float>(dir[1]),
-                    dfz = static_cast<float>(dir[2]);
+    // warp w owns pixel rows 4w..4w+3 of the 8x8 tile
+    const int px = tx * kWorkTile + (lane & 7), py = ty * kWorkTile + warp * 4 + (lane >> 3);
+    const bool in_img = px < W && py < H;
+    const int wx0 = __reduce_min_sync(0xffffffffu, in_img ? px : 0x7fffffff);
+    const int wx1 = __reduce_max_sync(0xffffffffu, in_img ? px : -1);
+    const int wy0 = __reduce_min_sync(0xffffffffu, in_img ? py : 0x7fffffff);
+    const int wy1 = __reduce_max_sync(0xffffffffu, in_img ? py : -1);
+    double dir[3] = {0.0, 0.0, 1.0};
+    if (in_img) pixel_dir(a.cam, px + 0.5, py + 0.5, dir);
+    sm.dir[threadIdx.x][0] = dir[0];
+    sm.dir[threadIdx.x][1] = dir[1];
+    sm.dir[threadIdx.x][2] = dir[2];
+    const float dfx = static_cast<float>(dir[0]), dfy = static_cast<float>(dir[1]), dfz = static_cast<float>(dir[2]);
 
-        double T = 1.0;
-        double acc[3] = {0.0, 0.0, 0.0};
-        int32_t k_id[KK];
-        double k_w[KK], k_t[KK];
-        uint32_t k_seq[KK];
+    double T = 1.0;
+    double acc[3] = {0.0, 0.0, 0.0};
+    int32_t k_id[KK];
+    double k_w[KK], k_t[KK];
+    uint32_t k_seq[KK];
 #pragma unroll
-        for (int s = 0; s < KK; ++s) {
-            k_id[s] = -1;
-            k_w[s] = 0.0;
-            k_t[s] = 0.0;
-            k_seq[s] = 0;
+    for (int s = 0; s < KK; ++s) {
+        k_id[s] = -1;
+        k_w[s] = 0.0;
+        k_t[s] = 0.0;
+        k_seq[s] = 0;
+    }
+    int k_size = 0;
+    uint32_t counter = 0;
+    bool active = in_img;
+    int dbg_n = 0;
+    const bool dbg_row = kDebug && in_img && py >= a.dbg_y0 && py < a.dbg_y1;
+    const int64_t dbg_q = kDebug ? (static_cast<int64_t>(py - a.dbg_y0) * W + px) : 0;
+    const double2* rec2 = reinterpret_cast<const double2*>(a.rec);
+
+    for (int cb = list_begin; cb < list_end; cb += kChunk) {
+        const int cn = min(kChunk, list_end - cb);
+        __syncthreads();
+        for (int e = threadIdx.x; e < cn * 4; e += kThreads) {
+            const int j = e >> 2, q = e & 3;
+            const int32_t id = __ldg(a.list_ids + cb + j);
+            sm.f[j][q] = __ldg(a.recf + static_cast<int64_t>(id) * 4 + q);
+            if (q == 0) sm.id[j] = id;
         }
-        int k_size = 0;
-        uint32_t counter = 0;
-        bool active = in_img;
-        int dbg_n = 0;
-        const bool dbg_row = kDebug && in_img && py >= a.dbg_y0 && py < a.dbg_y1;
-        const int64_t dbg_q = kDebug ? (static_cast<int64_t>(py - a.dbg_y0) * W + px) : 0;
-
-        for (int cb = list_begin; cb < list_end; cb += kChunk) {
-            const int cn = min(kChunk, list_end - cb);
-            __syncthreads();
-            for (int e = threadIdx.x; e < cn * 4; e += kThreads) {
-                const int j = e >> 2, q = e & 3;
-                const int32_t id = __ldg(a.list_ids + cb + j);
-                sm.f[j][q] = __ldg(a.recf + static_cast<int64_t>(id) * 4 + q);
-                if (q == 0) sm.id[j] = id;
-            }
-            for (int e = threadIdx.x; e < cn * kRecPairs; e += kThreads) {
-                const int j = e / kRecPairs, q = e - j * kRecPairs;
-                const int32_t id = __ldg(a.list_ids + cb + j);
-                sm.d[j][q] = __ldg(reinterpret_cast<const double2*>(a.rec) + static_cast<int64_t>(id) * kRecPairs + q);
-            }
-            __syncthreads();
-            if (__any_sync(0xffffffffu, active)) {
-                for (int sb = 0; sb < cn; sb += kSub) {
-                    const int sn = min(kSub, cn - sb);
-                    // ---- A. prefilter this group of primitives
-                    uint32_t mask = 0;
+        __syncthreads();
+        if (__any_sync(0xffffffffu, active)) {
+            for (int sb = 0; sb < cn; sb += kSub) {
+                const int sn = min(kSub, cn - sb);
+                // ---- A. screen-space cull + fp32 prefilter of this group
+                uint32_t mask = 0;
 #pragma unroll 4
-                    for (int b = 0; b < sn; ++b) {
-                        // screen-space cull: the pixel rect bounds every pixel the primitive can hit
-                        const float4 f3 = sm.f[sb + b][3];
-                        const int rx = __float_as_int(f3.z), ry = __float_as_int(f3.w);
-                        const int x0 = rx & 0xffff, x1 = rx >> 16, y0 = ry & 0xffff, y1 = ry >> 16;
-                        if (x1 < wx0 || x0 > wx1 || y1 < wy0 || y0 > wy1) continue;  // warp-uniform
-                        if (active && px >= x0 && px <= x1 && py >= y0 && py <= y1 &&
-                            prefilter(&sm.f[sb + b][0], dfx, dfy, dfz, near_eps_f))
-                            mask |= 1u << b;
-                    }
-                    // warp-wide pool: exclusive offsets of each lane's survivors
-                    const int cnt = __popc(mask);
-                    int incl = cnt;
+                for (int b = 0; b < sn; ++b) {
+                    const float4 f3 = sm.f[sb + b][3];
+                    const int rx = __float_as_int(f3.z), ry = __float_as_int(f3.w);
+                    const int x0 = rx & 0xffff, x1 = rx >> 16, y0 = ry & 0xffff, y1 = ry >> 16;
+                    if (x1 < wx0 || x0 > wx1 || y1 < wy0 || y0 > wy1) continue;  // warp-uniform
+                    if (active && px >= x0 && px <= x1 && py >= y0 && py <= y1 &&
+                        prefilter(&sm.f[sb + b][0], dfx, dfy, dfz, near_eps_f))
+                        mask |= 1u << b;
+                }
+                // warp-wide pool: exclusive offsets of each lane's survivors
+                const int cnt = __popc(mask);
+                int incl = cnt;
 #pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= o) incl += y;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const int off = incl - cnt;
+                const int total = __shfl_sync(0xffffffffu, incl, 31);
+                if (total == 0) continue;
+                {
+                    uint32_t m = mask;
+                    int k = off;
+                    while (m) {
+                        const int b = __ffs(m) - 1;
+                        m &= m - 1;
+                        sm.q[warp][k++] = static_cast<uint16_t>((lane << 8) | (sb + b));
                     }
-                    const int off = incl - cnt;
-                    const int total = __shfl_sync(0xffffffffu, incl, 31);
-                    if (total == 0) continue;
-                    {
-                        uint32_t m = mask;
-                        int k = off;
-                        while (m) {
-                            const int b = __ffs(m) - 1;
-                            m &= m - 1;
-                            sm.q[warp][k++] = static_cast<uint16_t>((lane << 8) | (sb + b));
-                        }
+                }
+                __syncwarp();
+                // ---- B1. exact fp64 evaluation of the pooled pairs, all lanes busy
+                for (int e = lane; e < total; e += 32) {
+                    const int ent = sm.q[warp][e];
+                    const int owner = ent >> 8, j = ent & 0xff;
+                    const double* dd = sm.dir[warp * 32 + owner];
+                    const double d0 = dd[0], d1 = dd[1], d2 = dd[2];
+                    const int32_t id = sm.id[j];
+                    double r[REC_FIELDS];
+#pragma unroll
+                    for (int q = 0; q < kRecPairs; ++q) {
+                        const double2 v = __ldg(rec2 + static_cast<int64_t>(id) * kRecPairs + q);
+                        r[2 * q] = v.x;
+                        r[2 * q + 1] = v.y;
                     }
-                    __syncwarp();
-                    // ---- B1. exact fp64 evaluation of the pooled pairs, all lanes busy
-                    for (int e = lane; e < total; e += 32) {
-                        const int ent = sm.q[warp][e];
-                        const int owner = ent >> 8, j = ent & 0xff;
-                        const double* dd = sm.dir[warp * 32 + owner];
-                        const double d0 = dd[0], d1 = dd[1], d2 = dd[2];
-                        const double* r = reinterpret_cast<const double*>(&sm.d[j][0]);
-                        PoolEntry res;
-                        res.alpha = -1.0;
-                        res.t = 0.0;
-                        // intersect (intersect.hpp:23-42)
-                        const double denom = d0 * r[REC_NX] + d1 * r[REC_NY] + d2 * r[REC_NZ];
-                        if (fabs(denom) >= kMinNormalDot) {
-                            const double tt = r[REC_NUM] / denom;
-                            if (tt > near_eps) {
-                                const double e0 = (o0 + tt * d0) - r[REC_MUX];
-                                const double e1 = (o1 + tt * d1) - r[REC_MUY];
-                                const double e2 = (o2 + tt * d2) - r[REC_MUZ];
-                                const double du = e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z];
-                                const double dv = e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z];
-                                if (fabs(du) <= r[REC_ULIM] && fabs(dv) <= r[REC_VLIM]) {
-                                    const double u = du / r[REC_SX];
-                                    const double v = dv / r[REC_SY];
-                                    const double al = eval_kernel(u, v, r[REC_OP], r[REC_GX], r[REC_GY]);
-                                    if (al >= kAlphaMin) {
-                                        res.alpha = al;
-                                        res.t = tt;
-                                        eval_sh_f32(a.sh + static_cast<int64_t>(sm.id[j]) * NX_SH_VALUES,
-                                                    static_cast<float>(d0), static_cast<float>(d1),
-                                                    static_cast<float>(d2), a.sh_degree, res.rgb);
-                                    }
+                    PoolEntry res;
+                    res.alpha = -1.0;
+                    res.t = 0.0;
+                    // intersect (intersect.hpp:23-42)
+                    const double denom = d0 * r[REC_NX] + d1 * r[REC_NY] + d2 * r[REC_NZ];
+                    if (fabs(denom) >= kMinNormalDot) {
+                        const double tt = r[REC_NUM] / denom;
+                        if (tt > near_eps) {
+                            const double e0 = (o0 + tt * d0) - r[REC_MUX];
+                            const double e1 = (o1 + tt * d1) - r[REC_MUY];
+                            const double e2 = (o2 + tt * d2) - r[REC_MUZ];
+                            const double du = e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z];
+                            const double dv = e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z];
+                            if (fabs(du) <= r[REC_ULIM] && fabs(dv) <= r[REC_VLIM]) {
+                                const double u = du / r[REC_SX];
+                                const double v = dv / r[REC_SY];
+                                const double al = eval_kernel(u, v, r[REC_OP], r[REC_GX], r[REC_GY]);
+                                if (al >= kAlphaMin) {
+                                    res.alpha = al;
+                                    res.t = tt;
+                                    eval_sh_f32(a.sh + static_cast<int64_t>(id) * NX_SH_VALUES, static_cast<float>(d0),
+                                                static_cast<float>(d1), static_cast<float>(d2), a.sh_degree, res.rgb);
                                 }
                             }
                         }
-                        sm.res[warp][e] = res;
                     }
-                    __syncwarp();
-                    // ---- B2. per-pixel compositing of this lane's hits, in list order (renderer.cpp:144-153)
-                    for (int k = off; k < off + cnt && active; ++k) {
-                        const PoolEntry& res = sm.res[warp][k];
-                        if (res.alpha < 0.0) continue;
-                        const int32_t id = sm.id[sm.q[warp][k] & 0xff];
-                        const double alpha = alpha_max < res.alpha ? alpha_max : res.alpha;
-                        const double wgt = alpha * T;
-                        acc[0] += wgt * res.rgb[0];
-                        acc[1] += wgt * res.rgb[1];
-                        acc[2] += wgt * res.rgb[2];
-                        if (K > 0) {  // TopKBuffer::insert (framebuffers.hpp:33-48)
-                            const uint32_t seq = counter++;
-                            if (k_size < K) {
-#pragma unroll
-                                for (int s = 0; s < KK; ++s)
-                                    if (s == k_size) {
-                                        k_id[s] = id;
-                                        k_w[s] = wgt;
-                                        k_t[s] = res.t;
-                                        k_seq[s] = seq;
-                                    }
-                                ++k_size;
-                            } else {
-                                // last-ranked incumbent: smallest weight, latest arrival among ties
-                                int mi = 0;
-                                double wm = k_w[0];
-                                uint32_t qm = k_seq[0];
-#pragma unroll
-                                for (int s = 1; s < KK; ++s)
-                                    if (k_w[s] < wm || (k_w[s] == wm && k_seq[s] > qm)) {
-                                        mi = s;
-                                        wm = k_w[s];
-                                        qm = k_seq[s];
-                                    }
-#pragma unroll
-                                for (int s = 0; s < KK; ++s)
-                                    if (s == mi && wgt > wm) {
-                                        k_id[s] = id;
-                                        k_w[s] = wgt;
-                                        k_t[s] = res.t;
-                                        k_seq[s] = seq;
-                                    }
-                            }
-                        }
-                        if (kDebug && dbg_row) {
-                            if (dbg_n < a.dbg_max) a.dbg_hits[dbg_q * a.dbg_max + dbg_n] = id;
-                            ++dbg_n;
-                        }
-                        T *= 1.0 - alpha;
-                        if (T < min_T) active = false;
-                    }
-                    __syncwarp();
+                    sm.res[warp][e] = res;
                 }
+                __syncwarp();
+                // ---- B2. per-pixel compositing of this lane's hits, in list order (renderer.cpp:144-153)
+                for (int k = off; k < off + cnt && active; ++k) {
+                    const PoolEntry& res = sm.res[warp][k];
+                    if (res.alpha < 0.0) continue;
+                    const int32_t id = sm.id[sm.q[warp][k] & 0xff];
+                    const double alpha = alpha_max < res.alpha ? alpha_max : res.alpha;
+                    const double wgt = alpha * T;
+                    acc[0] += wgt * res.rgb[0];
+                    acc[1] += wgt * res.rgb[1];
+                    acc[2] += wgt * res.rgb[2];
+                    if (K > 0) {  // TopKBuffer::insert (framebuffers.hpp:33-48)
+                        const uint32_t seq = counter++;
+                        if (k_size < K) {
+#pragma unroll
+                            for (int s = 0; s < KK; ++s)
+                                if (s == k_size) {
+                                    k_id[s] = id;
+                                    k_w[s] = wgt;
+                                    k_t[s] = res.t;
+                                    k_seq[s] = seq;
+                                }
+                            ++k_size;
+                        } else {
+                            // last-ranked incumbent: smallest weight, latest arrival among ties
+                            int mi = 0;
+                            double wm = k_w[0];
+                            uint32_t qm = k_seq[0];
+#pragma unroll
+                            for (int s = 1; s < KK; ++s)
+                                if (k_w[s] < wm || (k_w[s] == wm && k_seq[s] > qm)) {
+                                    mi = s;
+                                    wm = k_w[s];
+                                    qm = k_seq[s];
+                                }
+#pragma unroll
+                            for (int s = 0; s < KK; ++s)
+                                if (s == mi && wgt > wm) {
+                                    k_id[s] = id;
+                                    k_w[s] = wgt;
+                                    k_t[s] = res.t;
+                                    k_seq[s] = seq;
+                                }
+                        }
+                    }
+                    if (kDebug && dbg_row) {
+                        if (dbg_n < a.dbg_max) a.dbg_hits[dbg_q * a.dbg_max + dbg_n] = id;
+                        ++dbg_n;
+                    }
+                    T *= 1.0 - alpha;
+                    if (T < min_T) active = false;
+                }
+                __syncwarp();
             }
-            if (!__syncthreads_or(active)) break;
         }
+        if (cb + kChunk < list_end && !__syncthreads_or(active)) break;
+    }
 
-        if (in_img) {
-            const int64_t pix = static_cast<int64_t>(py) * W + px;
-            a.fb.residual[pix] = static_cast<float>(T);
-            acc[0] += T * a.st.background[0];
-            acc[1] += T * a.st.background[1];
-            acc[2] += T * a.st.background[2];
-            if (K > 0) {
-                // finalize: weight desc, seq asc (framebuffers.hpp:51-56); slots >= size keep sentinels.
+    if (in_img) {
+        const int64_t pix = static_cast<int64_t>(py) * W + px;
+        a.fb.residual[pix] = static_cast<float>(T);
+        acc[0] += T * a.st.background[0];
+        acc[1] += T * a.st.background[1];
+        acc[2] += T * a.st.background[2];
+        if (K > 0) {
+            // finalize: weight desc, seq asc (framebuffers.hpp:51-56); slots >= size keep sentinels.
 #pragma unroll
-                for (int i = 0; i < K; ++i)
+            for (int i = 0; i < K; ++i)
 #pragma unroll
-                    for (int j = 0; j + 1 < K - i; ++j) {
-                        const bool swap = (j + 1 < k_size) &&
-                                          (k_w[j + 1] > k_w[j] || (k_w[j + 1] == k_w[j] && k_seq[j + 1] < k_seq[j]));
-                        if (swap) {
-                            const int32_t ti = k_id[j];
-                            k_id[j] = k_id[j + 1];
-                            k_id[j + 1] = ti;
-                            const double tw = k_w[j];
-                            k_w[j] = k_w[j + 1];
-                            k_w[j + 1] = tw;
-                            const double td = k_t[j];
-                            k_t[j] = k_t[j + 1];
-                            k_t[j + 1] = td;
-                            const uint32_t ts = k_seq[j];
-                            k_seq[j] = k_seq[j + 1];
-                            k_seq[j + 1] = ts;
-                        }
-                    }
-                // write slots; subtract the buffered primitives' own colours (renderer.cpp:157-164)
-#pragma unroll
-                for (int j = 0; j < K; ++j) {
-                    const int64_t sl = pix * K + j;
-                    a.fb.ids[sl] = k_id[j];
-                    a.fb.depths[sl] = k_t[j];
-                    a.fb.weights[sl] = k_w[j];
-                    if (j < k_size) {
-                        float col[3];
-                        eval_sh_f32(a.sh + static_cast<int64_t>(k_id[j]) * NX_SH_VALUES, dfx, dfy, dfz, a.sh_degree,
-                                    col);
-                        acc[0] -= k_w[j] * col[0];
-                        acc[1] -= k_w[j] * col[1];
-                        acc[2] -= k_w[j] * col[2];
+                for (int j = 0; j + 1 < K - i; ++j) {
+                    const bool swap = (j + 1 < k_size) &&
+                                      (k_w[j + 1] > k_w[j] || (k_w[j + 1] == k_w[j] && k_seq[j + 1] < k_seq[j]));
+                    if (swap) {
+                        const int32_t ti = k_id[j];
+                        k_id[j] = k_id[j + 1];
+                        k_id[j + 1] = ti;
+                        const double tw = k_w[j];
+                        k_w[j] = k_w[j + 1];
+                        k_w[j + 1] = tw;
+                        const double td = k_t[j];
+                        k_t[j] = k_t[j + 1];
+                        k_t[j + 1] = td;
+                        const uint32_t ts = k_seq[j];
+                        k_seq[j] = k_seq[j + 1];
+                        k_seq[j + 1] = ts;
                     }
                 }
+            // write slots; subtract the buffered primitives' own colours (renderer.cpp:157-164)
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const int64_t sl = pix * K + j;
+                a.fb.ids[sl] = k_id[j];
+                a.fb.depths[sl] = k_t[j];
+                a.fb.weights[sl] = k_w[j];
+                if (j < k_size) {
+                    float col[3];
+                    eval_sh_f32(a.sh + static_cast<int64_t>(k_id[j]) * NX_SH_VALUES, dfx, dfy, dfz, a.sh_degree, col);
+                    acc[0] -= k_w[j] * col[0];
+                    acc[1] -= k_w[j] * col[1];
+                    acc[2] -= k_w[j] * col[2];
+                }
             }
-            a.fb.base[pix * 3 + 0] = static_cast<float>(acc[0]);
-            a.fb.base[pix * 3 + 1] = static_cast<float>(acc[1]);
-            a.fb.base[pix * 3 + 2] = static_cast<float>(acc[2]);
-            if (kDebug && dbg_row) a.dbg_counts[dbg_q] = dbg_n;
         }
-        __syncthreads();  // sm.dir is rewritten by the next pixel pass
+        a.fb.base[pix * 3 + 0] = static_cast<float>(acc[0]);
+        a.fb.base[pix * 3 + 1] = static_cast<float>(acc[1]);
+        a.fb.base[pix * 3 + 2] = static_cast<float>(acc[2]);
+        if (kDebug && dbg_row) a.dbg_counts[dbg_q] = dbg_n;
     }
 }
 
@@ -378,6 +369,7 @@ void launch_one(const CompositeArgs& a, unsigned grid, cudaStream_t s) {
 template <bool kDebug>
 void launch_k(const CompositeArgs& a, cudaStream_t s) {
     const unsigned grid = static_cast<unsigned>(a.fb.tiles_x) * a.fb.tiles_y;
+    if (grid == 0) return;
     switch (a.fb.K) {
         case 0: launch_one<0, kDebug>(a, grid, s); break;
         case 1: launch_one<1, kDebug>(a, grid, s); break;

@@ -22,6 +22,10 @@ constexpr double kMinNormalDot = 1e-8;     // intersect.hpp:12
 constexpr double kProjectMinDepth = 1e-9;  // camera.hpp:38
 constexpr int kMaxTopK = NX_MAX_TOP_K;
 constexpr int kGeomFields = 12;            // fp64 geometry params per primitive
+// Work lists are built per 8x8 pixel tile (the composite's CTA), independent of
+// settings.tile: every hit of a primitive lies inside its padded pixel rect, so the
+// per-pixel contributor sequences do not depend on the list granularity.
+constexpr int kWorkTile = 8;
 
 // ---------------------------------------------------------------- scalar helpers
 // sigmoid / softplus (vec_math.hpp:69-84)
@@ -161,7 +165,8 @@ struct PreprocessArgs {
     SceneDev scene;
     nx_settings st;
     CamD cam;
-    int tiles_x, tiles_y;
+    int tiles_x, tiles_y;  // reference tiles (settings.tile)
+    int work_tile;         // pixel size of the work-list tiles (kWorkTile)
     double zmin_work;   // conservative camera-z bound of any hit (straddler refinement)
     double* rec;        // n x REC_FIELDS (AoS, 160 B per primitive)
     float4* recf;       // n x 4 fp32 prefilter records (64 B per primitive)

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const PreprocessArgs a)
                     prect = make_int4(clampi(ix0, 0, a.cam.W - 1), clampi(ix1, 0, a.cam.W - 1),
                                       clampi(iy0, 0, a.cam.H - 1), clampi(iy1, 0, a.cam.H - 1));
                     ref = pixel_to_tiles(prect, a.st.tile);
-                    work = ref;
+                    work = pixel_to_tiles(prect, a.work_tile);
                 }
             } else {
                 cls = CLS_STRADDLER;
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const PreprocessArgs a)
                                              {pv * R[1], pv * R[4], pv * R[7]}, a.zmin_work);
                 // Degenerate near-threshold opacity: keep the reference's all-tile list.
                 if (log(op / kAlphaMin) < 1e-3) prect = make_int4(0, a.cam.W - 1, 0, a.cam.H - 1);
-                work = pixel_to_tiles(prect, a.st.tile);
+                work = pixel_to_tiles(prect, a.work_tile);
                 kept = rect_tiles(work) > 0;
             }
         }

@@ -43,11 +43,13 @@ def test_config1_reference_tile_lists_bit_exact(renderer, reference, config1):
 def test_config1_work_lists_are_subsequences(renderer, reference, config1):
     scene, cam = config1
     ds = renderer.upload(scene)
-    w_off, w_ids, _, _ = renderer.tile_lists(ds, cam, reference_lists=False)
-    r_off, r_ids, _, _ = reference.tile_lists(scene, cam)
+    w_off, w_ids, wtx, wty = renderer.tile_lists(ds, cam, reference_lists=False)
+    r_off, r_ids, rtx, _ = reference.tile_lists(scene, cam)
+    assert (wtx, wty) == (32, 32)  # 8x8-pixel work tiles; each lies inside one 16x16 reference tile
     assert w_off[-1] < r_off[-1]
-    for t in range(len(r_off) - 1):
-        assert is_subsequence(w_ids[w_off[t]:w_off[t + 1]], r_ids[r_off[t]:r_off[t + 1]]), f"tile {t}"
+    for t in range(len(w_off) - 1):
+        parent = (t // wtx // 2) * rtx + (t % wtx) // 2
+        assert is_subsequence(w_ids[w_off[t]:w_off[t + 1]], r_ids[r_off[parent]:r_off[parent + 1]]), f"tile {t}"
 
 
 def test_config1_contributor_lists_bit_exact(renderer, reference, config1):
