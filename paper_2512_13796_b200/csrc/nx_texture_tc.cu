@@ -4,21 +4,22 @@
 // cores (tcgen05.mma, accumulators in TMEM), SH colour (eval_sh, sh.hpp:46-57)
 // and the Eq. 7 composite (renderer.cpp:219-236) in the epilogue.
 //
-// Persistent CTAs of 256 threads; one tile = 128 top-K slots (pixel-major,
-// slot-minor = the reference's query order, renderer.cpp:177-203) = the M=128
-// rows of every MMA. Per tile:
-//   gather   two threads per row, 8 levels each (grid_lookup, hash_grid.cpp:26-83;
-//            lattice position, floor and hashing in fp64/int64 like the reference,
-//            so the same table rows are read) -> 32 features -> smem (bf16 hi/lo)
-//   layer 1  D1[128x64]  = F[128x32] . W1^T   (TMEM cols   0..63)
-//   layer 2  D2[128x64]  = relu(D1) . W2^T    (TMEM cols  64..127)
-//   layer 3  D3[128x48]  = relu(D2) . W3^T    (TMEM cols 128..175)
-//   epilogue tcgen05.ld D3 rows -> 48 SH coefficients -> rgb, texture, final.
-// fp32-class accuracy from bf16 operands via the 3-term split
-// a.b ~= a_hi.b_hi + a_hi.b_lo + a_lo.b_hi (relative error ~2^-16), accumulated
-// in fp32 in TMEM. Operands use the K-major no-swizzle canonical layout:
-// 8-row x 16-byte core matrices, LBO = 128 B (next K chunk), SBO = 128*K/8 B
-// (next 8-row group).
+// Persistent CTAs of 128 threads, three per SM: one tile = 128 top-K slots of an
+// 8-pixel-wide block (neighbouring rows query neighbouring lattice cells) = the
+// M = 128 rows of every MMA, one thread per row (= its TMEM lane). Per tile:
+//   gather   16 levels per row (grid_lookup, hash_grid.cpp:26-83; lattice position,
+//            floor and hashing in fp64/int64 like the reference, so the same table
+//            rows are read), two-stage software pipeline -> 32 features -> smem
+//   layer 1  D = F[128x32] . W1^T          (TMEM cols 0..63)
+//   layer 2  D = relu(D) . W2^T            (same columns, drained first)
+//   layer 3  D = relu(D) . W3^T  [128x48]
+//   epilogue tcgen05.ld -> 48 SH coefficients -> rgb -> texture, final (Eq. 7).
+// Three CTAs per SM keep three such pipelines in flight, so one CTA's MMA wait
+// overlaps another's gathers. fp32-class accuracy from bf16 operands via the
+// 3-term split a.b ~= a_hi.b_hi + a_hi.b_lo + a_lo.b_hi (relative error ~2^-16),
+// accumulated in fp32 in TMEM. Operands use the K-major no-swizzle canonical
+// layout: 8-row x 16-byte core matrices, LBO = 128 B (next K chunk),
+// SBO = 128*K/8 B (next 8-row group).
 #include <cuda_bf16.h>
 
 #include "nx_internal.cuh"
@@ -27,14 +28,13 @@ namespace nx {
 
 namespace {
 
-constexpr int kTcThreads = 256;
+constexpr int kTcThreads = 128;
 constexpr int kRows = 128;
 constexpr int kLevels = 16;
 constexpr int kIn = 32, kHid = 64, kOut = 48;
 // D1, D2 and D3 share columns 0..63: each is drained (tcgen05.ld + wait + fence +
 // barrier) before the next layer's MMAs overwrite it.
 constexpr uint32_t kTmemCols = 64;
-constexpr uint32_t kColD1 = 0, kColD2 = 0, kColD3 = 0;
 
 // shared-memory carve-up (bytes)
 constexpr int kOffW1h = 0;
@@ -46,13 +46,11 @@ constexpr int kOffW3l = kOffW3h + kOut * kHid * 2;   // 6 KB each
 constexpr int kOffAh = kOffW3l + kOut * kHid * 2;
 constexpr int kOffAl = kOffAh + kRows * kHid * 2;    // 16 KB each
 constexpr int kOffRgb = kOffAl + kRows * kHid * 2;   // float [128][3]
-constexpr int kOffPart = kOffRgb + kRows * 3 * 4;    // float [128][3]
-constexpr int kOffBar = kOffPart + kRows * 3 * 4;    // mbarrier (8 B)
+constexpr int kOffBar = kOffRgb + kRows * 3 * 4;     // mbarrier (8 B)
 constexpr int kOffTmem = kOffBar + 8;                // tmem base (4 B)
-constexpr int kSmemUsed = kOffTmem + 8;
-// Request more than needed so that at most two CTAs share an SM (2 x 256 TMEM columns).
-constexpr int kSmemRequest = 100 * 1024;
-static_assert(kSmemUsed <= kSmemRequest, "smem carve-up");
+constexpr int kSmemUsed = kOffTmem + 8;              // ~70.5 KB: three CTAs per SM
+static_assert(kSmemUsed <= 72 * 1024, "three CTAs per SM");
+constexpr int kCtasPerSm = 3;
 
 struct TcConst {
     double level_scale[kLevels];  // HashGridConfig::level_scale by iterated product (hash_grid.cpp:7-13)
@@ -114,16 +112,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
-    uint32_t r[8];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -188,10 +176,39 @@ __device__ __forceinline__ LevelFetch fetch_level(int l, double x0, double x1, d
     return f;
 }
 
-__global__ void __launch_bounds__(kTcThreads, 2) texture_tc_kernel(const TextureArgs a, const TcConst cst,
-                                                                   int bw, int bh, int tiles_x, int64_t n_tiles) {
+__device__ __forceinline__ float2 interp(const LevelFetch& f) {
+    const float wx[2] = {1.0f - f.fr0, f.fr0}, wy[2] = {1.0f - f.fr1, f.fr1}, wz[2] = {1.0f - f.fr2, f.fr2};
+    float g0 = 0.f, g1 = 0.f;
+#pragma unroll
+    for (int ci = 0; ci < 8; ++ci) {
+        const float w = wx[ci & 1] * wy[(ci >> 1) & 1] * wz[(ci >> 2) & 1];
+        g0 += w * f.v[ci].x;
+        g1 += w * f.v[ci].y;
+    }
+    return make_float2(g0 * f.dw, g1 * f.dw);
+}
+
+// Issues one layer: D = A . B^T over K (3 split terms per 16-wide k-step), commit.
+__device__ __forceinline__ void issue_layer(uint8_t* smem, uint32_t dtm, int off_bh, int off_bl, int K,
+                                            uint32_t idesc, uint32_t bar) {
+    tc_fence_after();
+    const uint32_t ah = smem_u32(smem + kOffAh), al = smem_u32(smem + kOffAl);
+    const uint32_t bh = smem_u32(smem + off_bh), bl = smem_u32(smem + off_bl);
+    const uint32_t sbo = 16 * K;
+    for (int s = 0; s < K / 16; ++s) {
+        const uint32_t o = s * 256;
+        mma_bf16(dtm, smem_desc(ah + o, 128, sbo), smem_desc(bh + o, 128, sbo), idesc, s > 0);
+        mma_bf16(dtm, smem_desc(ah + o, 128, sbo), smem_desc(bl + o, 128, sbo), idesc, 1);
+        mma_bf16(dtm, smem_desc(al + o, 128, sbo), smem_desc(bh + o, 128, sbo), idesc, 1);
+    }
+    mma_commit(bar);
+}
+
+__global__ void __launch_bounds__(kTcThreads, kCtasPerSm) texture_tc_kernel(const TextureArgs a, const TcConst cst,
+                                                                            int bw, int bh, int tiles_x,
+                                                                            int64_t n_tiles) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t bar = smem_u32(smem + kOffBar);
 
     // ---- one-time setup: weights -> smem (bf16 hi/lo, K-major core-matrix layout)
@@ -234,14 +251,12 @@ __global__ void __launch_bounds__(kTcThreads, 2) texture_tc_kernel(const Texture
 
     const int K = a.fb.K;
     const int W = a.cam.W;
-    const int row = tid & (kRows - 1);  // == 32 * (warp % 4) + lane: the TMEM lane this thread reads
-    const int half = tid >> 7;          // gather: levels [8 half, 8 half + 8); epilogue: column half
-    const uint32_t lane_base = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+    const int row = tid;  // MMA row == TMEM lane 32 * warp + lane
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * warp) << 16);
     const uint32_t T = 1u << a.scene.field.log2_table;
     const uint32_t mask = T - 1u;
     const float2* tab = reinterpret_cast<const float2*>(a.scene.table);
-    const float* srgb = reinterpret_cast<const float*>(smem + kOffRgb);
-    float* spart = reinterpret_cast<float*>(smem + kOffPart);
+    float* srgb = reinterpret_cast<float*>(smem + kOffRgb);
     constexpr uint32_t kIdesc64 = idesc_bf16_f32(kRows, 64);
     constexpr uint32_t kIdesc48 = idesc_bf16_f32(kRows, 48);
     int n_queries = 0;
@@ -255,161 +270,119 @@ __global__ void __launch_bounds__(kTcThreads, 2) texture_tc_kernel(const Texture
         const bool in_tile = p_in < ppt && px < W && py < a.cam.H;
         const int64_t slot = in_tile ? (static_cast<int64_t>(py) * W + px) * K + j_in : 0;
         const bool valid = in_tile && a.fb.ids[slot] >= 0;
-        if (valid && half == 0) ++n_queries;
+        n_queries += valid;
         double dir[3] = {0.0, 0.0, 1.0};
-        float feats[16];
+        float feats[kIn];
         if (valid) {
             pixel_dir(a.cam, px + 0.5, py + 0.5, dir);
             const double t = a.fb.depths[slot];
-            const double x0 = a.cam.o[0] + t * dir[0];
+            const double x0 = a.cam.o[0] + t * dir[0];  // build_queries (renderer.cpp:196-198)
             const double x1 = a.cam.o[1] + t * dir[1];
             const double x2 = a.cam.o[2] + t * dir[2];
             const float ft = static_cast<float>(a.cam.fx / t);
-            // Two-stage software pipeline over the levels: the 8 corner gathers of level
-            // l+1 are in flight while level l is interpolated.
-            LevelFetch cur = fetch_level(half * 8, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
+            // two-stage software pipeline: level l+1's 8 gathers are in flight while
+            // level l is interpolated
+            LevelFetch cur = fetch_level(0, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
 #pragma unroll
-            for (int li = 0; li < 8; ++li) {
+            for (int l = 0; l < kLevels; ++l) {
                 LevelFetch nxt;
-                if (li < 7) nxt = fetch_level(half * 8 + li + 1, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
-                const float wx[2] = {1.0f - cur.fr0, cur.fr0}, wy[2] = {1.0f - cur.fr1, cur.fr1},
-                            wz[2] = {1.0f - cur.fr2, cur.fr2};
-                float g0 = 0.f, g1 = 0.f;
-#pragma unroll
-                for (int ci = 0; ci < 8; ++ci) {
-                    const float w = wx[ci & 1] * wy[(ci >> 1) & 1] * wz[(ci >> 2) & 1];
-                    g0 += w * cur.v[ci].x;
-                    g1 += w * cur.v[ci].y;
-                }
-                feats[2 * li] = g0 * cur.dw;
-                feats[2 * li + 1] = g1 * cur.dw;
-                if (li < 7) cur = nxt;
+                if (l + 1 < kLevels) nxt = fetch_level(l + 1, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
+                const float2 g = interp(cur);
+                feats[2 * l] = g.x;
+                feats[2 * l + 1] = g.y;
+                if (l + 1 < kLevels) cur = nxt;
             }
         } else {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) feats[i] = 0.f;
+            for (int i = 0; i < kIn; ++i) feats[i] = 0.f;
         }
-        // features k = 16 half + i -> two 8-wide chunks of the layer-1 A operand (K = 32)
-        store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 16 * half, kIn), feats);
-        store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 16 * half + 8, kIn), feats + 8);
+#pragma unroll
+        for (int c = 0; c < kIn / 8; ++c) store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 8 * c, kIn), feats + 8 * c);
         fence_async_smem();
         tc_fence_before();
         __syncthreads();
 
-        // ---- layer 1: D1 = F . W1^T  (K = 32: 2 k-steps x 3 split terms)
-        if (tid == 0) {
-            tc_fence_after();
-            const uint32_t ah = smem_u32(smem + kOffAh), al = smem_u32(smem + kOffAl);
-            const uint32_t bh = smem_u32(smem + kOffW1h), bl = smem_u32(smem + kOffW1l);
-#pragma unroll
-            for (int s = 0; s < kIn / 16; ++s) {
-                const uint32_t o = s * 256;
-                mma_bf16(tmem + kColD1, smem_desc(ah + o, 128, 512), smem_desc(bh + o, 128, 512), kIdesc64, s > 0);
-                mma_bf16(tmem + kColD1, smem_desc(ah + o, 128, 512), smem_desc(bl + o, 128, 512), kIdesc64, 1);
-                mma_bf16(tmem + kColD1, smem_desc(al + o, 128, 512), smem_desc(bh + o, 128, 512), kIdesc64, 1);
-            }
-            mma_commit(bar);
-        }
+        // ---- layer 1: D = F . W1^T (K = 32)
+        if (tid == 0) issue_layer(smem, tmem, kOffW1h, kOffW1l, kIn, kIdesc64, bar);
         mbar_wait(bar, phase);
         phase ^= 1;
         tc_fence_after();
 
-        // ---- hidden layers: relu(D) -> A (K = 64), then D_next = A . W^T
+        // ---- hidden layers: relu(D) -> A (K = 64), then D = A . W^T
 #pragma unroll 1
         for (int layer = 0; layer < 2; ++layer) {
-            const uint32_t dcol = layer == 0 ? kColD1 : kColD2;
-            float v[32];
-            tmem_ld16(tmem + lane_base + dcol + 32 * half, v);
-            tmem_ld16(tmem + lane_base + dcol + 32 * half + 16, v + 16);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+            for (int c = 0; c < kHid / 16; ++c) {
+                float v[16];
+                tmem_ld16(taddr + 16 * c, v);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 32 * half + 8 * c, kHid), v + 8 * c);
+                for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
+                store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 16 * c, kHid), v);
+                store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 16 * c + 8, kHid), v + 8);
+            }
             fence_async_smem();
             tc_fence_before();
             __syncthreads();
             if (tid == 0) {
-                tc_fence_after();
-                const uint32_t ah = smem_u32(smem + kOffAh), al = smem_u32(smem + kOffAl);
-                const uint32_t bh = smem_u32(smem + (layer == 0 ? kOffW2h : kOffW3h));
-                const uint32_t bl = smem_u32(smem + (layer == 0 ? kOffW2l : kOffW3l));
-                const uint32_t dn = tmem + (layer == 0 ? kColD2 : kColD3);
-                const uint32_t idesc = layer == 0 ? kIdesc64 : kIdesc48;
-#pragma unroll
-                for (int s = 0; s < kHid / 16; ++s) {
-                    const uint32_t o = s * 256;
-                    mma_bf16(dn, smem_desc(ah + o, 128, 1024), smem_desc(bh + o, 128, 1024), idesc, s > 0);
-                    mma_bf16(dn, smem_desc(ah + o, 128, 1024), smem_desc(bl + o, 128, 1024), idesc, 1);
-                    mma_bf16(dn, smem_desc(al + o, 128, 1024), smem_desc(bh + o, 128, 1024), idesc, 1);
-                }
-                mma_commit(bar);
+                if (layer == 0) issue_layer(smem, tmem, kOffW2h, kOffW2l, kHid, kIdesc64, bar);
+                else issue_layer(smem, tmem, kOffW3h, kOffW3l, kHid, kIdesc48, bar);
             }
             mbar_wait(bar, phase);
             phase ^= 1;
             tc_fence_after();
         }
 
-        // ---- epilogue: D3 (48 SH coefficients, k*3 + c) -> rgb. Column half h holds
-        // coefficients k in [8h, 8h + 8) (24 columns).
+        // ---- epilogue: D (48 SH coefficients, k*3 + c) -> rgb (eval_sh, sh.hpp:46-57)
         {
-            float y[24];
-            tmem_ld16(tmem + lane_base + kColD3 + 24 * half, y);
-            tmem_ld8(tmem + lane_base + kColD3 + 24 * half + 16, y + 16);
-            const float x = static_cast<float>(dir[0]), yy_ = static_cast<float>(dir[1]), z = static_cast<float>(dir[2]);
-            const float xx = x * x, yy = yy_ * yy_, zz = z * z;
-            float b[8];
-            if (half == 0) {  // sh_basis (sh.hpp:11-40), k = 0..7
-                b[0] = 0.28209479177387814f;
-                b[1] = -0.4886025119029199f * yy_;
-                b[2] = 0.4886025119029199f * z;
-                b[3] = -0.4886025119029199f * x;
-                b[4] = 1.0925484305920792f * x * yy_;
-                b[5] = -1.0925484305920792f * yy_ * z;
-                b[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
-                b[7] = -1.0925484305920792f * x * z;
-            } else {  // k = 8..15
-                b[0] = 0.5462742152960396f * (xx - yy);
-                b[1] = -0.5900435899266435f * yy_ * (3.0f * xx - yy);
-                b[2] = 2.890611442640554f * x * yy_ * z;
-                b[3] = -0.4570457994644658f * yy_ * (4.0f * zz - xx - yy);
-                b[4] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
-                b[5] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
-                b[6] = 1.445305721320277f * z * (xx - yy);
-                b[7] = -0.5900435899266435f * x * (xx - 3.0f * yy);
-            }
+            const float x = static_cast<float>(dir[0]), y = static_cast<float>(dir[1]), z = static_cast<float>(dir[2]);
+            const float xx = x * x, yy = y * y, zz = z * z;
+            float b[16];
+            b[0] = 0.28209479177387814f;
+            b[1] = -0.4886025119029199f * y;
+            b[2] = 0.4886025119029199f * z;
+            b[3] = -0.4886025119029199f * x;
+            b[4] = 1.0925484305920792f * x * y;
+            b[5] = -1.0925484305920792f * y * z;
+            b[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+            b[7] = -1.0925484305920792f * x * z;
+            b[8] = 0.5462742152960396f * (xx - yy);
+            b[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
+            b[10] = 2.890611442640554f * x * y * z;
+            b[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
+            b[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+            b[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
+            b[14] = 1.445305721320277f * z * (xx - yy);
+            b[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
             float c0 = 0.f, c1 = 0.f, c2 = 0.f;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                c0 = fmaf(y[3 * k + 0], b[k], c0);
-                c1 = fmaf(y[3 * k + 1], b[k], c1);
-                c2 = fmaf(y[3 * k + 2], b[k], c2);
-            }
-            if (half == 1) {
-                spart[row * 3 + 0] = c0;
-                spart[row * 3 + 1] = c1;
-                spart[row * 3 + 2] = c2;
-            }
-            tc_fence_before();
-            __syncthreads();
-            if (half == 0) {
-                float rgb[3] = {0.f, 0.f, 0.f};
-                if (valid) {
-                    rgb[0] = fmaxf(0.5f + (c0 + spart[row * 3 + 0]), 0.f);
-                    rgb[1] = fmaxf(0.5f + (c1 + spart[row * 3 + 1]), 0.f);
-                    rgb[2] = fmaxf(0.5f + (c2 + spart[row * 3 + 2]), 0.f);
-                }
-                float* dst = reinterpret_cast<float*>(smem + kOffRgb) + row * 3;
-                dst[0] = rgb[0];
-                dst[1] = rgb[1];
-                dst[2] = rgb[2];
-                if (in_tile) {
-                    a.fb.texture[slot * 3 + 0] = rgb[0];
-                    a.fb.texture[slot * 3 + 1] = rgb[1];
-                    a.fb.texture[slot * 3 + 2] = rgb[2];
+            for (int c = 0; c < kOut / 16; ++c) {
+                float v[16];
+                tmem_ld16(taddr + 16 * c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int o = 16 * c + i, k = o / 3;
+                    if (o % 3 == 0) c0 = fmaf(v[i], b[k], c0);
+                    else if (o % 3 == 1) c1 = fmaf(v[i], b[k], c1);
+                    else c2 = fmaf(v[i], b[k], c2);
                 }
             }
-            __syncthreads();
+            float rgb[3] = {0.f, 0.f, 0.f};
+            if (valid) {
+                rgb[0] = fmaxf(0.5f + c0, 0.f);
+                rgb[1] = fmaxf(0.5f + c1, 0.f);
+                rgb[2] = fmaxf(0.5f + c2, 0.f);
+            }
+            srgb[row * 3 + 0] = rgb[0];
+            srgb[row * 3 + 1] = rgb[1];
+            srgb[row * 3 + 2] = rgb[2];
+            if (in_tile) {
+                a.fb.texture[slot * 3 + 0] = rgb[0];
+                a.fb.texture[slot * 3 + 1] = rgb[1];
+                a.fb.texture[slot * 3 + 2] = rgb[2];
+            }
         }
+        tc_fence_before();
+        __syncthreads();
         // ---- Eq. 7: final = base + sum_j W[p,j] * texture[p,j] for this tile's pixels
         if (tid < ppt) {
             const int qx = tpx + tid % bw, qy = tpy + tid / bw;
@@ -430,16 +403,16 @@ __global__ void __launch_bounds__(kTcThreads, 2) texture_tc_kernel(const Texture
                 a.fb.final_img[pix * 3 + 2] = static_cast<float>(acc2);
             }
         }
-        tc_fence_before();
-        __syncthreads();
+        // srgb and the A buffers are rewritten by the next tile only after its gather,
+        // which every thread reaches after this point; the gather's barrier orders them.
     }
 
-    // queries counted by the half-0 threads
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) n_queries += __shfl_down_sync(0xffffffffu, n_queries, o);
-    if (lane == 0 && n_queries) atomicAdd(&a.stats->queries, static_cast<unsigned long long>(n_queries));
-    tc_fence_after();
+    if ((tid & 31) == 0 && n_queries) atomicAdd(&a.stats->queries, static_cast<unsigned long long>(n_queries));
+    tc_fence_before();
     __syncthreads();
+    tc_fence_after();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
 
@@ -468,10 +441,10 @@ int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(texture_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemRequest);
-    const int64_t grid = std::min<int64_t>(n_tiles, 2 * static_cast<int64_t>(sms));
+    cudaFuncSetAttribute(texture_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemUsed);
+    const int64_t grid = std::min<int64_t>(n_tiles, static_cast<int64_t>(kCtasPerSm) * sms);
     count_launch();
-    texture_tc_kernel<<<static_cast<unsigned>(grid), kTcThreads, kSmemRequest, s>>>(a, cst, bw, bh, tiles_x, n_tiles);
+    texture_tc_kernel<<<static_cast<unsigned>(grid), kTcThreads, kSmemUsed, s>>>(a, cst, bw, bh, tiles_x, n_tiles);
     return NX_OK;
 }
 
