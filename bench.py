@@ -299,8 +299,11 @@ def run_ours(args):
         vstats[v] = fr.stats()
     H, W, K = args.height, args.width, 2
 
+    # two frames in flight: frame i's texture pass (second stream) overlaps frame
+    # i+1's binning + compositing (first stream)
+    frames = [fr, r.frame()]
     for s in range(args.warmup):
-        r.render(ds, cams[views[s]], fr)
+        r.render(ds, cams[views[s]], frames[s % 2])
     r.synchronize()
 
     # ---- timed region: device time of K steps (CUDA events on the render stream)
@@ -315,7 +318,8 @@ def run_ours(args):
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for s in range(args.warmup, n_steps):
-        r.render(ds, cams[views[s]], fr)
+        r.render(ds, cams[views[s]], frames[s % 2])
+    r._check(r.lib.nx_ctx_join(r.ctx))  # the end event follows the last texture pass
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier(dist)
@@ -351,8 +355,10 @@ def run_ours(args):
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for s in range(args.warmup, n_steps):
-        r.render(ds, cams[views[s]], fr)
-        r._check(r.lib.nx_frame_download(r.ctx, fr.handle, C.byref(hf), None))
+        f2 = frames[s % 2]
+        r.render(ds, cams[views[s]], f2)
+        r._check(r.lib.nx_frame_download(r.ctx, f2.handle, C.byref(hf), None))
+    r._check(r.lib.nx_ctx_join(r.ctx))
     e1.record(stream)
     torch.cuda.synchronize()
     barrier(dist)
@@ -395,7 +401,8 @@ def run_ours(args):
             "gpu_launches": launches, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    fr.close()
+    for f2 in frames:
+        f2.close()
     ds.close()
     r.close()
     if dist is not None:

@@ -137,8 +137,12 @@ int nx_device_count(int* count);
 int nx_ctx_create(int device, nx_ctx** out);
 void nx_ctx_destroy(nx_ctx* ctx);
 const char* nx_ctx_last_error(const nx_ctx* ctx, int* status);
-void* nx_ctx_stream(nx_ctx* ctx);                  /* the context's own stream */
-int nx_ctx_synchronize(nx_ctx* ctx);
+void* nx_ctx_stream(nx_ctx* ctx);                  /* the context's own (first) stream */
+int nx_ctx_synchronize(nx_ctx* ctx);                /* both context streams */
+/* Makes the first stream wait for all work queued on the second one (texture
+ * passes and downloads issued with stream == NULL run there, overlapping the next
+ * frame's collection pass). */
+int nx_ctx_join(nx_ctx* ctx);
 
 /* Stage timing (CUDA events recorded between the stages of each frame). */
 #define NX_STAGE_PREPROCESS 0

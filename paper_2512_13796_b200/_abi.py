@@ -146,6 +146,7 @@ SIGNATURES = [
     ("nx_ctx_last_error", C.c_char_p, [P, C.POINTER(C.c_int)]),
     ("nx_ctx_stream", P, [P]),
     ("nx_ctx_synchronize", C.c_int, [P]),
+    ("nx_ctx_join", C.c_int, [P]),
     ("nx_ctx_set_profiling", C.c_int, [P, C.c_int]),
     ("nx_ctx_stage_times", C.c_int, [P, PF, C.c_int, C.POINTER(C.c_int)]),
     ("nx_stage_name", C.c_char_p, [C.c_int]),

@@ -62,6 +62,11 @@ std::atomic<unsigned long long> g_launches{0};
 
 const char* kStageNames[NX_NUM_STAGES] = {"preprocess", "depth_sort", "emit", "tile_sort", "composite", "texture"};
 
+// Profiling event points per frame (stage k spans two points; the texture pass may
+// run on the second stream, so it has its own start/end points).
+enum EvPoint { kEvPre, kEvDepth, kEvEmit, kEvTileSort, kEvComp, kEvCompEnd, kEvTex, kEvTexEnd, kEvPoints };
+constexpr int kEvSets = 4;
+
 }  // namespace
 
 void nx::count_launch(int n) { g_launches.fetch_add(static_cast<unsigned long long>(n), std::memory_order_relaxed); }
@@ -78,9 +83,11 @@ struct nx_ctx {
     DevBuf dbg_hits, dbg_counts;
     int32_t* h_pinned = nullptr;  // small readbacks
     bool profiling = false;
-    cudaEvent_t ev[2][NX_NUM_STAGES + 1] = {};
+    cudaStream_t stream2 = nullptr;  // texture pass + downloads: overlaps the next frame's collection
+    cudaEvent_t ev_join = nullptr;
+    cudaEvent_t ev[kEvSets][kEvPoints] = {};
     int ev_cur = 0;
-    bool ev_pending[2] = {false, false};  // profiled frames whose events are not folded yet
+    bool ev_pending[kEvSets] = {};  // profiled frames whose events are not folded yet
     double stage_acc[NX_NUM_STAGES] = {};
     int stage_frames = 0;
 };
@@ -104,6 +111,9 @@ struct nx_frame {
     DevBuf list_ids;
     FrameStatsD* stats = nullptr;  // device
     int64_t n_nexels = 0;
+    cudaEvent_t ev_ready = nullptr;  // collection pass of this frame done
+    cudaEvent_t ev_busy = nullptr;   // last texture pass / download of this frame done
+    bool busy_pending = false;
 };
 
 namespace {
@@ -238,25 +248,38 @@ SceneDev scene_dev(const nx_scene* s) {
     return d;
 }
 
-void record(nx_ctx* c, int stage, cudaStream_t s) {
-    if (c->profiling) cudaEventRecord(c->ev[c->ev_cur][stage], s);
+void record(nx_ctx* c, int point, cudaStream_t s) {
+    if (c->profiling) cudaEventRecord(c->ev[c->ev_cur][point], s);
 }
 
-// Folds a completed profiled frame's stage events into the running sums.
-void fold_set(nx_ctx* c, int set) {
+// Folds a profiled frame's stage events into the running sums. Non-blocking unless
+// `wait`: a set whose last event has not completed yet stays pending.
+void fold_set(nx_ctx* c, int set, bool wait) {
     if (!c->ev_pending[set]) return;
+    cudaEvent_t last = c->ev[set][kEvTexEnd];
+    if (wait) cudaEventSynchronize(last);
+    else if (cudaEventQuery(last) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    static const int kFrom[NX_NUM_STAGES] = {kEvPre, kEvDepth, kEvEmit, kEvTileSort, kEvComp, kEvTex};
+    static const int kTo[NX_NUM_STAGES] = {kEvDepth, kEvEmit, kEvTileSort, kEvComp, kEvCompEnd, kEvTexEnd};
     for (int i = 0; i < NX_NUM_STAGES; ++i) {
         float v = 0.f;
-        if (cudaEventElapsedTime(&v, c->ev[set][i], c->ev[set][i + 1]) == cudaSuccess) c->stage_acc[i] += v;
+        if (cudaEventElapsedTime(&v, c->ev[set][kFrom[i]], c->ev[set][kTo[i]]) == cudaSuccess) c->stage_acc[i] += v;
     }
     cudaGetLastError();
     c->stage_frames += 1;
     c->ev_pending[set] = false;
 }
 
-// Event sets alternate between frames, so the previous frame's set is folded at
-// the current frame's (already synchronised) mid-frame point: profiling adds no sync.
-void fold_stage_times(nx_ctx* c) { fold_set(c, c->ev_cur ^ 1); }
+// Called at the start of each profiled frame: folds whatever completed and moves to
+// the next event set of the ring (blocking only if that set is still in flight).
+void next_event_set(nx_ctx* c) {
+    for (int s = 0; s < kEvSets; ++s) fold_set(c, s, false);
+    c->ev_cur = (c->ev_cur + 1) % kEvSets;
+    fold_set(c, c->ev_cur, true);
+}
 
 int check_inputs(nx_ctx* c, const nx_scene* scene, const nx_camera* cam) {
     if (!c || !scene || !cam) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
@@ -301,11 +324,8 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
     NX_CUDA(c, c->scratch.ensure(scratch_ints * sizeof(int32_t)));
     NX_CUDA(c, cudaMemsetAsync(f->stats, 0, sizeof(FrameStatsD), s));
 
-    if (c->profiling) {
-        c->ev_cur ^= 1;
-        fold_set(c, c->ev_cur);  // only pending if the frame before last was never folded
-    }
-    record(c, NX_STAGE_PREPROCESS, s);
+    if (c->profiling) next_event_set(c);
+    record(c, kEvPre, s);
     PreprocessArgs pa;
     pa.scene = scene_dev(scene);
     pa.st = scene->st;
@@ -331,7 +351,7 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
     // The sorted count stays on the device: the sort runs over capacity n with the
     // device count (no host round trip).
     scan_exclusive(c->flag.as<int32_t>(), c->pos.as<int32_t>(), n, d_total, sc, s);
-    record(c, NX_STAGE_DEPTH_SORT, s);
+    record(c, kEvDepth, s);
     launch_compact(c->flag.as<int32_t>(), c->pos.as<int32_t>(), c->key.as<uint64_t>(), n, c->skeys_a.as<uint64_t>(),
                    c->sids_a.as<uint32_t>(), s);
     const bool in_b = radix_sort_pairs_u64(c->skeys_a.as<uint64_t>(), c->sids_a.as<uint32_t>(),
@@ -341,12 +361,11 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
 
     // K3: emit (tile, id) keys in sorted order. The one host round trip of the frame:
     // the key count sizes the key buffers.
-    record(c, NX_STAGE_EMIT, s);
+    record(c, kEvEmit, s);
     launch_rect_counts(sorted_ids, n, d_total, c->work_rect.as<int4>(), c->counts.as<int32_t>(), s);
     scan_exclusive(c->counts.as<int32_t>(), c->offsets.as<int32_t>(), n, d_total + 1, sc, s);
     NX_CUDA(c, cudaMemcpyAsync(c->h_pinned, d_total, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     NX_CUDA(c, cudaStreamSynchronize(s));
-    fold_stage_times(c);  // the previous profiled frame's events are complete
     const int64_t n_sorted = n > 0 ? c->h_pinned[0] : 0;
     const int64_t n_keys = n_sorted > 0 ? c->h_pinned[1] : 0;
     if (n_keys < 0) return set_err(c, NX_UNSUPPORTED, "tile-key count exceeds 2^31");
@@ -367,7 +386,7 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
                 c->tkeys_a.as<uint32_t>(), c->tvals_a.as<uint32_t>(), c->tile_counts.as<int32_t>(), s);
 
     // K4: stable sort by tile.
-    record(c, NX_STAGE_TILE_SORT, s);
+    record(c, kEvTileSort, s);
     const int tb = std::max(bits_for(n_tiles), 1);
     const bool t_in_b = radix_sort_pairs_u32(c->tkeys_a.as<uint32_t>(), c->tvals_a.as<uint32_t>(),
                                              c->tkeys_b.as<uint32_t>(), c->tvals_b.as<uint32_t>(), n_keys, nullptr, 0,
@@ -385,11 +404,13 @@ int collection(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame*
                int32_t* dbg_hits, int32_t* dbg_counts, int dbg_y0, int dbg_y1, int dbg_max) {
     int st;
     if ((st = check_inputs(c, scene, cam))) return st;
+    // the frame may still be read by its previous texture pass / download (second stream)
+    if (f->busy_pending) NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_busy, 0));
     if ((st = frame_shape(c, f, cam->width, cam->height, scene->st.top_k, scene->st.tile))) return st;
     f->n_nexels = scene->n;
     int64_t total = 0;
     if ((st = build_lists(c, scene, *cam, f, 0, s, &total))) return st;
-    record(c, NX_STAGE_COMPOSITE, s);
+    record(c, kEvComp, s);
     CompositeArgs ca;
     ca.rec = c->rec.as<double>();
     ca.recf = c->recf.as<float4>();
@@ -407,6 +428,8 @@ int collection(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame*
     ca.dbg_y1 = dbg_y1;
     ca.dbg_max = dbg_max;
     launch_composite(ca, s);
+    record(c, kEvCompEnd, s);
+    NX_CUDA(c, cudaEventRecord(f->ev_ready, s));
     NX_CUDA(c, cudaGetLastError());
     return NX_OK;
 }
@@ -414,7 +437,8 @@ int collection(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame*
 int texturing(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* f, cudaStream_t s) {
     if (f->W != cam->width || f->H != cam->height)
         return set_err(c, NX_INVALID_ARGUMENT, "frame does not match the camera (run collection_pass first)");
-    record(c, NX_STAGE_TEXTURE, s);
+    NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_ready, 0));  // no-op on the collection's own stream
+    record(c, kEvTex, s);
     TextureArgs ta;
     ta.scene = scene_dev(scene);
     ta.st = scene->st;
@@ -423,8 +447,10 @@ int texturing(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* 
     ta.stats = f->stats;
     const int st = launch_texture(ta, s);
     if (st) return set_err(c, st, "texture field shape not supported (n_in <= 64, n_hidden <= 128)");
-    record(c, NX_NUM_STAGES, s);
+    record(c, kEvTexEnd, s);
     if (c->profiling) c->ev_pending[c->ev_cur] = true;
+    NX_CUDA(c, cudaEventRecord(f->ev_busy, s));
+    f->busy_pending = true;
     NX_CUDA(c, cudaGetLastError());
     return NX_OK;
 }
@@ -471,6 +497,8 @@ int nx_ctx_create(int device, nx_ctx** out) {
     if (!c) return NX_OUT_OF_MEMORY;
     c->device = device;
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaMallocHost(&c->h_pinned, 64 * sizeof(int32_t)) != cudaSuccess) {
         delete c;
         return NX_CUDA_ERROR;
@@ -485,6 +513,7 @@ void nx_ctx_destroy(nx_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    cudaStreamSynchronize(c->stream2);
     for (DevBuf* b : {&c->rec, &c->recf, &c->cls, &c->ref_rect, &c->work_rect, &c->key, &c->flag, &c->pos, &c->skeys_a,
                       &c->skeys_b, &c->sids_a, &c->sids_b, &c->counts, &c->offsets, &c->tkeys_a, &c->tkeys_b,
                       &c->tvals_a, &c->tvals_b, &c->tile_counts, &c->scratch, &c->dbg_hits, &c->dbg_counts})
@@ -492,7 +521,9 @@ void nx_ctx_destroy(nx_ctx* c) {
     for (auto& set : c->ev)
         for (auto& e : set) cudaEventDestroy(e);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    cudaEventDestroy(c->ev_join);
     cudaStreamDestroy(c->stream);
+    cudaStreamDestroy(c->stream2);
     delete c;
 }
 
@@ -506,6 +537,14 @@ void* nx_ctx_stream(nx_ctx* c) { return c ? c->stream : nullptr; }
 
 int nx_ctx_synchronize(nx_ctx* c) {
     NX_CUDA(c, cudaStreamSynchronize(c->stream));
+    NX_CUDA(c, cudaStreamSynchronize(c->stream2));
+    return NX_OK;
+}
+
+int nx_ctx_join(nx_ctx* c) {
+    if (!c) return NX_INVALID_ARGUMENT;
+    NX_CUDA(c, cudaEventRecord(c->ev_join, c->stream2));
+    NX_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     return NX_OK;
 }
 
@@ -518,8 +557,7 @@ int nx_ctx_set_profiling(nx_ctx* c, int enable) {
 int nx_ctx_stage_times(nx_ctx* c, float* ms, int n, int* frames) {
     if (!c || !ms) return NX_INVALID_ARGUMENT;
     NX_CUDA(c, cudaDeviceSynchronize());
-    fold_set(c, c->ev_cur ^ 1);
-    fold_set(c, c->ev_cur);
+    for (int set = 0; set < kEvSets; ++set) fold_set(c, set, true);
     for (int i = 0; i < n && i < NX_NUM_STAGES; ++i)
         ms[i] = c->stage_frames ? static_cast<float>(c->stage_acc[i] / c->stage_frames) : 0.f;
     if (frames) *frames = c->stage_frames;
@@ -641,6 +679,11 @@ int nx_frame_create(nx_ctx* c, int width, int height, int top_k, nx_frame** out)
         return set_err(c, NX_OUT_OF_MEMORY, "frame stats");
     }
     cudaMemset(f->stats, 0, sizeof(FrameStatsD));
+    if (cudaEventCreateWithFlags(&f->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f->ev_busy, cudaEventDisableTiming) != cudaSuccess) {
+        nx_frame_destroy(f);
+        return set_err(c, NX_CUDA_ERROR, "frame events");
+    }
     int st = frame_shape(c, f, width, height, top_k, 16);
     if (st) {
         nx_frame_destroy(f);
@@ -656,7 +699,10 @@ void nx_frame_destroy(nx_frame* f) {
     for (DevBuf* b : {&f->base, &f->ids, &f->depths, &f->weights, &f->texture, &f->final_img, &f->residual,
                       &f->tile_offsets})
         b->release();
+    if (f->ev_busy) cudaEventSynchronize(f->ev_busy);
     if (f->stats) cudaFree(f->stats);
+    if (f->ev_ready) cudaEventDestroy(f->ev_ready);
+    if (f->ev_busy) cudaEventDestroy(f->ev_busy);
     delete f;
 }
 
@@ -677,9 +723,14 @@ int nx_frame_view_get(const nx_frame* f, nx_frame_view* v) {
     return NX_OK;
 }
 
-int nx_frame_download(nx_ctx* c, const nx_frame* f, const nx_host_frame* dst, void* stream) {
-    if (!c || !f || !dst) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
-    cudaStream_t s = pick_stream(c, stream);
+int nx_frame_download(nx_ctx* c, const nx_frame* fc, const nx_host_frame* dst, void* stream) {
+    if (!c || !fc || !dst) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    nx_frame* f = const_cast<nx_frame*>(fc);  // only the frame's ordering events change
+    // default: the second stream, after the frame's texture pass, so that the copy
+    // overlaps the next frame's collection pass on the first stream
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream2;
+    NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_ready, 0));
+    if (f->busy_pending) NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_busy, 0));
     const size_t npix = static_cast<size_t>(f->W) * f->H, ns = npix * f->K;
     auto cp = [&](void* d, const DevBuf& b, size_t bytes) -> cudaError_t {
         if (!d || !bytes) return cudaSuccess;
@@ -692,6 +743,8 @@ int nx_frame_download(nx_ctx* c, const nx_frame* f, const nx_host_frame* dst, vo
     NX_CUDA(c, cp(dst->texture, f->texture, ns * 3 * sizeof(float)));
     NX_CUDA(c, cp(dst->final_img, f->final_img, npix * 3 * sizeof(float)));
     NX_CUDA(c, cp(dst->residual, f->residual, npix * sizeof(float)));
+    NX_CUDA(c, cudaEventRecord(f->ev_busy, s));
+    f->busy_pending = true;
     return NX_OK;
 }
 
@@ -746,15 +799,18 @@ int nx_collection_pass(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, n
 
 int nx_texturing_pass(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* f, void* stream) {
     if (!c || !f || !scene || !cam) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
-    return texturing(c, scene, cam, f, pick_stream(c, stream));
+    return texturing(c, scene, cam, f, stream ? static_cast<cudaStream_t>(stream) : c->stream2);
 }
 
+// With the context's own streams the texture pass runs on the second stream, so it
+// overlaps the next frame's binning and compositing (into another frame) on the
+// first; a frame's reuse and its downloads are ordered by its events.
 int nx_render(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* f, void* stream) {
     if (!c || !f) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
     cudaStream_t s = pick_stream(c, stream);
     int st = collection(c, scene, cam, f, s, nullptr, nullptr, 0, 0, 0);
     if (st) return st;
-    return texturing(c, scene, cam, f, s);
+    return texturing(c, scene, cam, f, stream ? s : c->stream2);
 }
 
 int nx_debug_tile_lists(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, int reference_lists,
