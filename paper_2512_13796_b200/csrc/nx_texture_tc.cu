@@ -22,6 +22,8 @@
 // SBO = 128*K/8 B (next 8-row group).
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "nx_internal.cuh"
 
 namespace nx {
@@ -442,7 +444,14 @@ int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(texture_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemUsed);
-    const int64_t grid = std::min<int64_t>(n_tiles, static_cast<int64_t>(kCtasPerSm) * sms);
+    // Persistent CTAs on every slot (measured best: 3/SM 273 FPS vs 2/SM 265 FPS at
+    // config 2, profiles/r01); NX_TEXTURE_CTAS_PER_SM overrides for experiments.
+    static const int per_sm = [] {
+        const char* e = getenv("NX_TEXTURE_CTAS_PER_SM");
+        const int v = e ? atoi(e) : kCtasPerSm;
+        return v < 1 ? 1 : (v > kCtasPerSm ? kCtasPerSm : v);
+    }();
+    const int64_t grid = std::min<int64_t>(n_tiles, static_cast<int64_t>(per_sm) * sms);
     count_launch();
     texture_tc_kernel<<<static_cast<unsigned>(grid), kTcThreads, kSmemUsed, s>>>(a, cst, bw, bh, tiles_x, n_tiles);
     return NX_OK;
