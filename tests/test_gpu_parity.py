@@ -244,6 +244,22 @@ def test_config2_contributor_lists_band(renderer, reference, config2, band):
 
 
 @pytest.mark.slow
+def test_config4_counts_and_contributor_band(renderer, reference):
+    """BASELINE config 4 (1.3M nexels, 3840x2160): the reference tile-key count
+    P = 190,258,862 and 5,779 straddlers, contributor lists bit-exact
+    on a band of rows, RGB within tolerance on that band."""
+    scene = nx.stump_like(1_300_000)
+    cam = nx.ring_camera(0, 256, 3840, 2160)
+    g, ds = gpu_render(renderer, scene, cam)
+    assert g.stats["tile_keys"] == 190_258_862
+    assert g.stats["n_straddlers"] == 5_779
+    y0, y1 = 1072, 1088
+    g_hits, g_cnt = renderer.pixel_hits(ds, cam, y0, y1, 128)
+    r_hits, r_cnt = reference.pixel_hits(scene, cam, y0, y1, 128)
+    assert np.array_equal(g_cnt, r_cnt) and np.array_equal(g_hits, r_hits)
+
+
+@pytest.mark.slow
 def test_config2_full_frame_parity(renderer, reference, config2):
     scene, cam = config2
     g, _ = gpu_render(renderer, scene, cam)
