@@ -90,13 +90,15 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
+// try_wait with a suspend-time hint: the warp sleeps until the phase completes (or
+// the hint expires) instead of spinning on issue slots other warps could use.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
-        "r"(parity)
+        "r"(parity), "r"(1000000u)
         : "memory");
 }
 
@@ -121,20 +123,19 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// Writes 8 consecutive K values (one 16-byte core-matrix row) as bf16 hi and lo parts.
+// Writes 8 consecutive K values (one 16-byte core-matrix row) as bf16 hi and lo parts:
+// one packed conversion per pair for hi, the hi values re-expanded by shifts (exact),
+// lo = x - hi, one packed conversion per pair for lo.
 __device__ __forceinline__ void store_split8(uint8_t* smem, int off_hi, int off_lo, uint32_t byte_off, const float* x) {
-    float hi[8], lo[8];
+    uint32_t h[4], l[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        hi[i] = __bfloat162float(__float2bfloat16_rn(x[i]));
-        lo[i] = x[i] - hi[i];
+    for (int i = 0; i < 4; ++i) {
+        h[i] = pack_bf16(x[2 * i], x[2 * i + 1]);
+        const float h0 = __uint_as_float(h[i] << 16), h1 = __uint_as_float(h[i] & 0xffff0000u);
+        l[i] = pack_bf16(x[2 * i] - h0, x[2 * i + 1] - h1);
     }
-    const uint4 h = make_uint4(pack_bf16(hi[0], hi[1]), pack_bf16(hi[2], hi[3]), pack_bf16(hi[4], hi[5]),
-                               pack_bf16(hi[6], hi[7]));
-    const uint4 l = make_uint4(pack_bf16(lo[0], lo[1]), pack_bf16(lo[2], lo[3]), pack_bf16(lo[4], lo[5]),
-                               pack_bf16(lo[6], lo[7]));
-    *reinterpret_cast<uint4*>(smem + off_hi + byte_off) = h;
-    *reinterpret_cast<uint4*>(smem + off_lo + byte_off) = l;
+    *reinterpret_cast<uint4*>(smem + off_hi + byte_off) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(smem + off_lo + byte_off) = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
 __device__ __forceinline__ uint32_t map_positive32(long long x) {  // hash_grid.hpp:12-14
@@ -149,6 +150,14 @@ struct LevelFetch {
     float fr0, fr1, fr2, dw;
 };
 
+// map_positive for |x| < 2^30: the 32-bit wrap of the reference's 64-bit value.
+__device__ __forceinline__ uint32_t map_positive_small(int x) {
+    return x > 0 ? (static_cast<uint32_t>(x) << 1) - 1u : static_cast<uint32_t>(-x) << 1;
+}
+
+// kSmall: every lattice coordinate of the query fits in 30 bits (checked per query),
+// so the cell index and hash run in 32-bit integers with identical results.
+template <bool kSmall>
 __device__ __forceinline__ LevelFetch fetch_level(int l, double x0, double x1, double x2, const TcConst& cst,
                                                   const float2* __restrict__ tab, uint32_t T, uint32_t mask, float ft,
                                                   int no_downweight) {
@@ -156,8 +165,6 @@ __device__ __forceinline__ LevelFetch fetch_level(int l, double x0, double x1, d
     const double s = cst.level_scale[l];
     const double p0 = s * x0, p1 = s * x1, p2 = s * x2;
     const double fl0 = floor(p0), fl1 = floor(p1), fl2 = floor(p2);
-    const long long b0 = static_cast<long long>(fl0), b1 = static_cast<long long>(fl1),
-                    b2 = static_cast<long long>(fl2);
     f.fr0 = static_cast<float>(p0 - fl0);
     f.fr1 = static_cast<float>(p1 - fl1);
     f.fr2 = static_cast<float>(p2 - fl2);
@@ -166,9 +173,25 @@ __device__ __forceinline__ LevelFetch fetch_level(int l, double x0, double x1, d
         const float r = ft * cst.inv_level_scale[l];
         f.dw = 1.0f - __expf(-r * r * 0.15915494309189535f);
     }
-    const uint32_t ax0 = map_positive32(b0), ax1 = map_positive32(b0 + 1);
-    const uint32_t by0 = map_positive32(b1) * 2654435761u, by1 = map_positive32(b1 + 1) * 2654435761u;
-    const uint32_t cz0 = map_positive32(b2) * 805459861u, cz1 = map_positive32(b2 + 1) * 805459861u;
+    uint32_t ax0, ax1, by0, by1, cz0, cz1;
+    if (kSmall) {
+        const int b0 = static_cast<int>(fl0), b1 = static_cast<int>(fl1), b2 = static_cast<int>(fl2);
+        ax0 = map_positive_small(b0);
+        ax1 = map_positive_small(b0 + 1);
+        by0 = map_positive_small(b1) * 2654435761u;
+        by1 = map_positive_small(b1 + 1) * 2654435761u;
+        cz0 = map_positive_small(b2) * 805459861u;
+        cz1 = map_positive_small(b2 + 1) * 805459861u;
+    } else {
+        const long long b0 = static_cast<long long>(fl0), b1 = static_cast<long long>(fl1),
+                        b2 = static_cast<long long>(fl2);
+        ax0 = map_positive32(b0);
+        ax1 = map_positive32(b0 + 1);
+        by0 = map_positive32(b1) * 2654435761u;
+        by1 = map_positive32(b1 + 1) * 2654435761u;
+        cz0 = map_positive32(b2) * 805459861u;
+        cz1 = map_positive32(b2 + 1) * 805459861u;
+    }
     const float2* slab = tab + static_cast<size_t>(l) * T;
 #pragma unroll
     for (int ci = 0; ci < 8; ++ci) {
@@ -282,17 +305,29 @@ __global__ void __launch_bounds__(kTcThreads, kCtasPerSm) texture_tc_kernel(cons
             const double x1 = a.cam.o[1] + t * dir[1];
             const double x2 = a.cam.o[2] + t * dir[2];
             const float ft = static_cast<float>(a.cam.fx / t);
-            // two-stage software pipeline: level l+1's 8 gathers are in flight while
-            // level l is interpolated
-            LevelFetch cur = fetch_level(0, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
+            const bool small = fmax(fabs(x0), fmax(fabs(x1), fabs(x2))) * cst.level_scale[kLevels - 1] < 1073741824.0;
+            if (small) {
+                // two-stage software pipeline: level l+1's 8 gathers are in flight while
+                // level l is interpolated
+                LevelFetch cur = fetch_level<true>(0, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
 #pragma unroll
-            for (int l = 0; l < kLevels; ++l) {
-                LevelFetch nxt;
-                if (l + 1 < kLevels) nxt = fetch_level(l + 1, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
-                const float2 g = interp(cur);
-                feats[2 * l] = g.x;
-                feats[2 * l + 1] = g.y;
-                if (l + 1 < kLevels) cur = nxt;
+                for (int l = 0; l < kLevels; ++l) {
+                    LevelFetch nxt;
+                    if (l + 1 < kLevels)
+                        nxt = fetch_level<true>(l + 1, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
+                    const float2 g = interp(cur);
+                    feats[2 * l] = g.x;
+                    feats[2 * l + 1] = g.y;
+                    if (l + 1 < kLevels) cur = nxt;
+                }
+            } else {  // far-away samples: 64-bit lattice coordinates (rare; not pipelined)
+#pragma unroll
+                for (int l = 0; l < kLevels; ++l) {
+                    const float2 g =
+                        interp(fetch_level<false>(l, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight));
+                    feats[2 * l] = g.x;
+                    feats[2 * l + 1] = g.y;
+                }
             }
         } else {
 #pragma unroll
