@@ -83,7 +83,8 @@ struct nx_ctx {
     DevBuf dbg_hits, dbg_counts;
     int32_t* h_pinned = nullptr;  // small readbacks
     bool profiling = false;
-    cudaStream_t stream2 = nullptr;  // texture pass + downloads: overlaps the next frame's collection
+    cudaStream_t stream2 = nullptr;  // texture passes: overlap the next frame's collection
+    cudaStream_t stream3 = nullptr;  // downloads: the copy engine overlaps both
     cudaEvent_t ev_join = nullptr;
     cudaEvent_t ev[kEvSets][kEvPoints] = {};
     int ev_cur = 0;
@@ -498,6 +499,7 @@ int nx_ctx_create(int device, nx_ctx** out) {
     c->device = device;
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaMallocHost(&c->h_pinned, 64 * sizeof(int32_t)) != cudaSuccess) {
         delete c;
@@ -514,6 +516,7 @@ void nx_ctx_destroy(nx_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     cudaStreamSynchronize(c->stream2);
+    cudaStreamSynchronize(c->stream3);
     for (DevBuf* b : {&c->rec, &c->recf, &c->cls, &c->ref_rect, &c->work_rect, &c->key, &c->flag, &c->pos, &c->skeys_a,
                       &c->skeys_b, &c->sids_a, &c->sids_b, &c->counts, &c->offsets, &c->tkeys_a, &c->tkeys_b,
                       &c->tvals_a, &c->tvals_b, &c->tile_counts, &c->scratch, &c->dbg_hits, &c->dbg_counts})
@@ -524,6 +527,7 @@ void nx_ctx_destroy(nx_ctx* c) {
     cudaEventDestroy(c->ev_join);
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->stream2);
+    cudaStreamDestroy(c->stream3);
     delete c;
 }
 
@@ -538,13 +542,16 @@ void* nx_ctx_stream(nx_ctx* c) { return c ? c->stream : nullptr; }
 int nx_ctx_synchronize(nx_ctx* c) {
     NX_CUDA(c, cudaStreamSynchronize(c->stream));
     NX_CUDA(c, cudaStreamSynchronize(c->stream2));
+    NX_CUDA(c, cudaStreamSynchronize(c->stream3));
     return NX_OK;
 }
 
 int nx_ctx_join(nx_ctx* c) {
     if (!c) return NX_INVALID_ARGUMENT;
-    NX_CUDA(c, cudaEventRecord(c->ev_join, c->stream2));
-    NX_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    for (cudaStream_t s2 : {c->stream2, c->stream3}) {
+        NX_CUDA(c, cudaEventRecord(c->ev_join, s2));
+        NX_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    }
     return NX_OK;
 }
 
@@ -726,9 +733,9 @@ int nx_frame_view_get(const nx_frame* f, nx_frame_view* v) {
 int nx_frame_download(nx_ctx* c, const nx_frame* fc, const nx_host_frame* dst, void* stream) {
     if (!c || !fc || !dst) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
     nx_frame* f = const_cast<nx_frame*>(fc);  // only the frame's ordering events change
-    // default: the second stream, after the frame's texture pass, so that the copy
-    // overlaps the next frame's collection pass on the first stream
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream2;
+    // default: the third (copy) stream, after the frame's texture pass, so that the
+    // copy overlaps the next frames' passes on the other two streams
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream3;
     NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_ready, 0));
     if (f->busy_pending) NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_busy, 0));
     const size_t npix = static_cast<size_t>(f->W) * f->H, ns = npix * f->K;
