@@ -1,17 +1,11 @@
-#!/usr/bin/env bash
-# Profiling recipe (run on the GPU box via gpurun; one GPU, never multi-rank):
-#   1. launch list of one bench step (cold-cache, serialised per-kernel times)
-#   2. one `ncu --set full` capture of each of the two dominant kernels
-# Outputs land in gpurun_out/; summaries are copied to profiles/ by hand.
-set -u
-OUT=${OUT:-gpurun_out}
-mkdir -p "$OUT"
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches.csv" \
-    python bench.py --steps 2 --warmup 1 --no-cpu-baseline > "$OUT/launches_bench.log" 2>&1
-ncu --set full --clock-control none --import-source on -k regex:composite_kernel -s 1 -c 1 \
-    -o "$OUT/prof_composite" python tools/prof_frame.py --frames 2 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:texture_tc_kernel -s 1 -c 1 \
-    -o "$OUT/prof_texture" python tools/prof_frame.py --frames 2 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:preprocess_kernel -s 1 -c 1 \
-    -o "$OUT/prof_preprocess" python tools/prof_frame.py --frames 2 > /dev/null 2>&1
-echo done
+#!/bin/bash
+# One `ncu --set full` capture per hot kernel (config 2, a warm view), for profiles/.
+# Usage (on the GPU box): bash tools/profile_round.sh [tag]
+mkdir -p gpurun_out
+TAG=${1:-cur}
+for K in composite_kernel texture_tc_kernel preprocess_kernel; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k "regex:$K" -s 3 -c 1 \
+     -o gpurun_out/ncu_${K}_${TAG} -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
+     > gpurun_out/ncu_${K}_${TAG}.log 2>&1
+  tail -2 gpurun_out/ncu_${K}_${TAG}.log
+done
