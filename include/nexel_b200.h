@@ -113,6 +113,8 @@ typedef struct nx_host_frame {
     float* texture;
     float* final_img;
     float* residual;
+    double* base_f64;  /* fp64 base (Eq. 6) kept for render_backward; download: copied if the
+                          frame keeps it (nx_frame_set_backward); upload: makes the frame keep it */
 } nx_host_frame;
 
 /* Per-frame binning / work statistics (read back with nx_frame_stats). */
@@ -200,11 +202,52 @@ int nx_texturing_pass(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam,
 int nx_render(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam, nx_frame* frame,
               void* stream);
 
+/* ---- render_backward (renderer.hpp:30-53, renderer.cpp:251-401) ------- */
+/* UpstreamGrads (renderer.hpp:40-44): fp64 arrays in the FrameBuffers layouts; any
+ * pointer may be NULL (treated as zero). */
+typedef struct nx_upstream {
+    const double* d_final;    /* H*W*3 */
+    const double* d_weights;  /* H*W*K */
+    const double* d_texture;  /* H*W*K*3 */
+} nx_upstream;
+
+/* SceneGrads (renderer.hpp:31-36) = PrimitiveGrad per nexel (primitive.hpp:53-62,
+ * 60 doubles in Nexel field order: mu, quat, log_scale, opacity_raw, gamma_raw, sh)
+ * + FieldGrads (texture_field.hpp:41-47: table [level][row][feature], w1, w2, w3).
+ * All fp64; render_backward ACCUMULATES into them (+=) like the reference. */
+typedef struct nx_grads {
+    double* prims;   /* N*60 */
+    double* table;   /* levels * 2^log2_table * features */
+    double* w1;      /* hidden * levels*features */
+    double* w2;      /* hidden * hidden */
+    double* w3;      /* 48 * hidden */
+} nx_grads;
+
+/* Makes collection passes into `frame` keep the fp64 base the reverse pass needs
+ * (3 doubles per pixel). Must be enabled before the forward that render_backward
+ * differentiates. */
+int nx_frame_set_backward(nx_ctx* ctx, nx_frame* frame, int enable);
+/* render_backward: re-bins the scene for `cam` (as renderer.cpp:257 does), runs the
+ * field branch (field_backward_batch, texture_field.cpp:77-146) at the buffered
+ * crossings and the reverse compositing march, and accumulates into `grads`.
+ * `frame` must be the unmodified forward output for scene/cam (with the backward
+ * state kept). err_pixel (H*W, nullable) accumulates sum w * err_pixel into
+ * blended_error (N, nullable) per primitive. Device pointers; asynchronous on
+ * `stream`. Top-K membership is constant, as in the reference. */
+int nx_render_backward(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam, nx_frame* frame,
+                       const nx_upstream* up, const nx_grads* grads, const double* err_pixel,
+                       double* blended_error, void* stream);
+/* Same with HOST arrays (copied in, accumulated, copied back; synchronous): the
+ * binding for the reference-typed nexel::render_backward shim. */
+int nx_render_backward_host(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam, nx_frame* frame,
+                            const nx_upstream* up, const nx_grads* grads, const double* err_pixel,
+                            double* blended_error);
+
 /* ---- parity / debug (not on the timed path) ---------------------------- */
 /* Tile lists for `cam`: reference_lists=1 materialises the reference's lists
  * (Binning::tile_lists, renderer.cpp:102-110, straddlers in every tile) on
  * settings.tile tiles; reference_lists=0 returns the work lists the composite
- * kernel walks (8x8-pixel tiles; *tiles_x/*tiles_y report the list geometry).
+ * kernel walks (8x8-pixel tiles; *tiles_x, *tiles_y report the list geometry).
  * offsets: n_tiles+1 host ints; ids: `capacity` host ints; *total = keys. */
 int nx_debug_tile_lists(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam,
                         int reference_lists, int64_t* offsets, int32_t* ids,

@@ -203,6 +203,7 @@ class Reference:
         L.ref_downweight.restype = C.c_double
         L.ref_downweight.argtypes = [C.c_double] * 3
         L.ref_field_forward.argtypes = [P, C.c_int64, PD, C.c_int, PD]
+        L.ref_render_backward.argtypes = [P, Cm, PD, PD, PD, PD, PD, PD, PD, PD, PD, PD]
         self._scene = None
         self._scene_key = None
 
@@ -271,6 +272,25 @@ class Reference:
         out = np.empty((q.shape[0], 3))
         self._check(self.lib.ref_field_forward(h, q.shape[0], _dp(q), int(no_downweight), _dp(out)))
         return out
+
+    def render_backward(self, scene: Scene, cam: Camera, d_final=None, d_weights=None, d_texture=None,
+                        err_pixel=None):
+        """render + render_backward of the reference (renderer.cpp:239-401) with the
+        given upstream gradients; returns (prims (N,60), table, w1, w2, w3, blended_error)."""
+        h = self._handle(scene)
+        c = cam.to_c()
+        f = scene.field
+        g = [np.zeros((scene.nexels.shape[0], 60)), np.zeros(f.grid.param_count()), np.zeros(np.size(f.w1)),
+             np.zeros(np.size(f.w2)), np.zeros(np.size(f.w3))]
+        be = np.zeros(scene.nexels.shape[0]) if err_pixel is not None else None
+
+        def opt(a):
+            return None if a is None else _dp(np.ascontiguousarray(a, np.float64))
+        keep = [np.ascontiguousarray(a, np.float64) if a is not None else None
+                for a in (d_final, d_weights, d_texture, err_pixel)]
+        self._check(self.lib.ref_render_backward(h, C.byref(c), *(opt(a) for a in keep), *(_dp(a) for a in g),
+                                                 _dp(be) if be is not None else None))
+        return (*g, be)
 
     # ---- the reference test generators (tests/helpers.hpp:88-125)
     def random_scene(self, seed: int, n_prims: int, top_k: int, res: int, focal: float, dist: float,

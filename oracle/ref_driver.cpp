@@ -349,4 +349,38 @@ int ref_field_forward(const ref_scene* h, int64_t n, const double* q8, int no_do
     });
 }
 
+// nexel::render + nexel::render_backward (renderer.cpp:239-401) with the given
+// upstream gradients (any NULL = zero, renderer.hpp:40-44). Gradients of a fresh
+// SceneGrads are written to g_* (PrimitiveGrad = 60 doubles per nexel in Nexel
+// field order); blended_error (N, nullable) receives sum w * err_pixel.
+int ref_render_backward(const ref_scene* h, const nx_camera* c, const double* d_final,
+                        const double* d_weights, const double* d_texture, const double* err_pixel,
+                        double* g_prims, double* g_table, double* g_w1, double* g_w2, double* g_w3,
+                        double* blended_error) {
+    return guarded([&] {
+        const Scene& scene = h->scene;
+        const Camera cam = to_camera(*c);
+        RenderResult rr = render(scene, cam);
+        SceneGrads grads;
+        grads.allocate(scene);
+        UpstreamGrads up;
+        up.d_final = d_final;
+        up.d_weights = d_weights;
+        up.d_texture = d_texture;
+        render_backward(scene, cam, rr.fb, up, grads, err_pixel,
+                        blended_error ? &rr.blended_error : nullptr);
+        static_assert(sizeof(PrimitiveGrad) == NX_PARAMS_PER_NEXEL * sizeof(double), "60 doubles");
+        if (g_prims && !grads.prims.empty())
+            std::memcpy(g_prims, grads.prims.data(), grads.prims.size() * sizeof(PrimitiveGrad));
+        auto put = [](double* dst, const std::vector<double>& v) {
+            if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(double));
+        };
+        put(g_table, grads.field.table);
+        put(g_w1, grads.field.w1);
+        put(g_w2, grads.field.w2);
+        put(g_w3, grads.field.w3);
+        if (blended_error) put(blended_error, rr.blended_error);
+    });
+}
+
 }  // extern "C"

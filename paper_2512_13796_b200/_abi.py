@@ -105,6 +105,25 @@ class nx_host_frame(C.Structure):
         ("texture", C.c_void_p),
         ("final_img", C.c_void_p),
         ("residual", C.c_void_p),
+        ("base_f64", C.c_void_p),
+    ]
+
+
+class nx_upstream(C.Structure):
+    _fields_ = [
+        ("d_final", C.c_void_p),
+        ("d_weights", C.c_void_p),
+        ("d_texture", C.c_void_p),
+    ]
+
+
+class nx_grads(C.Structure):
+    _fields_ = [
+        ("prims", C.c_void_p),
+        ("table", C.c_void_p),
+        ("w1", C.c_void_p),
+        ("w2", C.c_void_p),
+        ("w3", C.c_void_p),
     ]
 
 
@@ -165,6 +184,11 @@ SIGNATURES = [
     ("nx_collection_pass", C.c_int, [P, P, C.POINTER(nx_camera), P, P]),
     ("nx_texturing_pass", C.c_int, [P, P, C.POINTER(nx_camera), P, P]),
     ("nx_render", C.c_int, [P, P, C.POINTER(nx_camera), P, P]),
+    ("nx_frame_set_backward", C.c_int, [P, P, C.c_int]),
+    ("nx_render_backward", C.c_int,
+     [P, P, C.POINTER(nx_camera), P, C.POINTER(nx_upstream), C.POINTER(nx_grads), P, P, P]),
+    ("nx_render_backward_host", C.c_int,
+     [P, P, C.POINTER(nx_camera), P, C.POINTER(nx_upstream), C.POINTER(nx_grads), PD, PD]),
     ("nx_debug_tile_lists", C.c_int,
      [P, P, C.POINTER(nx_camera), C.c_int, PI64, PI32, I64, PI64, PI32, PI32]),
     ("nx_debug_pixel_hits", C.c_int, [P, P, C.POINTER(nx_camera), C.c_int, C.c_int, C.c_int, PI32, PI32]),

@@ -202,8 +202,45 @@ class RenderResult:
     blended_error: np.ndarray
 
 
+@dataclasses.dataclass
+class UpstreamGrads:
+    """UpstreamGrads (renderer.hpp:40-44): fp64 arrays in the FrameBuffers layouts
+    (d_final H*W*3, d_weights H*W*K, d_texture H*W*K*3); None = zero."""
+    d_final: Optional[np.ndarray] = None
+    d_weights: Optional[np.ndarray] = None
+    d_texture: Optional[np.ndarray] = None
+
+
+@dataclasses.dataclass
+class SceneGrads:
+    """SceneGrads (renderer.hpp:31-36): ``prims`` (N, 60) PrimitiveGrad in Nexel field
+    order (primitive.hpp:53-62) + FieldGrads (texture_field.hpp:41-47)."""
+    prims: np.ndarray
+    table: np.ndarray
+    w1: np.ndarray
+    w2: np.ndarray
+    w3: np.ndarray
+
+    @classmethod
+    def allocate(cls, scene: "Scene") -> "SceneGrads":
+        """SceneGrads::allocate (renderer.cpp:245-248): zeros shaped like the scene."""
+        f = scene.field
+        return cls(np.zeros((scene.nexels.shape[0], _abi.NX_PARAMS_PER_NEXEL)), np.zeros(f.grid.param_count()),
+                   np.zeros(np.size(f.w1)), np.zeros(np.size(f.w2)), np.zeros(np.size(f.w3)))
+
+
 def _dp(a: np.ndarray):
     return a.ctypes.data_as(_abi.PD)
+
+
+def _f64(a, n: int, what: str):
+    """Contiguous fp64 view of an optional host array of n values."""
+    if a is None:
+        return None
+    a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+    if a.size != n:
+        raise NexelError("invalid-argument", f"{what}: expected {n} values, got {a.size}")
+    return a
 
 
 class DeviceScene:
@@ -237,6 +274,44 @@ class DeviceFrame:
         v = _abi.nx_frame_view()
         self.renderer.lib.nx_frame_view_get(self.handle, C.byref(v))
         return v
+
+    def set_backward(self, enable: bool = True):
+        """Keep the fp64 base the reverse pass needs (nx_frame_set_backward)."""
+        r = self.renderer
+        r._check(r.lib.nx_frame_set_backward(r.ctx, self.handle, int(enable)))
+
+    def base_f64(self) -> np.ndarray:
+        """The fp64 base (Eq. 6) kept for render_backward."""
+        v = self.view()
+        out = np.empty(v.width * v.height * 3, np.float64)
+        hf = _abi.nx_host_frame()
+        hf.base_f64 = out.ctypes.data
+        r = self.renderer
+        r._check(r.lib.nx_frame_download(r.ctx, self.handle, C.byref(hf), None))
+        r._check(r.lib.nx_ctx_synchronize(r.ctx))
+        return out
+
+    def upload(self, fb: "FrameBuffers"):
+        """Host FrameBuffers (e.g. from ``render``) -> this device frame, fp64 base kept."""
+        npix = fb.width * fb.height
+        arrs = {
+            "base": np.ascontiguousarray(fb.base, np.float32).reshape(-1),
+            "ids": np.ascontiguousarray(fb.ids, np.int32).reshape(-1),
+            "depths": np.ascontiguousarray(fb.depths, np.float64).reshape(-1),
+            "weights": np.ascontiguousarray(fb.weights, np.float64).reshape(-1),
+            "texture": np.ascontiguousarray(fb.texture, np.float32).reshape(-1),
+            "final_img": np.ascontiguousarray(fb.final_img, np.float32).reshape(-1),
+            "residual": np.ascontiguousarray(fb.residual, np.float32).reshape(-1),
+            "base_f64": np.ascontiguousarray(fb.base, np.float64).reshape(-1),
+        }
+        if arrs["base"].size != npix * 3 or arrs["ids"].size != npix * fb.top_k:
+            raise NexelError("invalid-argument", "FrameBuffers arrays do not match their shape")
+        hf = _abi.nx_host_frame()
+        for k, a in arrs.items():
+            setattr(hf, k, a.ctypes.data)
+        r = self.renderer
+        r._check(r.lib.nx_frame_upload(r.ctx, self.handle, fb.width, fb.height, fb.top_k, C.byref(hf), None))
+        r._check(r.lib.nx_ctx_synchronize(r.ctx))
 
     def stats(self) -> dict:
         st = _abi.nx_frame_stats()
@@ -334,6 +409,36 @@ class Renderer:
         c = cam.to_c()
         self._check(self.lib.nx_render(self.ctx, dscene.handle, C.byref(c), frame.handle, stream or None))
 
+    def render_backward(self, dscene: DeviceScene, cam: Camera, frame: DeviceFrame, up: UpstreamGrads,
+                        grads: SceneGrads, err_pixel: Optional[np.ndarray] = None,
+                        blended_error: Optional[np.ndarray] = None):
+        """render_backward (renderer.hpp:50-53) on host arrays: ACCUMULATES into
+        ``grads`` (and ``blended_error`` when ``err_pixel`` is given). ``frame`` must
+        hold the forward of ``cam`` rendered with ``frame.set_backward()`` enabled."""
+        v = frame.view()
+        npix, K = cam.width * cam.height, v.top_k
+        d_final = _f64(up.d_final, npix * 3, "d_final")
+        d_weights = _f64(up.d_weights, npix * K, "d_weights") if K else None
+        d_texture = _f64(up.d_texture, npix * K * 3, "d_texture") if K else None
+        u = _abi.nx_upstream()
+        u.d_final = d_final.ctypes.data if d_final is not None else None
+        u.d_weights = d_weights.ctypes.data if d_weights is not None else None
+        u.d_texture = d_texture.ctypes.data if d_texture is not None else None
+        arrs = [grads.prims, grads.table, grads.w1, grads.w2, grads.w3]
+        for a in arrs:
+            if a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise NexelError("invalid-argument", "SceneGrads arrays must be C-contiguous float64")
+        g = _abi.nx_grads()
+        g.prims, g.table, g.w1, g.w2, g.w3 = (a.ctypes.data for a in arrs)
+        err = _f64(err_pixel, npix, "err_pixel")
+        if blended_error is not None and (blended_error.dtype != np.float64 or not blended_error.flags.c_contiguous):
+            raise NexelError("invalid-argument", "blended_error must be C-contiguous float64")
+        c = cam.to_c()
+        self._check(self.lib.nx_render_backward_host(
+            self.ctx, dscene.handle, C.byref(c), frame.handle, C.byref(u), C.byref(g),
+            _dp(err) if err is not None else None,
+            _dp(blended_error) if (blended_error is not None and err is not None) else None))
+
     def synchronize(self):
         self._check(self.lib.nx_ctx_synchronize(self.ctx))
 
@@ -398,6 +503,14 @@ def _device_scene(r: Renderer, scene: Scene) -> DeviceScene:
     return ds
 
 
+def _value_frame(r: Renderer, device: int) -> DeviceFrame:
+    fr = _default.get(("frame", device))
+    if fr is None:
+        fr = _default[("frame", device)] = r.frame()
+        fr.set_backward(True)  # render_backward needs the fp64 base of the forward
+    return fr
+
+
 def _to_host_fb(fb: FrameBuffers) -> FrameBuffers:
     """Device-native dtypes -> the reference's fp64 FrameBuffers."""
     return FrameBuffers(fb.width, fb.height, fb.top_k, fb.base.astype(np.float64), fb.ids.copy(),
@@ -409,9 +522,10 @@ def collection_pass(scene: Scene, cam: Camera, out: RenderResult, device: int = 
     """collection_pass (renderer.hpp:22): fills base/ids/depths/weights/residual."""
     r = _renderer(device)
     ds = _device_scene(r, scene)
-    fr = _default.setdefault(("frame", device), r.frame())
+    fr = _value_frame(r, device)
     r.collection_pass(ds, cam, fr)
     fb = _to_host_fb(fr.download(["base", "ids", "depths", "weights", "residual"]))
+    fb.base = fr.base_f64()
     npix = cam.width * cam.height
     fb.texture = np.zeros(npix * scene.settings.top_k * 3)
     fb.final_img = np.zeros(npix * 3)
@@ -423,7 +537,7 @@ def texturing_pass(scene: Scene, cam: Camera, fb: FrameBuffers, device: int = 0)
     """texturing_pass (renderer.hpp:26): consumes fb's ids/depths/weights/base."""
     r = _renderer(device)
     ds = _device_scene(r, scene)
-    fr = _default.setdefault(("frame", device), r.frame())
+    fr = _value_frame(r, device)
     v = fr.view()
     if (v.width, v.height, v.top_k) != (fb.width, fb.height, fb.top_k):
         raise NexelError("invalid-argument", "FrameBuffers do not come from collection_pass on this camera")
@@ -437,10 +551,24 @@ def render(scene: Scene, cam: Camera, device: int = 0) -> RenderResult:
     """render (renderer.hpp:28) = collection_pass + texturing_pass."""
     r = _renderer(device)
     ds = _device_scene(r, scene)
-    fr = _default.setdefault(("frame", device), r.frame())
+    fr = _value_frame(r, device)
     r.render(ds, cam, fr)
     fb = _to_host_fb(fr.download())
+    fb.base = fr.base_f64()  # the reference's base is fp64; the device kept it for the reverse pass
     return RenderResult(fb, np.zeros(scene.nexels.shape[0]))
+
+
+def render_backward(scene: Scene, cam: Camera, fb: FrameBuffers, up: UpstreamGrads, grads: SceneGrads,
+                    err_pixel: Optional[np.ndarray] = None, blended_error: Optional[np.ndarray] = None,
+                    device: int = 0) -> None:
+    """render_backward (renderer.hpp:50-53): ``fb`` is the unmodified output of
+    ``render(scene, cam)``; accumulates into ``grads`` (and into ``blended_error``
+    when ``err_pixel`` is given). Top-K membership is treated as constant."""
+    r = _renderer(device)
+    ds = _device_scene(r, scene)
+    fr = _value_frame(r, device)
+    fr.upload(fb)
+    r.render_backward(ds, cam, fr, up, grads, err_pixel, blended_error)
 
 
 # ---------------------------------------------------------------- synthetic inputs (SURVEY.md §8(d))

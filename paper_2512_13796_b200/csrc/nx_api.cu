@@ -81,6 +81,10 @@ struct nx_ctx {
     DevBuf skeys_a, skeys_b, sids_a, sids_b, counts, offsets;
     DevBuf tkeys_a, tkeys_b, tvals_a, tvals_b, tile_counts, scratch;
     DevBuf dbg_hits, dbg_counts;
+    // render_backward scratch
+    nx_frame* bwd_lists = nullptr;   // work lists of the re-binned camera
+    DevBuf d_t_slot, act_grad;
+    DevBuf h_up[3], h_err, h_blend, h_grads[5];  // device copies for nx_render_backward_host
     int32_t* h_pinned = nullptr;  // small readbacks
     bool profiling = false;
     cudaStream_t stream2 = nullptr;  // texture passes: overlap the next frame's collection
@@ -108,6 +112,9 @@ struct nx_frame {
     int W = 0, H = 0, K = 0, tiles_x = 0, tiles_y = 0;  // reference tiles (settings.tile)
     int list_tile = kWorkTile, ltiles_x = 0, ltiles_y = 0;  // tiles of the last built lists
     DevBuf base, ids, depths, weights, texture, final_img, residual;
+    DevBuf base64;               // fp64 base kept for render_backward
+    bool keep_backward = false;  // collection passes write base64
+    bool base64_valid = false;   // base64 holds the last forward's (or an uploaded) base
     DevBuf tile_offsets;  // n_tiles + 1 (the work lists' ranges of the last collection pass)
     DevBuf list_ids;
     FrameStatsD* stats = nullptr;  // device
@@ -211,6 +218,7 @@ int frame_shape(nx_ctx* c, nx_frame* f, int W, int H, int K, int tile) {
     NX_CUDA(c, f->depths.ensure(ns * sizeof(double)));
     NX_CUDA(c, f->weights.ensure(ns * sizeof(double)));
     NX_CUDA(c, f->texture.ensure(ns * 3 * sizeof(float)));
+    if (f->keep_backward) NX_CUDA(c, f->base64.ensure(npix * 3 * sizeof(double)));
     f->W = W;
     f->H = H;
     f->K = K;
@@ -233,6 +241,7 @@ FrameDev frame_dev(const nx_frame* f) {
     d.texture = f->texture.as<float>();
     d.final_img = f->final_img.as<float>();
     d.residual = f->residual.as<float>();
+    d.base64 = f->keep_backward ? f->base64.as<double>() : nullptr;
     return d;
 }
 
@@ -429,6 +438,7 @@ int collection(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame*
     ca.dbg_y1 = dbg_y1;
     ca.dbg_max = dbg_max;
     launch_composite(ca, s);
+    f->base64_valid = f->keep_backward;
     record(c, kEvCompEnd, s);
     NX_CUDA(c, cudaEventRecord(f->ev_ready, s));
     NX_CUDA(c, cudaGetLastError());
@@ -521,6 +531,10 @@ void nx_ctx_destroy(nx_ctx* c) {
                       &c->skeys_b, &c->sids_a, &c->sids_b, &c->counts, &c->offsets, &c->tkeys_a, &c->tkeys_b,
                       &c->tvals_a, &c->tvals_b, &c->tile_counts, &c->scratch, &c->dbg_hits, &c->dbg_counts})
         b->release();
+    for (DevBuf* b : {&c->d_t_slot, &c->act_grad, &c->h_err, &c->h_blend}) b->release();
+    for (DevBuf& b : c->h_up) b.release();
+    for (DevBuf& b : c->h_grads) b.release();
+    if (c->bwd_lists) nx_frame_destroy(c->bwd_lists);
     for (auto& set : c->ev)
         for (auto& e : set) cudaEventDestroy(e);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
@@ -704,7 +718,7 @@ void nx_frame_destroy(nx_frame* f) {
     if (!f) return;
     if (f->ctx) cudaSetDevice(f->ctx->device);
     for (DevBuf* b : {&f->base, &f->ids, &f->depths, &f->weights, &f->texture, &f->final_img, &f->residual,
-                      &f->tile_offsets})
+                      &f->tile_offsets, &f->base64})
         b->release();
     if (f->ev_busy) cudaEventSynchronize(f->ev_busy);
     if (f->stats) cudaFree(f->stats);
@@ -750,6 +764,7 @@ int nx_frame_download(nx_ctx* c, const nx_frame* fc, const nx_host_frame* dst, v
     NX_CUDA(c, cp(dst->texture, f->texture, ns * 3 * sizeof(float)));
     NX_CUDA(c, cp(dst->final_img, f->final_img, npix * 3 * sizeof(float)));
     NX_CUDA(c, cp(dst->residual, f->residual, npix * sizeof(float)));
+    if (dst->base_f64 && f->base64_valid) NX_CUDA(c, cp(dst->base_f64, f->base64, npix * 3 * sizeof(double)));
     NX_CUDA(c, cudaEventRecord(f->ev_busy, s));
     f->busy_pending = true;
     return NX_OK;
@@ -760,6 +775,7 @@ int nx_frame_upload(nx_ctx* c, nx_frame* f, int width, int height, int top_k, co
     if (!c || !f || !src || width < 0 || height < 0 || top_k < 0 || top_k > NX_MAX_TOP_K)
         return set_err(c, NX_INVALID_ARGUMENT, "bad frame upload");
     cudaSetDevice(c->device);
+    if (src->base_f64) f->keep_backward = true;
     int st = frame_shape(c, f, width, height, top_k, 16);  // tiles are re-derived by collection_pass
     if (st) return st;
     cudaStream_t s = pick_stream(c, stream);
@@ -775,6 +791,10 @@ int nx_frame_upload(nx_ctx* c, nx_frame* f, int width, int height, int top_k, co
     NX_CUDA(c, cp(f->texture, src->texture, ns * 3 * sizeof(float)));
     NX_CUDA(c, cp(f->final_img, src->final_img, npix * 3 * sizeof(float)));
     NX_CUDA(c, cp(f->residual, src->residual, npix * sizeof(float)));
+    if (src->base_f64) {
+        NX_CUDA(c, cp(f->base64, src->base_f64, npix * 3 * sizeof(double)));
+        f->base64_valid = true;
+    }
     return NX_OK;
 }
 
@@ -818,6 +838,158 @@ int nx_render(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* 
     int st = collection(c, scene, cam, f, s, nullptr, nullptr, 0, 0, 0);
     if (st) return st;
     return texturing(c, scene, cam, f, stream ? s : c->stream2);
+}
+
+int nx_frame_set_backward(nx_ctx* c, nx_frame* f, int enable) {
+    if (!c || !f) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    f->keep_backward = enable != 0;
+    if (!f->keep_backward) {
+        f->base64.release();
+        f->base64_valid = false;
+        return NX_OK;
+    }
+    NX_CUDA(c, f->base64.ensure(std::max<size_t>(static_cast<size_t>(f->W) * f->H * 3, 1) * sizeof(double)));
+    return NX_OK;
+}
+
+// render_backward (renderer.cpp:251-401): field branch, then the reverse march of
+// the compositing branch, then activation_backward per primitive.
+int nx_render_backward(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* f, const nx_upstream* up,
+                       const nx_grads* g, const double* err_pixel, double* blended_error, void* stream) {
+    if (!c || !f || !up || !g) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    int st;
+    if ((st = check_inputs(c, scene, cam))) return st;
+    if (!g->prims || !g->table || !g->w1 || !g->w2 || !g->w3)
+        return set_err(c, NX_INVALID_ARGUMENT, "render_backward: every gradient array is required");
+    if (f->W != cam->width || f->H != cam->height || f->K != scene->st.top_k)
+        return set_err(c, NX_INVALID_ARGUMENT, "render_backward: the frame is not the forward output for this camera");
+    if (!f->base64_valid)
+        return set_err(c, NX_INVALID_ARGUMENT,
+                       "render_backward: the frame did not keep the backward state (nx_frame_set_backward before "
+                       "collection_pass)");
+    cudaSetDevice(c->device);
+    cudaStream_t s = pick_stream(c, stream);
+    NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_ready, 0));
+    if (f->busy_pending) NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_busy, 0));
+    if (!c->bwd_lists) {
+        if ((st = nx_frame_create(c, 0, 0, 0, &c->bwd_lists))) return st;
+    }
+    nx_frame* lf = c->bwd_lists;
+    lf->tiles_x = (cam->width + scene->st.tile - 1) / scene->st.tile;  // reference tiles (stats only)
+    lf->tiles_y = (cam->height + scene->st.tile - 1) / scene->st.tile;
+    int64_t total = 0;
+    const bool prof = c->profiling;
+    c->profiling = false;  // the stage events describe forward frames only
+    st = build_lists(c, scene, *cam, lf, 0, s, &total);
+    c->profiling = prof;
+    if (st) return st;
+
+    const int64_t n = scene->n, npix = static_cast<int64_t>(f->W) * f->H, ns = npix * f->K;
+    NX_CUDA(c, c->d_t_slot.ensure(std::max<int64_t>(ns, 1) * sizeof(double)));
+    NX_CUDA(c, c->act_grad.ensure(std::max<int64_t>(n, 1) * kActFields * sizeof(double)));
+    NX_CUDA(c, cudaMemsetAsync(c->act_grad.p, 0, std::max<int64_t>(n, 1) * kActFields * sizeof(double), s));
+    FrameDev fd = frame_dev(f);
+    fd.tiles_x = lf->ltiles_x;
+    fd.tiles_y = lf->ltiles_y;
+    const CamD cd = make_cam(*cam);
+    if (f->K > 0) {
+        if (up->d_final || up->d_texture) {
+            FieldBwdArgs fa;
+            fa.scene = scene_dev(scene);
+            fa.st = scene->st;
+            fa.cam = cd;
+            fa.fb = fd;
+            fa.d_final = up->d_final;
+            fa.d_texture = up->d_texture;
+            fa.d_t_slot = c->d_t_slot.as<double>();
+            fa.g_table = g->table;
+            fa.g_w1 = g->w1;
+            fa.g_w2 = g->w2;
+            fa.g_w3 = g->w3;
+            if ((st = launch_field_backward(fa, s)))
+                return set_err(c, st, "texture field shape not supported by render_backward");
+        } else {
+            NX_CUDA(c, cudaMemsetAsync(c->d_t_slot.p, 0, ns * sizeof(double), s));
+        }
+    }
+    CompositeBwdArgs ca;
+    ca.rec = c->rec.as<double>();
+    ca.recf = c->recf.as<float4>();
+    ca.n = std::max<int64_t>(n, 1);
+    ca.sh = scene->sh.as<float>();
+    ca.list_ids = lf->list_ids.as<int32_t>();
+    ca.tile_offsets = lf->tile_offsets.as<int32_t>();
+    ca.st = scene->st;
+    ca.cam = cd;
+    ca.fb = fd;
+    ca.sh_degree = scene->st.no_prim_sh ? 0 : 3;
+    ca.d_final = up->d_final;
+    ca.d_weights = f->K > 0 ? up->d_weights : nullptr;
+    ca.d_t_slot = c->d_t_slot.as<double>();
+    ca.err_pixel = blended_error ? err_pixel : nullptr;
+    ca.act_grad = c->act_grad.as<double>();
+    ca.prim_grad = g->prims;
+    launch_composite_backward(ca, s);
+    launch_prim_finalize(scene_dev(scene), scene->st.no_gamma, c->act_grad.as<double>(), g->prims,
+                         err_pixel ? blended_error : nullptr, s);
+    NX_CUDA(c, cudaEventRecord(f->ev_busy, s));
+    f->busy_pending = true;
+    NX_CUDA(c, cudaGetLastError());
+    return NX_OK;
+}
+
+int nx_render_backward_host(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* f,
+                            const nx_upstream* up, const nx_grads* g, const double* err_pixel,
+                            double* blended_error) {
+    if (!c || !f || !up || !g || !scene || !cam) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    int st;
+    if ((st = check_inputs(c, scene, cam))) return st;
+    cudaSetDevice(c->device);
+    cudaStream_t s = c->stream;
+    const size_t npix = static_cast<size_t>(cam->width) * cam->height, K = scene->st.top_k;
+    const size_t n = static_cast<size_t>(scene->n);
+    const nx_field_desc& fd = scene->field;
+    const size_t nin = static_cast<size_t>(fd.levels) * fd.features, nh = fd.n_hidden;
+    const size_t g_sizes[5] = {n * NX_PARAMS_PER_NEXEL,
+                               static_cast<size_t>(fd.levels) * (size_t(1) << fd.log2_table) * fd.features,
+                               nh * nin, nh * nh, NX_SH_VALUES * nh};
+    double* g_host[5] = {g->prims, g->table, g->w1, g->w2, g->w3};
+    for (double* p : g_host)
+        if (!p) return set_err(c, NX_INVALID_ARGUMENT, "render_backward: every gradient array is required");
+    nx_grads gd;
+    double** g_dev[5] = {&gd.prims, &gd.table, &gd.w1, &gd.w2, &gd.w3};
+    for (int i = 0; i < 5; ++i) {
+        NX_CUDA(c, c->h_grads[i].ensure(std::max<size_t>(g_sizes[i], 1) * sizeof(double)));
+        *g_dev[i] = c->h_grads[i].as<double>();
+        NX_CUDA(c, cudaMemcpyAsync(*g_dev[i], g_host[i], g_sizes[i] * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    const double* u_host[3] = {up->d_final, up->d_weights, up->d_texture};
+    const size_t u_sizes[3] = {npix * 3, npix * K, npix * K * 3};
+    const double* u_dev[3] = {nullptr, nullptr, nullptr};
+    for (int i = 0; i < 3; ++i) {
+        if (!u_host[i] || !u_sizes[i]) continue;
+        NX_CUDA(c, c->h_up[i].ensure(u_sizes[i] * sizeof(double)));
+        NX_CUDA(c, cudaMemcpyAsync(c->h_up[i].p, u_host[i], u_sizes[i] * sizeof(double), cudaMemcpyHostToDevice, s));
+        u_dev[i] = c->h_up[i].as<double>();
+    }
+    nx_upstream ud{u_dev[0], u_dev[1], u_dev[2]};
+    double* err_dev = nullptr;
+    double* blend_dev = nullptr;
+    if (err_pixel && blended_error) {
+        NX_CUDA(c, c->h_err.ensure(std::max<size_t>(npix, 1) * sizeof(double)));
+        NX_CUDA(c, cudaMemcpyAsync(c->h_err.p, err_pixel, npix * sizeof(double), cudaMemcpyHostToDevice, s));
+        NX_CUDA(c, c->h_blend.ensure(std::max<size_t>(n, 1) * sizeof(double)));
+        NX_CUDA(c, cudaMemcpyAsync(c->h_blend.p, blended_error, n * sizeof(double), cudaMemcpyHostToDevice, s));
+        err_dev = c->h_err.as<double>();
+        blend_dev = c->h_blend.as<double>();
+    }
+    if ((st = nx_render_backward(c, scene, cam, f, &ud, &gd, err_dev, blend_dev, s))) return st;
+    for (int i = 0; i < 5; ++i)
+        NX_CUDA(c, cudaMemcpyAsync(g_host[i], *g_dev[i], g_sizes[i] * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (blend_dev)
+        NX_CUDA(c, cudaMemcpyAsync(blended_error, blend_dev, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    NX_CUDA(c, cudaStreamSynchronize(s));
+    return NX_OK;
 }
 
 int nx_debug_tile_lists(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, int reference_lists,

@@ -1,0 +1,483 @@
+// render_backward (renderer.cpp:251-401) on sm_100a: the compositing branch and
+// the per-primitive activation backward. The field branch (field_backward_batch)
+// lives in nx_field_backward.cu / nx_field_backward_tc.cu.
+//
+// Compositing branch (renderer.cpp:287-390). The reference re-marches every pixel
+// of every tile front to back, then walks the hits back to front with the suffix
+// accumulator A (dL/dw_j * w_j summed behind hit j, seeded by the background
+// term). Here one thread per pixel walks the same work lists as the forward
+// composite (identical hit sequences: the lists are order-preserving subsequences
+// that drop only provable misses) ONCE, front to back, using
+//     A_total = dot(dL/dfinal, base) + sum_j dL/dw_j * w_j   (buffered slots j)
+// — the fp64 base the forward kept (Eq. 6: the unbuffered colours plus the
+// background behind the terminal transmittance) — so that A before hit i is
+// A_total minus the running prefix of dL/dw * w. Everything on the geometric
+// chain is fp64 with the reference's formulas: eval_kernel_grad (kernel.hpp:
+// 40-68), intersect_backward (intersect.hpp:56-87); SH gradients (eval_sh_backward,
+// sh.hpp:76-83) are formed in fp32 and accumulated in fp64.
+//
+// Per group of primitives a warp (8x4 pixels) pools its survivors like the
+// forward (B1: exact fp64 intersect, all lanes busy), composites them per pixel
+// in list order (B2: weights, d_alpha, d_t), then reduces each primitive's
+// per-pixel gradients across the warp (B3: butterfly, or direct when at most two
+// lanes hit it) into per-primitive fp64 accumulators. Those hold the activated
+// gradient (17 values, ActivatedGrad intersect.hpp:45-51) + blended error; the
+// SH gradients go straight into the PrimitiveGrad array. activation_backward
+// (intersect.hpp:91-103) is linear in the activated gradient, so a final
+// per-primitive kernel applies it once to the sum.
+#include "nx_composite.cuh"
+
+namespace nx {
+
+namespace {
+
+constexpr int kThreads = kWorkTile * kWorkTile;  // 64: one thread per pixel of the 8x8 work tile
+constexpr int kWarps = kThreads / 32;
+constexpr int kChunk = 128;
+constexpr int kSub = 8;
+constexpr int kPool = 32 * kSub;
+constexpr int kRecPairs = REC_FIELDS / 2;
+
+struct BwdEntry {       // one evaluated (pixel, primitive) pair
+    double alpha;       // B1: raw kernel alpha (< 0: miss). B2: d_alpha, or NaN-free flag via `hit`
+    double t, u, v;     // B1: crossing and plane coordinates
+    double d_t;         // B2: upstream dL/dt (field branch) of a buffered hit
+    double werr;        // B2: w * err_pixel
+    float rgb[3];       // B1: primitive colour; B2: w * dL/dfinal * clamp mask (unbuffered), else 0
+    uint32_t flags;     // bit 0..2: SH clamp mask (B1); bit 3: composited (B2)
+};
+
+struct SmemLayout {
+    float4 f[kChunk][4];
+    int32_t id[kChunk];
+    double dir[kThreads][3];
+    uint16_t q[kWarps][kPool];
+    BwdEntry res[kWarps][kPool];
+};
+
+__device__ __forceinline__ double shfl_xor_d(double v, int m) {
+    return __hiloint2double(__shfl_xor_sync(0xffffffffu, __double2hiint(v), m),
+                            __shfl_xor_sync(0xffffffffu, __double2loint(v), m));
+}
+
+// eval_kernel_grad (kernel.hpp:40-68) + intersect_backward (intersect.hpp:56-87):
+// the activated-space gradient of one hit, g[0..16] = d_mu[3], d_R[9] (m[i][j]),
+// d_sigma[2], d_opacity, d_gamma[2].
+__device__ __forceinline__ void hit_backward(const double* r, const double* d, const double* o, double t, double u,
+                                             double v, double d_alpha, double d_t, double* g) {
+    const double op = r[REC_OP], gx = r[REC_GX], gy = r[REC_GY], sx = r[REC_SX], sy = r[REC_SY];
+    const double pu = axis_power(u, gx), pv = axis_power(v, gy);
+    double kd_u = 0.0, kd_v = 0.0, kd_op = 0.0, kd_gx = 0.0, kd_gy = 0.0;
+    if (!(isinf(pu) || isinf(pv))) {
+        const double k = exp(-0.5 * (pu + pv));
+        const double alpha = op * k;
+        kd_op = k;
+        if (u != 0.0) {
+            const double au = fabs(u);
+            kd_u = -alpha * gx * (pu / au) * (u > 0 ? 1.0 : -1.0);
+            kd_gx = -alpha * log(au) * pu;
+        }
+        if (v != 0.0) {
+            const double av = fabs(v);
+            kd_v = -alpha * gy * (pv / av) * (v > 0 ? 1.0 : -1.0);
+            kd_gy = -alpha * log(av) * pv;
+        }
+    }
+    const double v1[3] = {r[REC_V1X], r[REC_V1Y], r[REC_V1Z]};
+    const double v2[3] = {r[REC_V2X], r[REC_V2Y], r[REC_V2Z]};
+    const double n[3] = {r[REC_NX], r[REC_NY], r[REC_NZ]};
+    const double mu[3] = {r[REC_MUX], r[REC_MUY], r[REC_MUZ]};
+    const double denom = d[0] * n[0] + d[1] * n[1] + d[2] * n[2];
+    const double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+    g[14] = d_alpha * kd_op;
+    g[15] = d_alpha * kd_gx;
+    g[16] = d_alpha * kd_gy;
+    g[12] = d_alpha * kd_u * (-u / sx);
+    g[13] = d_alpha * kd_v * (-v / sy);
+    const double du = d_alpha * kd_u, dv = d_alpha * kd_v;
+    const double dv1 = d[0] * v1[0] + d[1] * v1[1] + d[2] * v1[2];
+    const double dv2 = d[0] * v2[0] + d[1] * v2[1] + d[2] * v2[2];
+    const double dt = d_t + du * dv1 / sx + dv * dv2 / sy;
+    const double cu = -du / sx, cv = -dv / sy, cn = dt / denom;
+    const double au = du / sx, av = dv / sy;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        g[i] = cu * v1[i] + cv * v2[i] + cn * n[i];
+        const double xm = x[i] - mu[i];
+        g[3 + 3 * i + 0] = au * xm;
+        g[3 + 3 * i + 1] = av * xm;
+        g[3 + 3 * i + 2] = cn * (-xm);
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(kThreads, 4) composite_bwd_kernel(const CompositeBwdArgs a) {
+    constexpr int KK = K > 0 ? K : 1;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    SmemLayout& sm = *reinterpret_cast<SmemLayout*>(smem_raw);
+
+    const int t = blockIdx.x;
+    const int tx = t % a.fb.tiles_x, ty = t / a.fb.tiles_x;
+    const int list_begin = a.tile_offsets[t], list_end = a.tile_offsets[t + 1];
+    const int W = a.cam.W, H = a.cam.H;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double near_eps = a.st.near_eps, alpha_max = a.st.alpha_max, min_T = a.st.min_transmittance;
+    const float near_eps_f = static_cast<float>(near_eps);
+    const double o[3] = {a.cam.o[0], a.cam.o[1], a.cam.o[2]};
+
+    const int px = tx * kWorkTile + (lane & 7), py = ty * kWorkTile + warp * 4 + (lane >> 3);
+    const bool in_img = px < W && py < H;
+    const int wx0 = __reduce_min_sync(0xffffffffu, in_img ? px : 0x7fffffff);
+    const int wx1 = __reduce_max_sync(0xffffffffu, in_img ? px : -1);
+    const int wy0 = __reduce_min_sync(0xffffffffu, in_img ? py : 0x7fffffff);
+    const int wy1 = __reduce_max_sync(0xffffffffu, in_img ? py : -1);
+    double dir[3] = {0.0, 0.0, 1.0};
+    if (in_img) pixel_dir(a.cam, px + 0.5, py + 0.5, dir);
+    sm.dir[threadIdx.x][0] = dir[0];
+    sm.dir[threadIdx.x][1] = dir[1];
+    sm.dir[threadIdx.x][2] = dir[2];
+    const float dfx = static_cast<float>(dir[0]), dfy = static_cast<float>(dir[1]), dfz = static_cast<float>(dir[2]);
+    float basis[16];
+    sh_basis_f32(dfx, dfy, dfz, basis);
+
+    // per-pixel upstream state
+    const int64_t pix = in_img ? static_cast<int64_t>(py) * W + px : 0;
+    double dfin[3] = {0.0, 0.0, 0.0};
+    if (in_img && a.d_final)
+        for (int c = 0; c < 3; ++c) dfin[c] = a.d_final[pix * 3 + c];
+    int32_t k_id[KK];
+    double k_dw[KK], k_dt[KK];
+    double A_total = 0.0;
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+        k_id[j] = -1;
+        k_dw[j] = 0.0;
+        k_dt[j] = 0.0;
+    }
+    if (in_img) {
+        A_total = dfin[0] * a.fb.base64[pix * 3 + 0] + dfin[1] * a.fb.base64[pix * 3 + 1] +
+                  dfin[2] * a.fb.base64[pix * 3 + 2];
+        if (K > 0) {
+#pragma unroll
+            for (int j = 0; j < KK; ++j) {
+                const int64_t sl = pix * K + j;
+                k_id[j] = a.fb.ids[sl];
+                if (k_id[j] < 0) continue;
+                const float* tex = a.fb.texture + sl * 3;
+                double dw = dfin[0] * tex[0] + dfin[1] * tex[1] + dfin[2] * tex[2];  // dot(dfin, tex)
+                if (a.d_weights) dw += a.d_weights[sl];
+                k_dw[j] = dw;
+                k_dt[j] = a.d_t_slot[sl];
+                A_total += dw * a.fb.weights[sl];
+            }
+        }
+    }
+    const double errp = (in_img && a.err_pixel) ? a.err_pixel[pix] : 0.0;
+    const bool want_err = a.err_pixel != nullptr;
+    const int n_sh = a.sh_degree >= 3 ? 16 : 1;
+
+    double T = 1.0, P = 0.0;
+    bool active = in_img;
+    const double2* rec2 = reinterpret_cast<const double2*>(a.rec);
+
+    for (int cb = list_begin; cb < list_end; cb += kChunk) {
+        const int cn = min(kChunk, list_end - cb);
+        __syncthreads();
+        for (int e = threadIdx.x; e < cn * 4; e += kThreads) {
+            const int j = e >> 2, q = e & 3;
+            const int32_t id = __ldg(a.list_ids + cb + j);
+            sm.f[j][q] = __ldg(a.recf + static_cast<int64_t>(id) * 4 + q);
+            if (q == 0) sm.id[j] = id;
+        }
+        __syncthreads();
+        if (__any_sync(0xffffffffu, active)) {
+            for (int sb = 0; sb < cn; sb += kSub) {
+                const int sn = min(kSub, cn - sb);
+                // ---- A. screen-space cull + fp32 prefilter (as the forward)
+                uint32_t mask = 0;
+#pragma unroll 4
+                for (int b = 0; b < sn; ++b) {
+                    const float4 f3 = sm.f[sb + b][3];
+                    const int rx = __float_as_int(f3.z), ry = __float_as_int(f3.w);
+                    const int x0 = rx & 0xffff, x1 = rx >> 16, y0 = ry & 0xffff, y1 = ry >> 16;
+                    if (x1 < wx0 || x0 > wx1 || y1 < wy0 || y0 > wy1) continue;
+                    if (active && px >= x0 && px <= x1 && py >= y0 && py <= y1 &&
+                        prefilter(&sm.f[sb + b][0], dfx, dfy, dfz, near_eps_f))
+                        mask |= 1u << b;
+                }
+                const int cnt = __popc(mask);
+                int incl = cnt;
+#pragma unroll
+                for (int of = 1; of < 32; of <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, of);
+                    if (lane >= of) incl += y;
+                }
+                const int off = incl - cnt;
+                const int total = __shfl_sync(0xffffffffu, incl, 31);
+                if (total == 0) continue;
+                {
+                    uint32_t m = mask;
+                    int k = off;
+                    while (m) {
+                        const int b = __ffs(m) - 1;
+                        m &= m - 1;
+                        sm.q[warp][k++] = static_cast<uint16_t>((lane << 8) | (sb + b));
+                    }
+                }
+                __syncwarp();
+                // ---- B1. exact fp64 intersect of the pooled pairs (intersect.hpp:23-42)
+                for (int e = lane; e < total; e += 32) {
+                    const int ent = sm.q[warp][e];
+                    const int owner = ent >> 8, j = ent & 0xff;
+                    const double* dd = sm.dir[warp * 32 + owner];
+                    const double d0 = dd[0], d1 = dd[1], d2 = dd[2];
+                    const int32_t id = sm.id[j];
+                    double r[REC_FIELDS];
+#pragma unroll
+                    for (int q = 0; q < kRecPairs; ++q) {
+                        const double2 v = __ldg(rec2 + static_cast<int64_t>(id) * kRecPairs + q);
+                        r[2 * q] = v.x;
+                        r[2 * q + 1] = v.y;
+                    }
+                    BwdEntry res;
+                    res.alpha = -1.0;
+                    res.t = res.u = res.v = 0.0;
+                    res.flags = 0;
+                    const double denom = d0 * r[REC_NX] + d1 * r[REC_NY] + d2 * r[REC_NZ];
+                    if (fabs(denom) >= kMinNormalDot) {
+                        const double tt = r[REC_NUM] / denom;
+                        if (tt > near_eps) {
+                            const double e0 = (o[0] + tt * d0) - r[REC_MUX];
+                            const double e1 = (o[1] + tt * d1) - r[REC_MUY];
+                            const double e2 = (o[2] + tt * d2) - r[REC_MUZ];
+                            const double du = e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z];
+                            const double dv = e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z];
+                            if (fabs(du) <= r[REC_ULIM] && fabs(dv) <= r[REC_VLIM]) {
+                                const double u = du / r[REC_SX];
+                                const double v = dv / r[REC_SY];
+                                const double al = eval_kernel(u, v, r[REC_OP], r[REC_GX], r[REC_GY]);
+                                if (al >= kAlphaMin) {
+                                    res.alpha = al;
+                                    res.t = tt;
+                                    res.u = u;
+                                    res.v = v;
+                                    uint32_t act;
+                                    eval_sh_f32(a.sh + static_cast<int64_t>(id) * NX_SH_VALUES, static_cast<float>(d0),
+                                                static_cast<float>(d1), static_cast<float>(d2), a.sh_degree, res.rgb,
+                                                &act);
+                                    res.flags = act;
+                                }
+                            }
+                        }
+                    }
+                    sm.res[warp][e] = res;
+                }
+                __syncwarp();
+                // ---- B2. per-pixel march in list order: weights, d_alpha, d_t (renderer.cpp:325-370)
+                for (int k = off; k < off + cnt && active; ++k) {
+                    BwdEntry& res = sm.res[warp][k];
+                    if (res.alpha < 0.0) continue;
+                    const int32_t id = sm.id[sm.q[warp][k] & 0xff];
+                    const bool clamped = res.alpha > alpha_max;
+                    const double alpha = clamped ? alpha_max : res.alpha;
+                    const double w = alpha * T;
+                    int slot = -1;
+#pragma unroll
+                    for (int j = 0; j < KK; ++j)
+                        if (K > 0 && slot < 0 && k_id[j] == id) slot = j;
+                    double dw = 0.0, d_t = 0.0;
+                    float wdf[3] = {0.f, 0.f, 0.f};
+                    if (slot >= 0) {
+#pragma unroll
+                        for (int j = 0; j < KK; ++j)
+                            if (j == slot) {
+                                dw = k_dw[j];
+                                d_t = k_dt[j];
+                            }
+                    } else {
+                        dw = dfin[0] * res.rgb[0] + dfin[1] * res.rgb[1] + dfin[2] * res.rgb[2];
+#pragma unroll
+                        for (int c = 0; c < 3; ++c)
+                            wdf[c] = (res.flags >> c) & 1u ? static_cast<float>(w * dfin[c]) : 0.f;
+                    }
+                    const double A = A_total - P - dw * w;  // sum of dL/dw * w behind this hit
+                    double d_alpha = dw * T - A / (1.0 - alpha);
+                    if (clamped) d_alpha = 0.0;
+                    P += dw * w;
+                    res.alpha = d_alpha;
+                    res.d_t = d_t;
+                    res.werr = w * errp;
+                    res.rgb[0] = wdf[0];
+                    res.rgb[1] = wdf[1];
+                    res.rgb[2] = wdf[2];
+                    res.flags = 8u;
+                    T *= 1.0 - alpha;
+                    if (T < min_T) active = false;
+                }
+                __syncwarp();
+                // ---- B3. per primitive of the group: warp-reduce the pixels' gradients
+                int cur = off;
+                for (int b = 0; b < sn; ++b) {
+                    int e = -1;
+                    if (cur < off + cnt && (sm.q[warp][cur] & 0xff) == sb + b) e = cur++;
+                    const bool hit = e >= 0 && (sm.res[warp][e].flags & 8u);
+                    const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+                    if (!hm) continue;
+                    const int32_t id = sm.id[sb + b];
+                    double g[kActFields];
+#pragma unroll
+                    for (int i = 0; i < kActFields; ++i) g[i] = 0.0;
+                    float wdf[3] = {0.f, 0.f, 0.f};
+                    if (hit) {
+                        const BwdEntry& res = sm.res[warp][e];
+                        double r[REC_FIELDS];
+#pragma unroll
+                        for (int q = 0; q < kRecPairs; ++q) {
+                            const double2 v = __ldg(rec2 + static_cast<int64_t>(id) * kRecPairs + q);
+                            r[2 * q] = v.x;
+                            r[2 * q + 1] = v.y;
+                        }
+                        hit_backward(r, dir, o, res.t, res.u, res.v, res.alpha, res.d_t, g);
+                        g[17] = res.werr;
+                        wdf[0] = res.rgb[0];
+                        wdf[1] = res.rgb[1];
+                        wdf[2] = res.rgb[2];
+                    }
+                    const bool sh_any = __any_sync(0xffffffffu, wdf[0] != 0.f || wdf[1] != 0.f || wdf[2] != 0.f);
+                    double* act = a.act_grad + static_cast<int64_t>(id) * kActFields;
+                    double* psh = a.prim_grad + static_cast<int64_t>(id) * NX_PARAMS_PER_NEXEL + 12;
+                    const int n_act = want_err ? kActFields : kActFields - 1;
+                    if (__popc(hm) <= 2) {
+                        // few pixels: each hitting lane accumulates its own contribution
+                        if (hit) {
+                            for (int i = 0; i < n_act; ++i)
+                                if (g[i] != 0.0) atomicAdd(act + i, g[i]);
+                            if (sh_any)
+                                for (int k = 0; k < n_sh; ++k)
+#pragma unroll
+                                    for (int c = 0; c < 3; ++c)
+                                        if (wdf[c] != 0.f) atomicAdd(psh + 3 * k + c, static_cast<double>(wdf[c] * basis[k]));
+                        }
+                    } else {
+                        // butterfly over the warp, then lane i adds value i
+                        double mine = 0.0;
+#pragma unroll
+                        for (int i = 0; i < kActFields; ++i) {
+                            double v = g[i];
+#pragma unroll
+                            for (int m = 16; m > 0; m >>= 1) v += shfl_xor_d(v, m);
+                            if (lane == i) mine = v;
+                        }
+                        if (lane < n_act && mine != 0.0) atomicAdd(act + lane, mine);
+                        if (sh_any) {
+                            // 3 * n_sh values: lane owns coefficient (k, c) for k*3+c = lane, lane+32
+                            float m0 = 0.f, m1 = 0.f;
+                            for (int k = 0; k < n_sh; ++k) {
+#pragma unroll
+                                for (int c = 0; c < 3; ++c) {
+                                    float v = wdf[c] * basis[k];
+#pragma unroll
+                                    for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+                                    const int idx = 3 * k + c;
+                                    if (idx == lane) m0 = v;
+                                    if (idx == lane + 32) m1 = v;
+                                }
+                            }
+                            if (lane < 3 * n_sh && m0 != 0.f) atomicAdd(psh + lane, static_cast<double>(m0));
+                            if (lane + 32 < 3 * n_sh && m1 != 0.f) atomicAdd(psh + lane + 32, static_cast<double>(m1));
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        if (cb + kChunk < list_end && !__syncthreads_or(active)) break;
+    }
+}
+
+template <int K>
+void launch_one(const CompositeBwdArgs& a, unsigned grid, cudaStream_t s) {
+    const size_t smem = sizeof(SmemLayout);
+    cudaFuncSetAttribute(composite_bwd_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    composite_bwd_kernel<K><<<grid, kThreads, smem, s>>>(a);
+}
+
+// quat_rotation_backward (primitive.cpp:22-45)
+__device__ void quat_rotation_backward(const double* q_raw, const double* g, double* dq) {
+    const double n = sqrt(q_raw[0] * q_raw[0] + q_raw[1] * q_raw[1] + q_raw[2] * q_raw[2] + q_raw[3] * q_raw[3]);
+    const double inv = 1.0 / n;
+    const double w = inv * q_raw[0], x = inv * q_raw[1], y = inv * q_raw[2], z = inv * q_raw[3];
+    // g[3*i + j] = d_R.m[i][j]
+    double du[4];
+    du[0] = 2 * (-z * g[1] + y * g[2] + z * g[3] - x * g[5] - y * g[6] + x * g[7]);
+    du[1] = 2 * (y * g[1] + z * g[2] + y * g[3] - 2 * x * g[4] - w * g[5] + z * g[6] + w * g[7] - 2 * x * g[8]);
+    du[2] = 2 * (-2 * y * g[0] + x * g[1] + w * g[2] + x * g[3] + z * g[5] - w * g[6] + z * g[7] - 2 * y * g[8]);
+    du[3] = 2 * (-2 * z * g[0] - w * g[1] + x * g[2] + w * g[3] - 2 * z * g[4] + y * g[5] + x * g[6] + y * g[7]);
+    const double u[4] = {w, x, y, z};
+    const double r = du[0] * u[0] + du[1] * u[1] + du[2] * u[2] + du[3] * u[3];
+    for (int k = 0; k < 4; ++k) dq[k] = (du[k] - r * u[k]) / n;
+}
+
+// activation_backward (intersect.hpp:91-103) applied to the per-primitive sum of the
+// activated gradients (it is linear in them), + the blended-error sum.
+__global__ void prim_finalize_kernel(const SceneDev scene, int no_gamma, const double* __restrict__ act_grad,
+                                     double* __restrict__ prim_grad, double* __restrict__ blended_error) {
+    const int64_t n = scene.n;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double g[kActFields];
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < kActFields; ++k) {
+        g[k] = act_grad[i * kActFields + k];
+        any |= g[k] != 0.0;
+    }
+    if (!any) return;
+    const double* geo = scene.geom;
+    double* out = prim_grad + i * NX_PARAMS_PER_NEXEL;
+    out[0] += g[0];
+    out[1] += g[1];
+    out[2] += g[2];
+    const double q[4] = {geo[3 * n + i], geo[4 * n + i], geo[5 * n + i], geo[6 * n + i]};
+    double dq[4];
+    quat_rotation_backward(q, g + 3, dq);
+    for (int k = 0; k < 4; ++k) out[3 + k] += dq[k];
+    out[7] += g[12] * exp(geo[7 * n + i]);
+    out[8] += g[13] * exp(geo[8 * n + i]);
+    const double op = sigmoid(geo[9 * n + i]);
+    out[9] += g[14] * op * (1.0 - op);
+    if (!no_gamma) {
+        out[10] += g[15] * sigmoid(geo[10 * n + i]);  // softplus_grad (vec_math.hpp:87)
+        out[11] += g[16] * sigmoid(geo[11 * n + i]);
+    }
+    if (blended_error) blended_error[i] += g[17];
+}
+
+}  // namespace
+
+void launch_composite_backward(const CompositeBwdArgs& a, cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(a.fb.tiles_x) * a.fb.tiles_y;
+    if (grid == 0) return;
+    count_launch();
+    switch (a.fb.K) {
+        case 0: launch_one<0>(a, grid, s); break;
+        case 1: launch_one<1>(a, grid, s); break;
+        case 2: launch_one<2>(a, grid, s); break;
+        case 3: launch_one<3>(a, grid, s); break;
+        case 4: launch_one<4>(a, grid, s); break;
+        case 5: launch_one<5>(a, grid, s); break;
+        case 6: launch_one<6>(a, grid, s); break;
+        case 7: launch_one<7>(a, grid, s); break;
+        default: launch_one<8>(a, grid, s); break;
+    }
+}
+
+void launch_prim_finalize(const SceneDev& scene, int no_gamma, const double* act_grad, double* prim_grad,
+                          double* blended_error, cudaStream_t s) {
+    if (scene.n <= 0) return;
+    count_launch();
+    prim_finalize_kernel<<<static_cast<unsigned>((scene.n + 255) / 256), 256, 0, s>>>(scene, no_gamma, act_grad,
+                                                                                     prim_grad, blended_error);
+}
+
+}  // namespace nx

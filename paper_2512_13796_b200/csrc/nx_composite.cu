@@ -20,7 +20,7 @@
 //      (renderer.cpp:144-153), all fp64.
 // Every decision is the reference's, taken in fp64 with its formulas; culling and
 // prefilter only skip provable misses, so contributor lists are bit-exact.
-#include "nx_internal.cuh"
+#include "nx_composite.cuh"
 
 namespace nx {
 
@@ -48,69 +48,6 @@ struct SmemLayout {
     uint16_t q[kWarps][kPool];
     PoolEntry res[kWarps][kPool];
 };
-
-// Primitive SH colour (eval_sh, sh.hpp:46-57) in fp32 from the ray direction:
-// colour outputs are tolerance-checked (max-abs 1e-3), decisions never use it.
-__device__ __forceinline__ void eval_sh_f32(const float* __restrict__ sh, float x, float y, float z, int degree,
-                                            float* rgb) {
-    float a0 = 0.5f + 0.28209479177387814f * __ldg(sh + 0);
-    float a1 = 0.5f + 0.28209479177387814f * __ldg(sh + 1);
-    float a2 = 0.5f + 0.28209479177387814f * __ldg(sh + 2);
-    if (degree >= 3) {
-        const float xx = x * x, yy = y * y, zz = z * z;
-        float b[16];
-        b[1] = -0.4886025119029199f * y;
-        b[2] = 0.4886025119029199f * z;
-        b[3] = -0.4886025119029199f * x;
-        b[4] = 1.0925484305920792f * x * y;
-        b[5] = -1.0925484305920792f * y * z;
-        b[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
-        b[7] = -1.0925484305920792f * x * z;
-        b[8] = 0.5462742152960396f * (xx - yy);
-        b[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
-        b[10] = 2.890611442640554f * x * y * z;
-        b[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
-        b[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
-        b[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
-        b[14] = 1.445305721320277f * z * (xx - yy);
-        b[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
-        const float4* s4 = reinterpret_cast<const float4*>(sh);
-        float c[48];
-#pragma unroll
-        for (int q = 0; q < 12; ++q) {
-            const float4 v = __ldg(s4 + q);
-            c[4 * q + 0] = v.x;
-            c[4 * q + 1] = v.y;
-            c[4 * q + 2] = v.z;
-            c[4 * q + 3] = v.w;
-        }
-#pragma unroll
-        for (int k = 1; k < 16; ++k) {
-            a0 = fmaf(c[3 * k + 0], b[k], a0);
-            a1 = fmaf(c[3 * k + 1], b[k], a1);
-            a2 = fmaf(c[3 * k + 2], b[k], a2);
-        }
-    }
-    rgb[0] = fmaxf(a0, 0.f);
-    rgb[1] = fmaxf(a1, 0.f);
-    rgb[2] = fmaxf(a2, 0.f);
-}
-
-// fp32 conservative prefilter: false only if the exact test provably misses.
-__device__ __forceinline__ bool prefilter(const float4* f, float dfx, float dfy, float dfz, float near_eps_f) {
-    const float4 f0 = f[0];
-    const float denom = dfx * f0.x + dfy * f0.y + dfz * f0.z;
-    if (!(fabsf(denom) >= 1e-2f)) return true;  // grazing: leave it to the exact path
-    const float ta = __fdividef(f0.w, denom);
-    if (!(ta * (1.0f + 1e-4f) > near_eps_f)) return false;  // t <= near_eps for sure
-    const float4 f1 = f[1], f2 = f[2], f3 = f[3];
-    const float ta1 = ta * (dfx * f1.x + dfy * f1.y + dfz * f1.z);
-    const float du = ta1 - f1.w;
-    if (fabsf(du) > f3.x + (1e-4f * (fabsf(ta1) + fabsf(ta) + fabsf(f1.w)) + 1e-7f)) return false;
-    const float ta2 = ta * (dfx * f2.x + dfy * f2.y + dfz * f2.z);
-    const float dv = ta2 - f2.w;
-    return !(fabsf(dv) > f3.y + (1e-4f * (fabsf(ta2) + fabsf(ta) + fabsf(f2.w)) + 1e-7f));
-}
 
 template <int K, bool kDebug>
 __global__ void __launch_bounds__(kThreads, 8) composite_kernel(const CompositeArgs a) {
@@ -355,6 +292,11 @@ __global__ void __launch_bounds__(kThreads, 8) composite_kernel(const CompositeA
         a.fb.base[pix * 3 + 0] = static_cast<float>(acc[0]);
         a.fb.base[pix * 3 + 1] = static_cast<float>(acc[1]);
         a.fb.base[pix * 3 + 2] = static_cast<float>(acc[2]);
+        if (a.fb.base64) {  // fp64 base kept for render_backward (nx_frame_set_backward)
+            a.fb.base64[pix * 3 + 0] = acc[0];
+            a.fb.base64[pix * 3 + 1] = acc[1];
+            a.fb.base64[pix * 3 + 2] = acc[2];
+        }
         if (kDebug && dbg_row) a.dbg_counts[dbg_q] = dbg_n;
     }
 }

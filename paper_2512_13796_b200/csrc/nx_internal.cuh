@@ -155,6 +155,7 @@ struct FrameDev {
     float* texture;
     float* final_img;
     float* residual;
+    double* base64;  // optional fp64 base (backward state), nullptr if not kept
 };
 
 // Host-side count of kernel launches issued by this library (all contexts).
@@ -222,5 +223,54 @@ int launch_texture(const TextureArgs& a, cudaStream_t s);  // returns NX_OK / NX
 // tcgen05 variant for the reference field shape (16 levels x 2 features, 64 hidden).
 bool texture_tc_supported(const nx_field_desc& fd);
 int launch_texture_tc(const TextureArgs& a, cudaStream_t s);
+
+// ---------------------------------------------------------------- backward (render_backward)
+// Per-primitive activated-space gradient accumulator (ActivatedGrad,
+// intersect.hpp:45-51) + the blended-error sum: d_mu[3], d_R[9] (row-major m[i][j],
+// columns v1, v2, n), d_sigma[2], d_opacity, d_gamma[2], blended error.
+constexpr int kActFields = 18;
+
+struct FieldBwdArgs {
+    SceneDev scene;
+    nx_settings st;
+    CamD cam;
+    FrameDev fb;
+    const double* d_final;    // H*W*3 or nullptr
+    const double* d_texture;  // H*W*K*3 or nullptr
+    double* d_t_slot;         // H*W*K out: dL/dt of each buffered crossing (0 for empty slots)
+    double* g_table;          // levels * 2^log2 * features (accumulated)
+    double* g_w1;
+    double* g_w2;
+    double* g_w3;
+};
+// field_backward_batch (texture_field.cpp:77-146) over the buffered slots.
+int launch_field_backward(const FieldBwdArgs& a, cudaStream_t s);
+int launch_field_backward_simt(const FieldBwdArgs& a, cudaStream_t s);
+bool field_backward_tc_supported(const nx_field_desc& fd);
+int launch_field_backward_tc(const FieldBwdArgs& a, cudaStream_t s);
+
+struct CompositeBwdArgs {
+    const double* rec;
+    const float4* recf;
+    int64_t n;
+    const float* sh;
+    const int32_t* list_ids;
+    const int32_t* tile_offsets;
+    nx_settings st;
+    CamD cam;
+    FrameDev fb;
+    int sh_degree;
+    const double* d_final;    // H*W*3 or nullptr
+    const double* d_weights;  // H*W*K or nullptr
+    const double* d_t_slot;   // H*W*K
+    const double* err_pixel;  // H*W or nullptr
+    double* act_grad;         // n x kActFields
+    double* prim_grad;        // n x 60 (the SH part is accumulated here directly)
+};
+// The per-pixel reverse march of render_backward (renderer.cpp:287-390).
+void launch_composite_backward(const CompositeBwdArgs& a, cudaStream_t s);
+// activation_backward (intersect.hpp:91-103) of the summed activated gradients.
+void launch_prim_finalize(const SceneDev& scene, int no_gamma, const double* act_grad, double* prim_grad,
+                          double* blended_error, cudaStream_t s);
 
 }  // namespace nx

@@ -46,3 +46,30 @@ def compare_frames(gpu, ref, *, rgb_tol=RGB_TOL, check_psnr=True):
 def is_subsequence(sub, full):
     it = iter(full.tolist())
     return all(x in it for x in sub.tolist())
+
+
+# render_backward: the reference accumulates in fp64 in a fixed order; the device path
+# takes the geometric chain in fp64 but colours (SH, texture) in fp32 and sums with
+# fp64 atomics, so gradients agree to ~1e-7 of each array's scale. The bar below is
+# GRAD_TOL of the array's largest magnitude, per gradient group.
+GRAD_TOL = 1e-5
+GROUPS = {"mu": slice(0, 3), "quat": slice(3, 7), "log_scale": slice(7, 9), "opacity": slice(9, 10),
+          "gamma": slice(10, 12), "sh": slice(12, 60)}
+
+
+def compare_grads(gpu, ref, tol=GRAD_TOL):
+    """gpu / ref: (prims (N,60), table, w1, w2, w3[, blended_error]). Returns the
+    per-group normwise errors and asserts each is <= tol."""
+    rep = {}
+    pairs = {f"prims.{k}": (gpu[0][:, s], ref[0][:, s]) for k, s in GROUPS.items()}
+    for i, k in enumerate(("table", "w1", "w2", "w3"), start=1):
+        pairs[k] = (gpu[i], ref[i])
+    if len(gpu) > 5 and gpu[5] is not None and ref[5] is not None:
+        pairs["blended_error"] = (gpu[5], ref[5])
+    for k, (a, b) in pairs.items():
+        scale = float(np.abs(b).max()) if b.size else 0.0
+        err = float(np.abs(a - b).max()) if a.size else 0.0
+        rep[k] = (err / scale) if scale > 0 else err
+        assert np.all(np.isfinite(a)), f"{k}: non-finite gradients"
+        assert rep[k] <= tol or err <= 1e-12, f"{k}: max err {err:.3e} vs scale {scale:.3e}"
+    return rep
