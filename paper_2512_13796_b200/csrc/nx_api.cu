@@ -303,10 +303,10 @@ int check_inputs(nx_ctx* c, const nx_scene* scene, const nx_camera* cam) {
 // Builds the per-tile lists (work lists, or the reference lists when
 // reference_lists) for `cam` into frame->list_ids / frame->tile_offsets.
 int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame* f, int reference_lists,
-                cudaStream_t s, int64_t* total_keys) {
+                cudaStream_t s, int64_t* total_keys, int work_tile = kWorkTile) {
     const int64_t n = scene->n;
-    // list geometry: reference lists per settings.tile, work lists per kWorkTile
-    const int lt = reference_lists ? scene->st.tile : kWorkTile;
+    // list geometry: reference lists per settings.tile, work lists per work_tile
+    const int lt = reference_lists ? scene->st.tile : work_tile;
     f->list_tile = lt;
     f->ltiles_x = (cam.width + lt - 1) / lt;
     f->ltiles_y = (cam.height + lt - 1) / lt;
@@ -342,7 +342,7 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
     pa.cam = cd;
     pa.tiles_x = f->tiles_x;
     pa.tiles_y = f->tiles_y;
-    pa.work_tile = kWorkTile;
+    pa.work_tile = lt;
     pa.zmin_work = 0.5 * scene->st.near_eps * min_axis_cosine(cam);
     pa.rec = c->rec.as<double>();
     pa.recf = c->recf.as<float4>();
@@ -880,7 +880,7 @@ int nx_render_backward(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, n
     int64_t total = 0;
     const bool prof = c->profiling;
     c->profiling = false;  // the stage events describe forward frames only
-    st = build_lists(c, scene, *cam, lf, 0, s, &total);
+    st = build_lists(c, scene, *cam, lf, 0, s, &total, kBwdTile);
     c->profiling = prof;
     if (st) return st;
 

@@ -31,21 +31,31 @@ namespace nx {
 
 namespace {
 
-constexpr int kThreads = kWorkTile * kWorkTile;  // 64: one thread per pixel of the 8x8 work tile
-constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 128;
-constexpr int kSub = 8;
+constexpr int kThreads = kBwdTile * kBwdTile;  // 256: one thread per pixel of the 16x16 work tile
+constexpr int kWarps = kThreads / 32;           // 8 warps of 8x4 pixels
+constexpr int kChunk = 64;                      // primitives staged (and accumulated) per round
+constexpr int kSub = 2;                         // primitives pooled per B1/B2/B3 round
 constexpr int kPool = 32 * kSub;
 constexpr int kRecPairs = REC_FIELDS / 2;
+constexpr int kAccStride = 68;                  // fp32 accumulator row: 18 activated + 48 SH (+2 pad)
+static_assert(kBwdTile == 16, "warp blocks are 8x4 pixels, two across a 16-pixel row");
 
-struct BwdEntry {       // one evaluated (pixel, primitive) pair
-    double alpha;       // B1: raw kernel alpha (< 0: miss). B2: d_alpha, or NaN-free flag via `hit`
-    double t, u, v;     // B1: crossing and plane coordinates
+constexpr int kStage = kActFields + 3;          // per-hit staged values: activated grads, werr, w dL/dfinal
+
+struct BwdHit {         // one evaluated (pixel, primitive) pair
+    double alpha;       // B1: raw kernel alpha (< 0: miss); B2: d_alpha
+    double t;           // B1: plane crossing
     double d_t;         // B2: upstream dL/dt (field branch) of a buffered hit
     double werr;        // B2: w * err_pixel
     float rgb[3];       // B1: primitive colour; B2: w * dL/dfinal * clamp mask (unbuffered), else 0
-    uint32_t flags;     // bit 0..2: SH clamp mask (B1); bit 3: composited (B2)
+    uint32_t flags;     // bits 0..2: SH clamp mask (B1)
 };
+// B3 overwrites a composited entry with its gradient values (float g[kStage]).
+union BwdEntry {
+    BwdHit h;
+    float g[kStage + 1];
+};
+constexpr uint16_t kComposited = 0x40;  // q entry flag set by B2 (list index j < kChunk = 64)
 
 struct SmemLayout {
     float4 f[kChunk][4];
@@ -53,12 +63,9 @@ struct SmemLayout {
     double dir[kThreads][3];
     uint16_t q[kWarps][kPool];
     BwdEntry res[kWarps][kPool];
+    float basis[kThreads][16];      // per-pixel SH basis (fp32)
+    float acc[kChunk][kAccStride];  // per-primitive gradient sums of the tile (flushed per chunk)
 };
-
-__device__ __forceinline__ double shfl_xor_d(double v, int m) {
-    return __hiloint2double(__shfl_xor_sync(0xffffffffu, __double2hiint(v), m),
-                            __shfl_xor_sync(0xffffffffu, __double2loint(v), m));
-}
 
 // eval_kernel_grad (kernel.hpp:40-68) + intersect_backward (intersect.hpp:56-87):
 // the activated-space gradient of one hit, g[0..16] = d_mu[3], d_R[9] (m[i][j]),
@@ -111,7 +118,7 @@ __device__ __forceinline__ void hit_backward(const double* r, const double* d, c
 }
 
 template <int K>
-__global__ void __launch_bounds__(kThreads, 4) composite_bwd_kernel(const CompositeBwdArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) composite_bwd_kernel(const CompositeBwdArgs a) {
     constexpr int KK = K > 0 ? K : 1;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     SmemLayout& sm = *reinterpret_cast<SmemLayout*>(smem_raw);
@@ -125,7 +132,8 @@ __global__ void __launch_bounds__(kThreads, 4) composite_bwd_kernel(const Compos
     const float near_eps_f = static_cast<float>(near_eps);
     const double o[3] = {a.cam.o[0], a.cam.o[1], a.cam.o[2]};
 
-    const int px = tx * kWorkTile + (lane & 7), py = ty * kWorkTile + warp * 4 + (lane >> 3);
+    // warp w owns the 8x4 block (w % 2, w / 2) of the 16x16 tile
+    const int px = tx * kBwdTile + (warp & 1) * 8 + (lane & 7), py = ty * kBwdTile + (warp >> 1) * 4 + (lane >> 3);
     const bool in_img = px < W && py < H;
     const int wx0 = __reduce_min_sync(0xffffffffu, in_img ? px : 0x7fffffff);
     const int wx1 = __reduce_max_sync(0xffffffffu, in_img ? px : -1);
@@ -137,8 +145,8 @@ __global__ void __launch_bounds__(kThreads, 4) composite_bwd_kernel(const Compos
     sm.dir[threadIdx.x][1] = dir[1];
     sm.dir[threadIdx.x][2] = dir[2];
     const float dfx = static_cast<float>(dir[0]), dfy = static_cast<float>(dir[1]), dfz = static_cast<float>(dir[2]);
-    float basis[16];
-    sh_basis_f32(dfx, dfy, dfz, basis);
+    sh_basis_f32(dfx, dfy, dfz, sm.basis[threadIdx.x]);
+    for (int e = threadIdx.x; e < kChunk * kAccStride; e += kThreads) (&sm.acc[0][0])[e] = 0.f;
 
     // per-pixel upstream state
     const int64_t pix = in_img ? static_cast<int64_t>(py) * W + px : 0;
@@ -173,8 +181,9 @@ __global__ void __launch_bounds__(kThreads, 4) composite_bwd_kernel(const Compos
         }
     }
     const double errp = (in_img && a.err_pixel) ? a.err_pixel[pix] : 0.0;
-    const bool want_err = a.err_pixel != nullptr;
+    const int n_act = a.err_pixel ? kActFields : kActFields - 1;
     const int n_sh = a.sh_degree >= 3 ? 16 : 1;
+    const int n_vals = kActFields + 3 * n_sh;  // accumulator columns in use
 
     double T = 1.0, P = 0.0;
     bool active = in_img;
@@ -195,8 +204,9 @@ __global__ void __launch_bounds__(kThreads, 4) composite_bwd_kernel(const Compos
                 const int sn = min(kSub, cn - sb);
                 // ---- A. screen-space cull + fp32 prefilter (as the forward)
                 uint32_t mask = 0;
-#pragma unroll 4
-                for (int b = 0; b < sn; ++b) {
+#pragma unroll
+                for (int b = 0; b < kSub; ++b) {
+                    if (b >= sn) break;
                     const float4 f3 = sm.f[sb + b][3];
                     const int rx = __float_as_int(f3.z), ry = __float_as_int(f3.w);
                     const int x0 = rx & 0xffff, x1 = rx >> 16, y0 = ry & 0xffff, y1 = ry >> 16;
@@ -228,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 4) composite_bwd_kernel(const Compos
                 // ---- B1. exact fp64 intersect of the pooled pairs (intersect.hpp:23-42)
                 for (int e = lane; e < total; e += 32) {
                     const int ent = sm.q[warp][e];
-                    const int owner = ent >> 8, j = ent & 0xff;
+                    const int owner = ent >> 8, j = ent & 0x3f;
                     const double* dd = sm.dir[warp * 32 + owner];
                     const double d0 = dd[0], d1 = dd[1], d2 = dd[2];
                     const int32_t id = sm.id[j];
@@ -239,9 +249,9 @@ __global__ void __launch_bounds__(kThreads, 4) composite_bwd_kernel(const Compos
                         r[2 * q] = v.x;
                         r[2 * q + 1] = v.y;
                     }
-                    BwdEntry res;
+                    BwdHit res;
                     res.alpha = -1.0;
-                    res.t = res.u = res.v = 0.0;
+                    res.t = 0.0;
                     res.flags = 0;
                     const double denom = d0 * r[REC_NX] + d1 * r[REC_NY] + d2 * r[REC_NZ];
                     if (fabs(denom) >= kMinNormalDot) {
@@ -259,8 +269,6 @@ __global__ void __launch_bounds__(kThreads, 4) composite_bwd_kernel(const Compos
                                 if (al >= kAlphaMin) {
                                     res.alpha = al;
                                     res.t = tt;
-                                    res.u = u;
-                                    res.v = v;
                                     uint32_t act;
                                     eval_sh_f32(a.sh + static_cast<int64_t>(id) * NX_SH_VALUES, static_cast<float>(d0),
                                                 static_cast<float>(d1), static_cast<float>(d2), a.sh_degree, res.rgb,
@@ -270,14 +278,14 @@ __global__ void __launch_bounds__(kThreads, 4) composite_bwd_kernel(const Compos
                             }
                         }
                     }
-                    sm.res[warp][e] = res;
+                    sm.res[warp][e].h = res;
                 }
                 __syncwarp();
                 // ---- B2. per-pixel march in list order: weights, d_alpha, d_t (renderer.cpp:325-370)
                 for (int k = off; k < off + cnt && active; ++k) {
-                    BwdEntry& res = sm.res[warp][k];
+                    BwdHit& res = sm.res[warp][k].h;
                     if (res.alpha < 0.0) continue;
-                    const int32_t id = sm.id[sm.q[warp][k] & 0xff];
+                    const int32_t id = sm.id[sm.q[warp][k] & 0x3f];
                     const bool clamped = res.alpha > alpha_max;
                     const double alpha = clamped ? alpha_max : res.alpha;
                     const double w = alpha * T;
@@ -310,86 +318,89 @@ __global__ void __launch_bounds__(kThreads, 4) composite_bwd_kernel(const Compos
                     res.rgb[0] = wdf[0];
                     res.rgb[1] = wdf[1];
                     res.rgb[2] = wdf[2];
-                    res.flags = 8u;
+                    sm.q[warp][k] |= kComposited;
                     T *= 1.0 - alpha;
                     if (T < min_T) active = false;
                 }
                 __syncwarp();
-                // ---- B3. per primitive of the group: warp-reduce the pixels' gradients
-                int cur = off;
-                for (int b = 0; b < sn; ++b) {
-                    int e = -1;
-                    if (cur < off + cnt && (sm.q[warp][cur] & 0xff) == sb + b) e = cur++;
-                    const bool hit = e >= 0 && (sm.res[warp][e].flags & 8u);
-                    const uint32_t hm = __ballot_sync(0xffffffffu, hit);
-                    if (!hm) continue;
-                    const int32_t id = sm.id[sb + b];
-                    double g[kActFields];
+                // ---- B3a. gradients of every composited pair, all lanes busy: eval_kernel_grad +
+                // intersect_backward in fp64 -> staged as fp32 in the entry
+#pragma unroll 1
+                for (int e = lane; e < total; e += 32) {
+                    const int ent = sm.q[warp][e];
+                    if (!(ent & kComposited)) continue;
+                    const BwdHit hh = sm.res[warp][e].h;
+                    const double* dd = sm.dir[warp * 32 + (ent >> 8)];
+                    const double d3[3] = {dd[0], dd[1], dd[2]};
+                    const int32_t id = sm.id[ent & 0x3f];
+                    double r[REC_FIELDS];
 #pragma unroll
-                    for (int i = 0; i < kActFields; ++i) g[i] = 0.0;
-                    float wdf[3] = {0.f, 0.f, 0.f};
-                    if (hit) {
-                        const BwdEntry& res = sm.res[warp][e];
-                        double r[REC_FIELDS];
-#pragma unroll
-                        for (int q = 0; q < kRecPairs; ++q) {
-                            const double2 v = __ldg(rec2 + static_cast<int64_t>(id) * kRecPairs + q);
-                            r[2 * q] = v.x;
-                            r[2 * q + 1] = v.y;
-                        }
-                        hit_backward(r, dir, o, res.t, res.u, res.v, res.alpha, res.d_t, g);
-                        g[17] = res.werr;
-                        wdf[0] = res.rgb[0];
-                        wdf[1] = res.rgb[1];
-                        wdf[2] = res.rgb[2];
+                    for (int q = 0; q < kRecPairs; ++q) {
+                        const double2 v = __ldg(rec2 + static_cast<int64_t>(id) * kRecPairs + q);
+                        r[2 * q] = v.x;
+                        r[2 * q + 1] = v.y;
                     }
-                    const bool sh_any = __any_sync(0xffffffffu, wdf[0] != 0.f || wdf[1] != 0.f || wdf[2] != 0.f);
-                    double* act = a.act_grad + static_cast<int64_t>(id) * kActFields;
-                    double* psh = a.prim_grad + static_cast<int64_t>(id) * NX_PARAMS_PER_NEXEL + 12;
-                    const int n_act = want_err ? kActFields : kActFields - 1;
-                    if (__popc(hm) <= 2) {
-                        // few pixels: each hitting lane accumulates its own contribution
-                        if (hit) {
-                            for (int i = 0; i < n_act; ++i)
-                                if (g[i] != 0.0) atomicAdd(act + i, g[i]);
-                            if (sh_any)
-                                for (int k = 0; k < n_sh; ++k)
+                    // the hit's plane coordinates, as intersect() formed them
+                    const double e0 = (o[0] + hh.t * d3[0]) - r[REC_MUX];
+                    const double e1 = (o[1] + hh.t * d3[1]) - r[REC_MUY];
+                    const double e2 = (o[2] + hh.t * d3[2]) - r[REC_MUZ];
+                    const double u = (e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z]) / r[REC_SX];
+                    const double v = (e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z]) / r[REC_SY];
+                    double gd[kActFields - 1];
+                    hit_backward(r, d3, o, hh.t, u, v, hh.alpha, hh.d_t, gd);
+                    float* g = sm.res[warp][e].g;
 #pragma unroll
-                                    for (int c = 0; c < 3; ++c)
-                                        if (wdf[c] != 0.f) atomicAdd(psh + 3 * k + c, static_cast<double>(wdf[c] * basis[k]));
-                        }
-                    } else {
-                        // butterfly over the warp, then lane i adds value i
-                        double mine = 0.0;
-#pragma unroll
-                        for (int i = 0; i < kActFields; ++i) {
-                            double v = g[i];
-#pragma unroll
-                            for (int m = 16; m > 0; m >>= 1) v += shfl_xor_d(v, m);
-                            if (lane == i) mine = v;
-                        }
-                        if (lane < n_act && mine != 0.0) atomicAdd(act + lane, mine);
-                        if (sh_any) {
-                            // 3 * n_sh values: lane owns coefficient (k, c) for k*3+c = lane, lane+32
-                            float m0 = 0.f, m1 = 0.f;
-                            for (int k = 0; k < n_sh; ++k) {
-#pragma unroll
-                                for (int c = 0; c < 3; ++c) {
-                                    float v = wdf[c] * basis[k];
-#pragma unroll
-                                    for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-                                    const int idx = 3 * k + c;
-                                    if (idx == lane) m0 = v;
-                                    if (idx == lane + 32) m1 = v;
-                                }
+                    for (int i = 0; i < kActFields - 1; ++i) g[i] = static_cast<float>(gd[i]);
+                    g[kActFields - 1] = static_cast<float>(hh.werr);
+                    g[kActFields + 0] = hh.rgb[0];
+                    g[kActFields + 1] = hh.rgb[1];
+                    g[kActFields + 2] = hh.rgb[2];
+                }
+                __syncwarp();
+                // ---- B3b. per primitive of the group: lane v sums value v over the pixels that hit
+                // it (SH values from the staged w dL/dfinal and the pixel's basis) -> tile accumulator
+                int cur = off;
+#pragma unroll 1
+                for (int b = 0; b < sn; ++b) {
+                    int my_e = -1;
+                    if (cur < off + cnt && (sm.q[warp][cur] & 0x3f) == sb + b) {
+                        if (sm.q[warp][cur] & kComposited) my_e = cur;
+                        ++cur;
+                    }
+                    const uint32_t hm = __ballot_sync(0xffffffffu, my_e >= 0);
+                    if (!hm) continue;
+                    float* accr = sm.acc[sb + b];
+#pragma unroll 1
+                    for (int r0 = 0; r0 < n_vals; r0 += 32) {  // warp-uniform rounds (shuffles inside)
+                        const int v = r0 + lane;
+                        const bool is_act = v < kActFields;
+                        const int sv = is_act ? 0 : v - kActFields;
+                        const int shk = sv / 3, shc = sv - 3 * (sv / 3);
+                        float sum = 0.f;
+                        for (uint32_t m = hm; m; m &= m - 1) {
+                            const int h = __ffs(m) - 1;
+                            const int eh = __shfl_sync(0xffffffffu, my_e, h);
+                            if (v < n_vals) {
+                                const float* g = sm.res[warp][eh].g;
+                                sum += is_act ? g[v] : g[kActFields + shc] * sm.basis[warp * 32 + h][shk];
                             }
-                            if (lane < 3 * n_sh && m0 != 0.f) atomicAdd(psh + lane, static_cast<double>(m0));
-                            if (lane + 32 < 3 * n_sh && m1 != 0.f) atomicAdd(psh + lane + 32, static_cast<double>(m1));
                         }
+                        if (v < n_vals && sum != 0.f && (!is_act || v < n_act)) atomicAdd(accr + v, sum);
                     }
                 }
                 __syncwarp();
             }
+        }
+        // ---- flush the chunk's accumulators: activated part -> act_grad, SH -> PrimitiveGrad
+        __syncthreads();
+        for (int e = threadIdx.x; e < cn * n_vals; e += kThreads) {
+            const int j = e / n_vals, v = e - j * n_vals;
+            const float val = sm.acc[j][v];
+            if (val == 0.f) continue;
+            sm.acc[j][v] = 0.f;
+            const int64_t id = sm.id[j];
+            if (v < kActFields) atomicAdd(a.act_grad + id * kActFields + v, static_cast<double>(val));
+            else atomicAdd(a.prim_grad + id * NX_PARAMS_PER_NEXEL + 12 + (v - kActFields), static_cast<double>(val));
         }
         if (cb + kChunk < list_end && !__syncthreads_or(active)) break;
     }

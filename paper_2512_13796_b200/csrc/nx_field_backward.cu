@@ -245,8 +245,4 @@ int launch_field_backward(const FieldBwdArgs& a, cudaStream_t s) {
     return launch_field_backward_simt(a, s);
 }
 
-// Until the tensor-core variant lands every shape takes the SIMT path.
-bool field_backward_tc_supported(const nx_field_desc&) { return false; }
-int launch_field_backward_tc(const FieldBwdArgs& a, cudaStream_t s) { return launch_field_backward_simt(a, s); }
-
 }  // namespace nx

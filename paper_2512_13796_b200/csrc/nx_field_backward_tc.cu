@@ -1,0 +1,616 @@
+// Field branch of render_backward, tensor-core variant for the reference field
+// shape (16 levels x 2 features -> 32 -> 64 -> 64 -> 48): field_backward_batch
+// (texture_field.cpp:77-146) over the buffered slots in three kernels, so that the
+// latency-bound hash-grid gathers / scatters run at full occupancy and the MLP runs
+// on tcgen05 with its weight gradients accumulated in TMEM:
+//
+//   G  features   one thread per slot: grid_lookup (hash_grid.cpp:26-83) at the
+//                 query (x = o + t d, build_queries renderer.cpp:177-203) -> F[32]
+//   M  mlp        persistent, one 128-slot tile per step, one thread per row:
+//                 forward  H1 = relu(F W1^T), H2 = relu(H1 W2^T), Y = H2 W3^T
+//                          (TextureMlp::forward, mlp.cpp:24-43)
+//                 SH       dY = dL/dcoeffs from dL/drgb = w dL/dfinal + dL/dtexture
+//                          (renderer.cpp:266-276; eval_sh_backward sh.hpp:76-83)
+//                 backward dH2 = (dY W3) * [H2 > 0], dH1 = (dH2 W2) * [H1 > 0],
+//                          dF = dH1 W1 (TextureMlp::backward, mlp.cpp:45-90)
+//                 weights  gW3^T += H2^T dY, gW2 += dH2^T H1, gW1 += dH1^T F, K = the
+//                          128 rows of the tile, accumulated in TMEM across all the
+//                          tiles of the CTA; partials reduced in a fixed order at the end
+//   S  scatter    one thread per slot: grid_lookup_backward (hash_grid.hpp:85-124):
+//                 table gradients (fp64 atomics, warp-aggregated where the warp
+//                 shares a cell), dL/dx, dL/dt -> d_t_slot = dL/dt + dot(dL/dx, dir)
+//
+// MMA operands are bf16 with the 3-term split (a.b ~ ah.bh + ah.bl + al.bh), as in
+// the forward. The activations live in three combined K-major buffers so that every
+// product — the row-wise chain (K = features) and the weight gradients (K = rows,
+// operands read MN-major from the same bytes) — is one descriptor away:
+//   C1 = [H2 | dH2]  (128 x 128)   C2 = [dY | H1]  (128 x 112)   C3 = [dH1 | F | pad]  (128 x 128)
+//   G1 (TMEM cols 64..175)  = C1^T . C2 : rows 0..63 x cols 0..47 = gW3^T, rows 64..127 x cols 48..111 = gW2
+//   G2 (TMEM cols 176..207) = C3^T . F  : rows 0..63 = gW1
+// The backward chain reads the weight buffers MN-major too (B = W^T without a copy).
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "nx_grid.cuh"
+#include "nx_tc.cuh"
+
+namespace nx {
+
+namespace {
+
+constexpr int kThreadsM = 128;
+constexpr int kRows = 128;
+constexpr int kIn = 32, kHid = 64, kOut = 48;
+constexpr int kC1 = 128, kC2 = 112, kC3 = 128;  // columns of the combined buffers
+constexpr int kWGrads = kHid * kIn + kHid * kHid + kOut * kHid;  // 9216 partial values per CTA
+constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kColD = 0, kColG1 = 64, kColG2 = 176;
+
+// shared-memory carve-up (bytes); every region 1 KB aligned
+constexpr int kOffW1h = 0;
+constexpr int kOffW1l = kOffW1h + kHid * kIn * 2;
+constexpr int kOffW2h = kOffW1l + kHid * kIn * 2;
+constexpr int kOffW2l = kOffW2h + kHid * kHid * 2;
+constexpr int kOffW3h = kOffW2l + kHid * kHid * 2;
+constexpr int kOffW3l = kOffW3h + kOut * kHid * 2;
+constexpr int kOffC1h = kOffW3l + kOut * kHid * 2;
+constexpr int kOffC1l = kOffC1h + kRows * kC1 * 2;
+constexpr int kOffC2h = kOffC1l + kRows * kC1 * 2;
+constexpr int kOffC2l = kOffC2h + kRows * kC2 * 2;
+constexpr int kOffC3h = kOffC2l + kRows * kC2 * 2;
+constexpr int kOffC3l = kOffC3h + kRows * kC3 * 2;
+constexpr int kOffBar = kOffC3l + kRows * kC3 * 2;
+constexpr int kOffTmem = kOffBar + 8;
+constexpr int kSmemM = kOffTmem + 8;
+static_assert(kSmemM <= 227 * 1024, "fits one CTA per SM");
+
+// ---------------------------------------------------------------- G: features
+__global__ void __launch_bounds__(128) features_kernel(const FieldBwdArgs a, const TcConst cst, float* __restrict__ fbuf,
+                                                       int64_t total) {
+    const int64_t sl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (sl >= total) return;
+    float feats[kIn];
+#pragma unroll
+    for (int i = 0; i < kIn; ++i) feats[i] = 0.f;
+    if (a.fb.ids[sl] >= 0) {
+        const int K = a.fb.K;
+        const int64_t pix = sl / K;
+        const int px = static_cast<int>(pix % a.cam.W), py = static_cast<int>(pix / a.cam.W);
+        double dir[3];
+        pixel_dir(a.cam, px + 0.5, py + 0.5, dir);
+        const double t = a.fb.depths[sl];
+        const double x0 = a.cam.o[0] + t * dir[0], x1 = a.cam.o[1] + t * dir[1], x2 = a.cam.o[2] + t * dir[2];
+        const float ft = static_cast<float>(a.cam.fx / t);
+        const uint32_t T = 1u << a.scene.field.log2_table, mask = T - 1u;
+        const float2* tab = reinterpret_cast<const float2*>(a.scene.table);
+        const bool small = fmax(fabs(x0), fmax(fabs(x1), fabs(x2))) * cst.level_scale[kLevels - 1] < 1073741824.0;
+        if (small) {
+            LevelFetch cur = fetch_level<true>(0, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
+#pragma unroll
+            for (int l = 0; l < kLevels; ++l) {
+                LevelFetch nxt;
+                if (l + 1 < kLevels) nxt = fetch_level<true>(l + 1, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
+                const float2 g = interp(cur);
+                feats[2 * l] = g.x;
+                feats[2 * l + 1] = g.y;
+                if (l + 1 < kLevels) cur = nxt;
+            }
+        } else {
+#pragma unroll
+            for (int l = 0; l < kLevels; ++l) {
+                const float2 g = interp(fetch_level<false>(l, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight));
+                feats[2 * l] = g.x;
+                feats[2 * l + 1] = g.y;
+            }
+        }
+    }
+    float4* dst = reinterpret_cast<float4*>(fbuf + sl * kIn);
+#pragma unroll
+    for (int q = 0; q < kIn / 4; ++q) dst[q] = make_float4(feats[4 * q], feats[4 * q + 1], feats[4 * q + 2], feats[4 * q + 3]);
+}
+
+// ---------------------------------------------------------------- M: MLP forward + backward on tcgen05
+// D = A . B^T over K, 3 split terms per 16-wide k-step. Descriptors: (start, lbo, sbo)
+// and the byte advance per k-step of each operand.
+struct Opnd {
+    uint32_t hi, lo;   // smem addresses of the hi / lo copies (start of the sub-matrix)
+    uint32_t lbo, sbo;
+    uint32_t step;     // bytes to advance per 16-wide k-step
+};
+
+__device__ __forceinline__ void issue_mma(uint32_t dtm, const Opnd& A, const Opnd& B, int ksteps, uint32_t idesc,
+                                          bool accumulate) {
+    for (int s = 0; s < ksteps; ++s) {
+        const uint32_t oa = s * A.step, ob = s * B.step;
+        const uint64_t ah = smem_desc(A.hi + oa, A.lbo, A.sbo), al = smem_desc(A.lo + oa, A.lbo, A.sbo);
+        const uint64_t bh = smem_desc(B.hi + ob, B.lbo, B.sbo), bl = smem_desc(B.lo + ob, B.lbo, B.sbo);
+        mma_bf16(dtm, ah, bh, idesc, (accumulate || s > 0) ? 1u : 0u);
+        mma_bf16(dtm, ah, bl, idesc, 1u);
+        mma_bf16(dtm, al, bh, idesc, 1u);
+    }
+}
+
+// K-major view of columns [c0, c0 + K) of a combined buffer with C columns (chain operand)
+__device__ __forceinline__ Opnd kmaj(uint8_t* smem, int off_h, int off_l, int C, int c0) {
+    const uint32_t base = (c0 / 8) * 128;
+    return {smem_u32(smem + off_h) + base, smem_u32(smem + off_l) + base, 128u, static_cast<uint32_t>(16 * C), 256u};
+}
+// MN-major view (transposed operand) of columns [c0, ...) of a buffer with C columns:
+// MN = columns (next 8 at 128 B), K = rows (next 8 at 16 C B)
+__device__ __forceinline__ Opnd mnmaj(uint8_t* smem, int off_h, int off_l, int C, int c0) {
+    const uint32_t base = (c0 / 8) * 128;
+    return {smem_u32(smem + off_h) + base, smem_u32(smem + off_l) + base, static_cast<uint32_t>(16 * C), 128u,
+            static_cast<uint32_t>(32 * C)};
+}
+
+__device__ __forceinline__ void load_weights_split(uint8_t* smem, const float* __restrict__ w, int rows, int K,
+                                                   int off_h, int off_l) {
+    for (int e = threadIdx.x; e < rows * K / 8; e += blockDim.x) {
+        const int n = e / (K / 8), c = e % (K / 8);
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(w + n * K + c * 8 + i);
+        store_split8(smem, off_h, off_l, kmajor_off(n, c * 8, K), x);
+    }
+}
+
+__global__ void __launch_bounds__(kThreadsM, 1) mlp_bwd_tc_kernel(const FieldBwdArgs a, float* __restrict__ fbuf,
+                                                                  float* __restrict__ partials, int64_t total,
+                                                                  int64_t n_tiles) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t bar = smem_u32(smem + kOffBar);
+    load_weights_split(smem, a.scene.w1, kHid, kIn, kOffW1h, kOffW1l);
+    load_weights_split(smem, a.scene.w2, kHid, kHid, kOffW2h, kOffW2l);
+    load_weights_split(smem, a.scene.w3, kOut, kHid, kOffW3h, kOffW3l);
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem + kOffTmem)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 32) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + kOffTmem);
+    const uint32_t lane_off = static_cast<uint32_t>(32 * warp) << 16;
+    const uint32_t tD = tmem + kColD + lane_off;
+    uint32_t phase = 0;
+    const int K = a.fb.K;
+    const int row = tid;
+
+    // operand views
+    const Opnd W1k = kmaj(smem, kOffW1h, kOffW1l, kIn, 0), W2k = kmaj(smem, kOffW2h, kOffW2l, kHid, 0),
+               W3k = kmaj(smem, kOffW3h, kOffW3l, kHid, 0);
+    const Opnd W1t = mnmaj(smem, kOffW1h, kOffW1l, kIn, 0), W2t = mnmaj(smem, kOffW2h, kOffW2l, kHid, 0),
+               W3t = mnmaj(smem, kOffW3h, kOffW3l, kHid, 0);
+    const Opnd F_k = kmaj(smem, kOffC3h, kOffC3l, kC3, 64), H1_k = kmaj(smem, kOffC2h, kOffC2l, kC2, 48),
+               H2_k = kmaj(smem, kOffC1h, kOffC1l, kC1, 0), dY_k = kmaj(smem, kOffC2h, kOffC2l, kC2, 0),
+               dH2_k = kmaj(smem, kOffC1h, kOffC1l, kC1, 64), dH1_k = kmaj(smem, kOffC3h, kOffC3l, kC3, 0);
+    const Opnd C1_t = mnmaj(smem, kOffC1h, kOffC1l, kC1, 0), C2_t = mnmaj(smem, kOffC2h, kOffC2l, kC2, 0),
+               C3_t = mnmaj(smem, kOffC3h, kOffC3l, kC3, 0), F_t = mnmaj(smem, kOffC3h, kOffC3l, kC3, 64);
+    constexpr uint32_t kI64 = idesc_bf16_f32(kRows, 64), kI48 = idesc_bf16_f32(kRows, 48);
+    constexpr uint32_t kI64b = idesc_bf16_f32(kRows, 64, false, true), kI32b = idesc_bf16_f32(kRows, 32, false, true);
+    constexpr uint32_t kIG1 = idesc_bf16_f32(kRows, kC2, true, true), kIG2 = idesc_bf16_f32(kRows, 32, true, true);
+
+    bool first = true;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int64_t sl = tile * kRows + row;
+        const bool valid = sl < total && a.fb.ids[sl] >= 0;
+        // ---- inputs of the row: features, dL/drgb, SH basis of the ray
+        float x[kIn];
+        float drgb[3] = {0.f, 0.f, 0.f};
+        float b[16];
+#pragma unroll
+        for (int i = 0; i < kIn; ++i) x[i] = 0.f;
+        if (valid) {
+            const float4* src = reinterpret_cast<const float4*>(fbuf + sl * kIn);
+#pragma unroll
+            for (int q = 0; q < kIn / 4; ++q) {
+                const float4 v = src[q];
+                x[4 * q] = v.x;
+                x[4 * q + 1] = v.y;
+                x[4 * q + 2] = v.z;
+                x[4 * q + 3] = v.w;
+            }
+            const int64_t pix = sl / K;
+            const double w = a.fb.weights[sl];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                double g = 0.0;
+                if (a.d_final) g += w * a.d_final[pix * 3 + c];
+                if (a.d_texture) g += a.d_texture[sl * 3 + c];
+                drgb[c] = static_cast<float>(g);
+            }
+            double dir[3];
+            pixel_dir(a.cam, static_cast<int>(pix % a.cam.W) + 0.5, static_cast<int>(pix / a.cam.W) + 0.5, dir);
+            const float dx = static_cast<float>(dir[0]), dy = static_cast<float>(dir[1]), dz = static_cast<float>(dir[2]);
+            const float xx = dx * dx, yy = dy * dy, zz = dz * dz;
+            b[0] = 0.28209479177387814f;
+            b[1] = -0.4886025119029199f * dy;
+            b[2] = 0.4886025119029199f * dz;
+            b[3] = -0.4886025119029199f * dx;
+            b[4] = 1.0925484305920792f * dx * dy;
+            b[5] = -1.0925484305920792f * dy * dz;
+            b[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+            b[7] = -1.0925484305920792f * dx * dz;
+            b[8] = 0.5462742152960396f * (xx - yy);
+            b[9] = -0.5900435899266435f * dy * (3.0f * xx - yy);
+            b[10] = 2.890611442640554f * dx * dy * dz;
+            b[11] = -0.4570457994644658f * dy * (4.0f * zz - xx - yy);
+            b[12] = 0.3731763325901154f * dz * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+            b[13] = -0.4570457994644658f * dx * (4.0f * zz - xx - yy);
+            b[14] = 1.445305721320277f * dz * (xx - yy);
+            b[15] = -0.5900435899266435f * dx * (xx - 3.0f * yy);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) b[k] = 0.f;
+        }
+#pragma unroll
+        for (int c = 0; c < kIn / 8; ++c) store_split8(smem, kOffC3h, kOffC3l, kmajor_off(row, 64 + 8 * c, kC3), x + 8 * c);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+
+        // ---- L1: D = F . W1^T -> H1 = relu -> C2[:, 48..111]
+        if (tid == 0) {
+            tc_fence_after();
+            issue_mma(tmem + kColD, F_k, W1k, kIn / 16, kI64, false);
+            mma_commit(bar);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+        uint64_t m1 = 0, m2 = 0;
+#pragma unroll
+        for (int c = 0; c < kHid / 16; ++c) {
+            float v[16];
+            tmem_ld16(tD + 16 * c, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                if (v[i] > 0.f) m1 |= 1ull << (16 * c + i);
+                v[i] = fmaxf(v[i], 0.f);
+            }
+            store_split8(smem, kOffC2h, kOffC2l, kmajor_off(row, 48 + 16 * c, kC2), v);
+            store_split8(smem, kOffC2h, kOffC2l, kmajor_off(row, 48 + 16 * c + 8, kC2), v + 8);
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        // ---- L2: D = H1 . W2^T -> H2 -> C1[:, 0..63]
+        if (tid == 0) {
+            tc_fence_after();
+            issue_mma(tmem + kColD, H1_k, W2k, kHid / 16, kI64, false);
+            mma_commit(bar);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < kHid / 16; ++c) {
+            float v[16];
+            tmem_ld16(tD + 16 * c, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                if (v[i] > 0.f) m2 |= 1ull << (16 * c + i);
+                v[i] = fmaxf(v[i], 0.f);
+            }
+            store_split8(smem, kOffC1h, kOffC1l, kmajor_off(row, 16 * c, kC1), v);
+            store_split8(smem, kOffC1h, kOffC1l, kmajor_off(row, 16 * c + 8, kC1), v + 8);
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        // ---- L3: Y = H2 . W3^T; SH clamp mask and dY = dL/dcoeffs -> C2[:, 0..47]
+        if (tid == 0) {
+            tc_fence_after();
+            issue_mma(tmem + kColD, H2_k, W3k, kHid / 16, kI48, false);
+            mma_commit(bar);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+        {
+            float y[kOut];
+#pragma unroll
+            for (int c = 0; c < kOut / 16; ++c) tmem_ld16(tD + 16 * c, y + 16 * c);
+            float acc[3] = {0.5f, 0.5f, 0.5f};
+#pragma unroll
+            for (int o = 0; o < kOut; ++o) acc[o % 3] = fmaf(y[o], b[o / 3], acc[o % 3]);
+            float dyv[kOut];
+#pragma unroll
+            for (int o = 0; o < kOut; ++o) dyv[o] = acc[o % 3] >= 0.f ? drgb[o % 3] * b[o / 3] : 0.f;
+#pragma unroll
+            for (int c = 0; c < kOut / 8; ++c) store_split8(smem, kOffC2h, kOffC2l, kmajor_off(row, 8 * c, kC2), dyv + 8 * c);
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        // ---- dH2 = (dY . W3) * [H2 > 0] -> C1[:, 64..127]
+        if (tid == 0) {
+            tc_fence_after();
+            issue_mma(tmem + kColD, dY_k, W3t, kOut / 16, kI64b, false);
+            mma_commit(bar);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < kHid / 16; ++c) {
+            float v[16];
+            tmem_ld16(tD + 16 * c, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = (m2 >> (16 * c + i)) & 1ull ? v[i] : 0.f;
+            store_split8(smem, kOffC1h, kOffC1l, kmajor_off(row, 64 + 16 * c, kC1), v);
+            store_split8(smem, kOffC1h, kOffC1l, kmajor_off(row, 64 + 16 * c + 8, kC1), v + 8);
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        // ---- G1 += C1^T . C2 (gW3^T, gW2); dH1 = (dH2 . W2) * [H1 > 0] -> C3[:, 0..63]
+        if (tid == 0) {
+            tc_fence_after();
+            issue_mma(tmem + kColG1, C1_t, C2_t, kRows / 16, kIG1, !first);
+            issue_mma(tmem + kColD, dH2_k, W2t, kHid / 16, kI64b, false);
+            mma_commit(bar);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < kHid / 16; ++c) {
+            float v[16];
+            tmem_ld16(tD + 16 * c, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = (m1 >> (16 * c + i)) & 1ull ? v[i] : 0.f;
+            store_split8(smem, kOffC3h, kOffC3l, kmajor_off(row, 16 * c, kC3), v);
+            store_split8(smem, kOffC3h, kOffC3l, kmajor_off(row, 16 * c + 8, kC3), v + 8);
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        // ---- G2 += C3^T . F (gW1); dF = dH1 . W1
+        if (tid == 0) {
+            tc_fence_after();
+            issue_mma(tmem + kColG2, C3_t, F_t, kRows / 16, kIG2, !first);
+            issue_mma(tmem + kColD, dH1_k, W1t, kHid / 16, kI32b, false);
+            mma_commit(bar);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+        {
+            float v[kIn];
+            tmem_ld16(tD, v);
+            tmem_ld16(tD + 16, v + 16);
+            if (valid) {
+                float4* dst = reinterpret_cast<float4*>(fbuf + sl * kIn);
+#pragma unroll
+                for (int q = 0; q < kIn / 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
+        }
+        tc_fence_before();
+        __syncthreads();  // the next tile rewrites C1..C3 only after every MMA above completed
+        first = false;
+    }
+    // ---- weight-gradient partials of this CTA: [w1 (64x32) | w2 (64x64) | w3 (48x64)]
+    tc_fence_after();
+    float* part = partials + static_cast<int64_t>(blockIdx.x) * kWGrads;
+    float* p1 = part;
+    float* p2 = part + kHid * kIn;
+    float* p3 = p2 + kHid * kHid;
+    float g1[kC2], g2[32];
+#pragma unroll
+    for (int c = 0; c < kC2 / 16; ++c) tmem_ld16(tmem + kColG1 + lane_off + 16 * c, g1 + 16 * c);
+    tmem_ld16(tmem + kColG2 + lane_off, g2);
+    tmem_ld16(tmem + kColG2 + lane_off + 16, g2 + 16);
+    if (first) {  // no tile: the accumulators were never written
+#pragma unroll
+        for (int i = 0; i < kC2; ++i) g1[i] = 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) g2[i] = 0.f;
+    }
+    if (row < kHid) {
+#pragma unroll
+        for (int o = 0; o < kOut; ++o) p3[o * kHid + row] = g1[o];  // gW3[o][i = row]
+#pragma unroll
+        for (int i = 0; i < kIn; ++i) p1[row * kIn + i] = g2[i];    // gW1[o = row][i]
+    } else {
+#pragma unroll
+        for (int i = 0; i < kHid; ++i) p2[(row - kHid) * kHid + i] = g1[48 + i];  // gW2[o = row-64][i]
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
+// Sums the CTA partials in CTA order (deterministic) into the fp64 weight gradients.
+__global__ void reduce_wgrads_kernel(const float* __restrict__ partials, int n_parts, double* g_w1, double* g_w2,
+                                     double* g_w3) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= kWGrads) return;
+    double s = 0.0;
+    for (int p = 0; p < n_parts; ++p) s += partials[static_cast<int64_t>(p) * kWGrads + i];
+    if (i < kHid * kIn) g_w1[i] += s;
+    else if (i < kHid * kIn + kHid * kHid) g_w2[i - kHid * kIn] += s;
+    else g_w3[i - kHid * kIn - kHid * kHid] += s;
+}
+
+// ---------------------------------------------------------------- S: grid_lookup_backward
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1)
+        v += __hiloint2double(__shfl_xor_sync(0xffffffffu, __double2hiint(v), m),
+                              __shfl_xor_sync(0xffffffffu, __double2loint(v), m));
+    return v;
+}
+
+template <bool kSmall>
+__device__ __forceinline__ void scatter_levels(const FieldBwdArgs& a, const TcConst& cst, bool valid, double x0,
+                                               double x1, double x2, float ft, const float* g, double t, double* dx,
+                                               double& dt, uint32_t vmask, int leader) {
+    const uint32_t T = 1u << a.scene.field.log2_table, mask = T - 1u;
+    const float2* tab = reinterpret_cast<const float2*>(a.scene.table);
+    const int lane = threadIdx.x & 31;
+#pragma unroll 1
+    for (int l = 0; l < kLevels; ++l) {
+        const LevelCell c = level_cell<kSmall>(l, x0, x1, x2, cst, mask, ft, a.st.no_downweight);
+        const float g0 = g[2 * l], g1 = g[2 * l + 1];
+        const float wx[2] = {1.0f - c.fr0, c.fr0}, wy[2] = {1.0f - c.fr1, c.fr1}, wz[2] = {1.0f - c.fr2, c.fr2};
+        const size_t slab = static_cast<size_t>(l) * T;
+        // position / fade gradients in fp64: the corner terms cancel (finite differences
+        // of the table across the cell) and are then scaled by s_l (up to 2^11)
+        double dp0 = 0.0, dp1 = 0.0, dp2 = 0.0, d_dw = 0.0;
+        const double fx[2] = {1.0 - static_cast<double>(c.fr0), c.fr0}, fy[2] = {1.0 - static_cast<double>(c.fr1), c.fr1},
+                     fz[2] = {1.0 - static_cast<double>(c.fr2), c.fr2};
+        float2 v[8];
+#pragma unroll
+        for (int ci = 0; ci < 8; ++ci) v[ci] = valid ? __ldg(tab + slab + c.row[ci]) : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int ci = 0; ci < 8; ++ci) {
+            const float ax = wx[ci & 1], ay = wy[(ci >> 1) & 1], az = wz[(ci >> 2) & 1];
+            const float cw = ax * ay * az;
+            // table gradient: dL/dtable[row][f] += g[f] * dw * corner_w (hash_grid.hpp:99-103)
+            const double u0 = valid ? static_cast<double>(g0 * c.dw * cw) : 0.0;
+            const double u1 = valid ? static_cast<double>(g1 * c.dw * cw) : 0.0;
+            const uint32_t lr = __shfl_sync(0xffffffffu, c.row[ci], leader);
+            const bool uniform = __all_sync(0xffffffffu, !valid || c.row[ci] == lr);
+            double* dst = a.g_table + (slab + c.row[ci]) * 2;
+            if (uniform) {
+                const double s0 = warp_sum_d(u0), s1 = warp_sum_d(u1);
+                if (lane == leader) {
+                    if (s0 != 0.0) atomicAdd(dst, s0);
+                    if (s1 != 0.0) atomicAdd(dst + 1, s1);
+                }
+            } else if (valid) {
+                if (u0 != 0.0) atomicAdd(dst, u0);
+                if (u1 != 0.0) atomicAdd(dst + 1, u1);
+            }
+            const double gdotf = static_cast<double>(g0) * v[ci].x + static_cast<double>(g1) * v[ci].y;
+            const double updotf = gdotf * c.dw;
+            const double bx = fx[ci & 1], by = fy[(ci >> 1) & 1], bz = fz[(ci >> 2) & 1];
+            dp0 += updotf * ((ci & 1) ? by * bz : -(by * bz));
+            dp1 += updotf * ((ci & 2) ? bx * bz : -(bx * bz));
+            dp2 += updotf * ((ci & 4) ? bx * by : -(bx * by));
+            d_dw += gdotf * (bx * by * bz);
+        }
+        const double s = cst.level_scale[l];
+        dx[0] += s * dp0;
+        dx[1] += s * dp1;
+        dx[2] += s * dp2;
+        if (!a.st.no_downweight) {
+            const double r = a.cam.fx / (s * t);
+            dt += d_dw * (static_cast<double>(c.dw) - 1.0) * r * r / (M_PI * t);
+        }
+    }
+    (void)vmask;
+}
+
+__global__ void __launch_bounds__(128) scatter_kernel(const FieldBwdArgs a, const TcConst cst,
+                                                      const float* __restrict__ fbuf, int64_t total) {
+    const int64_t sl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool in = sl < total;
+    const bool valid = in && a.fb.ids[sl] >= 0;
+    const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+    if (!vmask) {
+        if (in) a.d_t_slot[sl] = 0.0;
+        return;
+    }
+    const int leader = __ffs(vmask) - 1;
+    double dir[3] = {0.0, 0.0, 1.0};
+    double t = 1.0, x0 = 0.0, x1 = 0.0, x2 = 0.0;
+    float g[kIn];
+#pragma unroll
+    for (int i = 0; i < kIn; ++i) g[i] = 0.f;
+    if (valid) {
+        const int64_t pix = sl / a.fb.K;
+        pixel_dir(a.cam, static_cast<int>(pix % a.cam.W) + 0.5, static_cast<int>(pix / a.cam.W) + 0.5, dir);
+        t = a.fb.depths[sl];
+        x0 = a.cam.o[0] + t * dir[0];
+        x1 = a.cam.o[1] + t * dir[1];
+        x2 = a.cam.o[2] + t * dir[2];
+        const float4* src = reinterpret_cast<const float4*>(fbuf + sl * kIn);
+#pragma unroll
+        for (int q = 0; q < kIn / 4; ++q) {
+            const float4 v = src[q];
+            g[4 * q] = v.x;
+            g[4 * q + 1] = v.y;
+            g[4 * q + 2] = v.z;
+            g[4 * q + 3] = v.w;
+        }
+    } else {  // inactive lanes follow the leader's cell so that uniform levels stay uniform
+        x0 = x1 = x2 = 0.0;
+    }
+    const float ft = static_cast<float>(a.cam.fx / t);
+    double dx[3] = {0.0, 0.0, 0.0}, dt = 0.0;
+    const bool small = fmax(fabs(x0), fmax(fabs(x1), fabs(x2))) * cst.level_scale[kLevels - 1] < 1073741824.0;
+    if (__all_sync(0xffffffffu, small))
+        scatter_levels<true>(a, cst, valid, x0, x1, x2, ft, g, t, dx, dt, vmask, leader);
+    else
+        scatter_levels<false>(a, cst, valid, x0, x1, x2, ft, g, t, dx, dt, vmask, leader);
+    if (in) a.d_t_slot[sl] = valid ? dt + (dx[0] * dir[0] + dx[1] * dir[1] + dx[2] * dir[2]) : 0.0;
+}
+
+struct Scratch {
+    float* fbuf = nullptr;
+    size_t fcap = 0;
+    float* parts = nullptr;
+    size_t pcap = 0;
+};
+Scratch g_scratch[64];  // per device
+
+}  // namespace
+
+bool field_backward_tc_supported(const nx_field_desc& fd) {
+    return fd.levels == kLevels && fd.features == 2 && fd.n_hidden == kHid;
+}
+
+int launch_field_backward_tc(const FieldBwdArgs& a, cudaStream_t s) {
+    const int64_t total = static_cast<int64_t>(a.cam.W) * a.cam.H * a.fb.K;
+    if (total == 0) return NX_OK;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    Scratch& sc = g_scratch[dev & 63];
+    const size_t fneed = static_cast<size_t>(total) * kIn;
+    const int64_t n_tiles = (total + kRows - 1) / kRows;
+    const int grid_m = static_cast<int>(std::min<int64_t>(n_tiles, sms));
+    const size_t pneed = static_cast<size_t>(grid_m) * kWGrads;
+    if (fneed > sc.fcap) {
+        if (sc.fbuf) cudaFree(sc.fbuf);
+        sc.fbuf = nullptr;
+        sc.fcap = 0;
+        if (cudaMalloc(&sc.fbuf, fneed * sizeof(float)) != cudaSuccess) return NX_OUT_OF_MEMORY;
+        sc.fcap = fneed;
+    }
+    if (pneed > sc.pcap) {
+        if (sc.parts) cudaFree(sc.parts);
+        sc.parts = nullptr;
+        sc.pcap = 0;
+        if (cudaMalloc(&sc.parts, pneed * sizeof(float)) != cudaSuccess) return NX_OUT_OF_MEMORY;
+        sc.pcap = pneed;
+    }
+    TcConst cst;
+    double scale = a.scene.field.base_scale;
+    for (int l = 0; l < kLevels; ++l, scale *= a.scene.field.growth) {
+        cst.level_scale[l] = scale;
+        cst.inv_level_scale[l] = static_cast<float>(1.0 / scale);
+    }
+    const unsigned blocks = static_cast<unsigned>((total + 127) / 128);
+    count_launch(4);
+    features_kernel<<<blocks, 128, 0, s>>>(a, cst, sc.fbuf, total);
+    cudaFuncSetAttribute(mlp_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemM);
+    mlp_bwd_tc_kernel<<<grid_m, kThreadsM, kSmemM, s>>>(a, sc.fbuf, sc.parts, total, n_tiles);
+    reduce_wgrads_kernel<<<(kWGrads + 255) / 256, 256, 0, s>>>(sc.parts, grid_m, a.g_w1, a.g_w2, a.g_w3);
+    scatter_kernel<<<blocks, 128, 0, s>>>(a, cst, sc.fbuf, total);
+    return NX_OK;
+}
+
+}  // namespace nx

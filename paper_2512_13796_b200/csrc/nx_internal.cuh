@@ -26,6 +26,9 @@ constexpr int kGeomFields = 12;            // fp64 geometry params per primitive
 // settings.tile: every hit of a primitive lies inside its padded pixel rect, so the
 // per-pixel contributor sequences do not depend on the list granularity.
 constexpr int kWorkTile = 8;
+// The reverse march (render_backward) walks 16x16-pixel work lists: its CTAs are
+// 8 warps that share per-primitive gradient accumulators in shared memory.
+constexpr int kBwdTile = 16;
 
 // ---------------------------------------------------------------- scalar helpers
 // sigmoid / softplus (vec_math.hpp:69-84)

@@ -24,7 +24,8 @@
 
 #include <cstdlib>
 
-#include "nx_internal.cuh"
+#include "nx_grid.cuh"
+#include "nx_tc.cuh"
 
 namespace nx {
 
@@ -32,7 +33,6 @@ namespace {
 
 constexpr int kTcThreads = 128;
 constexpr int kRows = 128;
-constexpr int kLevels = 16;
 constexpr int kIn = 32, kHid = 64, kOut = 48;
 // D1, D2 and D3 share columns 0..63: each is drained (tcgen05.ld + wait + fence +
 // barrier) before the next layer's MMAs overwrite it.
@@ -54,164 +54,6 @@ constexpr int kSmemUsed = kOffTmem + 8;              // ~70.5 KB: three CTAs per
 static_assert(kSmemUsed <= 72 * 1024, "three CTAs per SM");
 constexpr int kCtasPerSm = 3;
 
-struct TcConst {
-    double level_scale[kLevels];  // HashGridConfig::level_scale by iterated product (hash_grid.cpp:7-13)
-    float inv_level_scale[kLevels];
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-// Byte offset of element (row, k) in a K-major no-swizzle operand with K columns (bf16).
-__device__ __forceinline__ uint32_t kmajor_off(int row, int k, int K) {
-    return static_cast<uint32_t>((row >> 3) * (K / 8) * 128 + (k >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2);
-}
-
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-    return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
-           (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);  // version 1, no swizzle
-}
-
-__host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
-           (static_cast<uint32_t>(M >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-
-// try_wait with a suspend-time hint: the warp sleeps until the phase completes (or
-// the hint expires) instead of spinning on issue slots other warps could use.
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
-        "r"(parity), "r"(1000000u)
-        : "memory");
-}
-
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);  // .x = a (low half)
-    return *reinterpret_cast<const uint32_t*>(&h);
-}
-
-// Writes 8 consecutive K values (one 16-byte core-matrix row) as bf16 hi and lo parts:
-// one packed conversion per pair for hi, the hi values re-expanded by shifts (exact),
-// lo = x - hi, one packed conversion per pair for lo.
-__device__ __forceinline__ void store_split8(uint8_t* smem, int off_hi, int off_lo, uint32_t byte_off, const float* x) {
-    uint32_t h[4], l[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        h[i] = pack_bf16(x[2 * i], x[2 * i + 1]);
-        const float h0 = __uint_as_float(h[i] << 16), h1 = __uint_as_float(h[i] & 0xffff0000u);
-        l[i] = pack_bf16(x[2 * i] - h0, x[2 * i + 1] - h1);
-    }
-    *reinterpret_cast<uint4*>(smem + off_hi + byte_off) = make_uint4(h[0], h[1], h[2], h[3]);
-    *reinterpret_cast<uint4*>(smem + off_lo + byte_off) = make_uint4(l[0], l[1], l[2], l[3]);
-}
-
-__device__ __forceinline__ uint32_t map_positive32(long long x) {  // hash_grid.hpp:12-14
-    return x > 0 ? static_cast<uint32_t>(2 * x - 1) : static_cast<uint32_t>(-2 * x);
-}
-
-// One level of grid_lookup (hash_grid.cpp:32-82): lattice cell in fp64/int64 like the
-// reference, the 8 hashed corner rows (hash_cell, hash_grid.hpp:17-23) gathered, the
-// fractional position and the level fade (downweight, hash_grid.hpp:28-31).
-struct LevelFetch {
-    float2 v[8];
-    float fr0, fr1, fr2, dw;
-};
-
-// map_positive for |x| < 2^30: the 32-bit wrap of the reference's 64-bit value.
-__device__ __forceinline__ uint32_t map_positive_small(int x) {
-    return x > 0 ? (static_cast<uint32_t>(x) << 1) - 1u : static_cast<uint32_t>(-x) << 1;
-}
-
-// kSmall: every lattice coordinate of the query fits in 30 bits (checked per query),
-// so the cell index and hash run in 32-bit integers with identical results.
-template <bool kSmall>
-__device__ __forceinline__ LevelFetch fetch_level(int l, double x0, double x1, double x2, const TcConst& cst,
-                                                  const float2* __restrict__ tab, uint32_t T, uint32_t mask, float ft,
-                                                  int no_downweight) {
-    LevelFetch f;
-    const double s = cst.level_scale[l];
-    const double p0 = s * x0, p1 = s * x1, p2 = s * x2;
-    const double fl0 = floor(p0), fl1 = floor(p1), fl2 = floor(p2);
-    f.fr0 = static_cast<float>(p0 - fl0);
-    f.fr1 = static_cast<float>(p1 - fl1);
-    f.fr2 = static_cast<float>(p2 - fl2);
-    f.dw = 1.0f;
-    if (!no_downweight) {
-        const float r = ft * cst.inv_level_scale[l];
-        f.dw = 1.0f - __expf(-r * r * 0.15915494309189535f);
-    }
-    uint32_t ax0, ax1, by0, by1, cz0, cz1;
-    if (kSmall) {
-        const int b0 = static_cast<int>(fl0), b1 = static_cast<int>(fl1), b2 = static_cast<int>(fl2);
-        ax0 = map_positive_small(b0);
-        ax1 = map_positive_small(b0 + 1);
-        by0 = map_positive_small(b1) * 2654435761u;
-        by1 = map_positive_small(b1 + 1) * 2654435761u;
-        cz0 = map_positive_small(b2) * 805459861u;
-        cz1 = map_positive_small(b2 + 1) * 805459861u;
-    } else {
-        const long long b0 = static_cast<long long>(fl0), b1 = static_cast<long long>(fl1),
-                        b2 = static_cast<long long>(fl2);
-        ax0 = map_positive32(b0);
-        ax1 = map_positive32(b0 + 1);
-        by0 = map_positive32(b1) * 2654435761u;
-        by1 = map_positive32(b1 + 1) * 2654435761u;
-        cz0 = map_positive32(b2) * 805459861u;
-        cz1 = map_positive32(b2 + 1) * 805459861u;
-    }
-    const float2* slab = tab + static_cast<size_t>(l) * T;
-#pragma unroll
-    for (int ci = 0; ci < 8; ++ci) {
-        const uint32_t rowi = ((ci & 1) ? ax1 : ax0) ^ ((ci & 2) ? by1 : by0) ^ ((ci & 4) ? cz1 : cz0);
-        f.v[ci] = __ldg(slab + (rowi & mask));
-    }
-    return f;
-}
-
-__device__ __forceinline__ float2 interp(const LevelFetch& f) {
-    const float wx[2] = {1.0f - f.fr0, f.fr0}, wy[2] = {1.0f - f.fr1, f.fr1}, wz[2] = {1.0f - f.fr2, f.fr2};
-    float g0 = 0.f, g1 = 0.f;
-#pragma unroll
-    for (int ci = 0; ci < 8; ++ci) {
-        const float w = wx[ci & 1] * wy[(ci >> 1) & 1] * wz[(ci >> 2) & 1];
-        g0 += w * f.v[ci].x;
-        g1 += w * f.v[ci].y;
-    }
-    return make_float2(g0 * f.dw, g1 * f.dw);
-}
 
 // Issues one layer: D = A . B^T over K (3 split terms per 16-wide k-step), commit.
 __device__ __forceinline__ void issue_layer(uint8_t* smem, uint32_t dtm, int off_bh, int off_bl, int K,

@@ -66,10 +66,13 @@ def compare_grads(gpu, ref, tol=GRAD_TOL):
         pairs[k] = (gpu[i], ref[i])
     if len(gpu) > 5 and gpu[5] is not None and ref[5] is not None:
         pairs["blended_error"] = (gpu[5], ref[5])
+    bad = []
     for k, (a, b) in pairs.items():
         scale = float(np.abs(b).max()) if b.size else 0.0
         err = float(np.abs(a - b).max()) if a.size else 0.0
         rep[k] = (err / scale) if scale > 0 else err
         assert np.all(np.isfinite(a)), f"{k}: non-finite gradients"
-        assert rep[k] <= tol or err <= 1e-12, f"{k}: max err {err:.3e} vs scale {scale:.3e}"
+        if not (rep[k] <= tol or err <= 1e-12):
+            bad.append(f"{k}: max err {err:.3e} vs scale {scale:.3e}")
+    assert not bad, "; ".join(bad) + " | " + str({k: f"{v:.1e}" for k, v in rep.items()})
     return rep

@@ -94,6 +94,31 @@ def test_stump_textured_gradients_match_reference(renderer, reference):
     print({k: f"{v:.1e}" for k, v in rep.items()})
 
 
+@pytest.mark.parametrize("n,view,size,grid_init,ablation", [
+    (10_000, 0, (256, 256), 1e-4, None),          # BASELINE config 1 shape
+    (10_000, 17, (160, 120), 1e-1, None),
+    (4_000, 40, (128, 96), 1e-1, "no_downweight"),
+    (4_000, 90, (128, 96), 1e-1, "no_prim_sh"),
+    (4_000, 130, (128, 96), 1e-1, "no_gamma"),
+    (4_000, 200, (128, 96), 1e-1, "k4"),
+])
+def test_stump_field_tc_gradients_match_reference(renderer, reference, n, view, size, grid_init, ablation):
+    # the reference field shape (16 levels x 2 x 64 hidden) takes the tcgen05 field backward
+    scene = nx.stump_like(n, log2_table=16, grid_init=grid_init)
+    st = scene.settings
+    if ablation == "k4":
+        st.top_k = 4
+    elif ablation:
+        setattr(st, ablation, True)
+    cam = nx.ring_camera(view, 256, *size)
+    up = upstream(cam, st.top_k, view)
+    err = np.random.default_rng(view).random(cam.width * cam.height)
+    g, _, _ = gpu_backward(renderer, scene, cam, up, err)
+    r = ref_backward(reference, scene, cam, up, err)
+    rep = compare_grads(g, r)
+    print(n, view, ablation, {k: f"{v:.1e}" for k, v in rep.items()})
+
+
 def test_backward_accumulates_like_the_reference(renderer, reference):
     scene, cam = reference.random_scene(31, 40, 2, 32, 40.0, 3.0)
     up = upstream(cam, 2, 31)
@@ -105,9 +130,9 @@ def test_backward_accumulates_like_the_reference(renderer, reference):
     renderer.render_backward(ds, cam, fr, up, g)
     once = [a.copy() for a in (g.prims, g.table, g.w1, g.w2, g.w3)]
     renderer.render_backward(ds, cam, fr, up, g)
-    # fp64 atomics: the second pass may round in a different order (ulp level)
+    # the accumulation order of the atomics may differ between the passes (fp32 tile sums)
     for a, b in zip((g.prims, g.table, g.w1, g.w2, g.w3), once):
-        assert np.allclose(a, 2 * b, rtol=1e-9, atol=1e-12 * max(np.abs(b).max(), 1e-300))
+        assert np.allclose(a, 2 * b, rtol=1e-6, atol=1e-9 * max(np.abs(b).max(), 1e-300))
 
 
 def test_backward_needs_the_forward_state(renderer, reference):
