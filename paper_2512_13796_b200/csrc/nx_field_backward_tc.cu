@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "nx_composite.cuh"
 #include "nx_grid.cuh"
 #include "nx_tc.cuh"
 
@@ -47,6 +48,9 @@ constexpr int kC1 = 128, kC2 = 112, kC3 = 128;  // columns of the combined buffe
 constexpr int kWGrads = kHid * kIn + kHid * kHid + kOut * kHid;  // 9216 partial values per CTA
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kColD = 0, kColG1 = 64, kColG2 = 176;
+// Per-slot scratch row (floats): [0, 32) features F, overwritten by dL/dF; [32, 37) the
+// ReLU / SH-clamp masks of the exact fp32 forward (m1 lo/hi, m2 lo/hi, clamp bits).
+constexpr int kStride = 40;
 
 // shared-memory carve-up (bytes); every region 1 KB aligned
 constexpr int kOffW1h = 0;
@@ -67,10 +71,39 @@ constexpr int kSmemM = kOffTmem + 8;
 static_assert(kSmemM <= 227 * 1024, "fits one CTA per SM");
 
 // ---------------------------------------------------------------- G: features
+// The ReLU masks and the SH clamp mask decide which gradients pass (mlp.cpp:67-68,
+// 79-80; sh.hpp:70). They come from an exact fp32 forward on the CUDA cores here, so
+// that they agree with the reference's fp64 forward except for pre-activations within
+// ~1e-7 of zero; the split-bf16 tensor-core forward (~1e-5) would flip ~1e-4 of them.
+// A mask bit is "ambiguous" when its fp32 pre-activation lies within the fp32 error
+// bound (2^-15 ||a||_1 max|w|) of the threshold; those slots are listed and re-decided
+// in fp64 by mask_fp64_kernel, so the masks agree with the reference's fp64 forward.
 __global__ void __launch_bounds__(128) features_kernel(const FieldBwdArgs a, const TcConst cst, float* __restrict__ fbuf,
-                                                       int64_t total) {
+                                                       int64_t total, int32_t* __restrict__ amb_list,
+                                                       int32_t* __restrict__ amb_count) {
+    __shared__ float sW[kHid * kIn + kHid * kHid + kOut * kHid];
+    __shared__ float sMax[kHid + kHid + 1];
+    float* sW1 = sW;
+    float* sW2 = sW1 + kHid * kIn;
+    float* sW3 = sW2 + kHid * kHid;
+    for (int e = threadIdx.x; e < kHid * kIn; e += blockDim.x) sW1[e] = __ldg(a.scene.w1 + e);
+    for (int e = threadIdx.x; e < kHid * kHid; e += blockDim.x) sW2[e] = __ldg(a.scene.w2 + e);
+    for (int e = threadIdx.x; e < kOut * kHid; e += blockDim.x) sW3[e] = __ldg(a.scene.w3 + e);
+    __syncthreads();
+    for (int o = threadIdx.x; o < 2 * kHid + 1; o += blockDim.x) {
+        float m = 0.f;
+        if (o < kHid)
+            for (int i = 0; i < kIn; ++i) m = fmaxf(m, fabsf(sW1[o * kIn + i]));
+        else if (o < 2 * kHid)
+            for (int i = 0; i < kHid; ++i) m = fmaxf(m, fabsf(sW2[(o - kHid) * kHid + i]));
+        else
+            for (int i = 0; i < kOut * kHid; ++i) m = fmaxf(m, fabsf(sW3[i]));
+        sMax[o] = m;
+    }
+    __syncthreads();
     const int64_t sl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (sl >= total) return;
+    uint32_t masks[5] = {0u, 0u, 0u, 0u, 0u};
     float feats[kIn];
 #pragma unroll
     for (int i = 0; i < kIn; ++i) feats[i] = 0.f;
@@ -106,9 +139,139 @@ __global__ void __launch_bounds__(128) features_kernel(const FieldBwdArgs a, con
             }
         }
     }
-    float4* dst = reinterpret_cast<float4*>(fbuf + sl * kIn);
+    if (a.fb.ids[sl] >= 0) {
+        // exact fp32 forward (TextureMlp::forward, mlp.cpp:24-43) for the masks only
+        float h1[kHid], h2[kHid];
+        bool amb = false;
+        float n1 = 0.f, n2 = 0.f, n3 = 0.f;
+#pragma unroll
+        for (int i = 0; i < kIn; ++i) n1 += fabsf(feats[i]);
+#pragma unroll 4
+        for (int o = 0; o < kHid; ++o) {
+            float acc = 0.f;
+#pragma unroll
+            for (int i = 0; i < kIn; ++i) acc = fmaf(sW1[o * kIn + i], feats[i], acc);
+            if (acc > 0.f) masks[o >> 5] |= 1u << (o & 31);
+            amb |= fabsf(acc) <= 3.05e-5f * n1 * sMax[o];
+            h1[o] = fmaxf(acc, 0.f);
+            n2 += h1[o];
+        }
+#pragma unroll 4
+        for (int o = 0; o < kHid; ++o) {
+            float acc = 0.f;
+#pragma unroll
+            for (int i = 0; i < kHid; ++i) acc = fmaf(sW2[o * kHid + i], h1[i], acc);
+            if (acc > 0.f) masks[2 + (o >> 5)] |= 1u << (o & 31);
+            amb |= fabsf(acc) <= 3.05e-5f * n2 * sMax[kHid + o];
+            h2[o] = fmaxf(acc, 0.f);
+            n3 += h2[o];
+        }
+        const int64_t pix = sl / a.fb.K;
+        double dir[3];
+        pixel_dir(a.cam, static_cast<int>(pix % a.cam.W) + 0.5, static_cast<int>(pix / a.cam.W) + 0.5, dir);
+        float b[16];
+        sh_basis_f32(static_cast<float>(dir[0]), static_cast<float>(dir[1]), static_cast<float>(dir[2]), b);
+        float c3[3] = {0.5f, 0.5f, 0.5f};
+#pragma unroll 1
+        for (int o = 0; o < kOut; ++o) {
+            float acc = 0.f;
+#pragma unroll
+            for (int i = 0; i < kHid; ++i) acc = fmaf(sW3[o * kHid + i], h2[i], acc);
+            c3[o % 3] = fmaf(acc, b[o / 3], c3[o % 3]);
+        }
+        masks[4] = (c3[0] >= 0.f ? 1u : 0u) | (c3[1] >= 0.f ? 2u : 0u) | (c3[2] >= 0.f ? 4u : 0u);
+        float bsum = 0.f;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) bsum += fabsf(b[k]);
+        const float bound3 = 6.1e-5f * n3 * sMax[2 * kHid] * bsum;
+        amb |= fabsf(c3[0]) <= bound3 || fabsf(c3[1]) <= bound3 || fabsf(c3[2]) <= bound3;
+        if (amb) amb_list[atomicAdd(amb_count, 1)] = static_cast<int32_t>(sl);
+    }
+    float4* dst = reinterpret_cast<float4*>(fbuf + sl * kStride);
 #pragma unroll
     for (int q = 0; q < kIn / 4; ++q) dst[q] = make_float4(feats[4 * q], feats[4 * q + 1], feats[4 * q + 2], feats[4 * q + 3]);
+    dst[kIn / 4] = make_float4(__uint_as_float(masks[0]), __uint_as_float(masks[1]), __uint_as_float(masks[2]),
+                               __uint_as_float(masks[3]));
+    dst[kIn / 4 + 1] = make_float4(__uint_as_float(masks[4]), 0.f, 0.f, 0.f);
+}
+
+// The listed slots' masks re-decided with the reference's fp64 forward: grid_lookup
+// (hash_grid.cpp:26-83) and TextureMlp::forward (mlp.cpp:24-43) in fp64, eval_sh_cached's
+// clamp (sh.hpp:61-73).
+__global__ void __launch_bounds__(128) mask_fp64_kernel(const FieldBwdArgs a, const int32_t* __restrict__ amb_list,
+                                                        const int32_t* __restrict__ amb_count, float* __restrict__ fbuf) {
+    const int n = *amb_count;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        const int64_t sl = amb_list[q];
+        const nx_field_desc& fd = a.scene.field;
+        const int64_t pix = sl / a.fb.K;
+        double dir[3];
+        pixel_dir(a.cam, static_cast<int>(pix % a.cam.W) + 0.5, static_cast<int>(pix / a.cam.W) + 0.5, dir);
+        const double t = a.fb.depths[sl];
+        const double x[3] = {a.cam.o[0] + t * dir[0], a.cam.o[1] + t * dir[1], a.cam.o[2] + t * dir[2]};
+        const uint32_t T = 1u << fd.log2_table, mask = T - 1u;
+        double feats[kIn];
+        double s = fd.base_scale;
+        for (int l = 0; l < kLevels; ++l, s *= fd.growth) {
+            const double p0 = s * x[0], p1 = s * x[1], p2 = s * x[2];
+            const double fl0 = floor(p0), fl1 = floor(p1), fl2 = floor(p2);
+            const long long b0 = static_cast<long long>(fl0), b1 = static_cast<long long>(fl1),
+                            b2 = static_cast<long long>(fl2);
+            const double fr[3] = {p0 - fl0, p1 - fl1, p2 - fl2};
+            double dw = 1.0;
+            if (!a.st.no_downweight) {
+                const double r = a.cam.fx / (s * t);
+                dw = 1.0 - exp(-r * r / (2.0 * M_PI));
+            }
+            double g0 = 0.0, g1 = 0.0;
+            for (int ci = 0; ci < 8; ++ci) {
+                const uint32_t row = (map_positive32(b0 + (ci & 1)) ^ (map_positive32(b1 + ((ci >> 1) & 1)) * 2654435761u) ^
+                                      (map_positive32(b2 + ((ci >> 2) & 1)) * 805459861u)) & mask;
+                const double cw = ((ci & 1) ? fr[0] : 1.0 - fr[0]) * ((ci & 2) ? fr[1] : 1.0 - fr[1]) *
+                                  ((ci & 4) ? fr[2] : 1.0 - fr[2]);
+                const float2 v = __ldg(reinterpret_cast<const float2*>(a.scene.table) + static_cast<size_t>(l) * T + row);
+                g0 += cw * v.x;
+                g1 += cw * v.y;
+            }
+            feats[2 * l] = g0 * dw;
+            feats[2 * l + 1] = g1 * dw;
+        }
+        uint32_t masks[5] = {0u, 0u, 0u, 0u, 0u};
+        double h1[kHid], h2[kHid];
+        for (int o = 0; o < kHid; ++o) {
+            double acc = 0.0;
+            for (int i = 0; i < kIn; ++i) acc += static_cast<double>(__ldg(a.scene.w1 + o * kIn + i)) * feats[i];
+            if (acc > 0.0) masks[o >> 5] |= 1u << (o & 31);
+            h1[o] = acc > 0.0 ? acc : 0.0;
+        }
+        for (int o = 0; o < kHid; ++o) {
+            double acc = 0.0;
+            for (int i = 0; i < kHid; ++i) acc += static_cast<double>(__ldg(a.scene.w2 + o * kHid + i)) * h1[i];
+            if (acc > 0.0) masks[2 + (o >> 5)] |= 1u << (o & 31);
+            h2[o] = acc > 0.0 ? acc : 0.0;
+        }
+        const double xx = dir[0] * dir[0], yy = dir[1] * dir[1], zz = dir[2] * dir[2];
+        const double dx = dir[0], dy = dir[1], dz = dir[2];
+        const double b[16] = {0.28209479177387814, -0.4886025119029199 * dy, 0.4886025119029199 * dz,
+                              -0.4886025119029199 * dx, 1.0925484305920792 * dx * dy, -1.0925484305920792 * dy * dz,
+                              0.31539156525252005 * (2.0 * zz - xx - yy), -1.0925484305920792 * dx * dz,
+                              0.5462742152960396 * (xx - yy), -0.5900435899266435 * dy * (3.0 * xx - yy),
+                              2.890611442640554 * dx * dy * dz, -0.4570457994644658 * dy * (4.0 * zz - xx - yy),
+                              0.3731763325901154 * dz * (2.0 * zz - 3.0 * xx - 3.0 * yy),
+                              -0.4570457994644658 * dx * (4.0 * zz - xx - yy), 1.445305721320277 * dz * (xx - yy),
+                              -0.5900435899266435 * dx * (xx - 3.0 * yy)};
+        double c3[3] = {0.5, 0.5, 0.5};
+        for (int o = 0; o < kOut; ++o) {
+            double acc = 0.0;
+            for (int i = 0; i < kHid; ++i) acc += static_cast<double>(__ldg(a.scene.w3 + o * kHid + i)) * h2[i];
+            c3[o % 3] += acc * b[o / 3];
+        }
+        masks[4] = (c3[0] >= 0.0 ? 1u : 0u) | (c3[1] >= 0.0 ? 2u : 0u) | (c3[2] >= 0.0 ? 4u : 0u);
+        float4* dst = reinterpret_cast<float4*>(fbuf + sl * kStride);
+        dst[kIn / 4] = make_float4(__uint_as_float(masks[0]), __uint_as_float(masks[1]), __uint_as_float(masks[2]),
+                                   __uint_as_float(masks[3]));
+        dst[kIn / 4 + 1] = make_float4(__uint_as_float(masks[4]), 0.f, 0.f, 0.f);
+    }
 }
 
 // ---------------------------------------------------------------- M: MLP forward + backward on tcgen05
@@ -186,8 +349,7 @@ __global__ void __launch_bounds__(kThreadsM, 1) mlp_bwd_tc_kernel(const FieldBwd
     const int row = tid;
 
     // operand views
-    const Opnd W1k = kmaj(smem, kOffW1h, kOffW1l, kIn, 0), W2k = kmaj(smem, kOffW2h, kOffW2l, kHid, 0),
-               W3k = kmaj(smem, kOffW3h, kOffW3l, kHid, 0);
+    const Opnd W1k = kmaj(smem, kOffW1h, kOffW1l, kIn, 0), W2k = kmaj(smem, kOffW2h, kOffW2l, kHid, 0);
     const Opnd W1t = mnmaj(smem, kOffW1h, kOffW1l, kIn, 0), W2t = mnmaj(smem, kOffW2h, kOffW2l, kHid, 0),
                W3t = mnmaj(smem, kOffW3h, kOffW3l, kHid, 0);
     const Opnd F_k = kmaj(smem, kOffC3h, kOffC3l, kC3, 64), H1_k = kmaj(smem, kOffC2h, kOffC2l, kC2, 48),
@@ -195,7 +357,7 @@ __global__ void __launch_bounds__(kThreadsM, 1) mlp_bwd_tc_kernel(const FieldBwd
                dH2_k = kmaj(smem, kOffC1h, kOffC1l, kC1, 64), dH1_k = kmaj(smem, kOffC3h, kOffC3l, kC3, 0);
     const Opnd C1_t = mnmaj(smem, kOffC1h, kOffC1l, kC1, 0), C2_t = mnmaj(smem, kOffC2h, kOffC2l, kC2, 0),
                C3_t = mnmaj(smem, kOffC3h, kOffC3l, kC3, 0), F_t = mnmaj(smem, kOffC3h, kOffC3l, kC3, 64);
-    constexpr uint32_t kI64 = idesc_bf16_f32(kRows, 64), kI48 = idesc_bf16_f32(kRows, 48);
+    constexpr uint32_t kI64 = idesc_bf16_f32(kRows, 64);
     constexpr uint32_t kI64b = idesc_bf16_f32(kRows, 64, false, true), kI32b = idesc_bf16_f32(kRows, 32, false, true);
     constexpr uint32_t kIG1 = idesc_bf16_f32(kRows, kC2, true, true), kIG2 = idesc_bf16_f32(kRows, 32, true, true);
 
@@ -209,8 +371,10 @@ __global__ void __launch_bounds__(kThreadsM, 1) mlp_bwd_tc_kernel(const FieldBwd
         float b[16];
 #pragma unroll
         for (int i = 0; i < kIn; ++i) x[i] = 0.f;
+        uint64_t m1 = 0, m2 = 0;
+        uint32_t shm = 0;
         if (valid) {
-            const float4* src = reinterpret_cast<const float4*>(fbuf + sl * kIn);
+            const float4* src = reinterpret_cast<const float4*>(fbuf + sl * kStride);
 #pragma unroll
             for (int q = 0; q < kIn / 4; ++q) {
                 const float4 v = src[q];
@@ -219,6 +383,10 @@ __global__ void __launch_bounds__(kThreadsM, 1) mlp_bwd_tc_kernel(const FieldBwd
                 x[4 * q + 2] = v.z;
                 x[4 * q + 3] = v.w;
             }
+            const float4 mk = src[kIn / 4];
+            m1 = static_cast<uint64_t>(__float_as_uint(mk.x)) | (static_cast<uint64_t>(__float_as_uint(mk.y)) << 32);
+            m2 = static_cast<uint64_t>(__float_as_uint(mk.z)) | (static_cast<uint64_t>(__float_as_uint(mk.w)) << 32);
+            shm = __float_as_uint(src[kIn / 4 + 1].x);
             const int64_t pix = sl / K;
             const double w = a.fb.weights[sl];
 #pragma unroll
@@ -267,16 +435,12 @@ __global__ void __launch_bounds__(kThreadsM, 1) mlp_bwd_tc_kernel(const FieldBwd
         mbar_wait(bar, phase);
         phase ^= 1;
         tc_fence_after();
-        uint64_t m1 = 0, m2 = 0;
 #pragma unroll
         for (int c = 0; c < kHid / 16; ++c) {
             float v[16];
             tmem_ld16(tD + 16 * c, v);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                if (v[i] > 0.f) m1 |= 1ull << (16 * c + i);
-                v[i] = fmaxf(v[i], 0.f);
-            }
+            for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
             store_split8(smem, kOffC2h, kOffC2l, kmajor_off(row, 48 + 16 * c, kC2), v);
             store_split8(smem, kOffC2h, kOffC2l, kmajor_off(row, 48 + 16 * c + 8, kC2), v + 8);
         }
@@ -297,35 +461,16 @@ __global__ void __launch_bounds__(kThreadsM, 1) mlp_bwd_tc_kernel(const FieldBwd
             float v[16];
             tmem_ld16(tD + 16 * c, v);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                if (v[i] > 0.f) m2 |= 1ull << (16 * c + i);
-                v[i] = fmaxf(v[i], 0.f);
-            }
+            for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
             store_split8(smem, kOffC1h, kOffC1l, kmajor_off(row, 16 * c, kC1), v);
             store_split8(smem, kOffC1h, kOffC1l, kmajor_off(row, 16 * c + 8, kC1), v + 8);
         }
-        fence_async_smem();
-        tc_fence_before();
-        __syncthreads();
-        // ---- L3: Y = H2 . W3^T; SH clamp mask and dY = dL/dcoeffs -> C2[:, 0..47]
-        if (tid == 0) {
-            tc_fence_after();
-            issue_mma(tmem + kColD, H2_k, W3k, kHid / 16, kI48, false);
-            mma_commit(bar);
-        }
-        mbar_wait(bar, phase);
-        phase ^= 1;
-        tc_fence_after();
+        // ---- dY = dL/dcoeffs (eval_sh_backward, sh.hpp:76-83) with the exact clamp mask -> C2[:, 0..47]
+        // (the coefficients themselves are not needed: Y only decides the clamp mask)
         {
-            float y[kOut];
-#pragma unroll
-            for (int c = 0; c < kOut / 16; ++c) tmem_ld16(tD + 16 * c, y + 16 * c);
-            float acc[3] = {0.5f, 0.5f, 0.5f};
-#pragma unroll
-            for (int o = 0; o < kOut; ++o) acc[o % 3] = fmaf(y[o], b[o / 3], acc[o % 3]);
             float dyv[kOut];
 #pragma unroll
-            for (int o = 0; o < kOut; ++o) dyv[o] = acc[o % 3] >= 0.f ? drgb[o % 3] * b[o / 3] : 0.f;
+            for (int o = 0; o < kOut; ++o) dyv[o] = (shm >> (o % 3)) & 1u ? drgb[o % 3] * b[o / 3] : 0.f;
 #pragma unroll
             for (int c = 0; c < kOut / 8; ++c) store_split8(smem, kOffC2h, kOffC2l, kmajor_off(row, 8 * c, kC2), dyv + 8 * c);
         }
@@ -390,7 +535,7 @@ __global__ void __launch_bounds__(kThreadsM, 1) mlp_bwd_tc_kernel(const FieldBwd
             tmem_ld16(tD, v);
             tmem_ld16(tD + 16, v + 16);
             if (valid) {
-                float4* dst = reinterpret_cast<float4*>(fbuf + sl * kIn);
+                float4* dst = reinterpret_cast<float4*>(fbuf + sl * kStride);
 #pragma unroll
                 for (int q = 0; q < kIn / 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
             }
@@ -536,7 +681,7 @@ __global__ void __launch_bounds__(128) scatter_kernel(const FieldBwdArgs a, cons
         x0 = a.cam.o[0] + t * dir[0];
         x1 = a.cam.o[1] + t * dir[1];
         x2 = a.cam.o[2] + t * dir[2];
-        const float4* src = reinterpret_cast<const float4*>(fbuf + sl * kIn);
+        const float4* src = reinterpret_cast<const float4*>(fbuf + sl * kStride);
 #pragma unroll
         for (int q = 0; q < kIn / 4; ++q) {
             const float4 v = src[q];
@@ -561,6 +706,8 @@ __global__ void __launch_bounds__(128) scatter_kernel(const FieldBwdArgs a, cons
 struct Scratch {
     float* fbuf = nullptr;
     size_t fcap = 0;
+    int32_t* amb = nullptr;  // [0] count, [1..] listed slots
+    size_t acap = 0;
     float* parts = nullptr;
     size_t pcap = 0;
 };
@@ -579,7 +726,7 @@ int launch_field_backward_tc(const FieldBwdArgs& a, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     Scratch& sc = g_scratch[dev & 63];
-    const size_t fneed = static_cast<size_t>(total) * kIn;
+    const size_t fneed = static_cast<size_t>(total) * kStride;
     const int64_t n_tiles = (total + kRows - 1) / kRows;
     const int grid_m = static_cast<int>(std::min<int64_t>(n_tiles, sms));
     const size_t pneed = static_cast<size_t>(grid_m) * kWGrads;
@@ -589,6 +736,13 @@ int launch_field_backward_tc(const FieldBwdArgs& a, cudaStream_t s) {
         sc.fcap = 0;
         if (cudaMalloc(&sc.fbuf, fneed * sizeof(float)) != cudaSuccess) return NX_OUT_OF_MEMORY;
         sc.fcap = fneed;
+    }
+    if (static_cast<size_t>(total) + 1 > sc.acap) {
+        if (sc.amb) cudaFree(sc.amb);
+        sc.amb = nullptr;
+        sc.acap = 0;
+        if (cudaMalloc(&sc.amb, (total + 1) * sizeof(int32_t)) != cudaSuccess) return NX_OUT_OF_MEMORY;
+        sc.acap = total + 1;
     }
     if (pneed > sc.pcap) {
         if (sc.parts) cudaFree(sc.parts);
@@ -604,8 +758,10 @@ int launch_field_backward_tc(const FieldBwdArgs& a, cudaStream_t s) {
         cst.inv_level_scale[l] = static_cast<float>(1.0 / scale);
     }
     const unsigned blocks = static_cast<unsigned>((total + 127) / 128);
-    count_launch(4);
-    features_kernel<<<blocks, 128, 0, s>>>(a, cst, sc.fbuf, total);
+    count_launch(5);
+    cudaMemsetAsync(sc.amb, 0, sizeof(int32_t), s);
+    features_kernel<<<blocks, 128, 0, s>>>(a, cst, sc.fbuf, total, sc.amb + 1, sc.amb);
+    mask_fp64_kernel<<<2 * sms, 128, 0, s>>>(a, sc.amb + 1, sc.amb, sc.fbuf);
     cudaFuncSetAttribute(mlp_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemM);
     mlp_bwd_tc_kernel<<<grid_m, kThreadsM, kSmemM, s>>>(a, sc.fbuf, sc.parts, total, n_tiles);
     reduce_wgrads_kernel<<<(kWGrads + 255) / 256, 256, 0, s>>>(sc.parts, grid_m, a.g_w1, a.g_w2, a.g_w3);

@@ -53,6 +53,12 @@ def is_subsequence(sub, full):
 # fp64 atomics, so gradients agree to ~1e-7 of each array's scale. The bar below is
 # GRAD_TOL of the array's largest magnitude, per gradient group.
 GRAD_TOL = 1e-5
+# The reference field shape takes the tensor-core field backward: MLP products from
+# bf16 operands with the 3-term split (relative error <= ~2^-16 per product, fp32
+# accumulation) while every ReLU / clamp mask is decided like the reference (exact
+# fp32 forward, fp64 re-decision of ambiguous slots). Field-driven gradients then agree
+# to a few 1e-5 of each array's scale.
+GRAD_TOL_TC = 5e-5
 GROUPS = {"mu": slice(0, 3), "quat": slice(3, 7), "log_scale": slice(7, 9), "opacity": slice(9, 10),
           "gamma": slice(10, 12), "sh": slice(12, 60)}
 
