@@ -589,77 +589,90 @@ __global__ void reduce_wgrads_kernel(const float* __restrict__ partials, int n_p
 }
 
 // ---------------------------------------------------------------- S: grid_lookup_backward
-__device__ __forceinline__ double warp_sum_d(double v) {
+__device__ __forceinline__ float warp_sum_f(float v) {
 #pragma unroll
-    for (int m = 16; m > 0; m >>= 1)
-        v += __hiloint2double(__shfl_xor_sync(0xffffffffu, __double2hiint(v), m),
-                              __shfl_xor_sync(0xffffffffu, __double2loint(v), m));
+    for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
     return v;
 }
 
+// grid_lookup_backward (hash_grid.hpp:85-124) in two phases: (1) the position / fade
+// gradient, which needs the table values — gathered two levels deep in flight, no
+// atomics in between; (2) the table gradients, which need only the corner rows and
+// weights — one fp64 atomic per warp where the warp shares the cell (the heavily shared
+// coarse levels), else one float2 vector atomic per lane into an fp32 copy merged into
+// the fp64 gradients afterwards (fine levels: few contributions per row, half the bytes).
 template <bool kSmall>
 __device__ __forceinline__ void scatter_levels(const FieldBwdArgs& a, const TcConst& cst, bool valid, double x0,
                                                double x1, double x2, float ft, const float* g, double t, double* dx,
-                                               double& dt, uint32_t vmask, int leader) {
+                                               double& dt, int leader, float2* __restrict__ tg32) {
     const uint32_t T = 1u << a.scene.field.log2_table, mask = T - 1u;
     const float2* tab = reinterpret_cast<const float2*>(a.scene.table);
     const int lane = threadIdx.x & 31;
-#pragma unroll 1
-    for (int l = 0; l < kLevels; ++l) {
-        const LevelCell c = level_cell<kSmall>(l, x0, x1, x2, cst, mask, ft, a.st.no_downweight);
-        const float g0 = g[2 * l], g1 = g[2 * l + 1];
-        const float wx[2] = {1.0f - c.fr0, c.fr0}, wy[2] = {1.0f - c.fr1, c.fr1}, wz[2] = {1.0f - c.fr2, c.fr2};
-        const size_t slab = static_cast<size_t>(l) * T;
-        // position / fade gradients in fp64: the corner terms cancel (finite differences
-        // of the table across the cell) and are then scaled by s_l (up to 2^11)
-        double dp0 = 0.0, dp1 = 0.0, dp2 = 0.0, d_dw = 0.0;
-        const double fx[2] = {1.0 - static_cast<double>(c.fr0), c.fr0}, fy[2] = {1.0 - static_cast<double>(c.fr1), c.fr1},
-                     fz[2] = {1.0 - static_cast<double>(c.fr2), c.fr2};
-        float2 v[8];
+    // ---- phase 1: d_x, d_t
+    LevelFetch cur = fetch_level<kSmall>(0, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
 #pragma unroll
-        for (int ci = 0; ci < 8; ++ci) v[ci] = valid ? __ldg(tab + slab + c.row[ci]) : make_float2(0.f, 0.f);
+    for (int l = 0; l < kLevels; ++l) {
+        LevelFetch nxt;
+        if (l + 1 < kLevels) nxt = fetch_level<kSmall>(l + 1, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
+        const float g0 = g[2 * l], g1 = g[2 * l + 1];
+        const float wx[2] = {1.0f - cur.fr0, cur.fr0}, wy[2] = {1.0f - cur.fr1, cur.fr1},
+                    wz[2] = {1.0f - cur.fr2, cur.fr2};
+        float dp0 = 0.f, dp1 = 0.f, dp2 = 0.f, d_dw = 0.f;
 #pragma unroll
         for (int ci = 0; ci < 8; ++ci) {
             const float ax = wx[ci & 1], ay = wy[(ci >> 1) & 1], az = wz[(ci >> 2) & 1];
-            const float cw = ax * ay * az;
-            // table gradient: dL/dtable[row][f] += g[f] * dw * corner_w (hash_grid.hpp:99-103)
-            const double u0 = valid ? static_cast<double>(g0 * c.dw * cw) : 0.0;
-            const double u1 = valid ? static_cast<double>(g1 * c.dw * cw) : 0.0;
-            const uint32_t lr = __shfl_sync(0xffffffffu, c.row[ci], leader);
-            const bool uniform = __all_sync(0xffffffffu, !valid || c.row[ci] == lr);
-            double* dst = a.g_table + (slab + c.row[ci]) * 2;
-            if (uniform) {
-                const double s0 = warp_sum_d(u0), s1 = warp_sum_d(u1);
-                if (lane == leader) {
-                    if (s0 != 0.0) atomicAdd(dst, s0);
-                    if (s1 != 0.0) atomicAdd(dst + 1, s1);
-                }
-            } else if (valid) {
-                if (u0 != 0.0) atomicAdd(dst, u0);
-                if (u1 != 0.0) atomicAdd(dst + 1, u1);
-            }
-            const double gdotf = static_cast<double>(g0) * v[ci].x + static_cast<double>(g1) * v[ci].y;
-            const double updotf = gdotf * c.dw;
-            const double bx = fx[ci & 1], by = fy[(ci >> 1) & 1], bz = fz[(ci >> 2) & 1];
-            dp0 += updotf * ((ci & 1) ? by * bz : -(by * bz));
-            dp1 += updotf * ((ci & 2) ? bx * bz : -(bx * bz));
-            dp2 += updotf * ((ci & 4) ? bx * by : -(bx * by));
-            d_dw += gdotf * (bx * by * bz);
+            const float gdotf = g0 * cur.v[ci].x + g1 * cur.v[ci].y;
+            const float updotf = gdotf * cur.dw;
+            dp0 += updotf * ((ci & 1) ? ay * az : -(ay * az));
+            dp1 += updotf * ((ci & 2) ? ax * az : -(ax * az));
+            dp2 += updotf * ((ci & 4) ? ax * ay : -(ax * ay));
+            d_dw += gdotf * (ax * ay * az);
         }
-        const double s = cst.level_scale[l];
-        dx[0] += s * dp0;
-        dx[1] += s * dp1;
-        dx[2] += s * dp2;
+        const double sl = cst.level_scale[l];
+        dx[0] += sl * dp0;
+        dx[1] += sl * dp1;
+        dx[2] += sl * dp2;
         if (!a.st.no_downweight) {
-            const double r = a.cam.fx / (s * t);
-            dt += d_dw * (static_cast<double>(c.dw) - 1.0) * r * r / (M_PI * t);
+            // downweight_grad_t via the cached factor (hash_grid.hpp:117-121)
+            const double r = a.cam.fx / (sl * t);
+            dt += static_cast<double>(d_dw) * (static_cast<double>(cur.dw) - 1.0) * r * r / (M_PI * t);
+        }
+        if (l + 1 < kLevels) cur = nxt;
+    }
+    // ---- phase 2: table gradients dL/dtable[row][f] += g[f] * dw * corner_w (hash_grid.hpp:99-103)
+#pragma unroll 1
+    for (int l = 0; l < kLevels; ++l) {
+        const LevelCell c = level_cell<kSmall>(l, x0, x1, x2, cst, mask, ft, a.st.no_downweight);
+        const float g0 = valid ? g[2 * l] * c.dw : 0.f, g1 = valid ? g[2 * l + 1] * c.dw : 0.f;
+        const float wx[2] = {1.0f - c.fr0, c.fr0}, wy[2] = {1.0f - c.fr1, c.fr1}, wz[2] = {1.0f - c.fr2, c.fr2};
+        double* slab = a.g_table + static_cast<size_t>(l) * T * 2;
+        float2* slab32 = tg32 + static_cast<size_t>(l) * T;
+        // the whole warp in one cell (coarse levels): one atomic per corner and feature
+        bool same = true;
+#pragma unroll
+        for (int ci = 0; ci < 8; ++ci) same &= c.row[ci] == __shfl_sync(0xffffffffu, c.row[ci], leader);
+        const bool uniform = __all_sync(0xffffffffu, !valid || same);
+#pragma unroll
+        for (int ci = 0; ci < 8; ++ci) {
+            const float cw = wx[ci & 1] * wy[(ci >> 1) & 1] * wz[(ci >> 2) & 1];
+            const float u0 = g0 * cw, u1 = g1 * cw;
+            double* dst = slab + static_cast<size_t>(c.row[ci]) * 2;
+            if (uniform) {
+                const float s0 = warp_sum_f(u0), s1 = warp_sum_f(u1);
+                if (lane == leader) {
+                    if (s0 != 0.f) atomicAdd(dst, static_cast<double>(s0));
+                    if (s1 != 0.f) atomicAdd(dst + 1, static_cast<double>(s1));
+                }
+            } else if (valid && (u0 != 0.f || u1 != 0.f)) {
+                atomicAdd(slab32 + c.row[ci], make_float2(u0, u1));
+            }
         }
     }
-    (void)vmask;
 }
 
 __global__ void __launch_bounds__(128) scatter_kernel(const FieldBwdArgs a, const TcConst cst,
-                                                      const float* __restrict__ fbuf, int64_t total) {
+                                                      const float* __restrict__ fbuf, int64_t total,
+                                                      float2* __restrict__ tg32) {
     const int64_t sl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool in = sl < total;
     const bool valid = in && a.fb.ids[sl] >= 0;
@@ -690,17 +703,27 @@ __global__ void __launch_bounds__(128) scatter_kernel(const FieldBwdArgs a, cons
             g[4 * q + 2] = v.z;
             g[4 * q + 3] = v.w;
         }
-    } else {  // inactive lanes follow the leader's cell so that uniform levels stay uniform
-        x0 = x1 = x2 = 0.0;
     }
     const float ft = static_cast<float>(a.cam.fx / t);
     double dx[3] = {0.0, 0.0, 0.0}, dt = 0.0;
     const bool small = fmax(fabs(x0), fmax(fabs(x1), fabs(x2))) * cst.level_scale[kLevels - 1] < 1073741824.0;
     if (__all_sync(0xffffffffu, small))
-        scatter_levels<true>(a, cst, valid, x0, x1, x2, ft, g, t, dx, dt, vmask, leader);
+        scatter_levels<true>(a, cst, valid, x0, x1, x2, ft, g, t, dx, dt, leader, tg32);
     else
-        scatter_levels<false>(a, cst, valid, x0, x1, x2, ft, g, t, dx, dt, vmask, leader);
+        scatter_levels<false>(a, cst, valid, x0, x1, x2, ft, g, t, dx, dt, leader, tg32);
     if (in) a.d_t_slot[sl] = valid ? dt + (dx[0] * dir[0] + dx[1] * dir[1] + dx[2] * dir[2]) : 0.0;
+}
+
+// g_table += the fp32 per-lane table gradients (and clears them for the next call).
+__global__ void merge_table_kernel(double* __restrict__ g_table, float* __restrict__ tg32, int64_t n) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const float v = tg32[i];
+        if (v != 0.f) {
+            g_table[i] += static_cast<double>(v);
+            tg32[i] = 0.f;
+        }
+    }
 }
 
 struct Scratch {
@@ -708,6 +731,8 @@ struct Scratch {
     size_t fcap = 0;
     int32_t* amb = nullptr;  // [0] count, [1..] listed slots
     size_t acap = 0;
+    float* tg32 = nullptr;   // fp32 table gradients of the per-lane scatters (kept zeroed)
+    size_t tcap = 0;
     float* parts = nullptr;
     size_t pcap = 0;
 };
@@ -744,6 +769,15 @@ int launch_field_backward_tc(const FieldBwdArgs& a, cudaStream_t s) {
         if (cudaMalloc(&sc.amb, (total + 1) * sizeof(int32_t)) != cudaSuccess) return NX_OUT_OF_MEMORY;
         sc.acap = total + 1;
     }
+    const size_t tneed = static_cast<size_t>(kLevels) * (size_t(1) << a.scene.field.log2_table) * 2;
+    if (tneed > sc.tcap) {
+        if (sc.tg32) cudaFree(sc.tg32);
+        sc.tg32 = nullptr;
+        sc.tcap = 0;
+        if (cudaMalloc(&sc.tg32, tneed * sizeof(float)) != cudaSuccess) return NX_OUT_OF_MEMORY;
+        if (cudaMemsetAsync(sc.tg32, 0, tneed * sizeof(float), s) != cudaSuccess) return NX_CUDA_ERROR;
+        sc.tcap = tneed;
+    }
     if (pneed > sc.pcap) {
         if (sc.parts) cudaFree(sc.parts);
         sc.parts = nullptr;
@@ -765,7 +799,9 @@ int launch_field_backward_tc(const FieldBwdArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(mlp_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemM);
     mlp_bwd_tc_kernel<<<grid_m, kThreadsM, kSmemM, s>>>(a, sc.fbuf, sc.parts, total, n_tiles);
     reduce_wgrads_kernel<<<(kWGrads + 255) / 256, 256, 0, s>>>(sc.parts, grid_m, a.g_w1, a.g_w2, a.g_w3);
-    scatter_kernel<<<blocks, 128, 0, s>>>(a, cst, sc.fbuf, total);
+    scatter_kernel<<<blocks, 128, 0, s>>>(a, cst, sc.fbuf, total, reinterpret_cast<float2*>(sc.tg32));
+    count_launch();
+    merge_table_kernel<<<8 * sms, 256, 0, s>>>(a.g_table, sc.tg32, static_cast<int64_t>(tneed));
     return NX_OK;
 }
 
