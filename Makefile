@@ -52,10 +52,11 @@ DROPIN := build/dropin
 DROPIN_TUS := camera primitive hash_grid mlp texture_field threading oracle
 DROPIN_CXX := -std=gnu++20 -O3 -DNDEBUG -fPIC -pthread -march=x86-64-v3 -I$(REF)/core/include
 RENAME_FWD := -Dcollection_pass=nexel_ref_collection_pass -Dtexturing_pass=nexel_ref_texturing_pass \
-              -Drender=nexel_ref_render -Dvalidate_settings=nexel_ref_validate_settings
+              -Drender=nexel_ref_render -Dvalidate_settings=nexel_ref_validate_settings \
+              -Drender_backward=nexel_ref_render_backward
 
 ifneq ($(wildcard $(REF)/core/src/renderer.cpp),)
-dropin: $(DROPIN)/libnexel_dropin.so $(DROPIN)/test_oracle_dropin
+dropin: $(DROPIN)/libnexel_dropin.so $(DROPIN)/test_oracle_dropin $(DROPIN)/test_dropin_backward
 else
 dropin:
 	@echo "reference sources not present; using the prebuilt $(DROPIN) if any"
@@ -79,6 +80,9 @@ $(DROPIN)/libnexel_dropin.so: $(DROPIN)/renderer_b200.o $(DROPIN)/ref_renderer_b
 	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
 
 $(DROPIN)/test_oracle_dropin: $(REF)/tests/test_oracle.cpp tests/cxx/doctest.h $(DROPIN)/libnexel_dropin.so
+	$(CXX) $(DROPIN_CXX) -Itests/cxx -I$(REF)/tests -o $@ $< -L$(DROPIN) -lnexel_dropin -Wl,-rpath,'$$ORIGIN'
+
+$(DROPIN)/test_dropin_backward: tests/cxx/test_dropin_backward.cpp tests/cxx/doctest.h $(DROPIN)/libnexel_dropin.so
 	$(CXX) $(DROPIN_CXX) -Itests/cxx -I$(REF)/tests -o $@ $< -L$(DROPIN) -lnexel_dropin -Wl,-rpath,'$$ORIGIN'
 
 clean:

@@ -42,6 +42,7 @@ def parse():
     p.add_argument("--height", type=int, default=1080)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU-baseline work")
+    p.add_argument("--train-steps", type=int, default=10, help="timed forward+backward steps (config 5); 0 = skip")
     return p.parse_args()
 
 
@@ -266,6 +267,68 @@ def run_reference_arm(args):
     barrier(dist)
 
 
+# ---------------------------------------------------------------- config 5: forward + backward
+def train_step_timing(args, r, ds, scene, cam, stream, dist, local):
+    """BASELINE.json configs[4]: one training step's render path = render (collection +
+    texturing, fp64 base kept) + render_backward with synthetic upstream gradients
+    (dL/dfinal, dL/dweights, dL/dtexture, err_pixel) into device SceneGrads, timed
+    with CUDA events on the render stream (reported beside the headline metric)."""
+    import torch
+    import ctypes as C
+    from paper_2512_13796_b200 import _abi
+    dev = torch.device("cuda", local)
+    K = scene.settings.top_k
+    npix = cam.width * cam.height
+    g = torch.Generator(device=dev).manual_seed(5)
+    up_t = [torch.randn(npix * 3, dtype=torch.float64, device=dev, generator=g),
+            torch.randn(npix * K, dtype=torch.float64, device=dev, generator=g),
+            torch.randn(npix * K * 3, dtype=torch.float64, device=dev, generator=g)]
+    err = torch.rand(npix, dtype=torch.float64, device=dev, generator=g)
+    f = scene.field
+    grads = [torch.zeros(scene.nexels.shape[0] * 60, dtype=torch.float64, device=dev),
+             torch.zeros(f.grid.param_count(), dtype=torch.float64, device=dev),
+             torch.zeros(f.w1.size, dtype=torch.float64, device=dev),
+             torch.zeros(f.w2.size, dtype=torch.float64, device=dev),
+             torch.zeros(f.w3.size, dtype=torch.float64, device=dev)]
+    blend = torch.zeros(scene.nexels.shape[0], dtype=torch.float64, device=dev)
+    up = _abi.nx_upstream(*(t.data_ptr() for t in up_t))
+    gg = _abi.nx_grads(*(t.data_ptr() for t in grads))
+    fr = r.frame()
+    fr.set_backward(True)
+    c = cam.to_c()
+    s = C.c_void_p(r.stream)
+
+    def step():
+        r._check(r.lib.nx_render(r.ctx, ds.handle, C.byref(c), fr.handle, s))
+        r._check(r.lib.nx_render_backward(r.ctx, ds.handle, C.byref(c), fr.handle, C.byref(up), C.byref(gg),
+                                          C.c_void_p(err.data_ptr()), C.c_void_p(blend.data_ptr()), s))
+
+    for _ in range(3):
+        step()
+    r.synchronize()
+    barrier(dist)
+    torch.cuda.synchronize()
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record(stream)
+    for _ in range(args.train_steps):
+        r._check(r.lib.nx_render(r.ctx, ds.handle, C.byref(c), fr.handle, s))
+    e1.record(stream)
+    for _ in range(args.train_steps):
+        step()
+    e2.record(stream)
+    torch.cuda.synchronize()
+    fwd_ms = max_over_ranks(dist, e0.elapsed_time(e1) / args.train_steps, f"cuda:{local}")
+    step_ms = max_over_ranks(dist, e1.elapsed_time(e2) / args.train_steps, f"cuda:{local}")
+    finite = bool(torch.isfinite(grads[0]).all().item() and torch.isfinite(grads[1]).all().item())
+    fr.close()
+    return {"config": "configs[4]: 400K nexels 1080p forward + backward (surfel / texture gradients)",
+            "ms_per_step": step_ms, "steps_per_s": 1e3 / step_ms, "forward_ms": fwd_ms,
+            "backward_ms": step_ms - fwd_ms, "steps": args.train_steps, "view": cam.name,
+            "grads_finite": finite,
+            "path": "nx_render + nx_render_backward (device SceneGrads, synthetic upstream gradients + err_pixel)",
+            "reference_backward_s": "101 s/frame at config 2 on 8 cores (SURVEY.md §8(f)); not re-timed here"}
+
+
 # ---------------------------------------------------------------- our arm
 def run_ours(args):
     world, rank, local, dist = dist_setup(args)
@@ -375,6 +438,10 @@ def run_ours(args):
     fbytes = frame_bytes(args.nexels, P, H, W, K, Q)
     frame_gbs = fbytes * (args.steps / (ms_local / 1e3)) / 1e9
 
+    train = train_step_timing(args, r, ds, scene, cams[views[args.warmup]] if len(views) > args.warmup else
+                              nx.ring_camera(0, N_VIEWS, args.width, args.height), stream, dist, local) \
+        if args.train_steps > 0 else None
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -399,6 +466,7 @@ def run_ours(args):
             "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "nx_render + nx_frame_download (all FrameBuffers) into pinned host memory"},
             "gpu_launches": launches, "clocks": clk,
+            "train_step": train,
         }
         print(json.dumps(line), flush=True)
     for f2 in frames:

@@ -1,7 +1,8 @@
-// Drop-in replacement for the forward path of proj/core/src/renderer.cpp:
-// nexel::validate_settings, collection_pass, texturing_pass and render with the
-// reference's signatures (include/nexel/renderer.hpp:22-28, scene.hpp:35), running
-// on the sm_100a library through its C-ABI (include/nexel_b200.h).
+// Drop-in replacement for the render path of proj/core/src/renderer.cpp:
+// nexel::validate_settings, collection_pass, texturing_pass, render and
+// render_backward with the reference's signatures (include/nexel/renderer.hpp:22-53,
+// scene.hpp:35), running on the sm_100a library through its C-ABI
+// (include/nexel_b200.h).
 //
 // Compiled against the reference's public headers and linked in place of
 // renderer.cpp's forward half. Semantics kept:
@@ -114,6 +115,7 @@ Device& bind(const Scene& scene) {
         const int st = nx_ctx_create(dev, &d.ctx);
         if (st != NX_OK) raise(st, "cannot create a CUDA context on device " + std::to_string(dev));
         check(d, nx_frame_create(d.ctx, 0, 0, 0, &d.frame));
+        check(d, nx_frame_set_backward(d.ctx, d.frame, 1));  // fp64 base, as FrameBuffers holds it
     }
     const uint64_t key = fingerprint(scene);
     const nx_settings st = to_nx(scene.settings);
@@ -161,16 +163,15 @@ void collection_pass(const Scene& scene, const Camera& cam, RenderResult& out) {
     const nx_camera c = to_nx(cam);
     check(d, nx_collection_pass(d.ctx, d.scene, &c, d.frame, nullptr));
     const size_t npix = static_cast<size_t>(cam.width) * cam.height;
-    std::vector<float> base(npix * 3), residual(npix);
+    std::vector<float> residual(npix);
     nx_host_frame h{};
-    h.base = base.data();
+    h.base_f64 = out.fb.base.data();  // the fp64 base (Eq. 6) the device kept
     h.residual = residual.data();
     h.ids = out.fb.ids.data();
     h.depths = out.fb.depths.data();
     h.weights = out.fb.weights.data();
     check(d, nx_frame_download(d.ctx, d.frame, &h, nullptr));
     check(d, nx_ctx_synchronize(d.ctx));
-    widen(base, out.fb.base);
     widen(residual, out.fb.residual);
     d.frame_owner = &out.fb;
 }
@@ -209,6 +210,45 @@ RenderResult render(const Scene& scene, const Camera& cam) {  // renderer.cpp:23
     collection_pass(scene, cam, out);
     texturing_pass(scene, cam, out.fb);
     return out;
+}
+
+// render_backward (renderer.hpp:50-53, renderer.cpp:251-401): the host FrameBuffers
+// (the forward's output) are uploaded, the reverse pass runs on the device and the
+// gradients are accumulated into `grads` / `blended_error` like the reference.
+void render_backward(const Scene& scene, const Camera& cam, const FrameBuffers& fb, const UpstreamGrads& up,
+                     SceneGrads& grads, const double* err_pixel, std::vector<double>* blended_error) {
+    validate_settings(scene.settings);
+    validate_camera(cam);
+    if (grads.prims.size() != scene.nexels.size() || grads.field.table.size() != scene.field.grid.table.size() ||
+        grads.field.w1.size() != scene.field.mlp.w1.size() || grads.field.w2.size() != scene.field.mlp.w2.size() ||
+        grads.field.w3.size() != scene.field.mlp.w3.size())
+        fail("invalid-argument", "render_backward: SceneGrads not allocated for this scene");
+    if (blended_error && blended_error->size() != scene.nexels.size())
+        fail("invalid-argument", "render_backward: blended_error does not match the scene");
+    Device& d = bind(scene);
+    std::lock_guard<std::mutex> lock(d.mu);
+    const size_t npix = static_cast<size_t>(fb.width) * fb.height;
+    std::vector<float> texture(fb.texture.begin(), fb.texture.end()), residual(fb.residual.begin(), fb.residual.end());
+    std::vector<float> base32(fb.base.begin(), fb.base.end());
+    nx_host_frame h{};
+    h.base = base32.data();
+    h.base_f64 = const_cast<double*>(fb.base.data());
+    h.ids = const_cast<int32_t*>(fb.ids.data());
+    h.depths = const_cast<double*>(fb.depths.data());
+    h.weights = const_cast<double*>(fb.weights.data());
+    h.texture = texture.data();
+    h.residual = residual.data();
+    (void)npix;
+    check(d, nx_frame_upload(d.ctx, d.frame, fb.width, fb.height, fb.top_k, &h, nullptr));
+    d.frame_owner = nullptr;
+    static_assert(sizeof(PrimitiveGrad) == NX_PARAMS_PER_NEXEL * sizeof(double), "PrimitiveGrad = 60 doubles");
+    nx_grads g{grads.prims.empty() ? nullptr : &grads.prims[0].mu.x, grads.field.table.data(), grads.field.w1.data(),
+               grads.field.w2.data(), grads.field.w3.data()};
+    const bool k = fb.top_k > 0;
+    nx_upstream u{up.d_final, k ? up.d_weights : nullptr, k ? up.d_texture : nullptr};
+    const nx_camera c = to_nx(cam);
+    check(d, nx_render_backward_host(d.ctx, d.scene, &c, d.frame, &u, &g, err_pixel,
+                                     blended_error ? blended_error->data() : nullptr));
 }
 
 }  // namespace nexel

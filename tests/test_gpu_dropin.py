@@ -2,7 +2,9 @@
 drop-in (paper_2512_13796_b200/host/renderer_b200.cpp over the C-ABI) in place of
 renderer.cpp's forward half: proj/tests/test_oracle.cpp (tiled renderer vs the
 brute-force naive_render <= 1e-6, termination on thin scenes, empty scene,
-k = 0 march). Built by `make dropin` (needs /root/reference at build time)."""
+k = 0 march), and the drop-in render_backward against the reference's own
+render_backward linked into the same library. Built by `make dropin` (needs
+/root/reference at build time)."""
 import os
 import subprocess
 
@@ -20,3 +22,16 @@ def test_reference_test_oracle_suite_passes_on_the_dropin():
     print(r.stdout[-2000:], r.stderr[-2000:])
     assert r.returncode == 0
     assert "6 test cases, 0 failed" in r.stdout
+
+
+BWD = os.path.join(ROOT, "build", "dropin", "test_dropin_backward")
+
+
+@pytest.mark.skipif(not os.path.exists(BWD), reason="drop-in backward test binary not built (make dropin)")
+def test_dropin_render_backward_matches_the_reference_in_the_same_library():
+    # nexel::render_backward (GPU, renderer_b200.cpp) vs the reference's own
+    # renderer.cpp render_backward (renamed nexel_ref_render_backward) on one forward
+    r = subprocess.run([BWD], capture_output=True, text=True, timeout=900)
+    print(r.stdout[-2000:], r.stderr[-2000:])
+    assert r.returncode == 0
+    assert "2 test cases, 0 failed" in r.stdout
