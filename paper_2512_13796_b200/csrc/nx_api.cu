@@ -113,6 +113,7 @@ struct nx_frame {
     int list_tile = kWorkTile, ltiles_x = 0, ltiles_y = 0;  // tiles of the last built lists
     DevBuf base, ids, depths, weights, texture, final_img, residual;
     DevBuf base64;               // fp64 base kept for render_backward
+    DevBuf tex_f;                // texture features (split tensor-core texture pass)
     bool keep_backward = false;  // collection passes write base64
     bool base64_valid = false;   // base64 holds the last forward's (or an uploaded) base
     DevBuf tile_offsets;  // n_tiles + 1 (the work lists' ranges of the last collection pass)
@@ -456,6 +457,11 @@ int texturing(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* 
     ta.cam = make_cam(*cam);
     ta.fb = frame_dev(f);
     ta.stats = f->stats;
+    ta.fscratch = nullptr;
+    if (texture_tc_supported(scene->st.top_k > 0 ? scene->field : nx_field_desc{}) && f->K > 0) {
+        NX_CUDA(c, f->tex_f.ensure(static_cast<size_t>(f->W) * f->H * f->K * 32 * sizeof(float)));
+        ta.fscratch = f->tex_f.as<float>();
+    }
     const int st = launch_texture(ta, s);
     if (st) return set_err(c, st, "texture field shape not supported (n_in <= 64, n_hidden <= 128)");
     record(c, kEvTexEnd, s);
@@ -718,7 +724,7 @@ void nx_frame_destroy(nx_frame* f) {
     if (!f) return;
     if (f->ctx) cudaSetDevice(f->ctx->device);
     for (DevBuf* b : {&f->base, &f->ids, &f->depths, &f->weights, &f->texture, &f->final_img, &f->residual,
-                      &f->tile_offsets, &f->base64})
+                      &f->tile_offsets, &f->base64, &f->tex_f})
         b->release();
     if (f->ev_busy) cudaEventSynchronize(f->ev_busy);
     if (f->stats) cudaFree(f->stats);

@@ -28,8 +28,14 @@ namespace {
 
 constexpr int kThreads = kWorkTile * kWorkTile;  // 64: one thread per pixel of the work tile
 constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 128;                      // primitives staged per round
-constexpr int kSub = 8;                          // primitives pooled per B1/B2 round (<= 256 entries per warp)
+#ifndef NX_COMPOSITE_CHUNK
+#define NX_COMPOSITE_CHUNK 128
+#endif
+#ifndef NX_COMPOSITE_SUB
+#define NX_COMPOSITE_SUB 4
+#endif
+constexpr int kChunk = NX_COMPOSITE_CHUNK;       // primitives staged per round
+constexpr int kSub = NX_COMPOSITE_SUB;           // primitives pooled per B1/B2 round (<= 256 entries per warp)
 constexpr int kPool = 32 * kSub;
 constexpr int kRecPairs = REC_FIELDS / 2;        // double2 per fp64 record (10)
 static_assert(kWorkTile == 8, "warp blocks are 8x4 pixels");
@@ -50,7 +56,10 @@ struct SmemLayout {
 };
 
 template <int K, bool kDebug>
-__global__ void __launch_bounds__(kThreads, 8) composite_kernel(const CompositeArgs a) {
+#ifndef NX_COMPOSITE_MINB
+#define NX_COMPOSITE_MINB 10
+#endif
+__global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(const CompositeArgs a) {
     constexpr int KK = K > 0 ? K : 1;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     SmemLayout& sm = *reinterpret_cast<SmemLayout*>(smem_raw);

@@ -221,6 +221,7 @@ struct TextureArgs {
     CamD cam;
     FrameDev fb;
     FrameStatsD* stats;
+    float* fscratch;  // H*W*K*32 interpolated features (split tensor-core path), per frame
 };
 int launch_texture(const TextureArgs& a, cudaStream_t s);  // returns NX_OK / NX_UNSUPPORTED
 // tcgen05 variant for the reference field shape (16 levels x 2 features, 64 hidden).

@@ -22,8 +22,11 @@
 // SBO = 128*K/8 B (next 8-row group).
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
+#include "nx_composite.cuh"
 #include "nx_grid.cuh"
 #include "nx_tc.cuh"
 
@@ -295,6 +298,222 @@ __global__ void __launch_bounds__(kTcThreads, kCtasPerSm) texture_tc_kernel(cons
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
 
+// ---------------------------------------------------------------- split variant
+// The same pass as two kernels: (1) the hash-grid gathers at full occupancy, one thread
+// per slot, features to a per-frame scratch (128 B per slot); (2) the MLP on tcgen05
+// over tiles of whole pixels (128/K pixels x K slots), SH colour, texture and Eq. 7.
+// The gathers are latency-bound and want many warps; the fused kernel can keep only
+// three 128-thread CTAs per SM resident (registers, shared memory).
+__global__ void __launch_bounds__(128) tex_features_kernel(const TextureArgs a, const TcConst cst, int64_t total) {
+    const int64_t sl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (sl >= total) return;
+    float feats[kIn];
+#pragma unroll
+    for (int i = 0; i < kIn; ++i) feats[i] = 0.f;
+    if (a.fb.ids[sl] >= 0) {
+        const int K = a.fb.K;
+        const int64_t pix = sl / K;
+        double dir[3];
+        pixel_dir(a.cam, static_cast<int>(pix % a.cam.W) + 0.5, static_cast<int>(pix / a.cam.W) + 0.5, dir);
+        const double t = a.fb.depths[sl];
+        const double x0 = a.cam.o[0] + t * dir[0], x1 = a.cam.o[1] + t * dir[1], x2 = a.cam.o[2] + t * dir[2];
+        const float ft = static_cast<float>(a.cam.fx / t);
+        const uint32_t T = 1u << a.scene.field.log2_table, mask = T - 1u;
+        const float2* tab = reinterpret_cast<const float2*>(a.scene.table);
+        const bool small = fmax(fabs(x0), fmax(fabs(x1), fabs(x2))) * cst.level_scale[kLevels - 1] < 1073741824.0;
+        if (small) {
+            LevelFetch cur = fetch_level<true>(0, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
+#pragma unroll
+            for (int l = 0; l < kLevels; ++l) {
+                LevelFetch nxt;
+                if (l + 1 < kLevels) nxt = fetch_level<true>(l + 1, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
+                const float2 g = interp(cur);
+                feats[2 * l] = g.x;
+                feats[2 * l + 1] = g.y;
+                if (l + 1 < kLevels) cur = nxt;
+            }
+        } else {
+#pragma unroll
+            for (int l = 0; l < kLevels; ++l) {
+                const float2 g = interp(fetch_level<false>(l, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight));
+                feats[2 * l] = g.x;
+                feats[2 * l + 1] = g.y;
+            }
+        }
+    }
+    float4* dst = reinterpret_cast<float4*>(a.fscratch + sl * kIn);
+#pragma unroll
+    for (int q = 0; q < kIn / 4; ++q) dst[q] = make_float4(feats[4 * q], feats[4 * q + 1], feats[4 * q + 2], feats[4 * q + 3]);
+}
+
+__global__ void __launch_bounds__(kTcThreads, kCtasPerSm) tex_mlp_kernel(const TextureArgs a, int ppt,
+                                                                        int64_t n_tiles) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t bar = smem_u32(smem + kOffBar);
+    for (int e = tid; e < kHid * kIn / 8; e += kTcThreads) {  // W1 [64][32]
+        const int n = e / (kIn / 8), c = e % (kIn / 8);
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(a.scene.w1 + n * kIn + c * 8 + i);
+        store_split8(smem, kOffW1h, kOffW1l, kmajor_off(n, c * 8, kIn), x);
+    }
+    for (int e = tid; e < kHid * kHid / 8; e += kTcThreads) {  // W2 [64][64]
+        const int n = e / (kHid / 8), c = e % (kHid / 8);
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(a.scene.w2 + n * kHid + c * 8 + i);
+        store_split8(smem, kOffW2h, kOffW2l, kmajor_off(n, c * 8, kHid), x);
+    }
+    for (int e = tid; e < kOut * kHid / 8; e += kTcThreads) {  // W3 [48][64]
+        const int n = e / (kHid / 8), c = e % (kHid / 8);
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(a.scene.w3 + n * kHid + c * 8 + i);
+        store_split8(smem, kOffW3h, kOffW3l, kmajor_off(n, c * 8, kHid), x);
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem + kOffTmem)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 32) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + kOffTmem);
+    uint32_t phase = 0;
+    const int K = a.fb.K;
+    const int64_t npix = static_cast<int64_t>(a.cam.W) * a.cam.H;
+    const int row = tid;
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * warp) << 16);
+    float* srgb = reinterpret_cast<float*>(smem + kOffRgb);
+    constexpr uint32_t kIdesc64 = idesc_bf16_f32(kRows, 64);
+    constexpr uint32_t kIdesc48 = idesc_bf16_f32(kRows, 48);
+    int n_queries = 0;
+    const int p_in = row / K, j_in = row - p_in * K;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int64_t pix = tile * ppt + p_in;
+        const bool in_tile = p_in < ppt && pix < npix;
+        const int64_t slot = in_tile ? pix * K + j_in : 0;
+        const bool valid = in_tile && a.fb.ids[slot] >= 0;
+        n_queries += valid;
+        float feats[kIn];
+        if (valid) {
+            const float4* src = reinterpret_cast<const float4*>(a.fscratch + slot * kIn);
+#pragma unroll
+            for (int q = 0; q < kIn / 4; ++q) {
+                const float4 v = src[q];
+                feats[4 * q] = v.x;
+                feats[4 * q + 1] = v.y;
+                feats[4 * q + 2] = v.z;
+                feats[4 * q + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < kIn; ++i) feats[i] = 0.f;
+        }
+#pragma unroll
+        for (int c = 0; c < kIn / 8; ++c) store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 8 * c, kIn), feats + 8 * c);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) issue_layer(smem, tmem, kOffW1h, kOffW1l, kIn, kIdesc64, bar);
+        // the pixel ray of this row while layer 1 runs
+        double dir[3] = {0.0, 0.0, 1.0};
+        if (in_tile) pixel_dir(a.cam, static_cast<int>(pix % a.cam.W) + 0.5, static_cast<int>(pix / a.cam.W) + 0.5, dir);
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+#pragma unroll 1
+        for (int layer = 0; layer < 2; ++layer) {
+#pragma unroll
+            for (int c = 0; c < kHid / 16; ++c) {
+                float v[16];
+                tmem_ld16(taddr + 16 * c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
+                store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 16 * c, kHid), v);
+                store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 16 * c + 8, kHid), v + 8);
+            }
+            fence_async_smem();
+            tc_fence_before();
+            __syncthreads();
+            if (tid == 0) {
+                if (layer == 0) issue_layer(smem, tmem, kOffW2h, kOffW2l, kHid, kIdesc64, bar);
+                else issue_layer(smem, tmem, kOffW3h, kOffW3l, kHid, kIdesc48, bar);
+            }
+            mbar_wait(bar, phase);
+            phase ^= 1;
+            tc_fence_after();
+        }
+        {
+            const float x = static_cast<float>(dir[0]), y = static_cast<float>(dir[1]), z = static_cast<float>(dir[2]);
+            float b[16];
+            sh_basis_f32(x, y, z, b);
+            float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+#pragma unroll
+            for (int c = 0; c < kOut / 16; ++c) {
+                float v[16];
+                tmem_ld16(taddr + 16 * c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int o = 16 * c + i, k = o / 3;
+                    if (o % 3 == 0) c0 = fmaf(v[i], b[k], c0);
+                    else if (o % 3 == 1) c1 = fmaf(v[i], b[k], c1);
+                    else c2 = fmaf(v[i], b[k], c2);
+                }
+            }
+            float rgb[3] = {0.f, 0.f, 0.f};
+            if (valid) {
+                rgb[0] = fmaxf(0.5f + c0, 0.f);
+                rgb[1] = fmaxf(0.5f + c1, 0.f);
+                rgb[2] = fmaxf(0.5f + c2, 0.f);
+            }
+            srgb[row * 3 + 0] = rgb[0];
+            srgb[row * 3 + 1] = rgb[1];
+            srgb[row * 3 + 2] = rgb[2];
+            if (in_tile) {
+                a.fb.texture[slot * 3 + 0] = rgb[0];
+                a.fb.texture[slot * 3 + 1] = rgb[1];
+                a.fb.texture[slot * 3 + 2] = rgb[2];
+            }
+        }
+        tc_fence_before();
+        __syncthreads();
+        // Eq. 7: final = base + sum_j W[p,j] * texture[p,j] (renderer.cpp:219-236)
+        if (tid < ppt) {
+            const int64_t qp = tile * ppt + tid;
+            if (qp < npix) {
+                double acc0 = a.fb.base[qp * 3 + 0], acc1 = a.fb.base[qp * 3 + 1], acc2 = a.fb.base[qp * 3 + 2];
+                for (int j = 0; j < K; ++j) {
+                    const int64_t sl = qp * K + j;
+                    if (a.fb.ids[sl] < 0) continue;
+                    const double w = a.fb.weights[sl];
+                    const float* tc = srgb + (tid * K + j) * 3;
+                    acc0 += w * tc[0];
+                    acc1 += w * tc[1];
+                    acc2 += w * tc[2];
+                }
+                a.fb.final_img[qp * 3 + 0] = static_cast<float>(acc0);
+                a.fb.final_img[qp * 3 + 1] = static_cast<float>(acc1);
+                a.fb.final_img[qp * 3 + 2] = static_cast<float>(acc2);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n_queries += __shfl_down_sync(0xffffffffu, n_queries, o);
+    if ((tid & 31) == 0 && n_queries) atomicAdd(&a.stats->queries, static_cast<unsigned long long>(n_queries));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
 }  // namespace
 
 bool texture_tc_supported(const nx_field_desc& fd) {
@@ -303,6 +522,31 @@ bool texture_tc_supported(const nx_field_desc& fd) {
 
 int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
     const int K = a.fb.K;
+    static const bool fused = [] {
+        const char* e = getenv("NX_TEXTURE_PATH");
+        return e && strcmp(e, "fused") == 0;
+    }();
+    if (a.fscratch && !fused) {  // split: gathers at full occupancy, then the tensor-core MLP
+        const int ppt = kRows / K;
+        const int64_t npix = static_cast<int64_t>(a.cam.W) * a.cam.H, total = npix * K;
+        if (total == 0) return NX_OK;
+        const int64_t n_tiles = (npix + ppt - 1) / ppt;
+        TcConst cst;
+        double sc = a.scene.field.base_scale;
+        for (int l = 0; l < kLevels; ++l, sc *= a.scene.field.growth) {
+            cst.level_scale[l] = sc;
+            cst.inv_level_scale[l] = static_cast<float>(1.0 / sc);
+        }
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(tex_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemUsed);
+        count_launch(2);
+        tex_features_kernel<<<static_cast<unsigned>((total + 127) / 128), 128, 0, s>>>(a, cst, total);
+        const int64_t grid = std::min<int64_t>(n_tiles, static_cast<int64_t>(kCtasPerSm) * sms);
+        tex_mlp_kernel<<<static_cast<unsigned>(grid), kTcThreads, kSmemUsed, s>>>(a, ppt, n_tiles);
+        return NX_OK;
+    }
     // Tiles are pixel blocks (8 wide) so that neighbouring rows query neighbouring
     // lattice cells; K that do not divide 128 use a one-row block of 128/K pixels.
     const int ppt = kRows / K;
