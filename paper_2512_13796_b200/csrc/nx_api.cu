@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -759,8 +760,24 @@ int nx_frame_download(nx_ctx* c, const nx_frame* fc, const nx_host_frame* dst, v
     NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_ready, 0));
     if (f->busy_pending) NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_busy, 0));
     const size_t npix = static_cast<size_t>(f->W) * f->H, ns = npix * f->K;
+    // Pinned, device-mapped destinations take the streaming copy kernel (nx_copy.cu);
+    // anything else a DMA memcpy. NX_DOWNLOAD=memcpy forces the DMA engine.
+    static const bool force_dma = [] {
+        const char* e = std::getenv("NX_DOWNLOAD");
+        return e && std::strcmp(e, "memcpy") == 0;
+    }();
+    CopyJobs jobs{};
     auto cp = [&](void* d, const DevBuf& b, size_t bytes) -> cudaError_t {
         if (!d || !bytes) return cudaSuccess;
+        if (!force_dma) {
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, d) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer &&
+                jobs.n < 8) {
+                jobs.j[jobs.n++] = {static_cast<const uint8_t*>(b.p), static_cast<uint8_t*>(at.devicePointer), bytes};
+                return cudaSuccess;
+            }
+            cudaGetLastError();  // unregistered host memory reports an error here: not fatal
+        }
         return cudaMemcpyAsync(d, b.p, bytes, cudaMemcpyDeviceToHost, s);
     };
     NX_CUDA(c, cp(dst->base, f->base, npix * 3 * sizeof(float)));
@@ -771,6 +788,8 @@ int nx_frame_download(nx_ctx* c, const nx_frame* fc, const nx_host_frame* dst, v
     NX_CUDA(c, cp(dst->final_img, f->final_img, npix * 3 * sizeof(float)));
     NX_CUDA(c, cp(dst->residual, f->residual, npix * sizeof(float)));
     if (dst->base_f64 && f->base64_valid) NX_CUDA(c, cp(dst->base_f64, f->base64, npix * 3 * sizeof(double)));
+    launch_stream_copy(jobs, s);
+    NX_CUDA(c, cudaGetLastError());
     NX_CUDA(c, cudaEventRecord(f->ev_busy, s));
     f->busy_pending = true;
     return NX_OK;

@@ -228,6 +228,19 @@ int launch_texture(const TextureArgs& a, cudaStream_t s);  // returns NX_OK / NX
 bool texture_tc_supported(const nx_field_desc& fd);
 int launch_texture_tc(const TextureArgs& a, cudaStream_t s);
 
+// ---------------------------------------------------------------- downloads
+struct CopyJob {
+    const uint8_t* src;  // device
+    uint8_t* dst;        // device-mapped pinned host memory
+    size_t bytes;
+};
+struct CopyJobs {
+    CopyJob j[8];
+    int n;
+};
+// Streaming (evict-first) device -> mapped-host copy of up to 8 buffers (nx_copy.cu).
+void launch_stream_copy(const CopyJobs& jobs, cudaStream_t s);
+
 // ---------------------------------------------------------------- backward (render_backward)
 // Per-primitive activated-space gradient accumulator (ActivatedGrad,
 // intersect.hpp:45-51) + the blended-error sum: d_mu[3], d_R[9] (row-major m[i][j],
