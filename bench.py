@@ -269,21 +269,33 @@ def run_reference_arm(args):
 
 # ---------------------------------------------------------------- config 5: forward + backward
 def train_step_timing(args, r, ds, scene, cam, stream, dist, local):
-    """BASELINE.json configs[4]: one training step's render path = render (collection +
-    texturing, fp64 base kept) + render_backward with synthetic upstream gradients
-    (dL/dfinal, dL/dweights, dL/dtexture, err_pixel) into device SceneGrads, timed
-    with CUDA events on the render stream (reported beside the headline metric)."""
+    """BASELINE.json configs[4]: the render path of one training step (trainer.cpp:
+    274-302) — render (collection + texturing, fp64 base kept), losses_backward against a
+    ground-truth image (the render of the grid_init 1e-1 variant),
+    the per-pixel error map, and render_backward into device SceneGrads — timed with
+    CUDA events on the render stream and reported beside the headline metric."""
     import torch
     import ctypes as C
+    import paper_2512_13796_b200 as nx
     from paper_2512_13796_b200 import _abi
     dev = torch.device("cuda", local)
     K = scene.settings.top_k
-    npix = cam.width * cam.height
-    g = torch.Generator(device=dev).manual_seed(5)
-    up_t = [torch.randn(npix * 3, dtype=torch.float64, device=dev, generator=g),
-            torch.randn(npix * K, dtype=torch.float64, device=dev, generator=g),
-            torch.randn(npix * K * 3, dtype=torch.float64, device=dev, generator=g)]
-    err = torch.rand(npix, dtype=torch.float64, device=dev, generator=g)
+    W, H = cam.width, cam.height
+    npix = W * H
+    # ground truth: the textured variant's render of the same view (outside the timed region)
+    target = nx.stump_like(args.nexels, grid_init=1e-1)
+    ts = r.upload(target)
+    tf = r.frame()
+    r.render(ts, cam, tf)
+    r.synchronize()
+    v = tf.view()
+    gt = _device_view(v.final_img, npix * 3, torch.float32, dev).double()  # a copy, fp64
+    tf.close()
+    ts.close()
+    d_final = torch.zeros(npix * 3, dtype=torch.float64, device=dev)
+    d_weights = torch.zeros(npix * K, dtype=torch.float64, device=dev)
+    d_texture = torch.zeros(npix * K * 3, dtype=torch.float64, device=dev)
+    err = torch.zeros(npix, dtype=torch.float64, device=dev)
     f = scene.field
     grads = [torch.zeros(scene.nexels.shape[0] * 60, dtype=torch.float64, device=dev),
              torch.zeros(f.grid.param_count(), dtype=torch.float64, device=dev),
@@ -291,15 +303,28 @@ def train_step_timing(args, r, ds, scene, cam, stream, dist, local):
              torch.zeros(f.w2.size, dtype=torch.float64, device=dev),
              torch.zeros(f.w3.size, dtype=torch.float64, device=dev)]
     blend = torch.zeros(scene.nexels.shape[0], dtype=torch.float64, device=dev)
-    up = _abi.nx_upstream(*(t.data_ptr() for t in up_t))
+    terms = torch.zeros(8, dtype=torch.float64, device=dev)
+    up = _abi.nx_upstream(d_final.data_ptr(), d_weights.data_ptr(), d_texture.data_ptr())
     gg = _abi.nx_grads(*(t.data_ptr() for t in grads))
+    lw = _abi.nx_loss_weights()
+    r.lib.nx_loss_weights_default(C.byref(lw))
     fr = r.frame()
     fr.set_backward(True)
     c = cam.to_c()
     s = C.c_void_p(r.stream)
+    fin = None
 
     def step():
+        nonlocal fin
         r._check(r.lib.nx_render(r.ctx, ds.handle, C.byref(c), fr.handle, s))
+        r._check(r.lib.nx_losses_backward(r.ctx, ds.handle, fr.handle, C.c_void_p(gt.data_ptr()), C.byref(lw),
+                                          C.c_void_p(d_final.data_ptr()), C.c_void_p(d_weights.data_ptr()),
+                                          C.c_void_p(d_texture.data_ptr()), C.byref(gg),
+                                          C.c_void_p(terms.data_ptr()), s))
+        if fin is None:
+            fin = _device_view(fr.view().final_img, npix * 3, torch.float32, dev)
+        with torch.cuda.stream(stream):  # err_pixel = mean_c |final - gt| (trainer.cpp:289-296)
+            torch.mean(torch.abs(fin.double().view(npix, 3) - gt.view(npix, 3)), dim=1, out=err)
         r._check(r.lib.nx_render_backward(r.ctx, ds.handle, C.byref(c), fr.handle, C.byref(up), C.byref(gg),
                                           C.c_void_p(err.data_ptr()), C.c_void_p(blend.data_ptr()), s))
 
@@ -319,14 +344,29 @@ def train_step_timing(args, r, ds, scene, cam, stream, dist, local):
     torch.cuda.synchronize()
     fwd_ms = max_over_ranks(dist, e0.elapsed_time(e1) / args.train_steps, f"cuda:{local}")
     step_ms = max_over_ranks(dist, e1.elapsed_time(e2) / args.train_steps, f"cuda:{local}")
+    t = terms.cpu().tolist()
     finite = bool(torch.isfinite(grads[0]).all().item() and torch.isfinite(grads[1]).all().item())
     fr.close()
     return {"config": "configs[4]: 400K nexels 1080p forward + backward (surfel / texture gradients)",
             "ms_per_step": step_ms, "steps_per_s": 1e3 / step_ms, "forward_ms": fwd_ms,
-            "backward_ms": step_ms - fwd_ms, "steps": args.train_steps, "view": cam.name,
-            "grads_finite": finite,
-            "path": "nx_render + nx_render_backward (device SceneGrads, synthetic upstream gradients + err_pixel)",
-            "reference_backward_s": "101 s/frame at config 2 on 8 cores (SURVEY.md §8(f)); not re-timed here"}
+            "losses_and_backward_ms": step_ms - fwd_ms, "steps": args.train_steps, "view": cam.name,
+            "loss_total": t[7], "grads_finite": finite,
+            "path": "nx_render + nx_losses_backward (gt = grid_init 1e-1 render) + err_pixel + nx_render_backward "
+                    "(device SceneGrads)",
+            "reference_s": "render ~55 s + render_backward 101 s per step at config 2 on 8 cores (SURVEY.md §6, "
+                           "§8(f)); not re-timed here"}
+
+
+def _device_view(ptr, n, dtype, dev):
+    """A torch view of a device array owned by the library (no copy)."""
+    import torch
+
+    class _CAI:
+        def __init__(self):
+            typestr = {torch.float32: "<f4", torch.float64: "<f8", torch.int32: "<i4"}[dtype]
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (int(ptr), False),
+                                             "version": 3}
+    return torch.as_tensor(_CAI(), device=dev)
 
 
 # ---------------------------------------------------------------- our arm

@@ -243,6 +243,35 @@ int nx_render_backward_host(nx_ctx* ctx, const nx_scene* scene, const nx_camera*
                             const nx_upstream* up, const nx_grads* grads, const double* err_pixel,
                             double* blended_error);
 
+/* ---- losses_backward (losses.hpp:52-56, losses.cpp:107-238) ------------ */
+/* LossWeights (losses.hpp:12-18). */
+typedef struct nx_loss_weights {
+    double dssim;    /* 0.2: blend inside the image term */
+    double alpha;    /* 0.005 */
+    double texture;  /* 0.5 */
+    double opacity;  /* 0.01 */
+    double grid;     /* 0.01 */
+} nx_loss_weights;
+/* LossTerms (losses.hpp:20-26). */
+typedef struct nx_loss_terms {
+    double l1, dssim, image, texture, alpha, opacity, grid, total;
+} nx_loss_terms;
+void nx_loss_weights_default(nx_loss_weights* out);
+/* losses_backward: the image term (1-dssim) L1 + dssim (1-SSIM)/2 on final_img (11x11
+ * Gaussian SSIM, ssim.cpp:99-151), the texture supervision and coverage terms on the
+ * buffered slots, and the opacity / grid regularisers. Writes (overwrites) the upstream
+ * gradients d_final (H*W*3), d_weights (H*W*K), d_texture (H*W*K*3) for
+ * nx_render_backward and ACCUMULATES the direct parameter terms into grads->prims
+ * (opacity_raw) and grads->table. gt: H*W*3 fp64. Device pointers; `terms` is a device
+ * nx_loss_terms written asynchronously on `stream`. */
+int nx_losses_backward(nx_ctx* ctx, const nx_scene* scene, const nx_frame* frame, const double* gt,
+                       const nx_loss_weights* w, double* d_final, double* d_weights, double* d_texture,
+                       const nx_grads* grads, nx_loss_terms* terms, void* stream);
+/* Same with HOST arrays and host `terms` (synchronous). */
+int nx_losses_backward_host(nx_ctx* ctx, const nx_scene* scene, const nx_frame* frame, const double* gt,
+                            const nx_loss_weights* w, double* d_final, double* d_weights, double* d_texture,
+                            const nx_grads* grads, nx_loss_terms* terms);
+
 /* ---- parity / debug (not on the timed path) ---------------------------- */
 /* Tile lists for `cam`: reference_lists=1 materialises the reference's lists
  * (Binning::tile_lists, renderer.cpp:102-110, straddlers in every tile) on

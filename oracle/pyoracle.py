@@ -204,6 +204,8 @@ class Reference:
         L.ref_downweight.argtypes = [C.c_double] * 3
         L.ref_field_forward.argtypes = [P, C.c_int64, PD, C.c_int, PD]
         L.ref_render_backward.argtypes = [P, Cm, PD, PD, PD, PD, PD, PD, PD, PD, PD, PD]
+        L.ref_losses_backward.argtypes = [P, C.c_int, C.c_int, C.c_int, PI32, PD, PD, PD, PD, PD, PD, PD, PD, PD,
+                                          PD, PD]
         self._scene = None
         self._scene_key = None
 
@@ -291,6 +293,24 @@ class Reference:
         self._check(self.lib.ref_render_backward(h, C.byref(c), *(opt(a) for a in keep), *(_dp(a) for a in g),
                                                  _dp(be) if be is not None else None))
         return (*g, be)
+
+    def losses_backward(self, scene: Scene, W: int, H: int, K: int, ids, weights, texture, final_img, gt, lw,
+                        g_prims=None, g_table=None):
+        """losses_backward of the reference (losses.cpp:107-238) on the given buffers;
+        returns (terms dict, d_final, d_weights, d_texture, g_prims, g_table)."""
+        h = self._handle(scene)
+        npix = W * H
+        ids = np.ascontiguousarray(ids, np.int32)
+        arr = [np.ascontiguousarray(a, np.float64) for a in (weights, texture, final_img, gt, lw)]
+        d_final, d_weights, d_texture = np.zeros(npix * 3), np.zeros(max(npix * K, 1)), np.zeros(max(npix * K * 3, 1))
+        gp = np.zeros((scene.nexels.shape[0], 60)) if g_prims is None else np.array(g_prims, np.float64)
+        gtab = np.zeros(scene.field.grid.param_count()) if g_table is None else np.array(g_table, np.float64)
+        terms = np.zeros(8)
+        self._check(self.lib.ref_losses_backward(h, W, H, K, ids.ctypes.data_as(PI32), *(_dp(a) for a in arr),
+                                                 _dp(d_final), _dp(d_weights), _dp(d_texture), _dp(gp), _dp(gtab),
+                                                 _dp(terms)))
+        keys = ("l1", "dssim", "image", "texture", "alpha", "opacity", "grid", "total")
+        return dict(zip(keys, terms.tolist())), d_final, d_weights[: npix * K], d_texture[: npix * K * 3], gp, gtab
 
     # ---- the reference test generators (tests/helpers.hpp:88-125)
     def random_scene(self, seed: int, n_prims: int, top_k: int, res: int, focal: float, dist: float,

@@ -15,6 +15,7 @@
 #include "renderer.cpp"  // -I /root/reference/proj/core/src: compiled in place, not copied
 #include "helpers.hpp"                                  // -I /root/reference/proj/tests
 
+#include "nexel/losses.hpp"
 #include "nexel/oracle.hpp"
 
 #include <cstdint>
@@ -380,6 +381,51 @@ int ref_render_backward(const ref_scene* h, const nx_camera* c, const double* d_
         put(g_w2, grads.field.w2);
         put(g_w3, grads.field.w3);
         if (blended_error) put(blended_error, rr.blended_error);
+    });
+}
+
+// nexel::losses_backward (losses.cpp:107-238) on a given FrameBuffers (ids, weights,
+// texture, final_img: fp64 arrays as the reference holds them) and ground truth.
+// lw = {dssim, alpha, texture, opacity, grid}; terms = {l1, dssim, image, texture,
+// alpha, opacity, grid, total}. d_* are overwritten; g_prims (N*60) / g_table are
+// accumulated into, as the reference does.
+int ref_losses_backward(const ref_scene* h, int W, int H, int K, const int32_t* ids, const double* weights,
+                        const double* texture, const double* final_img, const double* gt, const double* lw,
+                        double* d_final, double* d_weights, double* d_texture, double* g_prims,
+                        double* g_table, double* terms) {
+    return guarded([&] {
+        const Scene& scene = h->scene;
+        FrameBuffers fb;
+        fb.allocate(W, H, K);
+        const size_t npix = static_cast<size_t>(W) * H;
+        std::memcpy(fb.ids.data(), ids, npix * K * sizeof(int32_t));
+        std::memcpy(fb.weights.data(), weights, npix * K * sizeof(double));
+        std::memcpy(fb.texture.data(), texture, npix * K * 3 * sizeof(double));
+        std::memcpy(fb.final_img.data(), final_img, npix * 3 * sizeof(double));
+        Image img;
+        img.allocate(W, H);
+        std::memcpy(img.px.data(), gt, npix * 3 * sizeof(double));
+        LossWeights w;
+        w.dssim = lw[0];
+        w.alpha = lw[1];
+        w.texture = lw[2];
+        w.opacity = lw[3];
+        w.grid = lw[4];
+        SceneGrads grads;
+        grads.allocate(scene);
+        std::memcpy(&grads.prims[0], g_prims, scene.nexels.size() * sizeof(PrimitiveGrad));
+        std::memcpy(grads.field.table.data(), g_table, grads.field.table.size() * sizeof(double));
+        std::vector<double> df, dw, dt;
+        const LossTerms t = losses_backward(scene, fb, img, w, df, dw, dt, grads);
+        std::memcpy(d_final, df.data(), df.size() * sizeof(double));
+        if (K) {
+            std::memcpy(d_weights, dw.data(), dw.size() * sizeof(double));
+            std::memcpy(d_texture, dt.data(), dt.size() * sizeof(double));
+        }
+        std::memcpy(g_prims, &grads.prims[0], scene.nexels.size() * sizeof(PrimitiveGrad));
+        std::memcpy(g_table, grads.field.table.data(), grads.field.table.size() * sizeof(double));
+        const double tv[8] = {t.l1, t.dssim, t.image, t.texture, t.alpha, t.opacity, t.grid, t.total};
+        std::memcpy(terms, tv, sizeof tv);
     });
 }
 

@@ -7,12 +7,12 @@ Drop-in for the reference's ``nexel::render`` / ``collection_pass`` /
 reference interface.
 """
 from .api import (Camera, DeviceFrame, DeviceScene, FrameBuffers, HashGridConfig, NexelError, RenderResult,
-                  RenderSettings, Renderer, Scene, SceneGrads, TextureField, UpstreamGrads, collection_pass, render,
-                  render_backward, ring_camera, stump_like, texturing_pass)
+                  LossWeights, RenderSettings, Renderer, Scene, SceneGrads, TextureField, UpstreamGrads, collection_pass, render,
+                  losses_backward, render_backward, ring_camera, stump_like, texturing_pass)
 from . import _abi
 
 __all__ = [
     "Camera", "DeviceFrame", "DeviceScene", "FrameBuffers", "HashGridConfig", "NexelError", "RenderResult",
-    "RenderSettings", "Renderer", "Scene", "SceneGrads", "TextureField", "UpstreamGrads", "collection_pass",
-    "render", "render_backward", "ring_camera", "stump_like", "texturing_pass", "_abi",
+    "LossWeights", "RenderSettings", "Renderer", "Scene", "SceneGrads", "TextureField", "UpstreamGrads", "collection_pass",
+    "losses_backward", "render", "render_backward", "ring_camera", "stump_like", "texturing_pass", "_abi",
 ]

@@ -127,6 +127,18 @@ class nx_grads(C.Structure):
     ]
 
 
+class nx_loss_weights(C.Structure):
+    _fields_ = [("dssim", C.c_double), ("alpha", C.c_double), ("texture", C.c_double), ("opacity", C.c_double),
+                ("grid", C.c_double)]
+
+
+class nx_loss_terms(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("l1", "dssim", "image", "texture", "alpha", "opacity", "grid", "total")]
+
+    def as_dict(self):
+        return {k: float(getattr(self, k)) for k, _ in self._fields_}
+
+
 class nx_frame_stats(C.Structure):
     _fields_ = [
         ("n_nexels", C.c_int64),
@@ -189,6 +201,11 @@ SIGNATURES = [
      [P, P, C.POINTER(nx_camera), P, C.POINTER(nx_upstream), C.POINTER(nx_grads), P, P, P]),
     ("nx_render_backward_host", C.c_int,
      [P, P, C.POINTER(nx_camera), P, C.POINTER(nx_upstream), C.POINTER(nx_grads), PD, PD]),
+    ("nx_loss_weights_default", None, [C.POINTER(nx_loss_weights)]),
+    ("nx_losses_backward", C.c_int,
+     [P, P, P, P, C.POINTER(nx_loss_weights), P, P, P, C.POINTER(nx_grads), P, P]),
+    ("nx_losses_backward_host", C.c_int,
+     [P, P, P, PD, C.POINTER(nx_loss_weights), PD, PD, PD, C.POINTER(nx_grads), C.POINTER(nx_loss_terms)]),
     ("nx_debug_tile_lists", C.c_int,
      [P, P, C.POINTER(nx_camera), C.c_int, PI64, PI32, I64, PI64, PI32, PI32]),
     ("nx_debug_pixel_hits", C.c_int, [P, P, C.POINTER(nx_camera), C.c_int, C.c_int, C.c_int, PI32, PI32]),

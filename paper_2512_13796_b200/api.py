@@ -229,6 +229,19 @@ class SceneGrads:
                    np.zeros(np.size(f.w1)), np.zeros(np.size(f.w2)), np.zeros(np.size(f.w3)))
 
 
+@dataclasses.dataclass
+class LossWeights:
+    """LossWeights (losses.hpp:12-18)."""
+    dssim: float = 0.2
+    alpha: float = 0.005
+    texture: float = 0.5
+    opacity: float = 0.01
+    grid: float = 0.01
+
+    def to_c(self) -> _abi.nx_loss_weights:
+        return _abi.nx_loss_weights(self.dssim, self.alpha, self.texture, self.opacity, self.grid)
+
+
 def _dp(a: np.ndarray):
     return a.ctypes.data_as(_abi.PD)
 
@@ -439,6 +452,26 @@ class Renderer:
             _dp(err) if err is not None else None,
             _dp(blended_error) if (blended_error is not None and err is not None) else None))
 
+    def losses_backward(self, dscene: DeviceScene, frame: DeviceFrame, gt: np.ndarray, w: LossWeights,
+                        grads: SceneGrads):
+        """losses_backward (losses.hpp:52-56) on the device frame: returns (LossTerms
+        dict, d_final, d_weights, d_texture); accumulates the opacity / grid terms into
+        ``grads``."""
+        v = frame.view()
+        npix, K = v.width * v.height, v.top_k
+        gt = _f64(gt, npix * 3, "gt")
+        d_final, d_weights, d_texture = np.zeros(npix * 3), np.zeros(npix * K), np.zeros(npix * K * 3)
+        for a in (grads.prims, grads.table):
+            if a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise NexelError("invalid-argument", "SceneGrads arrays must be C-contiguous float64")
+        g = _abi.nx_grads(grads.prims.ctypes.data, grads.table.ctypes.data, None, None, None)
+        t = _abi.nx_loss_terms()
+        cw = w.to_c()
+        self._check(self.lib.nx_losses_backward_host(self.ctx, dscene.handle, frame.handle, _dp(gt), C.byref(cw),
+                                                     _dp(d_final), _dp(d_weights) if K else None,
+                                                     _dp(d_texture) if K else None, C.byref(g), C.byref(t)))
+        return t.as_dict(), d_final, d_weights, d_texture
+
     def synchronize(self):
         self._check(self.lib.nx_ctx_synchronize(self.ctx))
 
@@ -569,6 +602,17 @@ def render_backward(scene: Scene, cam: Camera, fb: FrameBuffers, up: UpstreamGra
     fr = _value_frame(r, device)
     fr.upload(fb)
     r.render_backward(ds, cam, fr, up, grads, err_pixel, blended_error)
+
+
+def losses_backward(scene: Scene, fb: FrameBuffers, gt: np.ndarray, w: LossWeights, grads: SceneGrads,
+                    device: int = 0):
+    """losses_backward (losses.hpp:52-56): returns (LossTerms as a dict, d_final,
+    d_weights, d_texture) and accumulates the opacity / grid regularisers into ``grads``."""
+    r = _renderer(device)
+    ds = _device_scene(r, scene)
+    fr = _value_frame(r, device)
+    fr.upload(fb)
+    return r.losses_backward(ds, fr, gt, w, grads)
 
 
 # ---------------------------------------------------------------- synthetic inputs (SURVEY.md §8(d))

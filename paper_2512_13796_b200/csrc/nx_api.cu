@@ -86,6 +86,7 @@ struct nx_ctx {
     nx_frame* bwd_lists = nullptr;   // work lists of the re-binned camera
     DevBuf d_t_slot, act_grad;
     DevBuf h_up[3], h_err, h_blend, h_grads[5];  // device copies for nx_render_backward_host
+    DevBuf loss_scratch, h_gt, h_terms;          // losses_backward
     int32_t* h_pinned = nullptr;  // small readbacks
     bool profiling = false;
     cudaStream_t stream2 = nullptr;  // texture passes: overlap the next frame's collection
@@ -538,7 +539,8 @@ void nx_ctx_destroy(nx_ctx* c) {
                       &c->skeys_b, &c->sids_a, &c->sids_b, &c->counts, &c->offsets, &c->tkeys_a, &c->tkeys_b,
                       &c->tvals_a, &c->tvals_b, &c->tile_counts, &c->scratch, &c->dbg_hits, &c->dbg_counts})
         b->release();
-    for (DevBuf* b : {&c->d_t_slot, &c->act_grad, &c->h_err, &c->h_blend}) b->release();
+    for (DevBuf* b : {&c->d_t_slot, &c->act_grad, &c->h_err, &c->h_blend, &c->loss_scratch, &c->h_gt, &c->h_terms})
+        b->release();
     for (DevBuf& b : c->h_up) b.release();
     for (DevBuf& b : c->h_grads) b.release();
     if (c->bwd_lists) nx_frame_destroy(c->bwd_lists);
@@ -1013,6 +1015,79 @@ int nx_render_backward_host(nx_ctx* c, const nx_scene* scene, const nx_camera* c
         NX_CUDA(c, cudaMemcpyAsync(g_host[i], *g_dev[i], g_sizes[i] * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (blend_dev)
         NX_CUDA(c, cudaMemcpyAsync(blended_error, blend_dev, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    NX_CUDA(c, cudaStreamSynchronize(s));
+    return NX_OK;
+}
+
+void nx_loss_weights_default(nx_loss_weights* w) {  // LossWeights (losses.hpp:12-18)
+    if (!w) return;
+    w->dssim = 0.2;
+    w->alpha = 0.005;
+    w->texture = 0.5;
+    w->opacity = 0.01;
+    w->grid = 0.01;
+}
+
+// losses_backward (losses.cpp:107-238) on the frame's final_img / slots.
+int nx_losses_backward(nx_ctx* c, const nx_scene* scene, const nx_frame* fc, const double* gt,
+                       const nx_loss_weights* w, double* d_final, double* d_weights, double* d_texture,
+                       const nx_grads* g, nx_loss_terms* terms, void* stream) {
+    if (!c || !scene || !fc || !gt || !w || !d_final || !g || !g->prims || !g->table || !terms)
+        return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    nx_frame* f = const_cast<nx_frame*>(fc);
+    if (f->K > 0 && (!d_weights || !d_texture))
+        return set_err(c, NX_INVALID_ARGUMENT, "losses_backward: d_weights / d_texture are required when top_k > 0");
+    if (f->K != scene->st.top_k)
+        return set_err(c, NX_INVALID_ARGUMENT, "losses_backward: the frame does not match the scene's top_k");
+    cudaSetDevice(c->device);
+    cudaStream_t s = pick_stream(c, stream);
+    NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_ready, 0));
+    if (f->busy_pending) NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_busy, 0));
+    const int64_t npix = static_cast<int64_t>(f->W) * f->H;
+    NX_CUDA(c, c->loss_scratch.ensure(losses_scratch_bytes(npix)));
+    const int st = launch_losses_backward(scene_dev(scene), frame_dev(f), gt, *w, d_final, d_weights, d_texture,
+                                          g->prims, g->table, terms, c->loss_scratch.p, s);
+    if (st) return set_err(c, st, "losses_backward: field shape not supported");
+    NX_CUDA(c, cudaEventRecord(f->ev_busy, s));
+    f->busy_pending = true;
+    NX_CUDA(c, cudaGetLastError());
+    return NX_OK;
+}
+
+int nx_losses_backward_host(nx_ctx* c, const nx_scene* scene, const nx_frame* fc, const double* gt,
+                            const nx_loss_weights* w, double* d_final, double* d_weights, double* d_texture,
+                            const nx_grads* g, nx_loss_terms* terms) {
+    if (!c || !scene || !fc || !gt || !w || !d_final || !g || !g->prims || !g->table || !terms)
+        return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    cudaSetDevice(c->device);
+    cudaStream_t s = c->stream;
+    const size_t npix = static_cast<size_t>(fc->W) * fc->H, K = fc->K, n = static_cast<size_t>(scene->n);
+    const nx_field_desc& fd = scene->field;
+    const size_t ntab = static_cast<size_t>(fd.levels) * (size_t(1) << fd.log2_table) * fd.features;
+    // device copies: gt, outputs (d_final, d_weights, d_texture), grads (prims, table), terms
+    NX_CUDA(c, c->h_gt.ensure(std::max<size_t>(npix * 3, 1) * sizeof(double)));
+    NX_CUDA(c, cudaMemcpyAsync(c->h_gt.p, gt, npix * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+    const size_t u_sizes[3] = {npix * 3, npix * K, npix * K * 3};
+    double* u_host[3] = {d_final, d_weights, d_texture};
+    for (int i = 0; i < 3; ++i) NX_CUDA(c, c->h_up[i].ensure(std::max<size_t>(u_sizes[i], 1) * sizeof(double)));
+    const size_t g_sizes[2] = {n * NX_PARAMS_PER_NEXEL, ntab};
+    double* g_host[2] = {g->prims, g->table};
+    for (int i = 0; i < 2; ++i) {
+        NX_CUDA(c, c->h_grads[i].ensure(std::max<size_t>(g_sizes[i], 1) * sizeof(double)));
+        NX_CUDA(c, cudaMemcpyAsync(c->h_grads[i].p, g_host[i], g_sizes[i] * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    NX_CUDA(c, c->h_terms.ensure(sizeof(nx_loss_terms)));
+    nx_grads gd{c->h_grads[0].as<double>(), c->h_grads[1].as<double>(), nullptr, nullptr, nullptr};
+    int st = nx_losses_backward(c, scene, fc, c->h_gt.as<double>(), w, c->h_up[0].as<double>(),
+                                K ? c->h_up[1].as<double>() : nullptr, K ? c->h_up[2].as<double>() : nullptr, &gd,
+                                c->h_terms.as<nx_loss_terms>(), s);
+    if (st) return st;
+    for (int i = 0; i < 3; ++i)
+        if (u_host[i] && u_sizes[i])
+            NX_CUDA(c, cudaMemcpyAsync(u_host[i], c->h_up[i].p, u_sizes[i] * sizeof(double), cudaMemcpyDeviceToHost, s));
+    for (int i = 0; i < 2; ++i)
+        NX_CUDA(c, cudaMemcpyAsync(g_host[i], c->h_grads[i].p, g_sizes[i] * sizeof(double), cudaMemcpyDeviceToHost, s));
+    NX_CUDA(c, cudaMemcpyAsync(terms, c->h_terms.p, sizeof(nx_loss_terms), cudaMemcpyDeviceToHost, s));
     NX_CUDA(c, cudaStreamSynchronize(s));
     return NX_OK;
 }

@@ -228,6 +228,12 @@ int launch_texture(const TextureArgs& a, cudaStream_t s);  // returns NX_OK / NX
 bool texture_tc_supported(const nx_field_desc& fd);
 int launch_texture_tc(const TextureArgs& a, cudaStream_t s);
 
+// ---------------------------------------------------------------- losses_backward (nx_losses.cu)
+size_t losses_scratch_bytes(int64_t npix);
+int launch_losses_backward(const SceneDev& scene, const FrameDev& fb, const double* gt, const nx_loss_weights& w,
+                           double* d_final, double* d_weights, double* d_texture, double* g_prims, double* g_table,
+                           nx_loss_terms* terms, void* scratch, cudaStream_t s);
+
 // ---------------------------------------------------------------- downloads
 struct CopyJob {
     const uint8_t* src;  // device
