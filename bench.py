@@ -43,6 +43,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU-baseline work")
     p.add_argument("--train-steps", type=int, default=10, help="timed forward+backward steps (config 5); 0 = skip")
+    p.add_argument("--config", type=int, choices=[2, 4], default=2,
+                   help="2: 400K nexels 1080p, views sharded (headline); 4: 1.3M nexels 4K, image bands x views")
     return p.parse_args()
 
 
@@ -524,10 +526,129 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------- config 4: 1.3M nexels at 4K, bands
+def run_config4(args):
+    """BASELINE.json configs[3]: 1.3M nexels at 3840x2160 with image-band sharding:
+    every step renders one full 4K view, rank r owning rows band(r) (tile-aligned),
+    views advancing along the ring; no collective on the data path. value = full
+    frames/s (strong scaling: a frame's work is split across the ranks)."""
+    world, rank, local, dist = dist_setup(args)
+    import torch
+    import paper_2512_13796_b200 as nx
+    from paper_2512_13796_b200 import _abi
+    torch.cuda.set_device(local)
+    n = args.nexels if args.nexels != 400_000 else 1_300_000
+    W, H = (args.width, args.height) if (args.width, args.height) != (1920, 1080) else (3840, 2160)
+    K = 2
+    scene = nx.stump_like(n)
+    r = nx.Renderer(local)
+    ds = r.upload(scene)
+    y0, rows = nx.image_bands(H, world)[rank]
+    n_steps = args.warmup + args.steps
+    cams = [nx.band_camera(nx.ring_camera(s % N_VIEWS, N_VIEWS, W, H), y0, rows) for s in range(n_steps)]
+    frames = [r.frame(), r.frame()]
+    stats = []
+    for s in range(args.warmup, min(n_steps, args.warmup + 3)):  # untimed work statistics
+        r.render(ds, cams[s], frames[0])
+        stats.append(frames[0].stats())
+    for s in range(args.warmup):
+        r.render(ds, cams[s], frames[s % 2])
+    r.synchronize()
+    stream = torch.cuda.ExternalStream(r.stream, device=torch.device("cuda", local))
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = r.lib.nx_launch_count()
+    barrier(dist)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for s in range(args.warmup, n_steps):
+        r.render(ds, cams[s], frames[s % 2])
+    r._check(r.lib.nx_ctx_join(r.ctx))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(dist)
+    clk = clocks.stop()
+    launches = int(r.lib.nx_launch_count() - launches0)
+    ms = max_over_ranks(dist, e0.elapsed_time(e1), f"cuda:{local}")
+    fps = args.steps / (ms / 1e3)
+    # e2e: band render + download of the band's FrameBuffers into pinned memory
+    npix = W * rows
+    host = {k: torch.empty(sz, dtype=dt, pin_memory=True) for k, sz, dt in (
+        ("base", npix * 3, torch.float32), ("ids", npix * K, torch.int32), ("depths", npix * K, torch.float64),
+        ("weights", npix * K, torch.float64), ("texture", npix * K * 3, torch.float32),
+        ("final_img", npix * 3, torch.float32), ("residual", npix, torch.float32))}
+    hf = _abi.nx_host_frame()
+    for k, t in host.items():
+        setattr(hf, k, t.data_ptr())
+    frames.append(r.frame())
+    for s in range(3):
+        r.render(ds, cams[s], frames[s])
+        r._check(r.lib.nx_frame_download(r.ctx, frames[s].handle, C.byref(hf), None))
+    r._check(r.lib.nx_ctx_join(r.ctx))
+    barrier(dist)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for s in range(args.warmup, n_steps):
+        f2 = frames[s % 3]
+        r.render(ds, cams[s], f2)
+        r._check(r.lib.nx_frame_download(r.ctx, f2.handle, C.byref(hf), None))
+    r._check(r.lib.nx_ctx_join(r.ctx))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(dist)
+    e2e_ms = max_over_ranks(dist, e0.elapsed_time(e1), f"cuda:{local}")
+    d2h = sum(t.numel() * t.element_size() for t in host.values())
+    # frame roofline (SURVEY.md §8(d)) from this rank's band statistics, summed over ranks
+    mean = lambda key: sum(st[key] for st in stats) / max(len(stats), 1)
+    P, Q = mean("tile_keys"), mean("n_queries")
+    if dist is not None:
+        t = torch.tensor([P, Q], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t)
+        P, Q = float(t[0]), float(t[1])
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    fbytes = frame_bytes(n, P, H, W, K, Q)
+    if rank == 0:
+        line = {
+            "metric": f"rendered 4K frames/sec at {n // 1000}K nexels (config 4) + % HBM roofline",
+            "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config 4: stump_like {n} nexels, {W}x{H}, K=2, {world} image band(s) of one "
+                                   f"view per step, views along the 256-view ring", "nexels": n, "width": W,
+                       "height": H, "top_k": K, "bands": nx.image_bands(H, world),
+                       "l2": "inputs larger than L2, view changes every step"},
+            "frame_roofline": {"bytes_per_frame": fbytes, "achieved": fbytes * fps / 1e9, "peak": hbm_peak,
+                               "unit": "GB/s", "frac": fbytes * fps / 1e9 / hbm_peak,
+                               "formula": "240N + 8P + (28+24K)HW + 1024Q + 36864"},
+            "work": {"tile_keys_P": P, "queries_Q": Q},
+            "e2e": {"value": args.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": C.sizeof(_abi.nx_camera),
+                    "d2h_bytes_per_step": d2h * world,
+                    "path": "per rank: nx_render (band) + nx_frame_download of the band, 3 frames in flight"},
+            "gpu_launches": launches, "clocks": clk,
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    for f2 in frames:
+        f2.close()
+    ds.close()
+    r.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference_arm(args)
+    elif args.config == 4:
+        run_config4(args)
     else:
         run_ours(args)
 

@@ -6,13 +6,13 @@ Drop-in for the reference's ``nexel::render`` / ``collection_pass`` /
 ``include/nexel_b200.h``); this package is the host-side mirror of the
 reference interface.
 """
-from .api import (Camera, DeviceFrame, DeviceScene, FrameBuffers, HashGridConfig, NexelError, RenderResult,
+from .api import (Camera, band_camera, image_bands, DeviceFrame, DeviceScene, FrameBuffers, HashGridConfig, NexelError, RenderResult,
                   LossWeights, RenderSettings, Renderer, Scene, SceneGrads, TextureField, UpstreamGrads, collection_pass, render,
                   losses_backward, render_backward, ring_camera, stump_like, texturing_pass)
 from . import _abi
 
 __all__ = [
-    "Camera", "DeviceFrame", "DeviceScene", "FrameBuffers", "HashGridConfig", "NexelError", "RenderResult",
+    "Camera", "band_camera", "image_bands", "DeviceFrame", "DeviceScene", "FrameBuffers", "HashGridConfig", "NexelError", "RenderResult",
     "LossWeights", "RenderSettings", "Renderer", "Scene", "SceneGrads", "TextureField", "UpstreamGrads", "collection_pass",
     "losses_backward", "render", "render_backward", "ring_camera", "stump_like", "texturing_pass", "_abi",
 ]

@@ -637,6 +637,26 @@ def stump_like(n: int, coverage: float = 1.0, seed: int = 2512, ground_radius: f
     return Scene(nex, TextureField(grid, table, w1, w2, w3, d.n_hidden), RenderSettings.from_c(s), extent=8.0)
 
 
+def band_camera(cam: Camera, y0: int, rows: int) -> Camera:
+    """Rows [y0, y0 + rows) of ``cam`` as a camera of its own (principal point shifted):
+    every pixel keeps its ray (camera.hpp:32-35), hence its contributor list and
+    colour — the image-band sharding of SURVEY.md §8(e) needs no collective."""
+    if y0 < 0 or rows < 0 or y0 + rows > cam.height:
+        raise NexelError("invalid-argument", "band outside the image")
+    return Camera(cam.width, rows, cam.fx, cam.fy, cam.cx, cam.cy - y0, cam.R, cam.t, f"{cam.name}[{y0}:{y0 + rows}]")
+
+
+def image_bands(height: int, n: int, align: int = 16):
+    """n contiguous row bands covering the image, tile-aligned (the last one shorter)."""
+    step = -(-height // n)
+    step = -(-step // align) * align
+    out = []
+    for i in range(n):
+        y0 = min(i * step, height)
+        out.append((y0, max(0, min(height, y0 + step) - y0)))
+    return out
+
+
 def ring_camera(index: int, n_views: int = 256, width: int = 1920, height: int = 1080) -> Camera:
     lib = _abi.load()
     c = _abi.nx_camera()

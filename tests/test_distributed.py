@@ -75,3 +75,18 @@ def test_frame_bytes_formula_matches_survey():
     assert abs(b2 / 1e9 - 4.32) < 0.01
     b1 = bench.frame_bytes(10_000, 143_383, 256, 256, 2, 129_157)
     assert abs(b1 / 1e6 - 140.8) < 0.5
+
+
+def test_image_bands_partition_the_rows():
+    import paper_2512_13796_b200 as nx
+    for H in (2160, 1080, 256, 100):
+        for n in (1, 2, 3, 4, 8):
+            bands = nx.image_bands(H, n)
+            assert len(bands) == n
+            y = 0
+            for y0, rows in bands:
+                assert y0 == min(y, H) and rows >= 0
+                if rows:
+                    assert y0 % 16 == 0
+                y = y0 + rows
+            assert y == H

@@ -267,3 +267,27 @@ def test_config2_full_frame_parity(renderer, reference, config2):
     rep = compare_frames(g, r)
     assert abs(float(g.final_img.astype(np.float64).sum()) - 2766856.890023658) < 1.0
     print("config2 parity", rep)
+
+
+# ---------------------------------------------------------------- image bands (config 4 sharding)
+@pytest.mark.parametrize("n_bands", [2, 3, 8])
+def test_image_bands_reassemble_the_full_frame_bit_exact(renderer, n_bands):
+    # rank r renders rows band(r) of the view; every pixel keeps its
+    # ray, contributor list and colour, so the bands concatenate to the full frame
+    scene = nx.stump_like(20_000, log2_table=14, grid_init=1e-1)
+    cam = nx.ring_camera(11, 256, 320, 200)
+    full, _ = gpu_render(renderer, scene, cam)
+    ds = renderer.upload(scene)
+    fr = renderer.frame()
+    parts = []
+    bands = nx.image_bands(cam.height, n_bands)
+    assert sum(r for _, r in bands) == cam.height
+    for y0, rows in bands:
+        if rows == 0:
+            continue
+        renderer.render(ds, nx.band_camera(cam, y0, rows), fr)
+        parts.append(fr.download())
+    for key, per_px in (("ids", 2), ("depths", 2), ("weights", 2), ("base", 3), ("texture", 6), ("final_img", 3),
+                        ("residual", 1)):
+        got = np.concatenate([getattr(p, key) for p in parts])
+        assert np.array_equal(got, getattr(full, key)), key
