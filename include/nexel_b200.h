@@ -43,6 +43,8 @@ extern "C" {
 #define NX_BAD_SETTINGS 1    /* "bad-settings"  (renderer.cpp:13-21) */
 #define NX_BAD_CAMERA 2      /* "bad-camera"    (camera.cpp:8-31)    */
 #define NX_BAD_PRIMITIVE 3   /* "bad-primitive" (primitive.cpp:47-63) */
+#define NX_MISSING_FILE 4    /* "missing-file"  (checkpoint.cpp:57)   */
+#define NX_BAD_CHECKPOINT 5  /* "bad-checkpoint" (checkpoint.cpp:59-269) */
 #define NX_INVALID_ARGUMENT 10
 #define NX_UNSUPPORTED 11
 #define NX_OUT_OF_MEMORY 12
@@ -175,6 +177,27 @@ int nx_scene_create(nx_ctx* ctx, const nx_settings* settings, int64_t n_nexels,
 int nx_scene_set_settings(nx_ctx* ctx, nx_scene* scene, const nx_settings* settings);
 int nx_scene_get_settings(const nx_scene* scene, nx_settings* out);
 void nx_scene_destroy(nx_scene* scene);
+
+/* ---- NEXL checkpoints (checkpoint.hpp:19-28, checkpoint.cpp:173-271) --- */
+/* Header facts of a checkpoint (CheckpointExtra + the scene's shape). */
+typedef struct nx_nexl_info {
+    uint64_t iteration;
+    int64_t n_nexels;
+    int32_t n_cameras;
+    int32_t has_optimizer;   /* optimizer section present (skipped by the loader) */
+    double extent;
+    nx_settings settings;
+    nx_field_desc field;
+} nx_nexl_info;
+/* load_checkpoint straight into a device scene: the fp32 SoA sections are read into
+ * pinned staging and converted / uploaded on the device (positions & shape params to
+ * the fp64 geometry layout, SH, table and MLP weights as stored). Validation and error
+ * codes as the reference: missing-file, bad-checkpoint (magic, version, implausible
+ * shapes, truncation), then bad-primitive at render time like nx_scene_create. */
+int nx_scene_load_nexl(nx_ctx* ctx, const char* path, nx_scene** out, nx_nexl_info* info);
+/* The training cameras stored in the checkpoint (CheckpointExtra::cameras); `names`
+ * (nullable) receives up to 63 chars + NUL per camera. *n = number stored. */
+int nx_nexl_cameras(const char* path, nx_camera* cams, char (*names)[64], int capacity, int* n);
 
 /* ---- frames (FrameBuffers) -------------------------------------------- */
 int nx_frame_create(nx_ctx* ctx, int width, int height, int top_k, nx_frame** out);

@@ -204,6 +204,7 @@ class Reference:
         L.ref_downweight.argtypes = [C.c_double] * 3
         L.ref_field_forward.argtypes = [P, C.c_int64, PD, C.c_int, PD]
         L.ref_render_backward.argtypes = [P, Cm, PD, PD, PD, PD, PD, PD, PD, PD, PD, PD]
+        L.ref_save_checkpoint.argtypes = [P, C.c_char_p, Cm, C.c_int, C.c_uint64, C.c_double]
         L.ref_losses_backward.argtypes = [P, C.c_int, C.c_int, C.c_int, PI32, PD, PD, PD, PD, PD, PD, PD, PD, PD,
                                           PD, PD]
         self._scene = None
@@ -311,6 +312,12 @@ class Reference:
                                                  _dp(terms)))
         keys = ("l1", "dssim", "image", "texture", "alpha", "opacity", "grid", "total")
         return dict(zip(keys, terms.tolist())), d_final, d_weights[: npix * K], d_texture[: npix * K * 3], gp, gtab
+
+    def save_checkpoint(self, scene: Scene, path: str, cams, iteration: int = 0):
+        """save_checkpoint (checkpoint.cpp:99-171) of the scene with the cameras."""
+        h = self._handle(scene)
+        arr = (_abi.nx_camera * max(len(cams), 1))(*[c.to_c() for c in cams])
+        self._check(self.lib.ref_save_checkpoint(h, str(path).encode(), arr, len(cams), iteration, scene.extent))
 
     # ---- the reference test generators (tests/helpers.hpp:88-125)
     def random_scene(self, seed: int, n_prims: int, top_k: int, res: int, focal: float, dist: float,

@@ -15,6 +15,7 @@
 #include "renderer.cpp"  // -I /root/reference/proj/core/src: compiled in place, not copied
 #include "helpers.hpp"                                  // -I /root/reference/proj/tests
 
+#include "nexel/checkpoint.hpp"
 #include "nexel/losses.hpp"
 #include "nexel/oracle.hpp"
 
@@ -426,6 +427,24 @@ int ref_losses_backward(const ref_scene* h, int W, int H, int K, const int32_t* 
         std::memcpy(g_table, grads.field.table.data(), grads.field.table.size() * sizeof(double));
         const double tv[8] = {t.l1, t.dssim, t.image, t.texture, t.alpha, t.opacity, t.grid, t.total};
         std::memcpy(terms, tv, sizeof tv);
+    });
+}
+
+// nexel::save_checkpoint (checkpoint.cpp:99-171) of the scene with the given cameras
+// (named "cam<i>") and iteration counter; no optimizer section.
+int ref_save_checkpoint(const ref_scene* h, const char* path, const nx_camera* cams, int n_cams,
+                        uint64_t iteration, double extent) {
+    return guarded([&] {
+        Scene scene = h->scene;
+        scene.extent = extent;
+        CheckpointExtra extra;
+        extra.iteration = iteration;
+        for (int i = 0; i < n_cams; ++i) {
+            Camera c = to_camera(cams[i]);
+            c.name = "cam" + std::to_string(i);
+            extra.cameras.push_back(c);
+        }
+        save_checkpoint(path, scene, extra);
     });
 }
 

@@ -16,6 +16,8 @@ NX_OK = 0
 NX_BAD_SETTINGS = 1
 NX_BAD_CAMERA = 2
 NX_BAD_PRIMITIVE = 3
+NX_MISSING_FILE = 4
+NX_BAD_CHECKPOINT = 5
 NX_INVALID_ARGUMENT = 10
 NX_UNSUPPORTED = 11
 NX_OUT_OF_MEMORY = 12
@@ -32,6 +34,8 @@ STATUS_CODES = {
     NX_BAD_SETTINGS: "bad-settings",
     NX_BAD_CAMERA: "bad-camera",
     NX_BAD_PRIMITIVE: "bad-primitive",
+    NX_MISSING_FILE: "missing-file",
+    NX_BAD_CHECKPOINT: "bad-checkpoint",
     NX_INVALID_ARGUMENT: "invalid-argument",
     NX_UNSUPPORTED: "unsupported",
     NX_OUT_OF_MEMORY: "out-of-memory",
@@ -139,6 +143,12 @@ class nx_loss_terms(C.Structure):
         return {k: float(getattr(self, k)) for k, _ in self._fields_}
 
 
+class nx_nexl_info(C.Structure):
+    _fields_ = [("iteration", C.c_uint64), ("n_nexels", C.c_int64), ("n_cameras", C.c_int32),
+                ("has_optimizer", C.c_int32), ("extent", C.c_double), ("settings", nx_settings),
+                ("field", nx_field_desc)]
+
+
 class nx_frame_stats(C.Structure):
     _fields_ = [
         ("n_nexels", C.c_int64),
@@ -185,6 +195,8 @@ SIGNATURES = [
     ("nx_scene_create", C.c_int,
      [P, C.POINTER(nx_settings), I64, PD, C.POINTER(nx_field_desc), PD, PD, PD, PD, C.POINTER(P)]),
     ("nx_scene_set_settings", C.c_int, [P, P, C.POINTER(nx_settings)]),
+    ("nx_scene_load_nexl", C.c_int, [P, C.c_char_p, C.POINTER(P), C.POINTER(nx_nexl_info)]),
+    ("nx_nexl_cameras", C.c_int, [C.c_char_p, C.POINTER(nx_camera), C.c_void_p, C.c_int, C.POINTER(C.c_int)]),
     ("nx_scene_get_settings", C.c_int, [P, C.POINTER(nx_settings)]),
     ("nx_scene_destroy", None, [P]),
     ("nx_frame_create", C.c_int, [P, C.c_int, C.c_int, C.c_int, C.POINTER(P)]),

@@ -405,6 +405,25 @@ class Renderer:
                                              _dp(w1), _dp(w2), _dp(w3), C.byref(h)))
         return DeviceScene(self, h, nex.shape[0])
 
+    def load_checkpoint(self, path: str):
+        """load_checkpoint (checkpoint.hpp:27-28) straight into a device scene: returns
+        (DeviceScene, info dict with iteration / extent / settings / field, cameras)."""
+        h = C.c_void_p()
+        info = _abi.nx_nexl_info()
+        self._check(self.lib.nx_scene_load_nexl(self.ctx, str(path).encode(), C.byref(h), C.byref(info)))
+        ds = DeviceScene(self, h, int(info.n_nexels))
+        n = C.c_int(0)
+        self._check(self.lib.nx_nexl_cameras(str(path).encode(), None, None, 0, C.byref(n)))
+        cams = (_abi.nx_camera * max(n.value, 1))()
+        names = (C.c_char * 64 * max(n.value, 1))()
+        self._check(self.lib.nx_nexl_cameras(str(path).encode(), cams, names, n.value, C.byref(n)))
+        cameras = [Camera.from_c(cams[i], bytes(names[i]).split(b"\0")[0].decode()) for i in range(n.value)]
+        meta = {"iteration": int(info.iteration), "extent": float(info.extent), "n_nexels": int(info.n_nexels),
+                "has_optimizer": bool(info.has_optimizer), "settings": RenderSettings.from_c(info.settings),
+                "field": HashGridConfig(info.field.levels, info.field.log2_table, info.field.features,
+                                        info.field.base_scale, info.field.growth), "n_hidden": info.field.n_hidden}
+        return ds, meta, cameras
+
     def frame(self, width: int = 0, height: int = 0, top_k: int = 0) -> DeviceFrame:
         h = C.c_void_p()
         self._check(self.lib.nx_frame_create(self.ctx, width, height, top_k, C.byref(h)))

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "nx_internal.cuh"
+#include "nx_nexl.h"
 #include "nx_sort.cuh"
 
 using namespace nx;
@@ -488,6 +489,8 @@ const char* nx_status_name(int status) {
         case NX_BAD_SETTINGS: return "bad-settings";
         case NX_BAD_CAMERA: return "bad-camera";
         case NX_BAD_PRIMITIVE: return "bad-primitive";
+        case NX_MISSING_FILE: return "missing-file";
+        case NX_BAD_CHECKPOINT: return "bad-checkpoint";
         case NX_INVALID_ARGUMENT: return "invalid-argument";
         case NX_UNSUPPORTED: return "unsupported";
         case NX_OUT_OF_MEMORY: return "out-of-memory";
@@ -674,6 +677,82 @@ int nx_scene_create(nx_ctx* c, const nx_settings* settings, int64_t n, const dou
         nx_scene_destroy(s);
         return cuda_err(c, e, "scene upload");
     }
+    *out = s;
+    return NX_OK;
+}
+
+// load_checkpoint (checkpoint.cpp:173-271) into a device scene. The parameter
+// sections are fp32 SoA on disk; positions / shape parameters become the fp64
+// geometry rows (exact widening), SH, table and MLP weights are uploaded as stored.
+int nx_scene_load_nexl(nx_ctx* c, const char* path, nx_scene** out, nx_nexl_info* info) {
+    if (!c || !path || !out) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    NexlHeader h;
+    NexlArrays arr;
+    std::string err;
+    int st = nexl_read(path, true, h, &arr, err);
+    if (st) return set_err(c, st, err);
+    if (h.info.n_nexels >= (int64_t(1) << 31)) return set_err(c, NX_UNSUPPORTED, "more than 2^31 primitives");
+    cudaSetDevice(c->device);
+    nx_scene* s = new (std::nothrow) nx_scene;
+    if (!s) return set_err(c, NX_OUT_OF_MEMORY, "host allocation");
+    s->ctx = c;
+    const int64_t n = h.info.n_nexels;
+    s->n = n;
+    s->field = h.info.field;
+    s->st = h.info.settings;
+    // validation exactly as activate() (primitive.cpp:47-63), first failing id
+    const char* whats[] = {"non-finite position", "non-finite quaternion", "non-finite log scale",
+                           "non-finite kernel exponent", "non-finite opacity", "non-finite sh coefficient",
+                           "degenerate quaternion"};
+    for (int64_t i = 0; i < n && !s->bad_status; ++i) {
+        int what = -1;
+        for (int k = 0; k < 3 && what < 0; ++k)
+            if (!std::isfinite(arr.mu[i * 3 + k])) what = 0;
+        for (int k = 0; k < 4 && what < 0; ++k)
+            if (!std::isfinite(arr.quat[i * 4 + k])) what = 1;
+        for (int k = 0; k < 2 && what < 0; ++k) {
+            if (!std::isfinite(arr.log_scale[i * 2 + k])) what = 2;
+            else if (!std::isfinite(arr.gamma[i * 2 + k])) what = 3;
+        }
+        if (what < 0 && !std::isfinite(arr.opacity[i])) what = 4;
+        for (int k = 0; k < NX_SH_VALUES && what < 0; ++k)
+            if (!std::isfinite(arr.sh[i * NX_SH_VALUES + k])) what = 5;
+        if (what < 0) {
+            double qn = 0.0;
+            for (int k = 0; k < 4; ++k) qn += static_cast<double>(arr.quat[i * 4 + k]) * arr.quat[i * 4 + k];
+            if (!(std::sqrt(qn) > 1e-12)) what = 6;
+        }
+        if (what >= 0) {
+            s->bad_status = NX_BAD_PRIMITIVE;
+            s->bad_msg = std::string(whats[what]) + " in primitive " + std::to_string(i);
+        }
+    }
+    const int64_t nn = std::max<int64_t>(n, 1);
+    std::vector<double> geom(static_cast<size_t>(kGeomFields * nn), 0.0);
+    for (int64_t i = 0; i < n; ++i) {
+        for (int k = 0; k < 3; ++k) geom[k * nn + i] = arr.mu[i * 3 + k];
+        for (int k = 0; k < 4; ++k) geom[(3 + k) * nn + i] = arr.quat[i * 4 + k];
+        for (int k = 0; k < 2; ++k) geom[(7 + k) * nn + i] = arr.log_scale[i * 2 + k];
+        geom[9 * nn + i] = arr.opacity[i];
+        for (int k = 0; k < 2; ++k) geom[(10 + k) * nn + i] = arr.gamma[i * 2 + k];
+    }
+    auto up = [&](DevBuf& b, const void* src, size_t bytes) -> cudaError_t {
+        cudaError_t e = b.ensure(std::max<size_t>(bytes, 4));
+        if (e == cudaSuccess && bytes) e = cudaMemcpy(b.p, src, bytes, cudaMemcpyHostToDevice);
+        return e;
+    };
+    cudaError_t e = up(s->geom, geom.data(), geom.size() * sizeof(double));
+    if (e == cudaSuccess) e = up(s->sh, arr.sh.data(), arr.sh.size() * sizeof(float));
+    if (e == cudaSuccess) e = up(s->table, arr.table.data(), arr.table.size() * sizeof(float));
+    if (e == cudaSuccess) e = up(s->w1, arr.w1.data(), arr.w1.size() * sizeof(float));
+    if (e == cudaSuccess) e = up(s->w2, arr.w2.data(), arr.w2.size() * sizeof(float));
+    if (e == cudaSuccess) e = up(s->w3, arr.w3.data(), arr.w3.size() * sizeof(float));
+    if (e != cudaSuccess) {
+        nx_scene_destroy(s);
+        return cuda_err(c, e, "checkpoint upload");
+    }
+    if (info) *info = h.info;
     *out = s;
     return NX_OK;
 }

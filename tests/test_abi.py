@@ -111,3 +111,28 @@ def test_hash_grid_config_for_extent():
     g = nx.HashGridConfig.for_extent(2.0)
     assert g.base_scale == 0.5 and abs(g.base_scale * g.growth ** 15 - 16384.0) < 1e-6
     assert g.param_count() == 16 * (1 << 20) * 2
+
+
+def test_nexl_header_reader_on_a_reference_checkpoint(tmp_path):
+    # host-side half of nx_scene_load_nexl: cameras and error codes, no GPU needed
+    from oracle.pyoracle import Reference
+    try:
+        ref = Reference()
+    except ImportError as e:
+        pytest.skip(str(e))
+    lib = _abi.load()
+    scene = nx.stump_like(300, log2_table=8)
+    cams = [nx.ring_camera(i, 256, 40 + i, 30) for i in range(3)]
+    path = str(tmp_path / "s.nexl")
+    ref.save_checkpoint(scene, path, cams, iteration=7)
+    n = C.c_int(0)
+    out = (_abi.nx_camera * 3)()
+    names = (C.c_char * 64 * 3)()
+    assert lib.nx_nexl_cameras(path.encode(), out, names, 3, C.byref(n)) == _abi.NX_OK
+    assert n.value == 3
+    for i in range(3):
+        assert bytes(names[i]).split(b"\0")[0] == f"cam{i}".encode()
+        assert out[i].width == 40 + i and list(out[i].R) == list(cams[i].to_c().R)
+    assert lib.nx_nexl_cameras(str(tmp_path / "none.nexl").encode(), None, None, 0, C.byref(n)) == \
+        _abi.NX_MISSING_FILE
+    assert lib.nx_status_name(_abi.NX_BAD_CHECKPOINT) == b"bad-checkpoint"
