@@ -271,11 +271,13 @@ def run_reference_arm(args):
 
 # ---------------------------------------------------------------- config 5: forward + backward
 def train_step_timing(args, r, ds, scene, cam, stream, dist, local):
-    """BASELINE.json configs[4]: the render path of one training step (trainer.cpp:
-    274-302) — render (collection + texturing, fp64 base kept), losses_backward against a
-    ground-truth image (the render of the grid_init 1e-1 variant),
-    the per-pixel error map, and render_backward into device SceneGrads — timed with
-    CUDA events on the render stream and reported beside the headline metric."""
+    """BASELINE.json configs[4]: one training iteration (trainer.cpp:262-323) without
+    density control — zeroed SceneGrads, render (collection + texturing, fp64 base
+    kept), losses_backward against a ground-truth image (the render of the grid_init
+    1e-1 variant), the per-pixel error map, render_backward, the
+    gradient all-reduce across ranks (N > 1, one view per rank) and the Adam step of the
+    11 parameter groups — timed with CUDA events on the render stream and reported beside
+    the headline metric. The scene is trained in place (it is the benchmark's own copy)."""
     import torch
     import ctypes as C
     import paper_2512_13796_b200 as nx
@@ -310,6 +312,14 @@ def train_step_timing(args, r, ds, scene, cam, stream, dist, local):
     gg = _abi.nx_grads(*(t.data_ptr() for t in grads))
     lw = _abi.nx_loss_weights()
     r.lib.nx_loss_weights_default(C.byref(lw))
+    # Adam groups with the trainer's default rates (trainer.hpp:30-42, trainer.cpp:238-250)
+    ext = scene.extent
+    cfgs = [(1.6e-4 * ext, 1e-15), (1e-3, 1e-8), (5e-3, 1e-8), (5e-2, 1e-8), (2e-3, 1e-8), (2.5e-3, 1e-8),
+            (1.25e-4, 1e-8), (1e-2, 1e-8), (1e-3, 1e-8), (1e-3, 1e-8), (1e-3, 1e-8)]
+    acfg = (_abi.nx_adam_config * _abi.NX_NUM_GROUPS)(*[_abi.nx_adam_config(lr, 0.9, 0.999, eps)
+                                                          for lr, eps in cfgs])
+    opt = C.c_void_p()
+    r._check(r.lib.nx_optimizer_create(r.ctx, ds.handle, C.byref(opt)))
     fr = r.frame()
     fr.set_backward(True)
     c = cam.to_c()
@@ -318,6 +328,9 @@ def train_step_timing(args, r, ds, scene, cam, stream, dist, local):
 
     def step():
         nonlocal fin
+        with torch.cuda.stream(stream):  # SceneGrads::allocate (renderer.cpp:245-248), every iteration
+            for t in grads:
+                t.zero_()
         r._check(r.lib.nx_render(r.ctx, ds.handle, C.byref(c), fr.handle, s))
         r._check(r.lib.nx_losses_backward(r.ctx, ds.handle, fr.handle, C.c_void_p(gt.data_ptr()), C.byref(lw),
                                           C.c_void_p(d_final.data_ptr()), C.c_void_p(d_weights.data_ptr()),
@@ -329,6 +342,12 @@ def train_step_timing(args, r, ds, scene, cam, stream, dist, local):
             torch.mean(torch.abs(fin.double().view(npix, 3) - gt.view(npix, 3)), dim=1, out=err)
         r._check(r.lib.nx_render_backward(r.ctx, ds.handle, C.byref(c), fr.handle, C.byref(up), C.byref(gg),
                                           C.c_void_p(err.data_ptr()), C.c_void_p(blend.data_ptr()), s))
+        if dist is not None:  # data-parallel over views: mean of the ranks' gradients (NCCL)
+            with torch.cuda.stream(stream):
+                for t in grads:
+                    dist.all_reduce(t)
+                    t.div_(dist.get_world_size())
+        r._check(r.lib.nx_optimizer_step(r.ctx, opt, ds.handle, C.byref(gg), acfg, s))
 
     for _ in range(3):
         step()
@@ -349,12 +368,14 @@ def train_step_timing(args, r, ds, scene, cam, stream, dist, local):
     t = terms.cpu().tolist()
     finite = bool(torch.isfinite(grads[0]).all().item() and torch.isfinite(grads[1]).all().item())
     fr.close()
+    r.lib.nx_optimizer_destroy(opt)
     return {"config": "configs[4]: 400K nexels 1080p forward + backward (surfel / texture gradients)",
             "ms_per_step": step_ms, "steps_per_s": 1e3 / step_ms, "forward_ms": fwd_ms,
             "losses_and_backward_ms": step_ms - fwd_ms, "steps": args.train_steps, "view": cam.name,
             "loss_total": t[7], "grads_finite": finite,
-            "path": "nx_render + nx_losses_backward (gt = grid_init 1e-1 render) + err_pixel + nx_render_backward "
-                    "(device SceneGrads)",
+            "path": "zero SceneGrads + nx_render + nx_losses_backward (gt = grid_init 1e-1 render) + err_pixel + "
+                    "nx_render_backward + [NCCL all-reduce of the gradients, N > 1] + nx_optimizer_step (Adam, 11 "
+                    "groups); no density control",
             "reference_s": "render ~55 s + render_backward 101 s per step at config 2 on 8 cores (SURVEY.md §6, "
                            "§8(f)); not re-timed here"}
 

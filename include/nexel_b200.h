@@ -295,6 +295,41 @@ int nx_losses_backward_host(nx_ctx* ctx, const nx_scene* scene, const nx_frame* 
                             const nx_loss_weights* w, double* d_final, double* d_weights, double* d_texture,
                             const nx_grads* grads, nx_loss_terms* terms);
 
+/* ---- Adam on the device scene (adam.cpp:9-22, trainer.cpp:238-323) -------- */
+/* AdamConfig (adam.hpp:8-13). */
+typedef struct nx_adam_config {
+    double lr, beta1, beta2, eps;
+} nx_adam_config;
+/* Parameter groups in the trainer's order (trainer.cpp:238-250, one AdamState each). */
+#define NX_GROUP_POSITION 0
+#define NX_GROUP_QUAT 1
+#define NX_GROUP_SCALE 2
+#define NX_GROUP_OPACITY 3
+#define NX_GROUP_GAMMA 4
+#define NX_GROUP_SH_DC 5
+#define NX_GROUP_SH_REST 6
+#define NX_GROUP_GRID 7
+#define NX_GROUP_W1 8
+#define NX_GROUP_W2 9
+#define NX_GROUP_W3 10
+#define NX_NUM_GROUPS 11
+typedef struct nx_optimizer nx_optimizer;
+/* fp64 first / second moments for every parameter of the scene, zeroed (step 0). */
+int nx_optimizer_create(nx_ctx* ctx, const nx_scene* scene, nx_optimizer** out);
+void nx_optimizer_destroy(nx_optimizer* opt);
+/* One adam_step per group (cfg[NX_NUM_GROUPS]) on the device scene's parameters in
+ * place, from device SceneGrads: per group step += 1, m/v EMAs, bias-corrected update.
+ * Parameters the device stores in fp32 (SH, hash table, MLP weights) are updated in fp64
+ * and rounded back. A group with lr == 0 is skipped (its step does not advance). */
+int nx_optimizer_step(nx_ctx* ctx, nx_optimizer* opt, nx_scene* scene, const nx_grads* grads,
+                      const nx_adam_config* cfg, void* stream);
+/* Per-group step counters (AdamState::step). */
+int nx_optimizer_steps(const nx_optimizer* opt, int64_t* steps /* NX_NUM_GROUPS */);
+/* Reads the device scene back in the reference's layouts (fp64 host arrays; any NULL
+ * is skipped): 60 doubles per nexel, table, w1, w2, w3. */
+int nx_scene_download(nx_ctx* ctx, const nx_scene* scene, double* nexels, double* table, double* w1, double* w2,
+                      double* w3);
+
 /* ---- parity / debug (not on the timed path) ---------------------------- */
 /* Tile lists for `cam`: reference_lists=1 materialises the reference's lists
  * (Binning::tile_lists, renderer.cpp:102-110, straddlers in every tile) on

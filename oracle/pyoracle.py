@@ -205,6 +205,7 @@ class Reference:
         L.ref_field_forward.argtypes = [P, C.c_int64, PD, C.c_int, PD]
         L.ref_render_backward.argtypes = [P, Cm, PD, PD, PD, PD, PD, PD, PD, PD, PD, PD]
         L.ref_save_checkpoint.argtypes = [P, C.c_char_p, Cm, C.c_int, C.c_uint64, C.c_double]
+        L.ref_adam_step.argtypes = [PD, PD, PI64, PD, PD, PD, C.c_int64]
         L.ref_losses_backward.argtypes = [P, C.c_int, C.c_int, C.c_int, PI32, PD, PD, PD, PD, PD, PD, PD, PD, PD,
                                           PD, PD]
         self._scene = None
@@ -318,6 +319,14 @@ class Reference:
         h = self._handle(scene)
         arr = (_abi.nx_camera * max(len(cams), 1))(*[c.to_c() for c in cams])
         self._check(self.lib.ref_save_checkpoint(h, str(path).encode(), arr, len(cams), iteration, scene.extent))
+
+    def adam_step(self, m, v, step: int, cfg, params, grads):
+        """adam_step (adam.cpp:9-22): updates params, m, v in place; returns the new step."""
+        st = C.c_int64(step)
+        c = np.ascontiguousarray(cfg, np.float64)
+        self._check(self.lib.ref_adam_step(_dp(m), _dp(v), C.byref(st), _dp(c), _dp(params),
+                                           _dp(np.ascontiguousarray(grads, np.float64)), params.size))
+        return st.value
 
     # ---- the reference test generators (tests/helpers.hpp:88-125)
     def random_scene(self, seed: int, n_prims: int, top_k: int, res: int, focal: float, dist: float,

@@ -15,6 +15,7 @@
 #include "renderer.cpp"  // -I /root/reference/proj/core/src: compiled in place, not copied
 #include "helpers.hpp"                                  // -I /root/reference/proj/tests
 
+#include "nexel/adam.hpp"
 #include "nexel/checkpoint.hpp"
 #include "nexel/losses.hpp"
 #include "nexel/oracle.hpp"
@@ -445,6 +446,27 @@ int ref_save_checkpoint(const ref_scene* h, const char* path, const nx_camera* c
             extra.cameras.push_back(c);
         }
         save_checkpoint(path, scene, extra);
+    });
+}
+
+// nexel::adam_step (adam.cpp:9-22) on a flat block: m, v (count each) and *step are
+// the AdamState, cfg = {lr, beta1, beta2, eps}; params updated in place.
+int ref_adam_step(double* m, double* v, int64_t* step, const double* cfg, double* params, const double* grads,
+                  int64_t count) {
+    return guarded([&] {
+        AdamState st;
+        st.m.assign(m, m + count);
+        st.v.assign(v, v + count);
+        st.step = *step;
+        AdamConfig c;
+        c.lr = cfg[0];
+        c.beta1 = cfg[1];
+        c.beta2 = cfg[2];
+        c.eps = cfg[3];
+        adam_step(st, c, params, grads, static_cast<std::size_t>(count));
+        std::memcpy(m, st.m.data(), count * sizeof(double));
+        std::memcpy(v, st.v.data(), count * sizeof(double));
+        *step = st.step;
     });
 }
 

@@ -149,6 +149,14 @@ class nx_nexl_info(C.Structure):
                 ("field", nx_field_desc)]
 
 
+class nx_adam_config(C.Structure):
+    _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double)]
+
+
+NX_NUM_GROUPS = 11
+GROUP_NAMES = ("position", "quat", "scale", "opacity", "gamma", "sh_dc", "sh_rest", "grid", "w1", "w2", "w3")
+
+
 class nx_frame_stats(C.Structure):
     _fields_ = [
         ("n_nexels", C.c_int64),
@@ -218,6 +226,11 @@ SIGNATURES = [
      [P, P, P, P, C.POINTER(nx_loss_weights), P, P, P, C.POINTER(nx_grads), P, P]),
     ("nx_losses_backward_host", C.c_int,
      [P, P, P, PD, C.POINTER(nx_loss_weights), PD, PD, PD, C.POINTER(nx_grads), C.POINTER(nx_loss_terms)]),
+    ("nx_optimizer_create", C.c_int, [P, P, C.POINTER(P)]),
+    ("nx_optimizer_destroy", None, [P]),
+    ("nx_optimizer_step", C.c_int, [P, P, P, C.POINTER(nx_grads), C.POINTER(nx_adam_config), P]),
+    ("nx_optimizer_steps", C.c_int, [P, PI64]),
+    ("nx_scene_download", C.c_int, [P, P, PD, PD, PD, PD, PD]),
     ("nx_debug_tile_lists", C.c_int,
      [P, P, C.POINTER(nx_camera), C.c_int, PI64, PI32, I64, PI64, PI32, PI32]),
     ("nx_debug_pixel_hits", C.c_int, [P, P, C.POINTER(nx_camera), C.c_int, C.c_int, C.c_int, PI32, PI32]),

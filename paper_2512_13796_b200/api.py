@@ -491,6 +491,14 @@ class Renderer:
                                                      _dp(d_texture) if K else None, C.byref(g), C.byref(t)))
         return t.as_dict(), d_final, d_weights, d_texture
 
+    def download_scene(self, dscene: DeviceScene, field_like: TextureField):
+        """The device scene's parameters in the reference's layouts: (nexels (N, 60),
+        table, w1, w2, w3) as float64."""
+        nex = np.zeros((dscene.n, _abi.NX_PARAMS_PER_NEXEL))
+        arrs = [np.zeros(np.size(a)) for a in (field_like.table, field_like.w1, field_like.w2, field_like.w3)]
+        self._check(self.lib.nx_scene_download(self.ctx, dscene.handle, _dp(nex), *(_dp(a) for a in arrs)))
+        return (nex, *arrs)
+
     def synchronize(self):
         self._check(self.lib.nx_ctx_synchronize(self.ctx))
 

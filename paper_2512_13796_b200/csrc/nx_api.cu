@@ -1171,6 +1171,106 @@ int nx_losses_backward_host(nx_ctx* c, const nx_scene* scene, const nx_frame* fc
     return NX_OK;
 }
 
+// ---------------------------------------------------------------- Adam (adam.cpp, trainer.cpp:238-323)
+}  // extern "C"
+
+struct nx_optimizer {
+    nx_ctx* ctx = nullptr;
+    int64_t n = 0;
+    DevBuf m[NX_NUM_GROUPS], v[NX_NUM_GROUPS];
+    int64_t step[NX_NUM_GROUPS] = {};
+    int64_t size[NX_NUM_GROUPS] = {};
+};
+
+extern "C" {
+
+int nx_optimizer_create(nx_ctx* c, const nx_scene* scene, nx_optimizer** out) {
+    if (!c || !scene || !out) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    cudaSetDevice(c->device);
+    nx_optimizer* o = new (std::nothrow) nx_optimizer;
+    if (!o) return set_err(c, NX_OUT_OF_MEMORY, "host allocation");
+    o->ctx = c;
+    o->n = scene->n;
+    adam_group_sizes(scene_dev(scene), o->size);
+    for (int gi = 0; gi < NX_NUM_GROUPS; ++gi) {
+        const size_t bytes = std::max<int64_t>(o->size[gi], 1) * sizeof(double);
+        if (o->m[gi].ensure(bytes) != cudaSuccess || o->v[gi].ensure(bytes) != cudaSuccess ||
+            cudaMemset(o->m[gi].p, 0, bytes) != cudaSuccess || cudaMemset(o->v[gi].p, 0, bytes) != cudaSuccess) {
+            nx_optimizer_destroy(o);
+            return set_err(c, NX_OUT_OF_MEMORY, "optimizer state");
+        }
+    }
+    *out = o;
+    return NX_OK;
+}
+
+void nx_optimizer_destroy(nx_optimizer* o) {
+    if (!o) return;
+    if (o->ctx) cudaSetDevice(o->ctx->device);
+    for (int gi = 0; gi < NX_NUM_GROUPS; ++gi) {
+        o->m[gi].release();
+        o->v[gi].release();
+    }
+    delete o;
+}
+
+int nx_optimizer_steps(const nx_optimizer* o, int64_t* steps) {
+    if (!o || !steps) return NX_INVALID_ARGUMENT;
+    for (int gi = 0; gi < NX_NUM_GROUPS; ++gi) steps[gi] = o->step[gi];
+    return NX_OK;
+}
+
+int nx_optimizer_step(nx_ctx* c, nx_optimizer* o, nx_scene* scene, const nx_grads* g, const nx_adam_config* cfg,
+                      void* stream) {
+    if (!c || !o || !scene || !g || !cfg || !g->prims || !g->table || !g->w1 || !g->w2 || !g->w3)
+        return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    if (scene->n != o->n) return set_err(c, NX_INVALID_ARGUMENT, "optimizer_step: the scene changed size");
+    cudaSetDevice(c->device);
+    cudaStream_t s = pick_stream(c, stream);
+    const SceneDev sd = scene_dev(scene);
+    for (int gi = 0; gi < NX_NUM_GROUPS; ++gi) {
+        if (cfg[gi].lr == 0.0 || o->size[gi] == 0) continue;
+        ++o->step[gi];
+        launch_adam_group(gi, sd, scene->geom.as<double>(), scene->sh.as<float>(), scene->table.as<float>(),
+                          scene->w1.as<float>(), scene->w2.as<float>(), scene->w3.as<float>(), *g, o->m[gi].as<double>(),
+                          o->v[gi].as<double>(), cfg[gi], o->step[gi], s);
+    }
+    NX_CUDA(c, cudaGetLastError());
+    return NX_OK;
+}
+
+int nx_scene_download(nx_ctx* c, const nx_scene* scene, double* nexels, double* table, double* w1, double* w2,
+                      double* w3) {
+    if (!c || !scene) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    cudaSetDevice(c->device);
+    NX_CUDA(c, cudaDeviceSynchronize());
+    const int64_t n = scene->n, nn = std::max<int64_t>(n, 1);
+    if (nexels && n > 0) {
+        std::vector<double> geom(static_cast<size_t>(kGeomFields * nn));
+        std::vector<float> sh(static_cast<size_t>(NX_SH_VALUES * nn));
+        NX_CUDA(c, cudaMemcpy(geom.data(), scene->geom.p, geom.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        NX_CUDA(c, cudaMemcpy(sh.data(), scene->sh.p, sh.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n; ++i) {
+            double* p = nexels + i * NX_PARAMS_PER_NEXEL;
+            for (int k = 0; k < kGeomFields; ++k) p[k] = geom[k * nn + i];
+            for (int k = 0; k < NX_SH_VALUES; ++k) p[12 + k] = sh[i * NX_SH_VALUES + k];
+        }
+    }
+    const nx_field_desc& fd = scene->field;
+    const size_t nin = static_cast<size_t>(fd.levels) * fd.features, nh = fd.n_hidden;
+    const size_t sizes[4] = {static_cast<size_t>(fd.levels) * (size_t(1) << fd.log2_table) * fd.features, nh * nin,
+                             nh * nh, NX_SH_VALUES * nh};
+    double* dst[4] = {table, w1, w2, w3};
+    const DevBuf* src[4] = {&scene->table, &scene->w1, &scene->w2, &scene->w3};
+    for (int k = 0; k < 4; ++k) {
+        if (!dst[k]) continue;
+        std::vector<float> tmp(sizes[k]);
+        NX_CUDA(c, cudaMemcpy(tmp.data(), src[k]->p, sizes[k] * sizeof(float), cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < sizes[k]; ++i) dst[k][i] = tmp[i];
+    }
+    return NX_OK;
+}
+
 int nx_debug_tile_lists(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, int reference_lists,
                         int64_t* offsets, int32_t* ids, int64_t capacity, int64_t* total, int32_t* tiles_x,
                         int32_t* tiles_y) {

@@ -234,6 +234,12 @@ int launch_losses_backward(const SceneDev& scene, const FrameDev& fb, const doub
                            double* d_final, double* d_weights, double* d_texture, double* g_prims, double* g_table,
                            nx_loss_terms* terms, void* scratch, cudaStream_t s);
 
+// ---------------------------------------------------------------- Adam (nx_adam.cu)
+void adam_group_sizes(const SceneDev& sc, int64_t* sizes);
+void launch_adam_group(int group, const SceneDev& sc, double* geom, float* sh, float* table, float* w1, float* w2,
+                       float* w3, const nx_grads& g, double* m, double* v, const nx_adam_config& cfg, int64_t step,
+                       cudaStream_t s);
+
 // ---------------------------------------------------------------- downloads
 struct CopyJob {
     const uint8_t* src;  // device
