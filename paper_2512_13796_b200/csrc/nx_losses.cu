@@ -316,8 +316,10 @@ int launch_losses_backward(const SceneDev& scene, const FrameDev& fb, const doub
                            double* d_final, double* d_weights, double* d_texture, double* g_prims, double* g_table,
                            nx_loss_terms* terms, void* scratch, cudaStream_t s) {
     if (scene.field.levels > kMaxLevels) return NX_UNSUPPORTED;
-    static bool taps_ready = false;
-    if (!taps_ready) {  // gaussian_taps (ssim.cpp:15-28)
+    static uint64_t taps_ready = 0;  // per device: __constant__ memory is per device
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (!((taps_ready >> (cur & 63)) & 1)) {  // gaussian_taps (ssim.cpp:15-28)
         double t[kWin], sum = 0.0;
         for (int i = 0; i < kWin; ++i) {
             const double d = i - kHalf;
@@ -326,7 +328,7 @@ int launch_losses_backward(const SceneDev& scene, const FrameDev& fb, const doub
         }
         for (double& v : t) v /= sum;
         if (cudaMemcpyToSymbol(c_taps, t, sizeof t) != cudaSuccess) return NX_CUDA_ERROR;
-        taps_ready = true;
+        taps_ready |= uint64_t(1) << (cur & 63);
     }
     LossArgs a;
     a.W = fb.W;
