@@ -330,6 +330,25 @@ int nx_optimizer_steps(const nx_optimizer* opt, int64_t* steps /* NX_NUM_GROUPS 
 int nx_scene_download(nx_ctx* ctx, const nx_scene* scene, double* nexels, double* table, double* w1, double* w2,
                       double* w3);
 
+/* ---- density control (density.cpp:102-177, trainer.cpp:324-332) -------- */
+/* prune: removes the nexels with sigmoid(opacity_raw) < min_opacity, keeping the
+ * survivors' order; the optimizer's per-nexel rows follow (adam_remap_rows,
+ * adam.cpp:24-42; opt may be NULL). new_to_old (device, capacity N, nullable) receives
+ * the source row of each survivor; *n_out the new count. Synchronous. */
+int nx_scene_prune(nx_ctx* ctx, nx_scene* scene, nx_optimizer* opt, double min_opacity, int32_t* new_to_old,
+                   int64_t* n_out);
+/* densify_split: splits min(ceil(split_fraction N), budget - N) distinct nexels sampled
+ * without replacement with probability proportional to errors[i] (keys u_i^(1/e_i),
+ * largest first, ties to the lower index), each parent replaced by two children along
+ * its longest axis (the first reuses the parent's row, the second is appended). The
+ * uniforms are the caller's draws, one per nexel in order — what the reference's
+ * uniform_real_distribution<double>(0,1)(rng) yields — so the selection reproduces the
+ * reference's. errors / uniforms: device, N doubles. new_to_old: device, capacity
+ * N + splits (nullable). Synchronous. */
+int nx_scene_densify_split(nx_ctx* ctx, nx_scene* scene, nx_optimizer* opt, const double* errors,
+                           const double* uniforms, int64_t budget, double split_fraction, int32_t* new_to_old,
+                           int64_t* n_out, int64_t* split_count);
+
 /* ---- parity / debug (not on the timed path) ---------------------------- */
 /* Tile lists for `cam`: reference_lists=1 materialises the reference's lists
  * (Binning::tile_lists, renderer.cpp:102-110, straddlers in every tile) on

@@ -206,6 +206,10 @@ class Reference:
         L.ref_render_backward.argtypes = [P, Cm, PD, PD, PD, PD, PD, PD, PD, PD, PD, PD]
         L.ref_save_checkpoint.argtypes = [P, C.c_char_p, Cm, C.c_int, C.c_uint64, C.c_double]
         L.ref_adam_step.argtypes = [PD, PD, PI64, PD, PD, PD, C.c_int64]
+        L.ref_densify_split.argtypes = [PD, C.c_int64, C.c_int64, PD, C.c_int64, C.c_double, C.c_uint64, PD, PI32,
+                                        PI64, PI64]
+        L.ref_prune.argtypes = [PD, C.c_int64, C.c_double, PI32, PI64]
+        L.ref_adam_remap_rows.argtypes = [PD, PD, C.c_int64, C.c_int64, PI32, C.c_int64]
         L.ref_losses_backward.argtypes = [P, C.c_int, C.c_int, C.c_int, PI32, PD, PD, PD, PD, PD, PD, PD, PD, PD,
                                           PD, PD]
         self._scene = None
@@ -327,6 +331,41 @@ class Reference:
         self._check(self.lib.ref_adam_step(_dp(m), _dp(v), C.byref(st), _dp(c), _dp(params),
                                            _dp(np.ascontiguousarray(grads, np.float64)), params.size))
         return st.value
+
+    def densify_split(self, nexels, errors, budget: int, split_fraction: float, seed: int):
+        """densify_split (density.cpp:102-161) with mt19937_64(seed): returns (nexels,
+        new_to_old, split_count, uniforms consumed)."""
+        n = nexels.shape[0]
+        cap = n + int(np.ceil(split_fraction * n)) + 1
+        buf = np.zeros((cap, 60))
+        buf[:n] = nexels
+        u = np.zeros(n)
+        n2o = np.zeros(cap, np.int32)
+        n_out, sc = C.c_int64(), C.c_int64()
+        self._check(self.lib.ref_densify_split(_dp(buf), n, cap, _dp(np.ascontiguousarray(errors, np.float64)),
+                                               budget, split_fraction, seed, _dp(u), n2o.ctypes.data_as(PI32),
+                                               C.byref(n_out), C.byref(sc)))
+        return buf[: n_out.value], n2o[: n_out.value], sc.value, u
+
+    def prune(self, nexels, min_opacity: float):
+        n = nexels.shape[0]
+        buf = np.ascontiguousarray(nexels, np.float64).copy()
+        n2o = np.zeros(max(n, 1), np.int32)
+        n_out = C.c_int64()
+        self._check(self.lib.ref_prune(_dp(buf), n, min_opacity, n2o.ctypes.data_as(PI32), C.byref(n_out)))
+        return buf[: n_out.value], n2o[: n_out.value]
+
+    def adam_remap_rows(self, m, v, new_to_old, width: int):
+        """adam_remap_rows (adam.cpp:24-42): returns the remapped (m, v)."""
+        rows_new = len(new_to_old)
+        m2 = np.zeros(max(m.size, rows_new * width))
+        v2 = np.zeros(max(v.size, rows_new * width))
+        m2[: m.size] = m
+        v2[: v.size] = v
+        n2o = np.ascontiguousarray(new_to_old, np.int32)
+        self._check(self.lib.ref_adam_remap_rows(_dp(m2), _dp(v2), m.size // width, rows_new,
+                                                 n2o.ctypes.data_as(PI32), width))
+        return m2[: rows_new * width].copy(), v2[: rows_new * width].copy()
 
     # ---- the reference test generators (tests/helpers.hpp:88-125)
     def random_scene(self, seed: int, n_prims: int, top_k: int, res: int, focal: float, dist: float,

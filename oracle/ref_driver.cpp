@@ -17,6 +17,7 @@
 
 #include "nexel/adam.hpp"
 #include "nexel/checkpoint.hpp"
+#include "nexel/density.hpp"
 #include "nexel/losses.hpp"
 #include "nexel/oracle.hpp"
 
@@ -467,6 +468,56 @@ int ref_adam_step(double* m, double* v, int64_t* step, const double* cfg, double
         std::memcpy(m, st.m.data(), count * sizeof(double));
         std::memcpy(v, st.v.data(), count * sizeof(double));
         *step = st.step;
+    });
+}
+
+// nexel::densify_split (density.cpp:102-161) with std::mt19937_64(seed); nexels is
+// N x 60 in / (N + splits) x 60 out (capacity cap rows); uniforms (N) receives the
+// draws the call consumed (one per nexel, in order) for the device twin.
+int ref_densify_split(double* nexels, int64_t n, int64_t cap, const double* errors, int64_t budget,
+                      double split_fraction, uint64_t seed, double* uniforms, int32_t* new_to_old, int64_t* n_out,
+                      int64_t* split_count) {
+    return guarded([&] {
+        std::vector<Nexel> nx(static_cast<size_t>(n));
+        if (n) std::memcpy(nx.data(), nexels, n * sizeof(Nexel));
+        std::vector<double> err(errors, errors + n);
+        std::mt19937_64 draws(seed);
+        std::uniform_real_distribution<double> uni(0.0, 1.0);
+        for (int64_t i = 0; i < n; ++i) uniforms[i] = uni(draws);
+        std::mt19937_64 rng(seed);
+        const DensityUpdate up = densify_split(nx, err, static_cast<int>(budget), split_fraction, rng);
+        if (static_cast<int64_t>(nx.size()) > cap) throw Error("bad-settings", "capacity");
+        std::memcpy(nexels, nx.data(), nx.size() * sizeof(Nexel));
+        std::memcpy(new_to_old, up.new_to_old.data(), up.new_to_old.size() * sizeof(int32_t));
+        *n_out = static_cast<int64_t>(nx.size());
+        *split_count = up.split_count;
+    });
+}
+
+// nexel::prune (density.cpp:163-177); nexels compacted in place.
+int ref_prune(double* nexels, int64_t n, double min_opacity, int32_t* new_to_old, int64_t* n_out) {
+    return guarded([&] {
+        std::vector<Nexel> nx(static_cast<size_t>(n));
+        if (n) std::memcpy(nx.data(), nexels, n * sizeof(Nexel));
+        const DensityUpdate up = prune(nx, min_opacity);
+        if (!nx.empty()) std::memcpy(nexels, nx.data(), nx.size() * sizeof(Nexel));
+        if (!up.new_to_old.empty()) std::memcpy(new_to_old, up.new_to_old.data(), up.new_to_old.size() * sizeof(int32_t));
+        *n_out = static_cast<int64_t>(nx.size());
+    });
+}
+
+// nexel::adam_remap_rows (adam.cpp:24-42): m / v of `rows_old` rows of `width` become
+// `rows_new` rows (capacity) following new_to_old.
+int ref_adam_remap_rows(double* m, double* v, int64_t rows_old, int64_t rows_new, const int32_t* new_to_old,
+                        int64_t width) {
+    return guarded([&] {
+        AdamState st;
+        st.m.assign(m, m + rows_old * width);
+        st.v.assign(v, v + rows_old * width);
+        std::vector<int32_t> map(new_to_old, new_to_old + rows_new);
+        adam_remap_rows(st, map, static_cast<size_t>(width));
+        std::memcpy(m, st.m.data(), st.m.size() * sizeof(double));
+        std::memcpy(v, st.v.data(), st.v.size() * sizeof(double));
     });
 }
 

@@ -231,6 +231,8 @@ SIGNATURES = [
     ("nx_optimizer_step", C.c_int, [P, P, P, C.POINTER(nx_grads), C.POINTER(nx_adam_config), P]),
     ("nx_optimizer_steps", C.c_int, [P, PI64]),
     ("nx_scene_download", C.c_int, [P, P, PD, PD, PD, PD, PD]),
+    ("nx_scene_prune", C.c_int, [P, P, P, D, P, PI64]),
+    ("nx_scene_densify_split", C.c_int, [P, P, P, P, P, I64, D, P, PI64, PI64]),
     ("nx_debug_tile_lists", C.c_int,
      [P, P, C.POINTER(nx_camera), C.c_int, PI64, PI32, I64, PI64, PI32, PI32]),
     ("nx_debug_pixel_hits", C.c_int, [P, P, C.POINTER(nx_camera), C.c_int, C.c_int, C.c_int, PI32, PI32]),

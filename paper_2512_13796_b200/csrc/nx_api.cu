@@ -1239,6 +1239,149 @@ int nx_optimizer_step(nx_ctx* c, nx_optimizer* o, nx_scene* scene, const nx_grad
     return NX_OK;
 }
 
+// ---------------------------------------------------------------- density control
+namespace {
+constexpr int kRowWidth[7] = {3, 4, 2, 1, 2, 3, 45};  // per-nexel Adam groups (trainer.cpp kRowWidth)
+
+// Rebuilds the scene (and the optimizer's per-nexel rows) in the layout of n_new nexels
+// from new_to_old (device); geometry rows from geom_new when given (densify) else
+// gathered; SH gathered unless sh_done.
+int apply_row_map(nx_ctx* c, nx_scene* scene, nx_optimizer* opt, int64_t n_new, const int32_t* n2o,
+                  DevBuf* geom_new, bool sh_done, cudaStream_t s) {
+    const int64_t n = scene->n;
+    DevBuf g2, sh2;
+    if (!geom_new) {
+        NX_CUDA(c, g2.ensure(std::max<int64_t>(n_new, 1) * kGeomFields * sizeof(double)));
+        launch_gather_geom(scene->geom.as<double>(), n, g2.as<double>(), n_new, n2o, s);
+        geom_new = &g2;
+    }
+    if (!sh_done) {
+        NX_CUDA(c, sh2.ensure(std::max<int64_t>(n_new, 1) * NX_SH_VALUES * sizeof(float)));
+        launch_gather_rows_f32(scene->sh.as<float>(), sh2.as<float>(), n_new, NX_SH_VALUES, n2o, s);
+        std::swap(scene->sh, sh2);
+    }
+    if (opt) {
+        for (int gi = 0; gi < 7; ++gi) {
+            DevBuf m2, v2;
+            const size_t bytes = std::max<int64_t>(n_new * kRowWidth[gi], 1) * sizeof(double);
+            NX_CUDA(c, m2.ensure(bytes));
+            NX_CUDA(c, v2.ensure(bytes));
+            launch_gather_rows_f64(opt->m[gi].as<double>(), m2.as<double>(), n_new, kRowWidth[gi], n2o, s);
+            launch_gather_rows_f64(opt->v[gi].as<double>(), v2.as<double>(), n_new, kRowWidth[gi], n2o, s);
+            NX_CUDA(c, cudaStreamSynchronize(s));
+            std::swap(opt->m[gi], m2);
+            std::swap(opt->v[gi], v2);
+            m2.release();
+            v2.release();
+            opt->size[gi] = n_new * kRowWidth[gi];
+        }
+        opt->n = n_new;
+    }
+    NX_CUDA(c, cudaStreamSynchronize(s));
+    std::swap(scene->geom, *geom_new);
+    geom_new->release();
+    sh2.release();
+    scene->n = n_new;
+    return NX_OK;
+}
+}  // namespace
+
+int nx_scene_prune(nx_ctx* c, nx_scene* scene, nx_optimizer* opt, double min_opacity, int32_t* new_to_old,
+                   int64_t* n_out) {
+    if (!c || !scene) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    if (opt && opt->n != scene->n) return set_err(c, NX_INVALID_ARGUMENT, "prune: optimizer and scene disagree");
+    cudaSetDevice(c->device);
+    cudaStream_t s = c->stream;
+    const int64_t n = scene->n, nn = std::max<int64_t>(n, 1);
+    NX_CUDA(c, c->flag.ensure(nn * sizeof(int32_t)));
+    NX_CUDA(c, c->pos.ensure(nn * sizeof(int32_t)));
+    NX_CUDA(c, c->scratch.ensure((scan_scratch_ints(nn) + 64) * sizeof(int32_t)));
+    int32_t* d_total = c->scratch.as<int32_t>();
+    launch_prune_flags(scene->geom.as<double>(), n, min_opacity, c->flag.as<int32_t>(), s);
+    scan_exclusive(c->flag.as<int32_t>(), c->pos.as<int32_t>(), n, d_total, d_total + 64, s);
+    int32_t kept = 0;
+    NX_CUDA(c, cudaMemcpyAsync(&kept, d_total, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    NX_CUDA(c, cudaStreamSynchronize(s));
+    if (n == 0) kept = 0;
+    DevBuf map;
+    NX_CUDA(c, map.ensure(std::max<int64_t>(kept, 1) * sizeof(int32_t)));
+    launch_compact_map(c->flag.as<int32_t>(), c->pos.as<int32_t>(), n, map.as<int32_t>(), s);
+    int st = apply_row_map(c, scene, opt, kept, map.as<int32_t>(), nullptr, false, s);
+    if (st) return st;
+    if (new_to_old && kept)
+        NX_CUDA(c, cudaMemcpyAsync(new_to_old, map.p, kept * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    NX_CUDA(c, cudaStreamSynchronize(s));
+    map.release();
+    if (n_out) *n_out = kept;
+    return NX_OK;
+}
+
+int nx_scene_densify_split(nx_ctx* c, nx_scene* scene, nx_optimizer* opt, const double* errors,
+                           const double* uniforms, int64_t budget, double split_fraction, int32_t* new_to_old,
+                           int64_t* n_out, int64_t* split_count) {
+    if (!c || !scene || !errors || !uniforms) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    if (opt && opt->n != scene->n) return set_err(c, NX_INVALID_ARGUMENT, "densify: optimizer and scene disagree");
+    cudaSetDevice(c->device);
+    cudaStream_t s = c->stream;
+    const int64_t n = scene->n;
+    if (split_count) *split_count = 0;
+    if (n_out) *n_out = n;
+    int64_t allowed = std::min<int64_t>(static_cast<int64_t>(std::ceil(split_fraction * static_cast<double>(n))),
+                                        budget - n);  // density.cpp:109
+    auto identity = [&]() -> int {
+        if (new_to_old && n) {
+            std::vector<int32_t> id(static_cast<size_t>(n));
+            for (int64_t i = 0; i < n; ++i) id[i] = static_cast<int32_t>(i);
+            NX_CUDA(c, cudaMemcpy(new_to_old, id.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
+        }
+        return NX_OK;
+    };
+    if (n == 0 || allowed <= 0) return identity();
+    const int64_t nn = std::max<int64_t>(n, 1);
+    NX_CUDA(c, c->skeys_a.ensure(nn * sizeof(uint64_t)));
+    NX_CUDA(c, c->skeys_b.ensure(nn * sizeof(uint64_t)));
+    NX_CUDA(c, c->sids_a.ensure(nn * sizeof(uint32_t)));
+    NX_CUDA(c, c->sids_b.ensure(nn * sizeof(uint32_t)));
+    NX_CUDA(c, c->scratch.ensure((radix_scratch_ints(nn) + 64) * sizeof(int32_t)));
+    unsigned long long* d_count = reinterpret_cast<unsigned long long*>(c->scratch.as<int32_t>());
+    NX_CUDA(c, cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s));
+    launch_split_keys(errors, uniforms, n, c->skeys_a.as<uint64_t>(), c->sids_a.as<uint32_t>(), d_count, s);
+    const bool in_b = radix_sort_pairs_u64(c->skeys_a.as<uint64_t>(), c->sids_a.as<uint32_t>(),
+                                           c->skeys_b.as<uint64_t>(), c->sids_b.as<uint32_t>(), n, nullptr, 0, 64,
+                                           c->scratch.as<int32_t>() + 64, s);
+    unsigned long long n_keys = 0;
+    NX_CUDA(c, cudaMemcpyAsync(&n_keys, d_count, sizeof n_keys, cudaMemcpyDeviceToHost, s));
+    NX_CUDA(c, cudaStreamSynchronize(s));
+    allowed = std::min<int64_t>(allowed, static_cast<int64_t>(n_keys));
+    if (allowed <= 0) return identity();
+    std::vector<int32_t> parents(static_cast<size_t>(allowed));
+    NX_CUDA(c, cudaMemcpy(parents.data(), in_b ? c->sids_b.p : c->sids_a.p, allowed * sizeof(int32_t),
+                          cudaMemcpyDeviceToHost));
+    std::sort(parents.begin(), parents.end());  // density.cpp:132-134
+    const int64_t n_new = n + allowed;
+    DevBuf d_par, map, g2, sh2;
+    NX_CUDA(c, d_par.ensure(allowed * sizeof(int32_t)));
+    NX_CUDA(c, cudaMemcpy(d_par.p, parents.data(), allowed * sizeof(int32_t), cudaMemcpyHostToDevice));
+    NX_CUDA(c, map.ensure(n_new * sizeof(int32_t)));
+    NX_CUDA(c, g2.ensure(n_new * kGeomFields * sizeof(double)));
+    NX_CUDA(c, sh2.ensure(n_new * NX_SH_VALUES * sizeof(float)));
+    NX_CUDA(c, cudaMemcpyAsync(sh2.p, scene->sh.p, n * NX_SH_VALUES * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    launch_split_children(g2.as<double>(), n_new, scene->geom.as<double>(), n, sh2.as<float>(), d_par.as<int32_t>(),
+                          allowed, map.as<int32_t>(), s);
+    std::swap(scene->sh, sh2);
+    int st = apply_row_map(c, scene, opt, n_new, map.as<int32_t>(), &g2, true, s);
+    if (st) return st;
+    if (new_to_old)
+        NX_CUDA(c, cudaMemcpyAsync(new_to_old, map.p, n_new * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    NX_CUDA(c, cudaStreamSynchronize(s));
+    sh2.release();
+    map.release();
+    d_par.release();
+    if (n_out) *n_out = n_new;
+    if (split_count) *split_count = allowed;
+    return NX_OK;
+}
+
 int nx_scene_download(nx_ctx* c, const nx_scene* scene, double* nexels, double* table, double* w1, double* w2,
                       double* w3) {
     if (!c || !scene) return set_err(c, NX_INVALID_ARGUMENT, "null argument");

@@ -240,6 +240,18 @@ void launch_adam_group(int group, const SceneDev& sc, double* geom, float* sh, f
                        float* w3, const nx_grads& g, double* m, double* v, const nx_adam_config& cfg, int64_t step,
                        cudaStream_t s);
 
+// ---------------------------------------------------------------- density control (nx_density.cu)
+void launch_prune_flags(const double* geom, int64_t n, double min_opacity, int32_t* flags, cudaStream_t s);
+void launch_compact_map(const int32_t* flags, const int32_t* pos, int64_t n, int32_t* n2o, cudaStream_t s);
+void launch_gather_geom(const double* geom, int64_t n, double* out, int64_t n_new, const int32_t* n2o, cudaStream_t s);
+void launch_gather_rows_f32(const float* in, float* out, int64_t n_new, int width, const int32_t* n2o, cudaStream_t s);
+void launch_gather_rows_f64(const double* in, double* out, int64_t n_new, int width, const int32_t* n2o,
+                            cudaStream_t s);
+void launch_split_keys(const double* errors, const double* uniforms, int64_t n, uint64_t* keys, uint32_t* ids,
+                       unsigned long long* n_keys, cudaStream_t s);
+void launch_split_children(double* geom_new, int64_t n_new, const double* geom_old, int64_t n, float* sh,
+                           const int32_t* parents, int64_t count, int32_t* n2o, cudaStream_t s);
+
 // ---------------------------------------------------------------- downloads
 struct CopyJob {
     const uint8_t* src;  // device
