@@ -33,7 +33,7 @@ namespace {
 
 constexpr int kThreads = kBwdTile * kBwdTile;  // 256: one thread per pixel of the 16x16 work tile
 constexpr int kWarps = kThreads / 32;           // 8 warps of 8x4 pixels
-constexpr int kChunk = 64;                      // primitives staged (and accumulated) per round
+constexpr int kChunk = 128;                     // primitives staged (and accumulated) per round
 constexpr int kSub = 2;                         // primitives pooled per B1/B2/B3 round
 constexpr int kPool = 32 * kSub;
 constexpr int kRecPairs = REC_FIELDS / 2;
@@ -55,7 +55,7 @@ union BwdEntry {
     BwdHit h;
     float g[kStage + 1];
 };
-constexpr uint16_t kComposited = 0x40;  // q entry flag set by B2 (list index j < kChunk = 64)
+constexpr uint16_t kComposited = 0x80;  // q entry flag set by B2 (list index j < kChunk = 128)
 
 struct SmemLayout {
     float4 f[kChunk][4];
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 2) composite_bwd_kernel(const Compos
                 // ---- B1. exact fp64 intersect of the pooled pairs (intersect.hpp:23-42)
                 for (int e = lane; e < total; e += 32) {
                     const int ent = sm.q[warp][e];
-                    const int owner = ent >> 8, j = ent & 0x3f;
+                    const int owner = ent >> 8, j = ent & 0x7f;
                     const double* dd = sm.dir[warp * 32 + owner];
                     const double d0 = dd[0], d1 = dd[1], d2 = dd[2];
                     const int32_t id = sm.id[j];
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 2) composite_bwd_kernel(const Compos
                 for (int k = off; k < off + cnt && active; ++k) {
                     BwdHit& res = sm.res[warp][k].h;
                     if (res.alpha < 0.0) continue;
-                    const int32_t id = sm.id[sm.q[warp][k] & 0x3f];
+                    const int32_t id = sm.id[sm.q[warp][k] & 0x7f];
                     const bool clamped = res.alpha > alpha_max;
                     const double alpha = clamped ? alpha_max : res.alpha;
                     const double w = alpha * T;
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 2) composite_bwd_kernel(const Compos
                     const BwdHit hh = sm.res[warp][e].h;
                     const double* dd = sm.dir[warp * 32 + (ent >> 8)];
                     const double d3[3] = {dd[0], dd[1], dd[2]};
-                    const int32_t id = sm.id[ent & 0x3f];
+                    const int32_t id = sm.id[ent & 0x7f];
                     double r[REC_FIELDS];
 #pragma unroll
                     for (int q = 0; q < kRecPairs; ++q) {
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 2) composite_bwd_kernel(const Compos
 #pragma unroll 1
                 for (int b = 0; b < sn; ++b) {
                     int my_e = -1;
-                    if (cur < off + cnt && (sm.q[warp][cur] & 0x3f) == sb + b) {
+                    if (cur < off + cnt && (sm.q[warp][cur] & 0x7f) == sb + b) {
                         if (sm.q[warp][cur] & kComposited) my_e = cur;
                         ++cur;
                     }
