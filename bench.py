@@ -248,21 +248,29 @@ def run_reference_arm(args):
         rows = max(16, rows // 16 * 16)
     for _ in range(args.warmup):
         impl.render(scene, band(y0, rows))
+    # the binning (build_binning over every primitive) is paid once per frame, not per
+    # band: frame time = binning + (band - binning) * H / rows
+    t_bin = 0.0
+    if kind == "reference":
+        t0 = time.perf_counter()
+        impl.tile_lists(scene, cam)
+        t_bin = time.perf_counter() - t0
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
         impl.render(scene, band(y0, rows))
         times.append(time.perf_counter() - t0)
-    total = sum(times)
-    fps = (args.steps * rows / H) / total
+    frame_s = [t_bin + max(t - t_bin, 0.0) * H / rows for t in times]
+    total = sum(frame_s)
+    fps = args.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload(args),
         "cpu_baseline": {"value": fps, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": f"each step renders rows {y0}-{y0 + rows} of {H} of view 0 "
-                                   f"(frame-equivalent = rows/H per step, binning included per step)"},
+                         "sample": f"each step renders rows {y0}-{y0 + rows} of {H} of view 0; frame time = "
+                                   f"binning {t_bin:.2f}s + (step - binning) x {H}/{rows}"},
         "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
