@@ -88,6 +88,7 @@ struct nx_ctx {
     DevBuf d_t_slot, act_grad;
     DevBuf h_up[3], h_err, h_blend, h_grads[5];  // device copies for nx_render_backward_host
     DevBuf loss_scratch, h_gt, h_terms;          // losses_backward
+    FieldBwdScratch field_bwd;                    // tensor-core field backward
     int32_t* h_pinned = nullptr;  // small readbacks
     bool profiling = false;
     cudaStream_t stream2 = nullptr;  // texture passes: overlap the next frame's collection
@@ -544,6 +545,7 @@ void nx_ctx_destroy(nx_ctx* c) {
         b->release();
     for (DevBuf* b : {&c->d_t_slot, &c->act_grad, &c->h_err, &c->h_blend, &c->loss_scratch, &c->h_gt, &c->h_terms})
         b->release();
+    c->field_bwd.release();
     for (DevBuf& b : c->h_up) b.release();
     for (DevBuf& b : c->h_grads) b.release();
     if (c->bwd_lists) nx_frame_destroy(c->bwd_lists);
@@ -1012,6 +1014,7 @@ int nx_render_backward(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, n
             fa.g_w1 = g->w1;
             fa.g_w2 = g->w2;
             fa.g_w3 = g->w3;
+            fa.scratch = &c->field_bwd;
             if ((st = launch_field_backward(fa, s)))
                 return set_err(c, st, "texture field shape not supported by render_backward");
         } else {

@@ -726,17 +726,6 @@ __global__ void merge_table_kernel(double* __restrict__ g_table, float* __restri
     }
 }
 
-struct Scratch {
-    float* fbuf = nullptr;
-    size_t fcap = 0;
-    int32_t* amb = nullptr;  // [0] count, [1..] listed slots
-    size_t acap = 0;
-    float* tg32 = nullptr;   // fp32 table gradients of the per-lane scatters (kept zeroed)
-    size_t tcap = 0;
-    float* parts = nullptr;
-    size_t pcap = 0;
-};
-Scratch g_scratch[64];  // per device
 
 }  // namespace
 
@@ -750,7 +739,7 @@ int launch_field_backward_tc(const FieldBwdArgs& a, cudaStream_t s) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    Scratch& sc = g_scratch[dev & 63];
+    FieldBwdScratch& sc = *a.scratch;
     const size_t fneed = static_cast<size_t>(total) * kStride;
     const int64_t n_tiles = (total + kRows - 1) / kRows;
     const int grid_m = static_cast<int>(std::min<int64_t>(n_tiles, sms));

@@ -271,6 +271,25 @@ void launch_stream_copy(const CopyJobs& jobs, cudaStream_t s);
 // columns v1, v2, n), d_sigma[2], d_opacity, d_gamma[2], blended error.
 constexpr int kActFields = 18;
 
+// Device scratch of the tensor-core field backward, owned by the context (grow-only;
+// the fp32 table-gradient copy is kept zeroed between calls).
+struct FieldBwdScratch {
+    float* fbuf = nullptr;
+    size_t fcap = 0;
+    int32_t* amb = nullptr;
+    size_t acap = 0;
+    float* tg32 = nullptr;
+    size_t tcap = 0;
+    float* parts = nullptr;
+    size_t pcap = 0;
+    void release() {
+        for (void* p : {static_cast<void*>(fbuf), static_cast<void*>(amb), static_cast<void*>(tg32),
+                        static_cast<void*>(parts)})
+            if (p) cudaFree(p);
+        *this = FieldBwdScratch{};
+    }
+};
+
 struct FieldBwdArgs {
     SceneDev scene;
     nx_settings st;
@@ -283,6 +302,7 @@ struct FieldBwdArgs {
     double* g_w1;
     double* g_w2;
     double* g_w3;
+    FieldBwdScratch* scratch;  // the context's
 };
 // field_backward_batch (texture_field.cpp:77-146) over the buffered slots.
 int launch_field_backward(const FieldBwdArgs& a, cudaStream_t s);
