@@ -516,9 +516,13 @@ def run_ours(args):
     fbytes = frame_bytes(args.nexels, P, H, W, K, Q)
     frame_gbs = fbytes * (args.steps / (ms_local / 1e3)) / 1e9
 
-    train = train_step_timing(args, r, ds, scene, cams[views[args.warmup]] if len(views) > args.warmup else
-                              nx.ring_camera(0, N_VIEWS, args.width, args.height), stream, dist, local) \
-        if args.train_steps > 0 else None
+    train = None
+    if args.train_steps > 0:  # reported beside the headline; a failure here never voids it
+        try:
+            train = train_step_timing(args, r, ds, scene, cams[views[args.warmup]] if len(views) > args.warmup else
+                                      nx.ring_camera(0, N_VIEWS, args.width, args.height), stream, dist, local)
+        except Exception as e:  # noqa: BLE001
+            train = {"error": f"{type(e).__name__}: {e}"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
