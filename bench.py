@@ -375,17 +375,77 @@ def train_step_timing(args, r, ds, scene, cam, stream, dist, local):
     step_ms = max_over_ranks(dist, e1.elapsed_time(e2) / args.train_steps, f"cuda:{local}")
     t = terms.cpu().tolist()
     finite = bool(torch.isfinite(grads[0]).all().item() and torch.isfinite(grads[1]).all().item())
+    st = fr.stats()
     fr.close()
     r.lib.nx_optimizer_destroy(opt)
+    # backward roofline: read the frame (76 HW) and the upstream
+    # gradients ((12 + 16K) HW), write the primitive gradients (240 N), read-modify-write the
+    # grid gradients (2 x 1024 Q), read the tile lists (4 P)
+    n = scene.nexels.shape[0]
+    bwd_bytes = 76 * npix + (12 + 16 * K) * npix + 240 * n + 2048 * st["n_queries"] + 4 * st["tile_keys"]
+    bwd_ms = step_ms - fwd_ms
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    cpu = None
+    if dist is None and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_backward_sample(scene, cam)
+        except Exception as e:  # noqa: BLE001 — reported, never required
+            cpu = {"value": None, "sample": f"failed: {e}"}
     return {"config": "configs[4]: 400K nexels 1080p forward + backward (surfel / texture gradients)",
             "ms_per_step": step_ms, "steps_per_s": 1e3 / step_ms, "forward_ms": fwd_ms,
             "losses_and_backward_ms": step_ms - fwd_ms, "steps": args.train_steps, "view": cam.name,
             "loss_total": t[7], "grads_finite": finite,
+            "roofline": {"bound": "hbm", "kernel": "losses + render_backward + Adam (whole backward half)",
+                         "achieved": bwd_bytes / (bwd_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": bwd_bytes / (bwd_ms / 1e3) / 1e9 / hbm_peak, "bytes": bwd_bytes,
+                         "formula": "76HW + (12+16K)HW + 240N + 2048Q + 4P"},
+            "cpu_baseline": cpu,
             "path": "zero SceneGrads + nx_render + nx_losses_backward (gt = grid_init 1e-1 render) + err_pixel + "
                     "nx_render_backward + [NCCL all-reduce of the gradients, N > 1] + nx_optimizer_step (Adam, 11 "
                     "groups); no density control",
             "reference_s": "render ~55 s + render_backward 101 s per step at config 2 on 8 cores (SURVEY.md §6, "
-                           "§8(f)); not re-timed here"}
+                           "§8(f)); cpu_baseline re-times the reference's render_backward on this box"}
+
+
+def cpu_reference_backward_sample(scene, cam, rows: int = 64):
+    """The reference's render_backward (oracle/_ref) on all host cores over a band of
+    rows of the view. Both band calls pay one full binning (build_binning visits every
+    primitive whatever the band), so (render + backward) - render is the band's backward
+    compute alone; render_backward re-bins once per frame, so
+    per frame = binning + band backward x H / rows."""
+    import numpy as np
+    from oracle.pyoracle import Reference
+    import paper_2512_13796_b200 as nx
+    ref = Reference()
+    cores = os.cpu_count() or 1
+    os.environ["NEXEL_THREADS"] = str(cores)
+    H = cam.height
+    y0 = (H // 2 // 16) * 16
+    band = nx.Camera(cam.width, rows, cam.fx, cam.fy, cam.cx, cam.cy - y0, cam.R, cam.t)
+    K = scene.settings.top_k
+    npix = cam.width * rows
+    g = np.random.default_rng(0)
+    up = [g.standard_normal(npix * 3), g.standard_normal(npix * K), g.standard_normal(npix * K * 3)]
+    t0 = time.perf_counter()
+    ref.tile_lists(scene, cam)
+    t_bin = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ref.render(scene, band)
+    t_fwd = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ref.render_backward(scene, band, *up)
+    t_both = time.perf_counter() - t0
+    t_band = max(t_both - t_fwd, 1e-3)
+    frame_s = t_bin + t_band * H / rows
+    return {"value": 1.0 / frame_s, "unit": "backward passes/s", "cores": cores, "kind": "reference",
+            "sample": f"render_backward of rows {y0}-{y0 + rows} of {H}: band {t_band:.2f}s (render+backward "
+                      f"{t_both:.2f}s - render {t_fwd:.2f}s), per frame = binning {t_bin:.2f}s + band x {H}/{rows}", "frame_seconds": frame_s}
 
 
 def _device_view(ptr, n, dtype, dev):

@@ -49,6 +49,13 @@ struct DevBuf {
         if (e == cudaSuccess) cap = want;
         return e;
     }
+    // for exact accumulators (nx_xacc.cuh): a fresh allocation is zeroed; readers keep it zero
+    cudaError_t ensure_zeroed(size_t bytes, cudaStream_t s) {
+        if (bytes <= cap && p) return cudaSuccess;
+        cudaError_t e = ensure(bytes);
+        if (e == cudaSuccess) e = cudaMemsetAsync(p, 0, cap, s);
+        return e;
+    }
     void release() {
         if (p) cudaFree(p);
         p = nullptr;
@@ -85,7 +92,7 @@ struct nx_ctx {
     DevBuf dbg_hits, dbg_counts;
     // render_backward scratch
     nx_frame* bwd_lists = nullptr;   // work lists of the re-binned camera
-    DevBuf d_t_slot, act_grad;
+    DevBuf d_t_slot, act_grad, xacc_prims;
     DevBuf h_up[3], h_err, h_blend, h_grads[5];  // device copies for nx_render_backward_host
     DevBuf loss_scratch, h_gt, h_terms;          // losses_backward
     FieldBwdScratch field_bwd;                    // tensor-core field backward
@@ -543,7 +550,7 @@ void nx_ctx_destroy(nx_ctx* c) {
                       &c->skeys_b, &c->sids_a, &c->sids_b, &c->counts, &c->offsets, &c->tkeys_a, &c->tkeys_b,
                       &c->tvals_a, &c->tvals_b, &c->tile_counts, &c->scratch, &c->dbg_hits, &c->dbg_counts})
         b->release();
-    for (DevBuf* b : {&c->d_t_slot, &c->act_grad, &c->h_err, &c->h_blend, &c->loss_scratch, &c->h_gt, &c->h_terms})
+    for (DevBuf* b : {&c->d_t_slot, &c->act_grad, &c->xacc_prims, &c->h_err, &c->h_blend, &c->loss_scratch, &c->h_gt, &c->h_terms})
         b->release();
     c->field_bwd.release();
     for (DevBuf& b : c->h_up) b.release();
@@ -995,7 +1002,9 @@ int nx_render_backward(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, n
     const int64_t n = scene->n, npix = static_cast<int64_t>(f->W) * f->H, ns = npix * f->K;
     NX_CUDA(c, c->d_t_slot.ensure(std::max<int64_t>(ns, 1) * sizeof(double)));
     NX_CUDA(c, c->act_grad.ensure(std::max<int64_t>(n, 1) * kActFields * sizeof(double)));
-    NX_CUDA(c, cudaMemsetAsync(c->act_grad.p, 0, std::max<int64_t>(n, 1) * kActFields * sizeof(double), s));
+    const Xacc pacc{nullptr, std::max<int64_t>(n, 1) * kPrimAccVals};
+    NX_CUDA(c, c->xacc_prims.ensure_zeroed(xacc_bytes(pacc.m), s));
+    const Xacc prim_acc{c->xacc_prims.as<unsigned long long>(), pacc.m};
     FrameDev fd = frame_dev(f);
     fd.tiles_x = lf->ltiles_x;
     fd.tiles_y = lf->ltiles_y;
@@ -1036,10 +1045,9 @@ int nx_render_backward(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, n
     ca.d_weights = f->K > 0 ? up->d_weights : nullptr;
     ca.d_t_slot = c->d_t_slot.as<double>();
     ca.err_pixel = blended_error ? err_pixel : nullptr;
-    ca.act_grad = c->act_grad.as<double>();
-    ca.prim_grad = g->prims;
+    ca.acc = prim_acc;
     launch_composite_backward(ca, s);
-    launch_prim_finalize(scene_dev(scene), scene->st.no_gamma, c->act_grad.as<double>(), g->prims,
+    launch_prim_finalize(scene_dev(scene), scene->st.no_gamma, prim_acc, c->act_grad.as<double>(), g->prims,
                          err_pixel ? blended_error : nullptr, s);
     NX_CUDA(c, cudaEventRecord(f->ev_busy, s));
     f->busy_pending = true;

@@ -16,16 +16,21 @@
 // 40-68), intersect_backward (intersect.hpp:56-87); SH gradients (eval_sh_backward,
 // sh.hpp:76-83) are formed in fp32 and accumulated in fp64.
 //
-// Per group of primitives a warp (8x4 pixels) pools its survivors like the
-// forward (B1: exact fp64 intersect, all lanes busy), composites them per pixel
-// in list order (B2: weights, d_alpha, d_t), then reduces each primitive's
-// per-pixel gradients across the warp (B3: butterfly, or direct when at most two
-// lanes hit it) into per-primitive fp64 accumulators. Those hold the activated
-// gradient (17 values, ActivatedGrad intersect.hpp:45-51) + blended error; the
-// SH gradients go straight into the PrimitiveGrad array. activation_backward
+// Each warp (8x4 pixels of the 16x16 tile) walks the tile's list on its own — its
+// own 32-primitive staging, no CTA barriers, so a warp whose pixels terminate early
+// stops early. Per group of primitives it pools its survivors like the forward
+// (B1: exact fp64 intersect, all lanes busy), composites them per pixel in list
+// order (B2: weights, d_alpha, d_t), evaluates every composited pair's gradient (B3a)
+// and sums each primitive's per-pixel gradients across the warp in lane order (B3b).
+// Those warp sums — the activated gradient (17 values, ActivatedGrad intersect.hpp:
+// 45-51), the blended error and the 48 SH gradients — go into per-primitive exact
+// accumulators (nx_xacc.cuh), so the result does not depend on the order in which
+// warps and tiles meet: render_backward is bit-reproducible, as the reference's is.
+// A per-value kernel then reads the accumulators back; activation_backward
 // (intersect.hpp:91-103) is linear in the activated gradient, so a final
 // per-primitive kernel applies it once to the sum.
 #include "nx_composite.cuh"
+#include "nx_xacc.cuh"
 
 namespace nx {
 
@@ -33,11 +38,10 @@ namespace {
 
 constexpr int kThreads = kBwdTile * kBwdTile;  // 256: one thread per pixel of the 16x16 work tile
 constexpr int kWarps = kThreads / 32;           // 8 warps of 8x4 pixels
-constexpr int kChunk = 128;                     // primitives staged (and accumulated) per round
+constexpr int kChunk = 32;                      // primitives staged per warp round
 constexpr int kSub = 2;                         // primitives pooled per B1/B2/B3 round
 constexpr int kPool = 32 * kSub;
 constexpr int kRecPairs = REC_FIELDS / 2;
-constexpr int kAccStride = 68;                  // fp32 accumulator row: 18 activated + 48 SH (+2 pad)
 static_assert(kBwdTile == 16, "warp blocks are 8x4 pixels, two across a 16-pixel row");
 
 constexpr int kStage = kActFields + 3;          // per-hit staged values: activated grads, werr, w dL/dfinal
@@ -55,16 +59,18 @@ union BwdEntry {
     BwdHit h;
     float g[kStage + 1];
 };
-constexpr uint16_t kComposited = 0x80;  // q entry flag set by B2 (list index j < kChunk = 128)
+constexpr uint16_t kComposited = 0x80;  // q entry flag set by B2 (list index j < kChunk)
 
-struct SmemLayout {
+struct WarpSmem {        // one warp's private staging (no sharing between warps)
     float4 f[kChunk][4];
+    double dir[32][3];
+    float basis[32][16];  // per-pixel SH basis (fp32)
+    BwdEntry res[kPool];
     int32_t id[kChunk];
-    double dir[kThreads][3];
-    uint16_t q[kWarps][kPool];
-    BwdEntry res[kWarps][kPool];
-    float basis[kThreads][16];      // per-pixel SH basis (fp32)
-    float acc[kChunk][kAccStride];  // per-primitive gradient sums of the tile (flushed per chunk)
+    uint16_t q[kPool];
+};
+struct SmemLayout {
+    WarpSmem w[kWarps];
 };
 
 // eval_kernel_grad (kernel.hpp:40-68) + intersect_backward (intersect.hpp:56-87):
@@ -121,13 +127,13 @@ template <int K>
 __global__ void __launch_bounds__(kThreads, 2) composite_bwd_kernel(const CompositeBwdArgs a) {
     constexpr int KK = K > 0 ? K : 1;
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    SmemLayout& sm = *reinterpret_cast<SmemLayout*>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WarpSmem& sm = reinterpret_cast<SmemLayout*>(smem_raw)->w[warp];
 
     const int t = blockIdx.x;
     const int tx = t % a.fb.tiles_x, ty = t / a.fb.tiles_x;
     const int list_begin = a.tile_offsets[t], list_end = a.tile_offsets[t + 1];
     const int W = a.cam.W, H = a.cam.H;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double near_eps = a.st.near_eps, alpha_max = a.st.alpha_max, min_T = a.st.min_transmittance;
     const float near_eps_f = static_cast<float>(near_eps);
     const double o[3] = {a.cam.o[0], a.cam.o[1], a.cam.o[2]};
@@ -141,12 +147,11 @@ __global__ void __launch_bounds__(kThreads, 2) composite_bwd_kernel(const Compos
     const int wy1 = __reduce_max_sync(0xffffffffu, in_img ? py : -1);
     double dir[3] = {0.0, 0.0, 1.0};
     if (in_img) pixel_dir(a.cam, px + 0.5, py + 0.5, dir);
-    sm.dir[threadIdx.x][0] = dir[0];
-    sm.dir[threadIdx.x][1] = dir[1];
-    sm.dir[threadIdx.x][2] = dir[2];
+    sm.dir[lane][0] = dir[0];
+    sm.dir[lane][1] = dir[1];
+    sm.dir[lane][2] = dir[2];
     const float dfx = static_cast<float>(dir[0]), dfy = static_cast<float>(dir[1]), dfz = static_cast<float>(dir[2]);
-    sh_basis_f32(dfx, dfy, dfz, sm.basis[threadIdx.x]);
-    for (int e = threadIdx.x; e < kChunk * kAccStride; e += kThreads) (&sm.acc[0][0])[e] = 0.f;
+    sh_basis_f32(dfx, dfy, dfz, sm.basis[lane]);
 
     // per-pixel upstream state
     const int64_t pix = in_img ? static_cast<int64_t>(py) * W + px : 0;
@@ -183,226 +188,214 @@ __global__ void __launch_bounds__(kThreads, 2) composite_bwd_kernel(const Compos
     const double errp = (in_img && a.err_pixel) ? a.err_pixel[pix] : 0.0;
     const int n_act = a.err_pixel ? kActFields : kActFields - 1;
     const int n_sh = a.sh_degree >= 3 ? 16 : 1;
-    const int n_vals = kActFields + 3 * n_sh;  // accumulator columns in use
+    const int n_vals = kActFields + 3 * n_sh;  // accumulated values in use
+    const Xacc acc = a.acc;
 
     double T = 1.0, P = 0.0;
     bool active = in_img;
     const double2* rec2 = reinterpret_cast<const double2*>(a.rec);
 
     for (int cb = list_begin; cb < list_end; cb += kChunk) {
+        if (!__any_sync(0xffffffffu, active)) break;
         const int cn = min(kChunk, list_end - cb);
-        __syncthreads();
-        for (int e = threadIdx.x; e < cn * 4; e += kThreads) {
-            const int j = e >> 2, q = e & 3;
-            const int32_t id = __ldg(a.list_ids + cb + j);
-            sm.f[j][q] = __ldg(a.recf + static_cast<int64_t>(id) * 4 + q);
-            if (q == 0) sm.id[j] = id;
+        __syncwarp();
+        if (lane < cn) {
+            const int32_t id = __ldg(a.list_ids + cb + lane);
+            sm.id[lane] = id;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) sm.f[lane][q] = __ldg(a.recf + static_cast<int64_t>(id) * 4 + q);
         }
-        __syncthreads();
-        if (__any_sync(0xffffffffu, active)) {
-            for (int sb = 0; sb < cn; sb += kSub) {
-                const int sn = min(kSub, cn - sb);
-                // ---- A. screen-space cull + fp32 prefilter (as the forward)
-                uint32_t mask = 0;
+        __syncwarp();
+        for (int sb = 0; sb < cn; sb += kSub) {
+            const int sn = min(kSub, cn - sb);
+            // ---- A. screen-space cull + fp32 prefilter (as the forward)
+            uint32_t mask = 0;
 #pragma unroll
-                for (int b = 0; b < kSub; ++b) {
-                    if (b >= sn) break;
-                    const float4 f3 = sm.f[sb + b][3];
-                    const int rx = __float_as_int(f3.z), ry = __float_as_int(f3.w);
-                    const int x0 = rx & 0xffff, x1 = rx >> 16, y0 = ry & 0xffff, y1 = ry >> 16;
-                    if (x1 < wx0 || x0 > wx1 || y1 < wy0 || y0 > wy1) continue;
-                    if (active && px >= x0 && px <= x1 && py >= y0 && py <= y1 &&
-                        prefilter(&sm.f[sb + b][0], dfx, dfy, dfz, near_eps_f))
-                        mask |= 1u << b;
-                }
-                const int cnt = __popc(mask);
-                int incl = cnt;
+            for (int b = 0; b < kSub; ++b) {
+                if (b >= sn) break;
+                const float4 f3 = sm.f[sb + b][3];
+                const int rx = __float_as_int(f3.z), ry = __float_as_int(f3.w);
+                const int x0 = rx & 0xffff, x1 = rx >> 16, y0 = ry & 0xffff, y1 = ry >> 16;
+                if (x1 < wx0 || x0 > wx1 || y1 < wy0 || y0 > wy1) continue;
+                if (active && px >= x0 && px <= x1 && py >= y0 && py <= y1 &&
+                    prefilter(&sm.f[sb + b][0], dfx, dfy, dfz, near_eps_f))
+                    mask |= 1u << b;
+            }
+            const int cnt = __popc(mask);
+            int incl = cnt;
 #pragma unroll
-                for (int of = 1; of < 32; of <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, incl, of);
-                    if (lane >= of) incl += y;
+            for (int of = 1; of < 32; of <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, of);
+                if (lane >= of) incl += y;
+            }
+            const int off = incl - cnt;
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            if (total == 0) continue;
+            {
+                uint32_t m = mask;
+                int k = off;
+                while (m) {
+                    const int b = __ffs(m) - 1;
+                    m &= m - 1;
+                    sm.q[k++] = static_cast<uint16_t>((lane << 8) | (sb + b));
                 }
-                const int off = incl - cnt;
-                const int total = __shfl_sync(0xffffffffu, incl, 31);
-                if (total == 0) continue;
-                {
-                    uint32_t m = mask;
-                    int k = off;
-                    while (m) {
-                        const int b = __ffs(m) - 1;
-                        m &= m - 1;
-                        sm.q[warp][k++] = static_cast<uint16_t>((lane << 8) | (sb + b));
-                    }
-                }
-                __syncwarp();
-                // ---- B1. exact fp64 intersect of the pooled pairs (intersect.hpp:23-42)
-                for (int e = lane; e < total; e += 32) {
-                    const int ent = sm.q[warp][e];
-                    const int owner = ent >> 8, j = ent & 0x7f;
-                    const double* dd = sm.dir[warp * 32 + owner];
-                    const double d0 = dd[0], d1 = dd[1], d2 = dd[2];
-                    const int32_t id = sm.id[j];
-                    double r[REC_FIELDS];
+            }
+            __syncwarp();
+            // ---- B1. exact fp64 intersect of the pooled pairs (intersect.hpp:23-42)
+            for (int e = lane; e < total; e += 32) {
+                const int ent = sm.q[e];
+                const int owner = ent >> 8, j = ent & 0x7f;
+                const double d0 = sm.dir[owner][0], d1 = sm.dir[owner][1], d2 = sm.dir[owner][2];
+                const int32_t id = sm.id[j];
+                double r[REC_FIELDS];
 #pragma unroll
-                    for (int q = 0; q < kRecPairs; ++q) {
-                        const double2 v = __ldg(rec2 + static_cast<int64_t>(id) * kRecPairs + q);
-                        r[2 * q] = v.x;
-                        r[2 * q + 1] = v.y;
-                    }
-                    BwdHit res;
-                    res.alpha = -1.0;
-                    res.t = 0.0;
-                    res.flags = 0;
-                    const double denom = d0 * r[REC_NX] + d1 * r[REC_NY] + d2 * r[REC_NZ];
-                    if (fabs(denom) >= kMinNormalDot) {
-                        const double tt = r[REC_NUM] / denom;
-                        if (tt > near_eps) {
-                            const double e0 = (o[0] + tt * d0) - r[REC_MUX];
-                            const double e1 = (o[1] + tt * d1) - r[REC_MUY];
-                            const double e2 = (o[2] + tt * d2) - r[REC_MUZ];
-                            const double du = e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z];
-                            const double dv = e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z];
-                            if (fabs(du) <= r[REC_ULIM] && fabs(dv) <= r[REC_VLIM]) {
-                                const double u = du / r[REC_SX];
-                                const double v = dv / r[REC_SY];
-                                const double al = eval_kernel(u, v, r[REC_OP], r[REC_GX], r[REC_GY]);
-                                if (al >= kAlphaMin) {
-                                    res.alpha = al;
-                                    res.t = tt;
-                                    uint32_t act;
-                                    eval_sh_f32(a.sh + static_cast<int64_t>(id) * NX_SH_VALUES, static_cast<float>(d0),
-                                                static_cast<float>(d1), static_cast<float>(d2), a.sh_degree, res.rgb,
-                                                &act);
-                                    res.flags = act;
-                                }
+                for (int q = 0; q < kRecPairs; ++q) {
+                    const double2 v = __ldg(rec2 + static_cast<int64_t>(id) * kRecPairs + q);
+                    r[2 * q] = v.x;
+                    r[2 * q + 1] = v.y;
+                }
+                BwdHit res;
+                res.alpha = -1.0;
+                res.t = 0.0;
+                res.flags = 0;
+                const double denom = d0 * r[REC_NX] + d1 * r[REC_NY] + d2 * r[REC_NZ];
+                if (fabs(denom) >= kMinNormalDot) {
+                    const double tt = r[REC_NUM] / denom;
+                    if (tt > near_eps) {
+                        const double e0 = (o[0] + tt * d0) - r[REC_MUX];
+                        const double e1 = (o[1] + tt * d1) - r[REC_MUY];
+                        const double e2 = (o[2] + tt * d2) - r[REC_MUZ];
+                        const double du = e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z];
+                        const double dv = e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z];
+                        if (fabs(du) <= r[REC_ULIM] && fabs(dv) <= r[REC_VLIM]) {
+                            const double u = du / r[REC_SX];
+                            const double v = dv / r[REC_SY];
+                            const double al = eval_kernel(u, v, r[REC_OP], r[REC_GX], r[REC_GY]);
+                            if (al >= kAlphaMin) {
+                                res.alpha = al;
+                                res.t = tt;
+                                uint32_t act;
+                                eval_sh_f32(a.sh + static_cast<int64_t>(id) * NX_SH_VALUES, static_cast<float>(d0),
+                                            static_cast<float>(d1), static_cast<float>(d2), a.sh_degree, res.rgb,
+                                            &act);
+                                res.flags = act;
                             }
                         }
                     }
-                    sm.res[warp][e].h = res;
                 }
-                __syncwarp();
-                // ---- B2. per-pixel march in list order: weights, d_alpha, d_t (renderer.cpp:325-370)
-                for (int k = off; k < off + cnt && active; ++k) {
-                    BwdHit& res = sm.res[warp][k].h;
-                    if (res.alpha < 0.0) continue;
-                    const int32_t id = sm.id[sm.q[warp][k] & 0x7f];
-                    const bool clamped = res.alpha > alpha_max;
-                    const double alpha = clamped ? alpha_max : res.alpha;
-                    const double w = alpha * T;
-                    int slot = -1;
+                sm.res[e].h = res;
+            }
+            __syncwarp();
+            // ---- B2. per-pixel march in list order: weights, d_alpha, d_t (renderer.cpp:325-370)
+            for (int k = off; k < off + cnt && active; ++k) {
+                BwdHit& res = sm.res[k].h;
+                if (res.alpha < 0.0) continue;
+                const int32_t id = sm.id[sm.q[k] & 0x7f];
+                const bool clamped = res.alpha > alpha_max;
+                const double alpha = clamped ? alpha_max : res.alpha;
+                const double w = alpha * T;
+                int slot = -1;
+#pragma unroll
+                for (int j = 0; j < KK; ++j)
+                    if (K > 0 && slot < 0 && k_id[j] == id) slot = j;
+                double dw = 0.0, d_t = 0.0;
+                float wdf[3] = {0.f, 0.f, 0.f};
+                if (slot >= 0) {
 #pragma unroll
                     for (int j = 0; j < KK; ++j)
-                        if (K > 0 && slot < 0 && k_id[j] == id) slot = j;
-                    double dw = 0.0, d_t = 0.0;
-                    float wdf[3] = {0.f, 0.f, 0.f};
-                    if (slot >= 0) {
-#pragma unroll
-                        for (int j = 0; j < KK; ++j)
-                            if (j == slot) {
-                                dw = k_dw[j];
-                                d_t = k_dt[j];
-                            }
-                    } else {
-                        dw = dfin[0] * res.rgb[0] + dfin[1] * res.rgb[1] + dfin[2] * res.rgb[2];
-#pragma unroll
-                        for (int c = 0; c < 3; ++c)
-                            wdf[c] = (res.flags >> c) & 1u ? static_cast<float>(w * dfin[c]) : 0.f;
-                    }
-                    const double A = A_total - P - dw * w;  // sum of dL/dw * w behind this hit
-                    double d_alpha = dw * T - A / (1.0 - alpha);
-                    if (clamped) d_alpha = 0.0;
-                    P += dw * w;
-                    res.alpha = d_alpha;
-                    res.d_t = d_t;
-                    res.werr = w * errp;
-                    res.rgb[0] = wdf[0];
-                    res.rgb[1] = wdf[1];
-                    res.rgb[2] = wdf[2];
-                    sm.q[warp][k] |= kComposited;
-                    T *= 1.0 - alpha;
-                    if (T < min_T) active = false;
-                }
-                __syncwarp();
-                // ---- B3a. gradients of every composited pair, all lanes busy: eval_kernel_grad +
-                // intersect_backward in fp64 -> staged as fp32 in the entry
-#pragma unroll 1
-                for (int e = lane; e < total; e += 32) {
-                    const int ent = sm.q[warp][e];
-                    if (!(ent & kComposited)) continue;
-                    const BwdHit hh = sm.res[warp][e].h;
-                    const double* dd = sm.dir[warp * 32 + (ent >> 8)];
-                    const double d3[3] = {dd[0], dd[1], dd[2]};
-                    const int32_t id = sm.id[ent & 0x7f];
-                    double r[REC_FIELDS];
-#pragma unroll
-                    for (int q = 0; q < kRecPairs; ++q) {
-                        const double2 v = __ldg(rec2 + static_cast<int64_t>(id) * kRecPairs + q);
-                        r[2 * q] = v.x;
-                        r[2 * q + 1] = v.y;
-                    }
-                    // the hit's plane coordinates, as intersect() formed them
-                    const double e0 = (o[0] + hh.t * d3[0]) - r[REC_MUX];
-                    const double e1 = (o[1] + hh.t * d3[1]) - r[REC_MUY];
-                    const double e2 = (o[2] + hh.t * d3[2]) - r[REC_MUZ];
-                    const double u = (e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z]) / r[REC_SX];
-                    const double v = (e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z]) / r[REC_SY];
-                    double gd[kActFields - 1];
-                    hit_backward(r, d3, o, hh.t, u, v, hh.alpha, hh.d_t, gd);
-                    float* g = sm.res[warp][e].g;
-#pragma unroll
-                    for (int i = 0; i < kActFields - 1; ++i) g[i] = static_cast<float>(gd[i]);
-                    g[kActFields - 1] = static_cast<float>(hh.werr);
-                    g[kActFields + 0] = hh.rgb[0];
-                    g[kActFields + 1] = hh.rgb[1];
-                    g[kActFields + 2] = hh.rgb[2];
-                }
-                __syncwarp();
-                // ---- B3b. per primitive of the group: lane v sums value v over the pixels that hit
-                // it (SH values from the staged w dL/dfinal and the pixel's basis) -> tile accumulator
-                int cur = off;
-#pragma unroll 1
-                for (int b = 0; b < sn; ++b) {
-                    int my_e = -1;
-                    if (cur < off + cnt && (sm.q[warp][cur] & 0x7f) == sb + b) {
-                        if (sm.q[warp][cur] & kComposited) my_e = cur;
-                        ++cur;
-                    }
-                    const uint32_t hm = __ballot_sync(0xffffffffu, my_e >= 0);
-                    if (!hm) continue;
-                    float* accr = sm.acc[sb + b];
-#pragma unroll 1
-                    for (int r0 = 0; r0 < n_vals; r0 += 32) {  // warp-uniform rounds (shuffles inside)
-                        const int v = r0 + lane;
-                        const bool is_act = v < kActFields;
-                        const int sv = is_act ? 0 : v - kActFields;
-                        const int shk = sv / 3, shc = sv - 3 * (sv / 3);
-                        float sum = 0.f;
-                        for (uint32_t m = hm; m; m &= m - 1) {
-                            const int h = __ffs(m) - 1;
-                            const int eh = __shfl_sync(0xffffffffu, my_e, h);
-                            if (v < n_vals) {
-                                const float* g = sm.res[warp][eh].g;
-                                sum += is_act ? g[v] : g[kActFields + shc] * sm.basis[warp * 32 + h][shk];
-                            }
+                        if (j == slot) {
+                            dw = k_dw[j];
+                            d_t = k_dt[j];
                         }
-                        if (v < n_vals && sum != 0.f && (!is_act || v < n_act)) atomicAdd(accr + v, sum);
-                    }
+                } else {
+                    dw = dfin[0] * res.rgb[0] + dfin[1] * res.rgb[1] + dfin[2] * res.rgb[2];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        wdf[c] = (res.flags >> c) & 1u ? static_cast<float>(w * dfin[c]) : 0.f;
                 }
-                __syncwarp();
+                const double A = A_total - P - dw * w;  // sum of dL/dw * w behind this hit
+                double d_alpha = dw * T - A / (1.0 - alpha);
+                if (clamped) d_alpha = 0.0;
+                P += dw * w;
+                res.alpha = d_alpha;
+                res.d_t = d_t;
+                res.werr = w * errp;
+                res.rgb[0] = wdf[0];
+                res.rgb[1] = wdf[1];
+                res.rgb[2] = wdf[2];
+                sm.q[k] |= kComposited;
+                T *= 1.0 - alpha;
+                if (T < min_T) active = false;
             }
+            __syncwarp();
+            // ---- B3a. gradients of every composited pair, all lanes busy: eval_kernel_grad +
+            // intersect_backward in fp64 -> staged as fp32 in the entry
+#pragma unroll 1
+            for (int e = lane; e < total; e += 32) {
+                const int ent = sm.q[e];
+                if (!(ent & kComposited)) continue;
+                const BwdHit hh = sm.res[e].h;
+                const int owner = ent >> 8;
+                const double d3[3] = {sm.dir[owner][0], sm.dir[owner][1], sm.dir[owner][2]};
+                const int32_t id = sm.id[ent & 0x7f];
+                double r[REC_FIELDS];
+#pragma unroll
+                for (int q = 0; q < kRecPairs; ++q) {
+                    const double2 v = __ldg(rec2 + static_cast<int64_t>(id) * kRecPairs + q);
+                    r[2 * q] = v.x;
+                    r[2 * q + 1] = v.y;
+                }
+                // the hit's plane coordinates, as intersect() formed them
+                const double e0 = (o[0] + hh.t * d3[0]) - r[REC_MUX];
+                const double e1 = (o[1] + hh.t * d3[1]) - r[REC_MUY];
+                const double e2 = (o[2] + hh.t * d3[2]) - r[REC_MUZ];
+                const double u = (e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z]) / r[REC_SX];
+                const double v = (e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z]) / r[REC_SY];
+                double gd[kActFields - 1];
+                hit_backward(r, d3, o, hh.t, u, v, hh.alpha, hh.d_t, gd);
+                float* g = sm.res[e].g;
+#pragma unroll
+                for (int i = 0; i < kActFields - 1; ++i) g[i] = static_cast<float>(gd[i]);
+                g[kActFields - 1] = static_cast<float>(hh.werr);
+                g[kActFields + 0] = hh.rgb[0];
+                g[kActFields + 1] = hh.rgb[1];
+                g[kActFields + 2] = hh.rgb[2];
+            }
+            __syncwarp();
+            // ---- B3b. per primitive of the group: lane v sums value v over the pixels that hit
+            // it in lane order (SH values from the staged w dL/dfinal and the pixel's basis),
+            // then adds the warp sum to the primitive's exact accumulator
+            int cur = off;
+#pragma unroll 1
+            for (int b = 0; b < sn; ++b) {
+                int my_e = -1;
+                if (cur < off + cnt && (sm.q[cur] & 0x7f) == sb + b) {
+                    if (sm.q[cur] & kComposited) my_e = cur;
+                    ++cur;
+                }
+                const uint32_t hm = __ballot_sync(0xffffffffu, my_e >= 0);
+                if (!hm) continue;
+                const int64_t row = static_cast<int64_t>(sm.id[sb + b]) * kPrimAccVals;
+#pragma unroll 1
+                for (int r0 = 0; r0 < n_vals; r0 += 32) {  // warp-uniform rounds (shuffles inside)
+                    const int v = r0 + lane;
+                    const bool is_act = v < kActFields;
+                    const int sv = is_act ? 0 : v - kActFields;
+                    const int shk = sv / 3, shc = sv - 3 * (sv / 3);
+                    float sum = 0.f;
+                    for (uint32_t m = hm; m; m &= m - 1) {
+                        const int h = __ffs(m) - 1;
+                        const int eh = __shfl_sync(0xffffffffu, my_e, h);
+                        if (v < n_vals) {
+                            const float* g = sm.res[eh].g;
+                            sum += is_act ? g[v] : g[kActFields + shc] * sm.basis[h][shk];
+                        }
+                    }
+                    if (v < n_vals && sum != 0.f && (!is_act || v < n_act)) xacc_add(acc, row + v, sum);
+                }
+            }
+            __syncwarp();
         }
-        // ---- flush the chunk's accumulators: activated part -> act_grad, SH -> PrimitiveGrad
-        __syncthreads();
-        for (int e = threadIdx.x; e < cn * n_vals; e += kThreads) {
-            const int j = e / n_vals, v = e - j * n_vals;
-            const float val = sm.acc[j][v];
-            if (val == 0.f) continue;
-            sm.acc[j][v] = 0.f;
-            const int64_t id = sm.id[j];
-            if (v < kActFields) atomicAdd(a.act_grad + id * kActFields + v, static_cast<double>(val));
-            else atomicAdd(a.prim_grad + id * NX_PARAMS_PER_NEXEL + 12 + (v - kActFields), static_cast<double>(val));
-        }
-        if (cb + kChunk < list_end && !__syncthreads_or(active)) break;
     }
 }
 
@@ -427,6 +420,19 @@ __device__ void quat_rotation_backward(const double* q_raw, const double* g, dou
     const double u[4] = {w, x, y, z};
     const double r = du[0] * u[0] + du[1] * u[1] + du[2] * u[2] + du[3] * u[3];
     for (int k = 0; k < 4; ++k) dq[k] = (du[k] - r * u[k]) / n;
+}
+
+// Reads the exact per-primitive sums back (zeroing them): the activated part into
+// act_grad for prim_finalize_kernel, the SH part added to PrimitiveGrad.
+__global__ void prim_take_kernel(const Xacc acc, int64_t n, double* __restrict__ act_grad,
+                                 double* __restrict__ prim_grad) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= n * kPrimAccVals) return;
+    const int64_t i = idx / kPrimAccVals;
+    const int v = static_cast<int>(idx - i * kPrimAccVals);
+    const double val = xacc_take(acc, idx);
+    if (v < kActFields) act_grad[i * kActFields + v] = val;
+    else if (val != 0.0) prim_grad[i * NX_PARAMS_PER_NEXEL + 12 + (v - kActFields)] += val;
 }
 
 // activation_backward (intersect.hpp:91-103) applied to the per-primitive sum of the
@@ -483,9 +489,12 @@ void launch_composite_backward(const CompositeBwdArgs& a, cudaStream_t s) {
     }
 }
 
-void launch_prim_finalize(const SceneDev& scene, int no_gamma, const double* act_grad, double* prim_grad,
+void launch_prim_finalize(const SceneDev& scene, int no_gamma, const Xacc& acc, double* act_grad, double* prim_grad,
                           double* blended_error, cudaStream_t s) {
     if (scene.n <= 0) return;
+    count_launch();
+    const int64_t nv = scene.n * kPrimAccVals;
+    prim_take_kernel<<<static_cast<unsigned>((nv + 255) / 256), 256, 0, s>>>(acc, scene.n, act_grad, prim_grad);
     count_launch();
     prim_finalize_kernel<<<static_cast<unsigned>((scene.n + 255) / 256), 256, 0, s>>>(scene, no_gamma, act_grad,
                                                                                      prim_grad, blended_error);

@@ -3,8 +3,8 @@
 // field_backward_batch (texture_field.cpp:77-146): grid_lookup (hash_grid.cpp:
 // 26-83) + TextureMlp::forward (mlp.cpp:24-43) recomputed, eval_sh_backward
 // (sh.hpp:76-83), TextureMlp::backward (mlp.cpp:45-90) and grid_lookup_backward
-// (hash_grid.hpp:85-124). Outputs: table / MLP weight gradients (accumulated in
-// fp64) and, per slot, dL/dt + dot(dL/dx, dir) — the crossing-depth gradient the
+// (hash_grid.hpp:85-124). Outputs: table / MLP weight gradients (exact
+// order-independent accumulators, nx_xacc.cuh, read back into the fp64 gradients) and, per slot, dL/dt + dot(dL/dx, dir) — the crossing-depth gradient the
 // compositing branch folds into intersect_backward (renderer.cpp:283-284).
 //
 // This file holds the general-shape SIMT variant (one thread per slot, fp64
@@ -52,7 +52,7 @@ __device__ __forceinline__ void sh_basis_d(const double* d, double* b) {
     b[15] = -0.5900435899266435 * x * (xx - 3.0 * yy);
 }
 
-__global__ void __launch_bounds__(128) field_bwd_simt_kernel(const FieldBwdArgs a) {
+__global__ void __launch_bounds__(128) field_bwd_simt_kernel(const FieldBwdArgs a, const Xacc tacc, const Xacc wacc) {
     const nx_field_desc& fd = a.scene.field;
     const int K = a.fb.K;
     const int64_t total = static_cast<int64_t>(a.cam.W) * a.cam.H * K;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(128) field_bwd_simt_kernel(const FieldBwdArgs 
         const double g = dy[o];
         if (g == 0.0) continue;
         for (int i = 0; i < nh; ++i) {
-            if (h2[i] != 0.0) atomicAdd(a.g_w3 + o * nh + i, g * h2[i]);
+            if (h2[i] != 0.0) xacc_add(wacc, nh * nin + nh * nh + o * nh + i, g * h2[i]);
             dh[i] += g * static_cast<double>(__ldg(a.scene.w3 + o * nh + i));
         }
     }
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(128) field_bwd_simt_kernel(const FieldBwdArgs 
         const double g = dh[o];
         if (g == 0.0) continue;
         for (int i = 0; i < nh; ++i) {
-            if (h1[i] != 0.0) atomicAdd(a.g_w2 + o * nh + i, g * h1[i]);
+            if (h1[i] != 0.0) xacc_add(wacc, nh * nin + o * nh + i, g * h1[i]);
             dh1[i] += g * static_cast<double>(__ldg(a.scene.w2 + o * nh + i));
         }
     }
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(128) field_bwd_simt_kernel(const FieldBwdArgs 
         const double g = dh1[o];
         if (g == 0.0) continue;
         for (int i = 0; i < nin; ++i) {
-            if (feats[i] != 0.0) atomicAdd(a.g_w1 + o * nin + i, g * feats[i]);
+            if (feats[i] != 0.0) xacc_add(wacc, o * nin + i, g * feats[i]);
             dfeat[i] += g * static_cast<double>(__ldg(a.scene.w1 + o * nin + i));
         }
     }
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(128) field_bwd_simt_kernel(const FieldBwdArgs 
                 double gdotf = 0.0;
                 for (int fi = 0; fi < F; ++fi) {
                     const double up = g[fi] * dw;
-                    if (up * cw != 0.0) atomicAdd(a.g_table + (slab + row) * F + fi, up * cw);
+                    if (up * cw != 0.0) xacc_add(tacc, static_cast<int64_t>((slab + row) * F + fi), up * cw);
                     gdotf += g[fi] * static_cast<double>(__ldg(tab + (slab + row) * F + fi));
                 }
                 const double updotf = gdotf * dw;
@@ -222,6 +222,17 @@ __global__ void __launch_bounds__(128) field_bwd_simt_kernel(const FieldBwdArgs 
     a.d_t_slot[sl] = dt + (dx[0] * dir[0] + dx[1] * dir[1] + dx[2] * dir[2]);
 }
 
+// g_w1 / g_w2 / g_w3 += the exact weight-gradient sums ([w1 | w2 | w3] in one accumulator).
+__global__ void take_weights_kernel(const Xacc acc, int64_t n1, int64_t n2, double* g_w1, double* g_w2, double* g_w3) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= acc.m) return;
+    const double v = xacc_take(acc, i);
+    if (v == 0.0) return;
+    if (i < n1) g_w1[i] += v;
+    else if (i < n1 + n2) g_w2[i - n1] += v;
+    else g_w3[i - n1 - n2] += v;
+}
+
 }  // namespace
 
 int launch_field_backward_simt(const FieldBwdArgs& a, cudaStream_t s) {
@@ -229,8 +240,20 @@ int launch_field_backward_simt(const FieldBwdArgs& a, cudaStream_t s) {
     if (fd.levels * fd.features > kMaxIn || fd.n_hidden > kMaxHidden) return NX_UNSUPPORTED;
     const int64_t total = static_cast<int64_t>(a.cam.W) * a.cam.H * a.fb.K;
     if (total == 0) return NX_OK;
-    count_launch();
-    field_bwd_simt_kernel<<<static_cast<unsigned>((total + 127) / 128), 128, 0, s>>>(a);
+    const int64_t nin = static_cast<int64_t>(fd.levels) * fd.features, nh = fd.n_hidden;
+    const int64_t n1 = nh * nin, n2 = nh * nh, nw = n1 + n2 + NX_SH_VALUES * nh;
+    const int64_t nt = static_cast<int64_t>(fd.levels) * (int64_t(1) << fd.log2_table) * fd.features;
+    FieldBwdScratch& sc = *a.scratch;
+    if (int st = sc.table_acc(nt, s)) return st;
+    if (int st = sc.weight_acc(nw, s)) return st;
+    const Xacc tacc{sc.tx, nt}, wacc{sc.wx, nw};
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    count_launch(3);
+    field_bwd_simt_kernel<<<static_cast<unsigned>((total + 127) / 128), 128, 0, s>>>(a, tacc, wacc);
+    take_table_kernel<<<8 * sms, 256, 0, s>>>(a.g_table, tacc);
+    take_weights_kernel<<<static_cast<unsigned>((nw + 255) / 256), 256, 0, s>>>(wacc, n1, n2, a.g_w1, a.g_w2, a.g_w3);
     return NX_OK;
 }
 

@@ -17,8 +17,9 @@
 //                          128 rows of the tile, accumulated in TMEM across all the
 //                          tiles of the CTA; partials reduced in a fixed order at the end
 //   S  scatter    one thread per slot: grid_lookup_backward (hash_grid.hpp:85-124):
-//                 table gradients (fp64 atomics, warp-aggregated where the warp
-//                 shares a cell), dL/dx, dL/dt -> d_t_slot = dL/dt + dot(dL/dx, dir)
+//                 table gradients (exact order-independent accumulators, nx_xacc.cuh;
+//                 warp-aggregated where the warp shares a cell), dL/dx, dL/dt ->
+//                 d_t_slot = dL/dt + dot(dL/dx, dir)
 //
 // MMA operands are bf16 with the 3-term split (a.b ~ ah.bh + ah.bl + al.bh), as in
 // the forward. The activations live in three combined K-major buffers so that every
@@ -589,22 +590,18 @@ __global__ void reduce_wgrads_kernel(const float* __restrict__ partials, int n_p
 }
 
 // ---------------------------------------------------------------- S: grid_lookup_backward
-__device__ __forceinline__ float warp_sum_f(float v) {
-#pragma unroll
-    for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-    return v;
-}
-
 // grid_lookup_backward (hash_grid.hpp:85-124) in two phases: (1) the position / fade
 // gradient, which needs the table values — gathered two levels deep in flight, no
 // atomics in between; (2) the table gradients, which need only the corner rows and
-// weights — one fp64 atomic per warp where the warp shares the cell (the heavily shared
-// coarse levels), else one float2 vector atomic per lane into an fp32 copy merged into
-// the fp64 gradients afterwards (fine levels: few contributions per row, half the bytes).
+// weights — into exact accumulators (nx_xacc.cuh), so that the table gradients do not
+// depend on the order of the atomics. Neighbouring slots of a warp share corner rows at
+// every level but the very finest (a warp covers 16 adjacent pixels), so the lanes that
+// hit the same row (__match_any_sync) are summed first, in lane order, and their leader
+// adds the sum: one accumulator update per distinct row of the warp.
 template <bool kSmall>
 __device__ __forceinline__ void scatter_levels(const FieldBwdArgs& a, const TcConst& cst, bool valid, double x0,
                                                double x1, double x2, float ft, const float* g, double t, double* dx,
-                                               double& dt, int leader, float2* __restrict__ tg32) {
+                                               double& dt, const Xacc& tacc, float2* __restrict__ wsh) {
     const uint32_t T = 1u << a.scene.field.log2_table, mask = T - 1u;
     const float2* tab = reinterpret_cast<const float2*>(a.scene.table);
     const int lane = threadIdx.x & 31;
@@ -645,34 +642,32 @@ __device__ __forceinline__ void scatter_levels(const FieldBwdArgs& a, const TcCo
         const LevelCell c = level_cell<kSmall>(l, x0, x1, x2, cst, mask, ft, a.st.no_downweight);
         const float g0 = valid ? g[2 * l] * c.dw : 0.f, g1 = valid ? g[2 * l + 1] * c.dw : 0.f;
         const float wx[2] = {1.0f - c.fr0, c.fr0}, wy[2] = {1.0f - c.fr1, c.fr1}, wz[2] = {1.0f - c.fr2, c.fr2};
-        double* slab = a.g_table + static_cast<size_t>(l) * T * 2;
-        float2* slab32 = tg32 + static_cast<size_t>(l) * T;
-        // the whole warp in one cell (coarse levels): one atomic per corner and feature
-        bool same = true;
-#pragma unroll
-        for (int ci = 0; ci < 8; ++ci) same &= c.row[ci] == __shfl_sync(0xffffffffu, c.row[ci], leader);
-        const bool uniform = __all_sync(0xffffffffu, !valid || same);
+        const int64_t slab = static_cast<int64_t>(l) * T * 2;
 #pragma unroll
         for (int ci = 0; ci < 8; ++ci) {
             const float cw = wx[ci & 1] * wy[(ci >> 1) & 1] * wz[(ci >> 2) & 1];
-            const float u0 = g0 * cw, u1 = g1 * cw;
-            double* dst = slab + static_cast<size_t>(c.row[ci]) * 2;
-            if (uniform) {
-                const float s0 = warp_sum_f(u0), s1 = warp_sum_f(u1);
-                if (lane == leader) {
-                    if (s0 != 0.f) atomicAdd(dst, static_cast<double>(s0));
-                    if (s1 != 0.f) atomicAdd(dst + 1, static_cast<double>(s1));
+            const uint32_t peers = __match_any_sync(0xffffffffu, valid ? c.row[ci] : 0xffffffffu);
+            wsh[lane] = make_float2(g0 * cw, g1 * cw);
+            __syncwarp();
+            if (valid && lane == __ffs(peers) - 1) {
+                float s0 = 0.f, s1 = 0.f;
+                for (uint32_t m = peers; m; m &= m - 1) {
+                    const float2 u = wsh[__ffs(m) - 1];
+                    s0 += u.x;
+                    s1 += u.y;
                 }
-            } else if (valid && (u0 != 0.f || u1 != 0.f)) {
-                atomicAdd(slab32 + c.row[ci], make_float2(u0, u1));
+                const int64_t dst = slab + static_cast<int64_t>(c.row[ci]) * 2;
+                xacc_add(tacc, dst, s0);
+                xacc_add(tacc, dst + 1, s1);
             }
+            __syncwarp();
         }
     }
 }
 
 __global__ void __launch_bounds__(128) scatter_kernel(const FieldBwdArgs a, const TcConst cst,
                                                       const float* __restrict__ fbuf, int64_t total,
-                                                      float2* __restrict__ tg32) {
+                                                      const Xacc tacc) {
     const int64_t sl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool in = sl < total;
     const bool valid = in && a.fb.ids[sl] >= 0;
@@ -681,7 +676,7 @@ __global__ void __launch_bounds__(128) scatter_kernel(const FieldBwdArgs a, cons
         if (in) a.d_t_slot[sl] = 0.0;
         return;
     }
-    const int leader = __ffs(vmask) - 1;
+    __shared__ float2 wsh[128];
     double dir[3] = {0.0, 0.0, 1.0};
     double t = 1.0, x0 = 0.0, x1 = 0.0, x2 = 0.0;
     float g[kIn];
@@ -708,23 +703,24 @@ __global__ void __launch_bounds__(128) scatter_kernel(const FieldBwdArgs a, cons
     double dx[3] = {0.0, 0.0, 0.0}, dt = 0.0;
     const bool small = fmax(fabs(x0), fmax(fabs(x1), fabs(x2))) * cst.level_scale[kLevels - 1] < 1073741824.0;
     if (__all_sync(0xffffffffu, small))
-        scatter_levels<true>(a, cst, valid, x0, x1, x2, ft, g, t, dx, dt, leader, tg32);
+        scatter_levels<true>(a, cst, valid, x0, x1, x2, ft, g, t, dx, dt, tacc, wsh + (threadIdx.x & ~31));
     else
-        scatter_levels<false>(a, cst, valid, x0, x1, x2, ft, g, t, dx, dt, leader, tg32);
+        scatter_levels<false>(a, cst, valid, x0, x1, x2, ft, g, t, dx, dt, tacc, wsh + (threadIdx.x & ~31));
     if (in) a.d_t_slot[sl] = valid ? dt + (dx[0] * dir[0] + dx[1] * dir[1] + dx[2] * dir[2]) : 0.0;
 }
 
-// g_table += the fp32 per-lane table gradients (and clears them for the next call).
-__global__ void merge_table_kernel(double* __restrict__ g_table, float* __restrict__ tg32, int64_t n) {
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+}  // namespace
+
+// g_table += the exact table-gradient sums (and clears the accumulators for the next call).
+__global__ void take_table_kernel(double* __restrict__ g, const Xacc acc) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < acc.m;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const float v = tg32[i];
-        if (v != 0.f) {
-            g_table[i] += static_cast<double>(v);
-            tg32[i] = 0.f;
-        }
+        const double v = xacc_take(acc, i);
+        if (v != 0.0) g[i] += v;
     }
 }
+
+namespace {
 
 
 }  // namespace
@@ -758,15 +754,8 @@ int launch_field_backward_tc(const FieldBwdArgs& a, cudaStream_t s) {
         if (cudaMalloc(&sc.amb, (total + 1) * sizeof(int32_t)) != cudaSuccess) return NX_OUT_OF_MEMORY;
         sc.acap = total + 1;
     }
-    const size_t tneed = static_cast<size_t>(kLevels) * (size_t(1) << a.scene.field.log2_table) * 2;
-    if (tneed > sc.tcap) {
-        if (sc.tg32) cudaFree(sc.tg32);
-        sc.tg32 = nullptr;
-        sc.tcap = 0;
-        if (cudaMalloc(&sc.tg32, tneed * sizeof(float)) != cudaSuccess) return NX_OUT_OF_MEMORY;
-        if (cudaMemsetAsync(sc.tg32, 0, tneed * sizeof(float), s) != cudaSuccess) return NX_CUDA_ERROR;
-        sc.tcap = tneed;
-    }
+    const int64_t tneed = static_cast<int64_t>(kLevels) * (int64_t(1) << a.scene.field.log2_table) * 2;
+    if (int st = sc.table_acc(tneed, s)) return st;
     if (pneed > sc.pcap) {
         if (sc.parts) cudaFree(sc.parts);
         sc.parts = nullptr;
@@ -788,9 +777,10 @@ int launch_field_backward_tc(const FieldBwdArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(mlp_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemM);
     mlp_bwd_tc_kernel<<<grid_m, kThreadsM, kSmemM, s>>>(a, sc.fbuf, sc.parts, total, n_tiles);
     reduce_wgrads_kernel<<<(kWGrads + 255) / 256, 256, 0, s>>>(sc.parts, grid_m, a.g_w1, a.g_w2, a.g_w3);
-    scatter_kernel<<<blocks, 128, 0, s>>>(a, cst, sc.fbuf, total, reinterpret_cast<float2*>(sc.tg32));
+    const Xacc tacc{sc.tx, tneed};
+    scatter_kernel<<<blocks, 128, 0, s>>>(a, cst, sc.fbuf, total, tacc);
     count_launch();
-    merge_table_kernel<<<8 * sms, 256, 0, s>>>(a.g_table, sc.tg32, static_cast<int64_t>(tneed));
+    take_table_kernel<<<8 * sms, 256, 0, s>>>(a.g_table, tacc);
     return NX_OK;
 }
 

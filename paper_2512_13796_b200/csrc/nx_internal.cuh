@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include "../../include/nexel_b200.h"
+#include "nx_xacc.cuh"
 
 #define NX_HD __host__ __device__ __forceinline__
 
@@ -270,25 +271,44 @@ void launch_stream_copy(const CopyJobs& jobs, cudaStream_t s);
 // intersect.hpp:45-51) + the blended-error sum: d_mu[3], d_R[9] (row-major m[i][j],
 // columns v1, v2, n), d_sigma[2], d_opacity, d_gamma[2], blended error.
 constexpr int kActFields = 18;
+// Exact per-primitive accumulator values of the compositing branch: the activated
+// fields + the 48 SH gradients (nx_xacc.cuh).
+constexpr int kPrimAccVals = kActFields + NX_SH_VALUES;
 
-// Device scratch of the tensor-core field backward, owned by the context (grow-only;
-// the fp32 table-gradient copy is kept zeroed between calls).
+// Device scratch of the field backward, owned by the context (grow-only; the exact
+// accumulators are zeroed when allocated and kept zero between calls by their readers).
 struct FieldBwdScratch {
     float* fbuf = nullptr;
     size_t fcap = 0;
     int32_t* amb = nullptr;
     size_t acap = 0;
-    float* tg32 = nullptr;
-    size_t tcap = 0;
+    unsigned long long* tx = nullptr;  // table-gradient accumulators (nx_xacc.cuh)
+    size_t txcap = 0;                  // bytes
+    unsigned long long* wx = nullptr;  // MLP weight-gradient accumulators (SIMT path)
+    size_t wxcap = 0;
     float* parts = nullptr;
     size_t pcap = 0;
+    static int grow_zeroed(unsigned long long*& p, size_t& cap, size_t bytes, cudaStream_t s) {
+        if (bytes <= cap && p) return NX_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) return NX_OUT_OF_MEMORY;
+        if (cudaMemsetAsync(p, 0, bytes, s) != cudaSuccess) return NX_CUDA_ERROR;
+        cap = bytes;
+        return NX_OK;
+    }
+    int table_acc(int64_t m, cudaStream_t s) { return grow_zeroed(tx, txcap, xacc_bytes(m), s); }
+    int weight_acc(int64_t m, cudaStream_t s) { return grow_zeroed(wx, wxcap, xacc_bytes(m), s); }
     void release() {
-        for (void* p : {static_cast<void*>(fbuf), static_cast<void*>(amb), static_cast<void*>(tg32),
-                        static_cast<void*>(parts)})
+        for (void* p : {static_cast<void*>(fbuf), static_cast<void*>(amb), static_cast<void*>(tx),
+                        static_cast<void*>(wx), static_cast<void*>(parts)})
             if (p) cudaFree(p);
         *this = FieldBwdScratch{};
     }
 };
+// g += the accumulators' sums, zeroing them (nx_field_backward_tc.cu)
+__global__ void take_table_kernel(double* __restrict__ g, const Xacc acc);
 
 struct FieldBwdArgs {
     SceneDev scene;
@@ -325,13 +345,14 @@ struct CompositeBwdArgs {
     const double* d_weights;  // H*W*K or nullptr
     const double* d_t_slot;   // H*W*K
     const double* err_pixel;  // H*W or nullptr
-    double* act_grad;         // n x kActFields
-    double* prim_grad;        // n x 60 (the SH part is accumulated here directly)
+    Xacc acc;                 // n x kPrimAccVals exact accumulators (zero on entry)
 };
 // The per-pixel reverse march of render_backward (renderer.cpp:287-390).
 void launch_composite_backward(const CompositeBwdArgs& a, cudaStream_t s);
 // activation_backward (intersect.hpp:91-103) of the summed activated gradients.
-void launch_prim_finalize(const SceneDev& scene, int no_gamma, const double* act_grad, double* prim_grad,
+// Reads the accumulators back (zeroing them) into act_grad / the SH gradients, then
+// applies activation_backward.
+void launch_prim_finalize(const SceneDev& scene, int no_gamma, const Xacc& acc, double* act_grad, double* prim_grad,
                           double* blended_error, cudaStream_t s);
 
 }  // namespace nx

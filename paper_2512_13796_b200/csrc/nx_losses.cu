@@ -9,8 +9,9 @@
 //   alpha    mean (1 - buffered mass) (losses.cpp:183-195);
 //   opacity  mean sigmoid(opacity_raw) -> grads.prims[i].opacity_raw (losses.cpp:201-210);
 //   grid     sum_l s_l^-3 sum table^2 -> grads.field.table (losses.cpp:212-228).
-// Every pixel term is one thread (per channel for SSIM); sums are fp64 atomics of
-// block partials; a last kernel forms LossTerms on the device.
+// Every pixel term is one thread (per channel for SSIM); block partials meet in exact
+// order-independent accumulators (nx_xacc.cuh), so the terms are bit-reproducible; a
+// last kernel forms LossTerms on the device.
 #include <algorithm>
 #include <cmath>
 
@@ -26,10 +27,12 @@ constexpr int kThreads = 256;
 constexpr int kMaxLevels = 64;
 
 // Sums accumulated by the kernels (device, zeroed per call).
+enum { kSumSsim, kSumL1, kSumTex, kSumAlpha, kSumOpacity, kSumGrid0, kSumVals = kSumGrid0 + kMaxLevels };
 struct LossSums {
-    double ssim, l1, tex, tex_included, alpha, opacity;
-    double grid_level[kMaxLevels];
+    double tex_included;  // a count of pixels: exact in any order
+    unsigned long long words[kSumVals * kXaccWordsTotal];
 };
+__device__ __forceinline__ Xacc sums_acc(LossSums* s) { return Xacc{s->words, kSumVals}; }
 
 struct LossArgs {
     int W, H, K;
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(kThreads) ssim_vpass_kernel(const LossArgs a) 
         dmap(a, c, 2)[i] = scale * (2 * a1 / (b1 * b2));
     }
     const double t = block_sum(s_val, sh);
-    if (threadIdx.x == 0 && t != 0.0) atomicAdd(&a.sums->ssim, t);
+    if (threadIdx.x == 0) xacc_add(sums_acc(a.sums), kSumSsim, t);
 }
 
 // adjoint blur, horizontal half, of the three partial maps
@@ -185,7 +188,7 @@ __global__ void __launch_bounds__(kThreads) ssim_bwd_vpass_kernel(const LossArgs
         a.d_final[i * 3 + c] = (1.0 - a.w.dssim) * sgn(diff) * l1_scale - 0.5 * a.w.dssim * d_ssim;
     }
     const double t = block_sum(l1, sh);
-    if (threadIdx.x == 0 && t != 0.0) atomicAdd(&a.sums->l1, t);
+    if (threadIdx.x == 0) xacc_add(sums_acc(a.sums), kSumL1, t);
 }
 
 // texture supervision and coverage, pass 1: included count, texture error, coverage
@@ -210,9 +213,9 @@ __global__ void __launch_bounds__(kThreads) tex_alpha_sums_kernel(const LossArgs
     const double s0 = block_sum(inc, sh);
     if (threadIdx.x == 0 && s0 != 0.0) atomicAdd(&a.sums->tex_included, s0);
     const double s1 = block_sum(err, sh);
-    if (threadIdx.x == 0 && s1 != 0.0) atomicAdd(&a.sums->tex, s1);
+    if (threadIdx.x == 0) xacc_add(sums_acc(a.sums), kSumTex, s1);
     const double s2 = block_sum(cov, sh);
-    if (threadIdx.x == 0 && s2 != 0.0) atomicAdd(&a.sums->alpha, s2);
+    if (threadIdx.x == 0) xacc_add(sums_acc(a.sums), kSumAlpha, s2);
 }
 
 // pass 2: d_texture and d_weights of every slot (overwritten)
@@ -265,7 +268,7 @@ __global__ void __launch_bounds__(kThreads) opacity_kernel(const LossArgs a) {
         a.g_prims[i * NX_PARAMS_PER_NEXEL + 9] += (a.w.opacity / static_cast<double>(a.n_prims)) * o * (1.0 - o);
     }
     const double t = block_sum(o, sh);
-    if (threadIdx.x == 0 && t != 0.0) atomicAdd(&a.sums->opacity, t);
+    if (threadIdx.x == 0) xacc_add(sums_acc(a.sums), kSumOpacity, t);
 }
 
 // grid regulariser (losses.cpp:212-228): one level slab per blockIdx.y
@@ -282,27 +285,30 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(const LossArgs a) {
         a.g_table[base + e] += a.w.grid * 2.0 * v / s3;
     }
     const double t = block_sum(acc, sh);
-    if (threadIdx.x == 0 && t != 0.0) atomicAdd(&a.sums->grid_level[l], t);
+    if (threadIdx.x == 0) xacc_add(sums_acc(a.sums), kSumGrid0 + l, t);
 }
 
 // LossTerms (losses.cpp:137-139, 162, 195, 209, 227, 231-232)
 __global__ void terms_kernel(const LossArgs a) {
-    const LossSums& s = *a.sums;
+    const Xacc acc = sums_acc(a.sums);
+    const double tex_included = a.sums->tex_included;
+    const double s_ssim = xacc_take(acc, kSumSsim), s_l1 = xacc_take(acc, kSumL1), s_tex = xacc_take(acc, kSumTex),
+                 s_alpha = xacc_take(acc, kSumAlpha), s_opacity = xacc_take(acc, kSumOpacity);
     const double npix = static_cast<double>(a.W) * a.H;
     nx_loss_terms t;
-    t.l1 = s.l1 / (3.0 * npix);
-    t.dssim = (1.0 - s.ssim / (3.0 * npix)) / 2.0;
+    t.l1 = s_l1 / (3.0 * npix);
+    t.dssim = (1.0 - s_ssim / (3.0 * npix)) / 2.0;
     t.image = (1.0 - a.w.dssim) * t.l1 + a.w.dssim * t.dssim;
     if (a.K > 0) {
-        t.texture = s.tex_included > 0 ? s.tex / (3.0 * s.tex_included) : 0.0;
-        t.alpha = s.alpha / npix;
+        t.texture = tex_included > 0 ? s_tex / (3.0 * tex_included) : 0.0;
+        t.alpha = s_alpha / npix;
     } else {
         t.texture = 0.0;
         t.alpha = 1.0;
     }
-    t.opacity = a.n_prims > 0 ? s.opacity / static_cast<double>(a.n_prims) : 0.0;
+    t.opacity = a.n_prims > 0 ? s_opacity / static_cast<double>(a.n_prims) : 0.0;
     double g = 0.0;
-    for (int l = 0; l < a.levels; ++l) g += s.grid_level[l] / a.s3[l];
+    for (int l = 0; l < a.levels; ++l) g += xacc_take(acc, kSumGrid0 + l) / a.s3[l];
     t.grid = g;
     t.total = t.image + a.w.texture * t.texture + a.w.alpha * t.alpha + a.w.opacity * t.opacity + a.w.grid * t.grid;
     *a.terms = t;

@@ -85,3 +85,22 @@ def test_value_api_losses_then_render_backward(reference):
     terms, df, dw, dt = nx.losses_backward(scene, res.fb, gt, LossWeights(), g)
     nx.render_backward(scene, cam, res.fb, nx.UpstreamGrads(df, dw, dt), g)
     assert np.isfinite(terms["total"]) and np.isfinite(g.prims).all() and np.abs(g.prims).max() > 0
+
+
+def test_loss_terms_are_bit_reproducible(renderer):
+    """Block partials meet in exact accumulators: the same frame gives the same bits."""
+    scene = nx.stump_like(20_000, log2_table=14, grid_init=1e-1)
+    cam = nx.ring_camera(9, 256, 256, 192)
+    gt = np.random.default_rng(3).random(cam.width * cam.height * 3)
+    ds = renderer.upload(scene)
+    fr = renderer.frame()
+    renderer.render(ds, cam, fr)
+    outs = []
+    for _ in range(3):
+        g = SceneGrads.allocate(scene)
+        terms, d_final, d_weights, d_texture = renderer.losses_backward(ds, fr, gt, LossWeights(), g)
+        outs.append((terms, d_final, d_weights, d_texture, g.prims, g.table))
+    for o in outs[1:]:
+        assert o[0] == outs[0][0]
+        for a, b in zip(o[1:], outs[0][1:]):
+            assert np.array_equal(a, b)
