@@ -49,14 +49,18 @@ oracle:
 # symbols of its renderer.cpp. Then the reference's own test_oracle.cpp is built
 # unmodified against it (tests/cxx/doctest.h stands in for doctest).
 DROPIN := build/dropin
-DROPIN_TUS := camera primitive hash_grid mlp texture_field threading oracle
+DROPIN_TUS := camera primitive hash_grid mlp texture_field threading oracle losses ssim checkpoint adam density metrics
+# the bundle / synthetic-dataset TUs (nlohmann/json, vendored in the venv) for the C++ tests
+JSON_INC := /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
+CUDA_HOME ?= /usr/local/cuda
 DROPIN_CXX := -std=gnu++20 -O3 -DNDEBUG -fPIC -pthread -march=x86-64-v3 -I$(REF)/core/include
 RENAME_FWD := -Dcollection_pass=nexel_ref_collection_pass -Dtexturing_pass=nexel_ref_texturing_pass \
               -Drender=nexel_ref_render -Dvalidate_settings=nexel_ref_validate_settings \
               -Drender_backward=nexel_ref_render_backward
 
 ifneq ($(wildcard $(REF)/core/src/renderer.cpp),)
-dropin: $(DROPIN)/libnexel_dropin.so $(DROPIN)/test_oracle_dropin $(DROPIN)/test_dropin_backward
+dropin: $(DROPIN)/libnexel_dropin.so $(DROPIN)/test_oracle_dropin $(DROPIN)/test_dropin_backward \
+        $(DROPIN)/test_train_dropin $(DROPIN)/test_dropin_train
 else
 dropin:
 	@echo "reference sources not present; using the prebuilt $(DROPIN) if any"
@@ -74,10 +78,42 @@ $(DROPIN)/renderer_b200.o: $(PKG)/host/renderer_b200.cpp include/nexel_b200.h
 	@mkdir -p $(DROPIN)
 	$(CXX) $(DROPIN_CXX) -c -o $@ $<
 
-$(DROPIN)/libnexel_dropin.so: $(DROPIN)/renderer_b200.o $(DROPIN)/ref_renderer_backward.o \
+# nexel::train / mean_psnr on the device (host/trainer_b200.cpp); the reference's
+# trainer.cpp keeps config parsing and initialize_scene, its own train / mean_psnr
+# exported as nexel_ref_train / nexel_ref_mean_psnr over the reference's CPU renderer
+$(DROPIN)/trainer_b200.o: $(PKG)/host/trainer_b200.cpp include/nexel_b200.h
+	@mkdir -p $(DROPIN)
+	$(CXX) $(DROPIN_CXX) -I$(CUDA_HOME)/include -c -o $@ $<
+
+$(DROPIN)/ref_trainer_renamed.o: $(REF)/core/src/trainer.cpp
+	@mkdir -p $(DROPIN)
+	$(CXX) $(DROPIN_CXX) -Dtrain=nexel_ref_train -Dmean_psnr=nexel_ref_mean_psnr -Drender=nexel_ref_render \
+	    -Drender_backward=nexel_ref_render_backward -c -o $@ $<
+
+$(DROPIN)/ref_json_%.o: $(REF)/core/src/%.cpp
+	@mkdir -p $(DROPIN)
+	$(CXX) $(DROPIN_CXX) -I$(JSON_INC) -c -o $@ $<
+
+$(DROPIN)/png_stub.o: tests/cxx/png_stub.cpp
+	@mkdir -p $(DROPIN)
+	$(CXX) $(DROPIN_CXX) -c -o $@ $<
+
+$(DROPIN)/libnexel_dropin.so: $(DROPIN)/renderer_b200.o $(DROPIN)/ref_renderer_backward.o $(DROPIN)/trainer_b200.o \
+                              $(DROPIN)/ref_trainer_renamed.o \
                               $(addprefix $(DROPIN)/ref_,$(addsuffix .o,$(DROPIN_TUS))) $(PKG)/libnexel_b200.so
-	$(CXX) -shared -pthread -o $@ $(filter %.o,$^) -L$(PKG) -lnexel_b200 \
-	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+	$(CXX) -shared -pthread -o $@ $(filter %.o,$^) -L$(PKG) -lnexel_b200 -L$(CUDA_HOME)/lib64 -lcudart \
+	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,$(CUDA_HOME)/lib64
+
+TRAIN_TEST_OBJS := $(DROPIN)/ref_json_bundle.o $(DROPIN)/ref_json_synthetic.o $(DROPIN)/png_stub.o
+
+# the reference's own test_train.cpp, unmodified, against the GPU-backed train
+$(DROPIN)/test_train_dropin: $(REF)/tests/test_train.cpp tests/cxx/doctest.h $(TRAIN_TEST_OBJS) $(DROPIN)/libnexel_dropin.so
+	$(CXX) $(DROPIN_CXX) -Itests/cxx -I$(REF)/tests -o $@ $< $(TRAIN_TEST_OBJS) -L$(DROPIN) -lnexel_dropin \
+	    -Wl,-rpath,'$$ORIGIN'
+
+$(DROPIN)/test_dropin_train: tests/cxx/test_dropin_train.cpp tests/cxx/doctest.h $(TRAIN_TEST_OBJS) $(DROPIN)/libnexel_dropin.so
+	$(CXX) $(DROPIN_CXX) -Itests/cxx -I$(REF)/tests -o $@ $< $(TRAIN_TEST_OBJS) -L$(DROPIN) -lnexel_dropin \
+	    -Wl,-rpath,'$$ORIGIN'
 
 $(DROPIN)/test_oracle_dropin: $(REF)/tests/test_oracle.cpp tests/cxx/doctest.h $(DROPIN)/libnexel_dropin.so
 	$(CXX) $(DROPIN_CXX) -Itests/cxx -I$(REF)/tests -o $@ $< -L$(DROPIN) -lnexel_dropin -Wl,-rpath,'$$ORIGIN'

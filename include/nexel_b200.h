@@ -290,6 +290,10 @@ void nx_loss_weights_default(nx_loss_weights* out);
 int nx_losses_backward(nx_ctx* ctx, const nx_scene* scene, const nx_frame* frame, const double* gt,
                        const nx_loss_weights* w, double* d_final, double* d_weights, double* d_texture,
                        const nx_grads* grads, nx_loss_terms* terms, void* stream);
+/* Per-pixel error of the frame's final image against gt, err[p] = sum_c |final - gt| / 3
+ * (trainer.cpp:288-295): the err_pixel render_backward spreads onto the primitives.
+ * gt: H*W*3 fp64, err: H*W fp64, device pointers, on `stream`. */
+int nx_pixel_error(nx_ctx* ctx, const nx_frame* frame, const double* gt, double* err, void* stream);
 /* Same with HOST arrays and host `terms` (synchronous). */
 int nx_losses_backward_host(nx_ctx* ctx, const nx_scene* scene, const nx_frame* frame, const double* gt,
                             const nx_loss_weights* w, double* d_final, double* d_weights, double* d_texture,
@@ -314,13 +318,29 @@ typedef struct nx_adam_config {
 #define NX_GROUP_W3 10
 #define NX_NUM_GROUPS 11
 typedef struct nx_optimizer nx_optimizer;
-/* fp64 first / second moments for every parameter of the scene, zeroed (step 0). */
+/* fp64 first / second moments for every parameter of the scene, zeroed (step 0), and
+ * fp64 master copies of the parameters the device scene stores in fp32 (SH, hash table,
+ * MLP weights), initialised from the scene's fp32 values: Adam updates the masters in
+ * fp64, like the reference's fp64 parameters, and refreshes the scene's fp32 copies. */
 int nx_optimizer_create(nx_ctx* ctx, const nx_scene* scene, nx_optimizer** out);
+/* Parameter count of a group (AdamState size once stepped). */
+int nx_optimizer_size(const nx_optimizer* opt, int group, int64_t* count);
+/* Sets the fp64 master values of a group from HOST memory (count = its size, in the
+ * group's row layout: per-nexel rows of the group's width, or the flat field block),
+ * e.g. the exact fp64 initialisation the fp32 scene upload rounded. Geometry groups
+ * (0..4) are fp64 in the scene already and are written there. Synchronous. */
+int nx_optimizer_set_params(nx_ctx* ctx, nx_optimizer* opt, nx_scene* scene, int group, const double* host,
+                            int64_t count);
+/* Reads a group back to HOST memory (any NULL skipped): the fp64 parameter values
+ * (masters / scene geometry) and the moments, in the group's row layout. Synchronous. */
+int nx_optimizer_download(nx_ctx* ctx, const nx_optimizer* opt, const nx_scene* scene, int group, double* params,
+                          double* m, double* v);
 void nx_optimizer_destroy(nx_optimizer* opt);
 /* One adam_step per group (cfg[NX_NUM_GROUPS]) on the device scene's parameters in
  * place, from device SceneGrads: per group step += 1, m/v EMAs, bias-corrected update.
- * Parameters the device stores in fp32 (SH, hash table, MLP weights) are updated in fp64
- * and rounded back. A group with lr == 0 is skipped (its step does not advance). */
+ * Parameters the device stores in fp32 (SH, hash table, MLP weights) are updated on the
+ * optimizer's fp64 masters, whose rounding refreshes the scene. lr == 0 steps the moments like adam_step; a group with lr < 0 is
+ * skipped (its step does not advance). */
 int nx_optimizer_step(nx_ctx* ctx, nx_optimizer* opt, nx_scene* scene, const nx_grads* grads,
                       const nx_adam_config* cfg, void* stream);
 /* Per-group step counters (AdamState::step). */

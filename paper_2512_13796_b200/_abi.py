@@ -230,6 +230,10 @@ SIGNATURES = [
     ("nx_optimizer_destroy", None, [P]),
     ("nx_optimizer_step", C.c_int, [P, P, P, C.POINTER(nx_grads), C.POINTER(nx_adam_config), P]),
     ("nx_optimizer_steps", C.c_int, [P, PI64]),
+    ("nx_optimizer_size", C.c_int, [P, C.c_int, PI64]),
+    ("nx_optimizer_set_params", C.c_int, [P, P, P, C.c_int, PD, I64]),
+    ("nx_optimizer_download", C.c_int, [P, P, P, C.c_int, PD, PD, PD]),
+    ("nx_pixel_error", C.c_int, [P, P, P, P, P]),
     ("nx_scene_download", C.c_int, [P, P, PD, PD, PD, PD, PD]),
     ("nx_scene_prune", C.c_int, [P, P, P, D, P, PI64]),
     ("nx_scene_densify_split", C.c_int, [P, P, P, P, P, I64, D, P, PI64, PI64]),

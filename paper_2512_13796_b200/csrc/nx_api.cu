@@ -1144,6 +1144,17 @@ int nx_losses_backward(nx_ctx* c, const nx_scene* scene, const nx_frame* fc, con
     return NX_OK;
 }
 
+int nx_pixel_error(nx_ctx* c, const nx_frame* fc, const double* gt, double* err, void* stream) {
+    if (!c || !fc || !gt || !err) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    nx_frame* f = const_cast<nx_frame*>(fc);
+    cudaSetDevice(c->device);
+    cudaStream_t s = pick_stream(c, stream);
+    NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_ready, 0));
+    launch_pixel_error(frame_dev(f).final_img, gt, static_cast<int64_t>(f->W) * f->H, err, s);
+    NX_CUDA(c, cudaGetLastError());
+    return NX_OK;
+}
+
 int nx_losses_backward_host(nx_ctx* c, const nx_scene* scene, const nx_frame* fc, const double* gt,
                             const nx_loss_weights* w, double* d_final, double* d_weights, double* d_texture,
                             const nx_grads* g, nx_loss_terms* terms) {
@@ -1189,6 +1200,7 @@ struct nx_optimizer {
     nx_ctx* ctx = nullptr;
     int64_t n = 0;
     DevBuf m[NX_NUM_GROUPS], v[NX_NUM_GROUPS];
+    DevBuf master[NX_NUM_GROUPS];  // fp64 values of the groups the scene stores in fp32 (5..10)
     int64_t step[NX_NUM_GROUPS] = {};
     int64_t size[NX_NUM_GROUPS] = {};
 };
@@ -1206,12 +1218,76 @@ int nx_optimizer_create(nx_ctx* c, const nx_scene* scene, nx_optimizer** out) {
     for (int gi = 0; gi < NX_NUM_GROUPS; ++gi) {
         const size_t bytes = std::max<int64_t>(o->size[gi], 1) * sizeof(double);
         if (o->m[gi].ensure(bytes) != cudaSuccess || o->v[gi].ensure(bytes) != cudaSuccess ||
-            cudaMemset(o->m[gi].p, 0, bytes) != cudaSuccess || cudaMemset(o->v[gi].p, 0, bytes) != cudaSuccess) {
+            cudaMemset(o->m[gi].p, 0, bytes) != cudaSuccess || cudaMemset(o->v[gi].p, 0, bytes) != cudaSuccess ||
+            (gi >= NX_GROUP_SH_DC && o->master[gi].ensure(bytes) != cudaSuccess)) {
             nx_optimizer_destroy(o);
             return set_err(c, NX_OUT_OF_MEMORY, "optimizer state");
         }
     }
+    nx_scene* sc = const_cast<nx_scene*>(scene);
+    for (int gi = NX_GROUP_SH_DC; gi < NX_NUM_GROUPS; ++gi)
+        launch_group_io(gi, scene_dev(scene), sc->geom.as<double>(), sc->sh.as<float>(), sc->table.as<float>(),
+                        sc->w1.as<float>(), sc->w2.as<float>(), sc->w3.as<float>(), o->master[gi].as<double>(), true,
+                        c->stream);
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) {
+        nx_optimizer_destroy(o);
+        return set_err(c, NX_CUDA_ERROR, "optimizer masters");
+    }
     *out = o;
+    return NX_OK;
+}
+
+int nx_optimizer_size(const nx_optimizer* o, int group, int64_t* count) {
+    if (!o || !count || group < 0 || group >= NX_NUM_GROUPS) return NX_INVALID_ARGUMENT;
+    *count = o->size[group];
+    return NX_OK;
+}
+
+int nx_optimizer_set_params(nx_ctx* c, nx_optimizer* o, nx_scene* scene, int group, const double* host,
+                            int64_t count) {
+    if (!c || !o || !scene || !host) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    if (group < 0 || group >= NX_NUM_GROUPS || count != o->size[group] || scene->n != o->n)
+        return set_err(c, NX_INVALID_ARGUMENT, "optimizer_set_params: bad group or size");
+    if (count == 0) return NX_OK;
+    cudaSetDevice(c->device);
+    cudaStream_t s = c->stream;
+    DevBuf rows;
+    NX_CUDA(c, rows.ensure(count * sizeof(double)));
+    NX_CUDA(c, cudaMemcpyAsync(rows.p, host, count * sizeof(double), cudaMemcpyHostToDevice, s));
+    // the scene's copy (geometry: the values themselves; fp32 groups: their rounding)
+    launch_group_io(group, scene_dev(scene), scene->geom.as<double>(), scene->sh.as<float>(), scene->table.as<float>(),
+                    scene->w1.as<float>(), scene->w2.as<float>(), scene->w3.as<float>(), rows.as<double>(), false, s);
+    if (group >= NX_GROUP_SH_DC)
+        NX_CUDA(c, cudaMemcpyAsync(o->master[group].p, rows.p, count * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    NX_CUDA(c, cudaStreamSynchronize(s));
+    return NX_OK;
+}
+
+int nx_optimizer_download(nx_ctx* c, const nx_optimizer* o, const nx_scene* scene, int group, double* params,
+                          double* m, double* v) {
+    if (!c || !o || !scene) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    if (group < 0 || group >= NX_NUM_GROUPS || scene->n != o->n)
+        return set_err(c, NX_INVALID_ARGUMENT, "optimizer_download: bad group or scene");
+    const int64_t count = o->size[group];
+    if (count == 0) return NX_OK;
+    cudaSetDevice(c->device);
+    cudaStream_t s = c->stream;
+    NX_CUDA(c, cudaStreamSynchronize(s));
+    if (params) {
+        if (group >= NX_GROUP_SH_DC) {
+            NX_CUDA(c, cudaMemcpy(params, o->master[group].p, count * sizeof(double), cudaMemcpyDeviceToHost));
+        } else {
+            DevBuf rows;
+            NX_CUDA(c, rows.ensure(count * sizeof(double)));
+            nx_scene* sc = const_cast<nx_scene*>(scene);
+            launch_group_io(group, scene_dev(scene), sc->geom.as<double>(), sc->sh.as<float>(), sc->table.as<float>(),
+                            sc->w1.as<float>(), sc->w2.as<float>(), sc->w3.as<float>(), rows.as<double>(), true, s);
+            NX_CUDA(c, cudaMemcpyAsync(params, rows.p, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+            NX_CUDA(c, cudaStreamSynchronize(s));
+        }
+    }
+    if (m) NX_CUDA(c, cudaMemcpy(m, o->m[group].p, count * sizeof(double), cudaMemcpyDeviceToHost));
+    if (v) NX_CUDA(c, cudaMemcpy(v, o->v[group].p, count * sizeof(double), cudaMemcpyDeviceToHost));
     return NX_OK;
 }
 
@@ -1221,6 +1297,7 @@ void nx_optimizer_destroy(nx_optimizer* o) {
     for (int gi = 0; gi < NX_NUM_GROUPS; ++gi) {
         o->m[gi].release();
         o->v[gi].release();
+        o->master[gi].release();
     }
     delete o;
 }
@@ -1240,11 +1317,12 @@ int nx_optimizer_step(nx_ctx* c, nx_optimizer* o, nx_scene* scene, const nx_grad
     cudaStream_t s = pick_stream(c, stream);
     const SceneDev sd = scene_dev(scene);
     for (int gi = 0; gi < NX_NUM_GROUPS; ++gi) {
-        if (cfg[gi].lr == 0.0 || o->size[gi] == 0) continue;
+        if (cfg[gi].lr < 0.0 || o->size[gi] == 0) continue;
         ++o->step[gi];
         launch_adam_group(gi, sd, scene->geom.as<double>(), scene->sh.as<float>(), scene->table.as<float>(),
                           scene->w1.as<float>(), scene->w2.as<float>(), scene->w3.as<float>(), *g, o->m[gi].as<double>(),
-                          o->v[gi].as<double>(), cfg[gi], o->step[gi], s);
+                          o->v[gi].as<double>(), gi >= NX_GROUP_SH_DC ? o->master[gi].as<double>() : nullptr, cfg[gi],
+                          o->step[gi], s);
     }
     NX_CUDA(c, cudaGetLastError());
     return NX_OK;
@@ -1256,9 +1334,11 @@ constexpr int kRowWidth[7] = {3, 4, 2, 1, 2, 3, 45};  // per-nexel Adam groups (
 
 // Rebuilds the scene (and the optimizer's per-nexel rows) in the layout of n_new nexels
 // from new_to_old (device); geometry rows from geom_new when given (densify) else
-// gathered; SH gathered unless sh_done.
+// gathered; SH gathered unless sh_done. Moments follow new_to_old (-1: fresh zeros,
+// adam_remap_rows); the SH masters follow src_rows (the row each new row's values come
+// from: a split child's parent), new_to_old when null.
 int apply_row_map(nx_ctx* c, nx_scene* scene, nx_optimizer* opt, int64_t n_new, const int32_t* n2o,
-                  DevBuf* geom_new, bool sh_done, cudaStream_t s) {
+                  DevBuf* geom_new, bool sh_done, cudaStream_t s, const int32_t* src_rows = nullptr) {
     const int64_t n = scene->n;
     DevBuf g2, sh2;
     if (!geom_new) {
@@ -1279,11 +1359,19 @@ int apply_row_map(nx_ctx* c, nx_scene* scene, nx_optimizer* opt, int64_t n_new, 
             NX_CUDA(c, v2.ensure(bytes));
             launch_gather_rows_f64(opt->m[gi].as<double>(), m2.as<double>(), n_new, kRowWidth[gi], n2o, s);
             launch_gather_rows_f64(opt->v[gi].as<double>(), v2.as<double>(), n_new, kRowWidth[gi], n2o, s);
+            DevBuf p2;
+            if (gi >= NX_GROUP_SH_DC) {
+                NX_CUDA(c, p2.ensure(bytes));
+                launch_gather_rows_f64(opt->master[gi].as<double>(), p2.as<double>(), n_new, kRowWidth[gi],
+                                       src_rows ? src_rows : n2o, s);
+            }
             NX_CUDA(c, cudaStreamSynchronize(s));
             std::swap(opt->m[gi], m2);
             std::swap(opt->v[gi], v2);
+            if (gi >= NX_GROUP_SH_DC) std::swap(opt->master[gi], p2);
             m2.release();
             v2.release();
+            p2.release();
             opt->size[gi] = n_new * kRowWidth[gi];
         }
         opt->n = n_new;
@@ -1380,7 +1468,15 @@ int nx_scene_densify_split(nx_ctx* c, nx_scene* scene, nx_optimizer* opt, const 
     launch_split_children(g2.as<double>(), n_new, scene->geom.as<double>(), n, sh2.as<float>(), d_par.as<int32_t>(),
                           allowed, map.as<int32_t>(), s);
     std::swap(scene->sh, sh2);
-    int st = apply_row_map(c, scene, opt, n_new, map.as<int32_t>(), &g2, true, s);
+    DevBuf src;  // the SH masters' source rows: kept rows themselves, a child its parent
+    if (opt) {
+        std::vector<int32_t> h(static_cast<size_t>(n_new));
+        for (int64_t i = 0; i < n; ++i) h[i] = static_cast<int32_t>(i);
+        for (int64_t r = 0; r < allowed; ++r) h[n + r] = parents[r];
+        NX_CUDA(c, src.ensure(n_new * sizeof(int32_t)));
+        NX_CUDA(c, cudaMemcpy(src.p, h.data(), n_new * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    int st = apply_row_map(c, scene, opt, n_new, map.as<int32_t>(), &g2, true, s, opt ? src.as<int32_t>() : nullptr);
     if (st) return st;
     if (new_to_old)
         NX_CUDA(c, cudaMemcpyAsync(new_to_old, map.p, n_new * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));

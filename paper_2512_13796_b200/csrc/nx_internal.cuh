@@ -237,9 +237,15 @@ int launch_losses_backward(const SceneDev& scene, const FrameDev& fb, const doub
 
 // ---------------------------------------------------------------- Adam (nx_adam.cu)
 void adam_group_sizes(const SceneDev& sc, int64_t* sizes);
+// master: the group's fp64 master values (groups 5..10; nullptr: step the fp32 values)
 void launch_adam_group(int group, const SceneDev& sc, double* geom, float* sh, float* table, float* w1, float* w2,
-                       float* w3, const nx_grads& g, double* m, double* v, const nx_adam_config& cfg, int64_t step,
-                       cudaStream_t s);
+                       float* w3, const nx_grads& g, double* m, double* v, double* master, const nx_adam_config& cfg,
+                       int64_t step, cudaStream_t s);
+// a group's values <-> its row layout (rows: device, the group's size)
+void launch_group_io(int group, const SceneDev& sc, double* geom, float* sh, float* table, float* w1, float* w2,
+                     float* w3, double* rows, bool to_rows, cudaStream_t s);
+// err[p] = sum_c |final - gt| / 3 (trainer.cpp:288-295)
+void launch_pixel_error(const float* final_img, const double* gt, int64_t npix, double* err, cudaStream_t s);
 
 // ---------------------------------------------------------------- density control (nx_density.cu)
 void launch_prune_flags(const double* geom, int64_t n, double min_opacity, int32_t* flags, cudaStream_t s);

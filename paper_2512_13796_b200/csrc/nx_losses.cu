@@ -314,7 +314,23 @@ __global__ void terms_kernel(const LossArgs a) {
     *a.terms = t;
 }
 
+__global__ void pixel_error_kernel(const float* __restrict__ final_img, const double* __restrict__ gt, int64_t npix,
+                                   double* __restrict__ err) {
+    const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= npix) return;
+    double e = 0.0;
+    for (int c = 0; c < 3; ++c) e += fabs(static_cast<double>(final_img[p * 3 + c]) - gt[p * 3 + c]);
+    err[p] = e / 3.0;
+}
+
 }  // namespace
+
+void launch_pixel_error(const float* final_img, const double* gt, int64_t npix, double* err, cudaStream_t s) {
+    if (npix <= 0) return;
+    count_launch();
+    pixel_error_kernel<<<static_cast<unsigned>((npix + kThreads - 1) / kThreads), kThreads, 0, s>>>(final_img, gt,
+                                                                                                   npix, err);
+}
 
 size_t losses_scratch_bytes(int64_t npix) { return sizeof(LossSums) + 256 + static_cast<size_t>(33) * npix * sizeof(double); }
 

@@ -35,3 +35,32 @@ def test_dropin_render_backward_matches_the_reference_in_the_same_library():
     print(r.stdout[-2000:], r.stderr[-2000:])
     assert r.returncode == 0
     assert "2 test cases, 0 failed" in r.stdout
+
+
+TRAIN_REF = os.path.join(ROOT, "build", "dropin", "test_train_dropin")
+
+
+@pytest.mark.skipif(not os.path.exists(TRAIN_REF), reason="drop-in train test binary not built (make dropin)")
+def test_reference_test_train_suite_passes_on_the_dropin():
+    # proj/tests/test_train.cpp, unmodified, against the GPU-backed nexel::train
+    # (host/trainer_b200.cpp): config parsing, initialisation, iterations moving every
+    # group, run-to-run determinism (bit-identical scenes, moments and checkpoint
+    # bytes), the densify / prune window, eval hooks, mean_psnr and input rejection
+    r = subprocess.run([TRAIN_REF], capture_output=True, text=True, timeout=900)
+    print(r.stdout[-3000:], r.stderr[-2000:])
+    assert r.returncode == 0
+    assert "10 test cases, 0 failed" in r.stdout
+
+
+TRAIN_CMP = os.path.join(ROOT, "build", "dropin", "test_dropin_train")
+
+
+@pytest.mark.skipif(not os.path.exists(TRAIN_CMP), reason="drop-in train comparison binary not built (make dropin)")
+def test_dropin_train_follows_the_reference_train():
+    # GPU nexel::train vs the reference's own train (nexel_ref_train, CPU renderer)
+    # in the same library: primitive counts per iteration, loss terms, final
+    # parameters, Adam steps; bit-reproducible; zero iterations = the initialisation
+    r = subprocess.run([TRAIN_CMP], capture_output=True, text=True, timeout=1800)
+    print(r.stdout[-3000:], r.stderr[-2000:])
+    assert r.returncode == 0
+    assert "4 test cases, 0 failed" in r.stdout
