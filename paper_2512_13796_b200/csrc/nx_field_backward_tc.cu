@@ -72,39 +72,15 @@ constexpr int kSmemM = kOffTmem + 8;
 static_assert(kSmemM <= 227 * 1024, "fits one CTA per SM");
 
 // ---------------------------------------------------------------- G: features
-// The ReLU masks and the SH clamp mask decide which gradients pass (mlp.cpp:67-68,
-// 79-80; sh.hpp:70). They come from an exact fp32 forward on the CUDA cores here, so
-// that they agree with the reference's fp64 forward except for pre-activations within
-// ~1e-7 of zero; the split-bf16 tensor-core forward (~1e-5) would flip ~1e-4 of them.
-// A mask bit is "ambiguous" when its fp32 pre-activation lies within the fp32 error
-// bound (2^-15 ||a||_1 max|w|) of the threshold; those slots are listed and re-decided
-// in fp64 by mask_fp64_kernel, so the masks agree with the reference's fp64 forward.
+// Per slot: the 16-level features F (grid_lookup) and, from the same gathered corners,
+// the per-level sums the scatter's position / fade gradient needs (level_sums: the
+// un-faded features and the trilinear Jacobian, 8 floats per level, level-major SoA
+// jbuf[(l * 8 + k) * total + slot]), so that the table is gathered once per backward.
+// The masks come next, from mask_tc_kernel.
 __global__ void __launch_bounds__(128) features_kernel(const FieldBwdArgs a, const TcConst cst, float* __restrict__ fbuf,
-                                                       int64_t total, int32_t* __restrict__ amb_list,
-                                                       int32_t* __restrict__ amb_count) {
-    __shared__ float sW[kHid * kIn + kHid * kHid + kOut * kHid];
-    __shared__ float sMax[kHid + kHid + 1];
-    float* sW1 = sW;
-    float* sW2 = sW1 + kHid * kIn;
-    float* sW3 = sW2 + kHid * kHid;
-    for (int e = threadIdx.x; e < kHid * kIn; e += blockDim.x) sW1[e] = __ldg(a.scene.w1 + e);
-    for (int e = threadIdx.x; e < kHid * kHid; e += blockDim.x) sW2[e] = __ldg(a.scene.w2 + e);
-    for (int e = threadIdx.x; e < kOut * kHid; e += blockDim.x) sW3[e] = __ldg(a.scene.w3 + e);
-    __syncthreads();
-    for (int o = threadIdx.x; o < 2 * kHid + 1; o += blockDim.x) {
-        float m = 0.f;
-        if (o < kHid)
-            for (int i = 0; i < kIn; ++i) m = fmaxf(m, fabsf(sW1[o * kIn + i]));
-        else if (o < 2 * kHid)
-            for (int i = 0; i < kHid; ++i) m = fmaxf(m, fabsf(sW2[(o - kHid) * kHid + i]));
-        else
-            for (int i = 0; i < kOut * kHid; ++i) m = fmaxf(m, fabsf(sW3[i]));
-        sMax[o] = m;
-    }
-    __syncthreads();
+                                                       float* __restrict__ jbuf, int64_t total) {
     const int64_t sl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (sl >= total) return;
-    uint32_t masks[5] = {0u, 0u, 0u, 0u, 0u};
     float feats[kIn];
 #pragma unroll
     for (int i = 0; i < kIn; ++i) feats[i] = 0.f;
@@ -129,71 +105,29 @@ __global__ void __launch_bounds__(128) features_kernel(const FieldBwdArgs a, con
                 const float2 g = interp(cur);
                 feats[2 * l] = g.x;
                 feats[2 * l + 1] = g.y;
+                float js[8];
+                level_sums(cur, js);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) jbuf[static_cast<int64_t>(l * 8 + k) * total + sl] = js[k];
                 if (l + 1 < kLevels) cur = nxt;
             }
         } else {
 #pragma unroll
             for (int l = 0; l < kLevels; ++l) {
-                const float2 g = interp(fetch_level<false>(l, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight));
+                const LevelFetch f = fetch_level<false>(l, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
+                const float2 g = interp(f);
                 feats[2 * l] = g.x;
                 feats[2 * l + 1] = g.y;
+                float js[8];
+                level_sums(f, js);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) jbuf[static_cast<int64_t>(l * 8 + k) * total + sl] = js[k];
             }
         }
-    }
-    if (a.fb.ids[sl] >= 0) {
-        // exact fp32 forward (TextureMlp::forward, mlp.cpp:24-43) for the masks only
-        float h1[kHid], h2[kHid];
-        bool amb = false;
-        float n1 = 0.f, n2 = 0.f, n3 = 0.f;
-#pragma unroll
-        for (int i = 0; i < kIn; ++i) n1 += fabsf(feats[i]);
-#pragma unroll 4
-        for (int o = 0; o < kHid; ++o) {
-            float acc = 0.f;
-#pragma unroll
-            for (int i = 0; i < kIn; ++i) acc = fmaf(sW1[o * kIn + i], feats[i], acc);
-            if (acc > 0.f) masks[o >> 5] |= 1u << (o & 31);
-            amb |= fabsf(acc) <= 3.05e-5f * n1 * sMax[o];
-            h1[o] = fmaxf(acc, 0.f);
-            n2 += h1[o];
-        }
-#pragma unroll 4
-        for (int o = 0; o < kHid; ++o) {
-            float acc = 0.f;
-#pragma unroll
-            for (int i = 0; i < kHid; ++i) acc = fmaf(sW2[o * kHid + i], h1[i], acc);
-            if (acc > 0.f) masks[2 + (o >> 5)] |= 1u << (o & 31);
-            amb |= fabsf(acc) <= 3.05e-5f * n2 * sMax[kHid + o];
-            h2[o] = fmaxf(acc, 0.f);
-            n3 += h2[o];
-        }
-        const int64_t pix = sl / a.fb.K;
-        double dir[3];
-        pixel_dir(a.cam, static_cast<int>(pix % a.cam.W) + 0.5, static_cast<int>(pix / a.cam.W) + 0.5, dir);
-        float b[16];
-        sh_basis_f32(static_cast<float>(dir[0]), static_cast<float>(dir[1]), static_cast<float>(dir[2]), b);
-        float c3[3] = {0.5f, 0.5f, 0.5f};
-#pragma unroll 1
-        for (int o = 0; o < kOut; ++o) {
-            float acc = 0.f;
-#pragma unroll
-            for (int i = 0; i < kHid; ++i) acc = fmaf(sW3[o * kHid + i], h2[i], acc);
-            c3[o % 3] = fmaf(acc, b[o / 3], c3[o % 3]);
-        }
-        masks[4] = (c3[0] >= 0.f ? 1u : 0u) | (c3[1] >= 0.f ? 2u : 0u) | (c3[2] >= 0.f ? 4u : 0u);
-        float bsum = 0.f;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) bsum += fabsf(b[k]);
-        const float bound3 = 6.1e-5f * n3 * sMax[2 * kHid] * bsum;
-        amb |= fabsf(c3[0]) <= bound3 || fabsf(c3[1]) <= bound3 || fabsf(c3[2]) <= bound3;
-        if (amb) amb_list[atomicAdd(amb_count, 1)] = static_cast<int32_t>(sl);
     }
     float4* dst = reinterpret_cast<float4*>(fbuf + sl * kStride);
 #pragma unroll
     for (int q = 0; q < kIn / 4; ++q) dst[q] = make_float4(feats[4 * q], feats[4 * q + 1], feats[4 * q + 2], feats[4 * q + 3]);
-    dst[kIn / 4] = make_float4(__uint_as_float(masks[0]), __uint_as_float(masks[1]), __uint_as_float(masks[2]),
-                               __uint_as_float(masks[3]));
-    dst[kIn / 4 + 1] = make_float4(__uint_as_float(masks[4]), 0.f, 0.f, 0.f);
 }
 
 // The listed slots' masks re-decided with the reference's fp64 forward: grid_lookup
@@ -577,6 +511,228 @@ __global__ void __launch_bounds__(kThreadsM, 1) mlp_bwd_tc_kernel(const FieldBwd
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
 
+// ---------------------------------------------------------------- M0: ReLU / clamp masks on tcgen05
+// The masks (which ReLU units and SH-clamped channels pass gradients, mlp.cpp:67-68,
+// 79-80; sh.hpp:70) from a tensor-core forward of the features F at fp32 accuracy:
+// every operand is split three ways (x = h + m + l in bf16, 24 significant bits) and
+// each product is formed from the six terms above 2^-24 (hh, hm, mh, hl, lh, mm), so
+// the pre-activations carry the error of an fp32 forward. As before (an fp32 CUDA-core
+// forward, profiles/r01), a unit whose pre-activation lies within 2^-15 ||a||_1 max|w_o|
+// of the threshold (SH: 2^-14 ||h2||_1 max|w3| sum|b|) is "ambiguous": the slot is
+// listed and mask_fp64_kernel re-decides it with the reference's fp64 forward.
+struct Opnd3 {
+    uint32_t p[3];  // hi, mid, lo copies
+    uint32_t lbo, sbo, step;
+};
+constexpr int kM3W1 = 0;                                // 3 x [64][32]
+constexpr int kM3W2 = kM3W1 + 3 * kHid * kIn * 2;       // 3 x [64][64]
+constexpr int kM3W3 = kM3W2 + 3 * kHid * kHid * 2;      // 3 x [48][64]
+constexpr int kM3A = kM3W3 + 3 * kOut * kHid * 2;       // 3 x [128][64] (F in columns 0..31)
+constexpr int kM3Max = kM3A + 3 * kRows * kHid * 2;     // per-row weight maxima
+constexpr int kM3Bar = kM3Max + 1024;
+constexpr int kM3Tmem = kM3Bar + 8;
+constexpr int kSmemMask = kM3Tmem + 8;
+constexpr uint32_t kMaskTmemCols = 64;
+static_assert(kSmemMask <= 113 * 1024, "two CTAs per SM");
+
+// 8 consecutive K values as three bf16 parts (exact re-expansion of each part by shifts)
+__device__ __forceinline__ void store_split3x8(uint8_t* smem, int off, int part_bytes, uint32_t byte_off,
+                                               const float* x) {
+    uint32_t h[4], m[4], l[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        h[i] = pack_bf16(x[2 * i], x[2 * i + 1]);
+        const float r0 = x[2 * i] - __uint_as_float(h[i] << 16), r1 = x[2 * i + 1] - __uint_as_float(h[i] & 0xffff0000u);
+        m[i] = pack_bf16(r0, r1);
+        l[i] = pack_bf16(r0 - __uint_as_float(m[i] << 16), r1 - __uint_as_float(m[i] & 0xffff0000u));
+    }
+    *reinterpret_cast<uint4*>(smem + off + byte_off) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(smem + off + part_bytes + byte_off) = make_uint4(m[0], m[1], m[2], m[3]);
+    *reinterpret_cast<uint4*>(smem + off + 2 * part_bytes + byte_off) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+__device__ __forceinline__ Opnd3 kmaj3(uint8_t* smem, int off, int part_bytes, int C) {
+    const uint32_t b = smem_u32(smem + off);
+    return {{b, b + static_cast<uint32_t>(part_bytes), b + 2u * static_cast<uint32_t>(part_bytes)},
+            128u, static_cast<uint32_t>(16 * C), 256u};
+}
+
+__device__ __forceinline__ void issue_mma3(uint32_t dtm, const Opnd3& A, const Opnd3& B, int ksteps, uint32_t idesc) {
+    constexpr int kTerms[6][2] = {{0, 0}, {0, 1}, {1, 0}, {0, 2}, {2, 0}, {1, 1}};
+    for (int s = 0; s < ksteps; ++s) {
+#pragma unroll
+        for (int t = 0; t < 6; ++t) {
+            const uint64_t da = smem_desc(A.p[kTerms[t][0]] + s * A.step, A.lbo, A.sbo);
+            const uint64_t db = smem_desc(B.p[kTerms[t][1]] + s * B.step, B.lbo, B.sbo);
+            mma_bf16(dtm, da, db, idesc, (s > 0 || t > 0) ? 1u : 0u);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreadsM) mask_tc_kernel(const FieldBwdArgs a, float* __restrict__ fbuf,
+                                                            int64_t total, int64_t n_tiles,
+                                                            int32_t* __restrict__ amb_list,
+                                                            int32_t* __restrict__ amb_count) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t bar = smem_u32(smem + kM3Bar);
+    const float* wsrc[3] = {a.scene.w1, a.scene.w2, a.scene.w3};
+    const int wrows[3] = {kHid, kHid, kOut}, wk[3] = {kIn, kHid, kHid}, woff[3] = {kM3W1, kM3W2, kM3W3};
+#pragma unroll 1
+    for (int m = 0; m < 3; ++m)
+        for (int e = tid; e < wrows[m] * wk[m] / 8; e += blockDim.x) {
+            const int n = e / (wk[m] / 8), c = e % (wk[m] / 8);
+            float x[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = __ldg(wsrc[m] + n * wk[m] + c * 8 + i);
+            store_split3x8(smem, woff[m], wrows[m] * wk[m] * 2, kmajor_off(n, c * 8, wk[m]), x);
+        }
+    float* sMax = reinterpret_cast<float*>(smem + kM3Max);  // [0,64) w1 rows, [64,128) w2 rows, 128: w3
+    for (int o = tid; o < 2 * kHid + 1; o += blockDim.x) {
+        float mx = 0.f;
+        if (o < kHid)
+            for (int i = 0; i < kIn; ++i) mx = fmaxf(mx, fabsf(__ldg(a.scene.w1 + o * kIn + i)));
+        else if (o < 2 * kHid)
+            for (int i = 0; i < kHid; ++i) mx = fmaxf(mx, fabsf(__ldg(a.scene.w2 + (o - kHid) * kHid + i)));
+        else
+            for (int i = 0; i < kOut * kHid; ++i) mx = fmaxf(mx, fabsf(__ldg(a.scene.w3 + i)));
+        sMax[o] = mx;
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem + kM3Tmem)),
+                     "r"(kMaskTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 32) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + kM3Tmem);
+    const uint32_t tD = tmem + (static_cast<uint32_t>(32 * warp) << 16);
+    constexpr int kAPart = kRows * kHid * 2;
+    const Opnd3 A = kmaj3(smem, kM3A, kAPart, kHid);
+    const Opnd3 W1k = kmaj3(smem, kM3W1, kHid * kIn * 2, kIn), W2k = kmaj3(smem, kM3W2, kHid * kHid * 2, kHid),
+                W3k = kmaj3(smem, kM3W3, kOut * kHid * 2, kHid);
+    constexpr uint32_t kI64 = idesc_bf16_f32(kRows, 64), kI48 = idesc_bf16_f32(kRows, 48);
+    const float max3 = sMax[2 * kHid];
+    uint32_t phase = 0;
+    const int row = tid;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int64_t sl = tile * kRows + row;
+        const bool valid = sl < total && a.fb.ids[sl] >= 0;
+        float x[kIn];
+        float n1 = 0.f;
+        if (valid) {
+            const float4* src = reinterpret_cast<const float4*>(fbuf + sl * kStride);
+#pragma unroll
+            for (int q = 0; q < kIn / 4; ++q) {
+                const float4 v = src[q];
+                x[4 * q] = v.x;
+                x[4 * q + 1] = v.y;
+                x[4 * q + 2] = v.z;
+                x[4 * q + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < kIn; ++i) x[i] = 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < kIn; ++i) n1 += fabsf(x[i]);
+#pragma unroll
+        for (int c = 0; c < kIn / 8; ++c) store_split3x8(smem, kM3A, kAPart, kmajor_off(row, 8 * c, kHid), x + 8 * c);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            issue_mma3(tmem, A, W1k, kIn / 16, kI64);
+            mma_commit(bar);
+        }
+        // the ray's SH basis while layer 1 runs
+        float b[16];
+        {
+            double dir[3] = {0.0, 0.0, 1.0};
+            if (valid) {
+                const int64_t pix = sl / a.fb.K;
+                pixel_dir(a.cam, static_cast<int>(pix % a.cam.W) + 0.5, static_cast<int>(pix / a.cam.W) + 0.5, dir);
+            }
+            sh_basis_f32(static_cast<float>(dir[0]), static_cast<float>(dir[1]), static_cast<float>(dir[2]), b);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+        uint32_t m1[2] = {0u, 0u}, m2[2] = {0u, 0u};
+        bool amb = false;
+        float nin = n1;
+#pragma unroll
+        for (int layer = 0; layer < 2; ++layer) {
+            const float* rmax = sMax + layer * kHid;
+            const float scale = 3.05e-5f * nin;
+            float nout = 0.f;
+#pragma unroll
+            for (int c = 0; c < kHid / 16; ++c) {
+                float v[16];
+                tmem_ld16(tD + 16 * c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int o = 16 * c + i;
+                    if (v[i] > 0.f) (layer == 0 ? m1 : m2)[o >> 5] |= 1u << (o & 31);
+                    amb |= fabsf(v[i]) <= scale * rmax[o];
+                    v[i] = fmaxf(v[i], 0.f);
+                    nout += v[i];
+                }
+                store_split3x8(smem, kM3A, kAPart, kmajor_off(row, 16 * c, kHid), v);
+                store_split3x8(smem, kM3A, kAPart, kmajor_off(row, 16 * c + 8, kHid), v + 8);
+            }
+            nin = nout;
+            fence_async_smem();
+            tc_fence_before();
+            __syncthreads();
+            if (tid == 0) {
+                tc_fence_after();
+                if (layer == 0) issue_mma3(tmem, A, W2k, kHid / 16, kI64);
+                else issue_mma3(tmem, A, W3k, kHid / 16, kI48);
+                mma_commit(bar);
+            }
+            mbar_wait(bar, phase);
+            phase ^= 1;
+            tc_fence_after();
+        }
+        // eval_sh_cached's clamp (sh.hpp:61-73): 0.5 + sum_k Y[3k + c] b_k >= 0
+        float c3[3] = {0.5f, 0.5f, 0.5f}, bsum = 0.f;
+#pragma unroll
+        for (int c = 0; c < kOut / 16; ++c) {
+            float v[16];
+            tmem_ld16(tD + 16 * c, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int o = 16 * c + i;
+                c3[o % 3] = fmaf(v[i], b[o / 3], c3[o % 3]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) bsum += fabsf(b[k]);
+        const float bound3 = 6.1e-5f * nin * max3 * bsum;
+        const uint32_t shm = (c3[0] >= 0.f ? 1u : 0u) | (c3[1] >= 0.f ? 2u : 0u) | (c3[2] >= 0.f ? 4u : 0u);
+        amb |= fabsf(c3[0]) <= bound3 || fabsf(c3[1]) <= bound3 || fabsf(c3[2]) <= bound3;
+        if (valid) {
+            float4* dst = reinterpret_cast<float4*>(fbuf + sl * kStride);
+            dst[kIn / 4] = make_float4(__uint_as_float(m1[0]), __uint_as_float(m1[1]), __uint_as_float(m2[0]),
+                                       __uint_as_float(m2[1]));
+            dst[kIn / 4 + 1] = make_float4(__uint_as_float(shm), 0.f, 0.f, 0.f);
+            if (amb) amb_list[atomicAdd(amb_count, 1)] = static_cast<int32_t>(sl);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kMaskTmemCols));
+}
+
 // Sums the CTA partials in CTA order (deterministic) into the fp64 weight gradients.
 __global__ void reduce_wgrads_kernel(const float* __restrict__ partials, int n_parts, double* g_w1, double* g_w2,
                                      double* g_w3) {
@@ -591,9 +747,9 @@ __global__ void reduce_wgrads_kernel(const float* __restrict__ partials, int n_p
 
 // ---------------------------------------------------------------- S: grid_lookup_backward
 // grid_lookup_backward (hash_grid.hpp:85-124) in two phases: (1) the position / fade
-// gradient, which needs the table values — gathered two levels deep in flight, no
-// atomics in between; (2) the table gradients, which need only the corner rows and
-// weights — into exact accumulators (nx_xacc.cuh), so that the table gradients do not
+// gradient from the per-level sums the features pass kept (jbuf: no second table
+// gather); (2) the table gradients, which need only the corner rows and weights — into
+// exact accumulators (nx_xacc.cuh), so that the table gradients do not
 // depend on the order of the atomics. Neighbouring slots of a warp share corner rows at
 // every level but the very finest (a warp covers 16 adjacent pixels), so the lanes that
 // hit the same row (__match_any_sync) are summed first, in lane order, and their leader
@@ -601,40 +757,32 @@ __global__ void reduce_wgrads_kernel(const float* __restrict__ partials, int n_p
 template <bool kSmall>
 __device__ __forceinline__ void scatter_levels(const FieldBwdArgs& a, const TcConst& cst, bool valid, double x0,
                                                double x1, double x2, float ft, const float* g, double t, double* dx,
-                                               double& dt, const Xacc& tacc, float2* __restrict__ wsh) {
+                                               double& dt, const Xacc& tacc, float2* __restrict__ wsh,
+                                               const float* __restrict__ jbuf, int64_t total, int64_t slot) {
     const uint32_t T = 1u << a.scene.field.log2_table, mask = T - 1u;
-    const float2* tab = reinterpret_cast<const float2*>(a.scene.table);
     const int lane = threadIdx.x & 31;
-    // ---- phase 1: d_x, d_t
-    LevelFetch cur = fetch_level<kSmall>(0, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
+    // ---- phase 1: d_x, d_t from the kept sums: dL/dp_d = dw (g . J_d), dL/d(dw) = g . S
+    if (valid) {
+#pragma unroll 4
+        for (int l = 0; l < kLevels; ++l) {
+            float js[8];
 #pragma unroll
-    for (int l = 0; l < kLevels; ++l) {
-        LevelFetch nxt;
-        if (l + 1 < kLevels) nxt = fetch_level<kSmall>(l + 1, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
-        const float g0 = g[2 * l], g1 = g[2 * l + 1];
-        const float wx[2] = {1.0f - cur.fr0, cur.fr0}, wy[2] = {1.0f - cur.fr1, cur.fr1},
-                    wz[2] = {1.0f - cur.fr2, cur.fr2};
-        float dp0 = 0.f, dp1 = 0.f, dp2 = 0.f, d_dw = 0.f;
-#pragma unroll
-        for (int ci = 0; ci < 8; ++ci) {
-            const float ax = wx[ci & 1], ay = wy[(ci >> 1) & 1], az = wz[(ci >> 2) & 1];
-            const float gdotf = g0 * cur.v[ci].x + g1 * cur.v[ci].y;
-            const float updotf = gdotf * cur.dw;
-            dp0 += updotf * ((ci & 1) ? ay * az : -(ay * az));
-            dp1 += updotf * ((ci & 2) ? ax * az : -(ax * az));
-            dp2 += updotf * ((ci & 4) ? ax * ay : -(ax * ay));
-            d_dw += gdotf * (ax * ay * az);
+            for (int k = 0; k < 8; ++k) js[k] = __ldg(jbuf + static_cast<int64_t>(l * 8 + k) * total + slot);
+            const float g0 = g[2 * l], g1 = g[2 * l + 1];
+            const float dw = level_fade(l, cst, ft, a.st.no_downweight);
+            const float dp0 = dw * (g0 * js[2] + g1 * js[5]), dp1 = dw * (g0 * js[3] + g1 * js[6]),
+                        dp2 = dw * (g0 * js[4] + g1 * js[7]);
+            const float d_dw = g0 * js[0] + g1 * js[1];
+            const double sl = cst.level_scale[l];
+            dx[0] += sl * dp0;
+            dx[1] += sl * dp1;
+            dx[2] += sl * dp2;
+            if (!a.st.no_downweight) {
+                // downweight_grad_t via the cached factor (hash_grid.hpp:117-121)
+                const double r = a.cam.fx / (sl * t);
+                dt += static_cast<double>(d_dw) * (static_cast<double>(dw) - 1.0) * r * r / (M_PI * t);
+            }
         }
-        const double sl = cst.level_scale[l];
-        dx[0] += sl * dp0;
-        dx[1] += sl * dp1;
-        dx[2] += sl * dp2;
-        if (!a.st.no_downweight) {
-            // downweight_grad_t via the cached factor (hash_grid.hpp:117-121)
-            const double r = a.cam.fx / (sl * t);
-            dt += static_cast<double>(d_dw) * (static_cast<double>(cur.dw) - 1.0) * r * r / (M_PI * t);
-        }
-        if (l + 1 < kLevels) cur = nxt;
     }
     // ---- phase 2: table gradients dL/dtable[row][f] += g[f] * dw * corner_w (hash_grid.hpp:99-103)
 #pragma unroll 1
@@ -667,7 +815,7 @@ __device__ __forceinline__ void scatter_levels(const FieldBwdArgs& a, const TcCo
 
 __global__ void __launch_bounds__(128) scatter_kernel(const FieldBwdArgs a, const TcConst cst,
                                                       const float* __restrict__ fbuf, int64_t total,
-                                                      const Xacc tacc) {
+                                                      const float* __restrict__ jbuf, const Xacc tacc) {
     const int64_t sl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool in = sl < total;
     const bool valid = in && a.fb.ids[sl] >= 0;
@@ -703,9 +851,11 @@ __global__ void __launch_bounds__(128) scatter_kernel(const FieldBwdArgs a, cons
     double dx[3] = {0.0, 0.0, 0.0}, dt = 0.0;
     const bool small = fmax(fabs(x0), fmax(fabs(x1), fabs(x2))) * cst.level_scale[kLevels - 1] < 1073741824.0;
     if (__all_sync(0xffffffffu, small))
-        scatter_levels<true>(a, cst, valid, x0, x1, x2, ft, g, t, dx, dt, tacc, wsh + (threadIdx.x & ~31));
+        scatter_levels<true>(a, cst, valid, x0, x1, x2, ft, g, t, dx, dt, tacc, wsh + (threadIdx.x & ~31), jbuf, total,
+                             sl);
     else
-        scatter_levels<false>(a, cst, valid, x0, x1, x2, ft, g, t, dx, dt, tacc, wsh + (threadIdx.x & ~31));
+        scatter_levels<false>(a, cst, valid, x0, x1, x2, ft, g, t, dx, dt, tacc, wsh + (threadIdx.x & ~31), jbuf, total,
+                              sl);
     if (in) a.d_t_slot[sl] = valid ? dt + (dx[0] * dir[0] + dx[1] * dir[1] + dx[2] * dir[2]) : 0.0;
 }
 
@@ -756,6 +906,14 @@ int launch_field_backward_tc(const FieldBwdArgs& a, cudaStream_t s) {
     }
     const int64_t tneed = static_cast<int64_t>(kLevels) * (int64_t(1) << a.scene.field.log2_table) * 2;
     if (int st = sc.table_acc(tneed, s)) return st;
+    const size_t jneed = static_cast<size_t>(total) * kLevels * 8;
+    if (jneed > sc.jcap) {
+        if (sc.jbuf) cudaFree(sc.jbuf);
+        sc.jbuf = nullptr;
+        sc.jcap = 0;
+        if (cudaMalloc(&sc.jbuf, jneed * sizeof(float)) != cudaSuccess) return NX_OUT_OF_MEMORY;
+        sc.jcap = jneed;
+    }
     if (pneed > sc.pcap) {
         if (sc.parts) cudaFree(sc.parts);
         sc.parts = nullptr;
@@ -770,15 +928,18 @@ int launch_field_backward_tc(const FieldBwdArgs& a, cudaStream_t s) {
         cst.inv_level_scale[l] = static_cast<float>(1.0 / scale);
     }
     const unsigned blocks = static_cast<unsigned>((total + 127) / 128);
-    count_launch(5);
+    count_launch(6);
     cudaMemsetAsync(sc.amb, 0, sizeof(int32_t), s);
-    features_kernel<<<blocks, 128, 0, s>>>(a, cst, sc.fbuf, total, sc.amb + 1, sc.amb);
+    features_kernel<<<blocks, 128, 0, s>>>(a, cst, sc.fbuf, sc.jbuf, total);
+    cudaFuncSetAttribute(mask_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMask);
+    mask_tc_kernel<<<static_cast<unsigned>(std::min<int64_t>(n_tiles, 2 * sms)), kThreadsM, kSmemMask, s>>>(
+        a, sc.fbuf, total, n_tiles, sc.amb + 1, sc.amb);
     mask_fp64_kernel<<<2 * sms, 128, 0, s>>>(a, sc.amb + 1, sc.amb, sc.fbuf);
     cudaFuncSetAttribute(mlp_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemM);
     mlp_bwd_tc_kernel<<<grid_m, kThreadsM, kSmemM, s>>>(a, sc.fbuf, sc.parts, total, n_tiles);
     reduce_wgrads_kernel<<<(kWGrads + 255) / 256, 256, 0, s>>>(sc.parts, grid_m, a.g_w1, a.g_w2, a.g_w3);
     const Xacc tacc{sc.tx, tneed};
-    scatter_kernel<<<blocks, 128, 0, s>>>(a, cst, sc.fbuf, total, tacc);
+    scatter_kernel<<<blocks, 128, 0, s>>>(a, cst, sc.fbuf, total, sc.jbuf, tacc);
     count_launch();
     take_table_kernel<<<8 * sms, 256, 0, s>>>(a.g_table, tacc);
     return NX_OK;

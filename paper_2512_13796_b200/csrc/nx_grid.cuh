@@ -91,6 +91,38 @@ __device__ __forceinline__ float2 interp(const LevelFetch& f) {
     return make_float2(g0 * f.dw, g1 * f.dw);
 }
 
+// Per level, what the backward's position / fade gradient needs from the gathered
+// corners (hash_grid.hpp:104-121), so that the scatter does not gather the table again:
+// o[0..1] = sum_c w_c T_c (the un-faded features), o[2 + 3 f + d] = sum_c (dw_c / dp_d) T_c,f
+// (the trilinear Jacobian of feature f along lattice axis d).
+__device__ __forceinline__ void level_sums(const LevelFetch& f, float* o) {
+    const float wx[2] = {1.0f - f.fr0, f.fr0}, wy[2] = {1.0f - f.fr1, f.fr1}, wz[2] = {1.0f - f.fr2, f.fr2};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = 0.f;
+#pragma unroll
+    for (int ci = 0; ci < 8; ++ci) {
+        const float ax = wx[ci & 1], ay = wy[(ci >> 1) & 1], az = wz[(ci >> 2) & 1];
+        const float w = ax * ay * az;
+        const float d0 = (ci & 1) ? ay * az : -(ay * az), d1 = (ci & 2) ? ax * az : -(ax * az),
+                    d2 = (ci & 4) ? ax * ay : -(ax * ay);
+        o[0] += w * f.v[ci].x;
+        o[1] += w * f.v[ci].y;
+        o[2] += d0 * f.v[ci].x;
+        o[3] += d1 * f.v[ci].x;
+        o[4] += d2 * f.v[ci].x;
+        o[5] += d0 * f.v[ci].y;
+        o[6] += d1 * f.v[ci].y;
+        o[7] += d2 * f.v[ci].y;
+    }
+}
+
+// The level fade alone (downweight, hash_grid.hpp:28-31), as fetch_level computes it.
+__device__ __forceinline__ float level_fade(int l, const TcConst& cst, float ft, int no_downweight) {
+    if (no_downweight) return 1.0f;
+    const float r = ft * cst.inv_level_scale[l];
+    return 1.0f - __expf(-r * r * 0.15915494309189535f);
+}
+
 // The lattice cell of one level without the gathers: the 8 corner rows (already
 // masked to the table), the fractional position and the level fade. Used by the
 // field backward, which scatters gradients to these rows.

@@ -294,6 +294,8 @@ struct FieldBwdScratch {
     size_t wxcap = 0;
     float* parts = nullptr;
     size_t pcap = 0;
+    float* jbuf = nullptr;  // per-slot level sums (features pass -> scatter)
+    size_t jcap = 0;
     static int grow_zeroed(unsigned long long*& p, size_t& cap, size_t bytes, cudaStream_t s) {
         if (bytes <= cap && p) return NX_OK;
         if (p) cudaFree(p);
@@ -308,7 +310,7 @@ struct FieldBwdScratch {
     int weight_acc(int64_t m, cudaStream_t s) { return grow_zeroed(wx, wxcap, xacc_bytes(m), s); }
     void release() {
         for (void* p : {static_cast<void*>(fbuf), static_cast<void*>(amb), static_cast<void*>(tx),
-                        static_cast<void*>(wx), static_cast<void*>(parts)})
+                        static_cast<void*>(wx), static_cast<void*>(parts), static_cast<void*>(jbuf)})
             if (p) cudaFree(p);
         *this = FieldBwdScratch{};
     }
