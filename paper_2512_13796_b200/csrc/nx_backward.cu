@@ -188,7 +188,6 @@ __global__ void __launch_bounds__(kThreads, 2) composite_bwd_kernel(const Compos
     const double errp = (in_img && a.err_pixel) ? a.err_pixel[pix] : 0.0;
     const int n_act = a.err_pixel ? kActFields : kActFields - 1;
     const int n_sh = a.sh_degree >= 3 ? 16 : 1;
-    const int n_vals = kActFields + 3 * n_sh;  // accumulated values in use
     const Xacc acc = a.acc;
 
     double T = 1.0, P = 0.0;
@@ -362,10 +361,14 @@ __global__ void __launch_bounds__(kThreads, 2) composite_bwd_kernel(const Compos
                 g[kActFields + 2] = hh.rgb[2];
             }
             __syncwarp();
-            // ---- B3b. per primitive of the group: lane v sums value v over the pixels that hit
-            // it in lane order (SH values from the staged w dL/dfinal and the pixel's basis),
-            // then adds the warp sum to the primitive's exact accumulator
+            // ---- B3b. per primitive of the group, one pass over the pixels that hit it (lane
+            // order): lanes 0..15 sum the SH gradients of coefficient k = lane for the three
+            // channels (w dL/dfinal x basis_k of the pixel), lanes 16..31 the activated values
+            // lane - 16 (and lanes 16, 17 also values 16, 17); the warp sums go into the
+            // primitive's exact accumulators
             int cur = off;
+            const bool sh_lane = lane < 16;
+            const int av = lane - 16;  // activated value of an act lane (and av + 16 for lanes 16, 17)
 #pragma unroll 1
             for (int b = 0; b < sn; ++b) {
                 int my_e = -1;
@@ -376,22 +379,31 @@ __global__ void __launch_bounds__(kThreads, 2) composite_bwd_kernel(const Compos
                 const uint32_t hm = __ballot_sync(0xffffffffu, my_e >= 0);
                 if (!hm) continue;
                 const int64_t row = static_cast<int64_t>(sm.id[sb + b]) * kPrimAccVals;
-#pragma unroll 1
-                for (int r0 = 0; r0 < n_vals; r0 += 32) {  // warp-uniform rounds (shuffles inside)
-                    const int v = r0 + lane;
-                    const bool is_act = v < kActFields;
-                    const int sv = is_act ? 0 : v - kActFields;
-                    const int shk = sv / 3, shc = sv - 3 * (sv / 3);
-                    float sum = 0.f;
-                    for (uint32_t m = hm; m; m &= m - 1) {
-                        const int h = __ffs(m) - 1;
-                        const int eh = __shfl_sync(0xffffffffu, my_e, h);
-                        if (v < n_vals) {
-                            const float* g = sm.res[eh].g;
-                            sum += is_act ? g[v] : g[kActFields + shc] * sm.basis[h][shk];
-                        }
+                float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+                for (uint32_t m = hm; m; m &= m - 1) {
+                    const int h = __ffs(m) - 1;
+                    const int eh = __shfl_sync(0xffffffffu, my_e, h);
+                    const float* g = sm.res[eh].g;
+                    if (sh_lane) {
+                        const float bk = sm.basis[h][lane];
+                        s0 = fmaf(g[kActFields + 0], bk, s0);
+                        s1 = fmaf(g[kActFields + 1], bk, s1);
+                        s2 = fmaf(g[kActFields + 2], bk, s2);
+                    } else {
+                        s0 += g[av];
+                        if (av < kActFields - 16) s1 += g[av + 16];
                     }
-                    if (v < n_vals && sum != 0.f && (!is_act || v < n_act)) xacc_add(acc, row + v, sum);
+                }
+                if (sh_lane) {
+                    if (lane < n_sh) {
+                        const int64_t base = row + kActFields + 3 * lane;
+                        if (s0 != 0.f) xacc_add(acc, base + 0, s0);
+                        if (s1 != 0.f) xacc_add(acc, base + 1, s1);
+                        if (s2 != 0.f) xacc_add(acc, base + 2, s2);
+                    }
+                } else {
+                    if (s0 != 0.f && av < n_act) xacc_add(acc, row + av, s0);
+                    if (av < kActFields - 16 && s1 != 0.f && av + 16 < n_act) xacc_add(acc, row + av + 16, s1);
                 }
             }
             __syncwarp();

@@ -794,21 +794,45 @@ __device__ __forceinline__ void scatter_levels(const FieldBwdArgs& a, const TcCo
 #pragma unroll
         for (int ci = 0; ci < 8; ++ci) {
             const float cw = wx[ci & 1] * wy[(ci >> 1) & 1] * wz[(ci >> 2) & 1];
-            const uint32_t peers = __match_any_sync(0xffffffffu, valid ? c.row[ci] : 0xffffffffu);
-            wsh[lane] = make_float2(g0 * cw, g1 * cw);
-            __syncwarp();
-            if (valid && lane == __ffs(peers) - 1) {
-                float s0 = 0.f, s1 = 0.f;
-                for (uint32_t m = peers; m; m &= m - 1) {
-                    const float2 u = wsh[__ffs(m) - 1];
-                    s0 += u.x;
-                    s1 += u.y;
+            const float u0 = g0 * cw, u1 = g1 * cw;
+            const uint32_t key = valid ? c.row[ci] : 0xffffffffu;
+            const uint32_t peers = __match_any_sync(0xffffffffu, key);
+            const uint32_t leaders = __ballot_sync(0xffffffffu, valid && lane == __ffs(peers) - 1);
+            const int max_size = __reduce_max_sync(0xffffffffu, valid ? __popc(peers) : 0);
+            if (__popc(leaders) * 4 <= max_size) {
+                // few large groups (coarse levels): one warp-wide tree sum per group
+                for (uint32_t L = leaders; L; L &= L - 1) {
+                    const int ld = __ffs(L) - 1;
+                    const bool mine = key == __shfl_sync(0xffffffffu, key, ld);
+                    float s0 = mine ? u0 : 0.f, s1 = mine ? u1 : 0.f;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+                        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+                    }
+                    if (lane == ld) {
+                        const int64_t dst = slab + static_cast<int64_t>(c.row[ci]) * 2;
+                        xacc_add(tacc, dst, s0);
+                        xacc_add(tacc, dst + 1, s1);
+                    }
                 }
-                const int64_t dst = slab + static_cast<int64_t>(c.row[ci]) * 2;
-                xacc_add(tacc, dst, s0);
-                xacc_add(tacc, dst + 1, s1);
+            } else {
+                // many small groups (fine levels): each leader sums its group in lane order
+                wsh[lane] = make_float2(u0, u1);
+                __syncwarp();
+                if (valid && lane == __ffs(peers) - 1) {
+                    float s0 = 0.f, s1 = 0.f;
+                    for (uint32_t m = peers; m; m &= m - 1) {
+                        const float2 u = wsh[__ffs(m) - 1];
+                        s0 += u.x;
+                        s1 += u.y;
+                    }
+                    const int64_t dst = slab + static_cast<int64_t>(c.row[ci]) * 2;
+                    xacc_add(tacc, dst, s0);
+                    xacc_add(tacc, dst + 1, s1);
+                }
+                __syncwarp();
             }
-            __syncwarp();
         }
     }
 }

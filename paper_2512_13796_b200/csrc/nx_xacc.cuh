@@ -42,8 +42,10 @@ __device__ __forceinline__ void xacc_special(const Xacc& x, int64_t i, unsigned 
     atomicOr(x.w + kXaccWords * x.m + i, f);
 }
 
-// fp32 addend: 24-bit significand -> at most two chunks.
-__device__ __forceinline__ void xacc_add(const Xacc& x, int64_t i, float v) {
+// fp32 addend: 24-bit significand -> at most two chunks. The common case (a normal
+// number inside the range) is a dozen instructions inline; zero / subnormal / tiny /
+// huge / non-finite addends take the out-of-line path.
+static __device__ __noinline__ void xacc_add_f32_slow(const Xacc& x, int64_t i, float v) {
     const uint32_t b = __float_as_uint(v);
     const int ex = static_cast<int>((b >> 23) & 0xff);
     const bool neg = b >> 31;
@@ -66,9 +68,24 @@ __device__ __forceinline__ void xacc_add(const Xacc& x, int64_t i, float v) {
         xacc_special(x, i, neg ? kXaccNegInf : kXaccPosInf);
         return;
     }
-    const uint64_t y = m << r;  // < 2^56
+    const uint64_t y = m << r;
     xacc_chunk(x, i, k, y & 0xffffffffull, neg);
     xacc_chunk(x, i, k + 1, y >> 32, neg);
+}
+
+__device__ __forceinline__ void xacc_add(const Xacc& x, int64_t i, float v) {
+    const uint32_t b = __float_as_uint(v);
+    const int s = static_cast<int>((b >> 23) & 0xff) - 150 - kXaccE0;
+    const int k = s >> 5;
+    if (s < 0 || k + 1 >= kXaccWords || ((b >> 23) & 0xff) == 0) {  // zero / subnormal / out of range / inf / NaN
+        if (b << 1) xacc_add_f32_slow(x, i, v);
+        return;
+    }
+    const uint64_t y = static_cast<uint64_t>((b & 0x7fffffu) | 0x800000u) << (s & 31);  // < 2^56
+    const uint64_t lo = y & 0xffffffffull, hi = y >> 32;
+    const bool neg = b >> 31;
+    if (lo) atomicAdd(x.w + k * x.m + i, neg ? (0ull - lo) : lo);
+    if (hi) atomicAdd(x.w + (k + 1) * x.m + i, neg ? (0ull - hi) : hi);
 }
 
 // fp64 addend: 53-bit significand -> at most three chunks.
