@@ -51,6 +51,9 @@ struct BwdHit {         // one evaluated (pixel, primitive) pair
     double t;           // B1: plane crossing
     double d_t;         // B2: upstream dL/dt (field branch) of a buffered hit
     double werr;        // B2: w * err_pixel
+    double pu, pv;      // B1: axis_power(u, gx), axis_power(v, gy) (kernel.hpp:16-22)
+    double lu, lv;      // B1: log|u|, log|v| (0 for a zero coordinate)
+    double k;           // B1: exp(-(pu + pv) / 2)
     float rgb[3];       // B1: primitive colour; B2: w * dL/dfinal * clamp mask (unbuffered), else 0
     uint32_t flags;     // bits 0..2: SH clamp mask (B1)
 };
@@ -59,6 +62,7 @@ union BwdEntry {
     BwdHit h;
     float g[kStage + 1];
 };
+static_assert(sizeof(BwdHit) <= sizeof(float) * (kStage + 1), "the kernel terms fit the gradient row");
 constexpr uint16_t kComposited = 0x80;  // q entry flag set by B2 (list index j < kChunk)
 
 struct WarpSmem {        // one warp's private staging (no sharing between warps)
@@ -75,26 +79,25 @@ struct SmemLayout {
 
 // eval_kernel_grad (kernel.hpp:40-68) + intersect_backward (intersect.hpp:56-87):
 // the activated-space gradient of one hit, g[0..16] = d_mu[3], d_R[9] (m[i][j]),
-// d_sigma[2], d_opacity, d_gamma[2].
+// d_sigma[2], d_opacity, d_gamma[2]. The kernel terms (axis powers, log|u|, log|v|,
+// exp(-(pu + pv)/2)) are the ones B1 formed for the hit (finite: a composited hit).
 __device__ __forceinline__ void hit_backward(const double* r, const double* d, const double* o, double t, double u,
-                                             double v, double d_alpha, double d_t, double* g) {
+                                             double v, const BwdHit& hh, double* g) {
     const double op = r[REC_OP], gx = r[REC_GX], gy = r[REC_GY], sx = r[REC_SX], sy = r[REC_SY];
-    const double pu = axis_power(u, gx), pv = axis_power(v, gy);
-    double kd_u = 0.0, kd_v = 0.0, kd_op = 0.0, kd_gx = 0.0, kd_gy = 0.0;
-    if (!(isinf(pu) || isinf(pv))) {
-        const double k = exp(-0.5 * (pu + pv));
-        const double alpha = op * k;
-        kd_op = k;
-        if (u != 0.0) {
-            const double au = fabs(u);
-            kd_u = -alpha * gx * (pu / au) * (u > 0 ? 1.0 : -1.0);
-            kd_gx = -alpha * log(au) * pu;
-        }
-        if (v != 0.0) {
-            const double av = fabs(v);
-            kd_v = -alpha * gy * (pv / av) * (v > 0 ? 1.0 : -1.0);
-            kd_gy = -alpha * log(av) * pv;
-        }
+    const double pu = hh.pu, pv = hh.pv, d_alpha = hh.alpha, d_t = hh.d_t;
+    double kd_u = 0.0, kd_v = 0.0, kd_gx = 0.0, kd_gy = 0.0;
+    const double k = hh.k;
+    const double alpha = op * k;
+    const double kd_op = k;
+    if (u != 0.0) {
+        const double au = fabs(u);
+        kd_u = -alpha * gx * (pu / au) * (u > 0 ? 1.0 : -1.0);
+        kd_gx = -alpha * hh.lu * pu;
+    }
+    if (v != 0.0) {
+        const double av = fabs(v);
+        kd_v = -alpha * gy * (pv / av) * (v > 0 ? 1.0 : -1.0);
+        kd_gy = -alpha * hh.lv * pv;
     }
     const double v1[3] = {r[REC_V1X], r[REC_V1Y], r[REC_V1Z]};
     const double v2[3] = {r[REC_V2X], r[REC_V2Y], r[REC_V2Z]};
@@ -269,10 +272,20 @@ __global__ void __launch_bounds__(kThreads, 2) composite_bwd_kernel(const Compos
                         if (fabs(du) <= r[REC_ULIM] && fabs(dv) <= r[REC_VLIM]) {
                             const double u = du / r[REC_SX];
                             const double v = dv / r[REC_SY];
-                            const double al = eval_kernel(u, v, r[REC_OP], r[REC_GX], r[REC_GY]);
+                            // eval_kernel (kernel.hpp:16-30), keeping its terms for B3a
+                            const double lu = u != 0.0 ? log(fabs(u)) : 0.0, lv = v != 0.0 ? log(fabs(v)) : 0.0;
+                            const double pu = axis_power_log(u, r[REC_GX], lu), pv = axis_power_log(v, r[REC_GY], lv);
+                            const double p = pu + pv;
+                            const double kk = isinf(p) ? 0.0 : exp(-0.5 * p);
+                            const double al = isinf(p) ? 0.0 : r[REC_OP] * kk;
                             if (al >= kAlphaMin) {
                                 res.alpha = al;
                                 res.t = tt;
+                                res.pu = pu;
+                                res.pv = pv;
+                                res.lu = lu;
+                                res.lv = lv;
+                                res.k = kk;
                                 uint32_t act;
                                 eval_sh_f32(a.sh + static_cast<int64_t>(id) * NX_SH_VALUES, static_cast<float>(d0),
                                             static_cast<float>(d1), static_cast<float>(d2), a.sh_degree, res.rgb,
@@ -351,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, 2) composite_bwd_kernel(const Compos
                 const double u = (e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z]) / r[REC_SX];
                 const double v = (e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z]) / r[REC_SY];
                 double gd[kActFields - 1];
-                hit_backward(r, d3, o, hh.t, u, v, hh.alpha, hh.d_t, gd);
+                hit_backward(r, d3, o, hh.t, u, v, hh, gd);
                 float* g = sm.res[e].g;
 #pragma unroll
                 for (int i = 0; i < kActFields - 1; ++i) g[i] = static_cast<float>(gd[i]);

@@ -54,6 +54,14 @@ NX_HD double axis_power(double u, double g) {
     if (e > 700.0) return INFINITY;
     return exp(e);
 }
+// axis_power with log|u| supplied (the same value axis_power forms, so bit-identical)
+NX_HD double axis_power_log(double u, double g, double lu) {
+    if (u == 0.0) return 0.0;
+    if (g == 1.0) return u * u;
+    const double e = 2.0 * g * lu;
+    if (e > 700.0) return INFINITY;
+    return exp(e);
+}
 NX_HD double eval_kernel(double u, double v, double o, double gx, double gy) {
     const double p = axis_power(u, gx) + axis_power(v, gy);
     if (isinf(p)) return 0.0;
