@@ -60,7 +60,7 @@ RENAME_FWD := -Dcollection_pass=nexel_ref_collection_pass -Dtexturing_pass=nexel
 
 ifneq ($(wildcard $(REF)/core/src/renderer.cpp),)
 dropin: $(DROPIN)/libnexel_dropin.so $(DROPIN)/test_oracle_dropin $(DROPIN)/test_dropin_backward \
-        $(DROPIN)/test_train_dropin $(DROPIN)/test_dropin_train
+        $(DROPIN)/test_train_dropin $(DROPIN)/test_dropin_train $(DROPIN)/bench_train
 else
 dropin:
 	@echo "reference sources not present; using the prebuilt $(DROPIN) if any"
@@ -110,6 +110,9 @@ TRAIN_TEST_OBJS := $(DROPIN)/ref_json_bundle.o $(DROPIN)/ref_json_synthetic.o $(
 $(DROPIN)/test_train_dropin: $(REF)/tests/test_train.cpp tests/cxx/doctest.h $(TRAIN_TEST_OBJS) $(DROPIN)/libnexel_dropin.so
 	$(CXX) $(DROPIN_CXX) -Itests/cxx -I$(REF)/tests -o $@ $< $(TRAIN_TEST_OBJS) -L$(DROPIN) -lnexel_dropin \
 	    -Wl,-rpath,'$$ORIGIN'
+
+$(DROPIN)/bench_train: tests/cxx/bench_train.cpp $(TRAIN_TEST_OBJS) $(DROPIN)/libnexel_dropin.so
+	$(CXX) $(DROPIN_CXX) -o $@ $< $(TRAIN_TEST_OBJS) -L$(DROPIN) -lnexel_dropin -Wl,-rpath,'$$ORIGIN'
 
 $(DROPIN)/test_dropin_train: tests/cxx/test_dropin_train.cpp tests/cxx/doctest.h $(TRAIN_TEST_OBJS) $(DROPIN)/libnexel_dropin.so
 	$(CXX) $(DROPIN_CXX) -Itests/cxx -I$(REF)/tests -o $@ $< $(TRAIN_TEST_OBJS) -L$(DROPIN) -lnexel_dropin \

@@ -82,6 +82,7 @@ void nx::count_launch(int n) { g_launches.fetch_add(static_cast<unsigned long lo
 
 struct nx_ctx {
     int device = 0;
+    int sms = 148;  // multiprocessors of the device
     cudaStream_t stream = nullptr;
     std::string err;
     int err_status = NX_OK;
@@ -93,6 +94,7 @@ struct nx_ctx {
     // render_backward scratch
     nx_frame* bwd_lists = nullptr;   // work lists of the re-binned camera
     DevBuf d_t_slot, act_grad, xacc_prims;
+    DevBuf dens_map, dens_par, dens_src;  // density-control maps (grow-only)
     DevBuf h_up[3], h_err, h_blend, h_grads[5];  // device copies for nx_render_backward_host
     DevBuf loss_scratch, h_gt, h_terms;          // losses_backward
     FieldBwdScratch field_bwd;                    // tensor-core field backward
@@ -112,6 +114,7 @@ struct nx_scene {
     nx_ctx* ctx = nullptr;
     int64_t n = 0;
     DevBuf geom, sh, table, w1, w2, w3;
+    DevBuf geom_spare, sh_spare;  // density control rebuilds into these and swaps (grow-only)
     nx_field_desc field{};
     nx_settings st{};
     int bad_status = NX_OK;
@@ -526,6 +529,7 @@ int nx_ctx_create(int device, nx_ctx** out) {
     nx_ctx* c = new (std::nothrow) nx_ctx;
     if (!c) return NX_OUT_OF_MEMORY;
     c->device = device;
+    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking) != cudaSuccess ||
@@ -550,7 +554,7 @@ void nx_ctx_destroy(nx_ctx* c) {
                       &c->skeys_b, &c->sids_a, &c->sids_b, &c->counts, &c->offsets, &c->tkeys_a, &c->tkeys_b,
                       &c->tvals_a, &c->tvals_b, &c->tile_counts, &c->scratch, &c->dbg_hits, &c->dbg_counts})
         b->release();
-    for (DevBuf* b : {&c->d_t_slot, &c->act_grad, &c->xacc_prims, &c->h_err, &c->h_blend, &c->loss_scratch, &c->h_gt, &c->h_terms})
+    for (DevBuf* b : {&c->d_t_slot, &c->act_grad, &c->xacc_prims, &c->dens_map, &c->dens_par, &c->dens_src, &c->h_err, &c->h_blend, &c->loss_scratch, &c->h_gt, &c->h_terms})
         b->release();
     c->field_bwd.release();
     for (DevBuf& b : c->h_up) b.release();
@@ -781,7 +785,7 @@ int nx_scene_get_settings(const nx_scene* s, nx_settings* out) {
 void nx_scene_destroy(nx_scene* s) {
     if (!s) return;
     if (s->ctx) cudaSetDevice(s->ctx->device);
-    for (DevBuf* b : {&s->geom, &s->sh, &s->table, &s->w1, &s->w2, &s->w3}) b->release();
+    for (DevBuf* b : {&s->geom, &s->sh, &s->table, &s->w1, &s->w2, &s->w3, &s->geom_spare, &s->sh_spare}) b->release();
     delete s;
 }
 
@@ -995,7 +999,10 @@ int nx_render_backward(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, n
     int64_t total = 0;
     const bool prof = c->profiling;
     c->profiling = false;  // the stage events describe forward frames only
-    st = build_lists(c, scene, *cam, lf, 0, s, &total, kBwdTile);
+    // 16x16 work tiles, unless that gives fewer than ~4 CTAs per SM (small images)
+    const int64_t tiles16 = static_cast<int64_t>((cam->width + 15) / 16) * ((cam->height + 15) / 16);
+    const int bwd_tile = tiles16 < 4 * c->sms ? 8 : kBwdTile;
+    st = build_lists(c, scene, *cam, lf, 0, s, &total, bwd_tile);
     c->profiling = prof;
     if (st) return st;
 
@@ -1046,6 +1053,7 @@ int nx_render_backward(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, n
     ca.d_t_slot = c->d_t_slot.as<double>();
     ca.err_pixel = blended_error ? err_pixel : nullptr;
     ca.acc = prim_acc;
+    ca.tile = bwd_tile;
     launch_composite_backward(ca, s);
     launch_prim_finalize(scene_dev(scene), scene->st.no_gamma, prim_acc, c->act_grad.as<double>(), g->prims,
                          err_pixel ? blended_error : nullptr, s);
@@ -1201,6 +1209,7 @@ struct nx_optimizer {
     int64_t n = 0;
     DevBuf m[NX_NUM_GROUPS], v[NX_NUM_GROUPS];
     DevBuf master[NX_NUM_GROUPS];  // fp64 values of the groups the scene stores in fp32 (5..10)
+    DevBuf m_spare[7], v_spare[7], master_spare[7];  // per-nexel rows rebuilt by density control
     int64_t step[NX_NUM_GROUPS] = {};
     int64_t size[NX_NUM_GROUPS] = {};
 };
@@ -1299,6 +1308,11 @@ void nx_optimizer_destroy(nx_optimizer* o) {
         o->v[gi].release();
         o->master[gi].release();
     }
+    for (int gi = 0; gi < 7; ++gi) {
+        o->m_spare[gi].release();
+        o->v_spare[gi].release();
+        o->master_spare[gi].release();
+    }
     delete o;
 }
 
@@ -1333,53 +1347,48 @@ namespace {
 constexpr int kRowWidth[7] = {3, 4, 2, 1, 2, 3, 45};  // per-nexel Adam groups (trainer.cpp kRowWidth)
 
 // Rebuilds the scene (and the optimizer's per-nexel rows) in the layout of n_new nexels
-// from new_to_old (device); geometry rows from geom_new when given (densify) else
-// gathered; SH gathered unless sh_done. Moments follow new_to_old (-1: fresh zeros,
+// from new_to_old (device), into the spare buffers that are then swapped in (no
+// allocation once they have grown): geometry already in scene->geom_spare when
+// geom_done (densify), else gathered; SH already in scene->sh (swapped) when sh_done. Moments follow new_to_old (-1: fresh zeros,
 // adam_remap_rows); the SH masters follow src_rows (the row each new row's values come
 // from: a split child's parent), new_to_old when null.
 int apply_row_map(nx_ctx* c, nx_scene* scene, nx_optimizer* opt, int64_t n_new, const int32_t* n2o,
-                  DevBuf* geom_new, bool sh_done, cudaStream_t s, const int32_t* src_rows = nullptr) {
+                  bool geom_done, bool sh_done, cudaStream_t s, const int32_t* src_rows = nullptr) {
     const int64_t n = scene->n;
-    DevBuf g2, sh2;
-    if (!geom_new) {
-        NX_CUDA(c, g2.ensure(std::max<int64_t>(n_new, 1) * kGeomFields * sizeof(double)));
-        launch_gather_geom(scene->geom.as<double>(), n, g2.as<double>(), n_new, n2o, s);
-        geom_new = &g2;
+    if (!geom_done) {
+        NX_CUDA(c, scene->geom_spare.ensure(std::max<int64_t>(n_new, 1) * kGeomFields * sizeof(double)));
+        launch_gather_geom(scene->geom.as<double>(), n, scene->geom_spare.as<double>(), n_new, n2o, s);
     }
     if (!sh_done) {
-        NX_CUDA(c, sh2.ensure(std::max<int64_t>(n_new, 1) * NX_SH_VALUES * sizeof(float)));
-        launch_gather_rows_f32(scene->sh.as<float>(), sh2.as<float>(), n_new, NX_SH_VALUES, n2o, s);
-        std::swap(scene->sh, sh2);
+        NX_CUDA(c, scene->sh_spare.ensure(std::max<int64_t>(n_new, 1) * NX_SH_VALUES * sizeof(float)));
+        launch_gather_rows_f32(scene->sh.as<float>(), scene->sh_spare.as<float>(), n_new, NX_SH_VALUES, n2o, s);
     }
     if (opt) {
         for (int gi = 0; gi < 7; ++gi) {
-            DevBuf m2, v2;
             const size_t bytes = std::max<int64_t>(n_new * kRowWidth[gi], 1) * sizeof(double);
-            NX_CUDA(c, m2.ensure(bytes));
-            NX_CUDA(c, v2.ensure(bytes));
-            launch_gather_rows_f64(opt->m[gi].as<double>(), m2.as<double>(), n_new, kRowWidth[gi], n2o, s);
-            launch_gather_rows_f64(opt->v[gi].as<double>(), v2.as<double>(), n_new, kRowWidth[gi], n2o, s);
-            DevBuf p2;
+            NX_CUDA(c, opt->m_spare[gi].ensure(bytes));
+            NX_CUDA(c, opt->v_spare[gi].ensure(bytes));
+            launch_gather_rows_f64(opt->m[gi].as<double>(), opt->m_spare[gi].as<double>(), n_new, kRowWidth[gi], n2o, s);
+            launch_gather_rows_f64(opt->v[gi].as<double>(), opt->v_spare[gi].as<double>(), n_new, kRowWidth[gi], n2o, s);
             if (gi >= NX_GROUP_SH_DC) {
-                NX_CUDA(c, p2.ensure(bytes));
-                launch_gather_rows_f64(opt->master[gi].as<double>(), p2.as<double>(), n_new, kRowWidth[gi],
-                                       src_rows ? src_rows : n2o, s);
+                NX_CUDA(c, opt->master_spare[gi].ensure(bytes));
+                launch_gather_rows_f64(opt->master[gi].as<double>(), opt->master_spare[gi].as<double>(), n_new,
+                                       kRowWidth[gi], src_rows ? src_rows : n2o, s);
             }
-            NX_CUDA(c, cudaStreamSynchronize(s));
-            std::swap(opt->m[gi], m2);
-            std::swap(opt->v[gi], v2);
-            if (gi >= NX_GROUP_SH_DC) std::swap(opt->master[gi], p2);
-            m2.release();
-            v2.release();
-            p2.release();
+        }
+    }
+    NX_CUDA(c, cudaStreamSynchronize(s));
+    if (opt) {
+        for (int gi = 0; gi < 7; ++gi) {
+            std::swap(opt->m[gi], opt->m_spare[gi]);
+            std::swap(opt->v[gi], opt->v_spare[gi]);
+            if (gi >= NX_GROUP_SH_DC) std::swap(opt->master[gi], opt->master_spare[gi]);
             opt->size[gi] = n_new * kRowWidth[gi];
         }
         opt->n = n_new;
     }
-    NX_CUDA(c, cudaStreamSynchronize(s));
-    std::swap(scene->geom, *geom_new);
-    geom_new->release();
-    sh2.release();
+    std::swap(scene->geom, scene->geom_spare);
+    if (!sh_done) std::swap(scene->sh, scene->sh_spare);
     scene->n = n_new;
     return NX_OK;
 }
@@ -1402,15 +1411,14 @@ int nx_scene_prune(nx_ctx* c, nx_scene* scene, nx_optimizer* opt, double min_opa
     NX_CUDA(c, cudaMemcpyAsync(&kept, d_total, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     NX_CUDA(c, cudaStreamSynchronize(s));
     if (n == 0) kept = 0;
-    DevBuf map;
+    DevBuf& map = c->dens_map;
     NX_CUDA(c, map.ensure(std::max<int64_t>(kept, 1) * sizeof(int32_t)));
     launch_compact_map(c->flag.as<int32_t>(), c->pos.as<int32_t>(), n, map.as<int32_t>(), s);
-    int st = apply_row_map(c, scene, opt, kept, map.as<int32_t>(), nullptr, false, s);
+    int st = apply_row_map(c, scene, opt, kept, map.as<int32_t>(), false, false, s);
     if (st) return st;
     if (new_to_old && kept)
         NX_CUDA(c, cudaMemcpyAsync(new_to_old, map.p, kept * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     NX_CUDA(c, cudaStreamSynchronize(s));
-    map.release();
     if (n_out) *n_out = kept;
     return NX_OK;
 }
@@ -1458,32 +1466,29 @@ int nx_scene_densify_split(nx_ctx* c, nx_scene* scene, nx_optimizer* opt, const 
                           cudaMemcpyDeviceToHost));
     std::sort(parents.begin(), parents.end());  // density.cpp:132-134
     const int64_t n_new = n + allowed;
-    DevBuf d_par, map, g2, sh2;
+    DevBuf &d_par = c->dens_par, &map = c->dens_map, &src = c->dens_src;
     NX_CUDA(c, d_par.ensure(allowed * sizeof(int32_t)));
     NX_CUDA(c, cudaMemcpy(d_par.p, parents.data(), allowed * sizeof(int32_t), cudaMemcpyHostToDevice));
     NX_CUDA(c, map.ensure(n_new * sizeof(int32_t)));
-    NX_CUDA(c, g2.ensure(n_new * kGeomFields * sizeof(double)));
-    NX_CUDA(c, sh2.ensure(n_new * NX_SH_VALUES * sizeof(float)));
-    NX_CUDA(c, cudaMemcpyAsync(sh2.p, scene->sh.p, n * NX_SH_VALUES * sizeof(float), cudaMemcpyDeviceToDevice, s));
-    launch_split_children(g2.as<double>(), n_new, scene->geom.as<double>(), n, sh2.as<float>(), d_par.as<int32_t>(),
-                          allowed, map.as<int32_t>(), s);
-    std::swap(scene->sh, sh2);
-    DevBuf src;  // the SH masters' source rows: kept rows themselves, a child its parent
-    if (opt) {
+    NX_CUDA(c, scene->geom_spare.ensure(n_new * kGeomFields * sizeof(double)));
+    NX_CUDA(c, scene->sh_spare.ensure(n_new * NX_SH_VALUES * sizeof(float)));
+    NX_CUDA(c, cudaMemcpyAsync(scene->sh_spare.p, scene->sh.p, n * NX_SH_VALUES * sizeof(float),
+                               cudaMemcpyDeviceToDevice, s));
+    launch_split_children(scene->geom_spare.as<double>(), n_new, scene->geom.as<double>(), n,
+                          scene->sh_spare.as<float>(), d_par.as<int32_t>(), allowed, map.as<int32_t>(), s);
+    std::swap(scene->sh, scene->sh_spare);
+    if (opt) {  // the SH masters' source rows: kept rows themselves, a child its parent
         std::vector<int32_t> h(static_cast<size_t>(n_new));
         for (int64_t i = 0; i < n; ++i) h[i] = static_cast<int32_t>(i);
         for (int64_t r = 0; r < allowed; ++r) h[n + r] = parents[r];
         NX_CUDA(c, src.ensure(n_new * sizeof(int32_t)));
-        NX_CUDA(c, cudaMemcpy(src.p, h.data(), n_new * sizeof(int32_t), cudaMemcpyHostToDevice));
+        NX_CUDA(c, cudaMemcpyAsync(src.p, h.data(), n_new * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     }
-    int st = apply_row_map(c, scene, opt, n_new, map.as<int32_t>(), &g2, true, s, opt ? src.as<int32_t>() : nullptr);
+    int st = apply_row_map(c, scene, opt, n_new, map.as<int32_t>(), true, true, s, opt ? src.as<int32_t>() : nullptr);
     if (st) return st;
     if (new_to_old)
         NX_CUDA(c, cudaMemcpyAsync(new_to_old, map.p, n_new * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     NX_CUDA(c, cudaStreamSynchronize(s));
-    sh2.release();
-    map.release();
-    d_par.release();
     if (n_out) *n_out = n_new;
     if (split_count) *split_count = allowed;
     return NX_OK;

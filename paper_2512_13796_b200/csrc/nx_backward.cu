@@ -36,13 +36,12 @@ namespace nx {
 
 namespace {
 
-constexpr int kThreads = kBwdTile * kBwdTile;  // 256: one thread per pixel of the 16x16 work tile
-constexpr int kWarps = kThreads / 32;           // 8 warps of 8x4 pixels
+// One thread per pixel of the work tile: 16x16 (8 warps of 8x4 pixels) for large
+// images, 8x8 (2 warps) when 16x16 tiles would leave the GPU short of CTAs.
 constexpr int kChunk = 32;                      // primitives staged per warp round
 constexpr int kSub = 2;                         // primitives pooled per B1/B2/B3 round
 constexpr int kPool = 32 * kSub;
 constexpr int kRecPairs = REC_FIELDS / 2;
-static_assert(kBwdTile == 16, "warp blocks are 8x4 pixels, two across a 16-pixel row");
 
 constexpr int kStage = kActFields + 3;          // per-hit staged values: activated grads, werr, w dL/dfinal
 
@@ -72,9 +71,6 @@ struct WarpSmem {        // one warp's private staging (no sharing between warps
     BwdEntry res[kPool];
     int32_t id[kChunk];
     uint16_t q[kPool];
-};
-struct SmemLayout {
-    WarpSmem w[kWarps];
 };
 
 // eval_kernel_grad (kernel.hpp:40-68) + intersect_backward (intersect.hpp:56-87):
@@ -126,12 +122,12 @@ __device__ __forceinline__ void hit_backward(const double* r, const double* d, c
     }
 }
 
-template <int K>
-__global__ void __launch_bounds__(kThreads, 2) composite_bwd_kernel(const CompositeBwdArgs a) {
+template <int K, int kTile>
+__global__ void __launch_bounds__(kTile * kTile, 512 / (kTile * kTile)) composite_bwd_kernel(const CompositeBwdArgs a) {
     constexpr int KK = K > 0 ? K : 1;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WarpSmem& sm = reinterpret_cast<SmemLayout*>(smem_raw)->w[warp];
+    WarpSmem& sm = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
 
     const int t = blockIdx.x;
     const int tx = t % a.fb.tiles_x, ty = t / a.fb.tiles_x;
@@ -141,8 +137,9 @@ __global__ void __launch_bounds__(kThreads, 2) composite_bwd_kernel(const Compos
     const float near_eps_f = static_cast<float>(near_eps);
     const double o[3] = {a.cam.o[0], a.cam.o[1], a.cam.o[2]};
 
-    // warp w owns the 8x4 block (w % 2, w / 2) of the 16x16 tile
-    const int px = tx * kBwdTile + (warp & 1) * 8 + (lane & 7), py = ty * kBwdTile + (warp >> 1) * 4 + (lane >> 3);
+    // warp w owns the 8x4 block (w % (kTile / 8), w / (kTile / 8)) of the tile
+    constexpr int kAcross = kTile / 8;
+    const int px = tx * kTile + (warp % kAcross) * 8 + (lane & 7), py = ty * kTile + (warp / kAcross) * 4 + (lane >> 3);
     const bool in_img = px < W && py < H;
     const int wx0 = __reduce_min_sync(0xffffffffu, in_img ? px : 0x7fffffff);
     const int wx1 = __reduce_max_sync(0xffffffffu, in_img ? px : -1);
@@ -426,9 +423,17 @@ __global__ void __launch_bounds__(kThreads, 2) composite_bwd_kernel(const Compos
 
 template <int K>
 void launch_one(const CompositeBwdArgs& a, unsigned grid, cudaStream_t s) {
-    const size_t smem = sizeof(SmemLayout);
-    cudaFuncSetAttribute(composite_bwd_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    composite_bwd_kernel<K><<<grid, kThreads, smem, s>>>(a);
+    if (a.tile == 8) {
+        const size_t smem = 2 * sizeof(WarpSmem);
+        cudaFuncSetAttribute(composite_bwd_kernel<K, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        composite_bwd_kernel<K, 8><<<grid, 64, smem, s>>>(a);
+    } else {
+        const size_t smem = 8 * sizeof(WarpSmem);
+        cudaFuncSetAttribute(composite_bwd_kernel<K, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        composite_bwd_kernel<K, 16><<<grid, 256, smem, s>>>(a);
+    }
 }
 
 // quat_rotation_backward (primitive.cpp:22-45)

@@ -29,7 +29,7 @@ constexpr int kGeomFields = 12;            // fp64 geometry params per primitive
 constexpr int kWorkTile = 8;
 // The reverse march (render_backward) walks 16x16-pixel work lists: its CTAs are
 // 8 warps that share per-primitive gradient accumulators in shared memory.
-constexpr int kBwdTile = 16;
+constexpr int kBwdTile = 16;  // render_backward work tiles (8 when 16 leaves the GPU short of CTAs)
 
 // ---------------------------------------------------------------- scalar helpers
 // sigmoid / softplus (vec_math.hpp:69-84)
@@ -362,6 +362,7 @@ struct CompositeBwdArgs {
     const double* d_t_slot;   // H*W*K
     const double* err_pixel;  // H*W or nullptr
     Xacc acc;                 // n x kPrimAccVals exact accumulators (zero on entry)
+    int tile;                 // work-tile side of the lists: 16, or 8 for small images
 };
 // The per-pixel reverse march of render_backward (renderer.cpp:287-390).
 void launch_composite_backward(const CompositeBwdArgs& a, cudaStream_t s);

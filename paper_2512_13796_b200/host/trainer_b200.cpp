@@ -30,6 +30,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -301,8 +302,20 @@ TrainResult train(const Bundle& bundle, const TrainConfig& cfg, const TrainHooks
     std::vector<int> perm;
     size_t perm_pos = 0;
     LossTerms terms;
+    // NEXEL_TRAIN_PROFILE=1: per-phase wall times (synchronising after each phase) on stderr
+    static const bool profile = std::getenv("NEXEL_TRAIN_PROFILE") != nullptr;
+    double phase_s[6] = {};
+    auto tp = std::chrono::steady_clock::now();
+    auto mark = [&](int phase) {
+        if (!profile) return;
+        cuda_check(cudaStreamSynchronize(cs), "sync");
+        const auto now = std::chrono::steady_clock::now();
+        phase_s[phase] += std::chrono::duration<double>(now - tp).count();
+        tp = now;
+    };
     for (int iter = 1; iter <= cfg.iterations; ++iter) {
         const auto t0 = std::chrono::steady_clock::now();
+        tp = t0;
         if (perm_pos == perm.size()) {  // trainer.cpp:280-284
             perm = bundle.train_views;
             std::shuffle(perm.begin(), perm.end(), rng);
@@ -313,6 +326,7 @@ TrainResult train(const Bundle& bundle, const TrainConfig& cfg, const TrainHooks
         const size_t npix = static_cast<size_t>(cam.width) * cam.height;
 
         r.check(nx_render(r.ctx, r.scene, &cam, r.frame, s));
+        mark(0);
         cuda_check(cudaMemsetAsync(g_prims, 0, n * NX_PARAMS_PER_NEXEL * sizeof(double), cs), "memset");
         cuda_check(cudaMemsetAsync(g_table, 0, n_table * sizeof(double), cs), "memset");
         cuda_check(cudaMemsetAsync(g_w1, 0, n_w1 * sizeof(double), cs), "memset");
@@ -336,13 +350,16 @@ TrainResult train(const Bundle& bundle, const TrainConfig& cfg, const TrainHooks
             fail("non-finite-loss", "loss diverged at iteration " + std::to_string(iter));
         }
         (void)npix;
+        mark(1);
         r.check(nx_pixel_error(r.ctx, r.frame, gt[view], err_pixel, s));
         const nx_upstream up{d_final, K ? d_weights : nullptr, K ? d_texture : nullptr};
         r.check(nx_render_backward(r.ctx, r.scene, &cam, r.frame, &up, &grads, err_pixel, err_accum, s));
+        mark(2);
 
         gcfg[kGroupPosition].lr = cfg.lr_position * ext *
                                   std::pow(decay, static_cast<double>(iter) / std::max(1, cfg.iterations));
         r.check(nx_optimizer_step(r.ctx, r.opt, r.scene, &grads, gcfg, s));
+        mark(3);
 
         if (cfg.densify_every > 0 && iter % cfg.densify_every == 0 && iter >= cfg.densify_start &&
             iter <= cfg.densify_end) {  // trainer.cpp:324-333
@@ -375,6 +392,7 @@ TrainResult train(const Bundle& bundle, const TrainConfig& cfg, const TrainHooks
             cuda_check(cudaMemsetAsync(err_accum, 0, std::max<size_t>(n, 1) * sizeof(double), cs), "memset");
         }
 
+        mark(4);
         cuda_check(cudaStreamSynchronize(cs), "sync");
         const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         out.last_loss = terms;
@@ -384,6 +402,11 @@ TrainResult train(const Bundle& bundle, const TrainConfig& cfg, const TrainHooks
                           device_mean_psnr(r, bundle, bundle.test_views, s));
     }
 
+    if (profile && cfg.iterations > 0) {
+        const char* names[5] = {"render", "losses", "backward", "adam", "density"};
+        for (int p = 0; p < 5; ++p)
+            std::fprintf(stderr, "train profile: %-8s %.3f ms/iteration\n", names[p], 1e3 * phase_s[p] / cfg.iterations);
+    }
     // ---- results: fp64 parameters and Adam states (trainer.cpp:346-348)
     out.scene = download_scene(r, init);
     int64_t steps[NX_NUM_GROUPS];

@@ -101,6 +101,7 @@ def test_stump_textured_gradients_match_reference(renderer, reference):
     (4_000, 90, (128, 96), 1e-1, "no_prim_sh"),
     (4_000, 130, (128, 96), 1e-1, "no_gamma"),
     (4_000, 200, (128, 96), 1e-1, "k4"),
+    (6_000, 60, (640, 480), 1e-1, None),          # >= 4 x SMs 16x16 tiles: the 16x16 work-tile kernel
 ])
 def test_stump_field_tc_gradients_match_reference(renderer, reference, n, view, size, grid_init, ablation):
     # the reference field shape (16 levels x 2 x 64 hidden) takes the tcgen05 field backward
