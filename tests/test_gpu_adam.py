@@ -66,3 +66,73 @@ def test_adam_steps_match_reference(renderer, reference):
         assert np.allclose(a, b, rtol=2e-6, atol=1e-6)
     assert not np.allclose(got[0][:, :3], scene.nexels[:, :3])  # the positions moved
     renderer.lib.nx_optimizer_destroy(opt)
+
+
+def test_fp64_masters_track_the_reference_exactly(renderer, reference):
+    """The fp32-stored groups (SH, table, MLP) are stepped on the optimizer's fp64 masters:
+    read back with nx_optimizer_download they agree with the reference's fp64 adam_step to
+    fp64 rounding, not just fp32 (the scene keeps their fp32 rounding for rendering)."""
+    scene = nx.stump_like(500, log2_table=8, grid_init=1e-1)
+    ds = renderer.upload(scene)
+    opt = C.c_void_p()
+    renderer._check(renderer.lib.nx_optimizer_create(renderer.ctx, ds.handle, C.byref(opt)))
+    f = scene.field
+    init = {5: scene.nexels[:, 12:15], 6: scene.nexels[:, 15:60], 7: f.table, 8: f.w1, 9: f.w2, 10: f.w3}
+    # seed the masters exactly (here the values are fp32-representable anyway) and read back
+    for gi, vals in init.items():
+        host = np.ascontiguousarray(vals, dtype=np.float64).reshape(-1)
+        renderer._check(renderer.lib.nx_optimizer_set_params(renderer.ctx, opt, ds.handle, gi,
+                                                             host.ctypes.data_as(C.POINTER(C.c_double)), host.size))
+    cfgs = [(1e-3, 0.9, 0.999, 1e-8)] * 11
+    ccfg = (_abi.nx_adam_config * 11)(*[_abi.nx_adam_config(*c) for c in cfgs])
+    rng = np.random.default_rng(7)
+    ref = {gi: np.ascontiguousarray(v, dtype=np.float64).reshape(-1).copy() for gi, v in init.items()}
+    state = {}
+    for _ in range(4):
+        g_prims = rng.standard_normal((500, 60))
+        g_f = [rng.standard_normal(np.size(a)) for a in (f.table, f.w1, f.w2, f.w3)]
+        dev = [torch.tensor(a.reshape(-1), dtype=torch.float64, device="cuda") for a in (g_prims, *g_f)]
+        gg = _abi.nx_grads(*(t.data_ptr() for t in dev))
+        torch.cuda.synchronize()
+        renderer._check(renderer.lib.nx_optimizer_step(renderer.ctx, opt, ds.handle, C.byref(gg), ccfg, None))
+        renderer.synchronize()
+        grads = {5: g_prims[:, 12:15], 6: g_prims[:, 15:60], 7: g_f[0], 8: g_f[1], 9: g_f[2], 10: g_f[3]}
+        for gi in ref:
+            gr = np.ascontiguousarray(grads[gi]).reshape(-1)
+            m, v, st = state.get(gi, (np.zeros(gr.size), np.zeros(gr.size), 0))
+            state[gi] = (m, v, reference.adam_step(m, v, st, cfgs[gi], ref[gi], gr))
+    for gi, want in ref.items():
+        n = C.c_int64()
+        renderer.lib.nx_optimizer_size(opt, gi, C.byref(n))
+        assert n.value == want.size
+        got, m, v = np.empty(want.size), np.empty(want.size), np.empty(want.size)
+        renderer._check(renderer.lib.nx_optimizer_download(renderer.ctx, opt, ds.handle, gi, _abi_ptr(got), _abi_ptr(m),
+                                                           _abi_ptr(v)))
+        # fp64 on both sides (the device contracts some products into FMAs): a few ulp of
+        # each array's scale
+        for a, b in ((got, want), (m, state[gi][0]), (v, state[gi][1])):
+            assert np.abs(a - b).max() <= 1e-13 * np.abs(b).max(), gi
+    renderer.lib.nx_optimizer_destroy(opt)
+
+
+def _abi_ptr(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def test_pixel_error_matches_the_trainer(renderer):
+    """nx_pixel_error: err[p] = sum_c |final - gt| / 3 (trainer.cpp:288-295)."""
+    scene = nx.stump_like(3_000, log2_table=10, grid_init=1e-1)
+    cam = nx.ring_camera(5, 256, 96, 64)
+    ds = renderer.upload(scene)
+    fr = renderer.frame()
+    renderer.render(ds, cam, fr)
+    fin = fr.download(["final_img"]).final_img.astype(np.float64)
+    gt = np.random.default_rng(1).random(fin.size)
+    gt_d = torch.tensor(gt, dtype=torch.float64, device="cuda")
+    err_d = torch.empty(cam.width * cam.height, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    renderer._check(renderer.lib.nx_pixel_error(renderer.ctx, fr.handle, C.c_void_p(gt_d.data_ptr()),
+                                                C.c_void_p(err_d.data_ptr()), None))
+    renderer.synchronize()
+    want = np.abs(fin - gt).reshape(-1, 3).sum(axis=1) / 3.0
+    assert np.allclose(err_d.cpu().numpy(), want, rtol=1e-15, atol=1e-15)
