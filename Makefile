@@ -60,7 +60,7 @@ RENAME_FWD := -Dcollection_pass=nexel_ref_collection_pass -Dtexturing_pass=nexel
 
 ifneq ($(wildcard $(REF)/core/src/renderer.cpp),)
 dropin: $(DROPIN)/libnexel_dropin.so $(DROPIN)/test_oracle_dropin $(DROPIN)/test_dropin_backward \
-        $(DROPIN)/test_train_dropin $(DROPIN)/test_dropin_train $(DROPIN)/bench_train
+        $(DROPIN)/test_train_dropin $(DROPIN)/test_dropin_train $(DROPIN)/bench_train $(DROPIN)/acceptance_dropin
 else
 dropin:
 	@echo "reference sources not present; using the prebuilt $(DROPIN) if any"
@@ -110,6 +110,13 @@ TRAIN_TEST_OBJS := $(DROPIN)/ref_json_bundle.o $(DROPIN)/ref_json_synthetic.o $(
 $(DROPIN)/test_train_dropin: $(REF)/tests/test_train.cpp tests/cxx/doctest.h $(TRAIN_TEST_OBJS) $(DROPIN)/libnexel_dropin.so
 	$(CXX) $(DROPIN_CXX) -Itests/cxx -I$(REF)/tests -o $@ $< $(TRAIN_TEST_OBJS) -L$(DROPIN) -lnexel_dropin \
 	    -Wl,-rpath,'$$ORIGIN'
+
+# the reference's acceptance suite (tests/acceptance.cpp), unmodified; criterion 10 drives
+# the CLI, which is not built here (CLI11 absent), so it points at /bin/false. Criterion 4
+# compares two host expressions of the Gaussian bit for bit: no FP contraction in this TU.
+$(DROPIN)/acceptance_dropin: $(REF)/tests/acceptance.cpp $(TRAIN_TEST_OBJS) $(DROPIN)/libnexel_dropin.so
+	$(CXX) $(DROPIN_CXX) -ffp-contract=off -I$(REF)/tests '-DNEXEL_CLI_PATH="/bin/false"' -o $@ $< $(TRAIN_TEST_OBJS) -L$(DROPIN) \
+	    -lnexel_dropin -Wl,-rpath,'$$ORIGIN'
 
 $(DROPIN)/bench_train: tests/cxx/bench_train.cpp $(TRAIN_TEST_OBJS) $(DROPIN)/libnexel_dropin.so
 	$(CXX) $(DROPIN_CXX) -o $@ $< $(TRAIN_TEST_OBJS) -L$(DROPIN) -lnexel_dropin -Wl,-rpath,'$$ORIGIN'
