@@ -60,7 +60,8 @@ RENAME_FWD := -Dcollection_pass=nexel_ref_collection_pass -Dtexturing_pass=nexel
 
 ifneq ($(wildcard $(REF)/core/src/renderer.cpp),)
 dropin: $(DROPIN)/libnexel_dropin.so $(DROPIN)/test_oracle_dropin $(DROPIN)/test_dropin_backward \
-        $(DROPIN)/test_train_dropin $(DROPIN)/test_dropin_train $(DROPIN)/bench_train $(DROPIN)/acceptance_dropin
+        $(DROPIN)/test_train_dropin $(DROPIN)/test_dropin_train $(DROPIN)/bench_train $(DROPIN)/acceptance_dropin \
+        $(DROPIN)/test_renderer_dropin
 else
 dropin:
 	@echo "reference sources not present; using the prebuilt $(DROPIN) if any"
@@ -117,6 +118,10 @@ $(DROPIN)/test_train_dropin: $(REF)/tests/test_train.cpp tests/cxx/doctest.h $(T
 $(DROPIN)/acceptance_dropin: $(REF)/tests/acceptance.cpp $(TRAIN_TEST_OBJS) $(DROPIN)/libnexel_dropin.so
 	$(CXX) $(DROPIN_CXX) -ffp-contract=off -I$(REF)/tests '-DNEXEL_CLI_PATH="/bin/false"' -o $@ $< $(TRAIN_TEST_OBJS) -L$(DROPIN) \
 	    -lnexel_dropin -Wl,-rpath,'$$ORIGIN'
+
+# the reference's renderer tests (tests/test_renderer.cpp), unmodified
+$(DROPIN)/test_renderer_dropin: $(REF)/tests/test_renderer.cpp tests/cxx/doctest.h $(DROPIN)/libnexel_dropin.so
+	$(CXX) $(DROPIN_CXX) -Itests/cxx -I$(REF)/tests -o $@ $< -L$(DROPIN) -lnexel_dropin -Wl,-rpath,'$$ORIGIN'
 
 $(DROPIN)/bench_train: tests/cxx/bench_train.cpp $(TRAIN_TEST_OBJS) $(DROPIN)/libnexel_dropin.so
 	$(CXX) $(DROPIN_CXX) -o $@ $< $(TRAIN_TEST_OBJS) -L$(DROPIN) -lnexel_dropin -Wl,-rpath,'$$ORIGIN'

@@ -117,6 +117,8 @@ typedef struct nx_host_frame {
     float* residual;
     double* base_f64;  /* fp64 base (Eq. 6) kept for render_backward; download: copied if the
                           frame keeps it (nx_frame_set_backward); upload: makes the frame keep it */
+    double* residual_f64;  /* fp64 terminal transmittance, kept with the fp64 base (same rules) —
+                              FrameBuffers::residual at the reference's precision */
 } nx_host_frame;
 
 /* Per-frame binning / work statistics (read back with nx_frame_stats). */

@@ -110,6 +110,7 @@ class nx_host_frame(C.Structure):
         ("final_img", C.c_void_p),
         ("residual", C.c_void_p),
         ("base_f64", C.c_void_p),
+        ("residual_f64", C.c_void_p),
     ]
 
 

@@ -127,6 +127,7 @@ struct nx_frame {
     int list_tile = kWorkTile, ltiles_x = 0, ltiles_y = 0;  // tiles of the last built lists
     DevBuf base, ids, depths, weights, texture, final_img, residual;
     DevBuf base64;               // fp64 base kept for render_backward
+    DevBuf residual64;           // fp64 terminal transmittance, kept with base64
     DevBuf tex_f;                // texture features (split tensor-core texture pass)
     bool keep_backward = false;  // collection passes write base64
     bool base64_valid = false;   // base64 holds the last forward's (or an uploaded) base
@@ -233,7 +234,10 @@ int frame_shape(nx_ctx* c, nx_frame* f, int W, int H, int K, int tile) {
     NX_CUDA(c, f->depths.ensure(ns * sizeof(double)));
     NX_CUDA(c, f->weights.ensure(ns * sizeof(double)));
     NX_CUDA(c, f->texture.ensure(ns * 3 * sizeof(float)));
-    if (f->keep_backward) NX_CUDA(c, f->base64.ensure(npix * 3 * sizeof(double)));
+    if (f->keep_backward) {
+        NX_CUDA(c, f->base64.ensure(npix * 3 * sizeof(double)));
+        NX_CUDA(c, f->residual64.ensure(npix * sizeof(double)));
+    }
     f->W = W;
     f->H = H;
     f->K = K;
@@ -257,6 +261,7 @@ FrameDev frame_dev(const nx_frame* f) {
     d.final_img = f->final_img.as<float>();
     d.residual = f->residual.as<float>();
     d.base64 = f->keep_backward ? f->base64.as<double>() : nullptr;
+    d.residual64 = f->keep_backward ? f->residual64.as<double>() : nullptr;
     return d;
 }
 
@@ -819,7 +824,7 @@ void nx_frame_destroy(nx_frame* f) {
     if (!f) return;
     if (f->ctx) cudaSetDevice(f->ctx->device);
     for (DevBuf* b : {&f->base, &f->ids, &f->depths, &f->weights, &f->texture, &f->final_img, &f->residual,
-                      &f->tile_offsets, &f->base64, &f->tex_f})
+                      &f->tile_offsets, &f->base64, &f->residual64, &f->tex_f})
         b->release();
     if (f->ev_busy) cudaEventSynchronize(f->ev_busy);
     if (f->stats) cudaFree(f->stats);
@@ -882,6 +887,7 @@ int nx_frame_download(nx_ctx* c, const nx_frame* fc, const nx_host_frame* dst, v
     NX_CUDA(c, cp(dst->final_img, f->final_img, npix * 3 * sizeof(float)));
     NX_CUDA(c, cp(dst->residual, f->residual, npix * sizeof(float)));
     if (dst->base_f64 && f->base64_valid) NX_CUDA(c, cp(dst->base_f64, f->base64, npix * 3 * sizeof(double)));
+    if (dst->residual_f64 && f->base64_valid) NX_CUDA(c, cp(dst->residual_f64, f->residual64, npix * sizeof(double)));
     launch_stream_copy(jobs, s);
     NX_CUDA(c, cudaGetLastError());
     NX_CUDA(c, cudaEventRecord(f->ev_busy, s));
@@ -894,7 +900,7 @@ int nx_frame_upload(nx_ctx* c, nx_frame* f, int width, int height, int top_k, co
     if (!c || !f || !src || width < 0 || height < 0 || top_k < 0 || top_k > NX_MAX_TOP_K)
         return set_err(c, NX_INVALID_ARGUMENT, "bad frame upload");
     cudaSetDevice(c->device);
-    if (src->base_f64) f->keep_backward = true;
+    if (src->base_f64 || src->residual_f64) f->keep_backward = true;
     int st = frame_shape(c, f, width, height, top_k, 16);  // tiles are re-derived by collection_pass
     if (st) return st;
     cudaStream_t s = pick_stream(c, stream);
@@ -914,6 +920,7 @@ int nx_frame_upload(nx_ctx* c, nx_frame* f, int width, int height, int top_k, co
         NX_CUDA(c, cp(f->base64, src->base_f64, npix * 3 * sizeof(double)));
         f->base64_valid = true;
     }
+    NX_CUDA(c, cp(f->residual64, src->residual_f64, npix * sizeof(double)));
     return NX_OK;
 }
 

@@ -56,10 +56,15 @@ struct BwdHit {         // one evaluated (pixel, primitive) pair
     float rgb[3];       // B1: primitive colour; B2: w * dL/dfinal * clamp mask (unbuffered), else 0
     uint32_t flags;     // bits 0..2: SH clamp mask (B1)
 };
-// B3 overwrites a composited entry with its gradient values (float g[kStage]).
-union BwdEntry {
-    BwdHit h;
-    float g[kStage + 1];
+// B3 overwrites a composited entry with its gradient values (float g[kStage]); the
+// blended-error term w * err stays fp64 beside it (summed in fp64: the density
+// control's split keys depend on it).
+struct BwdEntry {
+    union {
+        BwdHit h;
+        float g[kStage + 1];
+    };
+    double werr64;
 };
 static_assert(sizeof(BwdHit) <= sizeof(float) * (kStage + 1), "the kernel terms fit the gradient row");
 constexpr uint16_t kComposited = 0x80;  // q entry flag set by B2 (list index j < kChunk)
@@ -329,6 +334,7 @@ __global__ void __launch_bounds__(kTile * kTile, 512 / (kTile * kTile)) composit
                 res.alpha = d_alpha;
                 res.d_t = d_t;
                 res.werr = w * errp;
+                sm.res[k].werr64 = res.werr;
                 res.rgb[0] = wdf[0];
                 res.rgb[1] = wdf[1];
                 res.rgb[2] = wdf[2];
@@ -390,6 +396,7 @@ __global__ void __launch_bounds__(kTile * kTile, 512 / (kTile * kTile)) composit
                 if (!hm) continue;
                 const int64_t row = static_cast<int64_t>(sm.id[sb + b]) * kPrimAccVals;
                 float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+                double werr = 0.0;  // lane 17: the blended error, in fp64
                 for (uint32_t m = hm; m; m &= m - 1) {
                     const int h = __ffs(m) - 1;
                     const int eh = __shfl_sync(0xffffffffu, my_e, h);
@@ -401,7 +408,8 @@ __global__ void __launch_bounds__(kTile * kTile, 512 / (kTile * kTile)) composit
                         s2 = fmaf(g[kActFields + 2], bk, s2);
                     } else {
                         s0 += g[av];
-                        if (av < kActFields - 16) s1 += g[av + 16];
+                        if (av == 0) s1 += g[16];
+                        else if (av == 1) werr += sm.res[eh].werr64;
                     }
                 }
                 if (sh_lane) {
@@ -413,7 +421,8 @@ __global__ void __launch_bounds__(kTile * kTile, 512 / (kTile * kTile)) composit
                     }
                 } else {
                     if (s0 != 0.f && av < n_act) xacc_add(acc, row + av, s0);
-                    if (av < kActFields - 16 && s1 != 0.f && av + 16 < n_act) xacc_add(acc, row + av + 16, s1);
+                    if (av == 0 && s1 != 0.f) xacc_add(acc, row + 16, s1);
+                    if (av == 1 && werr != 0.0 && 17 < n_act) xacc_add(acc, row + 17, werr);
                 }
             }
             __syncwarp();

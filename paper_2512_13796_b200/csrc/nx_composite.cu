@@ -256,6 +256,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
     if (in_img) {
         const int64_t pix = static_cast<int64_t>(py) * W + px;
         a.fb.residual[pix] = static_cast<float>(T);
+        if (a.fb.residual64) a.fb.residual64[pix] = T;
         acc[0] += T * a.st.background[0];
         acc[1] += T * a.st.background[1];
         acc[2] += T * a.st.background[2];

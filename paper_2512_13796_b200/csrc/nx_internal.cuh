@@ -167,6 +167,7 @@ struct FrameDev {
     float* texture;
     float* final_img;
     float* residual;
+    double* residual64;  // fp64 terminal transmittance (nullptr unless the frame keeps backward state)
     double* base64;  // optional fp64 base (backward state), nullptr if not kept
 };
 

@@ -162,17 +162,14 @@ void collection_pass(const Scene& scene, const Camera& cam, RenderResult& out) {
     std::lock_guard<std::mutex> lock(d.mu);
     const nx_camera c = to_nx(cam);
     check(d, nx_collection_pass(d.ctx, d.scene, &c, d.frame, nullptr));
-    const size_t npix = static_cast<size_t>(cam.width) * cam.height;
-    std::vector<float> residual(npix);
     nx_host_frame h{};
-    h.base_f64 = out.fb.base.data();  // the fp64 base (Eq. 6) the device kept
-    h.residual = residual.data();
+    h.base_f64 = out.fb.base.data();          // the fp64 base (Eq. 6) the device kept
+    h.residual_f64 = out.fb.residual.data();  // and the fp64 terminal transmittance
     h.ids = out.fb.ids.data();
     h.depths = out.fb.depths.data();
     h.weights = out.fb.weights.data();
     check(d, nx_frame_download(d.ctx, d.frame, &h, nullptr));
     check(d, nx_ctx_synchronize(d.ctx));
-    widen(residual, out.fb.residual);
     d.frame_owner = &out.fb;
 }
 
@@ -228,8 +225,8 @@ void render_backward(const Scene& scene, const Camera& cam, const FrameBuffers& 
     Device& d = bind(scene);
     std::lock_guard<std::mutex> lock(d.mu);
     const size_t npix = static_cast<size_t>(fb.width) * fb.height;
-    std::vector<float> texture(fb.texture.begin(), fb.texture.end()), residual(fb.residual.begin(), fb.residual.end());
-    std::vector<float> base32(fb.base.begin(), fb.base.end());
+    std::vector<float> texture(fb.texture.begin(), fb.texture.end());
+    std::vector<float> base32(fb.base.begin(), fb.base.end()), residual(fb.residual.begin(), fb.residual.end());
     nx_host_frame h{};
     h.base = base32.data();
     h.base_f64 = const_cast<double*>(fb.base.data());
@@ -238,6 +235,7 @@ void render_backward(const Scene& scene, const Camera& cam, const FrameBuffers& 
     h.weights = const_cast<double*>(fb.weights.data());
     h.texture = texture.data();
     h.residual = residual.data();
+    h.residual_f64 = const_cast<double*>(fb.residual.data());
     (void)npix;
     check(d, nx_frame_upload(d.ctx, d.frame, fb.width, fb.height, fb.top_k, &h, nullptr));
     d.frame_owner = nullptr;
