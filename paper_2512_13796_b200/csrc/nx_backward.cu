@@ -395,8 +395,11 @@ __global__ void __launch_bounds__(kTile * kTile, 512 / (kTile * kTile)) composit
                 const uint32_t hm = __ballot_sync(0xffffffffu, my_e >= 0);
                 if (!hm) continue;
                 const int64_t row = static_cast<int64_t>(sm.id[sb + b]) * kPrimAccVals;
+                // the blended error in fp64: a fixed-pattern warp tree over the pixels' terms
+                double werr = my_e >= 0 ? sm.res[my_e].werr64 : 0.0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) werr += __shfl_xor_sync(0xffffffffu, werr, o);
                 float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-                double werr = 0.0;  // lane 17: the blended error, in fp64
                 for (uint32_t m = hm; m; m &= m - 1) {
                     const int h = __ffs(m) - 1;
                     const int eh = __shfl_sync(0xffffffffu, my_e, h);
@@ -408,8 +411,7 @@ __global__ void __launch_bounds__(kTile * kTile, 512 / (kTile * kTile)) composit
                         s2 = fmaf(g[kActFields + 2], bk, s2);
                     } else {
                         s0 += g[av];
-                        if (av == 0) s1 += g[16];
-                        else if (av == 1) werr += sm.res[eh].werr64;
+                        if (av < kActFields - 16) s1 += g[av + 16];
                     }
                 }
                 if (sh_lane) {
