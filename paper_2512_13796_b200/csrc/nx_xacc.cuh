@@ -12,9 +12,10 @@
 //
 // Layout: value i of an accumulator with m values owns words w[k * m + i] for
 // k < kXaccWords, plus a flags word w[kXaccWords * m + i] (+inf / -inf / NaN addends).
-// Range: addends below 2^kXaccE0 (~2.9e-39) are dropped; fp32 addends up to 2^55 and
-// fp64 addends up to 2^52 are exact, larger ones saturate to +-inf. Each word takes
-// < 2^32 per addend, so 2^31 addends per value cannot overflow it.
+// Range: the bits of an addend below 2^kXaccE0 (~2.9e-39) are dropped (toward zero), so
+// fp32 addends above 2^-104 and fp64 addends above 2^-75 (~2.6e-23) keep every bit;
+// fp32 addends up to 2^55 and fp64 addends up to 2^52 fit, larger ones saturate to +-inf.
+// Each word takes < 2^32 per addend, so 2^31 addends per value cannot overflow it.
 // Readers (xacc_take) zero what they read: accumulators stay zero between uses.
 #pragma once
 #include <cstdint>
