@@ -575,6 +575,25 @@ def run_ours(args):
     achieved = dom_bytes / (stage_ms[dom] / 1e3) / 1e9
     fbytes = frame_bytes(args.nexels, P, H, W, K, Q)
     frame_gbs = fbytes * (args.steps / (ms_local / 1e3)) / 1e9
+    # the texture decoder on the tensor cores (north star: tensor-pipe utilisation for the
+    # decoder): the MLP's algorithmic flops per query over its event-timed stage
+    decoder = None
+    dec_ms = stage_ms.get("texture_mlp", 0.0)
+    if dec_ms > 0:
+        dec_flops = Q * 2 * (32 * 64 + 64 * 64 + 64 * 48)
+        bf16_peak = float(peaks.get("bf16_tflops", 1590.0))  # fallback: B200_PROFILING.md
+        dec_tf = dec_flops / (dec_ms / 1e3) / 1e12
+        pipe = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+                pipe = json.load(fh).get("tex_mlp", {}).get("tensor_pipe_pct")
+        except (OSError, ValueError):
+            pass
+        decoder = {"bound": "tensor", "kernel": "tex_mlp (tcgen05, 3-term bf16 split)", "achieved": dec_tf,
+                   "unit": "TFLOP/s", "peak": bf16_peak, "frac": dec_tf / bf16_peak,
+                   "peak_source": "measured" if "bf16_tflops" in peaks else "fallback",
+                   "executed_tflops": 3 * dec_tf, "flops_per_launch": dec_flops, "launch_ms": dec_ms,
+                   "tensor_pipe_pct_ncu": pipe}
 
     train = None
     if args.train_steps > 0:  # reported beside the headline; a failure here never voids it
@@ -602,6 +621,7 @@ def run_ours(args):
                          "bytes_per_launch": dom_bytes, "launch_ms": stage_ms[dom]},
             "frame_roofline": {"bytes_per_frame": fbytes, "achieved": frame_gbs, "peak": hbm_peak, "unit": "GB/s",
                                "frac": frame_gbs / hbm_peak, "formula": "240N + 8P + (28+24K)HW + 1024Q + 36864"},
+            "decoder_roofline": decoder,
             "stages_ms": stage_ms, "profiled_frames": prof_frames,
             "work": {"tile_keys_P": P, "work_keys": Pw, "queries_Q": Q},
             "cpu_baseline": cpu,

@@ -156,8 +156,9 @@ int nx_ctx_join(nx_ctx* ctx);
 #define NX_STAGE_EMIT 2
 #define NX_STAGE_TILE_SORT 3
 #define NX_STAGE_COMPOSITE 4
-#define NX_STAGE_TEXTURE 5
-#define NX_NUM_STAGES 6
+#define NX_STAGE_TEXTURE 5      /* the whole texture pass */
+#define NX_STAGE_TEXTURE_MLP 6  /* its tensor-core decoder (0 on the fused / SIMT paths) */
+#define NX_NUM_STAGES 7
 int nx_ctx_set_profiling(nx_ctx* ctx, int enable);
 /* Mean per-stage device time (ms per frame) over the profiled frames since the last
  * call, then resets; synchronises. Stage events bracket each stage on the stream. */

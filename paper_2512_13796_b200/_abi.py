@@ -27,8 +27,8 @@ NX_NO_DEVICE = 14
 NX_MAX_TOP_K = 8
 NX_PARAMS_PER_NEXEL = 60
 NX_SH_VALUES = 48
-NX_NUM_STAGES = 6
-STAGE_NAMES = ("preprocess", "depth_sort", "emit", "tile_sort", "composite", "texture")
+NX_NUM_STAGES = 7
+STAGE_NAMES = ("preprocess", "depth_sort", "emit", "tile_sort", "composite", "texture", "texture_mlp")
 
 STATUS_CODES = {
     NX_BAD_SETTINGS: "bad-settings",

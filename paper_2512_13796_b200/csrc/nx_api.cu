@@ -69,11 +69,12 @@ struct DevBuf {
 
 std::atomic<unsigned long long> g_launches{0};
 
-const char* kStageNames[NX_NUM_STAGES] = {"preprocess", "depth_sort", "emit", "tile_sort", "composite", "texture"};
+const char* kStageNames[NX_NUM_STAGES] = {"preprocess", "depth_sort", "emit",   "tile_sort",
+                                          "composite",  "texture",    "texture_mlp"};
 
 // Profiling event points per frame (stage k spans two points; the texture pass may
 // run on the second stream, so it has its own start/end points).
-enum EvPoint { kEvPre, kEvDepth, kEvEmit, kEvTileSort, kEvComp, kEvCompEnd, kEvTex, kEvTexEnd, kEvPoints };
+enum EvPoint { kEvPre, kEvDepth, kEvEmit, kEvTileSort, kEvComp, kEvCompEnd, kEvTex, kEvTexMid, kEvTexEnd, kEvPoints };
 constexpr int kEvSets = 4;
 
 }  // namespace
@@ -292,8 +293,8 @@ void fold_set(nx_ctx* c, int set, bool wait) {
         cudaGetLastError();
         return;
     }
-    static const int kFrom[NX_NUM_STAGES] = {kEvPre, kEvDepth, kEvEmit, kEvTileSort, kEvComp, kEvTex};
-    static const int kTo[NX_NUM_STAGES] = {kEvDepth, kEvEmit, kEvTileSort, kEvComp, kEvCompEnd, kEvTexEnd};
+    static const int kFrom[NX_NUM_STAGES] = {kEvPre, kEvDepth, kEvEmit, kEvTileSort, kEvComp, kEvTex, kEvTexMid};
+    static const int kTo[NX_NUM_STAGES] = {kEvDepth, kEvEmit, kEvTileSort, kEvComp, kEvCompEnd, kEvTexEnd, kEvTexEnd};
     for (int i = 0; i < NX_NUM_STAGES; ++i) {
         float v = 0.f;
         if (cudaEventElapsedTime(&v, c->ev[set][kFrom[i]], c->ev[set][kTo[i]]) == cudaSuccess) c->stage_acc[i] += v;
@@ -477,12 +478,14 @@ int texturing(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* 
     ta.fb = frame_dev(f);
     ta.stats = f->stats;
     ta.fscratch = nullptr;
+    ta.ev_mid = c->profiling ? c->ev[c->ev_cur][kEvTexMid] : nullptr;  // recorded between gathers and decoder
     if (texture_tc_supported(scene->st.top_k > 0 ? scene->field : nx_field_desc{}) && f->K > 0) {
         NX_CUDA(c, f->tex_f.ensure(static_cast<size_t>(f->W) * f->H * f->K * 32 * sizeof(float)));
         ta.fscratch = f->tex_f.as<float>();
     }
     const int st = launch_texture(ta, s);
     if (st) return set_err(c, st, "texture field shape not supported (n_in <= 64, n_hidden <= 128)");
+    if (c->profiling && !ta.ev_mid_recorded) record(c, kEvTexMid, s);  // no separate decoder launch
     record(c, kEvTexEnd, s);
     if (c->profiling) c->ev_pending[c->ev_cur] = true;
     NX_CUDA(c, cudaEventRecord(f->ev_busy, s));

@@ -232,6 +232,8 @@ struct TextureArgs {
     FrameDev fb;
     FrameStatsD* stats;
     float* fscratch;  // H*W*K*32 interpolated features (split tensor-core path), per frame
+    cudaEvent_t ev_mid = nullptr;          // profiling: recorded between the gathers and the decoder
+    mutable bool ev_mid_recorded = false;  // set by the launcher when it recorded ev_mid
 };
 int launch_texture(const TextureArgs& a, cudaStream_t s);  // returns NX_OK / NX_UNSUPPORTED
 // tcgen05 variant for the reference field shape (16 levels x 2 features, 64 hidden).

@@ -543,6 +543,10 @@ int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
         cudaFuncSetAttribute(tex_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemUsed);
         count_launch(2);
         tex_features_kernel<<<static_cast<unsigned>((total + 127) / 128), 128, 0, s>>>(a, cst, total);
+        if (a.ev_mid) {
+            cudaEventRecord(a.ev_mid, s);
+            a.ev_mid_recorded = true;
+        }
         const int64_t grid = std::min<int64_t>(n_tiles, static_cast<int64_t>(kCtasPerSm) * sms);
         tex_mlp_kernel<<<static_cast<unsigned>(grid), kTcThreads, kSmemUsed, s>>>(a, ppt, n_tiles);
         return NX_OK;
