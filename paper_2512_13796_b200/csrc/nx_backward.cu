@@ -203,12 +203,18 @@ __global__ void __launch_bounds__(kTile * kTile, 512 / (kTile * kTile)) composit
         if (!__any_sync(0xffffffffu, active)) break;
         const int cn = min(kChunk, list_end - cb);
         __syncwarp();
-        if (lane < cn) {
+        if (lane < cn) {  // the prefilter records, gathered by id, with cp.async (as the forward)
             const int32_t id = __ldg(a.list_ids + cb + lane);
             sm.id[lane] = id;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) sm.f[lane][q] = __ldg(a.recf + static_cast<int64_t>(id) * 4 + q);
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&sm.f[lane][q]));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                             "l"(a.recf + static_cast<int64_t>(id) * 4 + q)
+                             : "memory");
+            }
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
         for (int sb = 0; sb < cn; sb += kSub) {
             const int sn = min(kSub, cn - sb);

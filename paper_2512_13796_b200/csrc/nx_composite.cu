@@ -110,12 +110,18 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
     for (int cb = list_begin; cb < list_end; cb += kChunk) {
         const int cn = min(kChunk, list_end - cb);
         __syncthreads();
+        // the chunk's fp32 prefilter records (gathered by id) into shared memory with
+        // asynchronous 16-byte copies (cp.async: global -> shared without a register trip)
         for (int e = threadIdx.x; e < cn * 4; e += kThreads) {
             const int j = e >> 2, q = e & 3;
             const int32_t id = __ldg(a.list_ids + cb + j);
-            sm.f[j][q] = __ldg(a.recf + static_cast<int64_t>(id) * 4 + q);
+            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&sm.f[j][q]));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                         "l"(a.recf + static_cast<int64_t>(id) * 4 + q)
+                         : "memory");
             if (q == 0) sm.id[j] = id;
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         if (__any_sync(0xffffffffu, active)) {
             for (int sb = 0; sb < cn; sb += kSub) {
