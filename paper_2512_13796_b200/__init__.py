@@ -7,12 +7,12 @@ Drop-in for the reference's ``nexel::render`` / ``collection_pass`` /
 reference interface.
 """
 from .api import (Camera, band_camera, image_bands, DeviceFrame, DeviceScene, FrameBuffers, HashGridConfig, NexelError, RenderResult,
-                  LossWeights, RenderSettings, Renderer, Scene, SceneGrads, TextureField, UpstreamGrads, collection_pass, render,
+                  LossWeights, Optimizer, RenderSettings, Renderer, Scene, SceneGrads, TextureField, UpstreamGrads, collection_pass, render,
                   losses_backward, render_backward, ring_camera, stump_like, texturing_pass)
 from . import _abi
 
 __all__ = [
     "Camera", "band_camera", "image_bands", "DeviceFrame", "DeviceScene", "FrameBuffers", "HashGridConfig", "NexelError", "RenderResult",
-    "LossWeights", "RenderSettings", "Renderer", "Scene", "SceneGrads", "TextureField", "UpstreamGrads", "collection_pass",
+    "LossWeights", "Optimizer", "RenderSettings", "Renderer", "Scene", "SceneGrads", "TextureField", "UpstreamGrads", "collection_pass",
     "losses_backward", "render", "render_backward", "ring_camera", "stump_like", "texturing_pass", "_abi",
 ]

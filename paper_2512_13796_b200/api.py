@@ -499,6 +499,15 @@ class Renderer:
         self._check(self.lib.nx_scene_download(self.ctx, dscene.handle, _dp(nex), *(_dp(a) for a in arrs)))
         return (nex, *arrs)
 
+    def optimizer(self, dscene: DeviceScene) -> "Optimizer":
+        """fp64 Adam state for the device scene (nx_optimizer_create)."""
+        return Optimizer(self, dscene)
+
+    def pixel_error(self, frame: DeviceFrame, gt_device_ptr: int, err_device_ptr: int, stream: int = 0):
+        """err[p] = sum_c |final - gt| / 3 on the device (trainer.cpp:288-295); device pointers."""
+        self._check(self.lib.nx_pixel_error(self.ctx, frame.handle, C.c_void_p(gt_device_ptr),
+                                            C.c_void_p(err_device_ptr), C.c_void_p(stream) if stream else None))
+
     def synchronize(self):
         self._check(self.lib.nx_ctx_synchronize(self.ctx))
 
@@ -543,6 +552,62 @@ class Renderer:
 
 # ---------------------------------------------------------------- reference-style value API
 _default: dict = {}
+
+
+class Optimizer:
+    """The trainer's Adam over the 11 parameter groups (adam.cpp:9-42, trainer.cpp:238-323)
+    on a device scene: fp64 moments, fp64 masters of the fp32-stored groups. Groups are
+    numbered like ParamGroup (trainer.hpp:64-77): position, quat, scale, opacity, gamma,
+    sh_dc, sh_rest, grid, w1, w2, w3."""
+    GROUPS = ("position", "quat", "scale", "opacity", "gamma", "sh_dc", "sh_rest", "grid", "w1", "w2", "w3")
+
+    def __init__(self, renderer: Renderer, dscene: DeviceScene):
+        self.r, self.ds = renderer, dscene
+        self.handle = C.c_void_p()
+        renderer._check(renderer.lib.nx_optimizer_create(renderer.ctx, dscene.handle, C.byref(self.handle)))
+
+    def step(self, grads_device: Sequence[int], configs: Sequence[Sequence[float]], stream: int = 0):
+        """One adam_step per group from device SceneGrads pointers (prims, table, w1, w2,
+        w3); configs: 11 (lr, beta1, beta2, eps); lr < 0 skips a group."""
+        g = _abi.nx_grads(*grads_device)
+        cfg = (_abi.nx_adam_config * _abi.NX_NUM_GROUPS)(*[_abi.nx_adam_config(*c) for c in configs])
+        self.r._check(self.r.lib.nx_optimizer_step(self.r.ctx, self.handle, self.ds.handle, C.byref(g), cfg,
+                                                   C.c_void_p(stream) if stream else None))
+
+    def steps(self):
+        out = (C.c_int64 * _abi.NX_NUM_GROUPS)()
+        self.r._check(self.r.lib.nx_optimizer_steps(self.handle, out))
+        return list(out)
+
+    def size(self, group: int) -> int:
+        n = C.c_int64()
+        self.r._check(self.r.lib.nx_optimizer_size(self.handle, group, C.byref(n)))
+        return n.value
+
+    def set_params(self, group: int, values: np.ndarray):
+        """Exact fp64 values of a group in its row layout (e.g. the unrounded initialisation)."""
+        v = np.ascontiguousarray(values, np.float64).reshape(-1)
+        self.r._check(self.r.lib.nx_optimizer_set_params(self.r.ctx, self.handle, self.ds.handle, group, _dp(v),
+                                                         v.size))
+
+    def download(self, group: int):
+        """(params, m, v) of a group as float64 arrays."""
+        n = self.size(group)
+        p, m, v = np.zeros(n), np.zeros(n), np.zeros(n)
+        self.r._check(self.r.lib.nx_optimizer_download(self.r.ctx, self.handle, self.ds.handle, group, _dp(p), _dp(m),
+                                                       _dp(v)))
+        return p, m, v
+
+    def close(self):
+        if self.handle:
+            self.r.lib.nx_optimizer_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 — interpreter shutdown
+            pass
 
 
 def _renderer(device: int = 0) -> Renderer:

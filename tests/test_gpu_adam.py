@@ -74,17 +74,13 @@ def test_fp64_masters_track_the_reference_exactly(renderer, reference):
     fp64 rounding, not just fp32 (the scene keeps their fp32 rounding for rendering)."""
     scene = nx.stump_like(500, log2_table=8, grid_init=1e-1)
     ds = renderer.upload(scene)
-    opt = C.c_void_p()
-    renderer._check(renderer.lib.nx_optimizer_create(renderer.ctx, ds.handle, C.byref(opt)))
+    opt = renderer.optimizer(ds)
     f = scene.field
     init = {5: scene.nexels[:, 12:15], 6: scene.nexels[:, 15:60], 7: f.table, 8: f.w1, 9: f.w2, 10: f.w3}
-    # seed the masters exactly (here the values are fp32-representable anyway) and read back
+    # seed the masters exactly (here the values are fp32-representable anyway)
     for gi, vals in init.items():
-        host = np.ascontiguousarray(vals, dtype=np.float64).reshape(-1)
-        renderer._check(renderer.lib.nx_optimizer_set_params(renderer.ctx, opt, ds.handle, gi,
-                                                             host.ctypes.data_as(C.POINTER(C.c_double)), host.size))
+        opt.set_params(gi, vals)
     cfgs = [(1e-3, 0.9, 0.999, 1e-8)] * 11
-    ccfg = (_abi.nx_adam_config * 11)(*[_abi.nx_adam_config(*c) for c in cfgs])
     rng = np.random.default_rng(7)
     ref = {gi: np.ascontiguousarray(v, dtype=np.float64).reshape(-1).copy() for gi, v in init.items()}
     state = {}
@@ -92,31 +88,23 @@ def test_fp64_masters_track_the_reference_exactly(renderer, reference):
         g_prims = rng.standard_normal((500, 60))
         g_f = [rng.standard_normal(np.size(a)) for a in (f.table, f.w1, f.w2, f.w3)]
         dev = [torch.tensor(a.reshape(-1), dtype=torch.float64, device="cuda") for a in (g_prims, *g_f)]
-        gg = _abi.nx_grads(*(t.data_ptr() for t in dev))
         torch.cuda.synchronize()
-        renderer._check(renderer.lib.nx_optimizer_step(renderer.ctx, opt, ds.handle, C.byref(gg), ccfg, None))
+        opt.step([t.data_ptr() for t in dev], cfgs)
         renderer.synchronize()
         grads = {5: g_prims[:, 12:15], 6: g_prims[:, 15:60], 7: g_f[0], 8: g_f[1], 9: g_f[2], 10: g_f[3]}
         for gi in ref:
             gr = np.ascontiguousarray(grads[gi]).reshape(-1)
             m, v, st = state.get(gi, (np.zeros(gr.size), np.zeros(gr.size), 0))
             state[gi] = (m, v, reference.adam_step(m, v, st, cfgs[gi], ref[gi], gr))
+    assert opt.steps() == [4] * 11
     for gi, want in ref.items():
-        n = C.c_int64()
-        renderer.lib.nx_optimizer_size(opt, gi, C.byref(n))
-        assert n.value == want.size
-        got, m, v = np.empty(want.size), np.empty(want.size), np.empty(want.size)
-        renderer._check(renderer.lib.nx_optimizer_download(renderer.ctx, opt, ds.handle, gi, _abi_ptr(got), _abi_ptr(m),
-                                                           _abi_ptr(v)))
+        assert opt.size(gi) == want.size
+        got, m, v = opt.download(gi)
         # fp64 on both sides (the device contracts some products into FMAs): a few ulp of
         # each array's scale
         for a, b in ((got, want), (m, state[gi][0]), (v, state[gi][1])):
             assert np.abs(a - b).max() <= 1e-13 * np.abs(b).max(), gi
-    renderer.lib.nx_optimizer_destroy(opt)
-
-
-def _abi_ptr(a):
-    return a.ctypes.data_as(C.POINTER(C.c_double))
+    opt.close()
 
 
 def test_pixel_error_matches_the_trainer(renderer):
@@ -131,8 +119,7 @@ def test_pixel_error_matches_the_trainer(renderer):
     gt_d = torch.tensor(gt, dtype=torch.float64, device="cuda")
     err_d = torch.empty(cam.width * cam.height, dtype=torch.float64, device="cuda")
     torch.cuda.synchronize()
-    renderer._check(renderer.lib.nx_pixel_error(renderer.ctx, fr.handle, C.c_void_p(gt_d.data_ptr()),
-                                                C.c_void_p(err_d.data_ptr()), None))
+    renderer.pixel_error(fr, gt_d.data_ptr(), err_d.data_ptr())
     renderer.synchronize()
     want = np.abs(fin - gt).reshape(-1, 3).sum(axis=1) / 3.0
     assert np.allclose(err_d.cpu().numpy(), want, rtol=1e-15, atol=1e-15)
