@@ -96,6 +96,13 @@ struct nx_ctx {
     nx_frame* bwd_lists = nullptr;   // work lists of the re-binned camera
     DevBuf d_t_slot, act_grad, xacc_prims;
     DevBuf dens_map, dens_par, dens_src;  // density-control maps (grow-only)
+    // provenance of the work lists / records in the shared buffers (rec, recf, tile keys):
+    // render_backward reuses a forward's lists when nothing rebuilt them since
+    uint64_t lists_gen = 0;
+    const nx_scene* lists_scene = nullptr;
+    uint64_t lists_scene_version = 0;
+    nx_camera lists_cam{};
+    int lists_tile = 0;
     DevBuf h_up[3], h_err, h_blend, h_grads[5];  // device copies for nx_render_backward_host
     DevBuf loss_scratch, h_gt, h_terms;          // losses_backward
     FieldBwdScratch field_bwd;                    // tensor-core field backward
@@ -111,11 +118,18 @@ struct nx_ctx {
     int stage_frames = 0;
 };
 
+// Scene versions are unique across scenes (a new scene may reuse a freed one's address).
+uint64_t next_scene_version() {
+    static std::atomic<uint64_t> v{0};
+    return ++v;
+}
+
 struct nx_scene {
     nx_ctx* ctx = nullptr;
     int64_t n = 0;
     DevBuf geom, sh, table, w1, w2, w3;
     DevBuf geom_spare, sh_spare;  // density control rebuilds into these and swaps (grow-only)
+    uint64_t version = next_scene_version();  // new on every change of parameters or settings
     nx_field_desc field{};
     nx_settings st{};
     int bad_status = NX_OK;
@@ -134,6 +148,7 @@ struct nx_frame {
     bool base64_valid = false;   // base64 holds the last forward's (or an uploaded) base
     DevBuf tile_offsets;  // n_tiles + 1 (the work lists' ranges of the last collection pass)
     DevBuf list_ids;
+    uint64_t lists_gen = 0;  // the ctx's list build these lists came from (0: none)
     FrameStatsD* stats = nullptr;  // device
     int64_t n_nexels = 0;
     cudaEvent_t ev_ready = nullptr;  // collection pass of this frame done
@@ -427,6 +442,12 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
     f->list_ids.p = t_in_b ? c->tvals_b.p : c->tvals_a.p;  // borrowed (not owned)
     f->list_ids.cap = 0;
     *total_keys = n_keys;
+    c->lists_gen += 1;
+    f->lists_gen = reference_lists ? 0 : c->lists_gen;
+    c->lists_scene = scene;
+    c->lists_scene_version = scene->version;
+    c->lists_cam = cam;
+    c->lists_tile = reference_lists ? 0 : lt;
     NX_CUDA(c, cudaGetLastError());
     return NX_OK;
 }
@@ -780,6 +801,7 @@ int nx_scene_load_nexl(nx_ctx* c, const char* path, nx_scene** out, nx_nexl_info
 
 int nx_scene_set_settings(nx_ctx* c, nx_scene* s, const nx_settings* settings) {
     if (!s || !settings) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    if (std::memcmp(&s->st, settings, sizeof(nx_settings)) != 0) s->version = next_scene_version();
     s->st = *settings;
     return NX_OK;
 }
@@ -1009,10 +1031,28 @@ int nx_render_backward(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, n
     int64_t total = 0;
     const bool prof = c->profiling;
     c->profiling = false;  // the stage events describe forward frames only
-    // 16x16 work tiles, unless that gives fewer than ~4 CTAs per SM (small images)
-    const int64_t tiles16 = static_cast<int64_t>((cam->width + 15) / 16) * ((cam->height + 15) / 16);
-    const int bwd_tile = tiles16 < 4 * c->sms ? 8 : kBwdTile;
-    st = build_lists(c, scene, *cam, lf, 0, s, &total, bwd_tile);
+    // 8x8 work tiles (measured at config 2: 6.1 ms vs 6.6 ms with 16x16 — shorter lists per
+    // warp; and small images keep enough CTAs); NX_BWD_TILE=16 selects the 16x16 variant
+    static const int forced_tile = [] {
+        const char* e = std::getenv("NX_BWD_TILE");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int bwd_tile = forced_tile == 16 ? 16 : 8;
+    // The reference re-bins here (renderer.cpp:257); the forward's work lists of this frame
+    // are the same lists when nothing has rebuilt the shared list buffers since, for the same
+    // scene version and camera — then they (and the primitive records) are reused.
+    const nx_camera& lc = c->lists_cam;
+    const bool same_cam = lc.width == cam->width && lc.height == cam->height && lc.fx == cam->fx &&
+                          lc.fy == cam->fy && lc.cx == cam->cx && lc.cy == cam->cy &&
+                          std::memcmp(lc.R, cam->R, sizeof lc.R) == 0 && std::memcmp(lc.t, cam->t, sizeof lc.t) == 0;
+    const bool reuse = bwd_tile == kWorkTile && f->lists_gen != 0 && f->lists_gen == c->lists_gen &&
+                       c->lists_scene == scene && c->lists_scene_version == scene->version &&
+                       c->lists_tile == kWorkTile && same_cam;
+    if (reuse) {
+        lf = f;
+    } else {
+        st = build_lists(c, scene, *cam, lf, 0, s, &total, bwd_tile);
+    }
     c->profiling = prof;
     if (st) return st;
 
@@ -1269,6 +1309,7 @@ int nx_optimizer_set_params(nx_ctx* c, nx_optimizer* o, nx_scene* scene, int gro
         return set_err(c, NX_INVALID_ARGUMENT, "optimizer_set_params: bad group or size");
     if (count == 0) return NX_OK;
     cudaSetDevice(c->device);
+    scene->version = next_scene_version();
     cudaStream_t s = c->stream;
     DevBuf rows;
     NX_CUDA(c, rows.ensure(count * sizeof(double)));
@@ -1339,6 +1380,7 @@ int nx_optimizer_step(nx_ctx* c, nx_optimizer* o, nx_scene* scene, const nx_grad
     if (scene->n != o->n) return set_err(c, NX_INVALID_ARGUMENT, "optimizer_step: the scene changed size");
     cudaSetDevice(c->device);
     cudaStream_t s = pick_stream(c, stream);
+    scene->version = next_scene_version();
     const SceneDev sd = scene_dev(scene);
     for (int gi = 0; gi < NX_NUM_GROUPS; ++gi) {
         if (cfg[gi].lr < 0.0 || o->size[gi] == 0) continue;
@@ -1400,6 +1442,7 @@ int apply_row_map(nx_ctx* c, nx_scene* scene, nx_optimizer* opt, int64_t n_new, 
     std::swap(scene->geom, scene->geom_spare);
     if (!sh_done) std::swap(scene->sh, scene->sh_spare);
     scene->n = n_new;
+    scene->version = next_scene_version();
     return NX_OK;
 }
 }  // namespace

@@ -36,8 +36,8 @@ namespace nx {
 
 namespace {
 
-// One thread per pixel of the work tile: 16x16 (8 warps of 8x4 pixels) for large
-// images, 8x8 (2 warps) when 16x16 tiles would leave the GPU short of CTAs.
+// One thread per pixel of the work tile: 8x8 (2 warps of 8x4 pixels, the forward's work
+// tiles, so the forward's lists can be reused) or 16x16 (8 warps; NX_BWD_TILE=16).
 constexpr int kChunk = 32;                      // primitives staged per warp round
 constexpr int kSub = 2;                         // primitives pooled per B1/B2/B3 round
 constexpr int kPool = 32 * kSub;

@@ -29,7 +29,7 @@ constexpr int kGeomFields = 12;            // fp64 geometry params per primitive
 constexpr int kWorkTile = 8;
 // The reverse march (render_backward) walks 16x16-pixel work lists: its CTAs are
 // 8 warps that share per-primitive gradient accumulators in shared memory.
-constexpr int kBwdTile = 16;  // render_backward work tiles (8 when 16 leaves the GPU short of CTAs)
+constexpr int kBwdTile = 8;  // render_backward work tiles (the forward's; 16 selectable)
 
 // ---------------------------------------------------------------- scalar helpers
 // sigmoid / softplus (vec_math.hpp:69-84)

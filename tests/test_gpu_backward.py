@@ -194,3 +194,41 @@ def test_value_api_render_backward(reference):
     nx.render_backward(scene, cam, res.fb, up, g, err, res.blended_error)
     r = ref_backward(reference, scene, cam, up, err)
     compare_grads((g.prims, g.table, g.w1, g.w2, g.w3, res.blended_error), r)
+
+
+def test_backward_reuses_or_rebuilds_the_forward_lists_identically(renderer, reference):
+    """render_backward reuses the frame's forward work lists when nothing rebuilt them since
+    (same scene version and camera) and re-bins otherwise (renderer.cpp:257): both give the
+    same bits."""
+    scene = nx.stump_like(20_000, log2_table=14, grid_init=1e-1)
+    cam_a, cam_b = nx.ring_camera(3, 256, 256, 192), nx.ring_camera(90, 256, 256, 192)
+    K = scene.settings.top_k
+    up = upstream(cam_a, K, 9)
+    err = np.random.default_rng(4).random(cam_a.width * cam_a.height)
+    ds = renderer.upload(scene)
+    fa, fb = renderer.frame(), renderer.frame()
+    fa.set_backward(True)
+    fb.set_backward(True)
+
+    def backward(frame):
+        g = SceneGrads.allocate(scene)
+        be = np.zeros(scene.nexels.shape[0])
+        renderer.render_backward(ds, cam_a, frame, up, g, err, be)
+        return (g.prims, g.table, g.w1, g.w2, g.w3, be)
+
+    renderer.render(ds, cam_a, fa)
+    reused = backward(fa)               # right after its forward: the lists are reused
+    renderer.render(ds, cam_b, fb)      # another frame rebuilds the shared lists
+    rebuilt = backward(fa)              # so this one re-bins
+    for a, b in zip(reused, rebuilt):
+        assert np.array_equal(a, b)
+    renderer.render(ds, cam_a, fa)
+    again = backward(fa)                # reused again after a fresh forward
+    st = scene.settings
+    st.no_downweight = True             # a settings change makes a new scene version ...
+    ds.set_settings(st)
+    st.no_downweight = False
+    ds.set_settings(st)
+    after_settings = backward(fa)       # ... so this re-bins, with the original settings
+    for a, b, c in zip(reused, again, after_settings):
+        assert np.array_equal(a, b) and np.array_equal(a, c)
