@@ -37,6 +37,10 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kChunk = NX_COMPOSITE_CHUNK;       // primitives staged per round
 constexpr int kSub = NX_COMPOSITE_SUB;           // primitives pooled per B1/B2 round (<= 256 entries per warp)
 constexpr int kPool = 32 * kSub;
+#ifndef NX_COMPOSITE_B1_UNROLL
+#define NX_COMPOSITE_B1_UNROLL 1
+#endif
+constexpr int kB1Unroll = NX_COMPOSITE_B1_UNROLL;  // B1 evaluations interleaved per lane (measured: 1)
 constexpr int kRecPairs = REC_FIELDS / 2;        // double2 per fp64 record (10)
 static_assert(kWorkTile == 8, "warp blocks are 8x4 pixels");
 
@@ -160,6 +164,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                 }
                 __syncwarp();
                 // ---- B1. exact fp64 evaluation of the pooled pairs, all lanes busy
+#pragma unroll kB1Unroll
                 for (int e = lane; e < total; e += 32) {
                     const int ent = sm.q[warp][e];
                     const int owner = ent >> 8, j = ent & 0xff;
