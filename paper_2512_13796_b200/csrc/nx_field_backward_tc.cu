@@ -132,23 +132,51 @@ __global__ void __launch_bounds__(128) features_kernel(const FieldBwdArgs a, con
 
 // The listed slots' masks re-decided with the reference's fp64 forward: grid_lookup
 // (hash_grid.cpp:26-83) and TextureMlp::forward (mlp.cpp:24-43) in fp64, eval_sh_cached's
-// clamp (sh.hpp:61-73).
-__global__ void __launch_bounds__(128) mask_fp64_kernel(const FieldBwdArgs a, const int32_t* __restrict__ amb_list,
-                                                        const int32_t* __restrict__ amb_count, float* __restrict__ fbuf) {
+// clamp (sh.hpp:61-73). One warp per listed slot: lanes 0..15 take a level of the grid
+// lookup each, then lane j forms outputs j and j + 32 of each layer — every dot product
+// in the reference's order (inputs ascending), from transposed weights in shared memory
+// (conflict-free) — and lane 0 sums the SH clamp terms in the reference's order.
+constexpr int kMaskWarps = 4;
+struct MaskSmem {
+    float w1t[kIn][kHid];   // w1 transposed: [input][output]
+    float w2t[kHid][kHid];
+    float w3t[kHid][kOut];
+    double x[kMaskWarps][kIn];
+    double h1[kMaskWarps][kHid];
+    double h2[kMaskWarps][kHid];
+    double y[kMaskWarps][kOut];
+};
+
+__global__ void __launch_bounds__(32 * kMaskWarps) mask_fp64_kernel(const FieldBwdArgs a,
+                                                                    const int32_t* __restrict__ amb_list,
+                                                                    const int32_t* __restrict__ amb_count,
+                                                                    float* __restrict__ fbuf) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    MaskSmem& sm = *reinterpret_cast<MaskSmem*>(smem_raw);
+    for (int e = threadIdx.x; e < kHid * kIn; e += blockDim.x) sm.w1t[e % kIn][e / kIn] = __ldg(a.scene.w1 + e);
+    for (int e = threadIdx.x; e < kHid * kHid; e += blockDim.x) sm.w2t[e % kHid][e / kHid] = __ldg(a.scene.w2 + e);
+    for (int e = threadIdx.x; e < kOut * kHid; e += blockDim.x) sm.w3t[e % kHid][e / kHid] = __ldg(a.scene.w3 + e);
+    __syncthreads();
     const int n = *amb_count;
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const nx_field_desc& fd = a.scene.field;
+    const uint32_t T = 1u << fd.log2_table, mask = T - 1u;
+    double* x = sm.x[warp];
+    double* h1 = sm.h1[warp];
+    double* h2 = sm.h2[warp];
+    double* y = sm.y[warp];
+    for (int q = blockIdx.x * kMaskWarps + warp; q < n; q += gridDim.x * kMaskWarps) {
         const int64_t sl = amb_list[q];
-        const nx_field_desc& fd = a.scene.field;
         const int64_t pix = sl / a.fb.K;
         double dir[3];
         pixel_dir(a.cam, static_cast<int>(pix % a.cam.W) + 0.5, static_cast<int>(pix / a.cam.W) + 0.5, dir);
         const double t = a.fb.depths[sl];
-        const double x[3] = {a.cam.o[0] + t * dir[0], a.cam.o[1] + t * dir[1], a.cam.o[2] + t * dir[2]};
-        const uint32_t T = 1u << fd.log2_table, mask = T - 1u;
-        double feats[kIn];
-        double s = fd.base_scale;
-        for (int l = 0; l < kLevels; ++l, s *= fd.growth) {
-            const double p0 = s * x[0], p1 = s * x[1], p2 = s * x[2];
+        if (lane < kLevels) {  // grid_lookup, level `lane`
+            const int l = lane;
+            double s = fd.base_scale;
+            for (int k = 0; k < l; ++k) s *= fd.growth;  // the reference's iterated level scale
+            const double x0 = a.cam.o[0] + t * dir[0], x1 = a.cam.o[1] + t * dir[1], x2 = a.cam.o[2] + t * dir[2];
+            const double p0 = s * x0, p1 = s * x1, p2 = s * x2;
             const double fl0 = floor(p0), fl1 = floor(p1), fl2 = floor(p2);
             const long long b0 = static_cast<long long>(fl0), b1 = static_cast<long long>(fl1),
                             b2 = static_cast<long long>(fl2);
@@ -168,44 +196,65 @@ __global__ void __launch_bounds__(128) mask_fp64_kernel(const FieldBwdArgs a, co
                 g0 += cw * v.x;
                 g1 += cw * v.y;
             }
-            feats[2 * l] = g0 * dw;
-            feats[2 * l + 1] = g1 * dw;
+            x[2 * l] = g0 * dw;
+            x[2 * l + 1] = g1 * dw;
         }
-        uint32_t masks[5] = {0u, 0u, 0u, 0u, 0u};
-        double h1[kHid], h2[kHid];
-        for (int o = 0; o < kHid; ++o) {
-            double acc = 0.0;
-            for (int i = 0; i < kIn; ++i) acc += static_cast<double>(__ldg(a.scene.w1 + o * kIn + i)) * feats[i];
-            if (acc > 0.0) masks[o >> 5] |= 1u << (o & 31);
-            h1[o] = acc > 0.0 ? acc : 0.0;
+        __syncwarp();
+        uint32_t m[4];
+        {  // layer 1
+            double a0 = 0.0, a1 = 0.0;
+            for (int i = 0; i < kIn; ++i) {
+                a0 += static_cast<double>(sm.w1t[i][lane]) * x[i];
+                a1 += static_cast<double>(sm.w1t[i][lane + 32]) * x[i];
+            }
+            m[0] = __ballot_sync(0xffffffffu, a0 > 0.0);
+            m[1] = __ballot_sync(0xffffffffu, a1 > 0.0);
+            h1[lane] = a0 > 0.0 ? a0 : 0.0;
+            h1[lane + 32] = a1 > 0.0 ? a1 : 0.0;
         }
-        for (int o = 0; o < kHid; ++o) {
-            double acc = 0.0;
-            for (int i = 0; i < kHid; ++i) acc += static_cast<double>(__ldg(a.scene.w2 + o * kHid + i)) * h1[i];
-            if (acc > 0.0) masks[2 + (o >> 5)] |= 1u << (o & 31);
-            h2[o] = acc > 0.0 ? acc : 0.0;
+        __syncwarp();
+        {  // layer 2
+            double a0 = 0.0, a1 = 0.0;
+            for (int i = 0; i < kHid; ++i) {
+                a0 += static_cast<double>(sm.w2t[i][lane]) * h1[i];
+                a1 += static_cast<double>(sm.w2t[i][lane + 32]) * h1[i];
+            }
+            m[2] = __ballot_sync(0xffffffffu, a0 > 0.0);
+            m[3] = __ballot_sync(0xffffffffu, a1 > 0.0);
+            h2[lane] = a0 > 0.0 ? a0 : 0.0;
+            h2[lane + 32] = a1 > 0.0 ? a1 : 0.0;
         }
-        const double xx = dir[0] * dir[0], yy = dir[1] * dir[1], zz = dir[2] * dir[2];
-        const double dx = dir[0], dy = dir[1], dz = dir[2];
-        const double b[16] = {0.28209479177387814, -0.4886025119029199 * dy, 0.4886025119029199 * dz,
-                              -0.4886025119029199 * dx, 1.0925484305920792 * dx * dy, -1.0925484305920792 * dy * dz,
-                              0.31539156525252005 * (2.0 * zz - xx - yy), -1.0925484305920792 * dx * dz,
-                              0.5462742152960396 * (xx - yy), -0.5900435899266435 * dy * (3.0 * xx - yy),
-                              2.890611442640554 * dx * dy * dz, -0.4570457994644658 * dy * (4.0 * zz - xx - yy),
-                              0.3731763325901154 * dz * (2.0 * zz - 3.0 * xx - 3.0 * yy),
-                              -0.4570457994644658 * dx * (4.0 * zz - xx - yy), 1.445305721320277 * dz * (xx - yy),
-                              -0.5900435899266435 * dx * (xx - 3.0 * yy)};
-        double c3[3] = {0.5, 0.5, 0.5};
-        for (int o = 0; o < kOut; ++o) {
-            double acc = 0.0;
-            for (int i = 0; i < kHid; ++i) acc += static_cast<double>(__ldg(a.scene.w3 + o * kHid + i)) * h2[i];
-            c3[o % 3] += acc * b[o / 3];
+        __syncwarp();
+        {  // layer 3 (48 outputs)
+            double a0 = 0.0, a1 = 0.0;
+            for (int i = 0; i < kHid; ++i) {
+                a0 += static_cast<double>(sm.w3t[i][lane]) * h2[i];
+                if (lane < kOut - 32) a1 += static_cast<double>(sm.w3t[i][lane + 32]) * h2[i];
+            }
+            y[lane] = a0;
+            if (lane < kOut - 32) y[lane + 32] = a1;
         }
-        masks[4] = (c3[0] >= 0.0 ? 1u : 0u) | (c3[1] >= 0.0 ? 2u : 0u) | (c3[2] >= 0.0 ? 4u : 0u);
-        float4* dst = reinterpret_cast<float4*>(fbuf + sl * kStride);
-        dst[kIn / 4] = make_float4(__uint_as_float(masks[0]), __uint_as_float(masks[1]), __uint_as_float(masks[2]),
-                                   __uint_as_float(masks[3]));
-        dst[kIn / 4 + 1] = make_float4(__uint_as_float(masks[4]), 0.f, 0.f, 0.f);
+        __syncwarp();
+        if (lane == 0) {
+            const double xx = dir[0] * dir[0], yy = dir[1] * dir[1], zz = dir[2] * dir[2];
+            const double dx = dir[0], dy = dir[1], dz = dir[2];
+            const double b[16] = {0.28209479177387814, -0.4886025119029199 * dy, 0.4886025119029199 * dz,
+                                  -0.4886025119029199 * dx, 1.0925484305920792 * dx * dy, -1.0925484305920792 * dy * dz,
+                                  0.31539156525252005 * (2.0 * zz - xx - yy), -1.0925484305920792 * dx * dz,
+                                  0.5462742152960396 * (xx - yy), -0.5900435899266435 * dy * (3.0 * xx - yy),
+                                  2.890611442640554 * dx * dy * dz, -0.4570457994644658 * dy * (4.0 * zz - xx - yy),
+                                  0.3731763325901154 * dz * (2.0 * zz - 3.0 * xx - 3.0 * yy),
+                                  -0.4570457994644658 * dx * (4.0 * zz - xx - yy), 1.445305721320277 * dz * (xx - yy),
+                                  -0.5900435899266435 * dx * (xx - 3.0 * yy)};
+            double c3[3] = {0.5, 0.5, 0.5};
+            for (int o = 0; o < kOut; ++o) c3[o % 3] += y[o] * b[o / 3];
+            const uint32_t shm = (c3[0] >= 0.0 ? 1u : 0u) | (c3[1] >= 0.0 ? 2u : 0u) | (c3[2] >= 0.0 ? 4u : 0u);
+            float4* dst = reinterpret_cast<float4*>(fbuf + sl * kStride);
+            dst[kIn / 4] = make_float4(__uint_as_float(m[0]), __uint_as_float(m[1]), __uint_as_float(m[2]),
+                                       __uint_as_float(m[3]));
+            dst[kIn / 4 + 1] = make_float4(__uint_as_float(shm), 0.f, 0.f, 0.f);
+        }
+        __syncwarp();
     }
 }
 
@@ -958,7 +1007,9 @@ int launch_field_backward_tc(const FieldBwdArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(mask_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMask);
     mask_tc_kernel<<<static_cast<unsigned>(std::min<int64_t>(n_tiles, 2 * sms)), kThreadsM, kSmemMask, s>>>(
         a, sc.fbuf, total, n_tiles, sc.amb + 1, sc.amb);
-    mask_fp64_kernel<<<2 * sms, 128, 0, s>>>(a, sc.amb + 1, sc.amb, sc.fbuf);
+    cudaFuncSetAttribute(mask_fp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(MaskSmem)));
+    mask_fp64_kernel<<<4 * sms, 32 * kMaskWarps, sizeof(MaskSmem), s>>>(a, sc.amb + 1, sc.amb, sc.fbuf);
     cudaFuncSetAttribute(mlp_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemM);
     mlp_bwd_tc_kernel<<<grid_m, kThreadsM, kSmemM, s>>>(a, sc.fbuf, sc.parts, total, n_tiles);
     reduce_wgrads_kernel<<<(kWGrads + 255) / 256, 256, 0, s>>>(sc.parts, grid_m, a.g_w1, a.g_w2, a.g_w3);
