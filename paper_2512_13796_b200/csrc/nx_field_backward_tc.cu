@@ -848,6 +848,7 @@ __device__ __forceinline__ void scatter_levels(const FieldBwdArgs& a, const TcCo
             const uint32_t peers = __match_any_sync(0xffffffffu, key);
             const uint32_t leaders = __ballot_sync(0xffffffffu, valid && lane == __ffs(peers) - 1);
             const int max_size = __reduce_max_sync(0xffffffffu, valid ? __popc(peers) : 0);
+            float my0 = 0.f, my1 = 0.f;  // this lane's group sum when it leads a group
             if (__popc(leaders) * 4 <= max_size) {
                 // few large groups (coarse levels): one warp-wide tree sum per group
                 for (uint32_t L = leaders; L; L &= L - 1) {
@@ -860,27 +861,26 @@ __device__ __forceinline__ void scatter_levels(const FieldBwdArgs& a, const TcCo
                         s1 += __shfl_xor_sync(0xffffffffu, s1, o);
                     }
                     if (lane == ld) {
-                        const int64_t dst = slab + static_cast<int64_t>(c.row[ci]) * 2;
-                        xacc_add(tacc, dst, s0);
-                        xacc_add(tacc, dst + 1, s1);
+                        my0 = s0;
+                        my1 = s1;
                     }
                 }
             } else {
                 // many small groups (fine levels): each leader sums its group in lane order
                 wsh[lane] = make_float2(u0, u1);
                 __syncwarp();
-                if (valid && lane == __ffs(peers) - 1) {
-                    float s0 = 0.f, s1 = 0.f;
+                if (valid && lane == __ffs(peers) - 1)
                     for (uint32_t m = peers; m; m &= m - 1) {
                         const float2 u = wsh[__ffs(m) - 1];
-                        s0 += u.x;
-                        s1 += u.y;
+                        my0 += u.x;
+                        my1 += u.y;
                     }
-                    const int64_t dst = slab + static_cast<int64_t>(c.row[ci]) * 2;
-                    xacc_add(tacc, dst, s0);
-                    xacc_add(tacc, dst + 1, s1);
-                }
                 __syncwarp();
+            }
+            if (valid && lane == __ffs(peers) - 1) {  // one accumulator update per distinct row
+                const int64_t dst = slab + static_cast<int64_t>(c.row[ci]) * 2;
+                xacc_add(tacc, dst, my0);
+                xacc_add(tacc, dst + 1, my1);
             }
         }
     }
