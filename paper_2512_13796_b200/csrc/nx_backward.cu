@@ -83,8 +83,8 @@ struct WarpSmem {        // one warp's private staging (no sharing between warps
 // d_sigma[2], d_opacity, d_gamma[2]. The kernel terms (axis powers, log|u|, log|v|,
 // exp(-(pu + pv)/2)) are the ones B1 formed for the hit (finite: a composited hit).
 __device__ __forceinline__ void hit_backward(const double* r, const double* d, const double* o, double t, double u,
-                                             double v, const BwdHit& hh, double* g) {
-    const double op = r[REC_OP], gx = r[REC_GX], gy = r[REC_GY], sx = r[REC_SX], sy = r[REC_SY];
+                                             double v, double rsx, double rsy, const BwdHit& hh, double* g) {
+    const double op = r[REC_OP], gx = r[REC_GX], gy = r[REC_GY];
     const double pu = hh.pu, pv = hh.pv, d_alpha = hh.alpha, d_t = hh.d_t;
     double kd_u = 0.0, kd_v = 0.0, kd_gx = 0.0, kd_gy = 0.0;
     const double k = hh.k;
@@ -106,17 +106,20 @@ __device__ __forceinline__ void hit_backward(const double* r, const double* d, c
     const double mu[3] = {r[REC_MUX], r[REC_MUY], r[REC_MUZ]};
     const double denom = d[0] * n[0] + d[1] * n[1] + d[2] * n[2];
     const double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+    // gradient values only (no decision depends on them): one reciprocal per divisor
+    // instead of the reference's nine divisions
+    const double rden = 1.0 / denom;
     g[14] = d_alpha * kd_op;
     g[15] = d_alpha * kd_gx;
     g[16] = d_alpha * kd_gy;
-    g[12] = d_alpha * kd_u * (-u / sx);
-    g[13] = d_alpha * kd_v * (-v / sy);
+    g[12] = d_alpha * kd_u * (-u * rsx);
+    g[13] = d_alpha * kd_v * (-v * rsy);
     const double du = d_alpha * kd_u, dv = d_alpha * kd_v;
     const double dv1 = d[0] * v1[0] + d[1] * v1[1] + d[2] * v1[2];
     const double dv2 = d[0] * v2[0] + d[1] * v2[1] + d[2] * v2[2];
-    const double dt = d_t + du * dv1 / sx + dv * dv2 / sy;
-    const double cu = -du / sx, cv = -dv / sy, cn = dt / denom;
-    const double au = du / sx, av = dv / sy;
+    const double au = du * rsx, av = dv * rsy;
+    const double dt = d_t + au * dv1 + av * dv2;
+    const double cu = -au, cv = -av, cn = dt * rden;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         g[i] = cu * v1[i] + cv * v2[i] + cn * n[i];
@@ -370,10 +373,11 @@ __global__ void __launch_bounds__(kTile * kTile, 512 / (kTile * kTile)) composit
                 const double e0 = (o[0] + hh.t * d3[0]) - r[REC_MUX];
                 const double e1 = (o[1] + hh.t * d3[1]) - r[REC_MUY];
                 const double e2 = (o[2] + hh.t * d3[2]) - r[REC_MUZ];
-                const double u = (e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z]) / r[REC_SX];
-                const double v = (e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z]) / r[REC_SY];
+                const double rsx = 1.0 / r[REC_SX], rsy = 1.0 / r[REC_SY];
+                const double u = (e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z]) * rsx;
+                const double v = (e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z]) * rsy;
                 double gd[kActFields - 1];
-                hit_backward(r, d3, o, hh.t, u, v, hh, gd);
+                hit_backward(r, d3, o, hh.t, u, v, rsx, rsy, hh, gd);
                 float* g = sm.res[e].g;
 #pragma unroll
                 for (int i = 0; i < kActFields - 1; ++i) g[i] = static_cast<float>(gd[i]);
