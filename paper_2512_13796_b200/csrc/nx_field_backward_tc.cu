@@ -811,6 +811,9 @@ __device__ __forceinline__ void scatter_levels(const FieldBwdArgs& a, const TcCo
     const uint32_t T = 1u << a.scene.field.log2_table, mask = T - 1u;
     const int lane = threadIdx.x & 31;
     // ---- phase 1: d_x, d_t from the kept sums: dL/dp_d = dw (g . J_d), dL/d(dw) = g . S
+    // fade t-gradient (hash_grid.hpp:117-121): r^2 / (pi t) with r = fx / (s t) is
+    // fx^2 / (pi t^3) / s^2 — one division per slot (a gradient value, no decision)
+    const double fade_c = a.cam.fx * a.cam.fx / (M_PI * t * t * t);
     if (valid) {
 #pragma unroll 4
         for (int l = 0; l < kLevels; ++l) {
@@ -828,8 +831,7 @@ __device__ __forceinline__ void scatter_levels(const FieldBwdArgs& a, const TcCo
             dx[2] += sl * dp2;
             if (!a.st.no_downweight) {
                 // downweight_grad_t via the cached factor (hash_grid.hpp:117-121)
-                const double r = a.cam.fx / (sl * t);
-                dt += static_cast<double>(d_dw) * (static_cast<double>(dw) - 1.0) * r * r / (M_PI * t);
+                dt += static_cast<double>(d_dw) * (static_cast<double>(dw) - 1.0) * fade_c * cst.inv_level_scale2[l];
             }
         }
     }
@@ -999,6 +1001,7 @@ int launch_field_backward_tc(const FieldBwdArgs& a, cudaStream_t s) {
     for (int l = 0; l < kLevels; ++l, scale *= a.scene.field.growth) {
         cst.level_scale[l] = scale;
         cst.inv_level_scale[l] = static_cast<float>(1.0 / scale);
+        cst.inv_level_scale2[l] = 1.0 / (scale * scale);
     }
     const unsigned blocks = static_cast<unsigned>((total + 127) / 128);
     count_launch(6);

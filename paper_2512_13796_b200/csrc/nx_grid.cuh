@@ -14,6 +14,7 @@ constexpr int kLevels = 16;
 struct TcConst {
     double level_scale[kLevels];  // HashGridConfig::level_scale by iterated product (hash_grid.cpp:7-13)
     float inv_level_scale[kLevels];
+    double inv_level_scale2[kLevels];  // 1 / level_scale^2 (the fade's t-gradient)
 };
 
 __device__ __forceinline__ uint32_t map_positive32(long long x) {  // hash_grid.hpp:12-14
