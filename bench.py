@@ -332,10 +332,8 @@ def train_step_timing(args, r, ds, scene, cam, stream, dist, local):
     fr.set_backward(True)
     c = cam.to_c()
     s = C.c_void_p(r.stream)
-    fin = None
 
     def step():
-        nonlocal fin
         with torch.cuda.stream(stream):  # SceneGrads::allocate (renderer.cpp:245-248), every iteration
             for t in grads:
                 t.zero_()
@@ -344,17 +342,14 @@ def train_step_timing(args, r, ds, scene, cam, stream, dist, local):
                                           C.c_void_p(d_final.data_ptr()), C.c_void_p(d_weights.data_ptr()),
                                           C.c_void_p(d_texture.data_ptr()), C.byref(gg),
                                           C.c_void_p(terms.data_ptr()), s))
-        if fin is None:
-            fin = _device_view(fr.view().final_img, npix * 3, torch.float32, dev)
-        with torch.cuda.stream(stream):  # err_pixel = mean_c |final - gt| (trainer.cpp:289-296)
-            torch.mean(torch.abs(fin.double().view(npix, 3) - gt.view(npix, 3)), dim=1, out=err)
+        # err_pixel = mean_c |final - gt| (trainer.cpp:289-296)
+        r._check(r.lib.nx_pixel_error(r.ctx, fr.handle, C.c_void_p(gt.data_ptr()), C.c_void_p(err.data_ptr()), s))
         r._check(r.lib.nx_render_backward(r.ctx, ds.handle, C.byref(c), fr.handle, C.byref(up), C.byref(gg),
                                           C.c_void_p(err.data_ptr()), C.c_void_p(blend.data_ptr()), s))
         if dist is not None:  # data-parallel over views: mean of the ranks' gradients (NCCL)
             with torch.cuda.stream(stream):
                 for t in grads:
-                    dist.all_reduce(t)
-                    t.div_(dist.get_world_size())
+                    dist.all_reduce(t, op=dist.ReduceOp.AVG)
         r._check(r.lib.nx_optimizer_step(r.ctx, opt, ds.handle, C.byref(gg), acfg, s))
 
     for _ in range(3):
@@ -406,7 +401,7 @@ def train_step_timing(args, r, ds, scene, cam, stream, dist, local):
                          "frac": bwd_bytes / (bwd_ms / 1e3) / 1e9 / hbm_peak, "bytes": bwd_bytes,
                          "formula": "76HW + (12+16K)HW + 240N + 2048Q + 4P"},
             "cpu_baseline": cpu,
-            "path": "zero SceneGrads + nx_render + nx_losses_backward (gt = grid_init 1e-1 render) + err_pixel + "
+            "path": "zero SceneGrads + nx_render + nx_losses_backward (gt = grid_init 1e-1 render) + nx_pixel_error + "
                     "nx_render_backward + [NCCL all-reduce of the gradients, N > 1] + nx_optimizer_step (Adam, 11 "
                     "groups); no density control",
             "reference_s": "render ~55 s + render_backward 101 s per step at config 2 on 8 cores (SURVEY.md §6, "
