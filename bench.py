@@ -617,6 +617,12 @@ def run_ours(args):
             "frame_roofline": {"bytes_per_frame": fbytes, "achieved": frame_gbs, "peak": hbm_peak, "unit": "GB/s",
                                "frac": frame_gbs / hbm_peak, "formula": "240N + 8P + (28+24K)HW + 1024Q + 36864"},
             "decoder_roofline": decoder,
+            # SURVEY.md §8(d) secondary compute figure: the reference-equivalent (pixel,
+            # primitive) intersection tests — every key of the reference's tile lists times
+            # the pixels of its tile (16x16) — per second
+            "intersection_tests": {"per_frame": P * 256.0, "per_s": P * 256.0 * fps,
+                                   "evaluated_per_frame_note": "the work lists and the fp32 prefilter leave "
+                                                               "~27M exact fp64 evaluations per frame"},
             "stages_ms": stage_ms, "profiled_frames": prof_frames,
             "work": {"tile_keys_P": P, "work_keys": Pw, "queries_Q": Q},
             "cpu_baseline": cpu,
