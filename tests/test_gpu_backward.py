@@ -232,3 +232,22 @@ def test_backward_reuses_or_rebuilds_the_forward_lists_identically(renderer, ref
     after_settings = backward(fa)       # ... so this re-bins, with the original settings
     for a, b, c in zip(reused, again, after_settings):
         assert np.array_equal(a, b) and np.array_equal(a, c)
+
+
+@pytest.mark.parametrize("y0", [472, 904])
+def test_config5_scale_band_gradients_match_reference(renderer, reference, y0):
+    """BASELINE config 5 scale: the 400K-nexel stump scene with the reference field shape
+    (2^20-row hash table, grid_init 1e-1: the texture branch carries real gradients) at
+    1920 x 1080, on a 64-row band of the view (a principal-point-shifted camera — every
+    pixel keeps its ray, so this is the full frame's backward restricted to those rows;
+    the reference's CPU render_backward of the whole frame takes ~30 s). All gradient
+    arrays against the reference compiled in place, at the tensor-core tolerance."""
+    scene = nx.stump_like(400_000, grid_init=1e-1)
+    cam = nx.band_camera(nx.ring_camera(0, 256, 1920, 1080), y0, 64)
+    up = upstream(cam, scene.settings.top_k, y0)
+    err = np.random.default_rng(y0).random(cam.width * cam.height)
+    g, _, _ = gpu_backward(renderer, scene, cam, up, err)
+    r = ref_backward(reference, scene, cam, up, err)
+    rep = compare_grads(g, r, GRAD_TOL_TC)
+    print(y0, {k: f"{v:.1e}" for k, v in rep.items()})
+    assert np.count_nonzero(r[0]) > 1000 and np.count_nonzero(r[1]) > 1000
