@@ -104,3 +104,16 @@ def test_loss_terms_are_bit_reproducible(renderer):
         assert o[0] == outs[0][0]
         for a, b in zip(o[1:], outs[0][1:]):
             assert np.array_equal(a, b)
+
+
+def test_config5_scale_losses_match_reference(renderer, reference):
+    """BASELINE config 5 scale: the 400K-nexel scene with the reference field (2^20 rows)
+    at 1920 x 1080 against the render of its grid_init 1e-1 variant, on a 96-row band of
+    the view (the band is an image of its own: SSIM's zero padding applies at its edges on
+    both sides). Full-size grid regulariser over the 33.5M table entries."""
+    cam = nx.band_camera(nx.ring_camera(0, 256, 1920, 1080), 480, 96)
+    target = nx.stump_like(400_000, grid_init=1e-1)
+    scene = nx.stump_like(400_000, grid_init=1e-4)
+    gt = nx.render(target, cam).fb.final_img
+    terms = run_both(renderer, reference, scene, cam, gt, LossWeights(), table_rtol=1e-6)
+    assert terms["texture"] > 0 and terms["image"] > 0
