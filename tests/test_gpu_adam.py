@@ -68,11 +68,12 @@ def test_adam_steps_match_reference(renderer, reference):
     renderer.lib.nx_optimizer_destroy(opt)
 
 
-def test_fp64_masters_track_the_reference_exactly(renderer, reference):
+@pytest.mark.parametrize("n,log2", [(500, 8), (400_000, 20)])  # the latter: BASELINE config-5 scale
+def test_fp64_masters_track_the_reference_exactly(renderer, reference, n, log2):
     """The fp32-stored groups (SH, table, MLP) are stepped on the optimizer's fp64 masters:
     read back with nx_optimizer_download they agree with the reference's fp64 adam_step to
     fp64 rounding, not just fp32 (the scene keeps their fp32 rounding for rendering)."""
-    scene = nx.stump_like(500, log2_table=8, grid_init=1e-1)
+    scene = nx.stump_like(n, log2_table=log2, grid_init=1e-1)
     ds = renderer.upload(scene)
     opt = renderer.optimizer(ds)
     f = scene.field
@@ -85,7 +86,7 @@ def test_fp64_masters_track_the_reference_exactly(renderer, reference):
     ref = {gi: np.ascontiguousarray(v, dtype=np.float64).reshape(-1).copy() for gi, v in init.items()}
     state = {}
     for _ in range(4):
-        g_prims = rng.standard_normal((500, 60))
+        g_prims = rng.standard_normal((n, 60))
         g_f = [rng.standard_normal(np.size(a)) for a in (f.table, f.w1, f.w2, f.w3)]
         dev = [torch.tensor(a.reshape(-1), dtype=torch.float64, device="cuda") for a in (g_prims, *g_f)]
         torch.cuda.synchronize()
