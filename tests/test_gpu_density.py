@@ -22,13 +22,15 @@ def dev(a, dtype=torch.float64):
     return torch.tensor(np.ascontiguousarray(a).reshape(-1), dtype=dtype, device="cuda")
 
 
-def test_densify_then_prune_match_reference(renderer, reference):
-    scene = nx.stump_like(3_000, log2_table=10, grid_init=1e-1)
+@pytest.mark.parametrize("n0", [3_000, 400_000])  # the latter: BASELINE config-5 scale (40K splits)
+def test_densify_then_prune_match_reference(renderer, reference, n0):
+    scene = nx.stump_like(n0, log2_table=10, grid_init=1e-1)
     n = scene.nexels.shape[0]
+    budget = n + n // 10 + n // 30
     rng = np.random.default_rng(4)
     errors = rng.random(n) * (rng.random(n) > 0.3)  # some zero errors: never sampled
-    ref_nex, ref_map, ref_splits, uniforms = reference.densify_split(scene.nexels, errors, 3_400, 0.1, 77)
-    assert ref_splits == 300 and ref_nex.shape[0] == 3_300
+    ref_nex, ref_map, ref_splits, uniforms = reference.densify_split(scene.nexels, errors, budget, 0.1, 77)
+    assert ref_splits == n // 10 and ref_nex.shape[0] == n + n // 10
 
     ds = renderer.upload(scene)
     opt = C.c_void_p()
@@ -57,12 +59,12 @@ def test_densify_then_prune_match_reference(renderer, reference):
     assert np.allclose(ref_params[:, :12], host[:, :12], rtol=1e-12, atol=1e-15)
 
     # ---- densify_split with the reference's draws
-    ref_nex, ref_map, ref_splits, uniforms = reference.densify_split(ref_params, errors, 3_400, 0.1, 77)
-    n2o = torch.zeros(n + 400, dtype=torch.int32, device="cuda")
+    ref_nex, ref_map, ref_splits, uniforms = reference.densify_split(ref_params, errors, budget, 0.1, 77)
+    n2o = torch.zeros(budget, dtype=torch.int32, device="cuda")
     n_out, sc = C.c_int64(), C.c_int64()
     e_t, u_t = dev(errors), dev(uniforms)
     renderer._check(renderer.lib.nx_scene_densify_split(renderer.ctx, ds.handle, opt, C.c_void_p(e_t.data_ptr()),
-                                                        C.c_void_p(u_t.data_ptr()), 3_400, 0.1,
+                                                        C.c_void_p(u_t.data_ptr()), budget, 0.1,
                                                         C.c_void_p(n2o.data_ptr()), C.byref(n_out), C.byref(sc)))
     assert (n_out.value, sc.value) == (ref_nex.shape[0], ref_splits)
     assert np.array_equal(n2o[: n_out.value].cpu().numpy(), ref_map)
