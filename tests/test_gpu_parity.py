@@ -243,6 +243,25 @@ def test_config2_contributor_lists_band(renderer, reference, config2, band):
     assert np.array_equal(g_hits, r_hits)
 
 
+@pytest.mark.parametrize("view", [16, 48, 80, 112, 144, 176, 208, 240])
+def test_config3_views_exact(renderer, reference, config2, view):
+    """BASELINE config 3 (400K nexels, 1920x1080, views of the 256-ring): for 8 views
+    spread around the ring, the reference tile lists (every key, full frame) and the
+    per-pixel contributor lists on a 16-row band bit-exact."""
+    scene, _ = config2
+    cam = nx.ring_camera(view, 256, 1920, 1080)
+    ds = renderer.upload(scene)
+    g_off, g_ids, _, _ = renderer.tile_lists(ds, cam, reference_lists=True)
+    r_off, r_ids, _, _ = reference.tile_lists(scene, cam)
+    assert np.array_equal(g_off, r_off)
+    assert np.array_equal(g_ids, r_ids)
+    y0 = 256 + 4 * view % 512
+    g_hits, g_cnt = renderer.pixel_hits(ds, cam, y0, y0 + 16, 128)
+    r_hits, r_cnt = reference.pixel_hits(scene, cam, y0, y0 + 16, 128)
+    assert np.array_equal(g_cnt, r_cnt) and np.array_equal(g_hits, r_hits)
+    assert g_cnt.sum() > 0
+
+
 @pytest.mark.slow
 def test_config4_counts_and_contributor_band(renderer, reference):
     """BASELINE config 4 (1.3M nexels, 3840x2160): the reference tile-key count
