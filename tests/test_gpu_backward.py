@@ -251,3 +251,25 @@ def test_config5_scale_band_gradients_match_reference(renderer, reference, y0):
     rep = compare_grads(g, r, GRAD_TOL_TC)
     print(y0, {k: f"{v:.1e}" for k, v in rep.items()})
     assert np.count_nonzero(r[0]) > 1000 and np.count_nonzero(r[1]) > 1000
+
+
+def test_config5_full_frame_backward_is_bit_reproducible(renderer):
+    """The whole BASELINE config-5 backward (400K nexels, 1920x1080, reference field
+    shape, ~4M buffered slots) twice on the same frame: identical bits (GPU only)."""
+    scene = nx.stump_like(400_000, grid_init=1e-1)
+    cam = nx.ring_camera(5, 256, 1920, 1080)
+    up = upstream(cam, scene.settings.top_k, 5)
+    err = np.random.default_rng(5).random(cam.width * cam.height)
+    ds = renderer.upload(scene)
+    fr = renderer.frame()
+    fr.set_backward(True)
+    renderer.render(ds, cam, fr)
+    runs = []
+    for _ in range(2):
+        g = SceneGrads.allocate(scene)
+        be = np.zeros(scene.nexels.shape[0])
+        renderer.render_backward(ds, cam, fr, up, g, err, be)
+        runs.append((g.prims, g.table, g.w1, g.w2, g.w3, be))
+    assert np.abs(runs[0][1]).max() > 0
+    for a, b in zip(*runs):
+        assert np.array_equal(a, b)
