@@ -126,6 +126,7 @@ uint64_t next_scene_version() {
 
 struct nx_scene {
     nx_ctx* ctx = nullptr;
+    int device = 0;  // the creating context's device (destroy must not touch a freed ctx)
     int64_t n = 0;
     DevBuf geom, sh, table, w1, w2, w3;
     DevBuf geom_spare, sh_spare;  // density control rebuilds into these and swaps (grow-only)
@@ -138,6 +139,7 @@ struct nx_scene {
 
 struct nx_frame {
     nx_ctx* ctx = nullptr;
+    int device = 0;  // the creating context's device
     int W = 0, H = 0, K = 0, tiles_x = 0, tiles_y = 0;  // reference tiles (settings.tile)
     int list_tile = kWorkTile, ltiles_x = 0, ltiles_y = 0;  // tiles of the last built lists
     DevBuf base, ids, depths, weights, texture, final_img, residual;
@@ -654,6 +656,7 @@ int nx_scene_create(nx_ctx* c, const nx_settings* settings, int64_t n, const dou
     nx_scene* s = new (std::nothrow) nx_scene;
     if (!s) return set_err(c, NX_OUT_OF_MEMORY, "host allocation");
     s->ctx = c;
+    s->device = c->device;
     s->n = n;
     s->field = *field;
     s->st = *settings;
@@ -739,6 +742,7 @@ int nx_scene_load_nexl(nx_ctx* c, const char* path, nx_scene** out, nx_nexl_info
     nx_scene* s = new (std::nothrow) nx_scene;
     if (!s) return set_err(c, NX_OUT_OF_MEMORY, "host allocation");
     s->ctx = c;
+    s->device = c->device;
     const int64_t n = h.info.n_nexels;
     s->n = n;
     s->field = h.info.field;
@@ -814,7 +818,7 @@ int nx_scene_get_settings(const nx_scene* s, nx_settings* out) {
 
 void nx_scene_destroy(nx_scene* s) {
     if (!s) return;
-    if (s->ctx) cudaSetDevice(s->ctx->device);
+    cudaSetDevice(s->device);
     for (DevBuf* b : {&s->geom, &s->sh, &s->table, &s->w1, &s->w2, &s->w3, &s->geom_spare, &s->sh_spare}) b->release();
     delete s;
 }
@@ -826,6 +830,7 @@ int nx_frame_create(nx_ctx* c, int width, int height, int top_k, nx_frame** out)
     nx_frame* f = new (std::nothrow) nx_frame;
     if (!f) return set_err(c, NX_OUT_OF_MEMORY, "host allocation");
     f->ctx = c;
+    f->device = c->device;
     if (cudaMalloc(&f->stats, sizeof(FrameStatsD)) != cudaSuccess) {
         delete f;
         return set_err(c, NX_OUT_OF_MEMORY, "frame stats");
@@ -847,11 +852,11 @@ int nx_frame_create(nx_ctx* c, int width, int height, int top_k, nx_frame** out)
 
 void nx_frame_destroy(nx_frame* f) {
     if (!f) return;
-    if (f->ctx) cudaSetDevice(f->ctx->device);
+    cudaSetDevice(f->device);
+    if (f->ev_busy) cudaEventSynchronize(f->ev_busy);  // texture pass / download still reading it
     for (DevBuf* b : {&f->base, &f->ids, &f->depths, &f->weights, &f->texture, &f->final_img, &f->residual,
                       &f->tile_offsets, &f->base64, &f->residual64, &f->tex_f})
         b->release();
-    if (f->ev_busy) cudaEventSynchronize(f->ev_busy);
     if (f->stats) cudaFree(f->stats);
     if (f->ev_ready) cudaEventDestroy(f->ev_ready);
     if (f->ev_busy) cudaEventDestroy(f->ev_busy);
@@ -1256,6 +1261,7 @@ int nx_losses_backward_host(nx_ctx* c, const nx_scene* scene, const nx_frame* fc
 
 struct nx_optimizer {
     nx_ctx* ctx = nullptr;
+    int device = 0;  // the creating context's device
     int64_t n = 0;
     DevBuf m[NX_NUM_GROUPS], v[NX_NUM_GROUPS];
     DevBuf master[NX_NUM_GROUPS];  // fp64 values of the groups the scene stores in fp32 (5..10)
@@ -1272,6 +1278,7 @@ int nx_optimizer_create(nx_ctx* c, const nx_scene* scene, nx_optimizer** out) {
     nx_optimizer* o = new (std::nothrow) nx_optimizer;
     if (!o) return set_err(c, NX_OUT_OF_MEMORY, "host allocation");
     o->ctx = c;
+    o->device = c->device;
     o->n = scene->n;
     adam_group_sizes(scene_dev(scene), o->size);
     for (int gi = 0; gi < NX_NUM_GROUPS; ++gi) {
@@ -1353,7 +1360,7 @@ int nx_optimizer_download(nx_ctx* c, const nx_optimizer* o, const nx_scene* scen
 
 void nx_optimizer_destroy(nx_optimizer* o) {
     if (!o) return;
-    if (o->ctx) cudaSetDevice(o->ctx->device);
+    cudaSetDevice(o->device);
     for (int gi = 0; gi < NX_NUM_GROUPS; ++gi) {
         o->m[gi].release();
         o->v[gi].release();
