@@ -14,9 +14,11 @@
 // A_total minus the running prefix of dL/dw * w. Everything on the geometric
 // chain is fp64 with the reference's formulas: eval_kernel_grad (kernel.hpp:
 // 40-68), intersect_backward (intersect.hpp:56-87); SH gradients (eval_sh_backward,
-// sh.hpp:76-83) are formed in fp32 and accumulated in fp64.
+// sh.hpp:76-83) are formed in fp32 and accumulated in fp64. The gradient formulas
+// multiply by one reciprocal per divisor (values only; every decision stays the
+// forward's), and each hit's kernel terms come from its B1 evaluation.
 //
-// Each warp (8x4 pixels of the 16x16 tile) walks the tile's list on its own — its
+// Each warp (8x4 pixels of the work tile) walks the tile's list on its own — its
 // own 32-primitive staging, no CTA barriers, so a warp whose pixels terminate early
 // stops early. Per group of primitives it pools its survivors like the forward
 // (B1: exact fp64 intersect, all lanes busy), composites them per pixel in list
