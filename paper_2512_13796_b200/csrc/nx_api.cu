@@ -111,6 +111,10 @@ struct nx_ctx {
     cudaStream_t stream2 = nullptr;  // texture passes: overlap the next frame's collection
     cudaStream_t stream3 = nullptr;  // downloads: the copy engine overlaps both
     cudaEvent_t ev_join = nullptr;
+    // render_backward: the table-gradient scatter beside the compositing backward
+    // (forked and joined back inside each call)
+    cudaStream_t stream_bwd = nullptr;
+    cudaEvent_t ev_bwd_fork = nullptr, ev_bwd_join = nullptr;
     cudaEvent_t ev[kEvSets][kEvPoints] = {};
     int ev_cur = 0;
     bool ev_pending[kEvSets] = {};  // profiled frames whose events are not folded yet
@@ -565,6 +569,9 @@ int nx_ctx_create(int device, nx_ctx** out) {
         cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->stream_bwd, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_bwd_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_bwd_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaMallocHost(&c->h_pinned, 64 * sizeof(int32_t)) != cudaSuccess) {
         delete c;
         return NX_CUDA_ERROR;
@@ -581,6 +588,7 @@ void nx_ctx_destroy(nx_ctx* c) {
     cudaStreamSynchronize(c->stream);
     cudaStreamSynchronize(c->stream2);
     cudaStreamSynchronize(c->stream3);
+    cudaStreamSynchronize(c->stream_bwd);
     for (DevBuf* b : {&c->rec, &c->recf, &c->cls, &c->ref_rect, &c->work_rect, &c->key, &c->flag, &c->pos, &c->skeys_a,
                       &c->skeys_b, &c->sids_a, &c->sids_b, &c->counts, &c->offsets, &c->tkeys_a, &c->tkeys_b,
                       &c->tvals_a, &c->tvals_b, &c->tile_counts, &c->scratch, &c->dbg_hits, &c->dbg_counts})
@@ -598,6 +606,9 @@ void nx_ctx_destroy(nx_ctx* c) {
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->stream2);
     cudaStreamDestroy(c->stream3);
+    cudaEventDestroy(c->ev_bwd_fork);
+    cudaEventDestroy(c->ev_bwd_join);
+    cudaStreamDestroy(c->stream_bwd);
     delete c;
 }
 
@@ -1071,6 +1082,7 @@ int nx_render_backward(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, n
     fd.tiles_x = lf->ltiles_x;
     fd.tiles_y = lf->ltiles_y;
     const CamD cd = make_cam(*cam);
+    bool join_side = false;  // the field backward forked work onto stream_bwd
     if (f->K > 0) {
         if (up->d_final || up->d_texture) {
             FieldBwdArgs fa;
@@ -1086,8 +1098,19 @@ int nx_render_backward(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, n
             fa.g_w2 = g->w2;
             fa.g_w3 = g->w3;
             fa.scratch = &c->field_bwd;
+            // NX_BWD_OVERLAP=0: everything on s
+            static const bool overlap = [] {
+                const char* e = std::getenv("NX_BWD_OVERLAP");
+                return !(e && e[0] == '0');
+            }();
+            if (overlap) {
+                fa.side = c->stream_bwd;
+                fa.ev_fork = c->ev_bwd_fork;
+                fa.ev_join = c->ev_bwd_join;
+            }
             if ((st = launch_field_backward(fa, s)))
                 return set_err(c, st, "texture field shape not supported by render_backward");
+            join_side = overlap;
         } else {
             NX_CUDA(c, cudaMemsetAsync(c->d_t_slot.p, 0, ns * sizeof(double), s));
         }
@@ -1112,6 +1135,7 @@ int nx_render_backward(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, n
     launch_composite_backward(ca, s);
     launch_prim_finalize(scene_dev(scene), scene->st.no_gamma, prim_acc, c->act_grad.as<double>(), g->prims,
                          err_pixel ? blended_error : nullptr, s);
+    if (join_side) NX_CUDA(c, cudaStreamWaitEvent(s, c->ev_bwd_join, 0));
     NX_CUDA(c, cudaEventRecord(f->ev_busy, s));
     f->busy_pending = true;
     NX_CUDA(c, cudaGetLastError());

@@ -803,13 +803,9 @@ __global__ void reduce_wgrads_kernel(const float* __restrict__ partials, int n_p
 // every level but the very finest (a warp covers 16 adjacent pixels), so the lanes that
 // hit the same row (__match_any_sync) are summed first, in lane order, and their leader
 // adds the sum: one accumulator update per distinct row of the warp.
-template <bool kSmall>
-__device__ __forceinline__ void scatter_levels(const FieldBwdArgs& a, const TcConst& cst, bool valid, double x0,
-                                               double x1, double x2, float ft, const float* g, double t, double* dx,
-                                               double& dt, const Xacc& tacc, float2* __restrict__ wsh,
-                                               const float* __restrict__ jbuf, int64_t total, int64_t slot) {
-    const uint32_t T = 1u << a.scene.field.log2_table, mask = T - 1u;
-    const int lane = threadIdx.x & 31;
+__device__ __forceinline__ void scatter_dt(const FieldBwdArgs& a, const TcConst& cst, bool valid, float ft,
+                                           const float* g, double t, double* dx, double& dt,
+                                           const float* __restrict__ jbuf, int64_t total, int64_t slot) {
     // ---- phase 1: d_x, d_t from the kept sums: dL/dp_d = dw (g . J_d), dL/d(dw) = g . S
     // fade t-gradient (hash_grid.hpp:117-121): r^2 / (pi t) with r = fx / (s t) is
     // fx^2 / (pi t^3) / s^2 — one division per slot (a gradient value, no decision)
@@ -835,6 +831,14 @@ __device__ __forceinline__ void scatter_levels(const FieldBwdArgs& a, const TcCo
             }
         }
     }
+}
+
+template <bool kSmall>
+__device__ __forceinline__ void scatter_table(const FieldBwdArgs& a, const TcConst& cst, bool valid, double x0,
+                                              double x1, double x2, float ft, const float* g, const Xacc& tacc,
+                                              float2* __restrict__ wsh) {
+    const uint32_t T = 1u << a.scene.field.log2_table, mask = T - 1u;
+    const int lane = threadIdx.x & 31;
     // ---- phase 2: table gradients dL/dtable[row][f] += g[f] * dw * corner_w (hash_grid.hpp:99-103)
 #pragma unroll 1
     for (int l = 0; l < kLevels; ++l) {
@@ -888,50 +892,70 @@ __device__ __forceinline__ void scatter_levels(const FieldBwdArgs& a, const TcCo
     }
 }
 
-__global__ void __launch_bounds__(128) scatter_kernel(const FieldBwdArgs a, const TcConst cst,
-                                                      const float* __restrict__ fbuf, int64_t total,
-                                                      const float* __restrict__ jbuf, const Xacc tacc) {
-    const int64_t sl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const bool in = sl < total;
-    const bool valid = in && a.fb.ids[sl] >= 0;
-    const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-    if (!vmask) {
-        if (in) a.d_t_slot[sl] = 0.0;
-        return;
-    }
-    __shared__ float2 wsh[128];
-    double dir[3] = {0.0, 0.0, 1.0};
-    double t = 1.0, x0 = 0.0, x1 = 0.0, x2 = 0.0;
-    float g[kIn];
+// per slot: the query point, its ray and dL/dF (fbuf); false for an empty slot
+__device__ __forceinline__ bool scatter_slot(const FieldBwdArgs& a, const float* __restrict__ fbuf, int64_t sl,
+                                             int64_t total, double* dir, double& t, double* x, float* g) {
+    dir[0] = 0.0;
+    dir[1] = 0.0;
+    dir[2] = 1.0;
+    t = 1.0;
+    x[0] = x[1] = x[2] = 0.0;
 #pragma unroll
     for (int i = 0; i < kIn; ++i) g[i] = 0.f;
-    if (valid) {
-        const int64_t pix = sl / a.fb.K;
-        pixel_dir(a.cam, static_cast<int>(pix % a.cam.W) + 0.5, static_cast<int>(pix / a.cam.W) + 0.5, dir);
-        t = a.fb.depths[sl];
-        x0 = a.cam.o[0] + t * dir[0];
-        x1 = a.cam.o[1] + t * dir[1];
-        x2 = a.cam.o[2] + t * dir[2];
-        const float4* src = reinterpret_cast<const float4*>(fbuf + sl * kStride);
+    if (sl >= total || a.fb.ids[sl] < 0) return false;
+    const int64_t pix = sl / a.fb.K;
+    pixel_dir(a.cam, static_cast<int>(pix % a.cam.W) + 0.5, static_cast<int>(pix / a.cam.W) + 0.5, dir);
+    t = a.fb.depths[sl];
+    x[0] = a.cam.o[0] + t * dir[0];
+    x[1] = a.cam.o[1] + t * dir[1];
+    x[2] = a.cam.o[2] + t * dir[2];
+    const float4* src = reinterpret_cast<const float4*>(fbuf + sl * kStride);
 #pragma unroll
-        for (int q = 0; q < kIn / 4; ++q) {
-            const float4 v = src[q];
-            g[4 * q] = v.x;
-            g[4 * q + 1] = v.y;
-            g[4 * q + 2] = v.z;
-            g[4 * q + 3] = v.w;
-        }
+    for (int q = 0; q < kIn / 4; ++q) {
+        const float4 v = src[q];
+        g[4 * q] = v.x;
+        g[4 * q + 1] = v.y;
+        g[4 * q + 2] = v.z;
+        g[4 * q + 3] = v.w;
+    }
+    return true;
+}
+
+// S1: d_t_slot = dL/dt + dot(dL/dx, dir) (renderer.cpp:283-284) — what the compositing
+// branch needs; the table gradients (S2) can then run beside it
+__global__ void __launch_bounds__(128) scatter_dt_kernel(const FieldBwdArgs a, const TcConst cst,
+                                                         const float* __restrict__ fbuf, int64_t total,
+                                                         const float* __restrict__ jbuf) {
+    const int64_t sl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    double dir[3], t, x[3];
+    float g[kIn];
+    const bool valid = scatter_slot(a, fbuf, sl, total, dir, t, x, g);
+    if (!valid) {
+        if (sl < total) a.d_t_slot[sl] = 0.0;
+        return;
     }
     const float ft = static_cast<float>(a.cam.fx / t);
     double dx[3] = {0.0, 0.0, 0.0}, dt = 0.0;
-    const bool small = fmax(fabs(x0), fmax(fabs(x1), fabs(x2))) * cst.level_scale[kLevels - 1] < 1073741824.0;
+    scatter_dt(a, cst, true, ft, g, t, dx, dt, jbuf, total, sl);
+    a.d_t_slot[sl] = dt + (dx[0] * dir[0] + dx[1] * dir[1] + dx[2] * dir[2]);
+}
+
+// S2: the table gradients
+__global__ void __launch_bounds__(128) scatter_table_kernel(const FieldBwdArgs a, const TcConst cst,
+                                                            const float* __restrict__ fbuf, int64_t total,
+                                                            const Xacc tacc) {
+    const int64_t sl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    double dir[3], t, x[3];
+    float g[kIn];
+    const bool valid = scatter_slot(a, fbuf, sl, total, dir, t, x, g);
+    if (!__any_sync(0xffffffffu, valid)) return;
+    __shared__ float2 wsh[128];
+    const float ft = static_cast<float>(a.cam.fx / t);
+    const bool small = fmax(fabs(x[0]), fmax(fabs(x[1]), fabs(x[2]))) * cst.level_scale[kLevels - 1] < 1073741824.0;
     if (__all_sync(0xffffffffu, small))
-        scatter_levels<true>(a, cst, valid, x0, x1, x2, ft, g, t, dx, dt, tacc, wsh + (threadIdx.x & ~31), jbuf, total,
-                             sl);
+        scatter_table<true>(a, cst, valid, x[0], x[1], x[2], ft, g, tacc, wsh + (threadIdx.x & ~31));
     else
-        scatter_levels<false>(a, cst, valid, x0, x1, x2, ft, g, t, dx, dt, tacc, wsh + (threadIdx.x & ~31), jbuf, total,
-                              sl);
-    if (in) a.d_t_slot[sl] = valid ? dt + (dx[0] * dir[0] + dx[1] * dir[1] + dx[2] * dir[2]) : 0.0;
+        scatter_table<false>(a, cst, valid, x[0], x[1], x[2], ft, g, tacc, wsh + (threadIdx.x & ~31));
 }
 
 }  // namespace
@@ -1017,9 +1041,18 @@ int launch_field_backward_tc(const FieldBwdArgs& a, cudaStream_t s) {
     mlp_bwd_tc_kernel<<<grid_m, kThreadsM, kSmemM, s>>>(a, sc.fbuf, sc.parts, total, n_tiles);
     reduce_wgrads_kernel<<<(kWGrads + 255) / 256, 256, 0, s>>>(sc.parts, grid_m, a.g_w1, a.g_w2, a.g_w3);
     const Xacc tacc{sc.tx, tneed};
-    scatter_kernel<<<blocks, 128, 0, s>>>(a, cst, sc.fbuf, total, sc.jbuf, tacc);
-    count_launch();
-    take_table_kernel<<<8 * sms, 256, 0, s>>>(a.g_table, tacc);
+    scatter_dt_kernel<<<blocks, 128, 0, s>>>(a, cst, sc.fbuf, total, sc.jbuf);
+    // the table gradients beside the compositing branch (which needs d_t_slot only)
+    cudaStream_t st = s;
+    if (a.side && a.ev_fork && a.ev_join) {
+        cudaEventRecord(a.ev_fork, s);
+        cudaStreamWaitEvent(a.side, a.ev_fork, 0);
+        st = a.side;
+    }
+    count_launch(2);
+    scatter_table_kernel<<<blocks, 128, 0, st>>>(a, cst, sc.fbuf, total, tacc);
+    take_table_kernel<<<8 * sms, 256, 0, st>>>(a.g_table, tacc);
+    if (st != s) cudaEventRecord(a.ev_join, st);
     return NX_OK;
 }
 

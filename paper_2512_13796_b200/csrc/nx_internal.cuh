@@ -342,6 +342,10 @@ struct FieldBwdArgs {
     double* g_w2;
     double* g_w3;
     FieldBwdScratch* scratch;  // the context's
+    // optional: the table-gradient scatter runs on `side` (forked after d_t_slot with
+    // ev_fork); ev_join is recorded there when it is done (the caller joins it)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 // field_backward_batch (texture_field.cpp:77-146) over the buffered slots.
 int launch_field_backward(const FieldBwdArgs& a, cudaStream_t s);
