@@ -168,6 +168,51 @@ def test_backward_is_bit_reproducible(renderer, reference, case):
             assert np.array_equal(a, b)
 
 
+_OVERLAP_SCRIPT = r"""
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2512_13796_b200 as nx
+from paper_2512_13796_b200 import SceneGrads, UpstreamGrads
+scene = nx.stump_like(30_000, log2_table=16, grid_init=1e-1)
+cam = nx.ring_camera(23, 256, 320, 240)
+K, npix = scene.settings.top_k, cam.width * cam.height
+rng = np.random.default_rng(5)
+up = UpstreamGrads(d_final=rng.standard_normal(npix * 3), d_weights=rng.standard_normal(npix * K),
+                   d_texture=rng.standard_normal(npix * K * 3))
+r = nx.Renderer(0)
+ds = r.upload(scene)
+fr = r.frame()
+fr.set_backward(True)
+r.render(ds, cam, fr)
+g = SceneGrads.allocate(scene)
+be = np.zeros(scene.nexels.shape[0])
+r.render_backward(ds, cam, fr, up, g, np.random.default_rng(6).random(npix), be)
+h = hashlib.sha256()
+for a in (g.prims, g.table, g.w1, g.w2, g.w3, be):
+    h.update(np.ascontiguousarray(a).tobytes())
+print(h.hexdigest(), float(np.abs(g.table).max()))
+"""
+
+
+def test_backward_side_stream_is_bit_identical():
+    """The table-gradient scatter on the context's side stream (default) and on the
+    caller's stream (NX_BWD_OVERLAP=0) give the same bits."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for overlap in ("1", "0"):
+        env = dict(os.environ, NX_BWD_OVERLAP=overlap)
+        res = subprocess.run([sys.executable, "-c", _OVERLAP_SCRIPT, root], env=env, capture_output=True,
+                             text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        outs.append(res.stdout.strip().splitlines()[-1].split())
+    assert float(outs[0][1]) > 0
+    assert outs[0][0] == outs[1][0]
+
+
 def test_backward_needs_the_forward_state(renderer, reference):
     scene, cam = reference.random_scene(32, 20, 2, 32, 40.0, 3.0)
     ds = renderer.upload(scene)
