@@ -941,7 +941,10 @@ __global__ void __launch_bounds__(128) scatter_dt_kernel(const FieldBwdArgs a, c
 }
 
 // S2: the table gradients
-__global__ void __launch_bounds__(128) scatter_table_kernel(const FieldBwdArgs a, const TcConst cst,
+#ifndef NX_SCATTER_MINB
+#define NX_SCATTER_MINB 1
+#endif
+__global__ void __launch_bounds__(128, NX_SCATTER_MINB) scatter_table_kernel(const FieldBwdArgs a, const TcConst cst,
                                                             const float* __restrict__ fbuf, int64_t total,
                                                             const Xacc tacc) {
     const int64_t sl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
