@@ -876,10 +876,23 @@ __device__ __forceinline__ void scatter_table(const FieldBwdArgs& a, const TcCon
                 wsh[lane] = make_float2(u0, u1);
                 __syncwarp();
                 if (valid && lane == __ffs(peers) - 1)
-                    for (uint32_t m = peers; m; m &= m - 1) {
-                        const float2 u = wsh[__ffs(m) - 1];
-                        my0 += u.x;
-                        my1 += u.y;
+                    for (uint32_t m = peers; m;) {
+                        // four members per round: independent loads, adds still in lane order
+                        int idx[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            idx[q] = __ffs(m) - 1;
+                            m &= m - 1;
+                        }
+                        float2 u[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) u[q] = wsh[idx[q] < 0 ? 0 : idx[q]];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (idx[q] >= 0) {
+                                my0 += u[q].x;
+                                my1 += u[q].y;
+                            }
                     }
                 __syncwarp();
             }
