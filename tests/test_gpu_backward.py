@@ -101,14 +101,16 @@ def test_stump_textured_gradients_match_reference(renderer, reference):
     (4_000, 90, (128, 96), 1e-1, "no_prim_sh"),
     (4_000, 130, (128, 96), 1e-1, "no_gamma"),
     (4_000, 200, (128, 96), 1e-1, "k4"),
+    (4_000, 210, (128, 96), 1e-1, "k3"),           # 128-slot tiles split pixels (3 does not divide 128)
+    (4_000, 220, (128, 96), 1e-1, "k1"),
     (6_000, 60, (640, 480), 1e-1, None),          # >= 4 x SMs 16x16 tiles: the 16x16 work-tile kernel
 ])
 def test_stump_field_tc_gradients_match_reference(renderer, reference, n, view, size, grid_init, ablation):
     # the reference field shape (16 levels x 2 x 64 hidden) takes the tcgen05 field backward
     scene = nx.stump_like(n, log2_table=16, grid_init=grid_init)
     st = scene.settings
-    if ablation == "k4":
-        st.top_k = 4
+    if ablation in ("k4", "k3", "k1"):
+        st.top_k = int(ablation[1])
     elif ablation:
         setattr(st, ablation, True)
     cam = nx.ring_camera(view, 256, *size)
