@@ -83,6 +83,19 @@ def test_config1_textured_variant(renderer, reference):
     assert np.abs(r.texture - 0.5).max() > 1e-2  # the texture really varies
 
 
+@pytest.mark.parametrize("k", [1, 3, 5, 8])
+def test_textured_top_k(renderer, reference, k):
+    """The reference field shape (tcgen05 decoder, 128-slot tiles) at top-K values that
+    do not divide a tile (3, 5) and at the extremes."""
+    scene = nx.stump_like(6_000, grid_init=1e-1)
+    scene.settings.top_k = k
+    cam = nx.ring_camera(40 + k, 256, 160, 120)
+    g, _ = gpu_render(renderer, scene, cam)
+    r = reference.render(scene, cam)
+    rep = compare_frames(g, r)
+    assert rep["psnr"] >= 60
+
+
 @pytest.mark.parametrize("view", [17, 64, 129, 200])
 def test_config3_views(renderer, reference, view):
     """Several views of the ring (config 3 shape at 256^2)."""
