@@ -48,7 +48,7 @@ def run_both(renderer, reference, scene, cam, gt, w, table_rtol=LOSS_RTOL):
     return terms
 
 
-@pytest.mark.parametrize("top_k", [2, 0, 4])
+@pytest.mark.parametrize("top_k", [2, 0, 4, 1, 3])
 def test_losses_match_reference_against_random_gt(renderer, reference, top_k):
     scene = nx.stump_like(3_000, log2_table=14, grid_init=1e-1)
     scene.settings.top_k = top_k
