@@ -215,6 +215,21 @@ def test_backward_side_stream_is_bit_identical():
     assert outs[0][0] == outs[1][0]
 
 
+def test_backward_of_an_empty_scene_is_zero(renderer, reference):
+    """No primitives: the background does not depend on the parameters — every gradient
+    (field included) is zero, like the reference's."""
+    base = nx.stump_like(2_000, log2_table=16, grid_init=1e-1)
+    scene = nx.Scene(np.zeros((0, 60)), base.field, base.settings)
+    cam = nx.ring_camera(5, 256, 96, 64)
+    up = upstream(cam, scene.settings.top_k, 3)
+    g, _, _ = gpu_backward(renderer, scene, cam, up)
+    r = ref_backward(reference, scene, cam, up)
+    for a in g[:5]:
+        assert not np.any(a)
+    for a in r[:5]:
+        assert not np.any(a)
+
+
 def test_backward_needs_the_forward_state(renderer, reference):
     scene, cam = reference.random_scene(32, 20, 2, 32, 40.0, 3.0)
     ds = renderer.upload(scene)
