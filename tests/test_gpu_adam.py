@@ -124,3 +124,21 @@ def test_pixel_error_matches_the_trainer(renderer):
     renderer.synchronize()
     want = np.abs(fin - gt).reshape(-1, 3).sum(axis=1) / 3.0
     assert np.allclose(err_d.cpu().numpy(), want, rtol=1e-15, atol=1e-15)
+
+
+def test_adam_on_an_empty_scene(renderer):
+    """No primitives: the primitive groups are empty, the field groups still step (zero
+    gradients leave them unchanged) and nothing faults."""
+    base = nx.stump_like(1_000, log2_table=10, grid_init=1e-1)
+    scene = nx.Scene(np.zeros((0, 60)), base.field, base.settings)
+    ds = renderer.upload(scene)
+    opt = renderer.optimizer(ds)
+    assert opt.size(0) == 0
+    before = opt.download(8)[0]
+    grads = [torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
+             for n in (0, base.field.grid.param_count(), base.field.w1.size, base.field.w2.size, base.field.w3.size)]
+    torch.cuda.synchronize()
+    opt.step([t.data_ptr() for t in grads], [(1e-3, 0.9, 0.999, 1e-8)] * 11)
+    renderer.synchronize()
+    assert all(s == 1 for s in opt.steps()[7:])
+    assert np.array_equal(opt.download(8)[0], before)
