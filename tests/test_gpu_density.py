@@ -104,3 +104,29 @@ def test_densify_then_prune_match_reference(renderer, reference, n0):
         host[:, COLS[gi]] = p.reshape(n2.value, -1)
     assert np.allclose(after[:, :12], host[:, :12], rtol=1e-11, atol=1e-14)
     renderer.lib.nx_optimizer_destroy(opt)
+
+
+def test_density_control_on_an_empty_scene(renderer, reference):
+    """densify_split and prune of an empty scene: nothing to split or keep, like the
+    reference's (density.cpp:102-177)."""
+    base = nx.stump_like(500, log2_table=10, grid_init=1e-1)
+    scene = nx.Scene(np.zeros((0, 60)), base.field, base.settings)
+    ref_nex, ref_map, ref_splits, _ = reference.densify_split(scene.nexels, np.zeros(0), 16, 0.1, 77)
+    ref_pruned, _ = reference.prune(scene.nexels, 0.5)
+    assert ref_nex.shape[0] == 0 and ref_splits == 0 and ref_pruned.shape[0] == 0
+    ds = renderer.upload(scene)
+    opt = renderer.optimizer(ds)
+    n2o = torch.zeros(16, dtype=torch.int32, device="cuda")
+    e_t = torch.zeros(1, dtype=torch.float64, device="cuda")
+    u_t = torch.zeros(1, dtype=torch.float64, device="cuda")
+    n_out, sc = C.c_int64(-1), C.c_int64(-1)
+    renderer._check(renderer.lib.nx_scene_densify_split(renderer.ctx, ds.handle, opt.handle,
+                                                        C.c_void_p(e_t.data_ptr()), C.c_void_p(u_t.data_ptr()), 16,
+                                                        0.1, C.c_void_p(n2o.data_ptr()), C.byref(n_out),
+                                                        C.byref(sc)))
+    assert (n_out.value, sc.value) == (0, 0)
+    pmap = torch.zeros(1, dtype=torch.int32, device="cuda")
+    n2 = C.c_int64(-1)
+    renderer._check(renderer.lib.nx_scene_prune(renderer.ctx, ds.handle, opt.handle, 0.5,
+                                                C.c_void_p(pmap.data_ptr()), C.byref(n2)))
+    assert n2.value == 0
