@@ -328,6 +328,12 @@ typedef struct nx_optimizer nx_optimizer;
 int nx_optimizer_create(nx_ctx* ctx, const nx_scene* scene, nx_optimizer** out);
 /* Parameter count of a group (AdamState size once stepped). */
 int nx_optimizer_size(const nx_optimizer* opt, int group, int64_t* count);
+/* nx_losses_backward with the grid regulariser (losses.cpp:212-228) evaluated on the
+ * optimizer's fp64 master of the hash table — the values being trained — instead of
+ * the scene's fp32 render copy (what the trainer drop-in calls). opt may be NULL. */
+int nx_losses_backward_opt(nx_ctx* ctx, const nx_scene* scene, const nx_frame* frame, const double* gt,
+                           const nx_loss_weights* w, double* d_final, double* d_weights, double* d_texture,
+                           const nx_grads* grads, nx_loss_terms* terms, const nx_optimizer* opt, void* stream);
 /* Sets the fp64 master values of a group from HOST memory (count = its size, in the
  * group's row layout: per-nexel rows of the group's width, or the flat field block),
  * e.g. the exact fp64 initialisation the fp32 scene upload rounded. Geometry groups

@@ -225,6 +225,8 @@ SIGNATURES = [
     ("nx_loss_weights_default", None, [C.POINTER(nx_loss_weights)]),
     ("nx_losses_backward", C.c_int,
      [P, P, P, P, C.POINTER(nx_loss_weights), P, P, P, C.POINTER(nx_grads), P, P]),
+    ("nx_losses_backward_opt", C.c_int,
+     [P, P, P, P, C.POINTER(nx_loss_weights), P, P, P, C.POINTER(nx_grads), P, P, P]),
     ("nx_losses_backward_host", C.c_int,
      [P, P, P, PD, C.POINTER(nx_loss_weights), PD, PD, PD, C.POINTER(nx_grads), C.POINTER(nx_loss_terms)]),
     ("nx_optimizer_create", C.c_int, [P, P, C.POINTER(P)]),

@@ -92,6 +92,7 @@ struct nx_ctx {
     DevBuf skeys_a, skeys_b, sids_a, sids_b, counts, offsets;
     DevBuf tkeys_a, tkeys_b, tvals_a, tvals_b, tile_counts, scratch;
     DevBuf dbg_hits, dbg_counts;
+    DevBuf valid_word;  // revalidation result (first failing primitive)
     // render_backward scratch
     nx_frame* bwd_lists = nullptr;   // work lists of the re-binned camera
     DevBuf d_t_slot, act_grad, xacc_prims;
@@ -139,6 +140,7 @@ struct nx_scene {
     nx_settings st{};
     int bad_status = NX_OK;
     std::string bad_msg;
+    uint64_t validated_version = 0;  // the version bad_status describes
 };
 
 struct nx_frame {
@@ -333,11 +335,42 @@ void next_event_set(nx_ctx* c) {
     fold_set(c, c->ev_cur, true);
 }
 
-int check_inputs(nx_ctx* c, const nx_scene* scene, const nx_camera* cam) {
+const char* const kBadWhat[] = {"non-finite position", "non-finite quaternion", "non-finite log scale",
+                                "non-finite kernel exponent", "non-finite opacity", "non-finite sh coefficient",
+                                "degenerate quaternion"};
+
+// The reference activates every primitive on every render (renderer.cpp:38,
+// primitive.cpp:47-63). Scenes are validated when created; after any change of their
+// parameters (Adam, set_params, densify, prune: a new version) the next render
+// re-runs the checks on the device before using them (one small read-back).
+int revalidate(nx_ctx* c, nx_scene* scene, cudaStream_t s) {
+    if (scene->validated_version == scene->version) return NX_OK;
+    NX_CUDA(c, c->valid_word.ensure(sizeof(unsigned long long)));
+    unsigned long long* first = c->valid_word.as<unsigned long long>();
+    NX_CUDA(c, cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), s));
+    launch_validate(scene->geom.as<double>(), scene->sh.as<float>(), scene->n, first, s);
+    unsigned long long* h = reinterpret_cast<unsigned long long*>(c->h_pinned + 32);
+    NX_CUDA(c, cudaMemcpyAsync(h, first, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    NX_CUDA(c, cudaStreamSynchronize(s));
+    const unsigned long long v = *h;
+    if (v == ~0ull) {
+        scene->bad_status = NX_OK;
+        scene->bad_msg.clear();
+    } else {
+        scene->bad_status = NX_BAD_PRIMITIVE;
+        scene->bad_msg = std::string(kBadWhat[v & 7]) + " in primitive " + std::to_string(v >> 3);
+    }
+    scene->validated_version = scene->version;
+    return NX_OK;
+}
+
+int check_inputs(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, cudaStream_t s = nullptr) {
     if (!c || !scene || !cam) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
     int st;
     if ((st = validate_settings(c, scene->st))) return st;
     if ((st = validate_camera(c, *cam))) return st;
+    // on the caller's stream, after whatever changed the parameters there
+    if ((st = revalidate(c, const_cast<nx_scene*>(scene), s ? s : c->stream))) return st;
     if (scene->bad_status) return set_err(c, scene->bad_status, scene->bad_msg);
     return NX_OK;
 }
@@ -461,7 +494,7 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
 int collection(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* f, cudaStream_t s,
                int32_t* dbg_hits, int32_t* dbg_counts, int dbg_y0, int dbg_y1, int dbg_max) {
     int st;
-    if ((st = check_inputs(c, scene, cam))) return st;
+    if ((st = check_inputs(c, scene, cam, s))) return st;
     // the frame may still be read by its previous texture pass / download (second stream)
     if (f->busy_pending) NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_busy, 0));
     if ((st = frame_shape(c, f, cam->width, cam->height, scene->st.top_k, scene->st.tile))) return st;
@@ -591,7 +624,7 @@ void nx_ctx_destroy(nx_ctx* c) {
     cudaStreamSynchronize(c->stream_bwd);
     for (DevBuf* b : {&c->rec, &c->recf, &c->cls, &c->ref_rect, &c->work_rect, &c->key, &c->flag, &c->pos, &c->skeys_a,
                       &c->skeys_b, &c->sids_a, &c->sids_b, &c->counts, &c->offsets, &c->tkeys_a, &c->tkeys_b,
-                      &c->tvals_a, &c->tvals_b, &c->tile_counts, &c->scratch, &c->dbg_hits, &c->dbg_counts})
+                      &c->tvals_a, &c->tvals_b, &c->tile_counts, &c->scratch, &c->dbg_hits, &c->dbg_counts, &c->valid_word})
         b->release();
     for (DevBuf* b : {&c->d_t_slot, &c->act_grad, &c->xacc_prims, &c->dens_map, &c->dens_par, &c->dens_src, &c->h_err, &c->h_blend, &c->loss_scratch, &c->h_gt, &c->h_terms})
         b->release();
@@ -672,9 +705,7 @@ int nx_scene_create(nx_ctx* c, const nx_settings* settings, int64_t n, const dou
     s->field = *field;
     s->st = *settings;
     // Validation exactly as activate() (primitive.cpp:47-63), first failing id.
-    const char* whats[] = {"non-finite position", "non-finite quaternion", "non-finite log scale",
-                           "non-finite kernel exponent", "non-finite opacity", "non-finite sh coefficient",
-                           "degenerate quaternion"};
+    const char* const* whats = kBadWhat;
     for (int64_t i = 0; i < n && !s->bad_status; ++i) {
         const double* p = nexels + i * NX_PARAMS_PER_NEXEL;
         int what = -1;
@@ -729,10 +760,14 @@ int nx_scene_create(nx_ctx* c, const nx_settings* settings, int64_t n, const dou
     if (e == cudaSuccess) e = upload_f32(s->w1, w1, nh * n_in);
     if (e == cudaSuccess) e = upload_f32(s->w2, w2, nh * nh);
     if (e == cudaSuccess) e = upload_f32(s->w3, w3, NX_SH_VALUES * nh);
+    // pageable cudaMemcpy may return before its DMA lands, and the context's
+    // non-blocking streams do not order after the legacy stream: finish it here
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         nx_scene_destroy(s);
         return cuda_err(c, e, "scene upload");
     }
+    s->validated_version = s->version;  // validated above, on the host
     *out = s;
     return NX_OK;
 }
@@ -759,9 +794,7 @@ int nx_scene_load_nexl(nx_ctx* c, const char* path, nx_scene** out, nx_nexl_info
     s->field = h.info.field;
     s->st = h.info.settings;
     // validation exactly as activate() (primitive.cpp:47-63), first failing id
-    const char* whats[] = {"non-finite position", "non-finite quaternion", "non-finite log scale",
-                           "non-finite kernel exponent", "non-finite opacity", "non-finite sh coefficient",
-                           "degenerate quaternion"};
+    const char* const* whats = kBadWhat;
     for (int64_t i = 0; i < n && !s->bad_status; ++i) {
         int what = -1;
         for (int k = 0; k < 3 && what < 0; ++k)
@@ -805,11 +838,13 @@ int nx_scene_load_nexl(nx_ctx* c, const char* path, nx_scene** out, nx_nexl_info
     if (e == cudaSuccess) e = up(s->w1, arr.w1.data(), arr.w1.size() * sizeof(float));
     if (e == cudaSuccess) e = up(s->w2, arr.w2.data(), arr.w2.size() * sizeof(float));
     if (e == cudaSuccess) e = up(s->w3, arr.w3.data(), arr.w3.size() * sizeof(float));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();  // pageable copies complete before stream work
     if (e != cudaSuccess) {
         nx_scene_destroy(s);
         return cuda_err(c, e, "checkpoint upload");
     }
     if (info) *info = h.info;
+    s->validated_version = s->version;  // validated above, on the host
     *out = s;
     return NX_OK;
 }
@@ -1025,7 +1060,7 @@ int nx_render_backward(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, n
                        const nx_grads* g, const double* err_pixel, double* blended_error, void* stream) {
     if (!c || !f || !up || !g) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
     int st;
-    if ((st = check_inputs(c, scene, cam))) return st;
+    if ((st = check_inputs(c, scene, cam, pick_stream(c, stream)))) return st;
     if (!g->prims || !g->table || !g->w1 || !g->w2 || !g->w3)
         return set_err(c, NX_INVALID_ARGUMENT, "render_backward: every gradient array is required");
     if (f->W != cam->width || f->H != cam->height || f->K != scene->st.top_k)
@@ -1206,9 +1241,11 @@ void nx_loss_weights_default(nx_loss_weights* w) {  // LossWeights (losses.hpp:1
 }
 
 // losses_backward (losses.cpp:107-238) on the frame's final_img / slots.
-int nx_losses_backward(nx_ctx* c, const nx_scene* scene, const nx_frame* fc, const double* gt,
-                       const nx_loss_weights* w, double* d_final, double* d_weights, double* d_texture,
-                       const nx_grads* g, nx_loss_terms* terms, void* stream) {
+}  // extern "C"
+namespace {
+int losses_backward(nx_ctx* c, const nx_scene* scene, const nx_frame* fc, const double* gt,
+                    const nx_loss_weights* w, double* d_final, double* d_weights, double* d_texture,
+                    const nx_grads* g, nx_loss_terms* terms, void* stream, const double* table64) {
     if (!c || !scene || !fc || !gt || !w || !d_final || !g || !g->prims || !g->table || !terms)
         return set_err(c, NX_INVALID_ARGUMENT, "null argument");
     nx_frame* f = const_cast<nx_frame*>(fc);
@@ -1223,12 +1260,20 @@ int nx_losses_backward(nx_ctx* c, const nx_scene* scene, const nx_frame* fc, con
     const int64_t npix = static_cast<int64_t>(f->W) * f->H;
     NX_CUDA(c, c->loss_scratch.ensure(losses_scratch_bytes(npix)));
     const int st = launch_losses_backward(scene_dev(scene), frame_dev(f), gt, *w, d_final, d_weights, d_texture,
-                                          g->prims, g->table, terms, c->loss_scratch.p, s);
+                                          g->prims, g->table, terms, c->loss_scratch.p, s, table64);
     if (st) return set_err(c, st, "losses_backward: field shape not supported");
     NX_CUDA(c, cudaEventRecord(f->ev_busy, s));
     f->busy_pending = true;
     NX_CUDA(c, cudaGetLastError());
     return NX_OK;
+}
+}  // namespace
+extern "C" {
+
+int nx_losses_backward(nx_ctx* c, const nx_scene* scene, const nx_frame* fc, const double* gt,
+                       const nx_loss_weights* w, double* d_final, double* d_weights, double* d_texture,
+                       const nx_grads* g, nx_loss_terms* terms, void* stream) {
+    return losses_backward(c, scene, fc, gt, w, d_final, d_weights, d_texture, g, terms, stream, nullptr);
 }
 
 int nx_pixel_error(nx_ctx* c, const nx_frame* fc, const double* gt, double* err, void* stream) {
@@ -1327,6 +1372,20 @@ int nx_optimizer_create(nx_ctx* c, const nx_scene* scene, nx_optimizer** out) {
     return NX_OK;
 }
 
+int nx_losses_backward_opt(nx_ctx* c, const nx_scene* scene, const nx_frame* fc, const double* gt,
+                           const nx_loss_weights* w, double* d_final, double* d_weights, double* d_texture,
+                           const nx_grads* g, nx_loss_terms* terms, const nx_optimizer* opt, void* stream) {
+    const double* table64 = nullptr;
+    if (opt) {
+        const nx_field_desc& fd = scene ? scene->field : nx_field_desc{};
+        const int64_t ntab = static_cast<int64_t>(fd.levels) * (int64_t(1) << fd.log2_table) * fd.features;
+        if (opt->size[NX_GROUP_GRID] != ntab)
+            return set_err(c, NX_INVALID_ARGUMENT, "losses_backward: the optimizer does not match the scene's table");
+        table64 = opt->master[NX_GROUP_GRID].as<double>();
+    }
+    return losses_backward(c, scene, fc, gt, w, d_final, d_weights, d_texture, g, terms, stream, table64);
+}
+
 int nx_optimizer_size(const nx_optimizer* o, int group, int64_t* count) {
     if (!o || !count || group < 0 || group >= NX_NUM_GROUPS) return NX_INVALID_ARGUMENT;
     *count = o->size[group];
@@ -1414,8 +1473,9 @@ int nx_optimizer_step(nx_ctx* c, nx_optimizer* o, nx_scene* scene, const nx_grad
     scene->version = next_scene_version();
     const SceneDev sd = scene_dev(scene);
     for (int gi = 0; gi < NX_NUM_GROUPS; ++gi) {
-        if (cfg[gi].lr < 0.0 || o->size[gi] == 0) continue;
-        ++o->step[gi];
+        if (cfg[gi].lr < 0.0) continue;
+        ++o->step[gi];  // adam.cpp:12: the step counts even when the group is empty
+        if (o->size[gi] == 0) continue;
         launch_adam_group(gi, sd, scene->geom.as<double>(), scene->sh.as<float>(), scene->table.as<float>(),
                           scene->w1.as<float>(), scene->w2.as<float>(), scene->w3.as<float>(), *g, o->m[gi].as<double>(),
                           o->v[gi].as<double>(), gi >= NX_GROUP_SH_DC ? o->master[gi].as<double>() : nullptr, cfg[gi],
@@ -1523,7 +1583,8 @@ int nx_scene_densify_split(nx_ctx* c, nx_scene* scene, nx_optimizer* opt, const 
         if (new_to_old && n) {
             std::vector<int32_t> id(static_cast<size_t>(n));
             for (int64_t i = 0; i < n; ++i) id[i] = static_cast<int32_t>(i);
-            NX_CUDA(c, cudaMemcpy(new_to_old, id.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
+            NX_CUDA(c, cudaMemcpyAsync(new_to_old, id.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+            NX_CUDA(c, cudaStreamSynchronize(s));
         }
         return NX_OK;
     };
@@ -1546,13 +1607,14 @@ int nx_scene_densify_split(nx_ctx* c, nx_scene* scene, nx_optimizer* opt, const 
     allowed = std::min<int64_t>(allowed, static_cast<int64_t>(n_keys));
     if (allowed <= 0) return identity();
     std::vector<int32_t> parents(static_cast<size_t>(allowed));
-    NX_CUDA(c, cudaMemcpy(parents.data(), in_b ? c->sids_b.p : c->sids_a.p, allowed * sizeof(int32_t),
-                          cudaMemcpyDeviceToHost));
+    NX_CUDA(c, cudaMemcpyAsync(parents.data(), in_b ? c->sids_b.p : c->sids_a.p, allowed * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, s));
+    NX_CUDA(c, cudaStreamSynchronize(s));
     std::sort(parents.begin(), parents.end());  // density.cpp:132-134
     const int64_t n_new = n + allowed;
     DevBuf &d_par = c->dens_par, &map = c->dens_map, &src = c->dens_src;
     NX_CUDA(c, d_par.ensure(allowed * sizeof(int32_t)));
-    NX_CUDA(c, cudaMemcpy(d_par.p, parents.data(), allowed * sizeof(int32_t), cudaMemcpyHostToDevice));
+    NX_CUDA(c, cudaMemcpyAsync(d_par.p, parents.data(), allowed * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     NX_CUDA(c, map.ensure(n_new * sizeof(int32_t)));
     NX_CUDA(c, scene->geom_spare.ensure(n_new * kGeomFields * sizeof(double)));
     NX_CUDA(c, scene->sh_spare.ensure(n_new * NX_SH_VALUES * sizeof(float)));

@@ -194,6 +194,10 @@ struct PreprocessArgs {
 };
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t s);
 
+// activate()'s validation (primitive.cpp:47-63) of a device scene: *first (preset to
+// ~0) receives min(id * 8 + check) over the failing primitives.
+void launch_validate(const double* geom, const float* sh, int64_t n, unsigned long long* first, cudaStream_t s);
+
 // Gathers (key, id) of flagged primitives at their scanned positions (id-ascending).
 void launch_compact(const int32_t* flag, const int32_t* pos, const uint64_t* key, int64_t n,
                     uint64_t* keys_out, uint32_t* ids_out, cudaStream_t s);
@@ -244,7 +248,7 @@ int launch_texture_tc(const TextureArgs& a, cudaStream_t s);
 size_t losses_scratch_bytes(int64_t npix);
 int launch_losses_backward(const SceneDev& scene, const FrameDev& fb, const double* gt, const nx_loss_weights& w,
                            double* d_final, double* d_weights, double* d_texture, double* g_prims, double* g_table,
-                           nx_loss_terms* terms, void* scratch, cudaStream_t s);
+                           nx_loss_terms* terms, void* scratch, cudaStream_t s, const double* table64 = nullptr);
 
 // ---------------------------------------------------------------- Adam (nx_adam.cu)
 void adam_group_sizes(const SceneDev& sc, int64_t* sizes);

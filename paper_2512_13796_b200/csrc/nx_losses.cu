@@ -44,6 +44,7 @@ struct LossArgs {
     const double* gt;
     const double* geom;  // kGeomFields x n SoA (opacity_raw is field 9)
     const float* table;
+    const double* table64;  // optional fp64 master of the table (nullptr: use `table`)
     int levels;
     int64_t level_entries;  // 2^log2 * features
     nx_loss_weights w;
@@ -280,7 +281,9 @@ __global__ void __launch_bounds__(kThreads) grid_kernel(const LossArgs a) {
     double acc = 0.0;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < a.level_entries;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const double v = a.table[base + e];
+        // the fp64 master of the table when the trainer keeps one (the values being
+        // optimised), else the scene's fp32 render copy
+        const double v = a.table64 ? a.table64[base + e] : static_cast<double>(a.table[base + e]);
         acc += v * v;
         a.g_table[base + e] += a.w.grid * 2.0 * v / s3;
     }
@@ -336,7 +339,7 @@ size_t losses_scratch_bytes(int64_t npix) { return sizeof(LossSums) + 256 + stat
 
 int launch_losses_backward(const SceneDev& scene, const FrameDev& fb, const double* gt, const nx_loss_weights& w,
                            double* d_final, double* d_weights, double* d_texture, double* g_prims, double* g_table,
-                           nx_loss_terms* terms, void* scratch, cudaStream_t s) {
+                           nx_loss_terms* terms, void* scratch, cudaStream_t s, const double* table64) {
     if (scene.field.levels > kMaxLevels) return NX_UNSUPPORTED;
     static uint64_t taps_ready = 0;  // per device: __constant__ memory is per device
     int cur = 0;
@@ -364,6 +367,7 @@ int launch_losses_backward(const SceneDev& scene, const FrameDev& fb, const doub
     a.gt = gt;
     a.geom = scene.geom;
     a.table = scene.table;
+    a.table64 = table64;
     a.levels = scene.field.levels;
     a.level_entries = (int64_t(1) << scene.field.log2_table) * scene.field.features;
     a.w = w;

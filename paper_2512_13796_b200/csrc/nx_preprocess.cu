@@ -9,6 +9,8 @@
 // conservative "work rect" that provably contains every pixel whose ray can hit
 // the primitive: the work lists are order-preserving
 // subsequences of the reference lists that drop only provable misses.
+#include <algorithm>
+
 #include "nx_internal.cuh"
 
 namespace nx {
@@ -287,7 +289,42 @@ __global__ void emit_kernel(const uint32_t* ids, const int32_t* offsets, int64_t
     atomicAdd(&tile_counts[tile], 1);
 }
 
+// activate()'s checks (primitive.cpp:47-63) over every primitive of a device scene,
+// in the reference's order within a primitive; the first failing primitive wins:
+// *first = min(id * 8 + what) (what: the index of the failed check).
+__global__ void validate_kernel(const double* __restrict__ geom, const float* __restrict__ sh, int64_t n,
+                                int64_t nn, unsigned long long* first) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double g[kGeomFields];
+#pragma unroll
+        for (int k = 0; k < kGeomFields; ++k) g[k] = geom[k * nn + i];
+        int what = -1;
+        for (int k = 0; k < 3 && what < 0; ++k)
+            if (!isfinite(g[k])) what = 0;
+        for (int k = 0; k < 4 && what < 0; ++k)
+            if (!isfinite(g[3 + k])) what = 1;
+        for (int k = 0; k < 2 && what < 0; ++k) {
+            if (!isfinite(g[7 + k])) what = 2;
+            else if (!isfinite(g[10 + k])) what = 3;
+        }
+        if (what < 0 && !isfinite(g[9])) what = 4;
+        const float* c = sh + i * NX_SH_VALUES;
+        for (int k = 0; k < NX_SH_VALUES && what < 0; ++k)
+            if (!isfinite(c[k])) what = 5;
+        if (what < 0 && !(sqrt(g[3] * g[3] + g[4] * g[4] + g[5] * g[5] + g[6] * g[6]) > 1e-12)) what = 6;
+        if (what >= 0) atomicMin(first, (static_cast<unsigned long long>(i) << 3) | static_cast<unsigned>(what));
+    }
+}
+
 }  // namespace
+
+void launch_validate(const double* geom, const float* sh, int64_t n, unsigned long long* first, cudaStream_t s) {
+    if (n <= 0) return;
+    count_launch();
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 8));
+    validate_kernel<<<blocks, 256, 0, s>>>(geom, sh, n, std::max<int64_t>(n, 1), first);
+}
 
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t s) {
     if (a.scene.n <= 0) return;

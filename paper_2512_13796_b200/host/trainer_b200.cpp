@@ -277,7 +277,8 @@ TrainResult train(const Bundle& bundle, const TrainConfig& cfg, const TrainHooks
         if (bundle.cameras[v].width != im.width || bundle.cameras[v].height != im.height || im.px.size() != npx * 3)
             fail("bad-settings", "train view " + std::to_string(v) + ": image does not match its camera");
         gt[v] = mem.alloc<double>(npx * 3);
-        cuda_check(cudaMemcpy(gt[v], im.px.data(), npx * 3 * sizeof(double), cudaMemcpyHostToDevice), "gt upload");
+        cuda_check(cudaMemcpyAsync(gt[v], im.px.data(), npx * 3 * sizeof(double), cudaMemcpyHostToDevice, cs),
+                   "gt upload");
         max_pix = std::max<int>(max_pix, static_cast<int>(npx));
     }
     const int K = init.settings.top_k;
@@ -334,8 +335,8 @@ TrainResult train(const Bundle& bundle, const TrainConfig& cfg, const TrainHooks
         cuda_check(cudaMemsetAsync(g_w3, 0, n_w3 * sizeof(double), cs), "memset");
         const nx_grads grads{g_prims, g_table, g_w1, g_w2, g_w3};
         const nx_loss_weights lw{cfg.loss.dssim, cfg.loss.alpha, cfg.loss.texture, cfg.loss.opacity, cfg.loss.grid};
-        r.check(nx_losses_backward(r.ctx, r.scene, r.frame, gt[view], &lw, d_final, K ? d_weights : nullptr,
-                                   K ? d_texture : nullptr, &grads, d_terms, s));
+        r.check(nx_losses_backward_opt(r.ctx, r.scene, r.frame, gt[view], &lw, d_final, K ? d_weights : nullptr,
+                                       K ? d_texture : nullptr, &grads, d_terms, r.opt, s));
         nx_loss_terms ht;
         cuda_check(cudaMemcpyAsync(&ht, d_terms, sizeof ht, cudaMemcpyDeviceToHost, cs), "terms");
         cuda_check(cudaStreamSynchronize(cs), "sync");
@@ -376,7 +377,8 @@ TrainResult train(const Bundle& bundle, const TrainConfig& cfg, const TrainHooks
                     ucap = n;
                     uniforms = mem.alloc<double>(ucap);
                 }
-                cuda_check(cudaMemcpy(uniforms, u.data(), n * sizeof(double), cudaMemcpyHostToDevice), "uniforms");
+                cuda_check(cudaMemcpyAsync(uniforms, u.data(), n * sizeof(double), cudaMemcpyHostToDevice, cs),
+                           "uniforms");
                 r.check(nx_scene_densify_split(r.ctx, r.scene, r.opt, err_accum, uniforms, cfg.budget,
                                                cfg.split_fraction, nullptr, &n_out, &splits));
             }

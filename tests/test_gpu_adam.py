@@ -127,8 +127,9 @@ def test_pixel_error_matches_the_trainer(renderer):
 
 
 def test_adam_on_an_empty_scene(renderer):
-    """No primitives: the primitive groups are empty, the field groups still step (zero
-    gradients leave them unchanged) and nothing faults."""
+    """No primitives: the primitive groups are empty but still count the step like the
+    reference's adam_step (adam.cpp:11-12 increments state.step whatever the count), the
+    field groups step (zero gradients leave them unchanged) and nothing faults."""
     base = nx.stump_like(1_000, log2_table=10, grid_init=1e-1)
     scene = nx.Scene(np.zeros((0, 60)), base.field, base.settings)
     ds = renderer.upload(scene)
@@ -140,5 +141,37 @@ def test_adam_on_an_empty_scene(renderer):
     torch.cuda.synchronize()
     opt.step([t.data_ptr() for t in grads], [(1e-3, 0.9, 0.999, 1e-8)] * 11)
     renderer.synchronize()
-    assert all(s == 1 for s in opt.steps()[7:])
+    assert opt.steps() == [1] * 11
     assert np.array_equal(opt.download(8)[0], before)
+
+
+def test_bad_primitive_after_a_parameter_change(renderer):
+    """The reference activates every primitive on every render (renderer.cpp:38,
+    primitive.cpp:47-63): a parameter change that makes a primitive non-finite or its
+    quaternion degenerate fails the next render with bad-primitive and the first failing
+    id; fixing the values clears it."""
+    scene = nx.stump_like(2_000, log2_table=10)
+    cam = nx.ring_camera(3, 256, 64, 48)
+    ds = renderer.upload(scene)
+    fr = renderer.frame()
+    renderer.render(ds, cam, fr)
+    opt = renderer.optimizer(ds)
+    pos, _, _ = opt.download(0)
+    bad = pos.copy()
+    bad[3 * 41 + 1] = np.nan
+    bad[3 * 1500] = np.inf
+    opt.set_params(0, bad)
+    with pytest.raises(nx.NexelError) as e:
+        renderer.render(ds, cam, fr)
+    assert e.value.code == "bad-primitive" and "non-finite position in primitive 41" in str(e.value)
+    q, _, _ = opt.download(1)
+    opt.set_params(0, pos)
+    q0 = q.copy()
+    q0[4 * 7:4 * 8] = 0.0
+    opt.set_params(1, q0)
+    with pytest.raises(nx.NexelError) as e:
+        renderer.render(ds, cam, fr)
+    assert e.value.code == "bad-primitive" and "degenerate quaternion in primitive 7" in str(e.value)
+    opt.set_params(1, q)
+    renderer.render(ds, cam, fr)  # valid again
+    opt.close()
