@@ -29,6 +29,10 @@ sys.path.insert(0, ROOT)
 METRIC = "rendered 1080p frames/sec at 400K nexels (1/2/4/8 B200) + % HBM roofline"
 UNIT = "frames/s"
 N_VIEWS = 256
+# what the path computes in: every decision, depth and weight in fp64 (the reference's
+# formulas), colours (SH, texture, base/final) in fp32, the decoder MLP as a 3-term
+# split-bf16 product on the tensor cores (~2^-16 relative per product)
+DTYPE = "f64 decisions/depths/weights, f32 colour, bf16x3 MLP"
 
 
 def parse():
@@ -41,7 +45,6 @@ def parse():
     p.add_argument("--width", type=int, default=1920)
     p.add_argument("--height", type=int, default=1080)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU-baseline work")
     p.add_argument("--train-steps", type=int, default=10, help="timed forward+backward steps (config 5); 0 = skip")
     p.add_argument("--config", type=int, choices=[2, 4], default=2,
                    help="2: 400K nexels 1080p, views sharded (headline); 4: 1.3M nexels 4K, image bands x views")
@@ -170,111 +173,97 @@ def barrier(dist):
 
 
 # ---------------------------------------------------------------- CPU baseline (the reference on host cores)
-def cpu_reference_sample(scene, view_cam, budget_s: float):
-    """Reference render path (oracle/_ref, compiled in place) on all host cores over a
-    band of rows of the view; frame time = binning + (band - binning) * H / rows."""
+def host_cpu():
+    """(model name, logical cores) of this host (state nproc and the lscpu model)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count() or 1
+
+
+def cpu_impl():
+    """The reference's own render path (oracle/_ref, compiled in place by oracle/Makefile)
+    on all host cores, else the scalar C restatement (oracle/) on one core."""
     from oracle.pyoracle import Oracle, Reference
-    import paper_2512_13796_b200 as nx
-    cores = os.cpu_count() or 1
+    model, cores = host_cpu()
     os.environ["NEXEL_THREADS"] = str(cores)
     try:
-        impl, kind = Reference(), "reference"
+        return Reference(), "reference", cores, model
     except ImportError:
-        impl, kind = Oracle(), "port"
-        cores = 1
-    H = view_cam.height
+        return Oracle(), "port", 1, model
 
-    def band_cam(y0, rows):
-        return nx.Camera(view_cam.width, rows, view_cam.fx, view_cam.fy, view_cam.cx, view_cam.cy - y0,
-                         view_cam.R, view_cam.t)
 
-    # binning cost (build_binning over all primitives; independent of the band size)
-    t_bin = 0.0
-    if kind == "reference":
+def time_full_frames(impl, scene, cams):
+    """Wall time of whole render(scene, cam) calls (renderer.cpp:239-244), scene
+    generation excluded (std::chrono-style steady clock around the call)."""
+    out = []
+    for cam in cams:
         t0 = time.perf_counter()
-        impl.tile_lists(scene, view_cam)
-        t_bin = time.perf_counter() - t0
-    rows = 32
-    y0 = (H // 2 // 16) * 16
-    t0 = time.perf_counter()
-    impl.render(scene, band_cam(y0, rows))
-    t_band = time.perf_counter() - t0
-    per_row = max(t_band - t_bin, 1e-3) / rows
-    rows = int(min(max(16, (budget_s / 3 - t_bin) / per_row), H - y0))
-    rows = max(16, (rows // 16) * 16)
-    times = []
-    for _ in range(3):
-        t0 = time.perf_counter()
-        impl.render(scene, band_cam(y0, rows))
-        times.append(time.perf_counter() - t0)
-    t_band = statistics.median(times)
-    frame_s = t_bin + max(t_band - t_bin, 0.0) * H / rows
-    sample = (f"rows {y0}-{y0 + rows} of {H} of view 0 (median of 3); frame time = binning {t_bin:.2f}s + "
-              f"(band {t_band:.2f}s - binning) x {H}/{rows}")
-    return {"value": 1.0 / frame_s, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
-            "lib": os.path.basename(getattr(impl, "path", "oracle")), "frame_seconds": frame_s}
+        impl.render(scene, cam)
+        out.append(time.perf_counter() - t0)
+    return out
+
+
+def cpu_reference_sample(scene, view_cam, config1=True):
+    """the reference render path on all host cores, whole frames,
+    median of 3 — config 2 (view 0 at 1920x1080) and config 1 (10K nexels, 256x256)."""
+    impl, kind, cores, model = cpu_impl()
+    times = time_full_frames(impl, scene, [view_cam] * 3)
+    frame_s = statistics.median(times)
+    out = {"value": 1.0 / frame_s, "unit": UNIT, "cores": cores, "kind": kind, "cpu_model": model,
+           "sample": f"3 whole frames of view 0 ({view_cam.width}x{view_cam.height}, {scene.nexels.shape[0]} nexels), "
+                     f"median; render(scene, cam) on {cores} threads (NEXEL_THREADS)",
+           "frame_seconds": frame_s, "frame_seconds_all": times,
+           "lib": os.path.basename(getattr(impl, "path", "oracle"))}
+    if config1 and kind == "reference":
+        s1, c1 = impl.stump_like(10_000), impl.ring_camera(0, N_VIEWS, 256, 256)
+        t1 = time_full_frames(impl, s1, [c1] * 3)
+        out["config1"] = {"value": 1.0 / statistics.median(t1), "unit": UNIT, "frame_seconds": statistics.median(t1),
+                          "sample": "config 1: stump_like 10K nexels, 256x256, view 0, 3 whole frames, median"}
+    return out
 
 
 def run_reference_arm(args):
-    world, rank, local, dist = dist_setup(args)
+    """--impl reference: the reference's own CPU renderer (oracle/_ref: its sources
+    compiled in place, never this repo's kernels) on all host cores, timing whole
+    render(scene, cam) frames of the same views as our arm (config 2/3: view s of the
+    ring at step s). The scene and cameras come from the generator linked into that
+    library, so the process maps no product library. Rank 0 alone runs under torchrun."""
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
-        barrier(dist)
         return
-    import paper_2512_13796_b200 as nx
-    scene = nx.stump_like(args.nexels)
-    cam = nx.ring_camera(0, N_VIEWS, args.width, args.height)
-    from oracle.pyoracle import Oracle, Reference
-    cores = os.cpu_count() or 1
-    os.environ["NEXEL_THREADS"] = str(cores)
-    try:
-        impl, kind = Reference(), "reference"
-    except ImportError:
-        impl, kind = Oracle(), "port"
-        cores = 1
-    H = cam.height
-    y0 = (H // 2 // 16) * 16
-    rows = 32
-
-    def band(y0, rows):
-        return nx.Camera(cam.width, rows, cam.fx, cam.fy, cam.cx, cam.cy - y0, cam.R, cam.t)
-
-    # size the per-step sample so the whole run stays within a few minutes
-    t0 = time.perf_counter()
-    impl.render(scene, band(y0, rows))
-    dt = time.perf_counter() - t0
-    per_step_budget = max(1.0, 150.0 / max(args.steps + args.warmup, 1))
-    if dt < per_step_budget / 2:
-        rows = int(min(H - y0, max(16, rows * per_step_budget / max(dt, 1e-3) * 0.8)))
-        rows = max(16, rows // 16 * 16)
-    for _ in range(args.warmup):
-        impl.render(scene, band(y0, rows))
-    # the binning (build_binning over every primitive) is paid once per frame, not per
-    # band: frame time = binning + (band - binning) * H / rows
-    t_bin = 0.0
-    if kind == "reference":
-        t0 = time.perf_counter()
-        impl.tile_lists(scene, cam)
-        t_bin = time.perf_counter() - t0
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        impl.render(scene, band(y0, rows))
-        times.append(time.perf_counter() - t0)
-    frame_s = [t_bin + max(t - t_bin, 0.0) * H / rows for t in times]
-    total = sum(frame_s)
+    impl, kind, cores, model = cpu_impl()
+    if kind != "reference":
+        raise SystemExit("oracle/_ref is not built: the reference arm needs the reference build")
+    cfg4 = args.config == 4
+    n = (args.nexels if args.nexels != 400_000 else 1_300_000) if cfg4 else args.nexels
+    W, H = ((args.width, args.height) if (args.width, args.height) != (1920, 1080) else (3840, 2160)) if cfg4 \
+        else (args.width, args.height)
+    scene = impl.stump_like(n)
+    cams = [impl.ring_camera(s % N_VIEWS, N_VIEWS, W, H) for s in range(args.warmup + args.steps)]
+    time_full_frames(impl, scene, cams[:args.warmup])
+    times = time_full_frames(impl, scene, cams[args.warmup:])
+    total = sum(times)
     fps = args.steps / total
     line = {
-        "impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC if not cfg4 else f"rendered 4K frames/sec at {n // 1000}K nexels (config 4)",
+        "value": fps, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload(args),
-        "cpu_baseline": {"value": fps, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": f"each step renders rows {y0}-{y0 + rows} of {H} of view 0; frame time = "
-                                   f"binning {t_bin:.2f}s + (step - binning) x {H}/{rows}"},
+        "data": "synthetic", "config": workload(args) if not cfg4 else {"workload": f"config 4: {n} nexels {W}x{H}"},
+        "cpu_baseline": {"value": fps, "unit": UNIT, "cores": cores, "kind": kind, "cpu_model": model,
+                         "sample": f"each step = one whole render(scene, cam) of ring view s ({W}x{H}), "
+                                   f"{cores} threads; per-frame seconds min {min(times):.2f} max {max(times):.2f}"},
         "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "lib": os.path.basename(impl.path),
     }
     print(json.dumps(line), flush=True)
-    barrier(dist)
 
 
 # ---------------------------------------------------------------- config 5: forward + backward
@@ -408,39 +397,29 @@ def train_step_timing(args, r, ds, scene, cam, stream, dist, local):
                            "§8(f)); cpu_baseline re-times the reference's render_backward on this box"}
 
 
-def cpu_reference_backward_sample(scene, cam, rows: int = 64):
-    """The reference's render_backward (oracle/_ref) on all host cores over a band of
-    rows of the view. Both band calls pay one full binning (build_binning visits every
-    primitive whatever the band), so (render + backward) - render is the band's backward
-    compute alone; render_backward re-bins once per frame, so
-    per frame = binning + band backward x H / rows."""
+def cpu_reference_backward_sample(scene, cam):
+    """The reference's render_backward (oracle/_ref) on all host cores over one whole
+    frame of the view (it re-bins internally, renderer.cpp:257), after a whole-frame
+    forward; random upstream gradients of the frame's shape."""
     import numpy as np
-    from oracle.pyoracle import Reference
-    import paper_2512_13796_b200 as nx
-    ref = Reference()
-    cores = os.cpu_count() or 1
-    os.environ["NEXEL_THREADS"] = str(cores)
-    H = cam.height
-    y0 = (H // 2 // 16) * 16
-    band = nx.Camera(cam.width, rows, cam.fx, cam.fy, cam.cx, cam.cy - y0, cam.R, cam.t)
+    impl, kind, cores, model = cpu_impl()
+    if kind != "reference":
+        return None
     K = scene.settings.top_k
-    npix = cam.width * rows
+    npix = cam.width * cam.height
     g = np.random.default_rng(0)
     up = [g.standard_normal(npix * 3), g.standard_normal(npix * K), g.standard_normal(npix * K * 3)]
     t0 = time.perf_counter()
-    ref.tile_lists(scene, cam)
-    t_bin = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    ref.render(scene, band)
+    impl.render(scene, cam)
     t_fwd = time.perf_counter() - t0
     t0 = time.perf_counter()
-    ref.render_backward(scene, band, *up)
+    impl.render_backward(scene, cam, *up)  # the driver renders, then calls render_backward
     t_both = time.perf_counter() - t0
-    t_band = max(t_both - t_fwd, 1e-3)
-    frame_s = t_bin + t_band * H / rows
-    return {"value": 1.0 / frame_s, "unit": "backward passes/s", "cores": cores, "kind": "reference",
-            "sample": f"render_backward of rows {y0}-{y0 + rows} of {H}: band {t_band:.2f}s (render+backward "
-                      f"{t_both:.2f}s - render {t_fwd:.2f}s), per frame = binning {t_bin:.2f}s + band x {H}/{rows}", "frame_seconds": frame_s}
+    t_bwd = max(t_both - t_fwd, 1e-3)
+    return {"value": 1.0 / t_bwd, "unit": "backward passes/s", "cores": cores, "kind": kind, "cpu_model": model,
+            "sample": f"whole frame of {cam.name} ({cam.width}x{cam.height}): render + render_backward {t_both:.1f} s "
+                      f"- render {t_fwd:.1f} s; {cores} threads", "frame_seconds": t_bwd,
+            "forward_seconds": t_fwd}
 
 
 def _device_view(ptr, n, dtype, dev):
@@ -601,7 +580,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference_sample(scene, cams[views[0]] if views else nx.ring_camera(0), args.cpu_budget)
+            cpu = cpu_reference_sample(scene, nx.ring_camera(0, N_VIEWS, args.width, args.height))
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {e}"}
@@ -610,7 +589,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload(args),
+            "vs_baseline": None, "dtype": DTYPE, "data": "synthetic", "config": workload(args),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic_of(dom), "peak_source": peak_src,
                          "bytes_per_launch": dom_bytes, "launch_ms": stage_ms[dom]},
@@ -728,12 +707,23 @@ def run_config4(args):
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     fbytes = frame_bytes(n, P, H, W, K, Q)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:  # one whole config-4 frame of the reference on all host cores
+            impl, kind, cores, model = cpu_impl()
+            cam0 = nx.ring_camera(args.warmup % N_VIEWS, N_VIEWS, W, H)
+            t = time_full_frames(impl, scene, [cam0])[0]
+            cpu = {"value": 1.0 / t, "unit": UNIT, "cores": cores, "kind": kind, "cpu_model": model,
+                   "sample": f"one whole {W}x{H} frame of view {args.warmup % N_VIEWS}, {n} nexels, {cores} threads",
+                   "frame_seconds": t}
+        except Exception as e:  # noqa: BLE001 — reported, never required
+            cpu = {"value": None, "sample": f"failed: {e}"}
     if rank == 0:
         line = {
             "metric": f"rendered 4K frames/sec at {n // 1000}K nexels (config 4) + % HBM roofline",
             "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
+            "dtype": DTYPE, "data": "synthetic",
             "config": {"workload": f"config 4: stump_like {n} nexels, {W}x{H}, K=2, {world} image band(s) of one "
                                    f"view per step, views along the 256-view ring", "nexels": n, "width": W,
                        "height": H, "top_k": K, "bands": nx.image_bands(H, world),
@@ -746,7 +736,7 @@ def run_config4(args):
                     "d2h_bytes_per_step": d2h * world,
                     "path": "per rank: nx_render (band) + nx_frame_download of the band, 3 frames in flight"},
             "gpu_launches": launches, "clocks": clk,
-            "cpu_baseline": None,
+            "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     for f2 in frames:

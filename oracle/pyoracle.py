@@ -170,6 +170,16 @@ def reference_lib_path() -> str | None:
 class Reference:
     """The reference's own render path (compiled in place from /root/reference)."""
 
+    def stump_like(self, n: int, **kw) -> Scene:
+        """The synthetic scene from the generator linked into this
+        library: the reference arm builds its inputs without the product library."""
+        from paper_2512_13796_b200.api import stump_like
+        return stump_like(n, lib=self.lib, **kw)
+
+    def ring_camera(self, index: int, n_views: int = 256, width: int = 1920, height: int = 1080) -> Camera:
+        from paper_2512_13796_b200.api import ring_camera
+        return ring_camera(index, n_views, width, height, lib=self.lib)
+
     def __init__(self, path: str | None = None):
         path = path or reference_lib_path()
         if not path or not os.path.exists(path):

@@ -708,9 +708,24 @@ def losses_backward(scene: Scene, fb: FrameBuffers, gt: np.ndarray, w: LossWeigh
 
 
 # ---------------------------------------------------------------- synthetic inputs
+def _synth(lib):
+    """The generator's entry points (nx_synth.cpp) on `lib`: the product library by
+    default, or the reference build in oracle/_ref, which links the same generator so
+    that bench.py's reference arm never loads libnexel_b200.so."""
+    if lib is None:
+        return _abi.load()
+    lib.nx_synth_stump_like.restype = C.c_int
+    lib.nx_synth_stump_like.argtypes = [C.c_int64, C.c_double, C.c_uint64, C.c_double, C.c_int32, C.c_double,
+                                        C.c_uint64, _abi.PD, C.POINTER(_abi.nx_settings),
+                                        C.POINTER(_abi.nx_field_desc), _abi.PD, _abi.PD, _abi.PD, _abi.PD]
+    lib.nx_synth_ring_camera.restype = C.c_int
+    lib.nx_synth_ring_camera.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_abi.nx_camera)]
+    return lib
+
+
 def stump_like(n: int, coverage: float = 1.0, seed: int = 2512, ground_radius: float = 4.0,
-               log2_table: int = 20, grid_init: float = 1e-4, field_seed: int = 2513) -> Scene:
-    lib = _abi.load()
+               log2_table: int = 20, grid_init: float = 1e-4, field_seed: int = 2513, lib=None) -> Scene:
+    lib = _synth(lib)
     s = _abi.nx_settings()
     d = _abi.nx_field_desc()
     nex = np.empty((n, 60), np.float64)
@@ -749,8 +764,8 @@ def image_bands(height: int, n: int, align: int = 16):
     return out
 
 
-def ring_camera(index: int, n_views: int = 256, width: int = 1920, height: int = 1080) -> Camera:
-    lib = _abi.load()
+def ring_camera(index: int, n_views: int = 256, width: int = 1920, height: int = 1080, lib=None) -> Camera:
+    lib = _synth(lib)
     c = _abi.nx_camera()
     st = lib.nx_synth_ring_camera(index, n_views, width, height, C.byref(c))
     if st != _abi.NX_OK:
