@@ -61,7 +61,7 @@ RENAME_FWD := -Dcollection_pass=nexel_ref_collection_pass -Dtexturing_pass=nexel
 ifneq ($(wildcard $(REF)/core/src/renderer.cpp),)
 dropin: $(DROPIN)/libnexel_dropin.so $(DROPIN)/test_oracle_dropin $(DROPIN)/test_dropin_backward \
         $(DROPIN)/test_train_dropin $(DROPIN)/test_dropin_train $(DROPIN)/bench_train $(DROPIN)/acceptance_dropin \
-        $(DROPIN)/test_renderer_dropin
+        $(DROPIN)/test_renderer_dropin $(DROPIN)/bench_render
 else
 dropin:
 	@echo "reference sources not present; using the prebuilt $(DROPIN) if any"
@@ -77,7 +77,7 @@ $(DROPIN)/ref_renderer_backward.o: $(REF)/core/src/renderer.cpp
 
 $(DROPIN)/renderer_b200.o: $(PKG)/host/renderer_b200.cpp include/nexel_b200.h
 	@mkdir -p $(DROPIN)
-	$(CXX) $(DROPIN_CXX) -c -o $@ $<
+	$(CXX) $(DROPIN_CXX) -I$(CUDA_HOME)/include -c -o $@ $<
 
 # nexel::train / mean_psnr on the device (host/trainer_b200.cpp); the reference's
 # trainer.cpp keeps config parsing and initialize_scene, its own train / mean_psnr
@@ -125,6 +125,10 @@ $(DROPIN)/test_renderer_dropin: $(REF)/tests/test_renderer.cpp tests/cxx/doctest
 
 $(DROPIN)/bench_train: tests/cxx/bench_train.cpp $(TRAIN_TEST_OBJS) $(DROPIN)/libnexel_dropin.so
 	$(CXX) $(DROPIN_CXX) -o $@ $< $(TRAIN_TEST_OBJS) -L$(DROPIN) -lnexel_dropin -Wl,-rpath,'$$ORIGIN'
+
+$(DROPIN)/bench_render: tests/cxx/bench_render.cpp $(DROPIN)/libnexel_dropin.so
+	$(CXX) $(DROPIN_CXX) -o $@ $< -L$(DROPIN) -lnexel_dropin -L$(PKG) -lnexel_b200 -Wl,-rpath,'$$ORIGIN' \
+	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
 
 $(DROPIN)/test_dropin_train: tests/cxx/test_dropin_train.cpp tests/cxx/doctest.h $(TRAIN_TEST_OBJS) $(DROPIN)/libnexel_dropin.so
 	$(CXX) $(DROPIN_CXX) -Itests/cxx -I$(REF)/tests -o $@ $< $(TRAIN_TEST_OBJS) -L$(DROPIN) -lnexel_dropin \

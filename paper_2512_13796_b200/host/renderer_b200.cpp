@@ -15,12 +15,17 @@
 // The device scene is cached per Scene content (fingerprint of every parameter).
 #include "nexel/renderer.hpp"
 
+#include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
+
+#include <cuda_runtime.h>
 
 #include "nexel/error.hpp"
 #include "../../include/nexel_b200.h"
@@ -29,7 +34,49 @@ namespace nexel {
 
 namespace {
 
+// Pinned, device-mapped staging for the downloads (grow-only): the device writes the
+// frame's buffers at link speed with the library's streaming copy, then host threads
+// widen / copy them into the caller's FrameBuffers vectors.
+struct Staging {
+    unsigned char* p = nullptr;
+    size_t cap = 0;
+    unsigned char* get(size_t bytes) {
+        if (bytes <= cap) return p;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        if (cudaHostAlloc(reinterpret_cast<void**>(&p), bytes, cudaHostAllocMapped) != cudaSuccess) {
+            cudaGetLastError();
+            fail("out-of-memory", "cannot allocate pinned staging for the frame download");
+        }
+        cap = bytes;
+        return p;
+    }
+};
+
+// f(begin, end) over [0, n) split across the host's cores (chunked, in parallel).
+template <typename F>
+void parallel_range(size_t n, F&& f) {
+    const size_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t parts = std::min<size_t>(std::min<size_t>(hw, 32), std::max<size_t>(1, n >> 16));
+    if (parts <= 1) return f(size_t(0), n);
+    std::vector<std::thread> pool;
+    const size_t step = (n + parts - 1) / parts;
+    for (size_t i = 1; i < parts; ++i)
+        pool.emplace_back([&, i] { f(std::min(n, i * step), std::min(n, (i + 1) * step)); });
+    f(size_t(0), std::min(n, step));
+    for (auto& t : pool) t.join();
+}
+
+template <typename S, typename D>
+void widen_into(const S* src, D* dst, size_t n) {
+    parallel_range(n, [&](size_t b, size_t e) {
+        for (size_t i = b; i < e; ++i) dst[i] = static_cast<D>(src[i]);
+    });
+}
+
 struct Device {
+    Staging staging;
     nx_ctx* ctx = nullptr;
     nx_scene* scene = nullptr;
     nx_frame* frame = nullptr;
@@ -61,12 +108,55 @@ uint64_t fnv(uint64_t h, const void* p, size_t n) {
     return h;
 }
 
+// Content hash of one large buffer: 16 independent 32-bit multiply-xor lanes over the
+// 4-byte words (the loop vectorises to AVX2/AVX-512 and runs at memory bandwidth), the
+// buffer split into chunks hashed on worker threads, chunk digests combined in order.
+// Every byte of the scene enters the digest; the cost is a streaming read (~10 ms for
+// the 460 MB of a 400K-nexel scene on 16 cores, vs 0.75 s for a byte-wise FNV).
+uint64_t hash_chunk(const unsigned char* b, size_t n) {
+    constexpr int kLanes = 16;
+    uint32_t acc[kLanes];
+    for (int l = 0; l < kLanes; ++l) acc[l] = 0x9e3779b9u * static_cast<uint32_t>(l + 1);
+    const size_t words = n / 4, blocks = words / kLanes;
+    for (size_t i = 0; i < blocks; ++i) {
+        uint32_t w[kLanes];
+        std::memcpy(w, b + i * kLanes * 4, sizeof w);
+        for (int l = 0; l < kLanes; ++l) acc[l] = ((acc[l] ^ w[l]) * 0x01000193u) ^ (acc[l] >> 15);
+    }
+    uint64_t h = fnv(1469598103934665603ull, acc, sizeof acc);
+    return fnv(h, b + blocks * kLanes * 4, n - blocks * kLanes * 4);
+}
+
+uint64_t hash_buffer(uint64_t h, const void* p, size_t n) {
+    const auto* b = static_cast<const unsigned char*>(p);
+    constexpr size_t kChunk = size_t(8) << 20;
+    const size_t chunks = (n + kChunk - 1) / kChunk;
+    h = fnv(h, &n, sizeof n);
+    if (chunks <= 1) {
+        const uint64_t d = hash_chunk(b, n);
+        return fnv(h, &d, sizeof d);
+    }
+    std::vector<uint64_t> dig(chunks);
+    std::atomic<size_t> next{0};
+    auto work = [&] {
+        for (size_t c; (c = next.fetch_add(1)) < chunks;)
+            dig[c] = hash_chunk(b + c * kChunk, std::min(kChunk, n - c * kChunk));
+    };
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nthreads = std::min<size_t>({chunks, hw, 32}) - 1;
+    std::vector<std::thread> pool;
+    for (size_t i = 0; i < nthreads; ++i) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+    return fnv(h, dig.data(), dig.size() * sizeof(uint64_t));
+}
+
 uint64_t fingerprint(const Scene& s) {
     uint64_t h = 1469598103934665603ull;
-    h = fnv(h, s.nexels.data(), s.nexels.size() * sizeof(Nexel));
-    h = fnv(h, s.field.grid.table.data(), s.field.grid.table.size() * sizeof(double));
+    h = hash_buffer(h, s.nexels.data(), s.nexels.size() * sizeof(Nexel));
+    h = hash_buffer(h, s.field.grid.table.data(), s.field.grid.table.size() * sizeof(double));
     for (const auto* w : {&s.field.mlp.w1, &s.field.mlp.w2, &s.field.mlp.w3})
-        h = fnv(h, w->data(), w->size() * sizeof(double));
+        h = hash_buffer(h, w->data(), w->size() * sizeof(double));
     const int shape[5] = {s.field.grid.cfg.levels, s.field.grid.cfg.log2_table, s.field.grid.cfg.features,
                           s.field.mlp.n_hidden, static_cast<int>(s.nexels.size())};
     h = fnv(h, shape, sizeof shape);
@@ -134,11 +224,6 @@ Device& bind(const Scene& scene) {
     return d;
 }
 
-template <typename T>
-void widen(const std::vector<T>& src, std::vector<double>& dst) {
-    dst.resize(src.size());
-    for (size_t i = 0; i < src.size(); ++i) dst[i] = static_cast<double>(src[i]);
-}
 
 }  // namespace
 
@@ -152,33 +237,34 @@ void validate_settings(const RenderSettings& s) {
     if (s.tile < 1) fail("bad-settings", "tile must be >= 1");
 }
 
-void collection_pass(const Scene& scene, const Camera& cam, RenderResult& out) {
-    validate_settings(scene.settings);
-    validate_camera(cam);  // the reference's own (camera.cpp:8-31): same messages
-    const int K = scene.settings.top_k;
-    out.fb.allocate(cam.width, cam.height, K);
-    out.blended_error.assign(scene.nexels.size(), 0.0);
-    Device& d = bind(scene);
+namespace {
+
+void collect(Device& d, const Scene& scene, const Camera& cam, RenderResult& out) {
+    (void)scene;
     std::lock_guard<std::mutex> lock(d.mu);
     const nx_camera c = to_nx(cam);
     check(d, nx_collection_pass(d.ctx, d.scene, &c, d.frame, nullptr));
+    FrameBuffers& fb = out.fb;
+    const size_t npix = static_cast<size_t>(fb.width) * fb.height, ns = npix * fb.top_k;
+    const size_t b_base = npix * 3 * 8, b_res = npix * 8, b_ids = ns * 4, b_dw = ns * 8;
+    unsigned char* st = d.staging.get(b_base + b_res + 2 * b_dw + b_ids);
     nx_host_frame h{};
-    h.base_f64 = out.fb.base.data();          // the fp64 base (Eq. 6) the device kept
-    h.residual_f64 = out.fb.residual.data();  // and the fp64 terminal transmittance
-    h.ids = out.fb.ids.data();
-    h.depths = out.fb.depths.data();
-    h.weights = out.fb.weights.data();
+    h.base_f64 = reinterpret_cast<double*>(st);  // the fp64 base (Eq. 6) the device kept
+    h.residual_f64 = reinterpret_cast<double*>(st + b_base);  // and the fp64 terminal transmittance
+    h.depths = reinterpret_cast<double*>(st + b_base + b_res);
+    h.weights = reinterpret_cast<double*>(st + b_base + b_res + b_dw);
+    h.ids = reinterpret_cast<int32_t*>(st + b_base + b_res + 2 * b_dw);
     check(d, nx_frame_download(d.ctx, d.frame, &h, nullptr));
     check(d, nx_ctx_synchronize(d.ctx));
+    widen_into(h.base_f64, fb.base.data(), npix * 3);
+    widen_into(h.residual_f64, fb.residual.data(), npix);
+    widen_into(h.depths, fb.depths.data(), ns);
+    widen_into(h.weights, fb.weights.data(), ns);
+    widen_into(h.ids, fb.ids.data(), ns);
     d.frame_owner = &out.fb;
 }
 
-void texturing_pass(const Scene& scene, const Camera& cam, FrameBuffers& fb) {
-    if (fb.top_k == 0) {  // renderer.cpp:208-211
-        fb.final_img = fb.base;
-        return;
-    }
-    Device& d = bind(scene);
+void texture(Device& d, const Scene& scene, const Camera& cam, FrameBuffers& fb) {
     std::lock_guard<std::mutex> lock(d.mu);
     const size_t npix = static_cast<size_t>(fb.width) * fb.height;
     if (d.frame_owner != &fb) {  // not the frame collection_pass just produced: upload it
@@ -192,20 +278,48 @@ void texturing_pass(const Scene& scene, const Camera& cam, FrameBuffers& fb) {
     }
     const nx_camera c = to_nx(cam);
     check(d, nx_texturing_pass(d.ctx, d.scene, &c, d.frame, nullptr));
-    std::vector<float> texture(npix * fb.top_k * 3), final_img(npix * 3);
+    (void)scene;
+    (void)npix;
+    const size_t ns = npix * fb.top_k;
+    unsigned char* st = d.staging.get((ns + npix) * 3 * sizeof(float));
     nx_host_frame h{};
-    h.texture = texture.data();
-    h.final_img = final_img.data();
+    h.texture = reinterpret_cast<float*>(st);
+    h.final_img = reinterpret_cast<float*>(st) + ns * 3;
     check(d, nx_frame_download(d.ctx, d.frame, &h, nullptr));
     check(d, nx_ctx_synchronize(d.ctx));
-    widen(texture, fb.texture);
-    widen(final_img, fb.final_img);
+    widen_into(h.texture, fb.texture.data(), ns * 3);
+    widen_into(h.final_img, fb.final_img.data(), npix * 3);
 }
 
-RenderResult render(const Scene& scene, const Camera& cam) {  // renderer.cpp:239-244
+}  // namespace
+
+void collection_pass(const Scene& scene, const Camera& cam, RenderResult& out) {
+    validate_settings(scene.settings);
+    validate_camera(cam);  // the reference's own (camera.cpp:8-31): same messages
+    out.fb.allocate(cam.width, cam.height, scene.settings.top_k);
+    out.blended_error.assign(scene.nexels.size(), 0.0);
+    collect(bind(scene), scene, cam, out);
+}
+
+void texturing_pass(const Scene& scene, const Camera& cam, FrameBuffers& fb) {
+    if (fb.top_k == 0) {  // renderer.cpp:208-211
+        fb.final_img = fb.base;
+        return;
+    }
+    texture(bind(scene), scene, cam, fb);
+}
+
+// renderer.cpp:239-244; the scene is bound (fingerprinted) once for both passes.
+RenderResult render(const Scene& scene, const Camera& cam) {
     RenderResult out;
-    collection_pass(scene, cam, out);
-    texturing_pass(scene, cam, out.fb);
+    validate_settings(scene.settings);
+    validate_camera(cam);
+    out.fb.allocate(cam.width, cam.height, scene.settings.top_k);
+    out.blended_error.assign(scene.nexels.size(), 0.0);
+    Device& d = bind(scene);
+    collect(d, scene, cam, out);
+    if (out.fb.top_k == 0) out.fb.final_img = out.fb.base;
+    else texture(d, scene, cam, out.fb);
     return out;
 }
 
