@@ -16,9 +16,11 @@ PKG := paper_2512_13796_b200
 SRC := $(PKG)/csrc
 CU_SRCS := $(SRC)/nx_api.cu $(SRC)/nx_preprocess.cu $(SRC)/nx_sort.cu $(SRC)/nx_composite.cu $(SRC)/nx_texture.cu \
            $(SRC)/nx_texture_tc.cu $(SRC)/nx_backward.cu $(SRC)/nx_field_backward.cu \
-           $(SRC)/nx_field_backward_tc.cu $(SRC)/nx_copy.cu $(SRC)/nx_losses.cu $(SRC)/nx_adam.cu $(SRC)/nx_density.cu
+           $(SRC)/nx_field_backward_tc.cu $(SRC)/nx_copy.cu $(SRC)/nx_losses.cu $(SRC)/nx_adam.cu $(SRC)/nx_density.cu \
+           $(SRC)/nx_fastmath.cu
 CPP_SRCS := $(SRC)/nx_synth.cpp $(SRC)/nx_nexl.cpp
-HDRS := include/nexel_b200.h $(SRC)/nx_internal.cuh $(SRC)/nx_xacc.cuh $(SRC)/nx_sort.cuh $(SRC)/nx_composite.cuh $(SRC)/nx_tc.cuh $(SRC)/nx_grid.cuh $(SRC)/nx_nexl.h
+HDRS := include/nexel_b200.h $(SRC)/nx_internal.cuh $(SRC)/nx_xacc.cuh $(SRC)/nx_sort.cuh $(SRC)/nx_composite.cuh $(SRC)/nx_tc.cuh $(SRC)/nx_grid.cuh $(SRC)/nx_nexl.h \
+        $(SRC)/nx_fastmath.cuh
 OBJDIR := build/obj
 CU_OBJS := $(patsubst $(SRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
 CPP_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJDIR)/%.o,$(CPP_SRCS))

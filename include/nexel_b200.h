@@ -392,6 +392,11 @@ int nx_debug_tile_lists(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam
 int nx_debug_pixel_hits(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam, int y0,
                         int y1, int max_hits, int32_t* hits, int32_t* counts);
 
+/* fp64 exp / log of the compositing kernels (table-driven, nx_fastmath.cuh) or CUDA's
+ * library routines, on n host arguments (allocates, synchronises; parity tests only). */
+enum { NX_FM_LOG = 0, NX_FM_EXP = 1, NX_FM_CUDA_LOG = 2, NX_FM_CUDA_EXP = 3 };
+int nx_debug_fastmath(int fn, const double* x, double* y, int64_t n);
+
 /* ---- synthetic inputs -------------------- */
 /* stump_like(N, c, seed, R_ground): fills nexels (n*60), settings and field desc;
  * table/w1/w2/w3 may be NULL to query sizes only (field desc is always filled). */

@@ -31,6 +31,7 @@
 // A per-value kernel then reads the accumulators back; activation_backward
 // (intersect.hpp:91-103) is linear in the activated gradient, so a final
 // per-primitive kernel applies it once to the sum.
+#include "nx_fastmath.cuh"
 #include "nx_composite.cuh"
 #include "nx_xacc.cuh"
 
@@ -286,10 +287,11 @@ __global__ void __launch_bounds__(kTile * kTile, 512 / (kTile * kTile)) composit
                             const double u = du / r[REC_SX];
                             const double v = dv / r[REC_SY];
                             // eval_kernel (kernel.hpp:16-30), keeping its terms for B3a
-                            const double lu = u != 0.0 ? log(fabs(u)) : 0.0, lv = v != 0.0 ? log(fabs(v)) : 0.0;
-                            const double pu = axis_power_log(u, r[REC_GX], lu), pv = axis_power_log(v, r[REC_GY], lv);
+                            // (the forward's table-driven exp / log, so both passes take the same decisions)
+                            double lu, lv;
+                            const double pu = fm_axis_power(u, r[REC_GX], lu), pv = fm_axis_power(v, r[REC_GY], lv);
                             const double p = pu + pv;
-                            const double kk = isinf(p) ? 0.0 : exp(-0.5 * p);
+                            const double kk = isinf(p) ? 0.0 : fm_exp(-0.5 * p);
                             const double al = isinf(p) ? 0.0 : r[REC_OP] * kk;
                             if (al >= kAlphaMin) {
                                 res.alpha = al;

@@ -4,23 +4,26 @@
 // One 64-thread CTA per 8x8-pixel work tile (two warps of 8x4 pixels), one thread
 // per pixel: many small CTAs per SM keep the load balanced across tiles whose hit
 // counts differ a lot. The tile's work list (ids in (depth, id) order) is walked in
-// chunks whose fp32 prefilter records are staged in shared memory (broadcast
-// reads); the fp64 records are read through L1 by the lanes that need them. Per
-// group of kSub primitives each warp
-//   A. culls in screen space (the primitive's padded pixel rect vs the warp's
-//      pixels) and prefilters in fp32 (conservative): a pair is
-//      dropped only if it provably fails the reference's t > near_eps or
-//      |u| <= ru, |v| <= rv conditions (hence alpha < 1/255);
-//   B1. pools the survivors of its 32 pixels and evaluates them with all lanes
-//      busy on the exact fp64 path — the reference's intersect() formulas
-//      (intersect.hpp:23-42) and eval_kernel (kernel.hpp:16-30) — plus the
-//      primitive's SH colour (fp32, colour only);
+// chunks whose fp32 prefilter records are staged in shared memory (broadcast reads).
+// Per chunk, each warp
+//   0. compacts the chunk to the primitives whose padded pixel rect meets its 8x4
+//      block (warp ballots, list order kept), then per group of kSub of those:
+//   S. starts asynchronous copies (cp.async) of the group's fp64 exact records and SH
+//      coefficients into its private shared staging — they land while A runs;
+//   A. tests each pixel against the primitive's pixel rect and prefilters in fp32
+//      (conservative): a pair is dropped only if it provably fails the
+//      reference's t > near_eps or |u| <= ru, |v| <= rv conditions (hence alpha < 1/255);
+//   B1. pools the survivors of its 32 pixels and evaluates them with all lanes busy on
+//      the exact fp64 path — the reference's intersect() formulas (intersect.hpp:23-42)
+//      and eval_kernel (kernel.hpp:16-30, table-driven exp / log: nx_fastmath.cuh) —
+//      plus the primitive's SH colour (fp32, colour only), all from the staging;
 //   B2. composites, per pixel and in list order, its own survivors: alpha clamp,
 //      weight, top-K insert, transmittance update and termination
 //      (renderer.cpp:144-153), all fp64.
 // Every decision is the reference's, taken in fp64 with its formulas; culling and
 // prefilter only skip provable misses, so contributor lists are bit-exact.
 #include "nx_composite.cuh"
+#include "nx_fastmath.cuh"
 
 namespace nx {
 
@@ -34,30 +37,61 @@ constexpr int kWarps = kThreads / 32;
 #ifndef NX_COMPOSITE_SUB
 #define NX_COMPOSITE_SUB 4
 #endif
-constexpr int kChunk = NX_COMPOSITE_CHUNK;       // primitives staged per round
-constexpr int kSub = NX_COMPOSITE_SUB;           // primitives pooled per B1/B2 round (<= 256 entries per warp)
+constexpr int kChunk = NX_COMPOSITE_CHUNK;       // primitives staged per round (<= 256)
+constexpr int kSub = NX_COMPOSITE_SUB;           // primitives pooled per B1/B2 round
 constexpr int kPool = 32 * kSub;
-#ifndef NX_COMPOSITE_B1_UNROLL
-#define NX_COMPOSITE_B1_UNROLL 1
-#endif
-constexpr int kB1Unroll = NX_COMPOSITE_B1_UNROLL;  // B1 evaluations interleaved per lane (measured: 1)
-constexpr int kRecPairs = REC_FIELDS / 2;        // double2 per fp64 record (10)
+constexpr int kRecPieces = REC_FIELDS * 8 / 16;  // 16-byte pieces of an fp64 record (10)
+constexpr int kShPieces = NX_SH_VALUES * 4 / 16; // 16-byte pieces of the SH coefficients (12)
 static_assert(kWorkTile == 8, "warp blocks are 8x4 pixels");
+static_assert(kChunk <= 256 && kSub <= 8, "pool entries pack (lane, group slot) in 16 bits");
 
 struct PoolEntry {  // one evaluated (pixel, primitive) pair
     double alpha;   // raw kernel alpha, < 0 for a miss
     double t;       // plane crossing
     float rgb[3];   // primitive colour along the ray
-    float pad;
+    int32_t id;
+};
+
+struct WarpStage {  // one warp's private staging
+    double rec[kSub][REC_FIELDS];    // exact records of the group's primitives
+    float sh[kSub][NX_SH_VALUES];    // and their SH coefficients
+    uint8_t sel[kChunk];             // chunk slots whose pixel rect meets the warp's block
+    uint16_t q[kPool];
+    PoolEntry res[kPool];
 };
 
 struct SmemLayout {
     float4 f[kChunk][4];
     int32_t id[kChunk];
     double dir[kThreads][3];
-    uint16_t q[kWarps][kPool];
-    PoolEntry res[kWarps][kPool];
+    WarpStage w[kWarps];
 };
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
+// Primitive SH colour (eval_sh, sh.hpp:46-57) in fp32 from staged coefficients: the
+// same operations, in the same order, as eval_sh_f32 (nx_composite.cuh).
+__device__ __forceinline__ void eval_sh_smem(const float* sh, float x, float y, float z, int degree, float* rgb) {
+    float a0 = 0.5f + 0.28209479177387814f * sh[0];
+    float a1 = 0.5f + 0.28209479177387814f * sh[1];
+    float a2 = 0.5f + 0.28209479177387814f * sh[2];
+    if (degree >= 3) {
+        float b[16];
+        sh_basis_f32(x, y, z, b);
+#pragma unroll
+        for (int k = 1; k < 16; ++k) {
+            a0 = fmaf(sh[3 * k + 0], b[k], a0);
+            a1 = fmaf(sh[3 * k + 1], b[k], a1);
+            a2 = fmaf(sh[3 * k + 2], b[k], a2);
+        }
+    }
+    rgb[0] = fmaxf(a0, 0.f);
+    rgb[1] = fmaxf(a1, 0.f);
+    rgb[2] = fmaxf(a2, 0.f);
+}
 
 template <int K, bool kDebug>
 #ifndef NX_COMPOSITE_MINB
@@ -65,6 +99,8 @@ template <int K, bool kDebug>
 #endif
 __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(const CompositeArgs a) {
     constexpr int KK = K > 0 ? K : 1;
+    constexpr bool kKeepRgb = K <= 4;  // top-K slots remember their colour (else re-evaluated at the end)
+    constexpr int KR = kKeepRgb ? KK : 1;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     SmemLayout& sm = *reinterpret_cast<SmemLayout*>(smem_raw);
 
@@ -73,9 +109,9 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
     const int list_begin = a.tile_offsets[t], list_end = a.tile_offsets[t + 1];
     const int W = a.cam.W, H = a.cam.H;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WarpStage& ws = sm.w[warp];
     const double near_eps = a.st.near_eps, alpha_max = a.st.alpha_max, min_T = a.st.min_transmittance;
     const float near_eps_f = static_cast<float>(near_eps);
-    const double o0 = a.cam.o[0], o1 = a.cam.o[1], o2 = a.cam.o[2];
 
     // warp w owns pixel rows 4w..4w+3 of the 8x8 tile
     const int px = tx * kWorkTile + (lane & 7), py = ty * kWorkTile + warp * 4 + (lane >> 3);
@@ -96,6 +132,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
     int32_t k_id[KK];
     double k_w[KK], k_t[KK];
     uint32_t k_seq[KK];
+    float k_rgb[KR][3];
 #pragma unroll
     for (int s = 0; s < KK; ++s) {
         k_id[s] = -1;
@@ -103,13 +140,14 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
         k_t[s] = 0.0;
         k_seq[s] = 0;
     }
+#pragma unroll
+    for (int s = 0; s < KR; ++s) k_rgb[s][0] = k_rgb[s][1] = k_rgb[s][2] = 0.f;
     int k_size = 0;
     uint32_t counter = 0;
     bool active = in_img;
     int dbg_n = 0;
     const bool dbg_row = kDebug && in_img && py >= a.dbg_y0 && py < a.dbg_y1;
     const int64_t dbg_q = kDebug ? (static_cast<int64_t>(py - a.dbg_y0) * W + px) : 0;
-    const double2* rec2 = reinterpret_cast<const double2*>(a.rec);
 
     for (int cb = list_begin; cb < list_end; cb += kChunk) {
         const int cn = min(kChunk, list_end - cb);
@@ -128,19 +166,47 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         if (__any_sync(0xffffffffu, active)) {
-            for (int sb = 0; sb < cn; sb += kSub) {
-                const int sn = min(kSub, cn - sb);
-                // ---- A. screen-space cull + fp32 prefilter of this group
-                uint32_t mask = 0;
-#pragma unroll 4
-                for (int b = 0; b < sn; ++b) {
-                    const float4 f3 = sm.f[sb + b][3];
+            // ---- 0. the chunk's primitives whose pixel rect meets this warp's block, in order
+            int nsel = 0;
+            for (int b0 = 0; b0 < cn; b0 += 32) {
+                const int b = b0 + lane;
+                bool ov = false;
+                if (b < cn) {
+                    const float4 f3 = sm.f[b][3];
                     const int rx = __float_as_int(f3.z), ry = __float_as_int(f3.w);
-                    const int x0 = rx & 0xffff, x1 = rx >> 16, y0 = ry & 0xffff, y1 = ry >> 16;
-                    if (x1 < wx0 || x0 > wx1 || y1 < wy0 || y0 > wy1) continue;  // warp-uniform
-                    if (active && px >= x0 && px <= x1 && py >= y0 && py <= y1 &&
-                        prefilter(&sm.f[sb + b][0], dfx, dfy, dfz, near_eps_f))
-                        mask |= 1u << b;
+                    ov = !((rx >> 16) < wx0 || (rx & 0xffff) > wx1 || (ry >> 16) < wy0 || (ry & 0xffff) > wy1);
+                }
+                const uint32_t m = __ballot_sync(0xffffffffu, ov);
+                if (ov) ws.sel[nsel + __popc(m & ((1u << lane) - 1u))] = static_cast<uint8_t>(b);
+                nsel += __popc(m);
+            }
+            __syncwarp();
+            for (int g0 = 0; g0 < nsel; g0 += kSub) {
+                const int gn = min(kSub, nsel - g0);
+                // ---- S. stage the group's exact records + SH coefficients (asynchronous)
+                for (int e = lane; e < gn * (kRecPieces + kShPieces); e += 32) {
+                    const int b = e / (kRecPieces + kShPieces), pc = e - b * (kRecPieces + kShPieces);
+                    const int64_t id = sm.id[ws.sel[g0 + b]];
+                    if (pc < kRecPieces)
+                        cp_async16(reinterpret_cast<float4*>(ws.rec[b]) + pc,
+                                   reinterpret_cast<const float4*>(a.rec + id * REC_FIELDS) + pc);
+                    else
+                        cp_async16(reinterpret_cast<float4*>(ws.sh[b]) + (pc - kRecPieces),
+                                   reinterpret_cast<const float4*>(a.sh + id * NX_SH_VALUES) + (pc - kRecPieces));
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+                // ---- A. per-pixel rect test + fp32 prefilter of the group
+                uint32_t mask = 0;
+                if (active) {
+#pragma unroll 4
+                    for (int b = 0; b < gn; ++b) {
+                        const int j = ws.sel[g0 + b];
+                        const float4 f3 = sm.f[j][3];
+                        const int rx = __float_as_int(f3.z), ry = __float_as_int(f3.w);
+                        if (px >= (rx & 0xffff) && px <= (rx >> 16) && py >= (ry & 0xffff) && py <= (ry >> 16) &&
+                            prefilter(&sm.f[j][0], dfx, dfy, dfz, near_eps_f))
+                            mask |= 1u << b;
+                    }
                 }
                 // warp-wide pool: exclusive offsets of each lane's survivors
                 const int cnt = __popc(mask);
@@ -152,66 +218,67 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                 }
                 const int off = incl - cnt;
                 const int total = __shfl_sync(0xffffffffu, incl, 31);
-                if (total == 0) continue;
+                if (total == 0) {
+                    asm volatile("cp.async.wait_all;" ::: "memory");  // the staging is reused next group
+                    __syncwarp();
+                    continue;
+                }
                 {
                     uint32_t m = mask;
                     int k = off;
                     while (m) {
                         const int b = __ffs(m) - 1;
                         m &= m - 1;
-                        sm.q[warp][k++] = static_cast<uint16_t>((lane << 8) | (sb + b));
+                        ws.q[k++] = static_cast<uint16_t>((lane << 8) | b);
                     }
                 }
+                asm volatile("cp.async.wait_all;" ::: "memory");
                 __syncwarp();
                 // ---- B1. exact fp64 evaluation of the pooled pairs, all lanes busy
-#pragma unroll kB1Unroll
                 for (int e = lane; e < total; e += 32) {
-                    const int ent = sm.q[warp][e];
-                    const int owner = ent >> 8, j = ent & 0xff;
+                    const int ent = ws.q[e];
+                    const int owner = ent >> 8, b = ent & 0xff;
                     const double* dd = sm.dir[warp * 32 + owner];
                     const double d0 = dd[0], d1 = dd[1], d2 = dd[2];
-                    const int32_t id = sm.id[j];
-                    double r[REC_FIELDS];
-#pragma unroll
-                    for (int q = 0; q < kRecPairs; ++q) {
-                        const double2 v = __ldg(rec2 + static_cast<int64_t>(id) * kRecPairs + q);
-                        r[2 * q] = v.x;
-                        r[2 * q + 1] = v.y;
-                    }
+                    const double* r = ws.rec[b];
                     PoolEntry res;
                     res.alpha = -1.0;
                     res.t = 0.0;
+                    res.id = sm.id[ws.sel[g0 + b]];
                     // intersect (intersect.hpp:23-42)
                     const double denom = d0 * r[REC_NX] + d1 * r[REC_NY] + d2 * r[REC_NZ];
                     if (fabs(denom) >= kMinNormalDot) {
                         const double tt = r[REC_NUM] / denom;
                         if (tt > near_eps) {
-                            const double e0 = (o0 + tt * d0) - r[REC_MUX];
-                            const double e1 = (o1 + tt * d1) - r[REC_MUY];
-                            const double e2 = (o2 + tt * d2) - r[REC_MUZ];
+                            const double e0 = (a.cam.o[0] + tt * d0) - r[REC_MUX];
+                            const double e1 = (a.cam.o[1] + tt * d1) - r[REC_MUY];
+                            const double e2 = (a.cam.o[2] + tt * d2) - r[REC_MUZ];
                             const double du = e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z];
                             const double dv = e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z];
                             if (fabs(du) <= r[REC_ULIM] && fabs(dv) <= r[REC_VLIM]) {
                                 const double u = du / r[REC_SX];
                                 const double v = dv / r[REC_SY];
-                                const double al = eval_kernel(u, v, r[REC_OP], r[REC_GX], r[REC_GY]);
+                                // eval_kernel (kernel.hpp:16-30) on the table-driven exp / log
+                                double lu, lv;
+                                const double p = fm_axis_power(u, r[REC_GX], lu) + fm_axis_power(v, r[REC_GY], lv);
+                                const double al = isinf(p) ? 0.0 : r[REC_OP] * fm_exp(-0.5 * p);
                                 if (al >= kAlphaMin) {
                                     res.alpha = al;
                                     res.t = tt;
-                                    eval_sh_f32(a.sh + static_cast<int64_t>(id) * NX_SH_VALUES, static_cast<float>(d0),
-                                                static_cast<float>(d1), static_cast<float>(d2), a.sh_degree, res.rgb);
+                                    eval_sh_smem(ws.sh[b], static_cast<float>(d0), static_cast<float>(d1),
+                                                 static_cast<float>(d2), a.sh_degree, res.rgb);
                                 }
                             }
                         }
                     }
-                    sm.res[warp][e] = res;
+                    ws.res[e] = res;
                 }
                 __syncwarp();
                 // ---- B2. per-pixel compositing of this lane's hits, in list order (renderer.cpp:144-153)
                 for (int k = off; k < off + cnt && active; ++k) {
-                    const PoolEntry& res = sm.res[warp][k];
+                    const PoolEntry& res = ws.res[k];
                     if (res.alpha < 0.0) continue;
-                    const int32_t id = sm.id[sm.q[warp][k] & 0xff];
+                    const int32_t id = res.id;
                     const double alpha = alpha_max < res.alpha ? alpha_max : res.alpha;
                     const double wgt = alpha * T;
                     acc[0] += wgt * res.rgb[0];
@@ -219,16 +286,9 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                     acc[2] += wgt * res.rgb[2];
                     if (K > 0) {  // TopKBuffer::insert (framebuffers.hpp:33-48)
                         const uint32_t seq = counter++;
+                        int slot = -1;
                         if (k_size < K) {
-#pragma unroll
-                            for (int s = 0; s < KK; ++s)
-                                if (s == k_size) {
-                                    k_id[s] = id;
-                                    k_w[s] = wgt;
-                                    k_t[s] = res.t;
-                                    k_seq[s] = seq;
-                                }
-                            ++k_size;
+                            slot = k_size++;
                         } else {
                             // last-ranked incumbent: smallest weight, latest arrival among ties
                             int mi = 0;
@@ -241,15 +301,21 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                                     wm = k_w[s];
                                     qm = k_seq[s];
                                 }
-#pragma unroll
-                            for (int s = 0; s < KK; ++s)
-                                if (s == mi && wgt > wm) {
-                                    k_id[s] = id;
-                                    k_w[s] = wgt;
-                                    k_t[s] = res.t;
-                                    k_seq[s] = seq;
-                                }
+                            if (wgt > wm) slot = mi;
                         }
+#pragma unroll
+                        for (int s = 0; s < KK; ++s)
+                            if (s == slot) {
+                                k_id[s] = id;
+                                k_w[s] = wgt;
+                                k_t[s] = res.t;
+                                k_seq[s] = seq;
+                                if (kKeepRgb) {
+                                    k_rgb[s % KR][0] = res.rgb[0];
+                                    k_rgb[s % KR][1] = res.rgb[1];
+                                    k_rgb[s % KR][2] = res.rgb[2];
+                                }
+                            }
                     }
                     if (kDebug && dbg_row) {
                         if (dbg_n < a.dbg_max) a.dbg_hits[dbg_q * a.dbg_max + dbg_n] = id;
@@ -292,6 +358,14 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                         const uint32_t ts = k_seq[j];
                         k_seq[j] = k_seq[j + 1];
                         k_seq[j + 1] = ts;
+                        if (kKeepRgb) {
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) {
+                                const float tc = k_rgb[j % KR][c];
+                                k_rgb[j % KR][c] = k_rgb[(j + 1) % KR][c];
+                                k_rgb[(j + 1) % KR][c] = tc;
+                            }
+                        }
                     }
                 }
             // write slots; subtract the buffered primitives' own colours (renderer.cpp:157-164)
@@ -303,7 +377,14 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                 a.fb.weights[sl] = k_w[j];
                 if (j < k_size) {
                     float col[3];
-                    eval_sh_f32(a.sh + static_cast<int64_t>(k_id[j]) * NX_SH_VALUES, dfx, dfy, dfz, a.sh_degree, col);
+                    if (kKeepRgb) {
+                        col[0] = k_rgb[j % KR][0];
+                        col[1] = k_rgb[j % KR][1];
+                        col[2] = k_rgb[j % KR][2];
+                    } else {
+                        eval_sh_f32(a.sh + static_cast<int64_t>(k_id[j]) * NX_SH_VALUES, dfx, dfy, dfz, a.sh_degree,
+                                    col);
+                    }
                     acc[0] -= k_w[j] * col[0];
                     acc[1] -= k_w[j] * col[1];
                     acc[2] -= k_w[j] * col[2];
