@@ -274,41 +274,21 @@ __global__ void __launch_bounds__(kTile * kTile, 512 / (kTile * kTile)) composit
                 res.alpha = -1.0;
                 res.t = 0.0;
                 res.flags = 0;
-                const double denom = d0 * r[REC_NX] + d1 * r[REC_NY] + d2 * r[REC_NZ];
-                if (fabs(denom) >= kMinNormalDot) {
-                    const double tt = r[REC_NUM] / denom;
-                    if (tt > near_eps) {
-                        const double e0 = (o[0] + tt * d0) - r[REC_MUX];
-                        const double e1 = (o[1] + tt * d1) - r[REC_MUY];
-                        const double e2 = (o[2] + tt * d2) - r[REC_MUZ];
-                        const double du = e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z];
-                        const double dv = e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z];
-                        if (fabs(du) <= r[REC_ULIM] && fabs(dv) <= r[REC_VLIM]) {
-                            const double u = du / r[REC_SX];
-                            const double v = dv / r[REC_SY];
-                            // eval_kernel (kernel.hpp:16-30), keeping its terms for B3a
-                            // (the forward's table-driven exp / log, so both passes take the same decisions)
-                            double lu, lv;
-                            const double pu = fm_axis_power(u, r[REC_GX], lu), pv = fm_axis_power(v, r[REC_GY], lv);
-                            const double p = pu + pv;
-                            const double kk = isinf(p) ? 0.0 : fm_exp(-0.5 * p);
-                            const double al = isinf(p) ? 0.0 : r[REC_OP] * kk;
-                            if (al >= kAlphaMin) {
-                                res.alpha = al;
-                                res.t = tt;
-                                res.pu = pu;
-                                res.pv = pv;
-                                res.lu = lu;
-                                res.lv = lv;
-                                res.k = kk;
-                                uint32_t act;
-                                eval_sh_f32(a.sh + static_cast<int64_t>(id) * NX_SH_VALUES, static_cast<float>(d0),
-                                            static_cast<float>(d1), static_cast<float>(d2), a.sh_degree, res.rgb,
-                                            &act);
-                                res.flags = act;
-                            }
-                        }
-                    }
+                // intersect + eval_kernel, keeping the kernel terms for B3a (the forward's
+                // exact_hit, so both passes take the same decisions)
+                const HitTerms h = exact_hit(r, d0, d1, d2, o[0], o[1], o[2], near_eps);
+                if (h.alpha >= 0.0) {
+                    res.alpha = h.alpha;
+                    res.t = h.t;
+                    res.pu = h.pu;
+                    res.pv = h.pv;
+                    res.lu = h.lu;
+                    res.lv = h.lv;
+                    res.k = h.k;
+                    uint32_t act;
+                    eval_sh_f32(a.sh + static_cast<int64_t>(id) * NX_SH_VALUES, static_cast<float>(d0),
+                                static_cast<float>(d1), static_cast<float>(d2), a.sh_degree, res.rgb, &act);
+                    res.flags = act;
                 }
                 sm.res[e].h = res;
             }

@@ -245,31 +245,13 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                     res.alpha = -1.0;
                     res.t = 0.0;
                     res.id = sm.id[ws.sel[g0 + b]];
-                    // intersect (intersect.hpp:23-42)
-                    const double denom = d0 * r[REC_NX] + d1 * r[REC_NY] + d2 * r[REC_NZ];
-                    if (fabs(denom) >= kMinNormalDot) {
-                        const double tt = r[REC_NUM] / denom;
-                        if (tt > near_eps) {
-                            const double e0 = (a.cam.o[0] + tt * d0) - r[REC_MUX];
-                            const double e1 = (a.cam.o[1] + tt * d1) - r[REC_MUY];
-                            const double e2 = (a.cam.o[2] + tt * d2) - r[REC_MUZ];
-                            const double du = e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z];
-                            const double dv = e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z];
-                            if (fabs(du) <= r[REC_ULIM] && fabs(dv) <= r[REC_VLIM]) {
-                                const double u = du / r[REC_SX];
-                                const double v = dv / r[REC_SY];
-                                // eval_kernel (kernel.hpp:16-30) on the table-driven exp / log
-                                double lu, lv;
-                                const double p = fm_axis_power(u, r[REC_GX], lu) + fm_axis_power(v, r[REC_GY], lv);
-                                const double al = isinf(p) ? 0.0 : r[REC_OP] * fm_exp(-0.5 * p);
-                                if (al >= kAlphaMin) {
-                                    res.alpha = al;
-                                    res.t = tt;
-                                    eval_sh_smem(ws.sh[b], static_cast<float>(d0), static_cast<float>(d1),
-                                                 static_cast<float>(d2), a.sh_degree, res.rgb);
-                                }
-                            }
-                        }
+                    // intersect (intersect.hpp:23-42) + eval_kernel (kernel.hpp:16-30)
+                    const HitTerms h = exact_hit(r, d0, d1, d2, a.cam.o[0], a.cam.o[1], a.cam.o[2], near_eps);
+                    if (h.alpha >= 0.0) {
+                        res.alpha = h.alpha;
+                        res.t = h.t;
+                        eval_sh_smem(ws.sh[b], static_cast<float>(d0), static_cast<float>(d1), static_cast<float>(d2),
+                                     a.sh_degree, res.rgb);
                     }
                     ws.res[e] = res;
                 }

@@ -116,7 +116,7 @@ NX_HD void pixel_dir(const CamD& c, double px, double py, double* dir) {
 }
 
 // ---------------------------------------------------------------- per-primitive composite record
-// AoS, 20 fp64 per primitive, staged into shared memory per chunk (broadcast reads).
+// AoS, 20 fp64 per primitive, staged into shared memory by the compositing kernels.
 enum RecField {
     REC_NUM = 0,  // dot(mu - origin, n): the per-camera numerator of t (intersect.hpp:29)
     REC_NX, REC_NY, REC_NZ,

@@ -76,3 +76,4 @@ def test_special_values_take_the_library_path():
     assert np.array_equal(np.isnan(got), np.isnan(ref))
     fin = ~np.isnan(ref)
     assert np.array_equal(got[fin], ref[fin])
+
