@@ -539,7 +539,8 @@ int texturing(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* 
     ta.stats = f->stats;
     ta.fscratch = nullptr;
     ta.ev_mid = c->profiling ? c->ev[c->ev_cur][kEvTexMid] : nullptr;  // recorded between gathers and decoder
-    if (texture_tc_supported(scene->st.top_k > 0 ? scene->field : nx_field_desc{}) && f->K > 0) {
+    if (texture_tc_supported(scene->st.top_k > 0 ? scene->field : nx_field_desc{}) && f->K > 0 &&
+        texture_tc_path() == 2) {
         NX_CUDA(c, f->tex_f.ensure(static_cast<size_t>(f->W) * f->H * f->K * 32 * sizeof(float)));
         ta.fscratch = f->tex_f.as<float>();
     }

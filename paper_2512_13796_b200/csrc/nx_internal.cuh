@@ -242,6 +242,8 @@ struct TextureArgs {
 int launch_texture(const TextureArgs& a, cudaStream_t s);  // returns NX_OK / NX_UNSUPPORTED
 // tcgen05 variant for the reference field shape (16 levels x 2 features, 64 hidden).
 bool texture_tc_supported(const nx_field_desc& fd);
+// 0: warp-specialised, 1: fused single-role, 2: split (default; needs TextureArgs::fscratch)
+int texture_tc_path();
 int launch_texture_tc(const TextureArgs& a, cudaStream_t s);
 
 // ---------------------------------------------------------------- losses_backward (nx_losses.cu)

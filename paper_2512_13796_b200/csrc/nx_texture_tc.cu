@@ -514,7 +514,347 @@ __global__ void __launch_bounds__(kTcThreads, kCtasPerSm) tex_mlp_kernel(const T
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
 
+// ---------------------------------------------------------------- warp-specialised variant
+// One persistent CTA per SM; the pass of a tile (128 rows = 128/K pixels x K slots of a
+// bw x bh pixel block) flows through three roles that run concurrently on different
+// tiles, handing buffers over with mbarriers:
+//   gather warps (16; two groups of 8, alternate tiles): per row, 8 of the 16 levels per
+//     thread (two threads per row), features -> bf16 hi/lo split -> the tile's smem A
+//     buffer (K-major), fence.proxy.async, arrive `full`;
+//   MMA warp (1 elected thread): layer 1 (A1 . W1^T), layer 2, layer 3 into the tile's
+//     64-column TMEM slot, one tcgen05.commit per layer to the slot's `done` barrier;
+//   epilogue warps (4, one TMEM lane each): D1 -> relu -> split -> A2 in the same smem
+//     buffer, arrive `a_ready`; D2 -> A3 likewise; D3 -> SH colour -> texture, Eq. 7,
+//     then free the TMEM slot and the buffer for the next tiles.
+// Step k of the MMA warp issues L3(k-2), L2(k-1), L1(k); step k of the epilogue drains
+// them in the same order, so three tiles are in the tensor-core pipeline while two more
+// are gathered. Five 32 KB A buffers + the weights: ~197 KB of shared memory; three TMEM
+// slots (192 of 256 allocated columns). No feature scratch goes through HBM.
+constexpr int kWsNB = 5;                  // smem A buffers (tiles between gather and epilogue)
+constexpr int kWsSlots = 3;               // TMEM slots (tiles in the tensor-core pipeline)
+constexpr int kWsGatherWarps = 16;
+constexpr int kWsThreads = (4 + 1 + kWsGatherWarps) * 32;  // 672
+constexpr int kWsBufBytes = 2 * kRows * kHid * 2;         // hi + lo, 64-wide bf16: 32 KB
+constexpr int kWsOffBuf = kOffAh;                          // = 36 KB (after the weights)
+constexpr int kWsOffRgb = kWsOffBuf + kWsNB * kWsBufBytes;  // float [2][128][3]
+constexpr int kWsOffBar = kWsOffRgb + 2 * kRows * 3 * 4;
+// barriers: full[NB], empty[NB], a_ready[NB], done[S], tmem_free[S]
+constexpr int kWsNumBars = 3 * kWsNB + 2 * kWsSlots;
+constexpr int kWsOffTmem = kWsOffBar + kWsNumBars * 8;
+constexpr int kWsSmem = kWsOffTmem + 16;
+static_assert(kWsSmem <= 227 * 1024, "one CTA per SM");
+static_assert(kOffW3l + kOut * kHid * 2 == kWsOffBuf, "weights precede the A buffers");
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void named_barrier_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Issues one layer from buffer offset `abuf` (hi at +0, lo at +16 KB).
+__device__ __forceinline__ void ws_issue_layer(uint8_t* smem, uint32_t dtm, int abuf, int off_bh, int off_bl, int K,
+                                               uint32_t idesc, uint32_t bar) {
+    const uint32_t ah = smem_u32(smem + abuf), al = smem_u32(smem + abuf + kRows * kHid * 2);
+    const uint32_t bh = smem_u32(smem + off_bh), bl = smem_u32(smem + off_bl);
+    const uint32_t sbo = 16 * K;
+    for (int s = 0; s < K / 16; ++s) {
+        const uint32_t o = s * 256;
+        mma_bf16(dtm, smem_desc(ah + o, 128, sbo), smem_desc(bh + o, 128, sbo), idesc, s > 0);
+        mma_bf16(dtm, smem_desc(ah + o, 128, sbo), smem_desc(bl + o, 128, sbo), idesc, 1);
+        mma_bf16(dtm, smem_desc(al + o, 128, sbo), smem_desc(bh + o, 128, sbo), idesc, 1);
+    }
+    mma_commit(bar);
+}
+
+struct WsTile {  // row -> slot of local tile k
+    int px, py, p_in;
+    bool in_tile;
+    int64_t slot;
+};
+
+__device__ __forceinline__ WsTile ws_tile(int64_t tile, int row, int K, int bw, int bh, int tiles_x, int W, int H) {
+    WsTile t;
+    const int tpx = static_cast<int>(tile % tiles_x) * bw, tpy = static_cast<int>(tile / tiles_x) * bh;
+    t.p_in = row / K;
+    const int j = row - t.p_in * K;
+    t.px = tpx + t.p_in % bw;
+    t.py = tpy + t.p_in / bw;
+    t.in_tile = t.p_in < bw * bh && t.px < W && t.py < H;
+    t.slot = t.in_tile ? (static_cast<int64_t>(t.py) * W + t.px) * K + j : 0;
+    return t;
+}
+
+__global__ void __launch_bounds__(kWsThreads, 1) texture_ws_kernel(const TextureArgs a, const TcConst cst, int bw,
+                                                                   int bh, int tiles_x, int64_t n_tiles) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t bars = smem_u32(smem + kWsOffBar);
+    auto full = [&](int b) { return bars + 8u * b; };
+    auto empty = [&](int b) { return bars + 8u * (kWsNB + b); };
+    auto a_ready = [&](int b) { return bars + 8u * (2 * kWsNB + b); };
+    auto done = [&](int sl) { return bars + 8u * (3 * kWsNB + sl); };
+    auto tmem_free = [&](int sl) { return bars + 8u * (3 * kWsNB + kWsSlots + sl); };
+
+    // ---- setup: weights -> smem (bf16 hi/lo), barriers, TMEM
+    for (int e = tid; e < kHid * kIn / 8; e += kWsThreads) {
+        const int n = e / (kIn / 8), c = e % (kIn / 8);
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(a.scene.w1 + n * kIn + c * 8 + i);
+        store_split8(smem, kOffW1h, kOffW1l, kmajor_off(n, c * 8, kIn), x);
+    }
+    for (int e = tid; e < kHid * kHid / 8; e += kWsThreads) {
+        const int n = e / (kHid / 8), c = e % (kHid / 8);
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(a.scene.w2 + n * kHid + c * 8 + i);
+        store_split8(smem, kOffW2h, kOffW2l, kmajor_off(n, c * 8, kHid), x);
+    }
+    for (int e = tid; e < kOut * kHid / 8; e += kWsThreads) {
+        const int n = e / (kHid / 8), c = e % (kHid / 8);
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(a.scene.w3 + n * kHid + c * 8 + i);
+        store_split8(smem, kOffW3h, kOffW3l, kmajor_off(n, c * 8, kHid), x);
+    }
+    if (warp == 4) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem + kWsOffTmem)),
+                     "r"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int b = 0; b < kWsNB; ++b) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(full(b)), "r"(32 * kWsGatherWarps / 2));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty(b)), "r"(kRows));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a_ready(b)), "r"(kRows));
+        }
+        for (int sl = 0; sl < kWsSlots; ++sl) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(done(sl)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tmem_free(sl)), "r"(kRows));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + kWsOffTmem);
+
+    const int K = a.fb.K, W = a.cam.W, H = a.cam.H;
+    const int64_t n_local = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    auto tile_of = [&](int64_t k) { return static_cast<int64_t>(blockIdx.x) + k * gridDim.x; };
+    auto buf_off = [&](int64_t k) { return kWsOffBuf + static_cast<int>(k % kWsNB) * kWsBufBytes; };
+    constexpr int kLoOff = kRows * kHid * 2;  // lo half of a buffer
+
+    if (warp >= 5) {
+        // ================= gather warps
+        const int gw = warp - 5, group = gw >> 3, t = (gw & 7) * 32 + lane;
+        const int row = t & (kRows - 1), half = t >> 7;
+        const uint32_t T = 1u << a.scene.field.log2_table, mask = T - 1u;
+        const float2* tab = reinterpret_cast<const float2*>(a.scene.table);
+        for (int64_t k = group; k < n_local; k += 2) {
+            const int b = static_cast<int>(k % kWsNB);
+            mbar_wait(empty(b), static_cast<uint32_t>(((k / kWsNB) & 1) ^ 1));
+            const WsTile wt = ws_tile(tile_of(k), row, K, bw, bh, tiles_x, W, H);
+            float feats[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) feats[i] = 0.f;
+            if (wt.in_tile && a.fb.ids[wt.slot] >= 0) {
+                double dir[3];
+                pixel_dir(a.cam, wt.px + 0.5, wt.py + 0.5, dir);
+                const double tq = a.fb.depths[wt.slot];
+                const double x0 = a.cam.o[0] + tq * dir[0];  // build_queries (renderer.cpp:196-198)
+                const double x1 = a.cam.o[1] + tq * dir[1];
+                const double x2 = a.cam.o[2] + tq * dir[2];
+                const float ft = static_cast<float>(a.cam.fx / tq);
+                const int l0 = half * 8;
+                const bool small =
+                    fmax(fabs(x0), fmax(fabs(x1), fabs(x2))) * cst.level_scale[kLevels - 1] < 1073741824.0;
+                if (small) {
+                    LevelFetch cur = fetch_level<true>(l0, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
+#pragma unroll
+                    for (int l = 0; l < 8; ++l) {
+                        LevelFetch nxt;
+                        if (l + 1 < 8)
+                            nxt = fetch_level<true>(l0 + l + 1, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
+                        const float2 g = interp(cur);
+                        feats[2 * l] = g.x;
+                        feats[2 * l + 1] = g.y;
+                        if (l + 1 < 8) cur = nxt;
+                    }
+                } else {
+#pragma unroll
+                    for (int l = 0; l < 8; ++l) {
+                        const float2 g = interp(
+                            fetch_level<false>(l0 + l, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight));
+                        feats[2 * l] = g.x;
+                        feats[2 * l + 1] = g.y;
+                    }
+                }
+            }
+            const int ab = buf_off(k);
+            store_split8(smem, ab, ab + kLoOff, kmajor_off(row, 16 * half, kIn), feats);
+            store_split8(smem, ab, ab + kLoOff, kmajor_off(row, 16 * half + 8, kIn), feats + 8);
+            fence_async_smem();
+            mbar_arrive(full(b));
+        }
+    } else if (warp == 4) {
+        // ================= MMA warp (one elected thread issues)
+        if (lane == 0) {
+            constexpr uint32_t kIdesc64 = idesc_bf16_f32(kRows, 64);
+            constexpr uint32_t kIdesc48 = idesc_bf16_f32(kRows, 48);
+            for (int64_t k = 0; k < n_local + 2; ++k) {
+                const int64_t k3 = k - 2, k2 = k - 1;
+                if (k3 >= 0 && k3 < n_local) {  // L3(k-2): A3 written by conv2
+                    mbar_wait(a_ready(static_cast<int>(k3 % kWsNB)), 1);
+                    tc_fence_after();
+                    ws_issue_layer(smem, tmem + 64u * static_cast<uint32_t>(k3 % kWsSlots), buf_off(k3), kOffW3h,
+                                   kOffW3l, kHid, kIdesc48, done(static_cast<int>(k3 % kWsSlots)));
+                }
+                if (k2 >= 0 && k2 < n_local) {  // L2(k-1): A2 written by conv1
+                    mbar_wait(a_ready(static_cast<int>(k2 % kWsNB)), 0);
+                    tc_fence_after();
+                    ws_issue_layer(smem, tmem + 64u * static_cast<uint32_t>(k2 % kWsSlots), buf_off(k2), kOffW2h,
+                                   kOffW2l, kHid, kIdesc64, done(static_cast<int>(k2 % kWsSlots)));
+                }
+                if (k < n_local) {  // L1(k): features gathered, TMEM slot released by final(k-3)
+                    mbar_wait(tmem_free(static_cast<int>(k % kWsSlots)), static_cast<uint32_t>(((k / kWsSlots) & 1) ^ 1));
+                    mbar_wait(full(static_cast<int>(k % kWsNB)), static_cast<uint32_t>((k / kWsNB) & 1));
+                    tc_fence_after();
+                    ws_issue_layer(smem, tmem + 64u * static_cast<uint32_t>(k % kWsSlots), buf_off(k), kOffW1h,
+                                   kOffW1l, kIn, kIdesc64, done(static_cast<int>(k % kWsSlots)));
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ================= epilogue warps (TMEM lanes 32 warp .. + 31; row = tid)
+        const int row = tid;
+        const uint32_t lane_addr = static_cast<uint32_t>(32 * warp) << 16;
+        float* srgb_base = reinterpret_cast<float*>(smem + kWsOffRgb);
+        const int ppt = bw * bh;
+        int n_queries = 0;
+        // completion parity of the i-th layer (0, 1, 2) of local tile k on its TMEM slot
+        auto done_parity = [&](int64_t k, int i) { return static_cast<uint32_t>((3 * (k / kWsSlots) + i) & 1); };
+        auto conv = [&](int64_t k, int layer) {  // D(layer) -> relu -> split -> A(layer + 1) in k's buffer
+            const int sl = static_cast<int>(k % kWsSlots);
+            mbar_wait(done(sl), done_parity(k, layer));
+            tc_fence_after();
+            const uint32_t taddr = tmem + 64u * static_cast<uint32_t>(sl) + lane_addr;
+            const int ab = buf_off(k);
+#pragma unroll
+            for (int c = 0; c < kHid / 16; ++c) {
+                float v[16];
+                tmem_ld16(taddr + 16 * c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
+                store_split8(smem, ab, ab + kLoOff, kmajor_off(row, 16 * c, kHid), v);
+                store_split8(smem, ab, ab + kLoOff, kmajor_off(row, 16 * c + 8, kHid), v + 8);
+            }
+            fence_async_smem();
+            tc_fence_before();
+            mbar_arrive(a_ready(static_cast<int>(k % kWsNB)));
+        };
+        for (int64_t k = 0; k < n_local + 2; ++k) {
+            const int64_t k3 = k - 2, k2 = k - 1;
+            if (k3 >= 0 && k3 < n_local) {  // final(k-2): D3 -> SH colour -> texture, Eq. 7
+                const int sl = static_cast<int>(k3 % kWsSlots);
+                mbar_wait(done(sl), done_parity(k3, 2));
+                tc_fence_after();
+                mbar_arrive(empty(static_cast<int>(k3 % kWsNB)));  // A3 consumed: the buffer is free
+                const int64_t tile = tile_of(k3);
+                const WsTile wt = ws_tile(tile, row, K, bw, bh, tiles_x, W, H);
+                const bool valid = wt.in_tile && a.fb.ids[wt.slot] >= 0;
+                n_queries += valid;
+                double dir[3] = {0.0, 0.0, 1.0};
+                if (wt.in_tile) pixel_dir(a.cam, wt.px + 0.5, wt.py + 0.5, dir);
+                float b[16];
+                sh_basis_f32(static_cast<float>(dir[0]), static_cast<float>(dir[1]), static_cast<float>(dir[2]), b);
+                const uint32_t taddr = tmem + 64u * static_cast<uint32_t>(sl) + lane_addr;
+                float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+#pragma unroll
+                for (int c = 0; c < kOut / 16; ++c) {
+                    float v[16];
+                    tmem_ld16(taddr + 16 * c, v);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int o = 16 * c + i, kk = o / 3;
+                        if (o % 3 == 0) c0 = fmaf(v[i], b[kk], c0);
+                        else if (o % 3 == 1) c1 = fmaf(v[i], b[kk], c1);
+                        else c2 = fmaf(v[i], b[kk], c2);
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(tmem_free(sl));  // D3 read: the slot is free for L1(k + 1)
+                float rgb[3] = {0.f, 0.f, 0.f};
+                if (valid) {
+                    rgb[0] = fmaxf(0.5f + c0, 0.f);
+                    rgb[1] = fmaxf(0.5f + c1, 0.f);
+                    rgb[2] = fmaxf(0.5f + c2, 0.f);
+                }
+                float* srgb = srgb_base + (k3 & 1) * kRows * 3;
+                srgb[row * 3 + 0] = rgb[0];
+                srgb[row * 3 + 1] = rgb[1];
+                srgb[row * 3 + 2] = rgb[2];
+                if (wt.in_tile) {
+                    a.fb.texture[wt.slot * 3 + 0] = rgb[0];
+                    a.fb.texture[wt.slot * 3 + 1] = rgb[1];
+                    a.fb.texture[wt.slot * 3 + 2] = rgb[2];
+                }
+                named_barrier_sync(1, kRows);
+                // Eq. 7: final = base + sum_j W[p,j] * texture[p,j] (renderer.cpp:219-236)
+                if (row < ppt) {
+                    const int tpx = static_cast<int>(tile % tiles_x) * bw, tpy = static_cast<int>(tile / tiles_x) * bh;
+                    const int qx = tpx + row % bw, qy = tpy + row / bw;
+                    if (qx < W && qy < H) {
+                        const int64_t pix = static_cast<int64_t>(qy) * W + qx;
+                        double acc0 = a.fb.base[pix * 3 + 0], acc1 = a.fb.base[pix * 3 + 1],
+                               acc2 = a.fb.base[pix * 3 + 2];
+                        for (int j = 0; j < K; ++j) {
+                            const int64_t q = pix * K + j;
+                            if (a.fb.ids[q] < 0) continue;
+                            const double w = a.fb.weights[q];
+                            const float* tc = srgb + (row * K + j) * 3;
+                            acc0 += w * tc[0];
+                            acc1 += w * tc[1];
+                            acc2 += w * tc[2];
+                        }
+                        a.fb.final_img[pix * 3 + 0] = static_cast<float>(acc0);
+                        a.fb.final_img[pix * 3 + 1] = static_cast<float>(acc1);
+                        a.fb.final_img[pix * 3 + 2] = static_cast<float>(acc2);
+                    }
+                }
+            }
+            if (k2 >= 0 && k2 < n_local) conv(k2, 1);  // D2 -> A3
+            if (k < n_local) conv(k, 0);               // D1 -> A2
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) n_queries += __shfl_down_sync(0xffffffffu, n_queries, o);
+        if (lane == 0 && n_queries) atomicAdd(&a.stats->queries, static_cast<unsigned long long>(n_queries));
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
 }  // namespace
+
+int texture_tc_path() {
+    // Default: split (measured fastest per frame at config 2: 2.83 ms vs 3.27 ms with the
+    // warp-specialised kernel, whose gathers have 16 warps per SM where the split
+    // gathers run at full occupancy, and whose 204 KB of shared memory keep the next
+    // frame's composite off the SM; the warp-specialised kernel moves 0.24 GB of DRAM
+    // per frame instead of ~1.2 GB).
+    static const int path = [] {
+        const char* e = getenv("NX_TEXTURE_PATH");
+        if (e && strcmp(e, "fused") == 0) return 1;
+        if (e && strcmp(e, "ws") == 0) return 0;
+        return 2;
+    }();
+    return path;
+}
 
 bool texture_tc_supported(const nx_field_desc& fd) {
     return fd.levels == kLevels && fd.features == 2 && fd.n_hidden == kHid;
@@ -522,11 +862,33 @@ bool texture_tc_supported(const nx_field_desc& fd) {
 
 int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
     const int K = a.fb.K;
-    static const bool fused = [] {
-        const char* e = getenv("NX_TEXTURE_PATH");
-        return e && strcmp(e, "fused") == 0;
-    }();
-    if (a.fscratch && !fused) {  // split: gathers at full occupancy, then the tensor-core MLP
+    // NX_TEXTURE_PATH selects the variant: "split" (default: gathers, then the MLP kernel
+    // over a feature scratch), "ws" (warp-specialised, no scratch) or "fused" (one CTA
+    // role, three per SM).
+    const int path = texture_tc_path();
+    if (path == 0 && K > 0) {
+        const int ppt = kRows / K;
+        const int bw = (kRows % K == 0 && ppt % 8 == 0) ? 8 : ppt;
+        const int bh = ppt / bw;
+        const int tiles_x = (a.cam.W + bw - 1) / bw;
+        const int64_t n_tiles = static_cast<int64_t>(tiles_x) * ((a.cam.H + bh - 1) / bh);
+        if (n_tiles == 0) return NX_OK;
+        TcConst cst;
+        double sc = a.scene.field.base_scale;
+        for (int l = 0; l < kLevels; ++l, sc *= a.scene.field.growth) {
+            cst.level_scale[l] = sc;
+            cst.inv_level_scale[l] = static_cast<float>(1.0 / sc);
+        }
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(texture_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWsSmem);
+        const int64_t grid = std::min<int64_t>(n_tiles, sms);
+        count_launch();
+        texture_ws_kernel<<<static_cast<unsigned>(grid), kWsThreads, kWsSmem, s>>>(a, cst, bw, bh, tiles_x, n_tiles);
+        return NX_OK;
+    }
+    if (a.fscratch && path == 2) {  // split: gathers at full occupancy, then the tensor-core MLP
         const int ppt = kRows / K;
         const int64_t npix = static_cast<int64_t>(a.cam.W) * a.cam.H, total = npix * K;
         if (total == 0) return NX_OK;
