@@ -20,8 +20,10 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
+#include <unordered_set>
 #include <vector>
 
 #include "nx_internal.cuh"
@@ -108,6 +110,12 @@ struct nx_ctx {
     DevBuf loss_scratch, h_gt, h_terms;          // losses_backward
     FieldBwdScratch field_bwd;                    // tensor-core field backward
     int32_t* h_pinned = nullptr;  // small readbacks
+    // Work-list key capacity of the asynchronous list builds (grow-only): sized from the
+    // first frame's count (one synchronous build) and from the counts later frames report
+    // back (asynchronously, nx_frame::h_counts); a frame that exceeded it is re-rendered
+    // when it is first read back (frame_settle).
+    int64_t key_cap = 0;
+    bool sync_lists = false;  // NX_SYNC_LISTS=1: size every build from its own count (host round trip)
     bool profiling = false;
     cudaStream_t stream2 = nullptr;  // texture passes: overlap the next frame's collection
     cudaStream_t stream3 = nullptr;  // downloads: the copy engine overlaps both
@@ -162,7 +170,33 @@ struct nx_frame {
     cudaEvent_t ev_ready = nullptr;  // collection pass of this frame done
     cudaEvent_t ev_busy = nullptr;   // last texture pass / download of this frame done
     bool busy_pending = false;
+    // asynchronous list build: the device key count comes back in h_counts (ev_counts);
+    // if it exceeded the capacity the build used, the frame is re-rendered from the
+    // scene / camera it was rendered from before anything reads it
+    int32_t* h_counts = nullptr;  // pinned [n_sorted, n_keys]
+    cudaEvent_t ev_counts = nullptr;
+    bool counts_pending = false;
+    int64_t key_cap_used = 0;
+    nx_camera cam{};
+    const nx_scene* src_scene = nullptr;
+    uint64_t src_version = 0;
+    bool textured = false;
 };
+
+namespace {
+// Scenes alive (a frame re-renders from its scene only if it still exists, unchanged).
+std::mutex g_scenes_mu;
+std::unordered_set<const nx_scene*> g_scenes;
+void scene_alive(const nx_scene* s, bool alive) {
+    std::lock_guard<std::mutex> lock(g_scenes_mu);
+    if (alive) g_scenes.insert(s);
+    else g_scenes.erase(s);
+}
+bool scene_is_alive(const nx_scene* s) {
+    std::lock_guard<std::mutex> lock(g_scenes_mu);
+    return g_scenes.count(s) > 0;
+}
+}  // namespace
 
 namespace {
 
@@ -378,7 +412,7 @@ int check_inputs(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, cudaStr
 // Builds the per-tile lists (work lists, or the reference lists when
 // reference_lists) for `cam` into frame->list_ids / frame->tile_offsets.
 int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame* f, int reference_lists,
-                cudaStream_t s, int64_t* total_keys, int work_tile = kWorkTile) {
+                cudaStream_t s, int64_t* total_keys, int work_tile = kWorkTile, bool allow_async = false) {
     const int64_t n = scene->n;
     // list geometry: reference lists per settings.tile, work lists per work_tile
     const int lt = reference_lists ? scene->st.tile : work_tile;
@@ -444,43 +478,67 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
                                            s);
     const uint32_t* sorted_ids = in_b ? c->sids_b.as<uint32_t>() : c->sids_a.as<uint32_t>();
 
-    // K3: emit (tile, id) keys in sorted order. The one host round trip of the frame:
-    // the key count sizes the key buffers.
+    // K3: emit (tile, id) keys in sorted order. The key count stays on the device: the
+    // keys go into buffers of the context's capacity (grow-only) and the count comes back
+    // asynchronously (frame_settle re-renders a frame that exceeded it). Without a
+    // capacity yet (first frame), for reference lists and for debug / backward builds,
+    // the count is read back first (one host round trip) and sizes the buffers exactly.
     record(c, kEvEmit, s);
     launch_rect_counts(sorted_ids, n, d_total, c->work_rect.as<int4>(), c->counts.as<int32_t>(), s);
     scan_exclusive(c->counts.as<int32_t>(), c->offsets.as<int32_t>(), n, d_total + 1, sc, s);
-    NX_CUDA(c, cudaMemcpyAsync(c->h_pinned, d_total, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    NX_CUDA(c, cudaStreamSynchronize(s));
-    const int64_t n_sorted = n > 0 ? c->h_pinned[0] : 0;
-    const int64_t n_keys = n_sorted > 0 ? c->h_pinned[1] : 0;
-    if (n_keys < 0) return set_err(c, NX_UNSUPPORTED, "tile-key count exceeds 2^31");
-    const int64_t nk = std::max<int64_t>(n_keys, 1);
-    NX_CUDA(c, c->tkeys_a.ensure(nk * sizeof(uint32_t)));
-    NX_CUDA(c, c->tkeys_b.ensure(nk * sizeof(uint32_t)));
-    NX_CUDA(c, c->tvals_a.ensure(nk * sizeof(uint32_t)));
-    NX_CUDA(c, c->tvals_b.ensure(nk * sizeof(uint32_t)));
-    const size_t need = radix_scratch_ints(nk) + 64;
+    const bool async = allow_async && !reference_lists && c->key_cap > 0 && !c->sync_lists && f->h_counts;
+    int64_t cap;
+    if (async) {
+        cap = c->key_cap;
+    } else {
+        NX_CUDA(c, cudaMemcpyAsync(c->h_pinned, d_total, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        NX_CUDA(c, cudaStreamSynchronize(s));
+        const int64_t n_sorted = n > 0 ? c->h_pinned[0] : 0;
+        const int64_t n_keys = n_sorted > 0 ? c->h_pinned[1] : 0;
+        if (n_keys < 0) return set_err(c, NX_UNSUPPORTED, "tile-key count exceeds 2^31");
+        cap = std::max<int64_t>(n_keys, 1);
+        if (!reference_lists) c->key_cap = std::max(c->key_cap, n_keys + n_keys / 4 + 4096);
+        *total_keys = n_keys;
+    }
+    NX_CUDA(c, c->tkeys_a.ensure(cap * sizeof(uint32_t)));
+    NX_CUDA(c, c->tkeys_b.ensure(cap * sizeof(uint32_t)));
+    NX_CUDA(c, c->tvals_a.ensure(cap * sizeof(uint32_t)));
+    NX_CUDA(c, c->tvals_b.ensure(cap * sizeof(uint32_t)));
+    const size_t need = radix_scratch_ints(cap) + 64;
     if (need * sizeof(int32_t) > c->scratch.cap) {
-        // grow scratch, preserving nothing (totals already read back)
-        NX_CUDA(c, c->scratch.ensure(need * sizeof(int32_t)));
+        // grow the scratch, keeping the device totals
+        DevBuf grown;
+        NX_CUDA(c, grown.ensure(need * sizeof(int32_t)));
+        NX_CUDA(c, cudaMemcpyAsync(grown.p, c->scratch.p, 64 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        NX_CUDA(c, cudaStreamSynchronize(s));
+        std::swap(c->scratch.p, grown.p);
+        std::swap(c->scratch.cap, grown.cap);
+        grown.release();
         d_total = c->scratch.as<int32_t>();
         sc = d_total + 64;
     }
     NX_CUDA(c, cudaMemsetAsync(c->tile_counts.as<int32_t>(), 0, (n_tiles + 1) * sizeof(int32_t), s));
-    launch_emit(sorted_ids, c->offsets.as<int32_t>(), n_sorted, n_keys, c->work_rect.as<int4>(), f->ltiles_x,
-                c->tkeys_a.as<uint32_t>(), c->tvals_a.as<uint32_t>(), c->tile_counts.as<int32_t>(), s);
+    launch_emit(sorted_ids, c->offsets.as<int32_t>(), n, d_total, cap, d_total + 1, c->work_rect.as<int4>(),
+                f->ltiles_x, c->tkeys_a.as<uint32_t>(), c->tvals_a.as<uint32_t>(), c->tile_counts.as<int32_t>(), s);
 
-    // K4: stable sort by tile.
+    // K4: stable sort by tile (over the device count, capped by the capacity).
     record(c, kEvTileSort, s);
     const int tb = std::max(bits_for(n_tiles), 1);
     const bool t_in_b = radix_sort_pairs_u32(c->tkeys_a.as<uint32_t>(), c->tvals_a.as<uint32_t>(),
-                                             c->tkeys_b.as<uint32_t>(), c->tvals_b.as<uint32_t>(), n_keys, nullptr, 0,
-                                             tb, sc, s);
+                                             c->tkeys_b.as<uint32_t>(), c->tvals_b.as<uint32_t>(), cap, d_total + 1,
+                                             0, tb, sc, s);
+    f->key_cap_used = cap;
+    f->counts_pending = false;
+    if (async) {
+        *total_keys = -1;  // on the device; f->h_counts once ev_counts completes
+        NX_CUDA(c, cudaMemcpyAsync(f->h_counts, d_total, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        NX_CUDA(c, cudaEventRecord(f->ev_counts, s));
+        f->counts_pending = true;
+    }
     // K5: tile ranges.
     scan_exclusive(c->tile_counts.as<int32_t>(), f->tile_offsets.as<int32_t>(), n_tiles + 1, nullptr, sc, s);
     f->list_ids.p = t_in_b ? c->tvals_b.p : c->tvals_a.p;  // borrowed (not owned)
     f->list_ids.cap = 0;
-    *total_keys = n_keys;
     c->lists_gen += 1;
     f->lists_gen = reference_lists ? 0 : c->lists_gen;
     c->lists_scene = scene;
@@ -492,6 +550,32 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
 }
 
 int collection(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* f, cudaStream_t s,
+               int32_t* dbg_hits, int32_t* dbg_counts, int dbg_y0, int dbg_y1, int dbg_max);
+int texturing(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* f, cudaStream_t s);
+
+// Before anything reads a frame back: if its list build ran on a capacity and the key
+// count it reported exceeds it, the capacity grows and the frame is rendered again from
+// the same scene (alive and unchanged) and camera, synchronously.
+int frame_settle(nx_ctx* c, nx_frame* f) {
+    if (!f->counts_pending) return NX_OK;
+    NX_CUDA(c, cudaEventSynchronize(f->ev_counts));
+    f->counts_pending = false;
+    const int64_t n_keys = f->h_counts[0] > 0 ? f->h_counts[1] : 0;
+    c->key_cap = std::max(c->key_cap, n_keys + n_keys / 4 + 4096);
+    if (n_keys <= f->key_cap_used) return NX_OK;
+    if (!f->src_scene || !scene_is_alive(f->src_scene) || f->src_scene->version != f->src_version)
+        return set_err(c, NX_INVALID_ARGUMENT,
+                       "frame exceeded the work-list capacity and its scene changed since: render it again");
+    const nx_camera cam = f->cam;
+    const bool tex = f->textured;
+    int st = collection(c, f->src_scene, &cam, f, c->stream, nullptr, nullptr, 0, 0, 0);
+    if (!st && tex) st = texturing(c, f->src_scene, &cam, f, c->stream);
+    if (st) return st;
+    NX_CUDA(c, cudaStreamSynchronize(c->stream));
+    return f->counts_pending ? frame_settle(c, f) : NX_OK;
+}
+
+int collection(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* f, cudaStream_t s,
                int32_t* dbg_hits, int32_t* dbg_counts, int dbg_y0, int dbg_y1, int dbg_max) {
     int st;
     if ((st = check_inputs(c, scene, cam, s))) return st;
@@ -500,7 +584,11 @@ int collection(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame*
     if ((st = frame_shape(c, f, cam->width, cam->height, scene->st.top_k, scene->st.tile))) return st;
     f->n_nexels = scene->n;
     int64_t total = 0;
-    if ((st = build_lists(c, scene, *cam, f, 0, s, &total))) return st;
+    f->cam = *cam;
+    f->src_scene = scene;
+    f->src_version = scene->version;
+    f->textured = false;
+    if ((st = build_lists(c, scene, *cam, f, 0, s, &total, kWorkTile, dbg_hits == nullptr))) return st;
     record(c, kEvComp, s);
     CompositeArgs ca;
     ca.rec = c->rec.as<double>();
@@ -539,10 +627,15 @@ int texturing(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* 
     ta.stats = f->stats;
     ta.fscratch = nullptr;
     ta.ev_mid = c->profiling ? c->ev[c->ev_cur][kEvTexMid] : nullptr;  // recorded between gathers and decoder
-    if (texture_tc_supported(scene->st.top_k > 0 ? scene->field : nx_field_desc{}) && f->K > 0 &&
-        texture_tc_path() == 2) {
-        NX_CUDA(c, f->tex_f.ensure(static_cast<size_t>(f->W) * f->H * f->K * 32 * sizeof(float)));
-        ta.fscratch = f->tex_f.as<float>();
+    if (texture_tc_supported(scene->st.top_k > 0 ? scene->field : nx_field_desc{}) && f->K > 0) {
+        const size_t bytes = texture_tc_scratch_bytes(f->W, f->H, f->K);
+        if (bytes) {
+            if (bytes > f->tex_f.cap) {  // zeroed once: padding rows of the tiles are never written
+                NX_CUDA(c, f->tex_f.ensure(bytes));
+                NX_CUDA(c, cudaMemsetAsync(f->tex_f.p, 0, f->tex_f.cap, s));
+            }
+            ta.fscratch = f->tex_f.as<float>();
+        }
     }
     const int st = launch_texture(ta, s);
     if (st) return set_err(c, st, "texture field shape not supported (n_in <= 64, n_hidden <= 128)");
@@ -551,6 +644,7 @@ int texturing(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* 
     if (c->profiling) c->ev_pending[c->ev_cur] = true;
     NX_CUDA(c, cudaEventRecord(f->ev_busy, s));
     f->busy_pending = true;
+    f->textured = true;
     NX_CUDA(c, cudaGetLastError());
     return NX_OK;
 }
@@ -599,6 +693,8 @@ int nx_ctx_create(int device, nx_ctx** out) {
     if (!c) return NX_OUT_OF_MEMORY;
     c->device = device;
     cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+    if (const char* e = std::getenv("NX_SYNC_LISTS")) c->sync_lists = std::atoi(e) != 0;
+    if (const char* e = std::getenv("NX_KEY_CAP")) c->key_cap = std::atoll(e);  // tests: start from a small capacity
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking) != cudaSuccess ||
@@ -769,6 +865,7 @@ int nx_scene_create(nx_ctx* c, const nx_settings* settings, int64_t n, const dou
         return cuda_err(c, e, "scene upload");
     }
     s->validated_version = s->version;  // validated above, on the host
+    scene_alive(s, true);
     *out = s;
     return NX_OK;
 }
@@ -846,6 +943,7 @@ int nx_scene_load_nexl(nx_ctx* c, const char* path, nx_scene** out, nx_nexl_info
     }
     if (info) *info = h.info;
     s->validated_version = s->version;  // validated above, on the host
+    scene_alive(s, true);
     *out = s;
     return NX_OK;
 }
@@ -865,6 +963,7 @@ int nx_scene_get_settings(const nx_scene* s, nx_settings* out) {
 
 void nx_scene_destroy(nx_scene* s) {
     if (!s) return;
+    scene_alive(s, false);
     cudaSetDevice(s->device);
     for (DevBuf* b : {&s->geom, &s->sh, &s->table, &s->w1, &s->w2, &s->w3, &s->geom_spare, &s->sh_spare}) b->release();
     delete s;
@@ -884,7 +983,10 @@ int nx_frame_create(nx_ctx* c, int width, int height, int top_k, nx_frame** out)
     }
     cudaMemset(f->stats, 0, sizeof(FrameStatsD));
     if (cudaEventCreateWithFlags(&f->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&f->ev_busy, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&f->ev_busy, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f->ev_counts, cudaEventDisableTiming) != cudaSuccess ||
+        cudaHostAlloc(reinterpret_cast<void**>(&f->h_counts), 2 * sizeof(int32_t), cudaHostAllocDefault) !=
+            cudaSuccess) {
         nx_frame_destroy(f);
         return set_err(c, NX_CUDA_ERROR, "frame events");
     }
@@ -907,11 +1009,17 @@ void nx_frame_destroy(nx_frame* f) {
     if (f->stats) cudaFree(f->stats);
     if (f->ev_ready) cudaEventDestroy(f->ev_ready);
     if (f->ev_busy) cudaEventDestroy(f->ev_busy);
+    if (f->ev_counts) {
+        cudaEventSynchronize(f->ev_counts);
+        cudaEventDestroy(f->ev_counts);
+    }
+    if (f->h_counts) cudaFreeHost(f->h_counts);
     delete f;
 }
 
 int nx_frame_view_get(const nx_frame* f, nx_frame_view* v) {
     if (!f || !v) return NX_INVALID_ARGUMENT;
+    if (const int st = frame_settle(f->ctx, const_cast<nx_frame*>(f))) return st;
     v->width = f->W;
     v->height = f->H;
     v->top_k = f->K;
@@ -930,6 +1038,7 @@ int nx_frame_view_get(const nx_frame* f, nx_frame_view* v) {
 int nx_frame_download(nx_ctx* c, const nx_frame* fc, const nx_host_frame* dst, void* stream) {
     if (!c || !fc || !dst) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
     nx_frame* f = const_cast<nx_frame*>(fc);  // only the frame's ordering events change
+    if (const int st = frame_settle(c, f)) return st;
     // default: the third (copy) stream, after the frame's texture pass, so that the
     // copy overlaps the next frames' passes on the other two streams
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream3;
@@ -1003,6 +1112,7 @@ int nx_frame_upload(nx_ctx* c, nx_frame* f, int width, int height, int top_k, co
 
 int nx_frame_stats_get(nx_ctx* c, const nx_frame* f, nx_frame_stats* out) {
     if (!c || !f || !out) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    if (const int st = frame_settle(c, const_cast<nx_frame*>(f))) return st;
     FrameStatsD h;
     NX_CUDA(c, cudaStreamSynchronize(c->stream));
     NX_CUDA(c, cudaDeviceSynchronize());
@@ -1061,6 +1171,7 @@ int nx_render_backward(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, n
                        const nx_grads* g, const double* err_pixel, double* blended_error, void* stream) {
     if (!c || !f || !up || !g) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
     int st;
+    if ((st = frame_settle(c, f))) return st;
     if ((st = check_inputs(c, scene, cam, pick_stream(c, stream)))) return st;
     if (!g->prims || !g->table || !g->w1 || !g->w2 || !g->w3)
         return set_err(c, NX_INVALID_ARGUMENT, "render_backward: every gradient array is required");
@@ -1250,6 +1361,7 @@ int losses_backward(nx_ctx* c, const nx_scene* scene, const nx_frame* fc, const 
     if (!c || !scene || !fc || !gt || !w || !d_final || !g || !g->prims || !g->table || !terms)
         return set_err(c, NX_INVALID_ARGUMENT, "null argument");
     nx_frame* f = const_cast<nx_frame*>(fc);
+    if (const int st = frame_settle(c, f)) return st;
     if (f->K > 0 && (!d_weights || !d_texture))
         return set_err(c, NX_INVALID_ARGUMENT, "losses_backward: d_weights / d_texture are required when top_k > 0");
     if (f->K != scene->st.top_k)
@@ -1280,6 +1392,7 @@ int nx_losses_backward(nx_ctx* c, const nx_scene* scene, const nx_frame* fc, con
 int nx_pixel_error(nx_ctx* c, const nx_frame* fc, const double* gt, double* err, void* stream) {
     if (!c || !fc || !gt || !err) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
     nx_frame* f = const_cast<nx_frame*>(fc);
+    if (const int st = frame_settle(c, f)) return st;
     cudaSetDevice(c->device);
     cudaStream_t s = pick_stream(c, stream);
     NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_ready, 0));

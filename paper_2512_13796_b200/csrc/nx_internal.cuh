@@ -207,10 +207,12 @@ void launch_rect_counts(const uint32_t* ids, int64_t n, const int32_t* n_dev, co
                         cudaStream_t s);
 
 // Emits (tile, id) for every tile of every sorted primitive's rect, in sorted
-// order (row-major tiles, renderer.cpp:106-110), and counts keys per tile.
-void launch_emit(const uint32_t* ids, const int32_t* offsets, int64_t n_sorted, int64_t n_keys,
-                 const int4* rect, int tiles_x, uint32_t* tile_keys, uint32_t* vals,
-                 int32_t* tile_counts, cudaStream_t s);
+// order (row-major tiles, renderer.cpp:106-110), and counts keys per tile. The sorted
+// count and key count are read on the device (*n_sorted_dev, *n_keys_dev); keys past
+// the capacity key_cap are not written (nor counted).
+void launch_emit(const uint32_t* ids, const int32_t* offsets, int64_t sorted_cap, const int32_t* n_sorted_dev,
+                 int64_t key_cap, const int32_t* n_keys_dev, const int4* rect, int tiles_x, uint32_t* tile_keys,
+                 uint32_t* vals, int32_t* tile_counts, cudaStream_t s);
 
 struct CompositeArgs {
     const double* rec;   // n x REC_FIELDS
@@ -242,8 +244,12 @@ struct TextureArgs {
 int launch_texture(const TextureArgs& a, cudaStream_t s);  // returns NX_OK / NX_UNSUPPORTED
 // tcgen05 variant for the reference field shape (16 levels x 2 features, 64 hidden).
 bool texture_tc_supported(const nx_field_desc& fd);
-// 0: warp-specialised, 1: fused single-role, 2: split (default; needs TextureArgs::fscratch)
+// 0: warp-specialised with gather warps, 1: fused single-role, 2: split (default:
+// gathers, then the MLP over an fp32 feature scratch), 3: bulk-fed warp-specialised
+// (gathers into pre-split operand tiles, then the MMA pipeline fed by cp.async.bulk)
 int texture_tc_path();
+// bytes of TextureArgs::fscratch the selected path needs for a W x H x K frame (0: none)
+size_t texture_tc_scratch_bytes(int W, int H, int K);
 int launch_texture_tc(const TextureArgs& a, cudaStream_t s);
 
 // ---------------------------------------------------------------- losses_backward (nx_losses.cu)

@@ -267,26 +267,32 @@ __global__ void rect_counts_kernel(const uint32_t* ids, int64_t n, const int32_t
     if (r < n) counts[r] = r < m ? rect_tiles(rect[ids[r]]) : 0;
 }
 
-// One thread per emitted key: binary search of the owning sorted primitive.
-__global__ void emit_kernel(const uint32_t* ids, const int32_t* offsets, int64_t n_sorted, int64_t n_keys,
+// One thread per emitted key: binary search of the owning sorted primitive. Counts on
+// the device; the grid covers the capacity (keys past it are dropped: the frame is
+// re-rendered with a larger capacity before it is read, nx_api.cu frame_settle).
+__global__ void emit_kernel(const uint32_t* ids, const int32_t* offsets, int64_t sorted_cap,
+                            const int32_t* n_sorted_dev, int64_t key_cap, const int32_t* n_keys_dev,
                             const int4* rect, int tiles_x, uint32_t* tile_keys, uint32_t* vals,
                             int32_t* tile_counts) {
-    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= n_keys) return;
-    int64_t lo = 0, hi = n_sorted - 1;  // last r with offsets[r] <= k
-    while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
-        if (offsets[mid] <= k) lo = mid;
-        else hi = mid - 1;
+    const int64_t n_sorted = min(sorted_cap, static_cast<int64_t>(max(*n_sorted_dev, 0)));
+    const int64_t n_keys = n_sorted > 0 ? min(key_cap, static_cast<int64_t>(max(*n_keys_dev, 0))) : 0;
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n_keys;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int64_t lo = 0, hi = n_sorted - 1;  // last r with offsets[r] <= k
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (offsets[mid] <= k) lo = mid;
+            else hi = mid - 1;
+        }
+        const uint32_t id = ids[lo];
+        const int4 rc = rect[id];
+        const int j = static_cast<int>(k - offsets[lo]);
+        const int w = rc.y - rc.x + 1;
+        const int tile = (rc.z + j / w) * tiles_x + rc.x + j % w;
+        tile_keys[k] = static_cast<uint32_t>(tile);
+        vals[k] = id;
+        atomicAdd(&tile_counts[tile], 1);
     }
-    const uint32_t id = ids[lo];
-    const int4 rc = rect[id];
-    const int j = static_cast<int>(k - offsets[lo]);
-    const int w = rc.y - rc.x + 1;
-    const int tile = (rc.z + j / w) * tiles_x + rc.x + j % w;
-    tile_keys[k] = static_cast<uint32_t>(tile);
-    vals[k] = id;
-    atomicAdd(&tile_counts[tile], 1);
 }
 
 // activate()'s checks (primitive.cpp:47-63) over every primitive of a device scene,
@@ -347,13 +353,17 @@ void launch_rect_counts(const uint32_t* ids, int64_t n, const int32_t* n_dev, co
     rect_counts_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(ids, n, n_dev, rect, counts);
 }
 
-void launch_emit(const uint32_t* ids, const int32_t* offsets, int64_t n_sorted, int64_t n_keys,
-                 const int4* rect, int tiles_x, uint32_t* tile_keys, uint32_t* vals, int32_t* tile_counts,
-                 cudaStream_t s) {
-    if (n_keys <= 0) return;
+void launch_emit(const uint32_t* ids, const int32_t* offsets, int64_t sorted_cap, const int32_t* n_sorted_dev,
+                 int64_t key_cap, const int32_t* n_keys_dev, const int4* rect, int tiles_x, uint32_t* tile_keys,
+                 uint32_t* vals, int32_t* tile_counts, cudaStream_t s) {
+    if (key_cap <= 0 || sorted_cap <= 0) return;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t grid = std::min<int64_t>((key_cap + 255) / 256, static_cast<int64_t>(sms) * 8);
     count_launch();
-    emit_kernel<<<static_cast<unsigned>((n_keys + 255) / 256), 256, 0, s>>>(ids, offsets, n_sorted, n_keys, rect,
-                                                                           tiles_x, tile_keys, vals, tile_counts);
+    emit_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(ids, offsets, sorted_cap, n_sorted_dev, key_cap,
+                                                             n_keys_dev, rect, tiles_x, tile_keys, vals, tile_counts);
 }
 
 }  // namespace nx

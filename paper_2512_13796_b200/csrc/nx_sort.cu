@@ -6,14 +6,24 @@
 //      exactly as std::sort with the reference comparator (renderer.cpp:102-105);
 //   2. the per-tile bucketing: tile-id keys over entries emitted in that order,
 //      stable => each tile's list is front to back (renderer.cpp:106-110).
-// Both are LSD radix sorts with 8-bit digits: per pass a block histogram, an
-// exclusive scan over the [digit][block] matrix, and a stable scatter that ranks
-// equal digits with warp match + a cross-warp prefix in shared memory.
+// Both are one-sweep LSD radix sorts with 8-bit digits: one upsweep launch builds the
+// global digit histograms of every pass; then one launch per pass ranks its block of
+// keys stably (warp match + cross-warp prefix in shared memory), publishes the block's
+// digit counts and finds its digit offsets by decoupled look-back over the preceding
+// blocks, then scatters. A pass whose keys all share one digit is a plain copy.
+// The exclusive scan is single-pass with the same look-back. Blocks take their index
+// from an atomic ticket (in launch order), so every block they wait on is running.
+// Counts may live on the device (n_dev): grids are sized by the host capacity and the
+// blocks past the device count leave at once (no host round trip).
 #include "nx_sort.cuh"
+
+#include <algorithm>
 
 namespace nx {
 
 namespace {
+
+constexpr uint32_t kFlagAgg = 1u, kFlagIncl = 2u;  // look-back status: aggregate / inclusive prefix
 
 __device__ __forceinline__ int warp_incl_scan(int v) {
     const int lane = threadIdx.x & 31;
@@ -25,7 +35,7 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
     return v;
 }
 
-// Block-wide exclusive scan of one int per thread (blockDim = kScanThreads).
+// Block-wide exclusive scan of one int per thread.
 __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int* total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int inc = warp_incl_scan(v);
@@ -41,28 +51,51 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int* total) {
     __syncthreads();
     const int r = s_warp[warp] + inc - v;
     if (total) *total = s_warp[32];
+    __syncthreads();
     return r;
 }
 
-__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const int32_t* in, int64_t n,
-                                                                   int32_t* block_sums) {
-    __shared__ int s_warp[33];
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
-    int v = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k)
-        if (base + k < n) v += in[base + k];
-    int total;
-    block_excl_scan(v, s_warp, &total);
-    if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
+__device__ __forceinline__ void st_status(uint64_t* p, uint32_t flag, uint32_t v) {
+    const unsigned long long w = (static_cast<unsigned long long>(flag) << 32) | v;
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
+    unsigned long long w;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+    return w;
 }
 
-// Scans up to kScanTile values in one block (exclusive), optional total.
-__global__ void __launch_bounds__(kScanThreads) scan_single_kernel(const int32_t* in, int32_t* out,
-                                                                   int64_t n, int32_t* total_out,
-                                                                   const int32_t* block_offsets) {
+// Exclusive prefix of `agg` over the blocks before `b` by decoupled look-back on
+// status[0..b) (stride `stride` between consecutive blocks' words). One thread.
+__device__ __forceinline__ uint32_t look_back(const uint64_t* status, int64_t stride, int b) {
+    uint32_t run = 0;
+    for (int p = b - 1; p >= 0;) {
+        const uint64_t w = ld_status(status + p * stride);
+        const uint32_t flag = static_cast<uint32_t>(w >> 32);
+        if (flag == 0) continue;  // predecessor not published yet (it is running: ticket order)
+        run += static_cast<uint32_t>(w);
+        if (flag == kFlagIncl) break;
+        --p;
+    }
+    return run;
+}
+
+// n = device count (capped by the host capacity n_cap) when n_dev != nullptr.
+__device__ __forceinline__ int64_t dev_count(int64_t n_cap, const int32_t* n_dev) {
+    return n_dev ? min(n_cap, static_cast<int64_t>(max(*n_dev, 0))) : n_cap;
+}
+
+// ---------------------------------------------------------------- single-pass scan
+// scratch: [0] ticket, [2..] status words (64-bit) per block
+__global__ void __launch_bounds__(kScanThreads) scan_onepass_kernel(const int32_t* in, int32_t* out, int64_t n,
+                                                                    int32_t* total_out, int32_t* scratch) {
     __shared__ int s_warp[33];
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+    __shared__ int s_block, s_prefix;
+    uint64_t* status = reinterpret_cast<uint64_t*>(scratch + 2);
+    if (threadIdx.x == 0) s_block = atomicAdd(scratch, 1);
+    __syncthreads();
+    const int b = s_block;
+    const int64_t base = static_cast<int64_t>(b) * kScanTile + threadIdx.x * kScanItems;
     int vals[kScanItems];
     int v = 0;
 #pragma unroll
@@ -72,142 +105,171 @@ __global__ void __launch_bounds__(kScanThreads) scan_single_kernel(const int32_t
     }
     int total;
     int run = block_excl_scan(v, s_warp, &total);
-    if (block_offsets) run += block_offsets[blockIdx.x];
+    if (threadIdx.x == 0) {
+        if (b == 0) {
+            st_status(status, kFlagIncl, static_cast<uint32_t>(total));
+            s_prefix = 0;
+        } else {
+            st_status(status + b, kFlagAgg, static_cast<uint32_t>(total));
+            const uint32_t pre = look_back(status, 1, b);
+            st_status(status + b, kFlagIncl, pre + static_cast<uint32_t>(total));
+            s_prefix = static_cast<int>(pre);
+        }
+    }
+    __syncthreads();
+    run += s_prefix;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         if (base + k < n) out[base + k] = run;
         run += vals[k];
     }
-    if (total_out && threadIdx.x == 0 && !block_offsets) *total_out = total;
-    if (total_out && block_offsets && blockIdx.x == gridDim.x - 1 && threadIdx.x == kScanThreads - 1)
-        *total_out = run;
+    if (total_out && b == gridDim.x - 1 && threadIdx.x == kScanThreads - 1) *total_out = run;
 }
 
-// One block scans n <= kScanLoopMax values in rounds of kScanTile with a carry
-// (one launch instead of three for the radix histogram matrices).
-__global__ void __launch_bounds__(kScanThreads) scan_loop_kernel(const int32_t* in, int32_t* out, int64_t n,
-                                                                 int32_t* total_out) {
-    __shared__ int s_warp[33];
-    int carry = 0;
-    for (int64_t round = 0; round * kScanTile < n; ++round) {
-        const int64_t base = round * kScanTile + threadIdx.x * kScanItems;
-        int vals[kScanItems];
-        int v = 0;
-#pragma unroll
-        for (int k = 0; k < kScanItems; ++k) {
-            vals[k] = base + k < n ? in[base + k] : 0;
-            v += vals[k];
-        }
-        int total;
-        int run = block_excl_scan(v, s_warp, &total) + carry;
-#pragma unroll
-        for (int k = 0; k < kScanItems; ++k) {
-            if (base + k < n) out[base + k] = run;
-            run += vals[k];
-        }
-        carry += total;
-        __syncthreads();
-    }
-    if (total_out && threadIdx.x == 0) *total_out = carry;
-}
-
-// n = device count (capped by the host capacity n_cap) when n_dev != nullptr.
-__device__ __forceinline__ int64_t dev_count(int64_t n_cap, const int32_t* n_dev) {
-    return n_dev ? min(n_cap, static_cast<int64_t>(*n_dev)) : n_cap;
-}
+// ---------------------------------------------------------------- one-sweep radix sort
+// scratch layout (int32 units): [0..16) tickets per pass, [16..16+256*8) global digit
+// histograms of up to 8 passes, then status words: pass p, block b, digit d at
+// status[(p * n_blocks + b) * 256 + d].
+constexpr int kMaxPasses = 8;
+constexpr int kHistOff = 16;
+constexpr int kStatusOff = kHistOff + kMaxPasses * kRadixBuckets;  // even: 64-bit aligned
+constexpr int kRadixItems = kRadixTile / kRadixThreads;            // per thread (4)
 
 template <typename K>
-__global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(const K* keys, int64_t n_cap,
-                                                                   const int32_t* n_dev, int shift,
-                                                                   int32_t* hist, int n_blocks) {
-    __shared__ int s_hist[kRadixBuckets];
+__global__ void __launch_bounds__(kRadixThreads) radix_upsweep_kernel(const K* keys, int64_t n_cap,
+                                                                      const int32_t* n_dev, int begin_bit,
+                                                                      int passes, int32_t* hist) {
+    __shared__ int s_hist[kMaxPasses][kRadixBuckets];
     const int64_t n = dev_count(n_cap, n_dev);
-    s_hist[threadIdx.x] = 0;
+    for (int p = 0; p < passes; ++p) s_hist[p][threadIdx.x] = 0;
     __syncthreads();
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * kRadixTile;
-    for (int i = threadIdx.x; i < kRadixTile; i += kRadixThreads) {
-        const int64_t g = base + i;
-        if (g < n) atomicAdd(&s_hist[static_cast<int>((keys[g] >> shift) & (kRadixBuckets - 1))], 1);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const K k = keys[i];
+        for (int p = 0; p < passes; ++p)
+            atomicAdd(&s_hist[p][static_cast<int>((k >> (begin_bit + p * kRadixBits)) & (kRadixBuckets - 1))], 1);
     }
     __syncthreads();
-    hist[static_cast<int64_t>(threadIdx.x) * n_blocks + blockIdx.x] = s_hist[threadIdx.x];
+    for (int p = 0; p < passes; ++p)
+        if (s_hist[p][threadIdx.x]) atomicAdd(&hist[p * kRadixBuckets + threadIdx.x], s_hist[p][threadIdx.x]);
 }
 
 template <typename K>
-__global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(const K* __restrict__ keys_in,
-                                                                      const uint32_t* __restrict__ vals_in,
-                                                                      K* __restrict__ keys_out,
-                                                                      uint32_t* __restrict__ vals_out,
-                                                                      int64_t n_cap,
-                                                                      const int32_t* __restrict__ n_dev,
-                                                                      int shift,
-                                                                      const int32_t* __restrict__ offsets,
-                                                                      int n_blocks) {
+__global__ void __launch_bounds__(kRadixThreads) radix_pass_kernel(const K* __restrict__ keys_in,
+                                                                   const uint32_t* __restrict__ vals_in,
+                                                                   K* __restrict__ keys_out,
+                                                                   uint32_t* __restrict__ vals_out, int64_t n_cap,
+                                                                   const int32_t* __restrict__ n_dev, int shift,
+                                                                   int pass, int n_blocks, int32_t* scratch) {
     constexpr int kWarps = kRadixThreads / 32;
-    __shared__ int s_base[kRadixBuckets];
     __shared__ int s_cnt[kWarps][kRadixBuckets];
-    const int64_t n = dev_count(n_cap, n_dev);
-    if (static_cast<int64_t>(blockIdx.x) * kRadixTile >= n) return;
+    __shared__ int s_local[kRadixBuckets];  // block-local running count per digit
+    __shared__ int s_glob[kRadixBuckets];   // global base of each digit for this block
+    __shared__ int s_warp[33];
+    __shared__ int s_block, s_trivial;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    s_base[tid] = offsets[static_cast<int64_t>(tid) * n_blocks + blockIdx.x];
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * kRadixTile;
+    const int64_t n = dev_count(n_cap, n_dev);
+    if (tid == 0) s_block = atomicAdd(scratch + pass, 1);
+    const int hcount = scratch[kHistOff + pass * kRadixBuckets + tid];
+    if (tid == 0) s_trivial = 0;
+    __syncthreads();
+    if (hcount == n) s_trivial = 1;  // every key has this digit: the pass is a copy
+    const int b = s_block;
+    const int64_t base = static_cast<int64_t>(b) * kRadixTile;
+    __syncthreads();
+    if (base >= n) return;
+    if (s_trivial) {
+        for (int i = tid; i < kRadixTile; i += kRadixThreads)
+            if (base + i < n) {
+                keys_out[base + i] = keys_in[base + i];
+                vals_out[base + i] = vals_in[base + i];
+            }
+        return;
+    }
+    // exclusive scan of the pass's global histogram: the digit's start in the output
+    const int gstart = block_excl_scan(hcount, s_warp, nullptr);
+    s_local[tid] = 0;
+    __syncthreads();
     const unsigned lt_mask = (1u << lane) - 1u;
-    for (int round = 0; round < kRadixTile / kRadixThreads; ++round) {
-        const int64_t i = base + static_cast<int64_t>(round) * kRadixThreads + tid;
-        if (base + static_cast<int64_t>(round) * kRadixThreads >= n) break;  // uniform
+    K key[kRadixItems];
+    uint32_t val[kRadixItems];
+    int loc[kRadixItems];
+    unsigned dig[kRadixItems];
+#pragma unroll
+    for (int r = 0; r < kRadixItems; ++r) {
+        const int64_t i = base + static_cast<int64_t>(r) * kRadixThreads + tid;
         const bool valid = i < n;
-        K k = 0;
-        uint32_t v = 0;
-        unsigned d = 0xffffffffu;
-        if (valid) {
-            k = keys_in[i];
-            v = vals_in[i];
-            d = static_cast<unsigned>((k >> shift) & (kRadixBuckets - 1));
-        }
+        key[r] = valid ? keys_in[i] : K(0);
+        val[r] = valid ? vals_in[i] : 0u;
+        dig[r] = valid ? static_cast<unsigned>((key[r] >> shift) & (kRadixBuckets - 1)) : 0xffffffffu;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) s_cnt[w][tid] = 0;
         __syncthreads();
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const unsigned peers = __match_any_sync(0xffffffffu, dig[r]);
         const int rank = __popc(peers & lt_mask);
-        if (valid && rank == 0) s_cnt[warp][d] = __popc(peers);
+        if (valid && rank == 0) s_cnt[warp][dig[r]] = __popc(peers);
         __syncthreads();
         int run = 0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
             const int c = s_cnt[w][tid];
-            s_cnt[w][tid] = s_base[tid] + run;
+            s_cnt[w][tid] = s_local[tid] + run;
             run += c;
         }
-        s_base[tid] += run;
+        s_local[tid] += run;
         __syncthreads();
-        if (valid) {
-            const int pos = s_cnt[warp][d] + rank;
-            keys_out[pos] = k;
-            vals_out[pos] = v;
-        }
+        loc[r] = valid ? s_cnt[warp][dig[r]] + rank : 0;
         __syncthreads();
+    }
+    // publish this block's digit counts, look back for the preceding blocks' totals
+    uint64_t* status = reinterpret_cast<uint64_t*>(scratch + kStatusOff) +
+                       static_cast<int64_t>(pass) * n_blocks * kRadixBuckets;
+    const uint32_t mine = static_cast<uint32_t>(s_local[tid]);
+    if (b == 0) {
+        st_status(status + tid, kFlagIncl, mine);
+        s_glob[tid] = gstart;
+    } else {
+        st_status(status + static_cast<int64_t>(b) * kRadixBuckets + tid, kFlagAgg, mine);
+        const uint32_t pre = look_back(status + tid, kRadixBuckets, b);
+        st_status(status + static_cast<int64_t>(b) * kRadixBuckets + tid, kFlagIncl, pre + mine);
+        s_glob[tid] = gstart + static_cast<int>(pre);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kRadixItems; ++r) {
+        if (dig[r] == 0xffffffffu) continue;
+        const int pos = s_glob[dig[r]] + loc[r];
+        keys_out[pos] = key[r];
+        vals_out[pos] = val[r];
     }
 }
 
 template <typename K>
-bool radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n,
-                     const int32_t* n_dev, int begin_bit, int end_bit, int32_t* scratch, cudaStream_t stream) {
+bool radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n, const int32_t* n_dev,
+                     int begin_bit, int end_bit, int32_t* scratch, cudaStream_t stream) {
     if (n <= 1) return false;
     const int n_blocks = static_cast<int>((n + kRadixTile - 1) / kRadixTile);
-    const int64_t hist_n = static_cast<int64_t>(n_blocks) * kRadixBuckets;
-    int32_t* hist = scratch;
-    int32_t* scan_scratch = scratch + hist_n;
+    const int passes = (end_bit - begin_bit + kRadixBits - 1) / kRadixBits;
+    if (passes <= 0) return false;
+    // tickets + histograms + status words start at zero
+    cudaMemsetAsync(scratch, 0,
+                    (kStatusOff + static_cast<size_t>(2) * passes * n_blocks * kRadixBuckets) * sizeof(int32_t),
+                    stream);
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int up_grid = static_cast<int>(std::min<int64_t>((n + kRadixThreads - 1) / kRadixThreads, 4 * sms));
+    count_launch(1 + passes);
+    radix_upsweep_kernel<K><<<up_grid, kRadixThreads, 0, stream>>>(keys, n, n_dev, begin_bit, passes,
+                                                                     scratch + kHistOff);
     bool in_alt = false;
-    for (int bit = begin_bit; bit < end_bit; bit += kRadixBits) {
+    for (int p = 0; p < passes; ++p) {
         K* ki = in_alt ? keys_alt : keys;
         uint32_t* vi = in_alt ? vals_alt : vals;
         K* ko = in_alt ? keys : keys_alt;
         uint32_t* vo = in_alt ? vals : vals_alt;
-        count_launch(2);
-        radix_hist_kernel<K><<<n_blocks, kRadixThreads, 0, stream>>>(ki, n, n_dev, bit, hist, n_blocks);
-        scan_exclusive(hist, hist, hist_n, nullptr, scan_scratch, stream);
-        radix_scatter_kernel<K><<<n_blocks, kRadixThreads, 0, stream>>>(ki, vi, ko, vo, n, n_dev, bit, hist,
-                                                                        n_blocks);
+        radix_pass_kernel<K><<<n_blocks, kRadixThreads, 0, stream>>>(ki, vi, ko, vo, n, n_dev,
+                                                                     begin_bit + p * kRadixBits, p, n_blocks, scratch);
         in_alt = !in_alt;
     }
     return in_alt;
@@ -217,7 +279,7 @@ bool radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, i
 
 size_t scan_scratch_ints(int64_t n) {
     const int64_t n_blocks = (n + kScanTile - 1) / kScanTile;
-    return static_cast<size_t>(n_blocks) + (n_blocks > 1 ? scan_scratch_ints(n_blocks) : 0) + 8;
+    return static_cast<size_t>(2 + 2 * n_blocks + 8);
 }
 
 void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int32_t* total, int32_t* scratch,
@@ -227,28 +289,14 @@ void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int32_t* total, 
         return;
     }
     const int64_t n_blocks = (n + kScanTile - 1) / kScanTile;
-    if (n_blocks == 1) {
-        count_launch(1);
-        scan_single_kernel<<<1, kScanThreads, 0, stream>>>(in, out, n, total, nullptr);
-        return;
-    }
-    if (n <= kScanLoopMax) {
-        count_launch(1);
-        scan_loop_kernel<<<1, kScanThreads, 0, stream>>>(in, out, n, total);
-        return;
-    }
-    // reduce per block, scan the block sums (recursively), then scan each block with its offset
-    count_launch(2);
-    scan_reduce_kernel<<<static_cast<unsigned>(n_blocks), kScanThreads, 0, stream>>>(in, n, scratch);
-    scan_exclusive(scratch, scratch, n_blocks, nullptr, scratch + n_blocks, stream);
-    scan_single_kernel<<<static_cast<unsigned>(n_blocks), kScanThreads, 0, stream>>>(in, out, n, total,
-                                                                                    scratch);
+    cudaMemsetAsync(scratch, 0, (2 + 2 * n_blocks) * sizeof(int32_t), stream);
+    count_launch(1);
+    scan_onepass_kernel<<<static_cast<unsigned>(n_blocks), kScanThreads, 0, stream>>>(in, out, n, total, scratch);
 }
 
 size_t radix_scratch_ints(int64_t n) {
     const int64_t n_blocks = (n + kRadixTile - 1) / kRadixTile;
-    const int64_t hist_n = n_blocks * kRadixBuckets;
-    return static_cast<size_t>(hist_n) + scan_scratch_ints(hist_n);
+    return static_cast<size_t>(kStatusOff + 2 * kMaxPasses * n_blocks * kRadixBuckets + 8);
 }
 
 bool radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,

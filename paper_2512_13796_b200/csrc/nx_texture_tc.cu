@@ -530,19 +530,32 @@ __global__ void __launch_bounds__(kTcThreads, kCtasPerSm) tex_mlp_kernel(const T
 // them in the same order, so three tiles are in the tensor-core pipeline while two more
 // are gathered. Five 32 KB A buffers + the weights: ~197 KB of shared memory; three TMEM
 // slots (192 of 256 allocated columns). No feature scratch goes through HBM.
-constexpr int kWsNB = 5;                  // smem A buffers (tiles between gather and epilogue)
-constexpr int kWsSlots = 3;               // TMEM slots (tiles in the tensor-core pipeline)
-constexpr int kWsGatherWarps = 16;
-constexpr int kWsThreads = (4 + 1 + kWsGatherWarps) * 32;  // 672
-constexpr int kWsBufBytes = 2 * kRows * kHid * 2;         // hi + lo, 64-wide bf16: 32 KB
-constexpr int kWsOffBuf = kOffAh;                          // = 36 KB (after the weights)
-constexpr int kWsOffRgb = kWsOffBuf + kWsNB * kWsBufBytes;  // float [2][128][3]
-constexpr int kWsOffBar = kWsOffRgb + 2 * kRows * 3 * 4;
-// barriers: full[NB], empty[NB], a_ready[NB], done[S], tmem_free[S]
-constexpr int kWsNumBars = 3 * kWsNB + 2 * kWsSlots;
-constexpr int kWsOffTmem = kWsOffBar + kWsNumBars * 8;
-constexpr int kWsSmem = kWsOffTmem + 16;
-static_assert(kWsSmem <= 227 * 1024, "one CTA per SM");
+// Layout per producer mode: kGather = the gather warps above; kBulk = one producer warp
+// that copies tiles of pre-gathered, pre-split features (tex_features_img_kernel) with
+// the bulk-copy engine (cp.async.bulk, mbarrier transaction counts).
+enum WsMode { kGather = 0, kBulk = 1 };
+template <int kMode>
+struct WsCfg {
+    static constexpr int NB = kMode == kGather ? 5 : 4;  // smem A buffers (tiles between producer and epilogue)
+    static constexpr int kProducerWarps = kMode == kGather ? 16 : 1;
+#ifndef NX_WS_EPI_GROUPS
+#define NX_WS_EPI_GROUPS 4
+#endif
+    static constexpr int kEpiGroups = kMode == kGather ? 1 : NX_WS_EPI_GROUPS;  // 4-warp epilogue groups
+    static constexpr int kSlots = kMode == kGather ? 3 : 2 * NX_WS_EPI_GROUPS;   // TMEM slots of 64 columns
+    static constexpr int kTmemCols = kSlots * 64 <= 256 ? 256 : 512;
+    static constexpr int kMmaWarp = 4 * kEpiGroups;
+    static constexpr int kThreads = (kMmaWarp + 1 + kProducerWarps) * 32;  // 672 / 352
+    static constexpr int kOffRgb = kOffAh + NB * 2 * kRows * kHid * 2;  // after the weights + A buffers
+    static constexpr int kOffBar = kOffRgb + kEpiGroups * 2 * kRows * 3 * 4;
+    static constexpr int kNumBars = 3 * NB + 2 * kSlots;  // full, empty, a_ready [NB]; done, tmem_free [slots]
+    static constexpr int kOffTmem = kOffBar + kNumBars * 8;
+    static constexpr int kSmem = kOffTmem + 16;
+    static_assert(kSmem <= 227 * 1024, "one CTA per SM");
+};
+constexpr int kWsBufBytes = 2 * kRows * kHid * 2;  // hi + lo, 64-wide bf16: 32 KB
+constexpr int kWsOffBuf = kOffAh;                  // = 36 KB (after the weights)
+constexpr int kImgBytes = 2 * kRows * kIn * 2;     // a tile's pre-split features: hi 8 KB + lo 8 KB
 static_assert(kOffW3l + kOut * kHid * 2 == kWsOffBuf, "weights precede the A buffers");
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
@@ -585,11 +598,20 @@ __device__ __forceinline__ WsTile ws_tile(int64_t tile, int row, int K, int bw, 
     return t;
 }
 
-__global__ void __launch_bounds__(kWsThreads, 1) texture_ws_kernel(const TextureArgs a, const TcConst cst, int bw,
-                                                                   int bh, int tiles_x, int64_t n_tiles) {
+template <int kMode>
+__global__ void __launch_bounds__(WsCfg<kMode>::kThreads, 1)
+    texture_ws_kernel(const TextureArgs a, const TcConst cst, int bw, int bh, int tiles_x, int64_t n_tiles) {
+    using Cfg = WsCfg<kMode>;
+    constexpr int kWsNB = Cfg::NB;
+    constexpr int kWsThreads = Cfg::kThreads;
+    constexpr int kWsOffRgb = Cfg::kOffRgb;
+    constexpr int kWsOffTmem = Cfg::kOffTmem;
+    constexpr int kWsSlots = Cfg::kSlots;
+    constexpr int kG = Cfg::kEpiGroups;
+    constexpr int kMmaWarp = Cfg::kMmaWarp;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t bars = smem_u32(smem + kWsOffBar);
+    const uint32_t bars = smem_u32(smem + Cfg::kOffBar);
     auto full = [&](int b) { return bars + 8u * b; };
     auto empty = [&](int b) { return bars + 8u * (kWsNB + b); };
     auto a_ready = [&](int b) { return bars + 8u * (2 * kWsNB + b); };
@@ -618,14 +640,15 @@ __global__ void __launch_bounds__(kWsThreads, 1) texture_ws_kernel(const Texture
         for (int i = 0; i < 8; ++i) x[i] = __ldg(a.scene.w3 + n * kHid + c * 8 + i);
         store_split8(smem, kOffW3h, kOffW3l, kmajor_off(n, c * 8, kHid), x);
     }
-    if (warp == 4) {
+    if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem + kWsOffTmem)),
-                     "r"(256));
+                     "r"(Cfg::kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
         for (int b = 0; b < kWsNB; ++b) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(full(b)), "r"(32 * kWsGatherWarps / 2));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(full(b)),
+                         "r"(kMode == kGather ? 32 * Cfg::kProducerWarps / 2 : 1));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty(b)), "r"(kRows));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a_ready(b)), "r"(kRows));
         }
@@ -647,9 +670,32 @@ __global__ void __launch_bounds__(kWsThreads, 1) texture_ws_kernel(const Texture
     auto buf_off = [&](int64_t k) { return kWsOffBuf + static_cast<int>(k % kWsNB) * kWsBufBytes; };
     constexpr int kLoOff = kRows * kHid * 2;  // lo half of a buffer
 
-    if (warp >= 5) {
+    if (kMode == kBulk && warp == kMmaWarp + 1) {
+        // ================= producer warp: bulk copies of the pre-split feature tiles
+        if (lane == 0) {
+            const uint8_t* img = reinterpret_cast<const uint8_t*>(a.fscratch);
+            for (int64_t k = 0; k < n_local; ++k) {
+                const int b = static_cast<int>(k % kWsNB);
+                mbar_wait(empty(b), static_cast<uint32_t>(((k / kWsNB) & 1) ^ 1));
+                const uint8_t* src = img + tile_of(k) * kImgBytes;
+                const uint32_t dst = smem_u32(smem + buf_off(k));
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full(b)), "r"(kImgBytes)
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                    "l"(src), "r"(kImgBytes / 2), "r"(full(b))
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        dst + kLoOff),
+                    "l"(src + kImgBytes / 2), "r"(kImgBytes / 2), "r"(full(b))
+                    : "memory");
+            }
+        }
+        __syncwarp();
+    } else if (kMode == kGather && warp > kMmaWarp) {
         // ================= gather warps
-        const int gw = warp - 5, group = gw >> 3, t = (gw & 7) * 32 + lane;
+        const int gw = warp - kMmaWarp - 1, group = gw >> 3, t = (gw & 7) * 32 + lane;
         const int row = t & (kRows - 1), half = t >> 7;
         const uint32_t T = 1u << a.scene.field.log2_table, mask = T - 1u;
         const float2* tab = reinterpret_cast<const float2*>(a.scene.table);
@@ -699,7 +745,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) texture_ws_kernel(const Texture
             fence_async_smem();
             mbar_arrive(full(b));
         }
-    } else if (warp == 4) {
+    } else if (warp == kMmaWarp) {
         // ================= MMA warp (one elected thread issues)
         if (lane == 0) {
             constexpr uint32_t kIdesc64 = idesc_bf16_f32(kRows, 64);
@@ -729,10 +775,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) texture_ws_kernel(const Texture
         }
         __syncwarp();
     } else {
-        // ================= epilogue warps (TMEM lanes 32 warp .. + 31; row = tid)
-        const int row = tid;
-        const uint32_t lane_addr = static_cast<uint32_t>(32 * warp) << 16;
-        float* srgb_base = reinterpret_cast<float*>(smem + kWsOffRgb);
+        // ================= epilogue warps (group g = warp / 4 takes the tiles k = g mod kG;
+        // TMEM lanes 32 (warp % 4) .. + 31; row = tid % 128)
+        const int g = warp >> 2;
+        const int row = tid & (kRows - 1);
+        const uint32_t lane_addr = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+        float* srgb_base = reinterpret_cast<float*>(smem + kWsOffRgb) + g * 2 * kRows * 3;
         const int ppt = bw * bh;
         int n_queries = 0;
         // completion parity of the i-th layer (0, 1, 2) of local tile k on its TMEM slot
@@ -758,7 +806,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) texture_ws_kernel(const Texture
         };
         for (int64_t k = 0; k < n_local + 2; ++k) {
             const int64_t k3 = k - 2, k2 = k - 1;
-            if (k3 >= 0 && k3 < n_local) {  // final(k-2): D3 -> SH colour -> texture, Eq. 7
+            if (k3 >= 0 && k3 < n_local && k3 % kG == g) {  // final(k-2): D3 -> SH colour -> texture, Eq. 7
                 const int sl = static_cast<int>(k3 % kWsSlots);
                 mbar_wait(done(sl), done_parity(k3, 2));
                 tc_fence_after();
@@ -793,7 +841,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) texture_ws_kernel(const Texture
                     rgb[1] = fmaxf(0.5f + c1, 0.f);
                     rgb[2] = fmaxf(0.5f + c2, 0.f);
                 }
-                float* srgb = srgb_base + (k3 & 1) * kRows * 3;
+                float* srgb = srgb_base + ((k3 / kG) & 1) * kRows * 3;
                 srgb[row * 3 + 0] = rgb[0];
                 srgb[row * 3 + 1] = rgb[1];
                 srgb[row * 3 + 2] = rgb[2];
@@ -802,7 +850,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) texture_ws_kernel(const Texture
                     a.fb.texture[wt.slot * 3 + 1] = rgb[1];
                     a.fb.texture[wt.slot * 3 + 2] = rgb[2];
                 }
-                named_barrier_sync(1, kRows);
+                named_barrier_sync(1 + g, kRows);
                 // Eq. 7: final = base + sum_j W[p,j] * texture[p,j] (renderer.cpp:219-236)
                 if (row < ppt) {
                     const int tpx = static_cast<int>(tile % tiles_x) * bw, tpy = static_cast<int>(tile / tiles_x) * bh;
@@ -826,8 +874,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) texture_ws_kernel(const Texture
                     }
                 }
             }
-            if (k2 >= 0 && k2 < n_local) conv(k2, 1);  // D2 -> A3
-            if (k < n_local) conv(k, 0);               // D1 -> A2
+            if (k2 >= 0 && k2 < n_local && k2 % kG == g) conv(k2, 1);  // D2 -> A3
+            if (k < n_local && k % kG == g) conv(k, 0);                // D1 -> A2
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) n_queries += __shfl_down_sync(0xffffffffu, n_queries, o);
@@ -836,24 +884,88 @@ __global__ void __launch_bounds__(kWsThreads, 1) texture_ws_kernel(const Texture
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+    if (warp == kMmaWarp)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::kTmemCols));
+}
+
+// The gathers of the bulk-fed variant: one thread per slot at full occupancy, features
+// split into bf16 hi / lo and stored as the tile's K-major operand image (16 KB per
+// 128-row tile: hi then lo), at the (tile, row) texture_ws_kernel<kBulk> assigns the slot.
+__global__ void __launch_bounds__(128) tex_features_img_kernel(const TextureArgs a, const TcConst cst, int bw, int bh,
+                                                               int tiles_x) {
+    const int64_t sl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int K = a.fb.K;
+    const int64_t total = static_cast<int64_t>(a.cam.W) * a.cam.H * K;
+    if (sl >= total) return;
+    float feats[kIn];
+#pragma unroll
+    for (int i = 0; i < kIn; ++i) feats[i] = 0.f;
+    const int64_t pix = sl / K;
+    const int j = static_cast<int>(sl - pix * K);
+    const int px = static_cast<int>(pix % a.cam.W), py = static_cast<int>(pix / a.cam.W);
+    if (a.fb.ids[sl] >= 0) {
+        double dir[3];
+        pixel_dir(a.cam, px + 0.5, py + 0.5, dir);
+        const double t = a.fb.depths[sl];
+        const double x0 = a.cam.o[0] + t * dir[0], x1 = a.cam.o[1] + t * dir[1], x2 = a.cam.o[2] + t * dir[2];
+        const float ft = static_cast<float>(a.cam.fx / t);
+        const uint32_t T = 1u << a.scene.field.log2_table, mask = T - 1u;
+        const float2* tab = reinterpret_cast<const float2*>(a.scene.table);
+        const bool small = fmax(fabs(x0), fmax(fabs(x1), fabs(x2))) * cst.level_scale[kLevels - 1] < 1073741824.0;
+        if (small) {
+            LevelFetch cur = fetch_level<true>(0, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
+#pragma unroll
+            for (int l = 0; l < kLevels; ++l) {
+                LevelFetch nxt;
+                if (l + 1 < kLevels) nxt = fetch_level<true>(l + 1, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight);
+                const float2 g = interp(cur);
+                feats[2 * l] = g.x;
+                feats[2 * l + 1] = g.y;
+                if (l + 1 < kLevels) cur = nxt;
+            }
+        } else {
+#pragma unroll
+            for (int l = 0; l < kLevels; ++l) {
+                const float2 g = interp(fetch_level<false>(l, x0, x1, x2, cst, tab, T, mask, ft, a.st.no_downweight));
+                feats[2 * l] = g.x;
+                feats[2 * l + 1] = g.y;
+            }
+        }
+    }
+    const int64_t tile = static_cast<int64_t>(py / bh) * tiles_x + px / bw;
+    const int row = ((py % bh) * bw + px % bw) * K + j;
+    uint8_t* img = reinterpret_cast<uint8_t*>(a.fscratch) + tile * kImgBytes;
+#pragma unroll
+    for (int c = 0; c < kIn / 8; ++c) store_split8(img, 0, kImgBytes / 2, kmajor_off(row, 8 * c, kIn), feats + 8 * c);
 }
 
 }  // namespace
 
 int texture_tc_path() {
-    // Default: split (measured fastest per frame at config 2: 2.83 ms vs 3.27 ms with the
-    // warp-specialised kernel, whose gathers have 16 warps per SM where the split
-    // gathers run at full occupancy, and whose 204 KB of shared memory keep the next
-    // frame's composite off the SM; the warp-specialised kernel moves 0.24 GB of DRAM
-    // per frame instead of ~1.2 GB).
+    // Measured at config 2 (ms per frame, two streams / one stream): split 2.84 / 3.09,
+    // bulk-fed warp-specialised with 4 epilogue groups 2.96 / 2.99 (2 groups: 3.16 /
+    // 3.19), gather warp-specialised 3.27 / 3.32. The warp-specialised kernels hold one
+    // ~170-200 KB CTA per SM, so the next frame's composite cannot share the SM while
+    // they run; split stays the default.
     static const int path = [] {
         const char* e = getenv("NX_TEXTURE_PATH");
         if (e && strcmp(e, "fused") == 0) return 1;
         if (e && strcmp(e, "ws") == 0) return 0;
+        if (e && strcmp(e, "bulk") == 0) return 3;
         return 2;
     }();
     return path;
+}
+
+size_t texture_tc_scratch_bytes(int W, int H, int K) {
+    if (K <= 0) return 0;
+    const int path = texture_tc_path();
+    if (path == 2) return static_cast<size_t>(W) * H * K * kIn * sizeof(float);
+    if (path != 3) return 0;
+    const int ppt = kRows / K;
+    const int bw = (kRows % K == 0 && ppt % 8 == 0) ? 8 : ppt;
+    const int bh = ppt / bw;
+    return static_cast<size_t>((W + bw - 1) / bw) * ((H + bh - 1) / bh) * kImgBytes;
 }
 
 bool texture_tc_supported(const nx_field_desc& fd) {
@@ -866,7 +978,7 @@ int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
     // over a feature scratch), "ws" (warp-specialised, no scratch) or "fused" (one CTA
     // role, three per SM).
     const int path = texture_tc_path();
-    if (path == 0 && K > 0) {
+    if ((path == 0 || (path == 3 && a.fscratch)) && K > 0) {
         const int ppt = kRows / K;
         const int bw = (kRows % K == 0 && ppt % 8 == 0) ? 8 : ppt;
         const int bh = ppt / bw;
@@ -882,10 +994,26 @@ int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(texture_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWsSmem);
         const int64_t grid = std::min<int64_t>(n_tiles, sms);
-        count_launch();
-        texture_ws_kernel<<<static_cast<unsigned>(grid), kWsThreads, kWsSmem, s>>>(a, cst, bw, bh, tiles_x, n_tiles);
+        if (path == 0) {
+            cudaFuncSetAttribute(texture_ws_kernel<kGather>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 WsCfg<kGather>::kSmem);
+            count_launch();
+            texture_ws_kernel<kGather><<<static_cast<unsigned>(grid), WsCfg<kGather>::kThreads, WsCfg<kGather>::kSmem,
+                                         s>>>(a, cst, bw, bh, tiles_x, n_tiles);
+            return NX_OK;
+        }
+        const int64_t total = static_cast<int64_t>(a.cam.W) * a.cam.H * K;
+        cudaFuncSetAttribute(texture_ws_kernel<kBulk>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             WsCfg<kBulk>::kSmem);
+        count_launch(2);
+        tex_features_img_kernel<<<static_cast<unsigned>((total + 127) / 128), 128, 0, s>>>(a, cst, bw, bh, tiles_x);
+        if (a.ev_mid) {
+            cudaEventRecord(a.ev_mid, s);
+            a.ev_mid_recorded = true;
+        }
+        texture_ws_kernel<kBulk><<<static_cast<unsigned>(grid), WsCfg<kBulk>::kThreads, WsCfg<kBulk>::kSmem, s>>>(
+            a, cst, bw, bh, tiles_x, n_tiles);
         return NX_OK;
     }
     if (a.fscratch && path == 2) {  // split: gathers at full occupancy, then the tensor-core MLP

@@ -4,6 +4,9 @@ seeded inputs. The cases follow the reference's own render tests
 (proj/tests/test_renderer.cpp, test_oracle.cpp, acceptance.cpp criteria 2-3)
 plus the BASELINE.json configs 1 and 2 (stump_like scenes, ring cameras).
 """
+import os
+import sys
+
 import numpy as np
 import pytest
 
@@ -12,6 +15,7 @@ from paper_2512_13796_b200 import NexelError, RenderSettings
 from parity import compare_frames, is_subsequence, psnr
 
 pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def gpu_render(renderer, scene, cam):
@@ -369,3 +373,43 @@ def test_image_bands_reassemble_the_full_frame_bit_exact(renderer, n_bands):
                         ("residual", 1)):
         got = np.concatenate([getattr(p, key) for p in parts])
         assert np.array_equal(got, getattr(full, key)), key
+
+
+_CAP_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2512_13796_b200 as nx
+scene = nx.stump_like(20000, grid_init=1e-1)
+r = nx.Renderer(0)
+ds = r.upload(scene)
+out = {}
+frames = [r.frame() for _ in range(3)]
+for i, f in enumerate(frames):          # three frames in flight before any read-back
+    r.render(ds, nx.ring_camera(7 * i, 256, 320, 240), f)
+for i, f in enumerate(frames):
+    g = f.download()
+    out[f"ids{i}"], out[f"final{i}"] = g.ids, g.final_img
+    out[f"keys{i}"] = np.array([f.stats()["work_keys"]])
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_async_list_capacity_overflow_rerenders_the_frame(tmp_path):
+    """The work lists are built on a device-side key count with a grow-only capacity (no
+    host round trip per frame). A frame whose count exceeded the capacity is rendered
+    again before it is read back: starting from a 1000-key capacity (NX_KEY_CAP), three
+    frames in flight come back identical to the default run."""
+    import subprocess
+    script = tmp_path / "cap.py"
+    script.write_text(_CAP_SCRIPT)
+    runs = {}
+    for name, env_extra in (("default", {}), ("tiny", {"NX_KEY_CAP": "1000"}), ("sync", {"NX_SYNC_LISTS": "1"})):
+        env = dict(os.environ, **env_extra)
+        fn = tmp_path / f"{name}.npz"
+        subprocess.run([sys.executable, str(script), ROOT, str(fn)], check=True, env=env, timeout=600)
+        runs[name] = np.load(fn)
+    for i in range(3):
+        assert runs["default"][f"keys{i}"][0] > 1000
+        for other in ("tiny", "sync"):
+            assert np.array_equal(runs["default"][f"ids{i}"], runs[other][f"ids{i}"]), (other, i)
+            assert np.array_equal(runs["default"][f"final{i}"], runs[other][f"final{i}"]), (other, i)
