@@ -78,6 +78,56 @@ def stage_bytes(stage, n, P, Pw, H, W, K, Q):
     return 8 * P
 
 
+def profile_json(rel):
+    try:
+        with open(os.path.join(ROOT, "profiles", rel)) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+def composite_compute_roofline(comp_ms):
+    """The composite kernel against its real roof, the fp64 pipe: executed fp64 flops per
+    launch (2 x DFMA + DMUL + DADD thread instructions, ncu, profiles/r02/frame_metrics.json)
+    over the event-timed launch, of the measured fp64 peak (tools/fp64_peak.cu,
+    profiles/r02/fp64_peak.json), with ncu's fp64-pipe utilisation beside it."""
+    fm, pk = profile_json("r02/frame_metrics.json"), profile_json("r02/fp64_peak.json")
+    if not fm or not pk or not comp_ms:
+        return None
+    c = fm["composite"]
+    flops = 2 * c["dfma"] + c["dmul"] + c["dadd"]
+    achieved = flops / (comp_ms / 1e3) / 1e12
+    pipe = None
+    try:
+        for line in open(os.path.join(ROOT, "profiles", "r02", "ncu_composite_summary.txt")):
+            if line.startswith("sm__pipe_fp64_cycles_active"):
+                pipe = float(line.split()[1])
+    except (OSError, ValueError):
+        pass
+    return {"bound": "fp64", "kernel": "composite", "achieved": achieved, "peak": pk["fp64_tflops"],
+            "unit": "TFLOP/s", "frac": achieved / pk["fp64_tflops"], "peak_source": "measured (tools/fp64_peak.cu)",
+            "flops_per_launch": flops, "flops_kind": "executed fp64 (2 DFMA + DMUL + DADD, ncu)",
+            "launch_ms": comp_ms, "fp64_pipe_pct_ncu": pipe,
+            "note": "latency-bound on dependent fp64 chains (intersect divisions, exp/log) at 28% occupancy; "
+                    "the HBM figure in `roofline` is kept for the contract"}
+
+
+def dropin_line():
+    """nexel::render (the reference's C++ API, host Scene in / FrameBuffers out) through the
+    drop-in library, at config 2: tests/cxx/bench_render.cpp, if built (make dropin)."""
+    exe = os.path.join(ROOT, "build", "dropin", "bench_render")
+    if not os.path.exists(exe):
+        return None
+    try:
+        out = subprocess.run([exe, "10"], capture_output=True, text=True, timeout=300).stdout
+        line = json.loads(out.strip().splitlines()[-1])
+        line["path"] = ("nexel::render(scene, cam): scene fingerprint, collection + texturing passes, download, "
+                        "FrameBuffers allocation (by value) and widening to the reference's doubles")
+        return line
+    except Exception as e:  # noqa: BLE001 - reported, never required
+        return {"error": f"{type(e).__name__}: {e}"}
+
+
 def traffic_of(stage: str):
     """DRAM bytes per launch of the stage's kernel from the committed ncu capture
     (profiles/traffic.json), or None if that kernel was not captured."""
@@ -569,6 +619,14 @@ def run_ours(args):
                    "executed_tflops": 3 * dec_tf, "flops_per_launch": dec_flops, "launch_ms": dec_ms,
                    "tensor_pipe_pct_ncu": pipe}
 
+    # measured DRAM per frame (every kernel of one frame, ncu: profiles/r02/frame_metrics.json)
+    frame_measured = None
+    fm = profile_json("r02/frame_metrics.json")
+    if fm:
+        dram_gbs = fm["frame_dram_bytes"] * (args.steps / (ms_local / 1e3)) / 1e9
+        frame_measured = {"dram_bytes_per_frame": fm["frame_dram_bytes"], "achieved": dram_gbs,
+                          "frac": dram_gbs / hbm_peak, "source": "profiles/r02/frame_metrics.json"}
+
     train = None
     if args.train_steps > 0:  # reported beside the headline; a failure here never voids it
         try:
@@ -594,7 +652,9 @@ def run_ours(args):
                          "frac": achieved / hbm_peak, "traffic": traffic_of(dom), "peak_source": peak_src,
                          "bytes_per_launch": dom_bytes, "launch_ms": stage_ms[dom]},
             "frame_roofline": {"bytes_per_frame": fbytes, "achieved": frame_gbs, "peak": hbm_peak, "unit": "GB/s",
-                               "frac": frame_gbs / hbm_peak, "formula": "240N + 8P + (28+24K)HW + 1024Q + 36864"},
+                               "frac": frame_gbs / hbm_peak, "formula": "240N + 8P + (28+24K)HW + 1024Q + 36864",
+                               "measured": frame_measured},
+            "compute_roofline": composite_compute_roofline(stage_ms.get("composite")),
             "decoder_roofline": decoder,
             # SURVEY.md §8(d) secondary compute figure: the reference-equivalent (pixel,
             # primitive) intersection tests — every key of the reference's tile lists times
@@ -609,6 +669,7 @@ def run_ours(args):
                     "path": "nx_render + nx_frame_download (all FrameBuffers) into pinned host memory, 3 frames in flight"},
             "gpu_launches": launches, "clocks": clk,
             "train_step": train,
+            "e2e_dropin": dropin_line() if (world == 1 and not args.no_cpu_baseline) else None,
         }
         print(json.dumps(line), flush=True)
     for f2 in frames:
