@@ -664,6 +664,12 @@ def run_ours(args):
                                                                "~27M exact fp64 evaluations per frame"},
             "stages_ms": stage_ms, "profiled_frames": prof_frames,
             "work": {"tile_keys_P": P, "work_keys": Pw, "queries_Q": Q},
+            # the safety net of the bit-exact claim: decisions of the timed views whose margin
+            # is below a generous bound on device-vs-reference math differences (all 0 = every
+            # discrete decision is the reference's beyond doubt; nx_internal.cuh NearKind)
+            "near_threshold": {k: int(sum(vstats[v][k] for v in set(timed_views)))
+                               for k in ("near_alpha", "near_transmittance", "near_topk", "near_depth", "near_rect",
+                                         "near_support")},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "nx_render + nx_frame_download (all FrameBuffers) into pinned host memory, 3 frames in flight"},

@@ -134,6 +134,14 @@ typedef struct nx_frame_stats {
     int64_t tile_keys;        /* reference tile-key count P (sum of tile-list lengths) */
     int64_t work_keys;        /* keys materialised and walked by the composite kernel */
     int64_t n_queries;        /* texture queries Q (non-empty slots) */
+    /* near-threshold decisions (margin below >= 100x what device vs reference math can
+     * differ by): zero means every decision of the frame is the reference's beyond doubt */
+    int64_t near_alpha;        /* hits with alpha within 1e-12 (relative) of 1/255 (kernel.hpp:11) */
+    int64_t near_transmittance;/* T within 1e-11 of min_transmittance at a composite step */
+    int64_t near_topk;         /* top-K comparisons between weights within 1e-11 */
+    int64_t near_depth;        /* sorted neighbours with depths within 1e-13 (renderer.cpp:102-105) */
+    int64_t near_rect;         /* rect floor / ceil arguments within 1e-9 px of an integer */
+    int64_t near_support;      /* 2 ln(255 o) within 1e-13 of 0 (support radius sign) */
 } nx_frame_stats;
 
 /* ---- context ---------------------------------------------------------- */

@@ -171,6 +171,12 @@ class nx_frame_stats(C.Structure):
         ("tile_keys", C.c_int64),
         ("work_keys", C.c_int64),
         ("n_queries", C.c_int64),
+        ("near_alpha", C.c_int64),
+        ("near_transmittance", C.c_int64),
+        ("near_topk", C.c_int64),
+        ("near_depth", C.c_int64),
+        ("near_rect", C.c_int64),
+        ("near_support", C.c_int64),
     ]
 
     def as_dict(self):

@@ -477,6 +477,7 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
                                            c->skeys_b.as<uint64_t>(), c->sids_b.as<uint32_t>(), n, d_total, 0, 64, sc,
                                            s);
     const uint32_t* sorted_ids = in_b ? c->sids_b.as<uint32_t>() : c->sids_a.as<uint32_t>();
+    const uint64_t* sorted_keys = in_b ? c->skeys_b.as<uint64_t>() : c->skeys_a.as<uint64_t>();
 
     // K3: emit (tile, id) keys in sorted order. The key count stays on the device: the
     // keys go into buffers of the context's capacity (grow-only) and the count comes back
@@ -484,7 +485,8 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
     // capacity yet (first frame), for reference lists and for debug / backward builds,
     // the count is read back first (one host round trip) and sizes the buffers exactly.
     record(c, kEvEmit, s);
-    launch_rect_counts(sorted_ids, n, d_total, c->work_rect.as<int4>(), c->counts.as<int32_t>(), s);
+    launch_rect_counts(sorted_ids, n, d_total, c->work_rect.as<int4>(), c->counts.as<int32_t>(), sorted_keys, f->stats,
+                       s);
     scan_exclusive(c->counts.as<int32_t>(), c->offsets.as<int32_t>(), n, d_total + 1, sc, s);
     const bool async = allow_async && !reference_lists && c->key_cap > 0 && !c->sync_lists && f->h_counts;
     int64_t cap;
@@ -606,6 +608,7 @@ int collection(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame*
     ca.dbg_y0 = dbg_y0;
     ca.dbg_y1 = dbg_y1;
     ca.dbg_max = dbg_max;
+    ca.stats = f->stats;
     launch_composite(ca, s);
     f->base64_valid = f->keep_backward;
     record(c, kEvCompEnd, s);
@@ -1129,6 +1132,12 @@ int nx_frame_stats_get(nx_ctx* c, const nx_frame* f, nx_frame_stats* out) {
     out->tile_keys = static_cast<int64_t>(h.tile_keys);
     out->work_keys = static_cast<int64_t>(h.work_keys);
     out->n_queries = static_cast<int64_t>(h.queries);
+    out->near_alpha = static_cast<int64_t>(h.near[NEAR_ALPHA]);
+    out->near_transmittance = static_cast<int64_t>(h.near[NEAR_TRANSMITTANCE]);
+    out->near_topk = static_cast<int64_t>(h.near[NEAR_TOPK]);
+    out->near_depth = static_cast<int64_t>(h.near[NEAR_DEPTH]);
+    out->near_rect = static_cast<int64_t>(h.near[NEAR_RECT]);
+    out->near_support = static_cast<int64_t>(h.near[NEAR_SUPPORT]);
     return NX_OK;
 }
 

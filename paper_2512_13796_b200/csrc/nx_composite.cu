@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                     res.id = sm.id[ws.sel[g0 + b]];
                     // intersect (intersect.hpp:23-42) + eval_kernel (kernel.hpp:16-30)
                     const HitTerms h = exact_hit(r, d0, d1, d2, a.cam.o[0], a.cam.o[1], a.cam.o[2], near_eps);
+                    if (h.near) atomicAdd(&a.stats->near[NEAR_ALPHA], 1ull);
                     if (h.alpha >= 0.0) {
                         res.alpha = h.alpha;
                         res.t = h.t;
@@ -284,6 +285,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                                     qm = k_seq[s];
                                 }
                             if (wgt > wm) slot = mi;
+                            if (wgt != wm && fabs(wgt - wm) <= kNearRel * wm) atomicAdd(&a.stats->near[NEAR_TOPK], 1ull);
                         }
 #pragma unroll
                         for (int s = 0; s < KK; ++s)
@@ -305,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                     }
                     T *= 1.0 - alpha;
                     if (T < min_T) active = false;
+                    if (fabs(T - min_T) <= kNearRel * min_T) atomicAdd(&a.stats->near[NEAR_TRANSMITTANCE], 1ull);
                 }
                 __syncwarp();
             }
@@ -327,6 +330,8 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                 for (int j = 0; j + 1 < K - i; ++j) {
                     const bool swap = (j + 1 < k_size) &&
                                       (k_w[j + 1] > k_w[j] || (k_w[j + 1] == k_w[j] && k_seq[j + 1] < k_seq[j]));
+                    if (j + 1 < k_size && k_w[j + 1] != k_w[j] && fabs(k_w[j + 1] - k_w[j]) <= kNearRel * k_w[j])
+                        atomicAdd(&a.stats->near[NEAR_TOPK], 1ull);
                     if (swap) {
                         const int32_t ti = k_id[j];
                         k_id[j] = k_id[j + 1];

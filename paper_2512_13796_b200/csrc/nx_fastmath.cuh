@@ -186,6 +186,7 @@ __device__ __forceinline__ double fm_axis_power(double u, double g, double& lu) 
 // the axis powers and exp(-p/2)), are filled for a hit.
 struct HitTerms {
     double alpha, t, u, v, lu, lv, pu, pv, k;
+    bool near;  // alpha within kNearAlpha of 1/255 (either side): a near-threshold decision
 };
 
 template <typename Rec>
@@ -193,6 +194,7 @@ __device__ __forceinline__ HitTerms exact_hit(const Rec& r, double d0, double d1
                                               double o2, double near_eps) {
     HitTerms h;
     h.alpha = -1.0;
+    h.near = false;
     const double denom = d0 * r[REC_NX] + d1 * r[REC_NY] + d2 * r[REC_NZ];
     if (!(fabs(denom) >= kMinNormalDot)) return h;
     h.t = r[REC_NUM] / denom;
@@ -211,6 +213,7 @@ __device__ __forceinline__ HitTerms exact_hit(const Rec& r, double d0, double d1
     h.k = isinf(q) ? 0.0 : fm_exp(-0.5 * q);
     const double al = isinf(q) ? 0.0 : r[REC_OP] * h.k;
     if (al >= kAlphaMin) h.alpha = al;
+    h.near = fabs(al - kAlphaMin) <= kNearAlpha * kAlphaMin;
     return h;
 }
 

@@ -139,12 +139,25 @@ enum PrimClass : int32_t {
     CLS_STRADDLER = 4,  // entry in every tile (reference); refined work rect here
 };
 
+// Near-threshold decisions (the safety net of the bit-exact claim): decisions taken in
+// fp64 with the reference's formulas whose margin is below a generous bound (>= 100x)
+// on the error the device math can have against the reference's (its own exp / log
+// routines instead of glibc's, exp(log / 2g) instead of pow, FMA contraction). Zero in
+// the parity tests; reported by the bench.
+enum NearKind { NEAR_ALPHA = 0, NEAR_TRANSMITTANCE, NEAR_TOPK, NEAR_DEPTH, NEAR_RECT, NEAR_SUPPORT, NEAR_KINDS };
+constexpr double kNearRel = 1e-11;        // T and top-K weights (products over up to ~100 hits)
+constexpr double kNearAlpha = 1e-12;      // alpha vs 1/255 (exp of a sum of powers: ~1e-14)
+constexpr double kNearDepth = 1e-13;      // camera-z of mu: a 3-term dot product + add (~4 ulp)
+constexpr double kNearPixel = 1e-9;       // rect floor / ceil arguments, in pixels (~1e-12 px)
+constexpr double kNearSupport = 1e-13;    // 2 ln(255 o) vs 0
+
 struct FrameStatsD {
     unsigned long long cls[5];
     unsigned long long straddlers_kept;
     unsigned long long tile_keys;
     unsigned long long work_keys;
     unsigned long long queries;
+    unsigned long long near[NEAR_KINDS];
 };
 
 struct SceneDev {
@@ -203,8 +216,9 @@ void launch_compact(const int32_t* flag, const int32_t* pos, const uint64_t* key
                     uint64_t* keys_out, uint32_t* ids_out, cudaStream_t s);
 
 // counts[r] = tiles of rect[ids[r]] (work or reference rect) for r < *n_dev, 0 up to n.
+// (+ counts sorted neighbours whose depths differ by less than kNearRel: NEAR_DEPTH)
 void launch_rect_counts(const uint32_t* ids, int64_t n, const int32_t* n_dev, const int4* rect, int32_t* counts,
-                        cudaStream_t s);
+                        const uint64_t* sorted_keys, FrameStatsD* stats, cudaStream_t s);
 
 // Emits (tile, id) for every tile of every sorted primitive's rect, in sorted
 // order (row-major tiles, renderer.cpp:106-110), and counts keys per tile. The sorted
@@ -228,6 +242,7 @@ struct CompositeArgs {
     int32_t* dbg_hits;   // optional: per-pixel hit ids (rows [dbg_y0, dbg_y1))
     int32_t* dbg_counts;
     int dbg_y0, dbg_y1, dbg_max;
+    FrameStatsD* stats;  // near-threshold counters
 };
 void launch_composite(const CompositeArgs& a, cudaStream_t s);
 

@@ -116,6 +116,10 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const PreprocessArgs a)
             gy = 1.0 + softplus(g[11 * n + i]);
         }
         const double ru = support_radius(op, gx), rv = support_radius(op, gy);
+        {  // near-threshold: support radius sign (kernel.hpp:72-76)
+            const double lim = 2.0 * log(op / kAlphaMin);
+            if (fabs(lim) < kNearSupport) atomicAdd(&a.stats->near[NEAR_SUPPORT], 1ull);
+        }
         int4 ref = empty_rect(), work = empty_rect();
         double depth = 0.0;
         int4 prect = empty_rect();  // pixel rect containing every possible hit (work mode)
@@ -153,6 +157,13 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const PreprocessArgs a)
             if (all_behind && !all_visible) {
                 cls = CLS_BEHIND;
             } else if (all_visible) {
+                {  // near-threshold: the rect's floor / ceil arguments next to an integer
+                    const double v[4] = {px0 - 1.5, px1 + 0.5, py0 - 1.5, py1 + 0.5};
+                    int near = 0;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) near |= fabs(v[q] - rint(v[q])) < kNearPixel;
+                    if (near) atomicAdd(&a.stats->near[NEAR_RECT], 1ull);
+                }
                 const int ix0 = x86_to_int(floor(px0 - 1.5)), ix1 = x86_to_int(ceil(px1 + 0.5));
                 const int iy0 = x86_to_int(floor(py0 - 1.5)), iy1 = x86_to_int(ceil(py1 + 0.5));
                 if (ix1 < 0 || iy1 < 0 || ix0 >= a.cam.W || iy0 >= a.cam.H) {
@@ -260,11 +271,20 @@ __global__ void compact_kernel(const int32_t* flag, const int32_t* pos, const ui
 
 // counts over the capacity n: entries past the device count are zero, so a scan over
 // the whole capacity yields the right offsets and total.
+__device__ __forceinline__ double key_depth(uint64_t k) {  // inverse of depth_key
+    const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    return __longlong_as_double(static_cast<long long>(b));
+}
+
 __global__ void rect_counts_kernel(const uint32_t* ids, int64_t n, const int32_t* n_dev, const int4* rect,
-                                   int32_t* counts) {
+                                   int32_t* counts, const uint64_t* keys, FrameStatsD* stats) {
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t m = n_dev ? min(n, static_cast<int64_t>(*n_dev)) : n;
     if (r < n) counts[r] = r < m ? rect_tiles(rect[ids[r]]) : 0;
+    if (keys && r + 1 < m && keys[r] != keys[r + 1]) {  // near-threshold: (depth, id) order of neighbours
+        const double d0 = key_depth(keys[r]), d1 = key_depth(keys[r + 1]);
+        if (fabs(d1 - d0) <= kNearDepth * fabs(d0)) atomicAdd(&stats->near[NEAR_DEPTH], 1ull);
+    }
 }
 
 // One thread per emitted key: binary search of the owning sorted primitive. Counts on
@@ -347,10 +367,11 @@ void launch_compact(const int32_t* flag, const int32_t* pos, const uint64_t* key
 }
 
 void launch_rect_counts(const uint32_t* ids, int64_t n, const int32_t* n_dev, const int4* rect, int32_t* counts,
-                        cudaStream_t s) {
+                        const uint64_t* sorted_keys, FrameStatsD* stats, cudaStream_t s) {
     if (n <= 0) return;
     count_launch();
-    rect_counts_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(ids, n, n_dev, rect, counts);
+    rect_counts_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(ids, n, n_dev, rect, counts,
+                                                                               sorted_keys, stats);
 }
 
 void launch_emit(const uint32_t* ids, const int32_t* offsets, int64_t sorted_cap, const int32_t* n_sorted_dev,
