@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--height", type=int, default=1080)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--train-steps", type=int, default=10, help="timed forward+backward steps (config 5); 0 = skip")
+    p.add_argument("--bands", type=int, default=0,
+                   help="config 4: image bands per view (default: the world size; world / bands view groups)")
     p.add_argument("--config", type=int, choices=[2, 4], default=2,
                    help="2: 400K nexels 1080p, views sharded (headline); 4: 1.3M nexels 4K, image bands x views")
     return p.parse_args()
@@ -58,6 +60,8 @@ def workload(args):
         "nexels": args.nexels, "width": args.width, "height": args.height, "top_k": 2,
         "scene": "stump_like(seed 2512, c=1.0, R_ground=4.0), field grid_init 1e-4 (SURVEY.md §8(d))",
         "l2": "inputs larger than L2 (scene 115 MB fp64/fp32 + 134 MB hash table), view changes every step",
+        "dealing": "one GPU: views in ring order; N > 1: dynamic, every rank pulls the next view from one shared "
+                   "atomic counter (views.DynamicDealer over the torch.distributed store)",
     }
 
 
@@ -525,6 +529,12 @@ def run_ours(args):
     r.synchronize()
 
     # ---- timed region: device time of K steps (CUDA events on the render stream)
+    from paper_2512_13796_b200.views import DynamicDealer, render_dealt
+    all_cams = {v: nx.ring_camera(v, N_VIEWS, args.width, args.height) for v in range(N_VIEWS)}
+    dealer = None
+    if world > 1:
+        store = dist.distributed_c10d._get_default_store()
+        dealer = DynamicDealer(args.steps * world, store=store, key="nx_bench_views", start=args.warmup * world)
     r.set_profiling(True)
     r.stage_times()  # reset accumulators
     clocks = ClockSampler(local)
@@ -535,8 +545,14 @@ def run_ours(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for s in range(args.warmup, n_steps):
-        r.render(ds, cams[views[s]], frames[s % 2])
+    if world > 1:
+        # views dealt from one atomic counter shared by the ranks (views.DynamicDealer: the
+        # store's add), so per-view cost differences balance out; no data-path collective
+        rendered = render_dealt(r, ds, all_cams, frames, dealer)
+    else:
+        for s in range(args.warmup, n_steps):
+            r.render(ds, cams[views[s]], frames[s % 2])
+        rendered = views[args.warmup:]
     r._check(r.lib.nx_ctx_join(r.ctx))  # the end event follows the last texture pass
     ev1.record(stream)
     torch.cuda.synchronize()
@@ -598,7 +614,7 @@ def run_ours(args):
     dom_bytes = stage_bytes(dom, args.nexels, P, Pw, H, W, K, Q)
     achieved = dom_bytes / (stage_ms[dom] / 1e3) / 1e9
     fbytes = frame_bytes(args.nexels, P, H, W, K, Q)
-    frame_gbs = fbytes * (args.steps / (ms_local / 1e3)) / 1e9
+    frame_gbs = fbytes * (len(rendered) / (ms_local / 1e3)) / 1e9
     # the texture decoder on the tensor cores (north star: tensor-pipe utilisation for the
     # decoder): the MLP's algorithmic flops per query over its event-timed stage
     decoder = None
@@ -623,7 +639,7 @@ def run_ours(args):
     frame_measured = None
     fm = profile_json("r02/frame_metrics.json")
     if fm:
-        dram_gbs = fm["frame_dram_bytes"] * (args.steps / (ms_local / 1e3)) / 1e9
+        dram_gbs = fm["frame_dram_bytes"] * (len(rendered) / (ms_local / 1e3)) / 1e9
         frame_measured = {"dram_bytes_per_frame": fm["frame_dram_bytes"], "achieved": dram_gbs,
                           "frac": dram_gbs / hbm_peak, "source": "profiles/r02/frame_metrics.json"}
 
@@ -703,9 +719,11 @@ def run_config4(args):
     scene = nx.stump_like(n)
     r = nx.Renderer(local)
     ds = r.upload(scene)
-    y0, rows = nx.image_bands(H, world)[rank]
+    from paper_2512_13796_b200.views import ShardPlan
+    plan = ShardPlan(world, rank, args.bands or world)  # view groups x image bands
+    y0, rows = plan.band_rows(H)
     n_steps = args.warmup + args.steps
-    cams = [nx.band_camera(nx.ring_camera(s % N_VIEWS, N_VIEWS, W, H), y0, rows) for s in range(n_steps)]
+    cams = [nx.band_camera(nx.ring_camera(v, N_VIEWS, W, H), y0, rows) for v in plan.views(n_steps)]
     frames = [r.frame(), r.frame()]
     stats = []
     for s in range(args.warmup, min(n_steps, args.warmup + 3)):  # untimed work statistics
@@ -731,7 +749,7 @@ def run_config4(args):
     clk = clocks.stop()
     launches = int(r.lib.nx_launch_count() - launches0)
     ms = max_over_ranks(dist, e0.elapsed_time(e1), f"cuda:{local}")
-    fps = args.steps / (ms / 1e3)
+    fps = args.steps * plan.groups / (ms / 1e3)  # full frames: one per view group per step
     # e2e: band render + download of the band's FrameBuffers into pinned memory
     npix = W * rows
     host = {k: torch.empty(sz, dtype=dt, pin_memory=True) for k, sz, dt in (
@@ -758,6 +776,7 @@ def run_config4(args):
     torch.cuda.synchronize()
     barrier(dist)
     e2e_ms = max_over_ranks(dist, e0.elapsed_time(e1), f"cuda:{local}")
+    e2e_fps = args.steps * plan.groups / (e2e_ms / 1e3)
     d2h = sum(t.numel() * t.element_size() for t in host.values())
     # frame roofline from this rank's band statistics, summed over ranks
     mean = lambda key: sum(st[key] for st in stats) / max(len(stats), 1)
@@ -789,17 +808,19 @@ def run_config4(args):
         line = {
             "metric": f"rendered 4K frames/sec at {n // 1000}K nexels (config 4) + % HBM roofline",
             "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if plan.groups == 1 else "weak", "vs_baseline": None,
             "dtype": DTYPE, "data": "synthetic",
-            "config": {"workload": f"config 4: stump_like {n} nexels, {W}x{H}, K=2, {world} image band(s) of one "
-                                   f"view per step, views along the 256-view ring", "nexels": n, "width": W,
-                       "height": H, "top_k": K, "bands": nx.image_bands(H, world),
+            "config": {"workload": f"config 4: stump_like {n} nexels, {W}x{H}, K=2, {plan.groups} view group(s) x "
+                                   f"{plan.bands} image band(s): each group renders one view per step along the "
+                                   f"256-view ring, each rank one band of it", "nexels": n, "width": W,
+                       "height": H, "top_k": K, "bands": nx.image_bands(H, plan.bands), "view_groups": plan.groups,
                        "l2": "inputs larger than L2, view changes every step"},
             "frame_roofline": {"bytes_per_frame": fbytes, "achieved": fbytes * fps / 1e9, "peak": hbm_peak,
                                "unit": "GB/s", "frac": fbytes * fps / 1e9 / hbm_peak,
                                "formula": "240N + 8P + (28+24K)HW + 1024Q + 36864"},
             "work": {"tile_keys_P": P, "queries_Q": Q},
-            "e2e": {"value": args.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": C.sizeof(_abi.nx_camera),
+            "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": C.sizeof(_abi.nx_camera),
                     "d2h_bytes_per_step": d2h * world,
                     "path": "per rank: nx_render (band) + nx_frame_download of the band, 3 frames in flight"},
             "gpu_launches": launches, "clocks": clk,

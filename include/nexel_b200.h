@@ -235,6 +235,10 @@ int nx_texturing_pass(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam,
 /* render = collection_pass + texturing_pass (renderer.cpp:239-244). */
 int nx_render(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam, nx_frame* frame,
               void* stream);
+/* A batch of views: cams[i] rendered into frames[i % n_frames],
+ * pipelined as back-to-back nx_render calls; n_frames frames are in flight. */
+int nx_render_views(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cams, int n_views,
+                    nx_frame* const* frames, int n_frames, void* stream);
 
 /* ---- render_backward (renderer.hpp:30-53, renderer.cpp:251-401) ------- */
 /* UpstreamGrads (renderer.hpp:40-44): fp64 arrays in the FrameBuffers layouts; any

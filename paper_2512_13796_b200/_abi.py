@@ -222,6 +222,7 @@ SIGNATURES = [
     ("nx_frame_stats_get", C.c_int, [P, P, C.POINTER(nx_frame_stats)]),
     ("nx_collection_pass", C.c_int, [P, P, C.POINTER(nx_camera), P, P]),
     ("nx_texturing_pass", C.c_int, [P, P, C.POINTER(nx_camera), P, P]),
+    ("nx_render_views", C.c_int, [P, P, C.POINTER(nx_camera), C.c_int, C.POINTER(P), C.c_int, P]),
     ("nx_render", C.c_int, [P, P, C.POINTER(nx_camera), P, P]),
     ("nx_frame_set_backward", C.c_int, [P, P, C.c_int]),
     ("nx_render_backward", C.c_int,

@@ -441,6 +441,14 @@ class Renderer:
         c = cam.to_c()
         self._check(self.lib.nx_render(self.ctx, dscene.handle, C.byref(c), frame.handle, stream or None))
 
+    def render_views(self, dscene: DeviceScene, cams: Sequence[Camera], frames: Sequence[DeviceFrame],
+                     stream: int = 0):
+        """nx_render_views: cams[i] into frames[i % len(frames)], pipelined (asynchronous)."""
+        arr = (_abi.nx_camera * len(cams))(*[c.to_c() for c in cams])
+        fr = (C.c_void_p * len(frames))(*[f.handle for f in frames])
+        self._check(self.lib.nx_render_views(self.ctx, dscene.handle, arr, len(cams), fr, len(frames),
+                                             stream or None))
+
     def render_backward(self, dscene: DeviceScene, cam: Camera, frame: DeviceFrame, up: UpstreamGrads,
                         grads: SceneGrads, err_pixel: Optional[np.ndarray] = None,
                         blended_error: Optional[np.ndarray] = None):

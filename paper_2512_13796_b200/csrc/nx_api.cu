@@ -1162,6 +1162,19 @@ int nx_render(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* 
     return texturing(c, scene, cam, f, stream ? s : c->stream2);
 }
 
+// A batch of views: cams[i] into frames[i % n_frames], pipelined like back-to-back
+// nx_render calls (each frame's texture pass overlaps the next view's collection).
+int nx_render_views(nx_ctx* c, const nx_scene* scene, const nx_camera* cams, int n_views, nx_frame* const* frames,
+                    int n_frames, void* stream) {
+    if (!c || !scene || (n_views > 0 && (!cams || !frames || n_frames < 1)))
+        return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    for (int i = 0; i < n_frames && i < n_views; ++i)
+        if (!frames[i]) return set_err(c, NX_INVALID_ARGUMENT, "null frame");
+    for (int i = 0; i < n_views; ++i)
+        if (const int st = nx_render(c, scene, &cams[i], frames[i % n_frames], stream)) return st;
+    return NX_OK;
+}
+
 int nx_frame_set_backward(nx_ctx* c, nx_frame* f, int enable) {
     if (!c || !f) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
     f->keep_backward = enable != 0;

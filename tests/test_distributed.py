@@ -90,3 +90,58 @@ def test_image_bands_partition_the_rows():
                     assert y0 % 16 == 0
                 y = y0 + rows
             assert y == H
+
+
+def _dyn_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import time
+    import torch.distributed as dist
+    from paper_2512_13796_b200.views import DynamicDealer
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    store = dist.distributed_c10d._get_default_store()
+    dealer = DynamicDealer(100, store=store, start=7)
+    got = []
+    while (v := dealer.next()) is not None:
+        got.append(v)
+        time.sleep(0.001 * (1 + rank))  # rank 1 is slower: it should draw fewer views
+    q.put((rank, got))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_dynamic_view_dealing_two_ranks():
+    """Views pulled from one shared atomic counter (the store's add): every view of the
+    run is rendered exactly once across the ranks, and the faster rank takes more."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dyn_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    allv = sorted(out[0] + out[1])
+    assert allv == sorted((7 + i) % 256 for i in range(100))
+    assert len(out[0]) > len(out[1])
+
+
+def test_view_groups_times_bands_cover_every_band_of_every_view():
+    """Config 4 sharding: world 8 = 2 view groups x 4 bands; per step every view the
+    groups render has all its bands rendered once, the bands partition the rows."""
+    from paper_2512_13796_b200.views import ShardPlan
+    world, H = 8, 2160
+    plans = [ShardPlan(world, r, 4) for r in range(world)]
+    for s in range(6):
+        seen = {}
+        for p in plans:
+            v = p.views(6)[s]
+            seen.setdefault(v, []).append(p.band_rows(H))
+        assert len(seen) == 2  # two views per step (one per group)
+        for v, bands in seen.items():
+            bands.sort()
+            assert bands[0][0] == 0 and sum(r for _, r in bands) == H
+    with pytest.raises(ValueError):
+        ShardPlan(8, 0, 3)
