@@ -347,53 +347,18 @@ def train_step_timing(args, r, ds, scene, cam, stream, dist, local):
     gt = _device_view(v.final_img, npix * 3, torch.float32, dev).double()  # a copy, fp64
     tf.close()
     ts.close()
-    d_final = torch.zeros(npix * 3, dtype=torch.float64, device=dev)
-    d_weights = torch.zeros(npix * K, dtype=torch.float64, device=dev)
-    d_texture = torch.zeros(npix * K * 3, dtype=torch.float64, device=dev)
-    err = torch.zeros(npix, dtype=torch.float64, device=dev)
-    f = scene.field
-    grads = [torch.zeros(scene.nexels.shape[0] * 60, dtype=torch.float64, device=dev),
-             torch.zeros(f.grid.param_count(), dtype=torch.float64, device=dev),
-             torch.zeros(f.w1.size, dtype=torch.float64, device=dev),
-             torch.zeros(f.w2.size, dtype=torch.float64, device=dev),
-             torch.zeros(f.w3.size, dtype=torch.float64, device=dev)]
-    blend = torch.zeros(scene.nexels.shape[0], dtype=torch.float64, device=dev)
-    terms = torch.zeros(8, dtype=torch.float64, device=dev)
-    up = _abi.nx_upstream(d_final.data_ptr(), d_weights.data_ptr(), d_texture.data_ptr())
-    gg = _abi.nx_grads(*(t.data_ptr() for t in grads))
-    lw = _abi.nx_loss_weights()
-    r.lib.nx_loss_weights_default(C.byref(lw))
-    # Adam groups with the trainer's default rates (trainer.hpp:30-42, trainer.cpp:238-250)
-    ext = scene.extent
-    cfgs = [(1.6e-4 * ext, 1e-15), (1e-3, 1e-8), (5e-3, 1e-8), (5e-2, 1e-8), (2e-3, 1e-8), (2.5e-3, 1e-8),
-            (1.25e-4, 1e-8), (1e-2, 1e-8), (1e-3, 1e-8), (1e-3, 1e-8), (1e-3, 1e-8)]
-    acfg = (_abi.nx_adam_config * _abi.NX_NUM_GROUPS)(*[_abi.nx_adam_config(lr, 0.9, 0.999, eps)
-                                                          for lr, eps in cfgs])
-    opt = C.c_void_p()
-    r._check(r.lib.nx_optimizer_create(r.ctx, ds.handle, C.byref(opt)))
-    fr = r.frame()
-    fr.set_backward(True)
+    # the data-parallel training iteration (train_dp.DataParallelStep): zeroed SceneGrads,
+    # render, losses_backward, error map, render_backward, gradient all-reduce across the
+    # ranks (NCCL, N > 1), Adam
+    from paper_2512_13796_b200.train_dp import DataParallelStep
+    dp = DataParallelStep(r, ds, scene, {0: cam}, {0: gt}, dist=dist, stream=stream)
+    fr = dp.frame
+    grads, terms = dp.grads, dp.terms
     c = cam.to_c()
     s = C.c_void_p(r.stream)
 
     def step():
-        with torch.cuda.stream(stream):  # SceneGrads::allocate (renderer.cpp:245-248), every iteration
-            for t in grads:
-                t.zero_()
-        r._check(r.lib.nx_render(r.ctx, ds.handle, C.byref(c), fr.handle, s))
-        r._check(r.lib.nx_losses_backward(r.ctx, ds.handle, fr.handle, C.c_void_p(gt.data_ptr()), C.byref(lw),
-                                          C.c_void_p(d_final.data_ptr()), C.c_void_p(d_weights.data_ptr()),
-                                          C.c_void_p(d_texture.data_ptr()), C.byref(gg),
-                                          C.c_void_p(terms.data_ptr()), s))
-        # err_pixel = mean_c |final - gt| (trainer.cpp:289-296)
-        r._check(r.lib.nx_pixel_error(r.ctx, fr.handle, C.c_void_p(gt.data_ptr()), C.c_void_p(err.data_ptr()), s))
-        r._check(r.lib.nx_render_backward(r.ctx, ds.handle, C.byref(c), fr.handle, C.byref(up), C.byref(gg),
-                                          C.c_void_p(err.data_ptr()), C.c_void_p(blend.data_ptr()), s))
-        if dist is not None:  # data-parallel over views: mean of the ranks' gradients (NCCL)
-            with torch.cuda.stream(stream):
-                for t in grads:
-                    dist.all_reduce(t, op=dist.ReduceOp.AVG)
-        r._check(r.lib.nx_optimizer_step(r.ctx, opt, ds.handle, C.byref(gg), acfg, s))
+        dp.step(0)
 
     for _ in range(3):
         step()
@@ -414,8 +379,7 @@ def train_step_timing(args, r, ds, scene, cam, stream, dist, local):
     t = terms.cpu().tolist()
     finite = bool(torch.isfinite(grads[0]).all().item() and torch.isfinite(grads[1]).all().item())
     st = fr.stats()
-    fr.close()
-    r.lib.nx_optimizer_destroy(opt)
+    dp.close()
     # backward roofline: read the frame (76 HW) and the upstream
     # gradients ((12 + 16K) HW), write the primitive gradients (240 N), read-modify-write the
     # grid gradients (2 x 1024 Q), read the tile lists (4 P)
