@@ -43,6 +43,10 @@ constexpr int kPool = 32 * kSub;
 constexpr int kRecPieces = REC_FIELDS * 8 / 16;  // 16-byte pieces of an fp64 record (10)
 constexpr int kShPieces = NX_SH_VALUES * 4 / 16; // 16-byte pieces of the SH coefficients (12)
 static_assert(kWorkTile == 8, "warp blocks are 8x4 pixels");
+#ifndef NX_NEAR_COUNTERS
+#define NX_NEAR_COUNTERS 1
+#endif
+constexpr bool kNear = NX_NEAR_COUNTERS;  // near-threshold decision counters (FrameStatsD::near)
 static_assert(kChunk <= 256 && kSub <= 8, "pool entries pack (lane, group slot) in 16 bits");
 
 struct PoolEntry {  // one evaluated (pixel, primitive) pair
@@ -145,6 +149,9 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
     int k_size = 0;
     uint32_t counter = 0;
     bool active = in_img;
+    // near-threshold decisions of this pixel (kNear), packed: alpha | T << 10 | top-K << 20
+    // (per-pixel counts stay far below 1024)
+    uint32_t n_near = 0;
     int dbg_n = 0;
     const bool dbg_row = kDebug && in_img && py >= a.dbg_y0 && py < a.dbg_y1;
     const int64_t dbg_q = kDebug ? (static_cast<int64_t>(py - a.dbg_y0) * W + px) : 0;
@@ -247,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                     res.id = sm.id[ws.sel[g0 + b]];
                     // intersect (intersect.hpp:23-42) + eval_kernel (kernel.hpp:16-30)
                     const HitTerms h = exact_hit(r, d0, d1, d2, a.cam.o[0], a.cam.o[1], a.cam.o[2], near_eps);
-                    if (h.near) atomicAdd(&a.stats->near[NEAR_ALPHA], 1ull);
+                    if (kNear) n_near += h.near ? 1u : 0u;
                     if (h.alpha >= 0.0) {
                         res.alpha = h.alpha;
                         res.t = h.t;
@@ -285,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                                     qm = k_seq[s];
                                 }
                             if (wgt > wm) slot = mi;
-                            if (wgt != wm && fabs(wgt - wm) <= kNearRel * wm) atomicAdd(&a.stats->near[NEAR_TOPK], 1ull);
+                            if (kNear) n_near += (wgt != wm) & (fabs(wgt - wm) <= kNearRel * wm) ? (1u << 20) : 0u;
                         }
 #pragma unroll
                         for (int s = 0; s < KK; ++s)
@@ -307,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                     }
                     T *= 1.0 - alpha;
                     if (T < min_T) active = false;
-                    if (fabs(T - min_T) <= kNearRel * min_T) atomicAdd(&a.stats->near[NEAR_TRANSMITTANCE], 1ull);
+                    if (kNear) n_near += fabs(T - min_T) <= kNearRel * min_T ? (1u << 10) : 0u;
                 }
                 __syncwarp();
             }
@@ -330,8 +337,8 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                 for (int j = 0; j + 1 < K - i; ++j) {
                     const bool swap = (j + 1 < k_size) &&
                                       (k_w[j + 1] > k_w[j] || (k_w[j + 1] == k_w[j] && k_seq[j + 1] < k_seq[j]));
-                    if (j + 1 < k_size && k_w[j + 1] != k_w[j] && fabs(k_w[j + 1] - k_w[j]) <= kNearRel * k_w[j])
-                        atomicAdd(&a.stats->near[NEAR_TOPK], 1ull);
+                    if (kNear && j + 1 < k_size && k_w[j + 1] != k_w[j] && fabs(k_w[j + 1] - k_w[j]) <= kNearRel * k_w[j])
+                        n_near += 1u << 20;
                     if (swap) {
                         const int32_t ti = k_id[j];
                         k_id[j] = k_id[j + 1];
@@ -387,6 +394,12 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
             a.fb.base64[pix * 3 + 2] = acc[2];
         }
         if (kDebug && dbg_row) a.dbg_counts[dbg_q] = dbg_n;
+    }
+    if (kNear && n_near) {
+        if (n_near & 1023u) atomicAdd(&a.stats->near[NEAR_ALPHA], static_cast<unsigned long long>(n_near & 1023u));
+        if ((n_near >> 10) & 1023u)
+            atomicAdd(&a.stats->near[NEAR_TRANSMITTANCE], static_cast<unsigned long long>((n_near >> 10) & 1023u));
+        if (n_near >> 20) atomicAdd(&a.stats->near[NEAR_TOPK], static_cast<unsigned long long>(n_near >> 20));
     }
 }
 
