@@ -70,8 +70,13 @@ typedef struct nx_settings {
     int32_t no_gamma;
     int32_t no_prim_sh;
     int32_t no_downweight;
-    int32_t reserved;
+    int32_t precision;          /* NX_PRECISION_DEFAULT: fp64 decisions / depths / weights, fp32 colour,
+                                   bf16x3 tensor-core decoder; NX_PRECISION_F64: fp64 colour as well
+                                   (SH, hash grid, decoder, base, texture, final — the reference's
+                                   FrameBuffers precision; fp64 copies of SH / table / MLP kept on the
+                                   device; render-only: no optimizer / density control) */
 } nx_settings;
+enum { NX_PRECISION_DEFAULT = 0, NX_PRECISION_F64 = 1 };
 
 /* HashGridConfig (hash_grid.hpp:39-56) + TextureMlp shapes (mlp.hpp:11-33). */
 typedef struct nx_field_desc {
@@ -119,6 +124,8 @@ typedef struct nx_host_frame {
                           frame keeps it (nx_frame_set_backward); upload: makes the frame keep it */
     double* residual_f64;  /* fp64 terminal transmittance, kept with the fp64 base (same rules) —
                               FrameBuffers::residual at the reference's precision */
+    double* texture_f64;   /* download only: fp64 texture / final of an NX_PRECISION_F64 render */
+    double* final_f64;
 } nx_host_frame;
 
 /* Per-frame binning / work statistics (read back with nx_frame_stats). */

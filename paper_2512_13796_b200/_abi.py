@@ -25,6 +25,8 @@ NX_CUDA_ERROR = 13
 NX_NO_DEVICE = 14
 
 NX_MAX_TOP_K = 8
+NX_PRECISION_DEFAULT = 0
+NX_PRECISION_F64 = 1
 NX_PARAMS_PER_NEXEL = 60
 NX_SH_VALUES = 48
 NX_NUM_STAGES = 7
@@ -55,7 +57,7 @@ class nx_settings(C.Structure):
         ("no_gamma", C.c_int32),
         ("no_prim_sh", C.c_int32),
         ("no_downweight", C.c_int32),
-        ("reserved", C.c_int32),
+        ("precision", C.c_int32),
     ]
 
 
@@ -111,6 +113,8 @@ class nx_host_frame(C.Structure):
         ("residual", C.c_void_p),
         ("base_f64", C.c_void_p),
         ("residual_f64", C.c_void_p),
+        ("texture_f64", C.c_void_p),
+        ("final_f64", C.c_void_p),
     ]
 
 

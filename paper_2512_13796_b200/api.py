@@ -50,6 +50,10 @@ class RenderSettings:
     no_gamma: bool = False
     no_prim_sh: bool = False
     no_downweight: bool = False
+    # not a reference knob: NX_PRECISION_F64 renders the colours at the reference's fp64
+    # precision (fp64 SH / hash grid / decoder); the default keeps fp32 colour and the
+    # bf16x3 tensor-core decoder (decisions, depths and weights are fp64 either way)
+    precision: int = 0
 
     def to_c(self) -> _abi.nx_settings:
         s = _abi.nx_settings()
@@ -63,13 +67,14 @@ class RenderSettings:
         s.no_gamma = int(bool(self.no_gamma))
         s.no_prim_sh = int(bool(self.no_prim_sh))
         s.no_downweight = int(bool(self.no_downweight))
+        s.precision = int(self.precision)
         return s
 
     @classmethod
     def from_c(cls, s: _abi.nx_settings) -> "RenderSettings":
         return cls(top_k=s.top_k, background=tuple(s.background), near_eps=s.near_eps, alpha_max=s.alpha_max,
                    min_transmittance=s.min_transmittance, tile=s.tile, no_gamma=bool(s.no_gamma),
-                   no_prim_sh=bool(s.no_prim_sh), no_downweight=bool(s.no_downweight))
+                   no_prim_sh=bool(s.no_prim_sh), no_downweight=bool(s.no_downweight), precision=int(s.precision))
 
 
 @dataclasses.dataclass
@@ -348,10 +353,17 @@ class DeviceFrame:
         hf = _abi.nx_host_frame()
         for k, arr in out.items():
             setattr(hf, k, arr.ctypes.data if k in want else None)
+        f64 = {}
+        if fields and ("texture_f64" in want or "final_f64" in want):  # NX_PRECISION_F64 renders
+            f64 = {"texture_f64": np.zeros((H * W * K * 3,)), "final_f64": np.zeros((H * W * 3,))}
+            hf.texture_f64, hf.final_f64 = f64["texture_f64"].ctypes.data, f64["final_f64"].ctypes.data
         r = self.renderer
         r._check(r.lib.nx_frame_download(r.ctx, self.handle, C.byref(hf), None))
         r._check(r.lib.nx_ctx_synchronize(r.ctx))
-        return FrameBuffers(W, H, K, **out)
+        fb = FrameBuffers(W, H, K, **out)
+        for k, v in f64.items():
+            setattr(fb, k, v)
+        return fb
 
     def close(self):
         if self.handle:

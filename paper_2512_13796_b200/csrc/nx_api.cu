@@ -143,6 +143,7 @@ struct nx_scene {
     int64_t n = 0;
     DevBuf geom, sh, table, w1, w2, w3;
     DevBuf geom_spare, sh_spare;  // density control rebuilds into these and swaps (grow-only)
+    DevBuf sh64, table64, w1_64, w2_64, w3_64;  // fp64 copies (NX_PRECISION_F64 scenes only)
     uint64_t version = next_scene_version();  // new on every change of parameters or settings
     nx_field_desc field{};
     nx_settings st{};
@@ -160,6 +161,8 @@ struct nx_frame {
     DevBuf base64;               // fp64 base kept for render_backward
     DevBuf residual64;           // fp64 terminal transmittance, kept with base64
     DevBuf tex_f;                // texture features (split tensor-core texture pass)
+    DevBuf texture64, final64;   // fp64 texture / final (NX_PRECISION_F64 renders)
+    bool f64 = false;            // the last collection pass rendered an NX_PRECISION_F64 scene
     bool keep_backward = false;  // collection passes write base64
     bool base64_valid = false;   // base64 holds the last forward's (or an uploaded) base
     DevBuf tile_offsets;  // n_tiles + 1 (the work lists' ranges of the last collection pass)
@@ -228,6 +231,8 @@ int validate_settings(nx_ctx* c, const nx_settings& s) {
     if (!(s.alpha_max > 0) || s.alpha_max >= 1) return set_err(c, NX_BAD_SETTINGS, "alpha_max must be in (0,1)");
     if (!(s.min_transmittance >= 0)) return set_err(c, NX_BAD_SETTINGS, "min_transmittance must be >= 0");
     if (s.tile < 1) return set_err(c, NX_BAD_SETTINGS, "tile must be >= 1");
+    if (s.precision != NX_PRECISION_DEFAULT && s.precision != NX_PRECISION_F64)
+        return set_err(c, NX_BAD_SETTINGS, "precision must be NX_PRECISION_DEFAULT or NX_PRECISION_F64");
     return NX_OK;
 }
 
@@ -292,9 +297,13 @@ int frame_shape(nx_ctx* c, nx_frame* f, int W, int H, int K, int tile) {
     NX_CUDA(c, f->depths.ensure(ns * sizeof(double)));
     NX_CUDA(c, f->weights.ensure(ns * sizeof(double)));
     NX_CUDA(c, f->texture.ensure(ns * 3 * sizeof(float)));
-    if (f->keep_backward) {
+    if (f->keep_backward || f->f64) {
         NX_CUDA(c, f->base64.ensure(npix * 3 * sizeof(double)));
         NX_CUDA(c, f->residual64.ensure(npix * sizeof(double)));
+    }
+    if (f->f64) {
+        NX_CUDA(c, f->texture64.ensure(ns * 3 * sizeof(double)));
+        NX_CUDA(c, f->final64.ensure(npix * 3 * sizeof(double)));
     }
     f->W = W;
     f->H = H;
@@ -318,8 +327,10 @@ FrameDev frame_dev(const nx_frame* f) {
     d.texture = f->texture.as<float>();
     d.final_img = f->final_img.as<float>();
     d.residual = f->residual.as<float>();
-    d.base64 = f->keep_backward ? f->base64.as<double>() : nullptr;
-    d.residual64 = f->keep_backward ? f->residual64.as<double>() : nullptr;
+    d.base64 = (f->keep_backward || f->f64) ? f->base64.as<double>() : nullptr;
+    d.residual64 = (f->keep_backward || f->f64) ? f->residual64.as<double>() : nullptr;
+    d.texture64 = f->f64 ? f->texture64.as<double>() : nullptr;
+    d.final64 = f->f64 ? f->final64.as<double>() : nullptr;
     return d;
 }
 
@@ -333,6 +344,12 @@ SceneDev scene_dev(const nx_scene* s) {
     d.w2 = s->w2.as<float>();
     d.w3 = s->w3.as<float>();
     d.field = s->field;
+    const bool f64 = s->st.precision == NX_PRECISION_F64 && s->sh64.p;
+    d.sh64 = f64 ? s->sh64.as<double>() : nullptr;
+    d.table64 = f64 ? s->table64.as<double>() : nullptr;
+    d.w1_64 = f64 ? s->w1_64.as<double>() : nullptr;
+    d.w2_64 = f64 ? s->w2_64.as<double>() : nullptr;
+    d.w3_64 = f64 ? s->w3_64.as<double>() : nullptr;
     return d;
 }
 
@@ -583,6 +600,7 @@ int collection(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame*
     if ((st = check_inputs(c, scene, cam, s))) return st;
     // the frame may still be read by its previous texture pass / download (second stream)
     if (f->busy_pending) NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_busy, 0));
+    f->f64 = scene->st.precision == NX_PRECISION_F64;
     if ((st = frame_shape(c, f, cam->width, cam->height, scene->st.top_k, scene->st.tile))) return st;
     f->n_nexels = scene->n;
     int64_t total = 0;
@@ -609,8 +627,9 @@ int collection(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame*
     ca.dbg_y1 = dbg_y1;
     ca.dbg_max = dbg_max;
     ca.stats = f->stats;
+    ca.sh64 = scene_dev(scene).sh64;
     launch_composite(ca, s);
-    f->base64_valid = f->keep_backward;
+    f->base64_valid = f->keep_backward || f->f64;
     record(c, kEvCompEnd, s);
     NX_CUDA(c, cudaEventRecord(f->ev_ready, s));
     NX_CUDA(c, cudaGetLastError());
@@ -621,6 +640,12 @@ int texturing(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* 
     if (f->W != cam->width || f->H != cam->height)
         return set_err(c, NX_INVALID_ARGUMENT, "frame does not match the camera (run collection_pass first)");
     NX_CUDA(c, cudaStreamWaitEvent(s, f->ev_ready, 0));  // no-op on the collection's own stream
+    if (scene->st.precision == NX_PRECISION_F64 && !f->f64) {  // e.g. a frame uploaded from host buffers
+        if (!f->base64_valid)
+            return set_err(c, NX_INVALID_ARGUMENT, "NX_PRECISION_F64 texturing needs the frame's fp64 base");
+        f->f64 = true;
+        if (const int st = frame_shape(c, f, f->W, f->H, f->K, scene->st.tile)) return st;
+    }
     record(c, kEvTex, s);
     TextureArgs ta;
     ta.scene = scene_dev(scene);
@@ -630,7 +655,7 @@ int texturing(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame* 
     ta.stats = f->stats;
     ta.fscratch = nullptr;
     ta.ev_mid = c->profiling ? c->ev[c->ev_cur][kEvTexMid] : nullptr;  // recorded between gathers and decoder
-    if (texture_tc_supported(scene->st.top_k > 0 ? scene->field : nx_field_desc{}) && f->K > 0) {
+    if (texture_tc_supported(scene->st.top_k > 0 ? scene->field : nx_field_desc{}) && f->K > 0 && !f->f64) {
         const size_t bytes = texture_tc_scratch_bytes(f->W, f->H, f->K);
         if (bytes) {
             if (bytes > f->tex_f.cap) {  // zeroed once: padding rows of the tiles are never written
@@ -860,6 +885,21 @@ int nx_scene_create(nx_ctx* c, const nx_settings* settings, int64_t n, const dou
     if (e == cudaSuccess) e = upload_f32(s->w1, w1, nh * n_in);
     if (e == cudaSuccess) e = upload_f32(s->w2, w2, nh * nh);
     if (e == cudaSuccess) e = upload_f32(s->w3, w3, NX_SH_VALUES * nh);
+    if (settings->precision == NX_PRECISION_F64) {  // fp64 copies of everything the colour path reads
+        std::vector<double> sh64(static_cast<size_t>(NX_SH_VALUES * nn), 0.0);
+        for (int64_t i = 0; i < n; ++i)
+            for (int k = 0; k < NX_SH_VALUES; ++k) sh64[i * NX_SH_VALUES + k] = nexels[i * NX_PARAMS_PER_NEXEL + 12 + k];
+        auto up64 = [&](DevBuf& b, const double* src, size_t count) -> cudaError_t {
+            cudaError_t e2 = b.ensure(std::max<size_t>(count, 1) * sizeof(double));
+            if (e2 == cudaSuccess && count) e2 = cudaMemcpy(b.p, src, count * sizeof(double), cudaMemcpyHostToDevice);
+            return e2;
+        };
+        if (e == cudaSuccess) e = up64(s->sh64, sh64.data(), sh64.size());
+        if (e == cudaSuccess) e = up64(s->table64, table, n_table);
+        if (e == cudaSuccess) e = up64(s->w1_64, w1, nh * n_in);
+        if (e == cudaSuccess) e = up64(s->w2_64, w2, nh * nh);
+        if (e == cudaSuccess) e = up64(s->w3_64, w3, NX_SH_VALUES * nh);
+    }
     // pageable cudaMemcpy may return before its DMA lands, and the context's
     // non-blocking streams do not order after the legacy stream: finish it here
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -953,6 +993,8 @@ int nx_scene_load_nexl(nx_ctx* c, const char* path, nx_scene** out, nx_nexl_info
 
 int nx_scene_set_settings(nx_ctx* c, nx_scene* s, const nx_settings* settings) {
     if (!s || !settings) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    if (settings->precision == NX_PRECISION_F64 && !s->sh64.p)
+        return set_err(c, NX_UNSUPPORTED, "NX_PRECISION_F64 needs a scene created with it (fp64 copies)");
     if (std::memcmp(&s->st, settings, sizeof(nx_settings)) != 0) s->version = next_scene_version();
     s->st = *settings;
     return NX_OK;
@@ -968,7 +1010,9 @@ void nx_scene_destroy(nx_scene* s) {
     if (!s) return;
     scene_alive(s, false);
     cudaSetDevice(s->device);
-    for (DevBuf* b : {&s->geom, &s->sh, &s->table, &s->w1, &s->w2, &s->w3, &s->geom_spare, &s->sh_spare}) b->release();
+    for (DevBuf* b : {&s->geom, &s->sh, &s->table, &s->w1, &s->w2, &s->w3, &s->geom_spare, &s->sh_spare, &s->sh64,
+                      &s->table64, &s->w1_64, &s->w2_64, &s->w3_64})
+        b->release();
     delete s;
 }
 
@@ -1007,7 +1051,7 @@ void nx_frame_destroy(nx_frame* f) {
     cudaSetDevice(f->device);
     if (f->ev_busy) cudaEventSynchronize(f->ev_busy);  // texture pass / download still reading it
     for (DevBuf* b : {&f->base, &f->ids, &f->depths, &f->weights, &f->texture, &f->final_img, &f->residual,
-                      &f->tile_offsets, &f->base64, &f->residual64, &f->tex_f})
+                      &f->tile_offsets, &f->base64, &f->residual64, &f->tex_f, &f->texture64, &f->final64})
         b->release();
     if (f->stats) cudaFree(f->stats);
     if (f->ev_ready) cudaEventDestroy(f->ev_ready);
@@ -1077,6 +1121,8 @@ int nx_frame_download(nx_ctx* c, const nx_frame* fc, const nx_host_frame* dst, v
     NX_CUDA(c, cp(dst->residual, f->residual, npix * sizeof(float)));
     if (dst->base_f64 && f->base64_valid) NX_CUDA(c, cp(dst->base_f64, f->base64, npix * 3 * sizeof(double)));
     if (dst->residual_f64 && f->base64_valid) NX_CUDA(c, cp(dst->residual_f64, f->residual64, npix * sizeof(double)));
+    if (dst->texture_f64 && f->f64) NX_CUDA(c, cp(dst->texture_f64, f->texture64, ns * 3 * sizeof(double)));
+    if (dst->final_f64 && f->f64) NX_CUDA(c, cp(dst->final_f64, f->final64, npix * 3 * sizeof(double)));
     launch_stream_copy(jobs, s);
     NX_CUDA(c, cudaGetLastError());
     NX_CUDA(c, cudaEventRecord(f->ev_busy, s));
@@ -1479,6 +1525,7 @@ extern "C" {
 
 int nx_optimizer_create(nx_ctx* c, const nx_scene* scene, nx_optimizer** out) {
     if (!c || !scene || !out) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    if (scene->sh64.p) return set_err(c, NX_UNSUPPORTED, "NX_PRECISION_F64 scenes are render-only (no optimizer)");
     cudaSetDevice(c->device);
     nx_optimizer* o = new (std::nothrow) nx_optimizer;
     if (!o) return set_err(c, NX_OUT_OF_MEMORY, "host allocation");
@@ -1677,6 +1724,7 @@ int apply_row_map(nx_ctx* c, nx_scene* scene, nx_optimizer* opt, int64_t n_new, 
 int nx_scene_prune(nx_ctx* c, nx_scene* scene, nx_optimizer* opt, double min_opacity, int32_t* new_to_old,
                    int64_t* n_out) {
     if (!c || !scene) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    if (scene->sh64.p) return set_err(c, NX_UNSUPPORTED, "NX_PRECISION_F64 scenes are render-only (no pruning)");
     if (opt && opt->n != scene->n) return set_err(c, NX_INVALID_ARGUMENT, "prune: optimizer and scene disagree");
     cudaSetDevice(c->device);
     cudaStream_t s = c->stream;
@@ -1707,6 +1755,7 @@ int nx_scene_densify_split(nx_ctx* c, nx_scene* scene, nx_optimizer* opt, const 
                            const double* uniforms, int64_t budget, double split_fraction, int32_t* new_to_old,
                            int64_t* n_out, int64_t* split_count) {
     if (!c || !scene || !errors || !uniforms) return set_err(c, NX_INVALID_ARGUMENT, "null argument");
+    if (scene->sh64.p) return set_err(c, NX_UNSUPPORTED, "NX_PRECISION_F64 scenes are render-only (no densify)");
     if (opt && opt->n != scene->n) return set_err(c, NX_INVALID_ARGUMENT, "densify: optimizer and scene disagree");
     cudaSetDevice(c->device);
     cudaStream_t s = c->stream;

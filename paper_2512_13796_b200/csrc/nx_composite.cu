@@ -49,26 +49,29 @@ static_assert(kWorkTile == 8, "warp blocks are 8x4 pixels");
 constexpr bool kNear = NX_NEAR_COUNTERS;  // near-threshold decision counters (FrameStatsD::near)
 static_assert(kChunk <= 256 && kSub <= 8, "pool entries pack (lane, group slot) in 16 bits");
 
-struct PoolEntry {  // one evaluated (pixel, primitive) pair
-    double alpha;   // raw kernel alpha, < 0 for a miss
-    double t;       // plane crossing
-    float rgb[3];   // primitive colour along the ray
+template <typename CT>  // colour type: float, or double for NX_PRECISION_F64
+struct PoolEntry {         // one evaluated (pixel, primitive) pair
+    double alpha;          // raw kernel alpha, < 0 for a miss
+    double t;              // plane crossing
+    CT rgb[3];             // primitive colour along the ray
     int32_t id;
 };
 
+template <typename CT>
 struct WarpStage {  // one warp's private staging
     double rec[kSub][REC_FIELDS];    // exact records of the group's primitives
-    float sh[kSub][NX_SH_VALUES];    // and their SH coefficients
+    float sh[kSub][NX_SH_VALUES];    // and their SH coefficients (fp32 colour path)
     uint8_t sel[kChunk];             // chunk slots whose pixel rect meets the warp's block
     uint16_t q[kPool];
-    PoolEntry res[kPool];
+    PoolEntry<CT> res[kPool];
 };
 
+template <typename CT>
 struct SmemLayout {
     float4 f[kChunk][4];
     int32_t id[kChunk];
     double dir[kThreads][3];
-    WarpStage w[kWarps];
+    WarpStage<CT> w[kWarps];
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -97,7 +100,7 @@ __device__ __forceinline__ void eval_sh_smem(const float* sh, float x, float y, 
     rgb[2] = fmaxf(a2, 0.f);
 }
 
-template <int K, bool kDebug>
+template <int K, bool kDebug, typename CT>
 #ifndef NX_COMPOSITE_MINB
 #define NX_COMPOSITE_MINB 10
 #endif
@@ -105,15 +108,16 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
     constexpr int KK = K > 0 ? K : 1;
     constexpr bool kKeepRgb = K <= 4;  // top-K slots remember their colour (else re-evaluated at the end)
     constexpr int KR = kKeepRgb ? KK : 1;
+    constexpr bool kF64 = sizeof(CT) == 8;  // NX_PRECISION_F64: fp64 SH colour from the fp64 copy
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    SmemLayout& sm = *reinterpret_cast<SmemLayout*>(smem_raw);
+    SmemLayout<CT>& sm = *reinterpret_cast<SmemLayout<CT>*>(smem_raw);
 
     const int t = blockIdx.x;
     const int tx = t % a.fb.tiles_x, ty = t / a.fb.tiles_x;
     const int list_begin = a.tile_offsets[t], list_end = a.tile_offsets[t + 1];
     const int W = a.cam.W, H = a.cam.H;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WarpStage& ws = sm.w[warp];
+    WarpStage<CT>& ws = sm.w[warp];
     const double near_eps = a.st.near_eps, alpha_max = a.st.alpha_max, min_T = a.st.min_transmittance;
     const float near_eps_f = static_cast<float>(near_eps);
 
@@ -136,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
     int32_t k_id[KK];
     double k_w[KK], k_t[KK];
     uint32_t k_seq[KK];
-    float k_rgb[KR][3];
+    CT k_rgb[KR][3];
 #pragma unroll
     for (int s = 0; s < KK; ++s) {
         k_id[s] = -1;
@@ -145,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
         k_seq[s] = 0;
     }
 #pragma unroll
-    for (int s = 0; s < KR; ++s) k_rgb[s][0] = k_rgb[s][1] = k_rgb[s][2] = 0.f;
+    for (int s = 0; s < KR; ++s) k_rgb[s][0] = k_rgb[s][1] = k_rgb[s][2] = CT(0);
     int k_size = 0;
     uint32_t counter = 0;
     bool active = in_img;
@@ -191,8 +195,9 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
             for (int g0 = 0; g0 < nsel; g0 += kSub) {
                 const int gn = min(kSub, nsel - g0);
                 // ---- S. stage the group's exact records + SH coefficients (asynchronous)
-                for (int e = lane; e < gn * (kRecPieces + kShPieces); e += 32) {
-                    const int b = e / (kRecPieces + kShPieces), pc = e - b * (kRecPieces + kShPieces);
+                constexpr int kPieces = kRecPieces + (kF64 ? 0 : kShPieces);
+                for (int e = lane; e < gn * kPieces; e += 32) {
+                    const int b = e / kPieces, pc = e - b * kPieces;
                     const int64_t id = sm.id[ws.sel[g0 + b]];
                     if (pc < kRecPieces)
                         cp_async16(reinterpret_cast<float4*>(ws.rec[b]) + pc,
@@ -248,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                     const double* dd = sm.dir[warp * 32 + owner];
                     const double d0 = dd[0], d1 = dd[1], d2 = dd[2];
                     const double* r = ws.rec[b];
-                    PoolEntry res;
+                    PoolEntry<CT> res;
                     res.alpha = -1.0;
                     res.t = 0.0;
                     res.id = sm.id[ws.sel[g0 + b]];
@@ -258,15 +263,21 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                     if (h.alpha >= 0.0) {
                         res.alpha = h.alpha;
                         res.t = h.t;
-                        eval_sh_smem(ws.sh[b], static_cast<float>(d0), static_cast<float>(d1), static_cast<float>(d2),
-                                     a.sh_degree, res.rgb);
+                        if constexpr (kF64) {
+                            const double dd3[3] = {d0, d1, d2};
+                            eval_sh_f64(a.sh64 + static_cast<int64_t>(res.id) * NX_SH_VALUES, dd3, a.sh_degree,
+                                        res.rgb);
+                        } else {
+                            eval_sh_smem(ws.sh[b], static_cast<float>(d0), static_cast<float>(d1),
+                                         static_cast<float>(d2), a.sh_degree, res.rgb);
+                        }
                     }
                     ws.res[e] = res;
                 }
                 __syncwarp();
                 // ---- B2. per-pixel compositing of this lane's hits, in list order (renderer.cpp:144-153)
                 for (int k = off; k < off + cnt && active; ++k) {
-                    const PoolEntry& res = ws.res[k];
+                    const PoolEntry<CT>& res = ws.res[k];
                     if (res.alpha < 0.0) continue;
                     const int32_t id = res.id;
                     const double alpha = alpha_max < res.alpha ? alpha_max : res.alpha;
@@ -355,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                         if (kKeepRgb) {
 #pragma unroll
                             for (int c = 0; c < 3; ++c) {
-                                const float tc = k_rgb[j % KR][c];
+                                const CT tc = k_rgb[j % KR][c];
                                 k_rgb[j % KR][c] = k_rgb[(j + 1) % KR][c];
                                 k_rgb[(j + 1) % KR][c] = tc;
                             }
@@ -370,11 +381,13 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                 a.fb.depths[sl] = k_t[j];
                 a.fb.weights[sl] = k_w[j];
                 if (j < k_size) {
-                    float col[3];
+                    CT col[3];
                     if (kKeepRgb) {
                         col[0] = k_rgb[j % KR][0];
                         col[1] = k_rgb[j % KR][1];
                         col[2] = k_rgb[j % KR][2];
+                    } else if constexpr (kF64) {
+                        eval_sh_f64(a.sh64 + static_cast<int64_t>(k_id[j]) * NX_SH_VALUES, dir, a.sh_degree, col);
                     } else {
                         eval_sh_f32(a.sh + static_cast<int64_t>(k_id[j]) * NX_SH_VALUES, dfx, dfy, dfz, a.sh_degree,
                                     col);
@@ -405,9 +418,17 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
 
 template <int K, bool kDebug>
 void launch_one(const CompositeArgs& a, unsigned grid, cudaStream_t s) {
-    const size_t smem = sizeof(SmemLayout);
-    cudaFuncSetAttribute(composite_kernel<K, kDebug>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    composite_kernel<K, kDebug><<<grid, kThreads, smem, s>>>(a);
+    if (a.sh64) {
+        const size_t smem = sizeof(SmemLayout<double>);
+        cudaFuncSetAttribute(composite_kernel<K, kDebug, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        composite_kernel<K, kDebug, double><<<grid, kThreads, smem, s>>>(a);
+        return;
+    }
+    const size_t smem = sizeof(SmemLayout<float>);
+    cudaFuncSetAttribute(composite_kernel<K, kDebug, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    composite_kernel<K, kDebug, float><<<grid, kThreads, smem, s>>>(a);
 }
 
 template <bool kDebug>

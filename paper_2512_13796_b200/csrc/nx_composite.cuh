@@ -62,6 +62,36 @@ __device__ __forceinline__ void eval_sh_f32(const float* __restrict__ sh, float 
     rgb[2] = fmaxf(a2, 0.f);
 }
 
+// sh_basis + eval_sh (sh.hpp:11-57) in fp64, the reference's operation order
+// (acc = 0.5, then acc += coeff_k * basis_k for k = 0, 1, ...): the NX_PRECISION_F64 colour.
+__device__ __forceinline__ void eval_sh_f64(const double* sh, const double* d, int degree, double* rgb) {
+    double b[16];
+    const double x = d[0], y = d[1], z = d[2];
+    const double xx = x * x, yy = y * y, zz = z * z;
+    b[0] = 0.28209479177387814;
+    b[1] = -0.4886025119029199 * y;
+    b[2] = 0.4886025119029199 * z;
+    b[3] = -0.4886025119029199 * x;
+    b[4] = 1.0925484305920792 * x * y;
+    b[5] = -1.0925484305920792 * y * z;
+    b[6] = 0.31539156525252005 * (2.0 * zz - xx - yy);
+    b[7] = -1.0925484305920792 * x * z;
+    b[8] = 0.5462742152960396 * (xx - yy);
+    b[9] = -0.5900435899266435 * y * (3.0 * xx - yy);
+    b[10] = 2.890611442640554 * x * y * z;
+    b[11] = -0.4570457994644658 * y * (4.0 * zz - xx - yy);
+    b[12] = 0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+    b[13] = -0.4570457994644658 * x * (4.0 * zz - xx - yy);
+    b[14] = 1.445305721320277 * z * (xx - yy);
+    b[15] = -0.5900435899266435 * x * (xx - 3.0 * yy);
+    const int n = degree >= 3 ? 16 : 1;
+    for (int c = 0; c < 3; ++c) {
+        double acc = 0.5;
+        for (int k = 0; k < n; ++k) acc += sh[k * 3 + c] * b[k];
+        rgb[c] = acc < 0.0 ? 0.0 : acc;
+    }
+}
+
 // fp32 conservative prefilter: false only if the exact test provably misses
 // (t <= near_eps, or |u| > ru, or |v| > rv).
 __device__ __forceinline__ bool prefilter(const float4* f, float dfx, float dfy, float dfz, float near_eps_f) {

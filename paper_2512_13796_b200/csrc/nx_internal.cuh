@@ -169,6 +169,12 @@ struct SceneDev {
     const float* w2;     // hidden x hidden
     const float* w3;     // 48 x hidden
     nx_field_desc field;
+    // NX_PRECISION_F64 scenes: fp64 copies of the colour inputs (else nullptr)
+    const double* sh64 = nullptr;
+    const double* table64 = nullptr;
+    const double* w1_64 = nullptr;
+    const double* w2_64 = nullptr;
+    const double* w3_64 = nullptr;
 };
 
 struct FrameDev {
@@ -182,6 +188,8 @@ struct FrameDev {
     float* residual;
     double* residual64;  // fp64 terminal transmittance (nullptr unless the frame keeps backward state)
     double* base64;  // optional fp64 base (backward state), nullptr if not kept
+    double* texture64 = nullptr;  // NX_PRECISION_F64: fp64 texture / final
+    double* final64 = nullptr;
 };
 
 // Host-side count of kernel launches issued by this library (all contexts).
@@ -243,6 +251,7 @@ struct CompositeArgs {
     int32_t* dbg_counts;
     int dbg_y0, dbg_y1, dbg_max;
     FrameStatsD* stats;  // near-threshold counters
+    const double* sh64 = nullptr;  // NX_PRECISION_F64: fp64 SH (the colour path runs in fp64)
 };
 void launch_composite(const CompositeArgs& a, cudaStream_t s);
 

@@ -16,7 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 
-#include "nx_internal.cuh"
+#include "nx_composite.cuh"
 
 namespace nx {
 
@@ -238,10 +238,129 @@ void launch_tex(const TextureArgs& a, cudaStream_t s) {
     texture_kernel<NIN, NH, F><<<blocks, threads, smem, s>>>(a);
 }
 
+
+// ---------------------------------------------------------------- NX_PRECISION_F64
+// texturing_pass (renderer.cpp:207-237) at the reference's precision: one thread per
+// pixel; per buffered slot the query of build_queries (renderer.cpp:177-203), grid_lookup
+// (hash_grid.cpp:26-83) on the fp64 table, TextureMlp::forward (mlp.cpp:24-43) on the
+// fp64 weights, eval_sh (sh.hpp:46-57) in fp64, then Eq. 7 on the fp64 base. The
+// reference's operation order throughout (its decoder sums are reassociated by its
+// compiler flags, so the last bits may differ: ~1e-16 relative).
+constexpr int kF64MaxIn = 64, kF64MaxHidden = 128;
+
+__device__ __forceinline__ uint32_t f64_map_positive(long long x) {  // hash_grid.hpp:12-14
+    return x > 0 ? static_cast<uint32_t>(2 * x - 1) : static_cast<uint32_t>(-2 * x);
+}
+
+__global__ void __launch_bounds__(64) texture_f64_kernel(const TextureArgs a) {
+    const int64_t npix = static_cast<int64_t>(a.cam.W) * a.cam.H;
+    const int64_t pix = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (pix >= npix) return;
+    const int K = a.fb.K;
+    const nx_field_desc& fd = a.scene.field;
+    const int L = fd.levels, F = fd.features, nin = L * F, nh = fd.n_hidden;
+    const uint32_t T = 1u << fd.log2_table, mask = T - 1u;
+    const int px = static_cast<int>(pix % a.cam.W), py = static_cast<int>(pix / a.cam.W);
+    double dir[3];
+    pixel_dir(a.cam, px + 0.5, py + 0.5, dir);
+    double acc[3] = {a.fb.base64[pix * 3 + 0], a.fb.base64[pix * 3 + 1], a.fb.base64[pix * 3 + 2]};
+    int n_q = 0;
+    for (int j = 0; j < K; ++j) {
+        const int64_t sl = pix * K + j;
+        if (a.fb.ids[sl] < 0) {
+            for (int c = 0; c < 3; ++c) {
+                a.fb.texture64[sl * 3 + c] = 0.0;
+                a.fb.texture[sl * 3 + c] = 0.f;
+            }
+            continue;
+        }
+        ++n_q;
+        const double t = a.fb.depths[sl];
+        const double x[3] = {a.cam.o[0] + t * dir[0], a.cam.o[1] + t * dir[1], a.cam.o[2] + t * dir[2]};
+        const double f = a.cam.fx;
+        double feats[kF64MaxIn];
+        double s = fd.base_scale;
+        for (int l = 0; l < L; ++l, s *= fd.growth) {
+            const double p0 = s * x[0], p1 = s * x[1], p2 = s * x[2];
+            const double fl0 = floor(p0), fl1 = floor(p1), fl2 = floor(p2);
+            const long long b0 = static_cast<long long>(fl0), b1 = static_cast<long long>(fl1),
+                            b2 = static_cast<long long>(fl2);
+            const double fr[3] = {p0 - fl0, p1 - fl1, p2 - fl2};
+            double dw = 1.0;
+            if (!a.st.no_downweight) {  // downweight (hash_grid.hpp:28-31)
+                const double r = f / (s * t);
+                dw = 1.0 - exp(-r * r / (2.0 * M_PI));
+            }
+            const double wx[2] = {1.0 - fr[0], fr[0]}, wy[2] = {1.0 - fr[1], fr[1]}, wz[2] = {1.0 - fr[2], fr[2]};
+            for (int fi = 0; fi < F; ++fi) feats[l * F + fi] = 0.0;
+            const size_t slab = static_cast<size_t>(l) * T;
+            for (int ci = 0; ci < 8; ++ci) {
+                const uint32_t row = (f64_map_positive(b0 + (ci & 1)) ^
+                                      (f64_map_positive(b1 + ((ci >> 1) & 1)) * 2654435761u) ^
+                                      (f64_map_positive(b2 + ((ci >> 2) & 1)) * 805459861u)) & mask;
+                const double w = wx[ci & 1] * wy[(ci >> 1) & 1] * wz[(ci >> 2) & 1];
+                const double* feat = a.scene.table64 + (slab + row) * F;
+                for (int fi = 0; fi < F; ++fi) feats[l * F + fi] += w * __ldg(feat + fi);
+            }
+            for (int fi = 0; fi < F; ++fi) feats[l * F + fi] *= dw;
+        }
+        double h1[kF64MaxHidden], h2[kF64MaxHidden], y[NX_SH_VALUES];
+        for (int o = 0; o < nh; ++o) {
+            double v = 0.0;
+            for (int i = 0; i < nin; ++i) v += __ldg(a.scene.w1_64 + o * nin + i) * feats[i];
+            h1[o] = v > 0.0 ? v : 0.0;
+        }
+        for (int o = 0; o < nh; ++o) {
+            double v = 0.0;
+            for (int i = 0; i < nh; ++i) v += __ldg(a.scene.w2_64 + o * nh + i) * h1[i];
+            h2[o] = v > 0.0 ? v : 0.0;
+        }
+        for (int o = 0; o < NX_SH_VALUES; ++o) {
+            double v = 0.0;
+            for (int i = 0; i < nh; ++i) v += __ldg(a.scene.w3_64 + o * nh + i) * h2[i];
+            y[o] = v;
+        }
+        double rgb[3];
+        eval_sh_f64(y, dir, 3, rgb);  // field_forward: always degree 3 (texture_field.cpp:33)
+        const double w = a.fb.weights[sl];
+        for (int c = 0; c < 3; ++c) {
+            a.fb.texture64[sl * 3 + c] = rgb[c];
+            a.fb.texture[sl * 3 + c] = static_cast<float>(rgb[c]);
+            acc[c] += w * rgb[c];
+        }
+    }
+    for (int c = 0; c < 3; ++c) {
+        a.fb.final64[pix * 3 + c] = acc[c];
+        a.fb.final_img[pix * 3 + c] = static_cast<float>(acc[c]);
+    }
+    if (n_q) atomicAdd(&a.stats->queries, static_cast<unsigned long long>(n_q));
+}
+
+__global__ void copy_base64_kernel(const double* base64, const float* base, double* final64, float* final_img,
+                                   int64_t n) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) {
+        final64[i] = base64[i];
+        final_img[i] = base[i];
+    }
+}
+
 }  // namespace
 
 int launch_texture(const TextureArgs& a, cudaStream_t s) {
     const int64_t npix = static_cast<int64_t>(a.cam.W) * a.cam.H;
+    if (a.fb.final64 && a.scene.table64) {  // NX_PRECISION_F64 render
+        if (npix == 0) return NX_OK;
+        const nx_field_desc& fd = a.scene.field;
+        if (fd.levels * fd.features > kF64MaxIn || fd.n_hidden > kF64MaxHidden) return NX_UNSUPPORTED;
+        count_launch();
+        if (a.fb.K == 0)
+            copy_base64_kernel<<<static_cast<unsigned>((npix * 3 + 255) / 256), 256, 0, s>>>(
+                a.fb.base64, a.fb.base, a.fb.final64, a.fb.final_img, npix * 3);
+        else
+            texture_f64_kernel<<<static_cast<unsigned>((npix + 63) / 64), 64, 0, s>>>(a);
+        return NX_OK;
+    }
     if (a.fb.K == 0) {
         if (npix * 3 > 0)
             count_launch(), copy_base_kernel<<<static_cast<unsigned>((npix * 3 + 255) / 256), 256, 0, s>>>(a.fb.base, a.fb.final_img,

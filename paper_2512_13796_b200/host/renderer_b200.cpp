@@ -226,6 +226,14 @@ nx_settings to_nx(const RenderSettings& r) {
     s.no_gamma = r.no_gamma;
     s.no_prim_sh = r.no_prim_sh;
     s.no_downweight = r.no_downweight;
+    // The reference API returns FrameBuffers in doubles: the drop-in renders its colours
+    // at that precision (NX_PRECISION_F64: fp64 SH / hash grid / decoder / base / texture /
+    // final); NEXEL_DROPIN_PRECISION=f32 selects the fp32-colour / tensor-core path.
+    static const bool f32 = [] {
+        const char* e = std::getenv("NEXEL_DROPIN_PRECISION");
+        return e && std::strcmp(e, "f32") == 0;
+    }();
+    s.precision = f32 ? NX_PRECISION_DEFAULT : NX_PRECISION_F64;
     return s;
 }
 
@@ -320,6 +328,7 @@ void texture(Device& d, const Scene& scene, const Camera& cam, FrameBuffers& fb)
         std::vector<float> base(fb.base.begin(), fb.base.end());
         nx_host_frame h{};
         h.base = base.data();
+        h.base_f64 = const_cast<double*>(fb.base.data());  // the fp64 base Eq. 7 starts from
         h.ids = fb.ids.data();
         h.depths = fb.depths.data();
         h.weights = fb.weights.data();
@@ -327,17 +336,26 @@ void texture(Device& d, const Scene& scene, const Camera& cam, FrameBuffers& fb)
     }
     const nx_camera c = to_nx(cam);
     check(d, nx_texturing_pass(d.ctx, d.scene, &c, d.frame, nullptr));
-    (void)scene;
-    (void)npix;
     const size_t ns = npix * fb.top_k;
-    unsigned char* st = d.staging.get((ns + npix) * 3 * sizeof(float));
+    const bool f64 = to_nx(scene.settings).precision == NX_PRECISION_F64;
+    unsigned char* st = d.staging.get((ns + npix) * 3 * sizeof(double));
     nx_host_frame h{};
-    h.texture = reinterpret_cast<float*>(st);
-    h.final_img = reinterpret_cast<float*>(st) + ns * 3;
+    if (f64) {
+        h.texture_f64 = reinterpret_cast<double*>(st);
+        h.final_f64 = reinterpret_cast<double*>(st) + ns * 3;
+    } else {
+        h.texture = reinterpret_cast<float*>(st);
+        h.final_img = reinterpret_cast<float*>(st) + ns * 3;
+    }
     check(d, nx_frame_download(d.ctx, d.frame, &h, nullptr));
     check(d, nx_ctx_synchronize(d.ctx));
-    widen_into(h.texture, fb.texture.data(), ns * 3);
-    widen_into(h.final_img, fb.final_img.data(), npix * 3);
+    if (f64) {
+        widen_into(h.texture_f64, fb.texture.data(), ns * 3);
+        widen_into(h.final_f64, fb.final_img.data(), npix * 3);
+    } else {
+        widen_into(h.texture, fb.texture.data(), ns * 3);
+        widen_into(h.final_img, fb.final_img.data(), npix * 3);
+    }
 }
 
 }  // namespace
@@ -390,8 +408,10 @@ RenderResult render(const Scene& scene, const Camera& cam) {
     check(d, nx_collection_pass(d.ctx, d.scene, &c, d.frame, nullptr));
     if (K > 0) check(d, nx_texturing_pass(d.ctx, d.scene, &c, d.frame, nullptr));
     // staging: fp64 base, fp64 residual, depths, weights, ids, then fp32 texture, final
-    const size_t b_base = npix * 3 * 8, b_res = npix * 8, b_dw = ns * 8, b_ids = ns * 4, b_tex = ns * 3 * 4,
-                 b_fin = npix * 3 * 4;
+    const bool f64 = to_nx(scene.settings).precision == NX_PRECISION_F64;
+    const size_t cs = f64 ? 8 : 4;  // colour element size of the texture / final download
+    const size_t b_base = npix * 3 * 8, b_res = npix * 8, b_dw = ns * 8, b_ids = ns * 4, b_tex = ns * 3 * cs,
+                 b_fin = npix * 3 * cs;
     unsigned char* st = d.staging.get(b_base + b_res + 2 * b_dw + b_ids + b_tex + b_fin);
     nx_host_frame h{};
     h.base_f64 = reinterpret_cast<double*>(st);
@@ -399,9 +419,16 @@ RenderResult render(const Scene& scene, const Camera& cam) {
     h.depths = reinterpret_cast<double*>(st + b_base + b_res);
     h.weights = reinterpret_cast<double*>(st + b_base + b_res + b_dw);
     h.ids = reinterpret_cast<int32_t*>(st + b_base + b_res + 2 * b_dw);
+    void* tex_st = st + b_base + b_res + 2 * b_dw + b_ids;
+    void* fin_st = st + b_base + b_res + 2 * b_dw + b_ids + b_tex;
     if (K > 0) {
-        h.texture = reinterpret_cast<float*>(st + b_base + b_res + 2 * b_dw + b_ids);
-        h.final_img = reinterpret_cast<float*>(st + b_base + b_res + 2 * b_dw + b_ids + b_tex);
+        if (f64) {
+            h.texture_f64 = static_cast<double*>(tex_st);
+            h.final_f64 = static_cast<double*>(fin_st);
+        } else {
+            h.texture = static_cast<float*>(tex_st);
+            h.final_img = static_cast<float*>(fin_st);
+        }
     }
     check(d, nx_frame_download(d.ctx, d.frame, &h, nullptr));
     const auto t2 = clk::now();
@@ -422,8 +449,8 @@ RenderResult render(const Scene& scene, const Camera& cam) {
                                {h.weights, fb.weights.data(), ns, 0},
                                {h.ids, fb.ids.data(), ns, 1}};
     if (K > 0) {
-        parts.push_back({h.texture, fb.texture.data(), ns * 3, 2});
-        parts.push_back({h.final_img, fb.final_img.data(), npix * 3, 2});
+        parts.push_back({tex_st, fb.texture.data(), ns * 3, f64 ? 0 : 2});
+        parts.push_back({fin_st, fb.final_img.data(), npix * 3, f64 ? 0 : 2});
     }
     size_t total = 0;
     for (const Part& p : parts) total += p.n;
