@@ -294,16 +294,28 @@ __global__ void emit_kernel(const uint32_t* ids, const int32_t* offsets, int64_t
                             const int32_t* n_sorted_dev, int64_t key_cap, const int32_t* n_keys_dev,
                             const int4* rect, int tiles_x, uint32_t* tile_keys, uint32_t* vals,
                             int32_t* tile_counts) {
+    __shared__ int64_t s_lo, s_hi;
     const int64_t n_sorted = min(sorted_cap, static_cast<int64_t>(max(*n_sorted_dev, 0)));
     const int64_t n_keys = n_sorted > 0 ? min(key_cap, static_cast<int64_t>(max(*n_keys_dev, 0))) : 0;
-    for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n_keys;
-         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        int64_t lo = 0, hi = n_sorted - 1;  // last r with offsets[r] <= k
+    // last r with offsets[r] <= k, within [lo, hi]
+    auto owner = [&](int64_t k, int64_t lo, int64_t hi) {
         while (lo < hi) {
             const int64_t mid = (lo + hi + 1) >> 1;
             if (offsets[mid] <= k) lo = mid;
             else hi = mid - 1;
         }
+        return lo;
+    };
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < n_keys;
+         base += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        // the block's keys are contiguous: two full searches bound everyone else's
+        __syncthreads();
+        if (threadIdx.x == 0) s_lo = owner(base, 0, n_sorted - 1);
+        if (threadIdx.x == 1) s_hi = owner(min(base + blockDim.x, n_keys) - 1, 0, n_sorted - 1);
+        __syncthreads();
+        const int64_t k = base + threadIdx.x;
+        if (k >= n_keys) continue;
+        const int64_t lo = owner(k, s_lo, s_hi);
         const uint32_t id = ids[lo];
         const int4 rc = rect[id];
         const int j = static_cast<int>(k - offsets[lo]);

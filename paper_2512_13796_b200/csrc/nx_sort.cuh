@@ -13,7 +13,10 @@ constexpr int kScanThreads = 1024;
 constexpr int kScanTile = kScanItems * kScanThreads;
 constexpr int64_t kScanLoopMax = 16 * kScanTile;  // single-launch scan up to 64K values
 constexpr int kRadixThreads = 256;
-constexpr int kRadixTile = 1024;     // items per block per pass (>= 1 CTA per SM at ~150K keys)
+#ifndef NX_RADIX_TILE
+#define NX_RADIX_TILE 2048
+#endif
+constexpr int kRadixTile = NX_RADIX_TILE;  // items per block per pass (look-back chains of n / tile blocks)
 constexpr int kRadixBits = 8;
 constexpr int kRadixBuckets = 1 << kRadixBits;
 
