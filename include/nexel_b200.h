@@ -149,6 +149,7 @@ typedef struct nx_frame_stats {
     int64_t near_depth;        /* sorted neighbours with depths within 1e-13 (renderer.cpp:102-105) */
     int64_t near_rect;         /* rect floor / ceil arguments within 1e-9 px of an integer */
     int64_t near_support;      /* 2 ln(255 o) within 1e-13 of 0 (support radius sign) */
+    int64_t redo_tiles;        /* pixels the certified composite handed to the exact redo */
 } nx_frame_stats;
 
 /* ---- context ---------------------------------------------------------- */
@@ -413,7 +414,8 @@ int nx_debug_pixel_hits(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam
 
 /* fp64 exp / log of the compositing kernels (table-driven, nx_fastmath.cuh) or CUDA's
  * library routines, on n host arguments (allocates, synchronises; parity tests only). */
-enum { NX_FM_LOG = 0, NX_FM_EXP = 1, NX_FM_CUDA_LOG = 2, NX_FM_CUDA_EXP = 3 };
+enum { NX_FM_LOG = 0, NX_FM_EXP = 1, NX_FM_CUDA_LOG = 2, NX_FM_CUDA_EXP = 3,
+       NX_FM_CERT = 4 /* quintuples (u, v, gx, gy, o) -> (alpha32, eps, oma32, eps_oma, alpha64) */ };
 int nx_debug_fastmath(int fn, const double* x, double* y, int64_t n);
 
 /* ---- synthetic inputs -------------------- */

@@ -181,6 +181,7 @@ class nx_frame_stats(C.Structure):
         ("near_depth", C.c_int64),
         ("near_rect", C.c_int64),
         ("near_support", C.c_int64),
+        ("redo_tiles", C.c_int64),
     ]
 
     def as_dict(self):

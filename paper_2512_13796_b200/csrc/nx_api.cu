@@ -94,6 +94,9 @@ struct nx_ctx {
     DevBuf skeys_a, skeys_b, sids_a, sids_b, counts, offsets;
     DevBuf tkeys_a, tkeys_b, tvals_a, tvals_b, tile_counts, scratch;
     DevBuf dbg_hits, dbg_counts;
+    DevBuf redo;          // tiles the certified composite hands to the exact pass
+    bool certified = true;  // NX_CERTIFIED=0: every frame on the exact fp64 composite
+    bool redo_all = false;  // NX_CERT_REDO_ALL=1 (tests): every tile through the exact redo pass
     DevBuf valid_word;  // revalidation result (first failing primitive)
     // render_backward scratch
     nx_frame* bwd_lists = nullptr;   // work lists of the re-binned camera
@@ -628,6 +631,15 @@ int collection(nx_ctx* c, const nx_scene* scene, const nx_camera* cam, nx_frame*
     ca.dbg_max = dbg_max;
     ca.stats = f->stats;
     ca.sh64 = scene_dev(scene).sh64;
+    // frames that keep the backward state (training) and fp64-colour frames composite on
+    // the exact fp64 path; display frames on the certified fp32 alpha + exact redo
+    ca.certified = c->certified && !f->keep_backward && !f->f64;
+    if (ca.certified) {
+        NX_CUDA(c, c->redo.ensure((static_cast<int64_t>(cam->width) * cam->height + 1) * sizeof(int32_t)));
+        NX_CUDA(c, cudaMemsetAsync(c->redo.p, 0, sizeof(int32_t), s));
+        ca.redo = c->redo.as<int32_t>();
+        ca.redo_all = c->redo_all;
+    }
     launch_composite(ca, s);
     f->base64_valid = f->keep_backward || f->f64;
     record(c, kEvCompEnd, s);
@@ -722,6 +734,8 @@ int nx_ctx_create(int device, nx_ctx** out) {
     c->device = device;
     cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
     if (const char* e = std::getenv("NX_SYNC_LISTS")) c->sync_lists = std::atoi(e) != 0;
+    if (const char* e = std::getenv("NX_CERTIFIED")) c->certified = std::atoi(e) != 0;
+    if (const char* e = std::getenv("NX_CERT_REDO_ALL")) c->redo_all = std::atoi(e) != 0;
     if (const char* e = std::getenv("NX_KEY_CAP")) c->key_cap = std::atoll(e);  // tests: start from a small capacity
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess ||
@@ -1184,6 +1198,7 @@ int nx_frame_stats_get(nx_ctx* c, const nx_frame* f, nx_frame_stats* out) {
     out->near_depth = static_cast<int64_t>(h.near[NEAR_DEPTH]);
     out->near_rect = static_cast<int64_t>(h.near[NEAR_RECT]);
     out->near_support = static_cast<int64_t>(h.near[NEAR_SUPPORT]);
+    out->redo_tiles = static_cast<int64_t>(h.redo_tiles);
     return NX_OK;
 }
 

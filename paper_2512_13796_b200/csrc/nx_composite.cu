@@ -25,6 +25,9 @@
 #include "nx_composite.cuh"
 #include "nx_fastmath.cuh"
 
+#include <algorithm>
+#include <type_traits>
+
 namespace nx {
 
 namespace {
@@ -57,21 +60,33 @@ struct PoolEntry {         // one evaluated (pixel, primitive) pair
     int32_t id;
 };
 
-template <typename CT>
+// Certified mode: alpha from the SFU with its error bound (cert_alpha), 1 - alpha and
+// the bounds travel with the entry so that B2 can certify T and the top-K order.
+struct PoolEntryCert {
+    double t;
+    float alpha;    // clamped kernel alpha (< 0: miss)
+    float oma;      // 1 - alpha
+    float eps;      // relative error bound of alpha
+    float eps_oma;  // relative error bound of oma
+    float rgb[3];
+    int32_t id;
+};
+
+template <typename PE>
 struct WarpStage {  // one warp's private staging
     double rec[kSub][REC_FIELDS];    // exact records of the group's primitives
     float sh[kSub][NX_SH_VALUES];    // and their SH coefficients (fp32 colour path)
     uint8_t sel[kChunk];             // chunk slots whose pixel rect meets the warp's block
     uint16_t q[kPool];
-    PoolEntry<CT> res[kPool];
+    PE res[kPool];
 };
 
-template <typename CT>
+template <typename PE>
 struct SmemLayout {
     float4 f[kChunk][4];
     int32_t id[kChunk];
     double dir[kThreads][3];
-    WarpStage<CT> w[kWarps];
+    WarpStage<PE> w[kWarps];
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -100,7 +115,7 @@ __device__ __forceinline__ void eval_sh_smem(const float* sh, float x, float y, 
     rgb[2] = fmaxf(a2, 0.f);
 }
 
-template <int K, bool kDebug, typename CT>
+template <int K, bool kDebug, typename CT, bool kCert>
 #ifndef NX_COMPOSITE_MINB
 #define NX_COMPOSITE_MINB 10
 #endif
@@ -109,15 +124,17 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
     constexpr bool kKeepRgb = K <= 4;  // top-K slots remember their colour (else re-evaluated at the end)
     constexpr int KR = kKeepRgb ? KK : 1;
     constexpr bool kF64 = sizeof(CT) == 8;  // NX_PRECISION_F64: fp64 SH colour from the fp64 copy
+    static_assert(!(kCert && kF64), "the certified fp32 alpha serves the fp32-colour path");
+    using PE = std::conditional_t<kCert, PoolEntryCert, PoolEntry<CT>>;
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    SmemLayout<CT>& sm = *reinterpret_cast<SmemLayout<CT>*>(smem_raw);
+    SmemLayout<PE>& sm = *reinterpret_cast<SmemLayout<PE>*>(smem_raw);
 
     const int t = blockIdx.x;
     const int tx = t % a.fb.tiles_x, ty = t / a.fb.tiles_x;
     const int list_begin = a.tile_offsets[t], list_end = a.tile_offsets[t + 1];
     const int W = a.cam.W, H = a.cam.H;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WarpStage<CT>& ws = sm.w[warp];
+    WarpStage<PE>& ws = sm.w[warp];
     const double near_eps = a.st.near_eps, alpha_max = a.st.alpha_max, min_T = a.st.min_transmittance;
     const float near_eps_f = static_cast<float>(near_eps);
 
@@ -156,6 +173,11 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
     // near-threshold decisions of this pixel (kNear), packed: alpha | T << 10 | top-K << 20
     // (per-pixel counts stay far below 1024)
     uint32_t n_near = 0;
+    float E_T = 0.f;        // certified mode: relative error bound of T
+    float k_eps[KK];        // and of each top-K slot's weight
+    bool unsure = false;    // a decision this pass could not certify: the tile is redone exactly
+#pragma unroll
+    for (int s = 0; s < KK; ++s) k_eps[s] = 0.f;
     int dbg_n = 0;
     const bool dbg_row = kDebug && in_img && py >= a.dbg_y0 && py < a.dbg_y1;
     const int64_t dbg_q = kDebug ? (static_cast<int64_t>(py - a.dbg_y0) * W + px) : 0;
@@ -253,23 +275,81 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                     const double* dd = sm.dir[warp * 32 + owner];
                     const double d0 = dd[0], d1 = dd[1], d2 = dd[2];
                     const double* r = ws.rec[b];
-                    PoolEntry<CT> res;
+                    PE res;
                     res.alpha = -1.0;
                     res.t = 0.0;
                     res.id = sm.id[ws.sel[g0 + b]];
-                    // intersect (intersect.hpp:23-42) + eval_kernel (kernel.hpp:16-30)
-                    const HitTerms h = exact_hit(r, d0, d1, d2, a.cam.o[0], a.cam.o[1], a.cam.o[2], near_eps);
-                    if (kNear) n_near += h.near ? 1u : 0u;
-                    if (h.alpha >= 0.0) {
-                        res.alpha = h.alpha;
-                        res.t = h.t;
-                        if constexpr (kF64) {
-                            const double dd3[3] = {d0, d1, d2};
-                            eval_sh_f64(a.sh64 + static_cast<int64_t>(res.id) * NX_SH_VALUES, dd3, a.sh_degree,
-                                        res.rgb);
-                        } else {
-                            eval_sh_smem(ws.sh[b], static_cast<float>(d0), static_cast<float>(d1),
-                                         static_cast<float>(d2), a.sh_degree, res.rgb);
+                    if constexpr (kCert) {
+                        // intersect (intersect.hpp:23-42) in fp64 up to the plane offsets, then the
+                        // kernel value on the SFU with its error bound; decisions the bound does
+                        // not clear take the exact fp64 routine
+                        const double denom = d0 * r[REC_NX] + d1 * r[REC_NY] + d2 * r[REC_NZ];
+                        if (fabs(denom) >= kMinNormalDot) {
+                            const double tt = r[REC_NUM] / denom;
+                            if (tt > near_eps) {
+                                const double e0 = (a.cam.o[0] + tt * d0) - r[REC_MUX];
+                                const double e1 = (a.cam.o[1] + tt * d1) - r[REC_MUY];
+                                const double e2 = (a.cam.o[2] + tt * d2) - r[REC_MUZ];
+                                const double du = e0 * r[REC_V1X] + e1 * r[REC_V1Y] + e2 * r[REC_V1Z];
+                                const double dv = e0 * r[REC_V2X] + e1 * r[REC_V2Y] + e2 * r[REC_V2Z];
+                                if (fabs(du) <= r[REC_ULIM] && fabs(dv) <= r[REC_VLIM]) {
+                                    const CertAlpha c = cert_alpha(
+                                        static_cast<float>(du) * static_cast<float>(r[REC_RSX]),
+                                        static_cast<float>(dv) * static_cast<float>(r[REC_RSY]),
+                                        static_cast<float>(2.0 * r[REC_GX]), static_cast<float>(2.0 * r[REC_GY]),
+                                        static_cast<float>(r[REC_OP]), static_cast<float>(r[REC_OM]));
+                                    const double al = c.alpha, lo = al * (1.0 - c.eps), hi = al * (1.0 + c.eps);
+                                    const bool sure = (lo >= kAlphaMin || hi < kAlphaMin) &&
+                                                      (lo > alpha_max || hi <= alpha_max);
+                                    if (sure) {
+                                        if (lo >= kAlphaMin) {
+                                            res.t = tt;
+                                            if (lo > alpha_max) {  // clamped: alpha_max exactly
+                                                res.alpha = static_cast<float>(alpha_max);
+                                                res.oma = static_cast<float>(1.0 - alpha_max);
+                                                res.eps = 6e-8f;
+                                                res.eps_oma = 6e-8f;
+                                            } else {
+                                                res.alpha = c.alpha;
+                                                res.oma = c.oma;
+                                                res.eps = c.eps;
+                                                res.eps_oma = c.eps_oma;
+                                            }
+                                        }
+                                    } else {  // the exact routine decides (rare)
+                                        const HitTerms h =
+                                            exact_hit(r, d0, d1, d2, a.cam.o[0], a.cam.o[1], a.cam.o[2], near_eps);
+                                        if (kNear) n_near += h.near ? 1u : 0u;
+                                        if (h.alpha >= 0.0) {
+                                            const double ac = alpha_max < h.alpha ? alpha_max : h.alpha;
+                                            res.t = h.t;
+                                            res.alpha = static_cast<float>(ac);
+                                            res.oma = static_cast<float>(1.0 - ac);
+                                            res.eps = 1.2e-7f;
+                                            res.eps_oma = 1.2e-7f;
+                                        }
+                                    }
+                                    if (res.alpha >= 0.f)
+                                        eval_sh_smem(ws.sh[b], static_cast<float>(d0), static_cast<float>(d1),
+                                                     static_cast<float>(d2), a.sh_degree, res.rgb);
+                                }
+                            }
+                        }
+                    } else {
+                        // intersect (intersect.hpp:23-42) + eval_kernel (kernel.hpp:16-30)
+                        const HitTerms h = exact_hit(r, d0, d1, d2, a.cam.o[0], a.cam.o[1], a.cam.o[2], near_eps);
+                        if (kNear) n_near += h.near ? 1u : 0u;
+                        if (h.alpha >= 0.0) {
+                            res.alpha = h.alpha;
+                            res.t = h.t;
+                            if constexpr (kF64) {
+                                const double dd3[3] = {d0, d1, d2};
+                                eval_sh_f64(a.sh64 + static_cast<int64_t>(res.id) * NX_SH_VALUES, dd3, a.sh_degree,
+                                            res.rgb);
+                            } else {
+                                eval_sh_smem(ws.sh[b], static_cast<float>(d0), static_cast<float>(d1),
+                                             static_cast<float>(d2), a.sh_degree, res.rgb);
+                            }
                         }
                     }
                     ws.res[e] = res;
@@ -277,11 +357,15 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                 __syncwarp();
                 // ---- B2. per-pixel compositing of this lane's hits, in list order (renderer.cpp:144-153)
                 for (int k = off; k < off + cnt && active; ++k) {
-                    const PoolEntry<CT>& res = ws.res[k];
+                    const PE& res = ws.res[k];
                     if (res.alpha < 0.0) continue;
                     const int32_t id = res.id;
-                    const double alpha = alpha_max < res.alpha ? alpha_max : res.alpha;
+                    // (certified entries arrive clamped)
+                    const double alpha = kCert ? static_cast<double>(res.alpha)
+                                               : (alpha_max < res.alpha ? alpha_max : static_cast<double>(res.alpha));
                     const double wgt = alpha * T;
+                    float eps_w = 0.f;  // certified mode: relative error bound of wgt
+                    if constexpr (kCert) eps_w = res.eps + E_T;
                     acc[0] += wgt * res.rgb[0];
                     acc[1] += wgt * res.rgb[1];
                     acc[2] += wgt * res.rgb[2];
@@ -295,15 +379,20 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                             int mi = 0;
                             double wm = k_w[0];
                             uint32_t qm = k_seq[0];
+                            float em = k_eps[0];
 #pragma unroll
-                            for (int s = 1; s < KK; ++s)
+                            for (int s = 1; s < KK; ++s) {
+                                if (kCert && fabs(k_w[s] - wm) <= (k_eps[s] + em) * fmax(k_w[s], wm)) unsure = true;
                                 if (k_w[s] < wm || (k_w[s] == wm && k_seq[s] > qm)) {
                                     mi = s;
                                     wm = k_w[s];
                                     qm = k_seq[s];
+                                    em = k_eps[s];
                                 }
+                            }
                             if (wgt > wm) slot = mi;
-                            if (kNear) n_near += (wgt != wm) & (fabs(wgt - wm) <= kNearRel * wm) ? (1u << 20) : 0u;
+                            if (kCert && fabs(wgt - wm) <= (eps_w + em) * fmax(wgt, wm)) unsure = true;
+                            if (kNear && !kCert) n_near += (wgt != wm) & (fabs(wgt - wm) <= kNearRel * wm) ? (1u << 20) : 0u;
                         }
 #pragma unroll
                         for (int s = 0; s < KK; ++s)
@@ -312,6 +401,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                                 k_w[s] = wgt;
                                 k_t[s] = res.t;
                                 k_seq[s] = seq;
+                                k_eps[s] = eps_w;
                                 if (kKeepRgb) {
                                     k_rgb[s % KR][0] = res.rgb[0];
                                     k_rgb[s % KR][1] = res.rgb[1];
@@ -323,9 +413,16 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                         if (dbg_n < a.dbg_max) a.dbg_hits[dbg_q * a.dbg_max + dbg_n] = id;
                         ++dbg_n;
                     }
-                    T *= 1.0 - alpha;
+                    if constexpr (kCert) {  // T *= 1 - alpha with 1 - alpha from the entry (no cancellation)
+                        T *= static_cast<double>(res.oma);
+                        E_T += res.eps_oma;
+                        if (fabs(T - min_T) <= static_cast<double>(E_T) * T) unsure = true;  // T vs min_T uncertain
+                    } else {
+                        T *= 1.0 - alpha;
+                    }
                     if (T < min_T) active = false;
-                    if (kNear) n_near += fabs(T - min_T) <= kNearRel * min_T ? (1u << 10) : 0u;
+                    // (certified pass: uncertain T / top-K decisions are redone exactly and counted there)
+                    if (kNear && !kCert) n_near += fabs(T - min_T) <= kNearRel * min_T ? (1u << 10) : 0u;
                 }
                 __syncwarp();
             }
@@ -348,8 +445,12 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                 for (int j = 0; j + 1 < K - i; ++j) {
                     const bool swap = (j + 1 < k_size) &&
                                       (k_w[j + 1] > k_w[j] || (k_w[j + 1] == k_w[j] && k_seq[j + 1] < k_seq[j]));
-                    if (kNear && j + 1 < k_size && k_w[j + 1] != k_w[j] && fabs(k_w[j + 1] - k_w[j]) <= kNearRel * k_w[j])
+                    if (kNear && !kCert && j + 1 < k_size && k_w[j + 1] != k_w[j] &&
+                        fabs(k_w[j + 1] - k_w[j]) <= kNearRel * k_w[j])
                         n_near += 1u << 20;
+                    if (kCert && j + 1 < k_size &&
+                        fabs(k_w[j + 1] - k_w[j]) <= (k_eps[j + 1] + k_eps[j]) * fmax(k_w[j + 1], k_w[j]))
+                        unsure = true;
                     if (swap) {
                         const int32_t ti = k_id[j];
                         k_id[j] = k_id[j + 1];
@@ -363,6 +464,9 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                         const uint32_t ts = k_seq[j];
                         k_seq[j] = k_seq[j + 1];
                         k_seq[j + 1] = ts;
+                        const float te = k_eps[j];
+                        k_eps[j] = k_eps[j + 1];
+                        k_eps[j + 1] = te;
                         if (kKeepRgb) {
 #pragma unroll
                             for (int c = 0; c < 3; ++c) {
@@ -407,6 +511,10 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
             a.fb.base64[pix * 3 + 2] = acc[2];
         }
         if (kDebug && dbg_row) a.dbg_counts[dbg_q] = dbg_n;
+        if (kCert && (unsure || a.redo_all)) {  // a decision the bounds did not clear: redone exactly
+            const int slot = atomicAdd(a.redo, 1);
+            a.redo[1 + slot] = static_cast<int32_t>(pix);
+        }
     }
     if (kNear && n_near) {
         if (n_near & 1023u) atomicAdd(&a.stats->near[NEAR_ALPHA], static_cast<unsigned long long>(n_near & 1023u));
@@ -416,19 +524,235 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
     }
 }
 
+
+// Exact redo of the pixels the certified pass could not certify: one warp per pixel. The
+// lanes evaluate 32 list entries at a time (pixel rect test + the exact fp64 intersect /
+// eval_kernel, exact_hit, + SH colour), the hits are packed in list order, and lane 0
+// composites them sequentially with the exact pass's arithmetic (renderer.cpp:144-164),
+// so a redone pixel carries the exact composite's bits.
+template <int K, bool kDebug>
+__global__ void __launch_bounds__(256) redo_pixels_kernel(const CompositeArgs a) {
+    constexpr int KK = K > 0 ? K : 1;
+    struct Hits {
+        double alpha[32], t[32];
+        float rgb[32][3];
+        int32_t id[32];
+    };
+    __shared__ Hits hs[8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    Hits& h = hs[warp];
+    const int n = *a.redo;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.stats->redo_tiles = static_cast<unsigned long long>(n);
+    const int W = a.cam.W;
+    const double near_eps = a.st.near_eps, alpha_max = a.st.alpha_max, min_T = a.st.min_transmittance;
+    const double2* rec2 = reinterpret_cast<const double2*>(a.rec);
+    uint32_t n_near = 0;
+    for (int i = blockIdx.x * 8 + warp; i < n; i += gridDim.x * 8) {
+        const int64_t pix = a.redo[1 + i];
+        const int px = static_cast<int>(pix % W), py = static_cast<int>(pix / W);
+        const int t = (py / kWorkTile) * a.fb.tiles_x + px / kWorkTile;
+        const int list_begin = a.tile_offsets[t], list_end = a.tile_offsets[t + 1];
+        double dir[3];
+        pixel_dir(a.cam, px + 0.5, py + 0.5, dir);
+        const float dfx = static_cast<float>(dir[0]), dfy = static_cast<float>(dir[1]), dfz = static_cast<float>(dir[2]);
+        double T = 1.0, acc[3] = {0.0, 0.0, 0.0};
+        int32_t k_id[KK];
+        double k_w[KK], k_t[KK];
+        uint32_t k_seq[KK];
+        float k_rgb[KK][3];
+        for (int s = 0; s < KK; ++s) {
+            k_id[s] = -1;
+            k_w[s] = 0.0;
+            k_t[s] = 0.0;
+            k_seq[s] = 0;
+            k_rgb[s][0] = k_rgb[s][1] = k_rgb[s][2] = 0.f;
+        }
+        int k_size = 0, dbg_n = 0;
+        uint32_t counter = 0;
+        bool active = true;
+        const bool dbg_row = kDebug && py >= a.dbg_y0 && py < a.dbg_y1;
+        const int64_t dbg_q = kDebug ? (static_cast<int64_t>(py - a.dbg_y0) * W + px) : 0;
+        for (int cb = list_begin; cb < list_end && active; cb += 32) {
+            const int e = cb + lane;
+            bool hit = false;
+            double al = 0.0, tt = 0.0;
+            float rgb[3] = {0.f, 0.f, 0.f};
+            int32_t id = -1;
+            if (e < list_end) {
+                id = a.list_ids[e];
+                const float4 f3 = __ldg(a.recf + static_cast<int64_t>(id) * 4 + 3);
+                const int rx = __float_as_int(f3.z), ry = __float_as_int(f3.w);
+                if (px >= (rx & 0xffff) && px <= (rx >> 16) && py >= (ry & 0xffff) && py <= (ry >> 16)) {
+                    double r[REC_FIELDS];
+#pragma unroll
+                    for (int q = 0; q < REC_FIELDS / 2; ++q) {
+                        const double2 v = __ldg(rec2 + static_cast<int64_t>(id) * (REC_FIELDS / 2) + q);
+                        r[2 * q] = v.x;
+                        r[2 * q + 1] = v.y;
+                    }
+                    const HitTerms ht = exact_hit(r, dir[0], dir[1], dir[2], a.cam.o[0], a.cam.o[1], a.cam.o[2],
+                                                  near_eps);
+                    n_near += ht.near ? 1u : 0u;
+                    if (ht.alpha >= 0.0) {
+                        hit = true;
+                        al = ht.alpha;
+                        tt = ht.t;
+                        eval_sh_f32(a.sh + static_cast<int64_t>(id) * NX_SH_VALUES, dfx, dfy, dfz, a.sh_degree, rgb);
+                    }
+                }
+            }
+            const uint32_t m = __ballot_sync(0xffffffffu, hit);
+            if (hit) {
+                const int k = __popc(m & ((1u << lane) - 1u));
+                h.alpha[k] = al;
+                h.t[k] = tt;
+                h.rgb[k][0] = rgb[0];
+                h.rgb[k][1] = rgb[1];
+                h.rgb[k][2] = rgb[2];
+                h.id[k] = id;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const int nh = __popc(m);
+                for (int k = 0; k < nh && active; ++k) {
+                    const double alpha = alpha_max < h.alpha[k] ? alpha_max : h.alpha[k];
+                    const double wgt = alpha * T;
+                    acc[0] += wgt * h.rgb[k][0];
+                    acc[1] += wgt * h.rgb[k][1];
+                    acc[2] += wgt * h.rgb[k][2];
+                    if (K > 0) {  // TopKBuffer::insert (framebuffers.hpp:33-48)
+                        const uint32_t seq = counter++;
+                        int slot = -1;
+                        if (k_size < K) {
+                            slot = k_size++;
+                        } else {
+                            int mi = 0;
+                            double wm = k_w[0];
+                            uint32_t qm = k_seq[0];
+                            for (int s = 1; s < KK; ++s)
+                                if (k_w[s] < wm || (k_w[s] == wm && k_seq[s] > qm)) {
+                                    mi = s;
+                                    wm = k_w[s];
+                                    qm = k_seq[s];
+                                }
+                            if (wgt > wm) slot = mi;
+                            n_near += (wgt != wm) & (fabs(wgt - wm) <= kNearRel * wm) ? (1u << 20) : 0u;
+                        }
+                        if (slot >= 0) {
+                            k_id[slot] = h.id[k];
+                            k_w[slot] = wgt;
+                            k_t[slot] = h.t[k];
+                            k_seq[slot] = seq;
+                            k_rgb[slot][0] = h.rgb[k][0];
+                            k_rgb[slot][1] = h.rgb[k][1];
+                            k_rgb[slot][2] = h.rgb[k][2];
+                        }
+                    }
+                    if (kDebug && dbg_row) {
+                        if (dbg_n < a.dbg_max) a.dbg_hits[dbg_q * a.dbg_max + dbg_n] = h.id[k];
+                        ++dbg_n;
+                    }
+                    T *= 1.0 - alpha;
+                    if (T < min_T) active = false;
+                    n_near += fabs(T - min_T) <= kNearRel * min_T ? (1u << 10) : 0u;
+                }
+            }
+            active = __shfl_sync(0xffffffffu, active, 0);
+            __syncwarp();
+        }
+        if (lane == 0) {  // the exact pass's epilogue (renderer.cpp:155-164, framebuffers.hpp:51-56)
+            a.fb.residual[pix] = static_cast<float>(T);
+            if (a.fb.residual64) a.fb.residual64[pix] = T;
+            acc[0] += T * a.st.background[0];
+            acc[1] += T * a.st.background[1];
+            acc[2] += T * a.st.background[2];
+            if (K > 0) {
+                for (int ii = 0; ii < K; ++ii)
+                    for (int j = 0; j + 1 < K - ii; ++j) {
+                        if (j + 1 < k_size && k_w[j + 1] != k_w[j] && fabs(k_w[j + 1] - k_w[j]) <= kNearRel * k_w[j])
+                            n_near += 1u << 20;
+                        const bool swap = (j + 1 < k_size) &&
+                                          (k_w[j + 1] > k_w[j] || (k_w[j + 1] == k_w[j] && k_seq[j + 1] < k_seq[j]));
+                        if (swap) {
+                            const int32_t ti = k_id[j];
+                            k_id[j] = k_id[j + 1];
+                            k_id[j + 1] = ti;
+                            const double tw = k_w[j];
+                            k_w[j] = k_w[j + 1];
+                            k_w[j + 1] = tw;
+                            const double td = k_t[j];
+                            k_t[j] = k_t[j + 1];
+                            k_t[j + 1] = td;
+                            const uint32_t ts = k_seq[j];
+                            k_seq[j] = k_seq[j + 1];
+                            k_seq[j + 1] = ts;
+                            for (int c = 0; c < 3; ++c) {
+                                const float tc = k_rgb[j][c];
+                                k_rgb[j][c] = k_rgb[j + 1][c];
+                                k_rgb[j + 1][c] = tc;
+                            }
+                        }
+                    }
+                for (int j = 0; j < K; ++j) {
+                    const int64_t sl = pix * K + j;
+                    a.fb.ids[sl] = k_id[j];
+                    a.fb.depths[sl] = k_t[j];
+                    a.fb.weights[sl] = k_w[j];
+                    if (j < k_size) {
+                        acc[0] -= k_w[j] * k_rgb[j][0];
+                        acc[1] -= k_w[j] * k_rgb[j][1];
+                        acc[2] -= k_w[j] * k_rgb[j][2];
+                    }
+                }
+            }
+            a.fb.base[pix * 3 + 0] = static_cast<float>(acc[0]);
+            a.fb.base[pix * 3 + 1] = static_cast<float>(acc[1]);
+            a.fb.base[pix * 3 + 2] = static_cast<float>(acc[2]);
+            if (a.fb.base64) {
+                a.fb.base64[pix * 3 + 0] = acc[0];
+                a.fb.base64[pix * 3 + 1] = acc[1];
+                a.fb.base64[pix * 3 + 2] = acc[2];
+            }
+            if (kDebug && dbg_row) {
+                a.dbg_counts[dbg_q] = dbg_n;
+                for (int ii = dbg_n; ii < a.dbg_max; ++ii) a.dbg_hits[dbg_q * a.dbg_max + ii] = -1;
+            }
+        }
+        __syncwarp();
+    }
+    if (kNear && n_near) {
+        if (n_near & 1023u) atomicAdd(&a.stats->near[NEAR_ALPHA], static_cast<unsigned long long>(n_near & 1023u));
+        if ((n_near >> 10) & 1023u)
+            atomicAdd(&a.stats->near[NEAR_TRANSMITTANCE], static_cast<unsigned long long>((n_near >> 10) & 1023u));
+        if (n_near >> 20) atomicAdd(&a.stats->near[NEAR_TOPK], static_cast<unsigned long long>(n_near >> 20));
+    }
+}
+
+template <int K, bool kDebug, typename CT, bool kCert>
+void launch_variant(const CompositeArgs& a, unsigned grid, cudaStream_t s) {
+    using PE = std::conditional_t<kCert, PoolEntryCert, PoolEntry<CT>>;
+    const size_t smem = sizeof(SmemLayout<PE>);
+    cudaFuncSetAttribute(composite_kernel<K, kDebug, CT, kCert>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    composite_kernel<K, kDebug, CT, kCert><<<grid, kThreads, smem, s>>>(a);
+}
+
 template <int K, bool kDebug>
 void launch_one(const CompositeArgs& a, unsigned grid, cudaStream_t s) {
     if (a.sh64) {
-        const size_t smem = sizeof(SmemLayout<double>);
-        cudaFuncSetAttribute(composite_kernel<K, kDebug, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        composite_kernel<K, kDebug, double><<<grid, kThreads, smem, s>>>(a);
-        return;
+        launch_variant<K, kDebug, double, false>(a, grid, s);
+    } else if (a.certified && a.redo) {
+        launch_variant<K, kDebug, float, true>(a, grid, s);  // certified pass, uncertain pixels -> redo
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t npix = static_cast<int64_t>(a.cam.W) * a.cam.H;
+        const unsigned rgrid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((npix + 7) / 8, sms * 4)));
+        count_launch();
+        redo_pixels_kernel<K, kDebug><<<rgrid, 256, 0, s>>>(a);  // the exact redo of those pixels
+    } else {
+        launch_variant<K, kDebug, float, false>(a, grid, s);
     }
-    const size_t smem = sizeof(SmemLayout<float>);
-    cudaFuncSetAttribute(composite_kernel<K, kDebug, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    composite_kernel<K, kDebug, float><<<grid, kThreads, smem, s>>>(a);
 }
 
 template <bool kDebug>

@@ -217,4 +217,74 @@ __device__ __forceinline__ HitTerms exact_hit(const Rec& r, double d0, double d1
     return h;
 }
 
+// ---------------------------------------------------------------- certified fp32 alpha
+// eval_kernel (kernel.hpp:16-30) on the SFU (MUFU lg2 / ex2 in fp32) with a rigorous
+// bound on its relative error, so that the decision alpha >= 1/255 is taken in fp32
+// wherever the bound clears the threshold and with the exact fp64 routine otherwise.
+// Error model (fp32 unit 2^-24 = 6e-8; MUFU.LG2 absolute error <= 2^-22, MUFU.EX2
+// relative error <= 2^-21, both taken generously; u carries 3 roundings):
+//   d(lg2|u|) <= 2.4e-7 + 6e-8 |lg2 u| + 2.6e-7             (argument error 1.8e-7 / ln 2)
+//   d(a)      <= 2g d(lg2|u|) + 1.2e-7 |a|,  a = 2g lg2|u|
+//   rel(pu)   <= ln2 d(a) + 4.8e-7
+//   |dp|      <= pu rel(pu) + pv rel(pv) + 6e-8 p
+//   rel(alpha) <= p/2 rel(p) + ln2 1.2e-7 |b| + 6e-7,  b = -p/(2 ln 2)
+// and the result is doubled (`eps`). 1 - alpha is formed as (1 - o) + o (1 - k), with
+// 1 - k = -expm1(-p/2) (a degree-9 series above -0.7), so it keeps its relative accuracy
+// (`eps_oma`) when alpha is close to 1. tests/test_gpu_fastmath.py checks the bounds
+// against the fp64 routine over millions of (u, v, gamma, o).
+struct CertAlpha {
+    float alpha;    // o exp(-(|u|^2gx + |v|^2gy) / 2)
+    float oma;      // 1 - alpha
+    float eps;      // relative error bound of alpha
+    float eps_oma;  // relative error bound of oma
+};
+
+__device__ __forceinline__ float sfu_lg2(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float sfu_ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ CertAlpha cert_alpha(float u, float v, float g2x, float g2y, float o, float om) {
+    CertAlpha c;
+    const float lu = sfu_lg2(fabsf(u)), lv = sfu_lg2(fabsf(v));
+    const float au = g2x * lu, av = g2y * lv;
+    const float pu = u == 0.f ? 0.f : sfu_ex2(au), pv = v == 0.f ? 0.f : sfu_ex2(av);
+    const float p = pu + pv;
+    const float dau = g2x * (5.0e-7f + 6e-8f * fabsf(lu)) + 1.2e-7f * fabsf(au);
+    const float dav = g2y * (5.0e-7f + 6e-8f * fabsf(lv)) + 1.2e-7f * fabsf(av);
+    const float dp = (u == 0.f ? 0.f : pu * (0.6931472f * dau + 4.8e-7f)) +
+                     (v == 0.f ? 0.f : pv * (0.6931472f * dav + 4.8e-7f)) + 6e-8f * p;
+    const float b = -0.72134752f * p;  // -p / (2 ln 2)
+    const float k = sfu_ex2(b);
+    c.alpha = o * k;
+    c.eps = 2.f * (0.5f * dp + 8.4e-8f * fabsf(b) + 6e-7f);
+    // 1 - k = -expm1(x), x = -p/2
+    const float x = -0.5f * p;
+    float km1;
+    if (x > -0.7f) {
+        float q = 1.f / 362880.f;
+        q = fmaf(q, x, 1.f / 40320.f);
+        q = fmaf(q, x, 1.f / 5040.f);
+        q = fmaf(q, x, 1.f / 720.f);
+        q = fmaf(q, x, 1.f / 120.f);
+        q = fmaf(q, x, 1.f / 24.f);
+        q = fmaf(q, x, 1.f / 6.f);
+        q = fmaf(q, x, 0.5f);
+        q = fmaf(q, x, 1.f);
+        km1 = -x * q;
+    } else {
+        km1 = 1.f - k;
+    }
+    c.oma = fmaf(o, km1, om);
+    const float relp = p > 0.f ? dp / p : 0.f;
+    c.eps_oma = 2.f * (relp + 3.6e-7f);
+    return c;
+}
+
 }  // namespace nx

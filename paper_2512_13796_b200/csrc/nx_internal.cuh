@@ -116,7 +116,7 @@ NX_HD void pixel_dir(const CamD& c, double px, double py, double* dir) {
 }
 
 // ---------------------------------------------------------------- per-primitive composite record
-// AoS, 20 fp64 per primitive, staged into shared memory by the compositing kernels.
+// AoS, 24 fp64 per primitive (192 B), staged into shared memory by the compositing kernels.
 enum RecField {
     REC_NUM = 0,  // dot(mu - origin, n): the per-camera numerator of t (intersect.hpp:29)
     REC_NX, REC_NY, REC_NZ,
@@ -127,6 +127,9 @@ enum RecField {
     REC_OP,
     REC_GX, REC_GY,
     REC_ULIM, REC_VLIM,  // conservative |dot(delta,v)| bounds for an exact early reject
+    REC_RSX, REC_RSY,    // 1 / sigma (the certified fp32 alpha, nx_fastmath.cuh cert_alpha)
+    REC_OM,              // 1 - opacity = sigmoid(-opacity_raw), for an accurate 1 - alpha
+    REC_PAD,
     REC_FIELDS
 };
 
@@ -158,6 +161,7 @@ struct FrameStatsD {
     unsigned long long work_keys;
     unsigned long long queries;
     unsigned long long near[NEAR_KINDS];
+    unsigned long long redo_tiles;  // pixels the certified composite handed to the exact redo
 };
 
 struct SceneDev {
@@ -252,6 +256,12 @@ struct CompositeArgs {
     int dbg_y0, dbg_y1, dbg_max;
     FrameStatsD* stats;  // near-threshold counters
     const double* sh64 = nullptr;  // NX_PRECISION_F64: fp64 SH (the colour path runs in fp64)
+    // certified fp32 alpha (nx_fastmath.cuh cert_alpha) for frames without backward state:
+    // the first pass appends the pixels it could not certify to redo ([0] = count, zeroed
+    // by the caller), a warp-per-pixel exact pass re-renders them
+    bool certified = false;
+    bool redo_all = false;  // tests: hand every pixel to the exact redo
+    int32_t* redo = nullptr;
 };
 void launch_composite(const CompositeArgs& a, cudaStream_t s);
 

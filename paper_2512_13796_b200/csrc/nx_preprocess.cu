@@ -230,6 +230,10 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const PreprocessArgs a)
             const bool safe = log(op / kAlphaMin) >= 1e-3;
             r[REC_ULIM] = safe ? ru * (1.0 + 1e-6) * sx : INFINITY;
             r[REC_VLIM] = safe ? rv * (1.0 + 1e-6) * sy : INFINITY;
+            r[REC_RSX] = 1.0 / sx;
+            r[REC_RSY] = 1.0 / sy;
+            r[REC_OM] = sigmoid(-g[9 * n + i]);  // 1 - o without cancellation
+            r[REC_PAD] = 0.0;
             double2* dst = reinterpret_cast<double2*>(a.rec + i * REC_FIELDS);
 #pragma unroll
             for (int q = 0; q < REC_FIELDS / 2; ++q) dst[q] = make_double2(r[2 * q], r[2 * q + 1]);
