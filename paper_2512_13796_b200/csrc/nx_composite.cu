@@ -174,10 +174,12 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
     // (per-pixel counts stay far below 1024)
     uint32_t n_near = 0;
     float E_T = 0.f;        // certified mode: relative error bound of T
-    float k_eps[KK];        // and of each top-K slot's weight
+    // and, per top-K slot, the alpha bound and E_T when it was inserted: two weights'
+    // ratio carries only their alphas' errors and the 1 - alpha factors between them
+    float k_ea[KK], k_et[KK];
     bool unsure = false;    // a decision this pass could not certify: the tile is redone exactly
 #pragma unroll
-    for (int s = 0; s < KK; ++s) k_eps[s] = 0.f;
+    for (int s = 0; s < KK; ++s) k_ea[s] = k_et[s] = 0.f;
     int dbg_n = 0;
     const bool dbg_row = kDebug && in_img && py >= a.dbg_y0 && py < a.dbg_y1;
     const int64_t dbg_q = kDebug ? (static_cast<int64_t>(py - a.dbg_y0) * W + px) : 0;
@@ -364,8 +366,8 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                     const double alpha = kCert ? static_cast<double>(res.alpha)
                                                : (alpha_max < res.alpha ? alpha_max : static_cast<double>(res.alpha));
                     const double wgt = alpha * T;
-                    float eps_w = 0.f;  // certified mode: relative error bound of wgt
-                    if constexpr (kCert) eps_w = res.eps + E_T;
+                    float eps_a = 0.f;  // certified mode: alpha's relative error bound
+                    if constexpr (kCert) eps_a = res.eps;
                     acc[0] += wgt * res.rgb[0];
                     acc[1] += wgt * res.rgb[1];
                     acc[2] += wgt * res.rgb[2];
@@ -379,19 +381,21 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                             int mi = 0;
                             double wm = k_w[0];
                             uint32_t qm = k_seq[0];
-                            float em = k_eps[0];
+                            float ea = k_ea[0], et = k_et[0];
 #pragma unroll
                             for (int s = 1; s < KK; ++s) {
-                                if (kCert && fabs(k_w[s] - wm) <= (k_eps[s] + em) * fmax(k_w[s], wm)) unsure = true;
+                                if (kCert && fabs(k_w[s] - wm) <= (k_ea[s] + ea + fabsf(k_et[s] - et)) * fmax(k_w[s], wm))
+                                    unsure = true;
                                 if (k_w[s] < wm || (k_w[s] == wm && k_seq[s] > qm)) {
                                     mi = s;
                                     wm = k_w[s];
                                     qm = k_seq[s];
-                                    em = k_eps[s];
+                                    ea = k_ea[s];
+                                    et = k_et[s];
                                 }
                             }
                             if (wgt > wm) slot = mi;
-                            if (kCert && fabs(wgt - wm) <= (eps_w + em) * fmax(wgt, wm)) unsure = true;
+                            if (kCert && fabs(wgt - wm) <= (eps_a + ea + (E_T - et)) * fmax(wgt, wm)) unsure = true;
                             if (kNear && !kCert) n_near += (wgt != wm) & (fabs(wgt - wm) <= kNearRel * wm) ? (1u << 20) : 0u;
                         }
 #pragma unroll
@@ -401,7 +405,8 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                                 k_w[s] = wgt;
                                 k_t[s] = res.t;
                                 k_seq[s] = seq;
-                                k_eps[s] = eps_w;
+                                k_ea[s] = eps_a;
+                                k_et[s] = E_T;
                                 if (kKeepRgb) {
                                     k_rgb[s % KR][0] = res.rgb[0];
                                     k_rgb[s % KR][1] = res.rgb[1];
@@ -449,7 +454,8 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                         fabs(k_w[j + 1] - k_w[j]) <= kNearRel * k_w[j])
                         n_near += 1u << 20;
                     if (kCert && j + 1 < k_size &&
-                        fabs(k_w[j + 1] - k_w[j]) <= (k_eps[j + 1] + k_eps[j]) * fmax(k_w[j + 1], k_w[j]))
+                        fabs(k_w[j + 1] - k_w[j]) <=
+                            (k_ea[j + 1] + k_ea[j] + fabsf(k_et[j + 1] - k_et[j])) * fmax(k_w[j + 1], k_w[j]))
                         unsure = true;
                     if (swap) {
                         const int32_t ti = k_id[j];
@@ -464,9 +470,11 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                         const uint32_t ts = k_seq[j];
                         k_seq[j] = k_seq[j + 1];
                         k_seq[j + 1] = ts;
-                        const float te = k_eps[j];
-                        k_eps[j] = k_eps[j + 1];
-                        k_eps[j + 1] = te;
+                        const float tea = k_ea[j], tet = k_et[j];
+                        k_ea[j] = k_ea[j + 1];
+                        k_et[j] = k_et[j + 1];
+                        k_ea[j + 1] = tea;
+                        k_et[j + 1] = tet;
                         if (kKeepRgb) {
 #pragma unroll
                             for (int c = 0; c < 3; ++c) {
