@@ -283,6 +283,21 @@ def cpu_reference_sample(scene, view_cam, config1=True):
     return out
 
 
+def mapped_repo_libs():
+    """Shared objects of this repository mapped into the process (the reference arm must
+    map oracle/_ref only, never the product library)."""
+    libs = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for line in f:
+                path = line.split()[-1] if line.strip() else ""
+                if path.endswith(".so") and os.path.abspath(path).startswith(ROOT):
+                    libs.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
 def run_reference_arm(args):
     """--impl reference: the reference's own CPU renderer (oracle/_ref: its sources
     compiled in place, never this repo's kernels) on all host cores, timing whole
@@ -316,6 +331,7 @@ def run_reference_arm(args):
                                    f"{cores} threads; per-frame seconds min {min(times):.2f} max {max(times):.2f}"},
         "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "lib": os.path.basename(impl.path),
+        "mapped_repo_libs": mapped_repo_libs(),
     }
     print(json.dumps(line), flush=True)
 
