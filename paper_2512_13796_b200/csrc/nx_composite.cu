@@ -35,7 +35,7 @@ namespace {
 constexpr int kThreads = kWorkTile * kWorkTile;  // 64: one thread per pixel of the work tile
 constexpr int kWarps = kThreads / 32;
 #ifndef NX_COMPOSITE_CHUNK
-#define NX_COMPOSITE_CHUNK 128
+#define NX_COMPOSITE_CHUNK 64
 #endif
 #ifndef NX_COMPOSITE_SUB
 #define NX_COMPOSITE_SUB 4
@@ -77,6 +77,7 @@ struct WarpStage {  // one warp's private staging
     double rec[kSub][REC_FIELDS];    // exact records of the group's primitives
     float sh[kSub][NX_SH_VALUES];    // and their SH coefficients (fp32 colour path)
     uint8_t sel[kChunk];             // chunk slots whose pixel rect meets the warp's block
+    uint32_t lmask[kChunk];          // and the lanes (pixels of the 8x4 block) inside that rect
     uint16_t q[kPool];
     PE res[kPool];
 };
@@ -203,16 +204,29 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
         if (__any_sync(0xffffffffu, active)) {
             // ---- 0. the chunk's primitives whose pixel rect meets this warp's block, in order
             int nsel = 0;
+            const int bx0 = tx * kWorkTile, by0 = ty * kWorkTile + warp * 4;  // the warp block's origin
             for (int b0 = 0; b0 < cn; b0 += 32) {
                 const int b = b0 + lane;
                 bool ov = false;
+                uint32_t lm = 0;
                 if (b < cn) {
                     const float4 f3 = sm.f[b][3];
                     const int rx = __float_as_int(f3.z), ry = __float_as_int(f3.w);
                     ov = !((rx >> 16) < wx0 || (rx & 0xffff) > wx1 || (ry >> 16) < wy0 || (ry & 0xffff) > wy1);
+                    if (ov) {  // lane l = pixel (bx0 + l % 8, by0 + l / 8): the rect's columns x its rows
+                        const int cx0 = max((rx & 0xffff) - bx0, 0), cx1 = min((rx >> 16) - bx0, 7);
+                        const int ry0 = max((ry & 0xffff) - by0, 0), ry1 = min((ry >> 16) - by0, 3);
+                        const uint32_t cols = (0xffu >> (7 - cx1)) & (0xffu << cx0);
+                        const uint32_t rows = (0xffffffffu >> (8 * (3 - ry1))) & (0xffffffffu << (8 * ry0));
+                        lm = (cols * 0x01010101u) & rows;
+                    }
                 }
                 const uint32_t m = __ballot_sync(0xffffffffu, ov);
-                if (ov) ws.sel[nsel + __popc(m & ((1u << lane) - 1u))] = static_cast<uint8_t>(b);
+                if (ov) {
+                    const int slot = nsel + __popc(m & ((1u << lane) - 1u));
+                    ws.sel[slot] = static_cast<uint8_t>(b);
+                    ws.lmask[slot] = lm;
+                }
                 nsel += __popc(m);
             }
             __syncwarp();
@@ -237,10 +251,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
 #pragma unroll 4
                     for (int b = 0; b < gn; ++b) {
                         const int j = ws.sel[g0 + b];
-                        const float4 f3 = sm.f[j][3];
-                        const int rx = __float_as_int(f3.z), ry = __float_as_int(f3.w);
-                        if (px >= (rx & 0xffff) && px <= (rx >> 16) && py >= (ry & 0xffff) && py <= (ry >> 16) &&
-                            prefilter(&sm.f[j][0], dfx, dfy, dfz, near_eps_f))
+                        if (((ws.lmask[g0 + b] >> lane) & 1u) && prefilter(&sm.f[j][0], dfx, dfy, dfz, near_eps_f))
                             mask |= 1u << b;
                     }
                 }
