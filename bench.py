@@ -125,8 +125,14 @@ def dropin_line():
     try:
         out = subprocess.run([exe, "10"], capture_output=True, text=True, timeout=300).stdout
         line = json.loads(out.strip().splitlines()[-1])
-        line["path"] = ("nexel::render(scene, cam): scene fingerprint, collection + texturing passes, download, "
-                        "FrameBuffers allocation (by value) and widening to the reference's doubles")
+        line["path"] = ("nexel::render(scene, cam): scene fingerprint, collection + texturing passes at "
+                        "NX_PRECISION_F64 (the reference's FrameBuffers precision), download, FrameBuffers "
+                        "allocation (by value)")
+        env = dict(os.environ, NEXEL_DROPIN_PRECISION="f32")
+        out = subprocess.run([exe, "10"], capture_output=True, text=True, timeout=300, env=env).stdout
+        f32 = json.loads(out.strip().splitlines()[-1])
+        line["f32_colour"] = {"value": f32["value"], "unit": f32["unit"], "ms_per_frame": f32["ms_per_frame"],
+                              "path": "the same with NEXEL_DROPIN_PRECISION=f32 (fp32 colour, bf16x3 decoder)"}
         return line
     except Exception as e:  # noqa: BLE001 - reported, never required
         return {"error": f"{type(e).__name__}: {e}"}

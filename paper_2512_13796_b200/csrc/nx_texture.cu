@@ -336,6 +336,130 @@ __global__ void __launch_bounds__(64) texture_f64_kernel(const TextureArgs a) {
     if (n_q) atomicAdd(&a.stats->queries, static_cast<unsigned long long>(n_q));
 }
 
+
+// The reference field shape (16 levels x 2 features -> 64 -> 64 -> 48) at NX_PRECISION_F64:
+// one thread per slot, the fp64 weights in shared memory (broadcast reads), features in
+// registers, layers 1 and 2 interleaved — h1[o1] is formed and immediately folded into the
+// h2 accumulators, so every h2[o2] still sums its 64 terms in ascending order like
+// TextureMlp::forward (mlp.cpp:24-43) — in two halves of h2 to bound the registers (layer 1
+// is formed twice). Then eval_sh in fp64; Eq. 7 runs per pixel in final_f64_kernel.
+constexpr int kF64In = 32, kF64Hid = 64, kF64Half = 32;
+constexpr int kF64WBytes = (kF64Hid * kF64In + kF64Hid * kF64Hid + NX_SH_VALUES * kF64Hid) * 8;  // 72 KB
+
+__global__ void __launch_bounds__(128) texture_f64_slot_kernel(const TextureArgs a) {
+    extern __shared__ __align__(16) double wsm[];
+    double* w1 = wsm;
+    double* w2 = w1 + kF64Hid * kF64In;
+    double* w3 = w2 + kF64Hid * kF64Hid;
+    for (int i = threadIdx.x; i < kF64Hid * kF64In; i += blockDim.x) w1[i] = a.scene.w1_64[i];
+    for (int i = threadIdx.x; i < kF64Hid * kF64Hid; i += blockDim.x) w2[i] = a.scene.w2_64[i];
+    for (int i = threadIdx.x; i < NX_SH_VALUES * kF64Hid; i += blockDim.x) w3[i] = a.scene.w3_64[i];
+    __syncthreads();
+    const int K = a.fb.K;
+    const int64_t total = static_cast<int64_t>(a.cam.W) * a.cam.H * K;
+    const int64_t sl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (sl >= total) return;
+    if (a.fb.ids[sl] < 0) {
+        for (int c = 0; c < 3; ++c) {
+            a.fb.texture64[sl * 3 + c] = 0.0;
+            a.fb.texture[sl * 3 + c] = 0.f;
+        }
+        return;
+    }
+    const nx_field_desc& fd = a.scene.field;
+    const uint32_t T = 1u << fd.log2_table, mask = T - 1u;
+    const int64_t pix = sl / K;
+    const int px = static_cast<int>(pix % a.cam.W), py = static_cast<int>(pix / a.cam.W);
+    double dir[3];
+    pixel_dir(a.cam, px + 0.5, py + 0.5, dir);
+    const double t = a.fb.depths[sl];
+    const double x[3] = {a.cam.o[0] + t * dir[0], a.cam.o[1] + t * dir[1], a.cam.o[2] + t * dir[2]};
+    const double f = a.cam.fx;
+    double feats[kF64In];
+    double s = fd.base_scale;
+#pragma unroll
+    for (int l = 0; l < kF64In / 2; ++l, s *= fd.growth) {  // grid_lookup (hash_grid.cpp:26-83), F == 2
+        const double p0 = s * x[0], p1 = s * x[1], p2 = s * x[2];
+        const double fl0 = floor(p0), fl1 = floor(p1), fl2 = floor(p2);
+        const long long b0 = static_cast<long long>(fl0), b1 = static_cast<long long>(fl1),
+                        b2 = static_cast<long long>(fl2);
+        const double fr0 = p0 - fl0, fr1 = p1 - fl1, fr2 = p2 - fl2;
+        double dw = 1.0;
+        if (!a.st.no_downweight) {  // downweight (hash_grid.hpp:28-31)
+            const double r = f / (s * t);
+            dw = 1.0 - exp(-r * r / (2.0 * M_PI));
+        }
+        const double wx[2] = {1.0 - fr0, fr0}, wy[2] = {1.0 - fr1, fr1}, wz[2] = {1.0 - fr2, fr2};
+        double a0 = 0.0, a1 = 0.0;
+        const double2* slab = reinterpret_cast<const double2*>(a.scene.table64) + static_cast<size_t>(l) * T;
+#pragma unroll
+        for (int ci = 0; ci < 8; ++ci) {
+            const uint32_t row = (f64_map_positive(b0 + (ci & 1)) ^ (f64_map_positive(b1 + ((ci >> 1) & 1)) * 2654435761u) ^
+                                  (f64_map_positive(b2 + ((ci >> 2) & 1)) * 805459861u)) & mask;
+            const double w = wx[ci & 1] * wy[(ci >> 1) & 1] * wz[(ci >> 2) & 1];
+            const double2 v = __ldg(slab + row);
+            a0 += w * v.x;
+            a1 += w * v.y;
+        }
+        feats[2 * l] = a0 * dw;
+        feats[2 * l + 1] = a1 * dw;
+    }
+    double h2[kF64Hid];
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        double acc2[kF64Half];
+#pragma unroll
+        for (int o2 = 0; o2 < kF64Half; ++o2) acc2[o2] = 0.0;
+#pragma unroll 1
+        for (int o1 = 0; o1 < kF64Hid; ++o1) {
+            double h = 0.0;
+#pragma unroll
+            for (int i = 0; i < kF64In; ++i) h += w1[o1 * kF64In + i] * feats[i];
+            h = h > 0.0 ? h : 0.0;
+#pragma unroll
+            for (int o2 = 0; o2 < kF64Half; ++o2) acc2[o2] += w2[(half * kF64Half + o2) * kF64Hid + o1] * h;
+        }
+#pragma unroll
+        for (int o2 = 0; o2 < kF64Half; ++o2) h2[half * kF64Half + o2] = acc2[o2] > 0.0 ? acc2[o2] : 0.0;
+    }
+    double y[NX_SH_VALUES];
+#pragma unroll 4
+    for (int o = 0; o < NX_SH_VALUES; ++o) {
+        double v = 0.0;
+#pragma unroll
+        for (int i = 0; i < kF64Hid; ++i) v += w3[o * kF64Hid + i] * h2[i];
+        y[o] = v;
+    }
+    double rgb[3];
+    eval_sh_f64(y, dir, 3, rgb);  // field_forward: always degree 3 (texture_field.cpp:33)
+    for (int c = 0; c < 3; ++c) {
+        a.fb.texture64[sl * 3 + c] = rgb[c];
+        a.fb.texture[sl * 3 + c] = static_cast<float>(rgb[c]);
+    }
+}
+
+// Eq. 7 per pixel (renderer.cpp:219-236): final = base + sum_j W[p,j] texture[p,j], slot order.
+__global__ void final_f64_kernel(const TextureArgs a) {
+    const int64_t npix = static_cast<int64_t>(a.cam.W) * a.cam.H;
+    const int64_t pix = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (pix >= npix) return;
+    const int K = a.fb.K;
+    double acc[3] = {a.fb.base64[pix * 3 + 0], a.fb.base64[pix * 3 + 1], a.fb.base64[pix * 3 + 2]};
+    int n_q = 0;
+    for (int j = 0; j < K; ++j) {
+        const int64_t sl = pix * K + j;
+        if (a.fb.ids[sl] < 0) continue;
+        ++n_q;
+        const double w = a.fb.weights[sl];
+        for (int c = 0; c < 3; ++c) acc[c] += w * a.fb.texture64[sl * 3 + c];
+    }
+    for (int c = 0; c < 3; ++c) {
+        a.fb.final64[pix * 3 + c] = acc[c];
+        a.fb.final_img[pix * 3 + c] = static_cast<float>(acc[c]);
+    }
+    if (n_q) atomicAdd(&a.stats->queries, static_cast<unsigned long long>(n_q));
+}
+
 __global__ void copy_base64_kernel(const double* base64, const float* base, double* final64, float* final_img,
                                    int64_t n) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -354,11 +478,18 @@ int launch_texture(const TextureArgs& a, cudaStream_t s) {
         const nx_field_desc& fd = a.scene.field;
         if (fd.levels * fd.features > kF64MaxIn || fd.n_hidden > kF64MaxHidden) return NX_UNSUPPORTED;
         count_launch();
-        if (a.fb.K == 0)
+        if (a.fb.K == 0) {
             copy_base64_kernel<<<static_cast<unsigned>((npix * 3 + 255) / 256), 256, 0, s>>>(
                 a.fb.base64, a.fb.base, a.fb.final64, a.fb.final_img, npix * 3);
-        else
+        } else if (fd.levels == kF64In / 2 && fd.features == 2 && fd.n_hidden == kF64Hid) {
+            const int64_t total = npix * a.fb.K;
+            cudaFuncSetAttribute(texture_f64_slot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kF64WBytes);
+            count_launch();
+            texture_f64_slot_kernel<<<static_cast<unsigned>((total + 127) / 128), 128, kF64WBytes, s>>>(a);
+            final_f64_kernel<<<static_cast<unsigned>((npix + 255) / 256), 256, 0, s>>>(a);
+        } else {
             texture_f64_kernel<<<static_cast<unsigned>((npix + 63) / 64), 64, 0, s>>>(a);
+        }
         return NX_OK;
     }
     if (a.fb.K == 0) {
