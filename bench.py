@@ -90,30 +90,31 @@ def profile_json(rel):
         return None
 
 
-def composite_compute_roofline(comp_ms):
-    """The composite kernel against its real roof, the fp64 pipe: executed fp64 flops per
-    launch (2 x DFMA + DMUL + DADD thread instructions, ncu, profiles/r02/frame_metrics.json)
-    over the event-timed launch, of the measured fp64 peak (tools/fp64_peak.cu,
-    profiles/r02/fp64_peak.json), with ncu's fp64-pipe utilisation beside it."""
+def composite_compute_roofline(comp_ms, sm_mhz):
+    """The composite kernel against its real roof. It is bound by instruction issue on
+    dependent chains (fp64 intersect, SFU kernel value, the per-pixel march), not by HBM
+    (~1 % DRAM) nor by one pipe: achieved = executed warp instructions per launch (ncu,
+    profiles/r02/frame_metrics.json) over the event-timed launch, of the issue peak (4
+    warp instructions per clock per SM x 148 SMs x the measured SM clock); the fp64 pipe
+    (executed 2 DFMA + DMUL + DADD flops of the measured fp64 peak, tools/fp64_peak.cu)
+    beside it."""
     fm, pk = profile_json("r02/frame_metrics.json"), profile_json("r02/fp64_peak.json")
-    if not fm or not pk or not comp_ms:
+    if not fm or not comp_ms or not fm["composite"].get("warp_inst"):
         return None
     c = fm["composite"]
+    ginst = c["warp_inst"] / (comp_ms / 1e3) / 1e9
+    peak = 4 * 148 * (sm_mhz or 1965.0) / 1e3  # G warp-instructions / s
     flops = 2 * c["dfma"] + c["dmul"] + c["dadd"]
-    achieved = flops / (comp_ms / 1e3) / 1e12
-    pipe = None
-    try:
-        for line in open(os.path.join(ROOT, "profiles", "r02", "ncu_composite_summary.txt")):
-            if line.startswith("sm__pipe_fp64_cycles_active"):
-                pipe = float(line.split()[1])
-    except (OSError, ValueError):
-        pass
-    return {"bound": "fp64", "kernel": "composite", "achieved": achieved, "peak": pk["fp64_tflops"],
-            "unit": "TFLOP/s", "frac": achieved / pk["fp64_tflops"], "peak_source": "measured (tools/fp64_peak.cu)",
-            "flops_per_launch": flops, "flops_kind": "executed fp64 (2 DFMA + DMUL + DADD, ncu)",
-            "launch_ms": comp_ms, "fp64_pipe_pct_ncu": pipe,
-            "note": "latency-bound on dependent fp64 chains (intersect divisions, exp/log) at 28% occupancy; "
-                    "the HBM figure in `roofline` is kept for the contract"}
+    fp64 = None
+    if pk:
+        fp64_tf = flops / (comp_ms / 1e3) / 1e12
+        fp64 = {"achieved": fp64_tf, "peak": pk["fp64_tflops"], "unit": "TFLOP/s", "frac": fp64_tf / pk["fp64_tflops"],
+                "flops_per_launch": flops, "peak_source": "measured (tools/fp64_peak.cu)"}
+    return {"bound": "issue", "kernel": "composite (certified fp32 alpha)", "achieved": ginst, "peak": peak,
+            "unit": "G warp-instructions/s", "frac": ginst / peak, "warp_inst_per_launch": c["warp_inst"],
+            "launch_ms": comp_ms, "fp64": fp64,
+            "note": "ncu: issue slots 58 % busy, 28 % occupancy (96 registers, 10 CTAs / SM); the HBM figure in "
+                    "`roofline` is kept for the contract"}
 
 
 def dropin_line():
@@ -656,7 +657,7 @@ def run_ours(args):
             "frame_roofline": {"bytes_per_frame": fbytes, "achieved": frame_gbs, "peak": hbm_peak, "unit": "GB/s",
                                "frac": frame_gbs / hbm_peak, "formula": "240N + 8P + (28+24K)HW + 1024Q + 36864",
                                "measured": frame_measured},
-            "compute_roofline": composite_compute_roofline(stage_ms.get("composite")),
+            "compute_roofline": composite_compute_roofline(stage_ms.get("composite"), clk.get("sm_mhz") if clk else None),
             "decoder_roofline": decoder,
             # SURVEY.md §8(d) secondary compute figure: the reference-equivalent (pixel,
             # primitive) intersection tests — every key of the reference's tile lists times
