@@ -994,7 +994,11 @@ int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int64_t grid = std::min<int64_t>(n_tiles, sms);
+        static const int ws_ctas = [] {  // experiments: CTAs of the warp-specialised kernels
+            const char* e = getenv("NX_WS_CTAS");
+            return e ? atoi(e) : 0;
+        }();
+        const int64_t grid = std::min<int64_t>(n_tiles, ws_ctas > 0 ? ws_ctas : sms);
         if (path == 0) {
             cudaFuncSetAttribute(texture_ws_kernel<kGather>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  WsCfg<kGather>::kSmem);
