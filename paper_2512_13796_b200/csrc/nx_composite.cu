@@ -50,6 +50,10 @@ static_assert(kWorkTile == 8, "warp blocks are 8x4 pixels");
 #define NX_NEAR_COUNTERS 1
 #endif
 constexpr bool kNear = NX_NEAR_COUNTERS;  // near-threshold decision counters (FrameStatsD::near)
+#ifndef NX_QUAD_CULL
+#define NX_QUAD_CULL 1
+#endif
+constexpr bool kQuadCull = NX_QUAD_CULL;  // per-warp cull of the projected support (sel phase)
 static_assert(kChunk <= 256 && kSub <= 8, "pool entries pack (lane, group slot) in 16 bits");
 
 template <typename CT>  // colour type: float, or double for NX_PRECISION_F64
@@ -87,6 +91,7 @@ struct SmemLayout {
     float4 f[kChunk][4];
     int32_t id[kChunk];
     double dir[kThreads][3];
+    float cdir[kWarps][4][3];  // the ray directions of each warp block's corner pixels
     WarpStage<PE> w[kWarps];
 };
 
@@ -151,6 +156,19 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
     sm.dir[threadIdx.x][0] = dir[0];
     sm.dir[threadIdx.x][1] = dir[1];
     sm.dir[threadIdx.x][2] = dir[2];
+    // the warp block's corner pixels (lanes 0, 7, 24, 31): the per-warp cull of the
+    // projected support below needs every corner in the image
+    const uint32_t in_mask = __ballot_sync(0xffffffffu, in_img);
+    constexpr uint32_t kCorners = (1u << 0) | (1u << 7) | (1u << 24) | (1u << 31);
+    const bool quad_ok = kQuadCull && (in_mask & kCorners) == kCorners;
+    {
+        const int ci = lane == 0 ? 0 : lane == 7 ? 1 : lane == 24 ? 2 : lane == 31 ? 3 : -1;
+        if (ci >= 0) {
+            sm.cdir[warp][ci][0] = static_cast<float>(dir[0]);
+            sm.cdir[warp][ci][1] = static_cast<float>(dir[1]);
+            sm.cdir[warp][ci][2] = static_cast<float>(dir[2]);
+        }
+    }
     const float dfx = static_cast<float>(dir[0]), dfy = static_cast<float>(dir[1]), dfz = static_cast<float>(dir[2]);
 
     double T = 1.0;
@@ -213,6 +231,36 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                     const float4 f3 = sm.f[b][3];
                     const int rx = __float_as_int(f3.z), ry = __float_as_int(f3.w);
                     ov = !((rx >> 16) < wx0 || (rx & 0xffff) > wx1 || (ry >> 16) < wy0 || (ry & 0xffff) > wy1);
+                    if (ov && quad_ok) {
+                        // The plane offsets (u, v) of the block's pixel rays are a projective
+                        // image of the pixel rectangle, so they lie in the quadrilateral of
+                        // the corner rays' offsets when all four cross the plane on one side:
+                        // if that quadrilateral (enlarged by the prefilter's slack) misses the
+                        // support box, every pixel of the block misses.
+                        const float4 f0 = sm.f[b][0], f1 = sm.f[b][1], f2 = sm.f[b][2];
+                        float umin = 3e38f, umax = -3e38f, vmin = 3e38f, vmax = -3e38f, su = 0.f, sv = 0.f;
+                        bool valid = true;
+                        float sgn = 0.f;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const float dx = sm.cdir[warp][c][0], dy = sm.cdir[warp][c][1], dz = sm.cdir[warp][c][2];
+                            const float den = dx * f0.x + dy * f0.y + dz * f0.z;
+                            valid &= fabsf(den) >= 1e-2f && (c == 0 || den * sgn > 0.f);
+                            sgn = den;
+                            const float ta = __fdividef(f0.w, den);
+                            const float ta1 = ta * (dx * f1.x + dy * f1.y + dz * f1.z);
+                            const float ta2 = ta * (dx * f2.x + dy * f2.y + dz * f2.z);
+                            const float u = ta1 - f1.w, v = ta2 - f2.w;
+                            umin = fminf(umin, u);
+                            umax = fmaxf(umax, u);
+                            vmin = fminf(vmin, v);
+                            vmax = fmaxf(vmax, v);
+                            su = fmaxf(su, 1e-4f * (fabsf(ta1) + fabsf(ta) + fabsf(f1.w)) + 1e-7f);
+                            sv = fmaxf(sv, 1e-4f * (fabsf(ta2) + fabsf(ta) + fabsf(f2.w)) + 1e-7f);
+                        }
+                        if (valid && (umin > f3.x + su || umax < -f3.x - su || vmin > f3.y + sv || vmax < -f3.y - sv))
+                            ov = false;
+                    }
                     if (ov) {  // lane l = pixel (bx0 + l % 8, by0 + l / 8): the rect's columns x its rows
                         const int cx0 = max((rx & 0xffff) - bx0, 0), cx1 = min((rx >> 16) - bx0, 7);
                         const int ry0 = max((ry & 0xffff) - by0, 0), ry1 = min((ry >> 16) - by0, 3);
