@@ -119,6 +119,7 @@ struct nx_ctx {
     // when it is first read back (frame_settle).
     int64_t key_cap = 0;
     bool sync_lists = false;  // NX_SYNC_LISTS=1: size every build from its own count (host round trip)
+    bool emit_cull = true;    // NX_EMIT_CULL=0: keep every work-rect key (no corner-ray cull)
     bool profiling = false;
     cudaStream_t stream2 = nullptr;  // texture passes: overlap the next frame's collection
     cudaStream_t stream3 = nullptr;  // downloads: the copy engine overlaps both
@@ -540,12 +541,28 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
         sc = d_total + 64;
     }
     NX_CUDA(c, cudaMemsetAsync(c->tile_counts.as<int32_t>(), 0, (n_tiles + 1) * sizeof(int32_t), s));
+    EmitCull cull;  // work lists: keys the corner-ray quadrilateral proves empty go past the last tile
+    cull.n_tiles = static_cast<int>(n_tiles);
+    if (!reference_lists && c->emit_cull) {
+        cull.recf = c->recf.as<float4>();
+        cull.tiles_x = f->ltiles_x;
+        cull.tile = lt;
+        cull.W = cam.width;
+        cull.H = cam.height;
+        cull.cx = static_cast<float>(cd.cx);
+        cull.cy = static_cast<float>(cd.cy);
+        cull.ifx = static_cast<float>(1.0 / cd.fx);
+        cull.ify = static_cast<float>(1.0 / cd.fy);
+        for (int q = 0; q < 9; ++q) cull.R[q] = static_cast<float>(cd.R[q]);
+    }
     launch_emit(sorted_ids, c->offsets.as<int32_t>(), n, d_total, cap, d_total + 1, c->work_rect.as<int4>(),
-                f->ltiles_x, c->tkeys_a.as<uint32_t>(), c->tvals_a.as<uint32_t>(), c->tile_counts.as<int32_t>(), s);
+                f->ltiles_x, c->tkeys_a.as<uint32_t>(), c->tvals_a.as<uint32_t>(), c->tile_counts.as<int32_t>(), cull,
+                s);
 
-    // K4: stable sort by tile (over the device count, capped by the capacity).
+    // K4: stable sort by tile (over the device count, capped by the capacity); the cull's
+    // sentinel n_tiles sorts past every list
     record(c, kEvTileSort, s);
-    const int tb = std::max(bits_for(n_tiles), 1);
+    const int tb = std::max(bits_for(n_tiles + 1), 1);
     const bool t_in_b = radix_sort_pairs_u32(c->tkeys_a.as<uint32_t>(), c->tvals_a.as<uint32_t>(),
                                              c->tkeys_b.as<uint32_t>(), c->tvals_b.as<uint32_t>(), cap, d_total + 1,
                                              0, tb, sc, s);
@@ -735,6 +752,7 @@ int nx_ctx_create(int device, nx_ctx** out) {
     cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
     if (const char* e = std::getenv("NX_SYNC_LISTS")) c->sync_lists = std::atoi(e) != 0;
     if (const char* e = std::getenv("NX_CERTIFIED")) c->certified = std::atoi(e) != 0;
+    if (const char* e = std::getenv("NX_EMIT_CULL")) c->emit_cull = std::atoi(e) != 0;
     if (const char* e = std::getenv("NX_CERT_REDO_ALL")) c->redo_all = std::atoi(e) != 0;
     if (const char* e = std::getenv("NX_KEY_CAP")) c->key_cap = std::atoll(e);  // tests: start from a small capacity
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||

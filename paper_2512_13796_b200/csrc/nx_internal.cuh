@@ -236,9 +236,17 @@ void launch_rect_counts(const uint32_t* ids, int64_t n, const int32_t* n_dev, co
 // order (row-major tiles, renderer.cpp:106-110), and counts keys per tile. The sorted
 // count and key count are read on the device (*n_sorted_dev, *n_keys_dev); keys past
 // the capacity key_cap are not written (nor counted).
+// The work-list cull of emit (tiles whose corner rays' support quadrilateral misses):
+// recf == nullptr disables it (reference lists stay the reference's).
+struct EmitCull {
+    const float4* recf = nullptr;
+    int n_tiles = 0, tiles_x = 0, tile = 8, W = 0, H = 0;
+    float cx = 0.f, cy = 0.f, ifx = 1.f, ify = 1.f;
+    float R[9] = {};
+};
 void launch_emit(const uint32_t* ids, const int32_t* offsets, int64_t sorted_cap, const int32_t* n_sorted_dev,
                  int64_t key_cap, const int32_t* n_keys_dev, const int4* rect, int tiles_x, uint32_t* tile_keys,
-                 uint32_t* vals, int32_t* tile_counts, cudaStream_t s);
+                 uint32_t* vals, int32_t* tile_counts, const EmitCull& cull, cudaStream_t s);
 
 struct CompositeArgs {
     const double* rec;   // n x REC_FIELDS

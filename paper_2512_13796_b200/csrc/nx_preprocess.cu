@@ -294,10 +294,55 @@ __global__ void rect_counts_kernel(const uint32_t* ids, int64_t n, const int32_t
 // One thread per emitted key: binary search of the owning sorted primitive. Counts on
 // the device; the grid covers the capacity (keys past it are dropped: the frame is
 // re-rendered with a larger capacity before it is read, nx_api.cu frame_settle).
+// Conservative cull of a (tile, primitive) key (work lists only): the plane offsets of
+// the tile's pixel rays are a projective image of the pixel rectangle, so they lie in the
+// quadrilateral of its corner rays' offsets (all four crossing the plane on one side);
+// if that quadrilateral, enlarged by the fp32 prefilter's slack, misses the support box
+// [-ulim, ulim] x [-vlim, vlim], no pixel of the tile can hit the primitive.
+__device__ __forceinline__ bool tile_misses(const float4* f, const EmitCull& cu, int tile) {
+    const int tx = tile % cu.tiles_x, ty = tile / cu.tiles_x;
+    const int x0 = tx * cu.tile, y0 = ty * cu.tile;
+    const int x1 = min(x0 + cu.tile - 1, cu.W - 1), y1 = min(y0 + cu.tile - 1, cu.H - 1);
+    const float4 f0 = f[0], f1 = f[1], f2 = f[2], f3 = f[3];
+    float umin = 3e38f, umax = -3e38f, vmin = 3e38f, vmax = -3e38f, su = 0.f, sv = 0.f, sgn = 0.f;
+    bool valid = true;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const float px = ((c & 1) ? x1 : x0) + 0.5f, py = ((c & 2) ? y1 : y0) + 0.5f;
+        // pixel_ray (camera.hpp:32-35) in fp32: R^T normalize(((px - cx)/fx, (py - cy)/fy, 1))
+        const float a0 = (px - cu.cx) * cu.ifx, a1 = (py - cu.cy) * cu.ify;
+        const float rn = rsqrtf(a0 * a0 + a1 * a1 + 1.f);
+        const float n0 = a0 * rn, n1 = a1 * rn, n2 = rn;
+        const float dx = cu.R[0] * n0 + cu.R[3] * n1 + cu.R[6] * n2;
+        const float dy = cu.R[1] * n0 + cu.R[4] * n1 + cu.R[7] * n2;
+        const float dz = cu.R[2] * n0 + cu.R[5] * n1 + cu.R[8] * n2;
+        const float den = dx * f0.x + dy * f0.y + dz * f0.z;
+        valid &= fabsf(den) >= 1e-2f && (c == 0 || den * sgn > 0.f);
+        sgn = den;
+        const float ta = __fdividef(f0.w, den);
+        const float ta1 = ta * (dx * f1.x + dy * f1.y + dz * f1.z);
+        const float ta2 = ta * (dx * f2.x + dy * f2.y + dz * f2.z);
+        const float u = ta1 - f1.w, v = ta2 - f2.w;
+        umin = fminf(umin, u);
+        umax = fmaxf(umax, u);
+        vmin = fminf(vmin, v);
+        vmax = fmaxf(vmax, v);
+        // the prefilter's slack (fp32 rounding of t and the offsets), doubled for the
+        // fp32 ray direction here
+        su = fmaxf(su, 2e-4f * (fabsf(ta1) + fabsf(ta) + fabsf(f1.w)) + 2e-7f);
+        sv = fmaxf(sv, 2e-4f * (fabsf(ta2) + fabsf(ta) + fabsf(f2.w)) + 2e-7f);
+    }
+    return valid && (umin > f3.x + su || umax < -f3.x - su || vmin > f3.y + sv || vmax < -f3.y - sv);
+}
+
+// One thread per emitted key: binary search of the owning sorted primitive. Counts on
+// the device; the grid covers the capacity (keys past it are dropped: the frame is
+// re-rendered with a larger capacity before it is read, nx_api.cu frame_settle). Keys
+// the cull proves empty go to the sentinel tile n_tiles (sorted past every list).
 __global__ void emit_kernel(const uint32_t* ids, const int32_t* offsets, int64_t sorted_cap,
                             const int32_t* n_sorted_dev, int64_t key_cap, const int32_t* n_keys_dev,
                             const int4* rect, int tiles_x, uint32_t* tile_keys, uint32_t* vals,
-                            int32_t* tile_counts) {
+                            int32_t* tile_counts, const EmitCull cu) {
     __shared__ int64_t s_lo, s_hi;
     const int64_t n_sorted = min(sorted_cap, static_cast<int64_t>(max(*n_sorted_dev, 0)));
     const int64_t n_keys = n_sorted > 0 ? min(key_cap, static_cast<int64_t>(max(*n_keys_dev, 0))) : 0;
@@ -324,10 +369,11 @@ __global__ void emit_kernel(const uint32_t* ids, const int32_t* offsets, int64_t
         const int4 rc = rect[id];
         const int j = static_cast<int>(k - offsets[lo]);
         const int w = rc.y - rc.x + 1;
-        const int tile = (rc.z + j / w) * tiles_x + rc.x + j % w;
+        int tile = (rc.z + j / w) * tiles_x + rc.x + j % w;
+        if (cu.recf && tile_misses(cu.recf + static_cast<int64_t>(id) * 4, cu, tile)) tile = cu.n_tiles;
         tile_keys[k] = static_cast<uint32_t>(tile);
         vals[k] = id;
-        atomicAdd(&tile_counts[tile], 1);
+        if (tile < cu.n_tiles) atomicAdd(&tile_counts[tile], 1);
     }
 }
 
@@ -392,7 +438,7 @@ void launch_rect_counts(const uint32_t* ids, int64_t n, const int32_t* n_dev, co
 
 void launch_emit(const uint32_t* ids, const int32_t* offsets, int64_t sorted_cap, const int32_t* n_sorted_dev,
                  int64_t key_cap, const int32_t* n_keys_dev, const int4* rect, int tiles_x, uint32_t* tile_keys,
-                 uint32_t* vals, int32_t* tile_counts, cudaStream_t s) {
+                 uint32_t* vals, int32_t* tile_counts, const EmitCull& cull, cudaStream_t s) {
     if (key_cap <= 0 || sorted_cap <= 0) return;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -400,7 +446,8 @@ void launch_emit(const uint32_t* ids, const int32_t* offsets, int64_t sorted_cap
     const int64_t grid = std::min<int64_t>((key_cap + 255) / 256, static_cast<int64_t>(sms) * 8);
     count_launch();
     emit_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(ids, offsets, sorted_cap, n_sorted_dev, key_cap,
-                                                             n_keys_dev, rect, tiles_x, tile_keys, vals, tile_counts);
+                                                             n_keys_dev, rect, tiles_x, tile_keys, vals, tile_counts,
+                                                             cull);
 }
 
 }  // namespace nx
