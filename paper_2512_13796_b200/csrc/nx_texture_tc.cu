@@ -1041,7 +1041,12 @@ int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
             cudaEventRecord(a.ev_mid, s);
             a.ev_mid_recorded = true;
         }
-        const int64_t grid = std::min<int64_t>(n_tiles, static_cast<int64_t>(kCtasPerSm) * sms);
+        static const int mlp_per_sm = [] {  // decoder CTAs per SM (NX_MLP_CTAS_PER_SM, experiments)
+            const char* e = getenv("NX_MLP_CTAS_PER_SM");
+            const int v = e ? atoi(e) : kCtasPerSm;
+            return v < 1 ? 1 : (v > kCtasPerSm ? kCtasPerSm : v);
+        }();
+        const int64_t grid = std::min<int64_t>(n_tiles, static_cast<int64_t>(mlp_per_sm) * sms);
         tex_mlp_kernel<<<static_cast<unsigned>(grid), kTcThreads, kSmemUsed, s>>>(a, ppt, n_tiles);
         return NX_OK;
     }
