@@ -939,20 +939,214 @@ __global__ void __launch_bounds__(128) tex_features_img_kernel(const TextureArgs
     for (int c = 0; c < kIn / 8; ++c) store_split8(img, 0, kImgBytes / 2, kmajor_off(row, 8 * c, kIn), feats + 8 * c);
 }
 
+
+// ---------------------------------------------------------------- split2: bulk-fed decoder
+// The split pass with the gathers writing pre-split operand tiles (tex_features_img_kernel)
+// and a single-role decoder that streams them with the bulk-copy engine: while a tile's
+// three layers run, the next tile's 16 KB operand image lands in the other of two
+// buffers (cp.async.bulk + mbarrier transaction count); layer 1 reads it in place (no
+// register round trip, no split on this side). Two 128-thread CTAs per SM (~101 KB).
+constexpr int kB2OffImg = kOffAh + 2 * kRows * kHid * 2;        // after the 64-wide A operand
+constexpr int kB2OffRgb = kB2OffImg + 2 * kImgBytes;             // two image buffers
+constexpr int kB2OffBar = kB2OffRgb + kRows * 3 * 4;             // mma, full[2]
+constexpr int kB2OffTmem = kB2OffBar + 3 * 8;
+constexpr int kB2Smem = kB2OffTmem + 8;
+static_assert(kB2Smem <= 113 * 1024, "two CTAs per SM");
+
+__device__ __forceinline__ void b2_issue_layer(uint8_t* smem, uint32_t dtm, int a_hi, int a_lo, int off_bh, int off_bl,
+                                               int K, uint32_t idesc, uint32_t bar) {
+    const uint32_t ah = smem_u32(smem + a_hi), al = smem_u32(smem + a_lo);
+    const uint32_t bh = smem_u32(smem + off_bh), bl = smem_u32(smem + off_bl);
+    const uint32_t sbo = 16 * K;
+    for (int s = 0; s < K / 16; ++s) {
+        const uint32_t o = s * 256;
+        mma_bf16(dtm, smem_desc(ah + o, 128, sbo), smem_desc(bh + o, 128, sbo), idesc, s > 0);
+        mma_bf16(dtm, smem_desc(ah + o, 128, sbo), smem_desc(bl + o, 128, sbo), idesc, 1);
+        mma_bf16(dtm, smem_desc(al + o, 128, sbo), smem_desc(bh + o, 128, sbo), idesc, 1);
+    }
+    mma_commit(bar);
+}
+
+__global__ void __launch_bounds__(kTcThreads, 2) tex_mlp_bulk_kernel(const TextureArgs a, int bw, int bh, int tiles_x,
+                                                                   int64_t n_tiles) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t bar = smem_u32(smem + kB2OffBar);
+    auto full = [&](int b) { return smem_u32(smem + kB2OffBar + 8 * (1 + b)); };
+    for (int e = tid; e < kHid * kIn / 8; e += kTcThreads) {  // W1 [64][32]
+        const int n = e / (kIn / 8), c = e % (kIn / 8);
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(a.scene.w1 + n * kIn + c * 8 + i);
+        store_split8(smem, kOffW1h, kOffW1l, kmajor_off(n, c * 8, kIn), x);
+    }
+    for (int e = tid; e < kHid * kHid / 8; e += kTcThreads) {  // W2 [64][64]
+        const int n = e / (kHid / 8), c = e % (kHid / 8);
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(a.scene.w2 + n * kHid + c * 8 + i);
+        store_split8(smem, kOffW2h, kOffW2l, kmajor_off(n, c * 8, kHid), x);
+    }
+    for (int e = tid; e < kOut * kHid / 8; e += kTcThreads) {  // W3 [48][64]
+        const int n = e / (kHid / 8), c = e % (kHid / 8);
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(a.scene.w3 + n * kHid + c * 8 + i);
+        store_split8(smem, kOffW3h, kOffW3l, kmajor_off(n, c * 8, kHid), x);
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem + kB2OffTmem)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 32) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full(0)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full(1)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + kB2OffTmem);
+    uint32_t phase = 0;
+    const int K = a.fb.K, W = a.cam.W, H = a.cam.H;
+    const int row = tid, ppt = bw * bh;
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * warp) << 16);
+    float* srgb = reinterpret_cast<float*>(smem + kB2OffRgb);
+    constexpr uint32_t kIdesc64 = idesc_bf16_f32(kRows, 64);
+    constexpr uint32_t kIdesc48 = idesc_bf16_f32(kRows, 48);
+    const uint8_t* img = reinterpret_cast<const uint8_t*>(a.fscratch);
+    auto load_tile = [&](int64_t tile, int b) {  // thread 0: the tile's 16 KB image into buffer b
+        const uint32_t dst = smem_u32(smem + kB2OffImg + b * kImgBytes);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full(b)), "r"(kImgBytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                     "l"(img + tile * kImgBytes), "r"(kImgBytes), "r"(full(b))
+                     : "memory");
+    };
+    int n_queries = 0;
+    int64_t k = 0;
+    if (tid == 0 && blockIdx.x < n_tiles) load_tile(blockIdx.x, 0);
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+        const int b = static_cast<int>(k & 1);
+        // the other buffer's last reader (the previous tile's layer 1) has completed
+        if (tid == 0 && tile + gridDim.x < n_tiles) load_tile(tile + gridDim.x, b ^ 1);
+        const WsTile wt = ws_tile(tile, row, K, bw, bh, tiles_x, W, H);
+        const bool valid = wt.in_tile && a.fb.ids[wt.slot] >= 0;
+        n_queries += valid;
+        mbar_wait(full(b), static_cast<uint32_t>((k >> 1) & 1));
+        tc_fence_after();
+        const int ib = kB2OffImg + b * kImgBytes;
+        if (tid == 0) b2_issue_layer(smem, tmem, ib, ib + kImgBytes / 2, kOffW1h, kOffW1l, kIn, kIdesc64, bar);
+        double dir[3] = {0.0, 0.0, 1.0};
+        if (wt.in_tile) pixel_dir(a.cam, wt.px + 0.5, wt.py + 0.5, dir);
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+#pragma unroll 1
+        for (int layer = 0; layer < 2; ++layer) {
+#pragma unroll
+            for (int c = 0; c < kHid / 16; ++c) {
+                float v[16];
+                tmem_ld16(taddr + 16 * c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
+                store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 16 * c, kHid), v);
+                store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 16 * c + 8, kHid), v + 8);
+            }
+            fence_async_smem();
+            tc_fence_before();
+            __syncthreads();
+            if (tid == 0) {
+                if (layer == 0) b2_issue_layer(smem, tmem, kOffAh, kOffAl, kOffW2h, kOffW2l, kHid, kIdesc64, bar);
+                else b2_issue_layer(smem, tmem, kOffAh, kOffAl, kOffW3h, kOffW3l, kHid, kIdesc48, bar);
+            }
+            mbar_wait(bar, phase);
+            phase ^= 1;
+            tc_fence_after();
+        }
+        {
+            float bb[16];
+            sh_basis_f32(static_cast<float>(dir[0]), static_cast<float>(dir[1]), static_cast<float>(dir[2]), bb);
+            float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+#pragma unroll
+            for (int c = 0; c < kOut / 16; ++c) {
+                float v[16];
+                tmem_ld16(taddr + 16 * c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int o = 16 * c + i, kk = o / 3;
+                    if (o % 3 == 0) c0 = fmaf(v[i], bb[kk], c0);
+                    else if (o % 3 == 1) c1 = fmaf(v[i], bb[kk], c1);
+                    else c2 = fmaf(v[i], bb[kk], c2);
+                }
+            }
+            float rgb[3] = {0.f, 0.f, 0.f};
+            if (valid) {
+                rgb[0] = fmaxf(0.5f + c0, 0.f);
+                rgb[1] = fmaxf(0.5f + c1, 0.f);
+                rgb[2] = fmaxf(0.5f + c2, 0.f);
+            }
+            srgb[row * 3 + 0] = rgb[0];
+            srgb[row * 3 + 1] = rgb[1];
+            srgb[row * 3 + 2] = rgb[2];
+            if (wt.in_tile) {
+                a.fb.texture[wt.slot * 3 + 0] = rgb[0];
+                a.fb.texture[wt.slot * 3 + 1] = rgb[1];
+                a.fb.texture[wt.slot * 3 + 2] = rgb[2];
+            }
+        }
+        tc_fence_before();
+        __syncthreads();
+        // Eq. 7: final = base + sum_j W[p,j] * texture[p,j] (renderer.cpp:219-236)
+        if (row < ppt) {
+            const int tpx = static_cast<int>(tile % tiles_x) * bw, tpy = static_cast<int>(tile / tiles_x) * bh;
+            const int qx = tpx + row % bw, qy = tpy + row / bw;
+            if (qx < W && qy < H) {
+                const int64_t pix = static_cast<int64_t>(qy) * W + qx;
+                double acc0 = a.fb.base[pix * 3 + 0], acc1 = a.fb.base[pix * 3 + 1], acc2 = a.fb.base[pix * 3 + 2];
+                for (int j = 0; j < K; ++j) {
+                    const int64_t q = pix * K + j;
+                    if (a.fb.ids[q] < 0) continue;
+                    const double w = a.fb.weights[q];
+                    const float* tc = srgb + (row * K + j) * 3;
+                    acc0 += w * tc[0];
+                    acc1 += w * tc[1];
+                    acc2 += w * tc[2];
+                }
+                a.fb.final_img[pix * 3 + 0] = static_cast<float>(acc0);
+                a.fb.final_img[pix * 3 + 1] = static_cast<float>(acc1);
+                a.fb.final_img[pix * 3 + 2] = static_cast<float>(acc2);
+            }
+        }
+        // srgb and the A operand are rewritten next tile only after its layer-1 wait and
+        // the barrier before layer 2, which every thread reaches after this point
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n_queries += __shfl_down_sync(0xffffffffu, n_queries, o);
+    if ((tid & 31) == 0 && n_queries) atomicAdd(&a.stats->queries, static_cast<unsigned long long>(n_queries));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
 }  // namespace
 
 int texture_tc_path() {
-    // Measured at config 2 (ms per frame, two streams / one stream): split 2.84 / 3.09,
-    // bulk-fed warp-specialised with 4 epilogue groups 2.96 / 2.99 (2 groups: 3.16 /
-    // 3.19), gather warp-specialised 3.27 / 3.32. The warp-specialised kernels hold one
-    // ~170-200 KB CTA per SM, so the next frame's composite cannot share the SM while
-    // they run; split stays the default.
+    // Measured at config 2 (ms per frame, two streams / one stream; round-2 composite):
+    // split2 2.45 / 2.80 (default), split 2.53 / 2.78, bulk-fed warp-specialised with 4
+    // epilogue groups 2.81 / 2.82, gather warp-specialised 3.05 / 3.12. The warp-
+    // specialised kernels hold one ~170-200 KB CTA per SM, so the next frame's composite
+    // cannot share the SM while they run.
     static const int path = [] {
         const char* e = getenv("NX_TEXTURE_PATH");
         if (e && strcmp(e, "fused") == 0) return 1;
         if (e && strcmp(e, "ws") == 0) return 0;
         if (e && strcmp(e, "bulk") == 0) return 3;
-        return 2;
+        if (e && strcmp(e, "split") == 0) return 2;
+        return 4;
     }();
     return path;
 }
@@ -961,7 +1155,7 @@ size_t texture_tc_scratch_bytes(int W, int H, int K) {
     if (K <= 0) return 0;
     const int path = texture_tc_path();
     if (path == 2) return static_cast<size_t>(W) * H * K * kIn * sizeof(float);
-    if (path != 3) return 0;
+    if (path != 3 && path != 4) return 0;
     const int ppt = kRows / K;
     const int bw = (kRows % K == 0 && ppt % 8 == 0) ? 8 : ppt;
     const int bh = ppt / bw;
@@ -978,7 +1172,7 @@ int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
     // over a feature scratch), "ws" (warp-specialised, no scratch) or "fused" (one CTA
     // role, three per SM).
     const int path = texture_tc_path();
-    if ((path == 0 || (path == 3 && a.fscratch)) && K > 0) {
+    if ((path == 0 || ((path == 3 || path == 4) && a.fscratch)) && K > 0) {
         const int ppt = kRows / K;
         const int bw = (kRows % K == 0 && ppt % 8 == 0) ? 8 : ppt;
         const int bh = ppt / bw;
@@ -1008,14 +1202,20 @@ int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
             return NX_OK;
         }
         const int64_t total = static_cast<int64_t>(a.cam.W) * a.cam.H * K;
-        cudaFuncSetAttribute(texture_ws_kernel<kBulk>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             WsCfg<kBulk>::kSmem);
         count_launch(2);
         tex_features_img_kernel<<<static_cast<unsigned>((total + 127) / 128), 128, 0, s>>>(a, cst, bw, bh, tiles_x);
         if (a.ev_mid) {
             cudaEventRecord(a.ev_mid, s);
             a.ev_mid_recorded = true;
         }
+        if (path == 4) {  // split2: the single-role decoder fed by bulk copies, two CTAs per SM
+            cudaFuncSetAttribute(tex_mlp_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kB2Smem);
+            const int64_t g2 = std::min<int64_t>(n_tiles, 2 * static_cast<int64_t>(sms));
+            tex_mlp_bulk_kernel<<<static_cast<unsigned>(g2), kTcThreads, kB2Smem, s>>>(a, bw, bh, tiles_x, n_tiles);
+            return NX_OK;
+        }
+        cudaFuncSetAttribute(texture_ws_kernel<kBulk>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             WsCfg<kBulk>::kSmem);
         texture_ws_kernel<kBulk><<<static_cast<unsigned>(grid), WsCfg<kBulk>::kThreads, WsCfg<kBulk>::kSmem, s>>>(
             a, cst, bw, bh, tiles_x, n_tiles);
         return NX_OK;

@@ -101,13 +101,13 @@ def test_tensor_core_texture_variants_are_bit_identical(K):
             "r = nx.Renderer(0); d = r.upload(s); f = r.frame(); r.render(d, c, f); g = f.download(); "
             "np.savez(sys.argv[1], t=g.texture, f=g.final_img, ids=g.ids)") % (os.path.dirname(HERE), n, K, w, h)
     out = {}
-    for path in ("bulk", "ws", "split", "fused"):
+    for path in ("bulk", "ws", "split", "fused", "split2"):
         fn = f"/tmp/nx_texv_{path}_{K}_{os.getpid()}.npz"
         env = dict(os.environ)
         env["NX_TEXTURE_PATH"] = path
         subprocess.run([sys.executable, "-c", code, fn], check=True, env=env, timeout=900)
         out[path] = np.load(fn)
     assert (out["bulk"]["ids"] >= 0).sum() > 0
-    for other in ("ws", "split", "fused"):
+    for other in ("ws", "split", "fused", "split2"):
         assert np.array_equal(out["bulk"]["t"], out[other]["t"]), other
         assert np.array_equal(out["bulk"]["f"], out[other]["f"]), other
