@@ -74,6 +74,9 @@ constexpr uint16_t kComposited = 0x80;  // q entry flag set by B2 (list index j 
 
 struct WarpSmem {        // one warp's private staging (no sharing between warps)
     float4 f[kChunk][4];
+    uint8_t sel[kChunk];     // chunk slots whose support may meet the warp's block (list order)
+    uint32_t lmask[kChunk];  // and the block's lanes inside their pixel rects
+    float cdir[4][3];        // the block's corner-pixel ray directions (support cull)
     double dir[32][3];
     float basis[32][16];  // per-pixel SH basis (fp32)
     BwdEntry res[kPool];
@@ -163,6 +166,19 @@ __global__ void __launch_bounds__(kTile * kTile, 512 / (kTile * kTile)) composit
     sm.dir[lane][2] = dir[2];
     const float dfx = static_cast<float>(dir[0]), dfy = static_cast<float>(dir[1]), dfz = static_cast<float>(dir[2]);
     sh_basis_f32(dfx, dfy, dfz, sm.basis[lane]);
+    // the block's corner pixels (lanes 0, 7, 24, 31) for the support cull (as the forward)
+    const uint32_t in_mask = __ballot_sync(0xffffffffu, in_img);
+    constexpr uint32_t kCorners = (1u << 0) | (1u << 7) | (1u << 24) | (1u << 31);
+    const bool quad_ok = (in_mask & kCorners) == kCorners;
+    {
+        const int ci = lane == 0 ? 0 : lane == 7 ? 1 : lane == 24 ? 2 : lane == 31 ? 3 : -1;
+        if (ci >= 0) {
+            sm.cdir[ci][0] = dfx;
+            sm.cdir[ci][1] = dfy;
+            sm.cdir[ci][2] = dfz;
+        }
+    }
+    const int bx0 = tx * kTile + (warp % kAcross) * 8, by0 = ty * kTile + (warp / kAcross) * 4;
 
     // per-pixel upstream state
     const int64_t pix = in_img ? static_cast<int64_t>(py) * W + px : 0;
@@ -222,19 +238,66 @@ __global__ void __launch_bounds__(kTile * kTile, 512 / (kTile * kTile)) composit
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
-        for (int sb = 0; sb < cn; sb += kSub) {
-            const int sn = min(kSub, cn - sb);
-            // ---- A. screen-space cull + fp32 prefilter (as the forward)
+        // the chunk's primitives whose support may meet this warp's block, in list order:
+        // pixel rect overlap, then the corner-ray quadrilateral (nx_composite.cu)
+        int nsel = 0;
+        {
+            bool ov = false;
+            uint32_t lm = 0;
+            if (lane < cn) {
+                const float4 f3 = sm.f[lane][3];
+                const int rx = __float_as_int(f3.z), ry = __float_as_int(f3.w);
+                ov = !((rx >> 16) < wx0 || (rx & 0xffff) > wx1 || (ry >> 16) < wy0 || (ry & 0xffff) > wy1);
+                if (ov && quad_ok) {
+                    const float4 f0 = sm.f[lane][0], f1 = sm.f[lane][1], f2 = sm.f[lane][2];
+                    float umin = 3e38f, umax = -3e38f, vmin = 3e38f, vmax = -3e38f, su = 0.f, sv = 0.f, sgn = 0.f;
+                    bool valid = true;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const float dx = sm.cdir[c][0], dy = sm.cdir[c][1], dz = sm.cdir[c][2];
+                        const float den = dx * f0.x + dy * f0.y + dz * f0.z;
+                        valid &= fabsf(den) >= 1e-2f && (c == 0 || den * sgn > 0.f);
+                        sgn = den;
+                        const float ta = __fdividef(f0.w, den);
+                        const float ta1 = ta * (dx * f1.x + dy * f1.y + dz * f1.z);
+                        const float ta2 = ta * (dx * f2.x + dy * f2.y + dz * f2.z);
+                        const float u = ta1 - f1.w, v = ta2 - f2.w;
+                        umin = fminf(umin, u);
+                        umax = fmaxf(umax, u);
+                        vmin = fminf(vmin, v);
+                        vmax = fmaxf(vmax, v);
+                        su = fmaxf(su, 1e-4f * (fabsf(ta1) + fabsf(ta) + fabsf(f1.w)) + 1e-7f);
+                        sv = fmaxf(sv, 1e-4f * (fabsf(ta2) + fabsf(ta) + fabsf(f2.w)) + 1e-7f);
+                    }
+                    if (valid && (umin > f3.x + su || umax < -f3.x - su || vmin > f3.y + sv || vmax < -f3.y - sv))
+                        ov = false;
+                }
+                if (ov) {
+                    const int cx0 = max((rx & 0xffff) - bx0, 0), cx1 = min((rx >> 16) - bx0, 7);
+                    const int ry0 = max((ry & 0xffff) - by0, 0), ry1 = min((ry >> 16) - by0, 3);
+                    const uint32_t cols = (0xffu >> (7 - cx1)) & (0xffu << cx0);
+                    const uint32_t rows = (0xffffffffu >> (8 * (3 - ry1))) & (0xffffffffu << (8 * ry0));
+                    lm = (cols * 0x01010101u) & rows;
+                }
+            }
+            const uint32_t m = __ballot_sync(0xffffffffu, ov);
+            if (ov) {
+                const int slot = __popc(m & ((1u << lane) - 1u));
+                sm.sel[slot] = static_cast<uint8_t>(lane);
+                sm.lmask[slot] = lm;
+            }
+            nsel = __popc(m);
+        }
+        __syncwarp();
+        for (int g0 = 0; g0 < nsel; g0 += kSub) {
+            const int gn = min(kSub, nsel - g0);
+            // ---- A. pixel rect (lane mask) + fp32 prefilter (as the forward)
             uint32_t mask = 0;
 #pragma unroll
             for (int b = 0; b < kSub; ++b) {
-                if (b >= sn) break;
-                const float4 f3 = sm.f[sb + b][3];
-                const int rx = __float_as_int(f3.z), ry = __float_as_int(f3.w);
-                const int x0 = rx & 0xffff, x1 = rx >> 16, y0 = ry & 0xffff, y1 = ry >> 16;
-                if (x1 < wx0 || x0 > wx1 || y1 < wy0 || y0 > wy1) continue;
-                if (active && px >= x0 && px <= x1 && py >= y0 && py <= y1 &&
-                    prefilter(&sm.f[sb + b][0], dfx, dfy, dfz, near_eps_f))
+                if (b >= gn) break;
+                const int j = sm.sel[g0 + b];
+                if (active && ((sm.lmask[g0 + b] >> lane) & 1u) && prefilter(&sm.f[j][0], dfx, dfy, dfz, near_eps_f))
                     mask |= 1u << b;
             }
             const int cnt = __popc(mask);
@@ -253,7 +316,7 @@ __global__ void __launch_bounds__(kTile * kTile, 512 / (kTile * kTile)) composit
                 while (m) {
                     const int b = __ffs(m) - 1;
                     m &= m - 1;
-                    sm.q[k++] = static_cast<uint16_t>((lane << 8) | (sb + b));
+                    sm.q[k++] = static_cast<uint16_t>((lane << 8) | sm.sel[g0 + b]);
                 }
             }
             __syncwarp();
@@ -380,15 +443,16 @@ __global__ void __launch_bounds__(kTile * kTile, 512 / (kTile * kTile)) composit
             const bool sh_lane = lane < 16;
             const int av = lane - 16;  // activated value of an act lane (and av + 16 for lanes 16, 17)
 #pragma unroll 1
-            for (int b = 0; b < sn; ++b) {
+            for (int b = 0; b < gn; ++b) {
+                const int j = sm.sel[g0 + b];
                 int my_e = -1;
-                if (cur < off + cnt && (sm.q[cur] & 0x7f) == sb + b) {
+                if (cur < off + cnt && (sm.q[cur] & 0x7f) == j) {
                     if (sm.q[cur] & kComposited) my_e = cur;
                     ++cur;
                 }
                 const uint32_t hm = __ballot_sync(0xffffffffu, my_e >= 0);
                 if (!hm) continue;
-                const int64_t row = static_cast<int64_t>(sm.id[sb + b]) * kPrimAccVals;
+                const int64_t row = static_cast<int64_t>(sm.id[j]) * kPrimAccVals;
                 // the blended error in fp64: a fixed-pattern warp tree over the pixels' terms
                 double werr = my_e >= 0 ? sm.res[my_e].werr64 : 0.0;
 #pragma unroll
