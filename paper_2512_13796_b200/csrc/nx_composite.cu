@@ -45,6 +45,11 @@ constexpr int kSub = NX_COMPOSITE_SUB;           // primitives pooled per B1/B2 
 constexpr int kPool = 32 * kSub;
 constexpr int kRecPieces = REC_FIELDS * 8 / 16;  // 16-byte pieces of an fp64 record (10)
 constexpr int kShPieces = NX_SH_VALUES * 4 / 16; // 16-byte pieces of the SH coefficients (12)
+// Staged rows are padded by 16 bytes (208-byte stride): the B1 lanes of a warp read up
+// to kSub different rows at once, and at the unpadded 192-byte stride rows 0 / 2 and
+// 1 / 3 fall on the same banks (two-way conflicts on every record and SH load).
+constexpr int kRecStride = REC_FIELDS + 2;
+constexpr int kShStride = NX_SH_VALUES + 4;
 static_assert(kWorkTile == 8, "warp blocks are 8x4 pixels");
 #ifndef NX_NEAR_COUNTERS
 #define NX_NEAR_COUNTERS 1
@@ -77,9 +82,9 @@ struct PoolEntryCert {
 };
 
 template <typename PE>
-struct WarpStage {  // one warp's private staging
-    double rec[kSub][REC_FIELDS];    // exact records of the group's primitives
-    float sh[kSub][NX_SH_VALUES];    // and their SH coefficients (fp32 colour path)
+struct alignas(16) WarpStage {  // one warp's private staging
+    double rec[kSub][kRecStride];    // exact records of the group's primitives
+    float sh[kSub][kShStride];       // and their SH coefficients (fp32 colour path)
     uint8_t sel[kChunk];             // chunk slots whose pixel rect meets the warp's block
     uint32_t lmask[kChunk];          // and the lanes (pixels of the 8x4 block) inside that rect
     uint16_t q[kPool];
@@ -102,18 +107,31 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 
 // Primitive SH colour (eval_sh, sh.hpp:46-57) in fp32 from staged coefficients: the
 // same operations, in the same order, as eval_sh_f32 (nx_composite.cuh).
+// The coefficients are read as 16-byte vectors (12 loads instead of 48).
 __device__ __forceinline__ void eval_sh_smem(const float* sh, float x, float y, float z, int degree, float* rgb) {
-    float a0 = 0.5f + 0.28209479177387814f * sh[0];
-    float a1 = 0.5f + 0.28209479177387814f * sh[1];
-    float a2 = 0.5f + 0.28209479177387814f * sh[2];
+    const float4* s4 = reinterpret_cast<const float4*>(sh);
+    const float4 v0 = s4[0];
+    float a0 = 0.5f + 0.28209479177387814f * v0.x;
+    float a1 = 0.5f + 0.28209479177387814f * v0.y;
+    float a2 = 0.5f + 0.28209479177387814f * v0.z;
     if (degree >= 3) {
         float b[16];
         sh_basis_f32(x, y, z, b);
+        float c[48];
+        c[3] = v0.w;
+#pragma unroll
+        for (int q = 1; q < 12; ++q) {
+            const float4 v = s4[q];
+            c[4 * q + 0] = v.x;
+            c[4 * q + 1] = v.y;
+            c[4 * q + 2] = v.z;
+            c[4 * q + 3] = v.w;
+        }
 #pragma unroll
         for (int k = 1; k < 16; ++k) {
-            a0 = fmaf(sh[3 * k + 0], b[k], a0);
-            a1 = fmaf(sh[3 * k + 1], b[k], a1);
-            a2 = fmaf(sh[3 * k + 2], b[k], a2);
+            a0 = fmaf(c[3 * k + 0], b[k], a0);
+            a1 = fmaf(c[3 * k + 1], b[k], a1);
+            a2 = fmaf(c[3 * k + 2], b[k], a2);
         }
     }
     rgb[0] = fmaxf(a0, 0.f);
@@ -175,19 +193,16 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
     double acc[3] = {0.0, 0.0, 0.0};
     int32_t k_id[KK];
     double k_w[KK], k_t[KK];
-    uint32_t k_seq[KK];
     CT k_rgb[KR][3];
 #pragma unroll
     for (int s = 0; s < KK; ++s) {
         k_id[s] = -1;
         k_w[s] = 0.0;
         k_t[s] = 0.0;
-        k_seq[s] = 0;
     }
 #pragma unroll
     for (int s = 0; s < KR; ++s) k_rgb[s][0] = k_rgb[s][1] = k_rgb[s][2] = CT(0);
     int k_size = 0;
-    uint32_t counter = 0;
     bool active = in_img;
     // near-threshold decisions of this pixel (kNear), packed: alpha | T << 10 | top-K << 20
     // (per-pixel counts stay far below 1024)
@@ -332,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                 // ---- B1. exact fp64 evaluation of the pooled pairs, all lanes busy
                 for (int e = lane; e < total; e += 32) {
                     const int ent = ws.q[e];
-                    const int owner = ent >> 8, b = ent & 0xff;
+                    const int owner = ent >> 8, b = ent & 0xf;
                     const double* dd = sm.dir[warp * 32 + owner];
                     const double d0 = dd[0], d1 = dd[1], d2 = dd[2];
                     const double* r = ws.rec[b];
@@ -430,46 +445,67 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                     acc[0] += wgt * res.rgb[0];
                     acc[1] += wgt * res.rgb[1];
                     acc[2] += wgt * res.rgb[2];
-                    if (K > 0) {  // TopKBuffer::insert (framebuffers.hpp:33-48)
-                        const uint32_t seq = counter++;
-                        int slot = -1;
+                    if (K > 0) {
+                        // TopKBuffer::insert (framebuffers.hpp:33-48) with the slots kept in the
+                        // finalize order (weight desc, arrival asc; framebuffers.hpp:51-56): the
+                        // last-ranked incumbent the reference replaces (smallest weight, latest
+                        // arrival among ties) is then always the last slot, and finalize has
+                        // nothing left to sort. A new entry arrives last, so among equal weights it
+                        // ranks behind every incumbent: it moves up only past strictly smaller ones.
+                        // Certified mode: every comparison taken is checked against the weights'
+                        // error bounds (the ratio of two weights carries their alphas' errors and
+                        // the 1 - alpha factors between their insertions).
+                        int pos = -1;
                         if (k_size < K) {
-                            slot = k_size++;
+                            pos = k_size++;
                         } else {
-                            // last-ranked incumbent: smallest weight, latest arrival among ties
-                            int mi = 0;
-                            double wm = k_w[0];
-                            uint32_t qm = k_seq[0];
-                            float ea = k_ea[0], et = k_et[0];
-#pragma unroll
-                            for (int s = 1; s < KK; ++s) {
-                                if (kCert && fabs(k_w[s] - wm) <= (k_ea[s] + ea + fabsf(k_et[s] - et)) * fmax(k_w[s], wm))
-                                    unsure = true;
-                                if (k_w[s] < wm || (k_w[s] == wm && k_seq[s] > qm)) {
-                                    mi = s;
-                                    wm = k_w[s];
-                                    qm = k_seq[s];
-                                    ea = k_ea[s];
-                                    et = k_et[s];
-                                }
-                            }
-                            if (wgt > wm) slot = mi;
-                            if (kCert && fabs(wgt - wm) <= (eps_a + ea + (E_T - et)) * fmax(wgt, wm)) unsure = true;
+                            const double wm = k_w[KK - 1];
+                            if (kCert && fabs(wgt - wm) <= (eps_a + k_ea[KK - 1] + (E_T - k_et[KK - 1])) * fmax(wgt, wm))
+                                unsure = true;
                             if (kNear && !kCert) n_near += (wgt != wm) & (fabs(wgt - wm) <= kNearRel * wm) ? (1u << 20) : 0u;
+                            if (wgt > wm) pos = KK - 1;
                         }
 #pragma unroll
                         for (int s = 0; s < KK; ++s)
-                            if (s == slot) {
+                            if (s == pos) {
                                 k_id[s] = id;
                                 k_w[s] = wgt;
                                 k_t[s] = res.t;
-                                k_seq[s] = seq;
                                 k_ea[s] = eps_a;
                                 k_et[s] = E_T;
                                 if (kKeepRgb) {
                                     k_rgb[s % KR][0] = res.rgb[0];
                                     k_rgb[s % KR][1] = res.rgb[1];
                                     k_rgb[s % KR][2] = res.rgb[2];
+                                }
+                            }
+#pragma unroll
+                        for (int s = KK - 1; s >= 1; --s)
+                            if (s == pos) {
+                                const double wp = k_w[s - 1];
+                                if (kCert && fabs(wgt - wp) <= (eps_a + k_ea[s - 1] + (E_T - k_et[s - 1])) * fmax(wgt, wp))
+                                    unsure = true;
+                                if (kNear && !kCert)
+                                    n_near += (wgt != wp) & (fabs(wgt - wp) <= kNearRel * wp) ? (1u << 20) : 0u;
+                                if (wgt > wp) {
+                                    pos = s - 1;
+                                    k_id[s] = k_id[s - 1];
+                                    k_w[s] = k_w[s - 1];
+                                    k_t[s] = k_t[s - 1];
+                                    k_ea[s] = k_ea[s - 1];
+                                    k_et[s] = k_et[s - 1];
+                                    k_id[s - 1] = id;
+                                    k_w[s - 1] = wgt;
+                                    k_t[s - 1] = res.t;
+                                    k_ea[s - 1] = eps_a;
+                                    k_et[s - 1] = E_T;
+                                    if (kKeepRgb) {
+#pragma unroll
+                                        for (int c = 0; c < 3; ++c) {
+                                            k_rgb[s % KR][c] = k_rgb[(s - 1) % KR][c];
+                                            k_rgb[(s - 1) % KR][c] = res.rgb[c];
+                                        }
+                                    }
                                 }
                             }
                     }
@@ -502,48 +538,8 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
         acc[1] += T * a.st.background[1];
         acc[2] += T * a.st.background[2];
         if (K > 0) {
-            // finalize: weight desc, seq asc (framebuffers.hpp:51-56); slots >= size keep sentinels.
-#pragma unroll
-            for (int i = 0; i < K; ++i)
-#pragma unroll
-                for (int j = 0; j + 1 < K - i; ++j) {
-                    const bool swap = (j + 1 < k_size) &&
-                                      (k_w[j + 1] > k_w[j] || (k_w[j + 1] == k_w[j] && k_seq[j + 1] < k_seq[j]));
-                    if (kNear && !kCert && j + 1 < k_size && k_w[j + 1] != k_w[j] &&
-                        fabs(k_w[j + 1] - k_w[j]) <= kNearRel * k_w[j])
-                        n_near += 1u << 20;
-                    if (kCert && j + 1 < k_size &&
-                        fabs(k_w[j + 1] - k_w[j]) <=
-                            (k_ea[j + 1] + k_ea[j] + fabsf(k_et[j + 1] - k_et[j])) * fmax(k_w[j + 1], k_w[j]))
-                        unsure = true;
-                    if (swap) {
-                        const int32_t ti = k_id[j];
-                        k_id[j] = k_id[j + 1];
-                        k_id[j + 1] = ti;
-                        const double tw = k_w[j];
-                        k_w[j] = k_w[j + 1];
-                        k_w[j + 1] = tw;
-                        const double td = k_t[j];
-                        k_t[j] = k_t[j + 1];
-                        k_t[j + 1] = td;
-                        const uint32_t ts = k_seq[j];
-                        k_seq[j] = k_seq[j + 1];
-                        k_seq[j + 1] = ts;
-                        const float tea = k_ea[j], tet = k_et[j];
-                        k_ea[j] = k_ea[j + 1];
-                        k_et[j] = k_et[j + 1];
-                        k_ea[j + 1] = tea;
-                        k_et[j + 1] = tet;
-                        if (kKeepRgb) {
-#pragma unroll
-                            for (int c = 0; c < 3; ++c) {
-                                const CT tc = k_rgb[j % KR][c];
-                                k_rgb[j % KR][c] = k_rgb[(j + 1) % KR][c];
-                                k_rgb[(j + 1) % KR][c] = tc;
-                            }
-                        }
-                    }
-                }
+            // finalize (framebuffers.hpp:51-56): the slots are already in rank order; slots >= size
+            // keep their sentinels.
             // write slots; subtract the buffered primitives' own colours (renderer.cpp:157-164)
 #pragma unroll
             for (int j = 0; j < K; ++j) {
