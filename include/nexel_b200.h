@@ -417,6 +417,14 @@ int nx_debug_pixel_hits(nx_ctx* ctx, const nx_scene* scene, const nx_camera* cam
 enum { NX_FM_LOG = 0, NX_FM_EXP = 1, NX_FM_CUDA_LOG = 2, NX_FM_CUDA_EXP = 3,
        NX_FM_CERT = 4 /* quintuples (u, v, gx, gy, o) -> (alpha32, eps, oma32, eps_oma, alpha64) */ };
 int nx_debug_fastmath(int fn, const double* x, double* y, int64_t n);
+/* The binning primitives on n host elements (allocate, synchronise; parity tests only):
+ * the stable LSD radix sort of (key, value) pairs over key bits [begin_bit, end_bit)
+ * (key_bytes 4 or 8; keys / vals sorted in place), launched on a capacity cap >= n with
+ * the count n on the device as the frame's sorts run; and the exclusive scan (total may
+ * be NULL). */
+int nx_debug_radix_sort(int key_bytes, void* keys, uint32_t* vals, int64_t n, int64_t cap, int begin_bit,
+                        int end_bit);
+int nx_debug_scan(const int32_t* in, int32_t* out, int64_t n, int64_t cap, int32_t* total);
 
 /* ---- synthetic inputs -------------------- */
 /* stump_like(N, c, seed, R_ground): fills nexels (n*60), settings and field desc;

@@ -256,6 +256,8 @@ SIGNATURES = [
      [P, P, C.POINTER(nx_camera), C.c_int, PI64, PI32, I64, PI64, PI32, PI32]),
     ("nx_debug_pixel_hits", C.c_int, [P, P, C.POINTER(nx_camera), C.c_int, C.c_int, C.c_int, PI32, PI32]),
     ("nx_debug_fastmath", C.c_int, [C.c_int, PD, PD, I64]),
+    ("nx_debug_radix_sort", C.c_int, [C.c_int, P, PI32, I64, I64, C.c_int, C.c_int]),
+    ("nx_debug_scan", C.c_int, [PI32, PI32, I64, I64, PI32]),
     ("nx_synth_stump_like", C.c_int,
      [I64, D, C.c_uint64, D, I32, D, C.c_uint64, PD, C.POINTER(nx_settings), C.POINTER(nx_field_desc), PD, PD,
       PD, PD]),

@@ -291,9 +291,6 @@ __global__ void rect_counts_kernel(const uint32_t* ids, int64_t n, const int32_t
     }
 }
 
-// One thread per emitted key: binary search of the owning sorted primitive. Counts on
-// the device; the grid covers the capacity (keys past it are dropped: the frame is
-// re-rendered with a larger capacity before it is read, nx_api.cu frame_settle).
 // Conservative cull of a (tile, primitive) key (work lists only): the plane offsets of
 // the tile's pixel rays are a projective image of the pixel rectangle, so they lie in the
 // quadrilateral of its corner rays' offsets (all four crossing the plane on one side);
@@ -335,45 +332,84 @@ __device__ __forceinline__ bool tile_misses(const float4* f, const EmitCull& cu,
     return valid && (umin > f3.x + su || umax < -f3.x - su || vmin > f3.y + sv || vmax < -f3.y - sv);
 }
 
-// One thread per emitted key: binary search of the owning sorted primitive. Counts on
-// the device; the grid covers the capacity (keys past it are dropped: the frame is
+// One thread per emitted key. Each CTA takes a contiguous range of keys; the owner of
+// its first key comes from a 256-ary search of the offsets (one load per thread per
+// round, three rounds at 180K primitives); after that, per 256 keys, the primitives that
+// start inside the window mark their first key and a block max-scan hands every key its
+// owner (the last r with offsets[r] <= k, so zero-count primitives are skipped as in a
+// binary search). Counts on the device; keys past the capacity are dropped (the frame is
 // re-rendered with a larger capacity before it is read, nx_api.cu frame_settle). Keys
 // the cull proves empty go to the sentinel tile n_tiles (sorted past every list).
-__global__ void emit_kernel(const uint32_t* ids, const int32_t* offsets, int64_t sorted_cap,
-                            const int32_t* n_sorted_dev, int64_t key_cap, const int32_t* n_keys_dev,
-                            const int4* rect, int tiles_x, uint32_t* tile_keys, uint32_t* vals,
-                            int32_t* tile_counts, const EmitCull cu) {
-    __shared__ int64_t s_lo, s_hi;
+constexpr int kEmitThreads = 256;
+__global__ void __launch_bounds__(kEmitThreads) emit_kernel(const uint32_t* ids, const int32_t* offsets,
+                                                            int64_t sorted_cap, const int32_t* n_sorted_dev,
+                                                            int64_t key_cap, const int32_t* n_keys_dev,
+                                                            const int4* rect, int tiles_x, uint32_t* tile_keys,
+                                                            uint32_t* vals, int32_t* tile_counts, const EmitCull cu) {
+    __shared__ int32_t s_own[kEmitThreads];
+    __shared__ int32_t s_wmax[kEmitThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int64_t n_sorted = min(sorted_cap, static_cast<int64_t>(max(*n_sorted_dev, 0)));
     const int64_t n_keys = n_sorted > 0 ? min(key_cap, static_cast<int64_t>(max(*n_keys_dev, 0))) : 0;
-    // last r with offsets[r] <= k, within [lo, hi]
-    auto owner = [&](int64_t k, int64_t lo, int64_t hi) {
-        while (lo < hi) {
-            const int64_t mid = (lo + hi + 1) >> 1;
-            if (offsets[mid] <= k) lo = mid;
-            else hi = mid - 1;
+    const int64_t per = ((n_keys + gridDim.x - 1) / gridDim.x + kEmitThreads - 1) / kEmitThreads * kEmitThreads;
+    const int64_t k0 = static_cast<int64_t>(blockIdx.x) * per, k1 = min(n_keys, k0 + per);
+    if (k0 >= k1) return;
+    // owner of k0 (offsets[0] = 0 <= k0 keeps the invariant offsets[lo] <= k0)
+    int64_t lo = 0, hi = n_sorted - 1;
+    while (lo < hi) {
+        const int64_t step = (hi - lo + kEmitThreads) / kEmitThreads;
+        const int64_t r = lo + tid * step;
+        const int c = __syncthreads_count(r <= hi && offsets[r] <= k0);
+        lo += (c - 1) * step;
+        hi = min(hi, lo + step - 1);
+    }
+    int32_t own = static_cast<int32_t>(lo);
+    for (int64_t base = k0; base < k1; base += kEmitThreads) {
+        s_own[tid] = -1;
+        __syncthreads();
+        for (int64_t r0 = own + 1;; r0 += kEmitThreads) {
+            const int64_t r = r0 + tid;
+            bool more = false;
+            if (r < n_sorted) {
+                const int64_t o = offsets[r];
+                if (o < base + kEmitThreads) {
+                    more = true;
+                    if (o >= base) atomicMax(&s_own[o - base], static_cast<int32_t>(r));
+                }
+            }
+            if (!__syncthreads_or(more)) break;
         }
-        return lo;
-    };
-    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < n_keys;
-         base += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        // the block's keys are contiguous: two full searches bound everyone else's
+        int32_t v = s_own[tid];
+        if (tid == 0) v = max(v, own);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v = max(v, y);
+        }
+        if (lane == 31) s_wmax[wid] = v;
         __syncthreads();
-        if (threadIdx.x == 0) s_lo = owner(base, 0, n_sorted - 1);
-        if (threadIdx.x == 1) s_hi = owner(min(base + blockDim.x, n_keys) - 1, 0, n_sorted - 1);
+        int32_t pre = -1, all = -1;
+#pragma unroll
+        for (int w = 0; w < kEmitThreads / 32; ++w) {
+            const int32_t m = s_wmax[w];
+            if (w < wid) pre = max(pre, m);
+            all = max(all, m);
+        }
+        v = max(v, pre);
+        const int64_t k = base + tid;
+        if (k < k1) {
+            const uint32_t id = ids[v];
+            const int4 rc = rect[id];
+            const int j = static_cast<int>(k - offsets[v]);
+            const int w = rc.y - rc.x + 1;
+            int tile = (rc.z + j / w) * tiles_x + rc.x + j % w;
+            if (cu.recf && tile_misses(cu.recf + static_cast<int64_t>(id) * 4, cu, tile)) tile = cu.n_tiles;
+            tile_keys[k] = static_cast<uint32_t>(tile);
+            vals[k] = id;
+            if (tile < cu.n_tiles) atomicAdd(&tile_counts[tile], 1);
+        }
+        own = all;  // the owner of the window's last key
         __syncthreads();
-        const int64_t k = base + threadIdx.x;
-        if (k >= n_keys) continue;
-        const int64_t lo = owner(k, s_lo, s_hi);
-        const uint32_t id = ids[lo];
-        const int4 rc = rect[id];
-        const int j = static_cast<int>(k - offsets[lo]);
-        const int w = rc.y - rc.x + 1;
-        int tile = (rc.z + j / w) * tiles_x + rc.x + j % w;
-        if (cu.recf && tile_misses(cu.recf + static_cast<int64_t>(id) * 4, cu, tile)) tile = cu.n_tiles;
-        tile_keys[k] = static_cast<uint32_t>(tile);
-        vals[k] = id;
-        if (tile < cu.n_tiles) atomicAdd(&tile_counts[tile], 1);
     }
 }
 

@@ -16,6 +16,7 @@
 // Counts may live on the device (n_dev): grids are sized by the host capacity and the
 // blocks past the device count leave at once (no host round trip).
 #include "nx_sort.cuh"
+#include "../../include/nexel_b200.h"
 
 #include <algorithm>
 
@@ -188,38 +189,47 @@ __global__ void __launch_bounds__(kRadixThreads) radix_pass_kernel(const K* __re
     }
     // exclusive scan of the pass's global histogram: the digit's start in the output
     const int gstart = block_excl_scan(hcount, s_warp, nullptr);
-    s_local[tid] = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s_cnt[w][tid] = 0;
     __syncthreads();
+    // Warp w ranks the tile's w-th run of 32 * kRadixItems keys (index order = warp, item,
+    // lane): per-warp digit counts in shared memory, peers found with match_any, only
+    // warp-level synchronisation until the per-digit offsets over the warps.
     const unsigned lt_mask = (1u << lane) - 1u;
     K key[kRadixItems];
     uint32_t val[kRadixItems];
     int loc[kRadixItems];
     unsigned dig[kRadixItems];
+    const int64_t wbase = base + static_cast<int64_t>(warp) * (32 * kRadixItems);
 #pragma unroll
     for (int r = 0; r < kRadixItems; ++r) {
-        const int64_t i = base + static_cast<int64_t>(r) * kRadixThreads + tid;
+        const int64_t i = wbase + r * 32 + lane;
         const bool valid = i < n;
         key[r] = valid ? keys_in[i] : K(0);
         val[r] = valid ? vals_in[i] : 0u;
         dig[r] = valid ? static_cast<unsigned>((key[r] >> shift) & (kRadixBuckets - 1)) : 0xffffffffu;
+    }
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) s_cnt[w][tid] = 0;
-        __syncthreads();
+    for (int r = 0; r < kRadixItems; ++r) {
         const unsigned peers = __match_any_sync(0xffffffffu, dig[r]);
         const int rank = __popc(peers & lt_mask);
-        if (valid && rank == 0) s_cnt[warp][dig[r]] = __popc(peers);
-        __syncthreads();
+        const bool valid = dig[r] != 0xffffffffu;
+        const int pre = valid ? s_cnt[warp][dig[r]] : 0;
+        __syncwarp();
+        if (valid && rank == 0) s_cnt[warp][dig[r]] = pre + __popc(peers);
+        __syncwarp();
+        loc[r] = pre + rank;
+    }
+    __syncthreads();
+    {  // digit tid: the warps' exclusive offsets inside the tile and the tile's count
         int run = 0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
             const int c = s_cnt[w][tid];
-            s_cnt[w][tid] = s_local[tid] + run;
+            s_cnt[w][tid] = run;
             run += c;
         }
-        s_local[tid] += run;
-        __syncthreads();
-        loc[r] = valid ? s_cnt[warp][dig[r]] + rank : 0;
-        __syncthreads();
+        s_local[tid] = run;
     }
     // publish this block's digit counts, look back for the preceding blocks' totals
     uint64_t* status = reinterpret_cast<uint64_t*>(scratch + kStatusOff) +
@@ -238,7 +248,7 @@ __global__ void __launch_bounds__(kRadixThreads) radix_pass_kernel(const K* __re
 #pragma unroll
     for (int r = 0; r < kRadixItems; ++r) {
         if (dig[r] == 0xffffffffu) continue;
-        const int pos = s_glob[dig[r]] + loc[r];
+        const int pos = s_glob[dig[r]] + s_cnt[warp][dig[r]] + loc[r];
         keys_out[pos] = key[r];
         vals_out[pos] = val[r];
     }
@@ -312,3 +322,66 @@ bool radix_sort_pairs_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, ui
 }
 
 }  // namespace nx
+
+// ---------------------------------------------------------------- parity entry points
+extern "C" int nx_debug_radix_sort(int key_bytes, void* keys, uint32_t* vals, int64_t n, int64_t cap, int begin_bit,
+                                   int end_bit) {
+    if ((key_bytes != 4 && key_bytes != 8) || n < 0 || cap < n || begin_bit < 0 || end_bit > 8 * key_bytes ||
+        begin_bit > end_bit || (n && (!keys || !vals)) || n > INT32_MAX)
+        return NX_INVALID_ARGUMENT;
+    if (n == 0) return NX_OK;
+    const size_t kb = static_cast<size_t>(cap) * key_bytes, vb = static_cast<size_t>(cap) * sizeof(uint32_t);
+    uint8_t *k0 = nullptr, *k1 = nullptr;
+    uint32_t *v0 = nullptr, *v1 = nullptr;
+    int32_t* sc = nullptr;
+    cudaError_t e = cudaMalloc(&k0, kb);
+    if (e == cudaSuccess) e = cudaMalloc(&k1, kb);
+    if (e == cudaSuccess) e = cudaMalloc(&v0, vb);
+    if (e == cudaSuccess) e = cudaMalloc(&v1, vb);
+    if (e == cudaSuccess) e = cudaMalloc(&sc, (nx::radix_scratch_ints(cap) + 1) * sizeof(int32_t));
+    int32_t* n_dev = sc ? sc + nx::radix_scratch_ints(cap) : nullptr;
+    const int32_t n32 = static_cast<int32_t>(n);
+    if (e == cudaSuccess) e = cudaMemset(k0, 0xff, kb);  // past the count: garbage the sort must not read
+    if (e == cudaSuccess) e = cudaMemcpy(k0, keys, static_cast<size_t>(n) * key_bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(v0, vals, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(n_dev, &n32, sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        bool alt;
+        if (key_bytes == 8)
+            alt = nx::radix_sort_pairs_u64(reinterpret_cast<uint64_t*>(k0), v0, reinterpret_cast<uint64_t*>(k1), v1,
+                                           cap, n_dev, begin_bit, end_bit, sc, nullptr);
+        else
+            alt = nx::radix_sort_pairs_u32(reinterpret_cast<uint32_t*>(k0), v0, reinterpret_cast<uint32_t*>(k1), v1,
+                                           cap, n_dev, begin_bit, end_bit, sc, nullptr);
+        e = cudaGetLastError();
+        if (e == cudaSuccess)
+            e = cudaMemcpy(keys, alt ? k1 : k0, static_cast<size_t>(n) * key_bytes, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemcpy(vals, alt ? v1 : v0, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost);
+    }
+    cudaFree(k0);
+    cudaFree(k1);
+    cudaFree(v0);
+    cudaFree(v1);
+    cudaFree(sc);
+    return e == cudaSuccess ? NX_OK : NX_CUDA_ERROR;
+}
+
+extern "C" int nx_debug_scan(const int32_t* in, int32_t* out, int64_t n, int64_t cap, int32_t* total) {
+    if (n < 0 || cap < n || (n && (!in || !out))) return NX_INVALID_ARGUMENT;
+    int32_t *d = nullptr, *sc = nullptr;
+    const size_t bytes = static_cast<size_t>(cap > 0 ? cap : 1) * sizeof(int32_t);
+    cudaError_t e = cudaMalloc(&d, bytes + sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&sc, nx::scan_scratch_ints(cap) * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMemset(d, 0, bytes + sizeof(int32_t));
+    if (e == cudaSuccess && n) e = cudaMemcpy(d, in, static_cast<size_t>(n) * sizeof(int32_t), cudaMemcpyHostToDevice);
+    int32_t* d_total = d + (cap > 0 ? cap : 1);
+    if (e == cudaSuccess) {
+        nx::scan_exclusive(d, d, cap, d_total, sc, nullptr);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess && n) e = cudaMemcpy(out, d, static_cast<size_t>(n) * sizeof(int32_t), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && total) e = cudaMemcpy(total, d_total, sizeof(int32_t), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    cudaFree(sc);
+    return e == cudaSuccess ? NX_OK : NX_CUDA_ERROR;
+}

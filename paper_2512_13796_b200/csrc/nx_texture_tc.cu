@@ -193,6 +193,19 @@ __global__ void __launch_bounds__(kTcThreads, kCtasPerSm) texture_tc_kernel(cons
         // ---- hidden layers: relu(D) -> A (K = 64), then D = A . W^T
 #pragma unroll 1
         for (int layer = 0; layer < 2; ++layer) {
+#if NX_TMEM_BATCH
+            {
+                uint32_t r[kHid];
+                tmem_ld_batch<kHid / 16>(taddr, r);
+#pragma unroll
+                for (int c = 0; c < kHid / 8; ++c) {
+                    float v[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) v[i] = fmaxf(__uint_as_float(r[8 * c + i]), 0.f);
+                    store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 8 * c, kHid), v);
+                }
+            }
+#else
 #pragma unroll
             for (int c = 0; c < kHid / 16; ++c) {
                 float v[16];
@@ -202,6 +215,7 @@ __global__ void __launch_bounds__(kTcThreads, kCtasPerSm) texture_tc_kernel(cons
                 store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 16 * c, kHid), v);
                 store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 16 * c + 8, kHid), v + 8);
             }
+#endif
             fence_async_smem();
             tc_fence_before();
             __syncthreads();
@@ -431,6 +445,19 @@ __global__ void __launch_bounds__(kTcThreads, kCtasPerSm) tex_mlp_kernel(const T
         tc_fence_after();
 #pragma unroll 1
         for (int layer = 0; layer < 2; ++layer) {
+#if NX_TMEM_BATCH
+            {
+                uint32_t r[kHid];
+                tmem_ld_batch<kHid / 16>(taddr, r);
+#pragma unroll
+                for (int c = 0; c < kHid / 8; ++c) {
+                    float v[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) v[i] = fmaxf(__uint_as_float(r[8 * c + i]), 0.f);
+                    store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 8 * c, kHid), v);
+                }
+            }
+#else
 #pragma unroll
             for (int c = 0; c < kHid / 16; ++c) {
                 float v[16];
@@ -440,6 +467,7 @@ __global__ void __launch_bounds__(kTcThreads, kCtasPerSm) tex_mlp_kernel(const T
                 store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 16 * c, kHid), v);
                 store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 16 * c + 8, kHid), v + 8);
             }
+#endif
             fence_async_smem();
             tc_fence_before();
             __syncthreads();
@@ -946,6 +974,9 @@ __global__ void __launch_bounds__(128) tex_features_img_kernel(const TextureArgs
 // three layers run, the next tile's 16 KB operand image lands in the other of two
 // buffers (cp.async.bulk + mbarrier transaction count); layer 1 reads it in place (no
 // register round trip, no split on this side). Two 128-thread CTAs per SM (~101 KB).
+#ifndef NX_TMEM_BATCH
+#define NX_TMEM_BATCH 1
+#endif
 constexpr int kB2OffImg = kOffAh + 2 * kRows * kHid * 2;        // after the 64-wide A operand
 constexpr int kB2OffRgb = kB2OffImg + 2 * kImgBytes;             // two image buffers
 constexpr int kB2OffBar = kB2OffRgb + kRows * 3 * 4;             // mma, full[2]
@@ -1035,6 +1066,27 @@ __global__ void __launch_bounds__(kTcThreads, 2) tex_mlp_bulk_kernel(const Textu
         const WsTile wt = ws_tile(tile, row, K, bw, bh, tiles_x, W, H);
         const bool valid = wt.in_tile && a.fb.ids[wt.slot] >= 0;
         n_queries += valid;
+        // Eq. 7 inputs of pixel `row` of the tile, loaded now: their latency hides behind
+        // the three layers instead of stalling the tile's end
+        constexpr int kPre = 4;
+        int64_t e_pix = -1;
+        double e_acc[3] = {0.0, 0.0, 0.0}, e_w[kPre];
+        int32_t e_id[kPre];
+        if (row < ppt) {
+            const int qx = static_cast<int>(tile % tiles_x) * bw + row % bw;
+            const int qy = static_cast<int>(tile / tiles_x) * bh + row / bw;
+            if (qx < W && qy < H) {
+                e_pix = static_cast<int64_t>(qy) * W + qx;
+                e_acc[0] = a.fb.base[e_pix * 3 + 0];
+                e_acc[1] = a.fb.base[e_pix * 3 + 1];
+                e_acc[2] = a.fb.base[e_pix * 3 + 2];
+#pragma unroll
+                for (int j = 0; j < kPre; ++j) {
+                    e_id[j] = j < K ? a.fb.ids[e_pix * K + j] : -1;
+                    e_w[j] = j < K ? a.fb.weights[e_pix * K + j] : 0.0;
+                }
+            }
+        }
         mbar_wait(full(b), static_cast<uint32_t>((k >> 1) & 1));
         tc_fence_after();
         const int ib = kB2OffImg + b * kImgBytes;
@@ -1046,6 +1098,19 @@ __global__ void __launch_bounds__(kTcThreads, 2) tex_mlp_bulk_kernel(const Textu
         tc_fence_after();
 #pragma unroll 1
         for (int layer = 0; layer < 2; ++layer) {
+#if NX_TMEM_BATCH
+            {
+                uint32_t r[kHid];
+                tmem_ld_batch<kHid / 16>(taddr, r);
+#pragma unroll
+                for (int c = 0; c < kHid / 8; ++c) {
+                    float v[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) v[i] = fmaxf(__uint_as_float(r[8 * c + i]), 0.f);
+                    store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 8 * c, kHid), v);
+                }
+            }
+#else
 #pragma unroll
             for (int c = 0; c < kHid / 16; ++c) {
                 float v[16];
@@ -1055,6 +1120,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) tex_mlp_bulk_kernel(const Textu
                 store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 16 * c, kHid), v);
                 store_split8(smem, kOffAh, kOffAl, kmajor_off(row, 16 * c + 8, kHid), v + 8);
             }
+#endif
             fence_async_smem();
             tc_fence_before();
             __syncthreads();
@@ -1070,6 +1136,20 @@ __global__ void __launch_bounds__(kTcThreads, 2) tex_mlp_bulk_kernel(const Textu
             float bb[16];
             sh_basis_f32(static_cast<float>(dir[0]), static_cast<float>(dir[1]), static_cast<float>(dir[2]), bb);
             float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+#if NX_TMEM_BATCH
+            {
+                uint32_t r[kOut];
+                tmem_ld_batch<kOut / 16>(taddr, r);
+#pragma unroll
+                for (int o = 0; o < kOut; ++o) {
+                    const float v = __uint_as_float(r[o]);
+                    const int kk = o / 3;
+                    if (o % 3 == 0) c0 = fmaf(v, bb[kk], c0);
+                    else if (o % 3 == 1) c1 = fmaf(v, bb[kk], c1);
+                    else c2 = fmaf(v, bb[kk], c2);
+                }
+            }
+#else
 #pragma unroll
             for (int c = 0; c < kOut / 16; ++c) {
                 float v[16];
@@ -1082,6 +1162,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) tex_mlp_bulk_kernel(const Textu
                     else c2 = fmaf(v[i], bb[kk], c2);
                 }
             }
+#endif
             float rgb[3] = {0.f, 0.f, 0.f};
             if (valid) {
                 rgb[0] = fmaxf(0.5f + c0, 0.f);
@@ -1100,12 +1181,20 @@ __global__ void __launch_bounds__(kTcThreads, 2) tex_mlp_bulk_kernel(const Textu
         tc_fence_before();
         __syncthreads();
         // Eq. 7: final = base + sum_j W[p,j] * texture[p,j] (renderer.cpp:219-236)
-        if (row < ppt) {
-            const int tpx = static_cast<int>(tile % tiles_x) * bw, tpy = static_cast<int>(tile / tiles_x) * bh;
-            const int qx = tpx + row % bw, qy = tpy + row / bw;
-            if (qx < W && qy < H) {
-                const int64_t pix = static_cast<int64_t>(qy) * W + qx;
-                double acc0 = a.fb.base[pix * 3 + 0], acc1 = a.fb.base[pix * 3 + 1], acc2 = a.fb.base[pix * 3 + 2];
+        if (e_pix >= 0) {
+            const int64_t pix = e_pix;
+            double acc0 = e_acc[0], acc1 = e_acc[1], acc2 = e_acc[2];
+            if (K <= kPre) {
+#pragma unroll
+                for (int j = 0; j < kPre; ++j) {
+                    if (j >= K || e_id[j] < 0) continue;
+                    const double w = e_w[j];
+                    const float* tc = srgb + (row * K + j) * 3;
+                    acc0 += w * tc[0];
+                    acc1 += w * tc[1];
+                    acc2 += w * tc[2];
+                }
+            } else {
                 for (int j = 0; j < K; ++j) {
                     const int64_t q = pix * K + j;
                     if (a.fb.ids[q] < 0) continue;
@@ -1115,10 +1204,10 @@ __global__ void __launch_bounds__(kTcThreads, 2) tex_mlp_bulk_kernel(const Textu
                     acc1 += w * tc[1];
                     acc2 += w * tc[2];
                 }
-                a.fb.final_img[pix * 3 + 0] = static_cast<float>(acc0);
-                a.fb.final_img[pix * 3 + 1] = static_cast<float>(acc1);
-                a.fb.final_img[pix * 3 + 2] = static_cast<float>(acc2);
             }
+            a.fb.final_img[pix * 3 + 0] = static_cast<float>(acc0);
+            a.fb.final_img[pix * 3 + 1] = static_cast<float>(acc1);
+            a.fb.final_img[pix * 3 + 2] = static_cast<float>(acc2);
         }
         // srgb and the A operand are rewritten next tile only after its layer-1 wait and
         // the barrier before layer 2, which every thread reaches after this point
