@@ -28,6 +28,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <sys/mman.h>
 
 #include "nexel/error.hpp"
 #include "../../include/nexel_b200.h"
@@ -106,6 +107,16 @@ void allocate_fast(FrameBuffers& fb, int w, int h, int k) {
         fb.ids.reserve(ns);
     }
     regions.push_back({reinterpret_cast<char*>(fb.ids.data()), ns * sizeof(std::int32_t)});
+    // Transparent huge pages for the fresh arrays (when the kernel offers them on
+    // request): one fault per 2 MB instead of per 4 KB page.
+    static const bool thp = std::getenv("NEXEL_DROPIN_NO_THP") == nullptr;
+    if (thp)
+        for (const auto& r : regions) {
+            constexpr uintptr_t kHuge = uintptr_t(2) << 20;
+            const uintptr_t b = (reinterpret_cast<uintptr_t>(r.first) + kHuge - 1) & ~(kHuge - 1);
+            const uintptr_t e = (reinterpret_cast<uintptr_t>(r.first) + r.second) & ~(kHuge - 1);
+            if (r.first && e > b) madvise(reinterpret_cast<void*>(b), e - b, MADV_HUGEPAGE);
+        }
     size_t pages = 0;
     for (const auto& r : regions) pages += (r.second + 4095) / 4096;
     parallel_range(pages * 4096 / 8, [&](size_t b, size_t e) {  // page i <-> elements [512 i, 512 i + 512)
@@ -124,12 +135,40 @@ void allocate_fast(FrameBuffers& fb, int w, int h, int k) {
     for (auto& t : pool) t.join();
 }
 
+// Where a Scene's arrays live and how long they are: a render may start on the device
+// copy of the last bound scene when this is unchanged, while the content hash runs.
+struct SceneSpan {
+    const void* p[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    size_t n[5] = {0, 0, 0, 0, 0};
+    bool operator==(const SceneSpan& o) const {
+        for (int i = 0; i < 5; ++i)
+            if (p[i] != o.p[i] || n[i] != o.n[i]) return false;
+        return true;
+    }
+};
+
+SceneSpan span_of(const Scene& s) {
+    SceneSpan r;
+    r.p[0] = s.nexels.data();
+    r.n[0] = s.nexels.size();
+    r.p[1] = s.field.grid.table.data();
+    r.n[1] = s.field.grid.table.size();
+    r.p[2] = s.field.mlp.w1.data();
+    r.n[2] = s.field.mlp.w1.size();
+    r.p[3] = s.field.mlp.w2.data();
+    r.n[3] = s.field.mlp.w2.size();
+    r.p[4] = s.field.mlp.w3.data();
+    r.n[4] = s.field.mlp.w3.size();
+    return r;
+}
+
 struct Device {
     Staging staging;
     nx_ctx* ctx = nullptr;
     nx_scene* scene = nullptr;
     nx_frame* frame = nullptr;
     uint64_t scene_key = 0;
+    SceneSpan scene_span;       // of the Scene the device scene was made from
     const FrameBuffers* frame_owner = nullptr;  // host FrameBuffers mirrored by `frame`
     std::mutex mu;
 };
@@ -253,8 +292,7 @@ nx_camera to_nx(const Camera& c) {
     return o;
 }
 
-// Context + device scene for `scene` (uploaded when its content changed).
-Device& bind(const Scene& scene) {
+Device& device_ctx() {
     Device& d = device();
     if (!d.ctx) {
         const char* env = std::getenv("NEXEL_CUDA_DEVICE");
@@ -264,7 +302,14 @@ Device& bind(const Scene& scene) {
         check(d, nx_frame_create(d.ctx, 0, 0, 0, &d.frame));
         check(d, nx_frame_set_backward(d.ctx, d.frame, 1));  // fp64 base, as FrameBuffers holds it
     }
-    const uint64_t key = fingerprint(scene);
+    return d;
+}
+
+// Context + device scene for `scene` (uploaded when its content changed; `key` = its
+// fingerprint when the caller already has it).
+Device& bind(const Scene& scene, const uint64_t* known_key = nullptr) {
+    Device& d = device_ctx();
+    const uint64_t key = known_key ? *known_key : fingerprint(scene);
     const nx_settings st = to_nx(scene.settings);
     if (!d.scene || key != d.scene_key) {
         if (d.scene) nx_scene_destroy(d.scene);
@@ -277,6 +322,7 @@ Device& bind(const Scene& scene) {
                                  scene.field.mlp.w2.data(), scene.field.mlp.w3.data(), &d.scene));
         d.scene_key = key;
     }
+    d.scene_span = span_of(scene);
     check(d, nx_scene_set_settings(d.ctx, d.scene, &st));
     return d;
 }
@@ -378,7 +424,8 @@ void texturing_pass(const Scene& scene, const Camera& cam, FrameBuffers& fb) {
 
 // renderer.cpp:239-244. The scene is bound (fingerprinted) once for both passes; both
 // passes and one download of every FrameBuffers array into the pinned staging are
-// queued at once, and the FrameBuffers are allocated (the API returns them by value:
+// queued at once (on the device copy of the last scene while the fingerprint confirms
+// it is unchanged), and the FrameBuffers are allocated (the API returns them by value:
 // ~300 MB of fresh pages at 1080p) while the device works; then one synchronisation
 // and one parallel widening pass. NEXEL_DROPIN_PROFILE=1 prints the phase times.
 RenderResult render(const Scene& scene, const Camera& cam) {
@@ -400,13 +447,20 @@ RenderResult render(const Scene& scene, const Camera& cam) {
             if (t.joinable()) t.join();
         }
     } joiner{alloc};
-    Device& d = bind(scene);
+    // The same Scene arrays as the last bound scene: the passes start on its device copy
+    // at once and the content hash runs while they do; a changed content (the hash
+    // differs) re-uploads and renders again, so the result always matches `scene`.
+    Device& d0 = device_ctx();
+    const bool speculative = d0.scene && span_of(scene) == d0.scene_span;
+    Device& d = speculative ? d0 : bind(scene);
+    if (speculative) {
+        const nx_settings sst = to_nx(scene.settings);
+        check(d, nx_scene_set_settings(d.ctx, d.scene, &sst));
+    }
     const auto t1 = clk::now();
     std::lock_guard<std::mutex> lock(d.mu);
     const size_t npix = static_cast<size_t>(cam.width) * cam.height, ns = npix * K;
     const nx_camera c = to_nx(cam);
-    check(d, nx_collection_pass(d.ctx, d.scene, &c, d.frame, nullptr));
-    if (K > 0) check(d, nx_texturing_pass(d.ctx, d.scene, &c, d.frame, nullptr));
     // staging: fp64 base, fp64 residual, depths, weights, ids, then fp32 texture, final
     const bool f64 = to_nx(scene.settings).precision == NX_PRECISION_F64;
     const size_t cs = f64 ? 8 : 4;  // colour element size of the texture / final download
@@ -430,7 +484,20 @@ RenderResult render(const Scene& scene, const Camera& cam) {
             h.final_img = static_cast<float*>(fin_st);
         }
     }
-    check(d, nx_frame_download(d.ctx, d.frame, &h, nullptr));
+    auto enqueue = [&] {
+        check(d, nx_collection_pass(d.ctx, d.scene, &c, d.frame, nullptr));
+        if (K > 0) check(d, nx_texturing_pass(d.ctx, d.scene, &c, d.frame, nullptr));
+        check(d, nx_frame_download(d.ctx, d.frame, &h, nullptr));
+    };
+    enqueue();
+    if (speculative) {
+        const uint64_t key = fingerprint(scene);
+        if (key != d.scene_key) {
+            check(d, nx_ctx_synchronize(d.ctx));  // the frame of the previous content is discarded
+            bind(scene, &key);
+            enqueue();
+        }
+    }
     const auto t2 = clk::now();
     alloc.join();
     const auto t3 = clk::now();
@@ -477,7 +544,8 @@ RenderResult render(const Scene& scene, const Camera& cam) {
     if (prof) {
         const auto t5 = clk::now();
         auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-        std::fprintf(stderr, "[dropin render] bind %.2f  enqueue %.2f  allocate (rest) %.2f  wait %.2f  widen %.2f ms\n",
+        std::fprintf(stderr,
+                     "[dropin render] bind %.2f  enqueue (+ hash) %.2f  allocate (rest) %.2f  wait %.2f  widen %.2f ms\n",
                      ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, t5));
     }
     return out;
