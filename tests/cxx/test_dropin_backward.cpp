@@ -2,7 +2,10 @@
 // against the reference's own render_backward (renderer.cpp:251-401, compiled in the
 // same library under the name nexel_ref_render_backward) on the same forward output:
 // random scenes from the reference's test helpers (tests/helpers.hpp:88-125),
-// K = 0..4, with and without the blended-error bookkeeping. Built by `make dropin`.
+// K = 0..4, with and without the blended-error bookkeeping; and the drop-in render after
+// the Scene is edited in place (same arrays: the pass that starts on the cached device
+// scene must be redone from the new content) against the reference's own render.
+// Built by `make dropin`.
 #define DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
 #include <doctest.h>
 
@@ -15,6 +18,7 @@
 #include "nexel/renderer.hpp"
 
 namespace nexel {
+RenderResult nexel_ref_render(const Scene& scene, const Camera& cam);
 void nexel_ref_render_backward(const Scene& scene, const Camera& cam, const FrameBuffers& fb,
                                const UpstreamGrads& up, SceneGrads& grads, const double* err_pixel,
                                std::vector<double>* blended_error);
@@ -99,4 +103,52 @@ TEST_CASE("drop-in render_backward accumulates and reports unallocated gradients
     CHECK(normwise(b, a) <= 1e-6);
     SceneGrads empty;
     CHECK_THROWS_AS(render_backward(scene, cam, rr.fb, up, empty), Error);
+}
+
+namespace {
+
+double max_abs_diff(const std::vector<double>& a, const std::vector<double>& b) {
+    double m = 0;
+    for (size_t i = 0; i < a.size(); ++i) m = std::max(m, std::abs(a[i] - b[i]));
+    return m;
+}
+
+void check_same_frame(const RenderResult& ours, const RenderResult& ref) {
+    CHECK(ours.fb.ids == ref.fb.ids);
+    CHECK(max_abs_diff(ours.fb.depths, ref.fb.depths) <= 1e-9);
+    CHECK(max_abs_diff(ours.fb.weights, ref.fb.weights) <= 1e-9);
+    CHECK(max_abs_diff(ours.fb.final_img, ref.fb.final_img) <= 1e-6);
+    CHECK(max_abs_diff(ours.fb.texture, ref.fb.texture) <= 1e-6);
+}
+
+}  // namespace
+
+TEST_CASE("drop-in render follows in-place edits of the Scene") {
+    std::mt19937_64 g(913);
+    Scene scene = random_scene(g, 80, 2);
+    const Camera cam = orbit_camera(g, 48, 50.0, 3.0);
+    const RenderResult first = render(scene, cam);  // binds the device scene
+    check_same_frame(first, nexel_ref_render(scene, cam));
+    const void* nexels_before = scene.nexels.data();
+    // geometry, opacity and colour of some primitives, and the hash table, edited in place
+    for (size_t i = 0; i < scene.nexels.size(); i += 3) {
+        scene.nexels[i].opacity_raw += 1.5;
+        scene.nexels[i].mu.x += 0.05;
+        scene.nexels[i].sh[0] -= 0.3;
+    }
+    for (size_t i = 0; i < scene.field.grid.table.size(); i += 7) scene.field.grid.table[i] += 0.05;
+    REQUIRE(scene.nexels.data() == nexels_before);
+    const RenderResult second = render(scene, cam);
+    const RenderResult ref = nexel_ref_render(scene, cam);
+    check_same_frame(second, ref);
+    CHECK(max_abs_diff(second.fb.final_img, first.fb.final_img) > 1e-3);  // the edit shows
+    // the same content again, unchanged arrays: the speculative pass stands
+    const RenderResult third = render(scene, cam);
+    CHECK(third.fb.ids == second.fb.ids);
+    CHECK(third.fb.final_img == second.fb.final_img);
+    // a copy (other arrays, same content) renders the same frame
+    const Scene copy = scene;
+    const RenderResult fourth = render(copy, cam);
+    CHECK(fourth.fb.ids == second.fb.ids);
+    CHECK(fourth.fb.final_img == second.fb.final_img);
 }

@@ -34,7 +34,7 @@ def test_dropin_render_backward_matches_the_reference_in_the_same_library():
     r = subprocess.run([BWD], capture_output=True, text=True, timeout=900)
     print(r.stdout[-2000:], r.stderr[-2000:])
     assert r.returncode == 0
-    assert "2 test cases, 0 failed" in r.stdout
+    assert "3 test cases, 0 failed" in r.stdout
 
 
 TRAIN_REF = os.path.join(ROOT, "build", "dropin", "test_train_dropin")
