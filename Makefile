@@ -63,7 +63,7 @@ RENAME_FWD := -Dcollection_pass=nexel_ref_collection_pass -Dtexturing_pass=nexel
 ifneq ($(wildcard $(REF)/core/src/renderer.cpp),)
 dropin: $(DROPIN)/libnexel_dropin.so $(DROPIN)/test_oracle_dropin $(DROPIN)/test_dropin_backward \
         $(DROPIN)/test_train_dropin $(DROPIN)/test_dropin_train $(DROPIN)/bench_train $(DROPIN)/acceptance_dropin \
-        $(DROPIN)/test_renderer_dropin $(DROPIN)/bench_render
+        $(DROPIN)/test_renderer_dropin $(DROPIN)/bench_render $(DROPIN)/dp_train
 else
 dropin:
 	@echo "reference sources not present; using the prebuilt $(DROPIN) if any"
@@ -84,7 +84,12 @@ $(DROPIN)/renderer_b200.o: $(PKG)/host/renderer_b200.cpp include/nexel_b200.h
 # nexel::train / mean_psnr on the device (host/trainer_b200.cpp); the reference's
 # trainer.cpp keeps config parsing and initialize_scene, its own train / mean_psnr
 # exported as nexel_ref_train / nexel_ref_mean_psnr over the reference's CPU renderer
-$(DROPIN)/trainer_b200.o: $(PKG)/host/trainer_b200.cpp include/nexel_b200.h
+$(DROPIN)/trainer_b200.o: $(PKG)/host/trainer_b200.cpp $(PKG)/host/dp_b200.hpp include/nexel_b200.h
+	@mkdir -p $(DROPIN)
+	$(CXX) $(DROPIN_CXX) -I$(CUDA_HOME)/include -c -o $@ $<
+
+# data-parallel communicators of nexel::train (NCCL loaded with dlopen on first use)
+$(DROPIN)/dp_b200.o: $(PKG)/host/dp_b200.cpp $(PKG)/host/dp_b200.hpp
 	@mkdir -p $(DROPIN)
 	$(CXX) $(DROPIN_CXX) -I$(CUDA_HOME)/include -c -o $@ $<
 
@@ -102,9 +107,10 @@ $(DROPIN)/png_stub.o: tests/cxx/png_stub.cpp
 	$(CXX) $(DROPIN_CXX) -c -o $@ $<
 
 $(DROPIN)/libnexel_dropin.so: $(DROPIN)/renderer_b200.o $(DROPIN)/ref_renderer_backward.o $(DROPIN)/trainer_b200.o \
+                              $(DROPIN)/dp_b200.o \
                               $(DROPIN)/ref_trainer_renamed.o \
                               $(addprefix $(DROPIN)/ref_,$(addsuffix .o,$(DROPIN_TUS))) $(PKG)/libnexel_b200.so
-	$(CXX) -shared -pthread -o $@ $(filter %.o,$^) -L$(PKG) -lnexel_b200 -L$(CUDA_HOME)/lib64 -lcudart \
+	$(CXX) -shared -pthread -o $@ $(filter %.o,$^) -L$(PKG) -lnexel_b200 -L$(CUDA_HOME)/lib64 -lcudart -ldl \
 	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,$(CUDA_HOME)/lib64
 
 TRAIN_TEST_OBJS := $(DROPIN)/ref_json_bundle.o $(DROPIN)/ref_json_synthetic.o $(DROPIN)/png_stub.o
@@ -124,6 +130,9 @@ $(DROPIN)/acceptance_dropin: $(REF)/tests/acceptance.cpp $(TRAIN_TEST_OBJS) $(DR
 # the reference's renderer tests (tests/test_renderer.cpp), unmodified
 $(DROPIN)/test_renderer_dropin: $(REF)/tests/test_renderer.cpp tests/cxx/doctest.h $(DROPIN)/libnexel_dropin.so
 	$(CXX) $(DROPIN_CXX) -Itests/cxx -I$(REF)/tests -o $@ $< -L$(DROPIN) -lnexel_dropin -Wl,-rpath,'$$ORIGIN'
+
+$(DROPIN)/dp_train: tests/cxx/dp_train.cpp $(TRAIN_TEST_OBJS) $(DROPIN)/libnexel_dropin.so
+	$(CXX) $(DROPIN_CXX) -o $@ $< $(TRAIN_TEST_OBJS) -L$(DROPIN) -lnexel_dropin -Wl,-rpath,'$$ORIGIN'
 
 $(DROPIN)/bench_train: tests/cxx/bench_train.cpp $(TRAIN_TEST_OBJS) $(DROPIN)/libnexel_dropin.so
 	$(CXX) $(DROPIN_CXX) -o $@ $< $(TRAIN_TEST_OBJS) -L$(DROPIN) -lnexel_dropin -Wl,-rpath,'$$ORIGIN'

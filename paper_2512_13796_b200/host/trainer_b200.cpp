@@ -22,6 +22,13 @@
 // group that never stepped — and last_loss). Every reduction on the device is
 // order-independent, so two runs give bit-identical results (test_train.cpp
 // "training is deterministic run to run").
+//
+// Data parallelism over views (dp_b200.hpp, NEXEL_DP_WORLD > 1): rank r trains on
+// position r of each iteration's `world` positions of the epoch stream (every rank
+// consumes the random stream identically), the gradients and the loss terms are averaged
+// across the ranks on the device before the Adam step, and the blended errors are summed
+// before density control, so every rank holds the same scene; with one rank the loop is
+// the reference's.
 #include "nexel/trainer.hpp"
 
 #include <cuda_runtime.h>
@@ -34,6 +41,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <memory>
 #include <random>
 #include <string>
 #include <vector>
@@ -42,6 +50,7 @@
 #include "nexel/metrics.hpp"
 #include "nexel/renderer.hpp"
 #include "../../include/nexel_b200.h"
+#include "dp_b200.hpp"
 
 namespace nexel {
 
@@ -248,9 +257,16 @@ TrainResult train(const Bundle& bundle, const TrainConfig& cfg, const TrainHooks
     // ---- device run state
     Run r;
     const char* env = std::getenv("NEXEL_CUDA_DEVICE");
-    const int device = env ? std::atoi(env) : 0;
+    int device = env ? std::atoi(env) : 0;
+    const int dp_world = dp_env_world(), dp_rank = dp_env_rank();
+    if (!env && dp_world > 1) {  // one GPU per rank unless the device is given
+        int count = 1;
+        cuda_check(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+        device = dp_rank % std::max(count, 1);
+    }
     r.check(nx_ctx_create(device, &r.ctx));
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    const std::unique_ptr<DpComm> dp = DpComm::from_env(device);
     void* s = nx_ctx_stream(r.ctx);
     cudaStream_t cs = static_cast<cudaStream_t>(s);
     const nx_settings st = to_nx(init.settings);
@@ -317,12 +333,16 @@ TrainResult train(const Bundle& bundle, const TrainConfig& cfg, const TrainHooks
     for (int iter = 1; iter <= cfg.iterations; ++iter) {
         const auto t0 = std::chrono::steady_clock::now();
         tp = t0;
-        if (perm_pos == perm.size()) {  // trainer.cpp:280-284
-            perm = bundle.train_views;
-            std::shuffle(perm.begin(), perm.end(), rng);
-            perm_pos = 0;
+        int view = -1;
+        for (int q = 0; q < dp_world; ++q) {  // this rank's position of the iteration's dp_world
+            if (perm_pos == perm.size()) {    // trainer.cpp:280-284
+                perm = bundle.train_views;
+                std::shuffle(perm.begin(), perm.end(), rng);
+                perm_pos = 0;
+            }
+            const int v = perm[perm_pos++];
+            if (q == dp_rank) view = v;
         }
-        const int view = perm[perm_pos++];
         const nx_camera cam = to_nx(bundle.cameras[view]);
         const size_t npix = static_cast<size_t>(cam.width) * cam.height;
 
@@ -337,12 +357,14 @@ TrainResult train(const Bundle& bundle, const TrainConfig& cfg, const TrainHooks
         const nx_loss_weights lw{cfg.loss.dssim, cfg.loss.alpha, cfg.loss.texture, cfg.loss.opacity, cfg.loss.grid};
         r.check(nx_losses_backward_opt(r.ctx, r.scene, r.frame, gt[view], &lw, d_final, K ? d_weights : nullptr,
                                        K ? d_texture : nullptr, &grads, d_terms, r.opt, s));
+        static_assert(sizeof(nx_loss_terms) == 8 * sizeof(double), "loss terms: 8 doubles");
+        if (dp) dp->all_reduce(reinterpret_cast<double*>(d_terms), 8, true, cs);  // the ranks' mean loss
         nx_loss_terms ht;
         cuda_check(cudaMemcpyAsync(&ht, d_terms, sizeof ht, cudaMemcpyDeviceToHost, cs), "terms");
         cuda_check(cudaStreamSynchronize(cs), "sync");
         terms = from_nx(ht);
         if (!terms.finite()) {  // trainer.cpp:291-299
-            if (!cfg.snapshot_path.empty()) {
+            if (!cfg.snapshot_path.empty() && dp_rank == 0) {
                 CheckpointExtra snap;
                 snap.cameras = bundle.cameras;
                 snap.iteration = static_cast<std::uint64_t>(iter);
@@ -355,6 +377,13 @@ TrainResult train(const Bundle& bundle, const TrainConfig& cfg, const TrainHooks
         r.check(nx_pixel_error(r.ctx, r.frame, gt[view], err_pixel, s));
         const nx_upstream up{d_final, K ? d_weights : nullptr, K ? d_texture : nullptr};
         r.check(nx_render_backward(r.ctx, r.scene, &cam, r.frame, &up, &grads, err_pixel, err_accum, s));
+        if (dp) {  // the replicas' mean gradient (in place, on the run's stream)
+            dp->all_reduce(g_prims, n * NX_PARAMS_PER_NEXEL, true, cs);
+            dp->all_reduce(g_table, n_table, true, cs);
+            dp->all_reduce(g_w1, n_w1, true, cs);
+            dp->all_reduce(g_w2, n_w2, true, cs);
+            dp->all_reduce(g_w3, n_w3, true, cs);
+        }
         mark(2);
 
         gcfg[kGroupPosition].lr = cfg.lr_position * ext *
@@ -364,6 +393,7 @@ TrainResult train(const Bundle& bundle, const TrainConfig& cfg, const TrainHooks
 
         if (cfg.densify_every > 0 && iter % cfg.densify_every == 0 && iter >= cfg.densify_start &&
             iter <= cfg.densify_end) {  // trainer.cpp:324-333
+            if (dp) dp->all_reduce(err_accum, n, false, cs);  // every rank's views' blended errors
             cuda_check(cudaStreamSynchronize(cs), "sync");
             const int allowed = std::min(static_cast<int>(std::ceil(cfg.split_fraction * static_cast<double>(n))),
                                          cfg.budget - static_cast<int>(n));
