@@ -998,7 +998,10 @@ __device__ __forceinline__ void b2_issue_layer(uint8_t* smem, uint32_t dtm, int 
     mma_commit(bar);
 }
 
-__global__ void __launch_bounds__(kTcThreads, 2) tex_mlp_bulk_kernel(const TextureArgs a, int bw, int bh, int tiles_x,
+#ifndef NX_B2_MINB
+#define NX_B2_MINB 2
+#endif
+__global__ void __launch_bounds__(kTcThreads, NX_B2_MINB) tex_mlp_bulk_kernel(const TextureArgs a, int bw, int bh, int tiles_x,
                                                                    int64_t n_tiles) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x, warp = tid >> 5;
