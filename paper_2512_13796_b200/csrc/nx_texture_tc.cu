@@ -919,7 +919,15 @@ __global__ void __launch_bounds__(WsCfg<kMode>::kThreads, 1)
 // The gathers of the bulk-fed variant: one thread per slot at full occupancy, features
 // split into bf16 hi / lo and stored as the tile's K-major operand image (16 KB per
 // 128-row tile: hi then lo), at the (tile, row) texture_ws_kernel<kBulk> assigns the slot.
-__global__ void __launch_bounds__(128) tex_features_img_kernel(const TextureArgs a, const TcConst cst, int bw, int bh,
+#ifndef NX_FEAT_MINB
+#define NX_FEAT_MINB 6  // 80 registers, 6 CTAs per SM (measured: 2.257 -> 2.250 ms per frame)
+#endif
+#ifdef NX_FEAT_MINB
+#define NX_FEAT_BOUNDS __launch_bounds__(128, NX_FEAT_MINB)
+#else
+#define NX_FEAT_BOUNDS __launch_bounds__(128)
+#endif
+__global__ void NX_FEAT_BOUNDS tex_features_img_kernel(const TextureArgs a, const TcConst cst, int bw, int bh,
                                                                int tiles_x) {
     const int64_t sl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int K = a.fb.K;
@@ -1224,6 +1232,250 @@ __global__ void __launch_bounds__(kTcThreads, NX_B2_MINB) tex_mlp_bulk_kernel(co
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
 
+// split2ts: the bulk-fed decoder with the hidden activations in tensor memory. The
+// epilogue writes the relu'd, bf16-split activations back to TMEM (tcgen05.st) and
+// layers 2 / 3 read their A operand from there: no shared-memory A buffer (~70 KB per
+// CTA, three CTAs per SM), no generic-to-async proxy fence. TMEM: accumulator columns
+// [0, 64), A hi [64, 96), A lo [96, 128).
+constexpr int kTsOffImg = kOffAh;                         // the weights, then two images
+constexpr int kTsOffRgb = kTsOffImg + 2 * kImgBytes;
+constexpr int kTsOffBar = kTsOffRgb + kRows * 3 * 4;
+constexpr int kTsOffTmem = kTsOffBar + 3 * 8;
+constexpr int kTsSmem = kTsOffTmem + 8;
+constexpr uint32_t kTsTmemCols = 128;
+static_assert(kTsSmem <= 74 * 1024, "three CTAs per SM");
+
+__device__ __forceinline__ void ts_issue_layer(uint32_t dtm, uint32_t a_hi, uint32_t a_lo, uint8_t* smem, int off_bh,
+                                               int off_bl, int K, uint32_t idesc, uint32_t bar) {
+    const uint32_t bh = smem_u32(smem + off_bh), bl = smem_u32(smem + off_bl);
+    const uint32_t sbo = 16 * K;
+    for (int s = 0; s < K / 16; ++s) {
+        const uint32_t o = s * 256;
+        mma_bf16_ts(dtm, a_hi + 8 * s, smem_desc(bh + o, 128, sbo), idesc, s > 0);
+        mma_bf16_ts(dtm, a_hi + 8 * s, smem_desc(bl + o, 128, sbo), idesc, 1);
+        mma_bf16_ts(dtm, a_lo + 8 * s, smem_desc(bh + o, 128, sbo), idesc, 1);
+    }
+    mma_commit(bar);
+}
+
+#ifndef NX_TS_MINB
+#define NX_TS_MINB 3
+#endif
+__global__ void __launch_bounds__(kTcThreads, NX_TS_MINB) tex_mlp_ts_kernel(const TextureArgs a, int bw, int bh, int tiles_x,
+                                                                   int64_t n_tiles) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t bar = smem_u32(smem + kTsOffBar);
+    auto full = [&](int b) { return smem_u32(smem + kTsOffBar + 8 * (1 + b)); };
+    for (int e = tid; e < kHid * kIn / 8; e += kTcThreads) {  // W1 [64][32]
+        const int n = e / (kIn / 8), c = e % (kIn / 8);
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(a.scene.w1 + n * kIn + c * 8 + i);
+        store_split8(smem, kOffW1h, kOffW1l, kmajor_off(n, c * 8, kIn), x);
+    }
+    for (int e = tid; e < kHid * kHid / 8; e += kTcThreads) {  // W2 [64][64]
+        const int n = e / (kHid / 8), c = e % (kHid / 8);
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(a.scene.w2 + n * kHid + c * 8 + i);
+        store_split8(smem, kOffW2h, kOffW2l, kmajor_off(n, c * 8, kHid), x);
+    }
+    for (int e = tid; e < kOut * kHid / 8; e += kTcThreads) {  // W3 [48][64]
+        const int n = e / (kHid / 8), c = e % (kHid / 8);
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(a.scene.w3 + n * kHid + c * 8 + i);
+        store_split8(smem, kOffW3h, kOffW3l, kmajor_off(n, c * 8, kHid), x);
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem + kTsOffTmem)),
+                     "r"(kTsTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 32) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full(0)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full(1)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + kTsOffTmem);
+    uint32_t phase = 0;
+    const int K = a.fb.K, W = a.cam.W, H = a.cam.H;
+    const int row = tid, ppt = bw * bh;
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * warp) << 16);
+    float* srgb = reinterpret_cast<float*>(smem + kTsOffRgb);
+    constexpr uint32_t kIdesc64 = idesc_bf16_f32(kRows, 64);
+    constexpr uint32_t kIdesc48 = idesc_bf16_f32(kRows, 48);
+    const uint8_t* img = reinterpret_cast<const uint8_t*>(a.fscratch);
+    auto load_tile = [&](int64_t tile, int b) {  // thread 0: the tile's 16 KB image into buffer b
+        const uint32_t dst = smem_u32(smem + kTsOffImg + b * kImgBytes);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full(b)), "r"(kImgBytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                     "l"(img + tile * kImgBytes), "r"(kImgBytes), "r"(full(b))
+                     : "memory");
+    };
+    int n_queries = 0;
+    int64_t k = 0;
+    if (tid == 0 && blockIdx.x < n_tiles) load_tile(blockIdx.x, 0);
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+        const int b = static_cast<int>(k & 1);
+        // the other buffer's last reader (the previous tile's layer 1) has completed
+        if (tid == 0 && tile + gridDim.x < n_tiles) load_tile(tile + gridDim.x, b ^ 1);
+        const WsTile wt = ws_tile(tile, row, K, bw, bh, tiles_x, W, H);
+        const bool valid = wt.in_tile && a.fb.ids[wt.slot] >= 0;
+        n_queries += valid;
+        // Eq. 7 inputs of pixel `row` of the tile, loaded now: their latency hides behind
+        // the three layers instead of stalling the tile's end
+        constexpr int kPre = 4;
+        int64_t e_pix = -1;
+        double e_acc[3] = {0.0, 0.0, 0.0}, e_w[kPre];
+        int32_t e_id[kPre];
+        if (row < ppt) {
+            const int qx = static_cast<int>(tile % tiles_x) * bw + row % bw;
+            const int qy = static_cast<int>(tile / tiles_x) * bh + row / bw;
+            if (qx < W && qy < H) {
+                e_pix = static_cast<int64_t>(qy) * W + qx;
+                e_acc[0] = a.fb.base[e_pix * 3 + 0];
+                e_acc[1] = a.fb.base[e_pix * 3 + 1];
+                e_acc[2] = a.fb.base[e_pix * 3 + 2];
+#pragma unroll
+                for (int j = 0; j < kPre; ++j) {
+                    e_id[j] = j < K ? a.fb.ids[e_pix * K + j] : -1;
+                    e_w[j] = j < K ? a.fb.weights[e_pix * K + j] : 0.0;
+                }
+            }
+        }
+        mbar_wait(full(b), static_cast<uint32_t>((k >> 1) & 1));
+        tc_fence_after();
+        const int ib = kTsOffImg + b * kImgBytes;
+        if (tid == 0) b2_issue_layer(smem, tmem, ib, ib + kImgBytes / 2, kOffW1h, kOffW1l, kIn, kIdesc64, bar);
+        double dir[3] = {0.0, 0.0, 1.0};
+        if (wt.in_tile) pixel_dir(a.cam, wt.px + 0.5, wt.py + 0.5, dir);
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+#pragma unroll 1
+        for (int layer = 0; layer < 2; ++layer) {
+            {
+                uint32_t r[kHid];
+                tmem_ld_batch<kHid / 16>(taddr, r);
+                uint32_t hi[kHid / 2], lo[kHid / 2];
+#pragma unroll
+                for (int i = 0; i < kHid / 2; ++i) {
+                    const float x0 = fmaxf(__uint_as_float(r[2 * i]), 0.f), x1 = fmaxf(__uint_as_float(r[2 * i + 1]), 0.f);
+                    hi[i] = pack_bf16(x0, x1);
+                    const float h0 = __uint_as_float(hi[i] << 16), h1 = __uint_as_float(hi[i] & 0xffff0000u);
+                    lo[i] = pack_bf16(x0 - h0, x1 - h1);
+                }
+                tmem_st32(taddr + 64, hi);
+                tmem_st32(taddr + 96, lo);
+                tmem_wait_st();
+            }
+            tc_fence_before();
+            __syncthreads();
+            tc_fence_after();
+            if (tid == 0) {
+                if (layer == 0) ts_issue_layer(tmem, tmem + 64, tmem + 96, smem, kOffW2h, kOffW2l, kHid, kIdesc64, bar);
+                else ts_issue_layer(tmem, tmem + 64, tmem + 96, smem, kOffW3h, kOffW3l, kHid, kIdesc48, bar);
+            }
+            mbar_wait(bar, phase);
+            phase ^= 1;
+            tc_fence_after();
+        }
+        {
+            float bb[16];
+            sh_basis_f32(static_cast<float>(dir[0]), static_cast<float>(dir[1]), static_cast<float>(dir[2]), bb);
+            float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+#if NX_TMEM_BATCH
+            {
+                uint32_t r[kOut];
+                tmem_ld_batch<kOut / 16>(taddr, r);
+#pragma unroll
+                for (int o = 0; o < kOut; ++o) {
+                    const float v = __uint_as_float(r[o]);
+                    const int kk = o / 3;
+                    if (o % 3 == 0) c0 = fmaf(v, bb[kk], c0);
+                    else if (o % 3 == 1) c1 = fmaf(v, bb[kk], c1);
+                    else c2 = fmaf(v, bb[kk], c2);
+                }
+            }
+#else
+#pragma unroll
+            for (int c = 0; c < kOut / 16; ++c) {
+                float v[16];
+                tmem_ld16(taddr + 16 * c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int o = 16 * c + i, kk = o / 3;
+                    if (o % 3 == 0) c0 = fmaf(v[i], bb[kk], c0);
+                    else if (o % 3 == 1) c1 = fmaf(v[i], bb[kk], c1);
+                    else c2 = fmaf(v[i], bb[kk], c2);
+                }
+            }
+#endif
+            float rgb[3] = {0.f, 0.f, 0.f};
+            if (valid) {
+                rgb[0] = fmaxf(0.5f + c0, 0.f);
+                rgb[1] = fmaxf(0.5f + c1, 0.f);
+                rgb[2] = fmaxf(0.5f + c2, 0.f);
+            }
+            srgb[row * 3 + 0] = rgb[0];
+            srgb[row * 3 + 1] = rgb[1];
+            srgb[row * 3 + 2] = rgb[2];
+            if (wt.in_tile) {
+                a.fb.texture[wt.slot * 3 + 0] = rgb[0];
+                a.fb.texture[wt.slot * 3 + 1] = rgb[1];
+                a.fb.texture[wt.slot * 3 + 2] = rgb[2];
+            }
+        }
+        tc_fence_before();
+        __syncthreads();
+        // Eq. 7: final = base + sum_j W[p,j] * texture[p,j] (renderer.cpp:219-236)
+        if (e_pix >= 0) {
+            const int64_t pix = e_pix;
+            double acc0 = e_acc[0], acc1 = e_acc[1], acc2 = e_acc[2];
+            if (K <= kPre) {
+#pragma unroll
+                for (int j = 0; j < kPre; ++j) {
+                    if (j >= K || e_id[j] < 0) continue;
+                    const double w = e_w[j];
+                    const float* tc = srgb + (row * K + j) * 3;
+                    acc0 += w * tc[0];
+                    acc1 += w * tc[1];
+                    acc2 += w * tc[2];
+                }
+            } else {
+                for (int j = 0; j < K; ++j) {
+                    const int64_t q = pix * K + j;
+                    if (a.fb.ids[q] < 0) continue;
+                    const double w = a.fb.weights[q];
+                    const float* tc = srgb + (row * K + j) * 3;
+                    acc0 += w * tc[0];
+                    acc1 += w * tc[1];
+                    acc2 += w * tc[2];
+                }
+            }
+            a.fb.final_img[pix * 3 + 0] = static_cast<float>(acc0);
+            a.fb.final_img[pix * 3 + 1] = static_cast<float>(acc1);
+            a.fb.final_img[pix * 3 + 2] = static_cast<float>(acc2);
+        }
+        // srgb and the A operand are rewritten next tile only after its layer-1 wait and
+        // the barrier before layer 2, which every thread reaches after this point
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n_queries += __shfl_down_sync(0xffffffffu, n_queries, o);
+    if ((tid & 31) == 0 && n_queries) atomicAdd(&a.stats->queries, static_cast<unsigned long long>(n_queries));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTsTmemCols));
+}
+
 }  // namespace
 
 int texture_tc_path() {
@@ -1238,6 +1490,7 @@ int texture_tc_path() {
         if (e && strcmp(e, "ws") == 0) return 0;
         if (e && strcmp(e, "bulk") == 0) return 3;
         if (e && strcmp(e, "split") == 0) return 2;
+        if (e && strcmp(e, "split2ts") == 0) return 5;
         return 4;
     }();
     return path;
@@ -1247,7 +1500,7 @@ size_t texture_tc_scratch_bytes(int W, int H, int K) {
     if (K <= 0) return 0;
     const int path = texture_tc_path();
     if (path == 2) return static_cast<size_t>(W) * H * K * kIn * sizeof(float);
-    if (path != 3 && path != 4) return 0;
+    if (path != 3 && path != 4 && path != 5) return 0;
     const int ppt = kRows / K;
     const int bw = (kRows % K == 0 && ppt % 8 == 0) ? 8 : ppt;
     const int bh = ppt / bw;
@@ -1264,7 +1517,7 @@ int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
     // over a feature scratch), "ws" (warp-specialised, no scratch) or "fused" (one CTA
     // role, three per SM).
     const int path = texture_tc_path();
-    if ((path == 0 || ((path == 3 || path == 4) && a.fscratch)) && K > 0) {
+    if ((path == 0 || ((path == 3 || path == 4 || path == 5) && a.fscratch)) && K > 0) {
         const int ppt = kRows / K;
         const int bw = (kRows % K == 0 && ppt % 8 == 0) ? 8 : ppt;
         const int bh = ppt / bw;
@@ -1299,6 +1552,16 @@ int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
         if (a.ev_mid) {
             cudaEventRecord(a.ev_mid, s);
             a.ev_mid_recorded = true;
+        }
+        if (path == 5) {  // split2ts: activations in tensor memory, three CTAs per SM
+            cudaFuncSetAttribute(tex_mlp_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTsSmem);
+            static const int per_sm = [] {  // resident decoder CTAs per SM (shared with the composite)
+                const char* e = getenv("NX_TS_CTAS_PER_SM");
+                return e ? std::max(1, atoi(e)) : 2;
+            }();
+            const int64_t g3 = std::min<int64_t>(n_tiles, per_sm * static_cast<int64_t>(sms));
+            tex_mlp_ts_kernel<<<static_cast<unsigned>(g3), kTcThreads, kTsSmem, s>>>(a, bw, bh, tiles_x, n_tiles);
+            return NX_OK;
         }
         if (path == 4) {  // split2: the single-role decoder fed by bulk copies, two CTAs per SM
             cudaFuncSetAttribute(tex_mlp_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kB2Smem);

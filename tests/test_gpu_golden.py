@@ -91,7 +91,8 @@ def test_tensor_core_texture_variants_are_bit_identical(K):
     """The bulk-fed warp-specialised texture pass, the warp-specialised kernel with
     gather warps, the split gathers + MLP kernels (default) and the single-role fused kernel
     run the same gathers and the same tcgen05 MMAs on the
-    same operands, so texture and final_img agree bit for bit (full 1080p frame at
+    same operands (split2ts with the hidden activations in tensor memory), so texture and
+    final_img agree bit for bit (full 1080p frame at
     K = 2 — 1020 tiles per SM in flight through the mbarrier pipeline — smaller ones
     for K that do not divide the 128-row tile)."""
     import subprocess
@@ -101,13 +102,13 @@ def test_tensor_core_texture_variants_are_bit_identical(K):
             "r = nx.Renderer(0); d = r.upload(s); f = r.frame(); r.render(d, c, f); g = f.download(); "
             "np.savez(sys.argv[1], t=g.texture, f=g.final_img, ids=g.ids)") % (os.path.dirname(HERE), n, K, w, h)
     out = {}
-    for path in ("bulk", "ws", "split", "fused", "split2"):
+    for path in ("bulk", "ws", "split", "fused", "split2", "split2ts"):
         fn = f"/tmp/nx_texv_{path}_{K}_{os.getpid()}.npz"
         env = dict(os.environ)
         env["NX_TEXTURE_PATH"] = path
         subprocess.run([sys.executable, "-c", code, fn], check=True, env=env, timeout=900)
         out[path] = np.load(fn)
     assert (out["bulk"]["ids"] >= 0).sum() > 0
-    for other in ("ws", "split", "fused", "split2"):
+    for other in ("ws", "split", "fused", "split2", "split2ts"):
         assert np.array_equal(out["bulk"]["t"], out[other]["t"]), other
         assert np.array_equal(out["bulk"]["f"], out[other]["f"]), other

@@ -1,7 +1,7 @@
 #!/bin/bash
-# ptxas register / spill summary of one .cu file's kernels: bash tools/regs.sh FILE [name regex]
+# ptxas register / spill summary of one .cu file's kernels: [REGS_FLAGS=-D...] bash tools/regs.sh FILE [name regex]
 /usr/local/cuda/bin/nvcc -O3 -lineinfo -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC,-O3 \
-  --expt-relaxed-constexpr -Xptxas -v -c -o /tmp/regs_$$.o "$1" 2>&1 | python3 -c "
+  --expt-relaxed-constexpr $REGS_FLAGS -Xptxas -v -c -o /tmp/regs_$$.o "$1" 2>&1 | python3 -c "
 import re, sys, subprocess
 pat = re.compile(sys.argv[1])
 name = None
