@@ -755,8 +755,16 @@ int nx_ctx_create(int device, nx_ctx** out) {
     if (const char* e = std::getenv("NX_EMIT_CULL")) c->emit_cull = std::atoi(e) != 0;
     if (const char* e = std::getenv("NX_CERT_REDO_ALL")) c->redo_all = std::atoi(e) != 0;
     if (const char* e = std::getenv("NX_KEY_CAP")) c->key_cap = std::atoll(e);  // tests: start from a small capacity
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+    // The collection stream outranks the texture stream: the block scheduler hands the next
+    // frame's latency-bound binning kernels SMs ahead of the remaining CTAs of the
+    // previous frame's texture gathers, which fill the gaps instead of blocking them
+    // (NX_STREAM_PRIORITY=0: equal priorities).
+    int prio_low = 0, prio_high = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
+    if (const char* e = std::getenv("NX_STREAM_PRIORITY"))
+        if (std::atoi(e) == 0) prio_low = prio_high = 0;
+    if (cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_high) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, prio_low) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->stream_bwd, cudaStreamNonBlocking) != cudaSuccess ||

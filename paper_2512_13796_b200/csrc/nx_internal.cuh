@@ -289,8 +289,9 @@ bool texture_tc_supported(const nx_field_desc& fd);
 // 0: warp-specialised with gather warps, 1: fused single-role, 2: split (gathers, then
 // the MLP over an fp32 feature scratch), 3: bulk-fed warp-specialised (gathers into
 // pre-split operand tiles, then the MMA pipeline fed by cp.async.bulk), 4: split2
-// (default: gathers into pre-split operand tiles, then a single-role decoder that
-// double-buffers them with cp.async.bulk)
+// (gathers into pre-split operand tiles, then a single-role decoder that double-buffers
+// them with cp.async.bulk), 5: split2ts (default: split2 with the decoder's hidden
+// activations in tensor memory, three CTAs per SM)
 int texture_tc_path();
 // bytes of TextureArgs::fscratch the selected path needs for a W x H x K frame (0: none)
 size_t texture_tc_scratch_bytes(int W, int H, int K);

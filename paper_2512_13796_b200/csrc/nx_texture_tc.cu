@@ -1479,9 +1479,10 @@ __global__ void __launch_bounds__(kTcThreads, NX_TS_MINB) tex_mlp_ts_kernel(cons
 }  // namespace
 
 int texture_tc_path() {
-    // Measured at config 2 (ms per frame, two streams / one stream; round-2 composite):
-    // split2 2.45 / 2.80 (default), split 2.53 / 2.78, bulk-fed warp-specialised with 4
-    // epilogue groups 2.81 / 2.82, gather warp-specialised 3.05 / 3.12. The warp-
+    // Measured at config 2 (ms per frame, two streams / one stream): split2ts 2.21 / 2.42
+    // (default; with the collection stream at the higher priority), split2 2.25 / 2.56,
+    // and with the earlier round-2 composite split 2.53 / 2.78, bulk-fed warp-specialised
+    // with 4 epilogue groups 2.81 / 2.82, gather warp-specialised 3.05 / 3.12. The warp-
     // specialised kernels hold one ~170-200 KB CTA per SM, so the next frame's composite
     // cannot share the SM while they run.
     static const int path = [] {
@@ -1490,8 +1491,8 @@ int texture_tc_path() {
         if (e && strcmp(e, "ws") == 0) return 0;
         if (e && strcmp(e, "bulk") == 0) return 3;
         if (e && strcmp(e, "split") == 0) return 2;
-        if (e && strcmp(e, "split2ts") == 0) return 5;
-        return 4;
+        if (e && strcmp(e, "split2") == 0) return 4;
+        return 5;
     }();
     return path;
 }
@@ -1557,7 +1558,7 @@ int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
             cudaFuncSetAttribute(tex_mlp_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTsSmem);
             static const int per_sm = [] {  // resident decoder CTAs per SM (shared with the composite)
                 const char* e = getenv("NX_TS_CTAS_PER_SM");
-                return e ? std::max(1, atoi(e)) : 2;
+                return e ? std::max(1, atoi(e)) : 3;
             }();
             const int64_t g3 = std::min<int64_t>(n_tiles, per_sm * static_cast<int64_t>(sms));
             tex_mlp_ts_kernel<<<static_cast<unsigned>(g3), kTcThreads, kTsSmem, s>>>(a, bw, bh, tiles_x, n_tiles);
