@@ -117,6 +117,32 @@ def composite_compute_roofline(comp_ms, sm_mhz):
                     "`roofline` is kept for the contract"}
 
 
+def pcie_roofline(d2h_bytes_per_frame, frames_per_s, device):
+    """The end-to-end bound: the FrameBuffers' device -> host bytes per second against
+    this box's measured device -> pinned-host copy bandwidth (192 MB copies, best of 3)."""
+    import torch
+    try:
+        n = 192 << 20
+        src = torch.empty(n, dtype=torch.uint8, device=f"cuda:{device}")
+        dst = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        best = 0.0
+        for _ in range(3):
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, n / (e0.elapsed_time(e1) / 1e3) / 1e9)
+        del src, dst
+    except Exception as e:  # noqa: BLE001 - reported, never required
+        return {"error": f"{type(e).__name__}: {e}"}
+    achieved = d2h_bytes_per_frame * frames_per_s / 1e9
+    return {"bound": "pcie", "achieved": achieved, "peak": best, "unit": "GB/s", "frac": achieved / best,
+            "peak_source": "measured in this run (device -> pinned host copy, 192 MB)"}
+
+
 def dropin_line():
     """nexel::render (the reference's C++ API, host Scene in / FrameBuffers out) through the
     drop-in library, at config 2: tests/cxx/bench_render.cpp, if built (make dropin)."""
@@ -522,8 +548,6 @@ def run_ours(args):
     if world > 1:
         store = dist.distributed_c10d._get_default_store()
         dealer = DynamicDealer(args.steps * world, store=store, key="nx_bench_views", start=args.warmup * world)
-    r.set_profiling(True)
-    r.stage_times()  # reset accumulators
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = r.lib.nx_launch_count()
@@ -547,6 +571,15 @@ def run_ours(args):
     launches = int(r.lib.nx_launch_count() - launches0)
     clk = clocks.stop()
     ms_local = ev0.elapsed_time(ev1)
+    # per-stage kernel durations for the rooflines: the timed views again, untimed, on ONE
+    # stream with stage events (with two streams the low-priority texture stream's span
+    # stretches while the next frame's collection kernels hold the SMs, so its events would
+    # time sharing, not the kernels)
+    r.set_profiling(True)
+    r.stage_times()  # reset accumulators
+    for v in views[args.warmup:][:20]:
+        r.render(ds, cams[v], frames[0], r.stream)
+    r.synchronize()
     stage_ms, prof_frames = r.stage_times()
     r.set_profiling(False)
     ms = max_over_ranks(dist, ms_local, f"cuda:{local}")
@@ -592,6 +625,7 @@ def run_ours(args):
     barrier(dist)
     e2e_ms = max_over_ranks(dist, e0.elapsed_time(e1), f"cuda:{local}")
     e2e_fps = frames_total / (e2e_ms / 1e3)
+    e2e_roof = pcie_roofline(d2h, e2e_fps / world, local)
 
     # ---- roofline of the dominant stage (algorithmic bytes per launch / mean launch time)
     timed_views = views[args.warmup:]
@@ -666,6 +700,7 @@ def run_ours(args):
                                    "evaluated_per_frame_note": "the work lists and the fp32 prefilter leave "
                                                                "~27M exact fp64 evaluations per frame"},
             "stages_ms": stage_ms, "profiled_frames": prof_frames,
+            "stages_note": "per-stage kernel time of the timed views re-rendered on one stream after the timed region",
             "work": {"tile_keys_P": P, "work_keys": Pw, "queries_Q": Q},
             # the safety net of the bit-exact claim: decisions of the timed views whose margin
             # is below a generous bound on device-vs-reference math differences (all 0 = every
@@ -675,7 +710,8 @@ def run_ours(args):
                                          "near_support")},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_fps, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "path": "nx_render + nx_frame_download (all FrameBuffers) into pinned host memory, 3 frames in flight"},
+                    "path": "nx_render + nx_frame_download (all FrameBuffers) into pinned host memory, 3 frames in flight",
+                    "roofline": e2e_roof},
             "gpu_launches": launches, "clocks": clk,
             "train_step": train,
             "e2e_dropin": dropin_line() if (world == 1 and not args.no_cpu_baseline) else None,
