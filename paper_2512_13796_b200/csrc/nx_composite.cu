@@ -189,10 +189,19 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
     }
     const float dfx = static_cast<float>(dir[0]), dfy = static_cast<float>(dir[1]), dfz = static_cast<float>(dir[2]);
 
-    double T = 1.0;
-    double acc[3] = {0.0, 0.0, 0.0};
+    // March precision: fp64 on the exact path; the certified pass marches in fp32 (its
+    // alphas are fp32 already) and folds each fp32 rounding of T and of a weight into
+    // the tracked bounds (kCertRound), so every decision it takes stays certified.
+#ifndef NX_CERT_F32_MARCH
+#define NX_CERT_F32_MARCH 1
+#endif
+    using TT = std::conditional_t<kCert && NX_CERT_F32_MARCH, float, double>;
+    constexpr float kCertRound = 1.2e-7f;  // > 2^-23: one fp32 rounding, with slack
+    TT T = 1.0;
+    TT acc[3] = {0.0, 0.0, 0.0};
     int32_t k_id[KK];
-    double k_w[KK], k_t[KK];
+    TT k_w[KK];
+    double k_t[KK];
     CT k_rgb[KR][3];
 #pragma unroll
     for (int s = 0; s < KK; ++s) {
@@ -437,9 +446,9 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                     if (res.alpha < 0.0) continue;
                     const int32_t id = res.id;
                     // (certified entries arrive clamped)
-                    const double alpha = kCert ? static_cast<double>(res.alpha)
-                                               : (alpha_max < res.alpha ? alpha_max : static_cast<double>(res.alpha));
-                    const double wgt = alpha * T;
+                    const TT alpha = kCert ? static_cast<TT>(res.alpha)
+                                           : static_cast<TT>(alpha_max < res.alpha ? alpha_max : static_cast<double>(res.alpha));
+                    const TT wgt = alpha * T;
                     float eps_a = 0.f;  // certified mode: alpha's relative error bound
                     if constexpr (kCert) eps_a = res.eps;
                     acc[0] += wgt * res.rgb[0];
@@ -459,8 +468,9 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                         if (k_size < K) {
                             pos = k_size++;
                         } else {
-                            const double wm = k_w[KK - 1];
-                            if (kCert && fabs(wgt - wm) <= (eps_a + k_ea[KK - 1] + (E_T - k_et[KK - 1])) * fmax(wgt, wm))
+                            const TT wm = k_w[KK - 1];
+                            if (kCert && fabs(wgt - wm) <= (eps_a + k_ea[KK - 1] + (E_T - k_et[KK - 1]) + 2.f * kCertRound) *
+                                                               fmax(wgt, wm))
                                 unsure = true;
                             if (kNear && !kCert) n_near += (wgt != wm) & (fabs(wgt - wm) <= kNearRel * wm) ? (1u << 20) : 0u;
                             if (wgt > wm) pos = KK - 1;
@@ -482,8 +492,9 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
 #pragma unroll
                         for (int s = KK - 1; s >= 1; --s)
                             if (s == pos) {
-                                const double wp = k_w[s - 1];
-                                if (kCert && fabs(wgt - wp) <= (eps_a + k_ea[s - 1] + (E_T - k_et[s - 1])) * fmax(wgt, wp))
+                                const TT wp = k_w[s - 1];
+                                if (kCert && fabs(wgt - wp) <= (eps_a + k_ea[s - 1] + (E_T - k_et[s - 1]) + 2.f * kCertRound) *
+                                                                   fmax(wgt, wp))
                                     unsure = true;
                                 if (kNear && !kCert)
                                     n_near += (wgt != wp) & (fabs(wgt - wp) <= kNearRel * wp) ? (1u << 20) : 0u;
@@ -514,13 +525,15 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                         ++dbg_n;
                     }
                     if constexpr (kCert) {  // T *= 1 - alpha with 1 - alpha from the entry (no cancellation)
-                        T *= static_cast<double>(res.oma);
-                        E_T += res.eps_oma;
-                        if (fabs(T - min_T) <= static_cast<double>(E_T) * T) unsure = true;  // T vs min_T uncertain
+                        T *= res.oma;
+                        E_T += res.eps_oma + kCertRound;
+                        // T vs min_T uncertain (fp32 min_T and the subtraction: one more rounding each)
+                        if (fabs(T - static_cast<TT>(min_T)) <= (E_T + 2.f * kCertRound) * fmax(T, static_cast<TT>(min_T)))
+                            unsure = true;
                     } else {
                         T *= 1.0 - alpha;
                     }
-                    if (T < min_T) active = false;
+                    if (static_cast<double>(T) < min_T) active = false;
                     // (certified pass: uncertain T / top-K decisions are redone exactly and counted there)
                     if (kNear && !kCert) n_near += fabs(T - min_T) <= kNearRel * min_T ? (1u << 10) : 0u;
                 }
@@ -534,9 +547,9 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
         const int64_t pix = static_cast<int64_t>(py) * W + px;
         a.fb.residual[pix] = static_cast<float>(T);
         if (a.fb.residual64) a.fb.residual64[pix] = T;
-        acc[0] += T * a.st.background[0];
-        acc[1] += T * a.st.background[1];
-        acc[2] += T * a.st.background[2];
+        acc[0] += T * static_cast<TT>(a.st.background[0]);
+        acc[1] += T * static_cast<TT>(a.st.background[1]);
+        acc[2] += T * static_cast<TT>(a.st.background[2]);
         if (K > 0) {
             // finalize (framebuffers.hpp:51-56): the slots are already in rank order; slots >= size
             // keep their sentinels.
