@@ -460,7 +460,7 @@ int build_lists(nx_ctx* c, const nx_scene* scene, const nx_camera& cam, nx_frame
     NX_CUDA(c, c->tile_counts.ensure((n_tiles + 1) * sizeof(int32_t)));
     NX_CUDA(c, f->tile_offsets.ensure((n_tiles + 1) * sizeof(int32_t)));
     const size_t scratch_ints =
-        std::max({scan_scratch_ints(nn), radix_scratch_ints(nn), scan_scratch_ints(n_tiles + 1)}) + 64;
+        std::max({scan_scratch_ints(nn), radix_scratch_ints64(nn), scan_scratch_ints(n_tiles + 1)}) + 64;
     NX_CUDA(c, c->scratch.ensure(scratch_ints * sizeof(int32_t)));
     NX_CUDA(c, cudaMemsetAsync(f->stats, 0, sizeof(FrameStatsD), s));
 
@@ -1820,7 +1820,7 @@ int nx_scene_densify_split(nx_ctx* c, nx_scene* scene, nx_optimizer* opt, const 
     NX_CUDA(c, c->skeys_b.ensure(nn * sizeof(uint64_t)));
     NX_CUDA(c, c->sids_a.ensure(nn * sizeof(uint32_t)));
     NX_CUDA(c, c->sids_b.ensure(nn * sizeof(uint32_t)));
-    NX_CUDA(c, c->scratch.ensure((radix_scratch_ints(nn) + 64) * sizeof(int32_t)));
+    NX_CUDA(c, c->scratch.ensure((radix_scratch_ints64(nn) + 64) * sizeof(int32_t)));
     unsigned long long* d_count = reinterpret_cast<unsigned long long*>(c->scratch.as<int32_t>());
     NX_CUDA(c, cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s));
     launch_split_keys(errors, uniforms, n, c->skeys_a.as<uint64_t>(), c->sids_a.as<uint32_t>(), d_count, s);

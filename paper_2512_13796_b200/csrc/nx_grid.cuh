@@ -71,11 +71,22 @@ __device__ __forceinline__ LevelFetch fetch_level(int l, double x0, double x1, d
         cz0 = map_positive32(b2) * 805459861u;
         cz1 = map_positive32(b2 + 1) * 805459861u;
     }
-    const float2* slab = tab + static_cast<size_t>(l) * T;
+    if (T <= (1u << 28)) {
+        // every row of the 16 levels indexes in 32 bits: (row & mask) | l T is one LOP3 and
+        // the address one wide multiply-add (instead of a 64-bit slab add + shift per corner)
+        const uint32_t lb = static_cast<uint32_t>(l) * T;
 #pragma unroll
-    for (int ci = 0; ci < 8; ++ci) {
-        const uint32_t rowi = ((ci & 1) ? ax1 : ax0) ^ ((ci & 2) ? by1 : by0) ^ ((ci & 4) ? cz1 : cz0);
-        f.v[ci] = __ldg(slab + (rowi & mask));
+        for (int ci = 0; ci < 8; ++ci) {
+            const uint32_t rowi = ((ci & 1) ? ax1 : ax0) ^ ((ci & 2) ? by1 : by0) ^ ((ci & 4) ? cz1 : cz0);
+            f.v[ci] = __ldg(tab + ((rowi & mask) | lb));
+        }
+    } else {
+        const float2* slab = tab + static_cast<size_t>(l) * T;
+#pragma unroll
+        for (int ci = 0; ci < 8; ++ci) {
+            const uint32_t rowi = ((ci & 1) ? ax1 : ax0) ^ ((ci & 2) ? by1 : by0) ^ ((ci & 4) ? cz1 : cz0);
+            f.v[ci] = __ldg(slab + (rowi & mask));
+        }
     }
     return f;
 }

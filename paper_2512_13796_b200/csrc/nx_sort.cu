@@ -134,7 +134,11 @@ __global__ void __launch_bounds__(kScanThreads) scan_onepass_kernel(const int32_
 constexpr int kMaxPasses = 8;
 constexpr int kHistOff = 16;
 constexpr int kStatusOff = kHistOff + kMaxPasses * kRadixBuckets;  // even: 64-bit aligned
-constexpr int kRadixItems = kRadixTile / kRadixThreads;            // per thread (4)
+template <typename K>
+constexpr int tile_of() {  // keys per block per pass
+    return sizeof(K) == 8 ? kRadixTile64 : kRadixTile;
+}
+static_assert(kRadixTile % kRadixThreads == 0 && kRadixTile64 % kRadixThreads == 0, "whole items per thread");
 
 template <typename K>
 __global__ void __launch_bounds__(kRadixThreads) radix_upsweep_kernel(const K* keys, int64_t n_cap,
@@ -163,6 +167,8 @@ __global__ void __launch_bounds__(kRadixThreads) radix_pass_kernel(const K* __re
                                                                    const int32_t* __restrict__ n_dev, int shift,
                                                                    int pass, int n_blocks, int32_t* scratch) {
     constexpr int kWarps = kRadixThreads / 32;
+    constexpr int kTile = tile_of<K>();
+    constexpr int kRadixItems = kTile / kRadixThreads;  // per thread
     __shared__ int s_cnt[kWarps][kRadixBuckets];
     __shared__ int s_local[kRadixBuckets];  // block-local running count per digit
     __shared__ int s_glob[kRadixBuckets];   // global base of each digit for this block
@@ -176,11 +182,11 @@ __global__ void __launch_bounds__(kRadixThreads) radix_pass_kernel(const K* __re
     __syncthreads();
     if (hcount == n) s_trivial = 1;  // every key has this digit: the pass is a copy
     const int b = s_block;
-    const int64_t base = static_cast<int64_t>(b) * kRadixTile;
+    const int64_t base = static_cast<int64_t>(b) * kTile;
     __syncthreads();
     if (base >= n) return;
     if (s_trivial) {
-        for (int i = tid; i < kRadixTile; i += kRadixThreads)
+        for (int i = tid; i < kTile; i += kRadixThreads)
             if (base + i < n) {
                 keys_out[base + i] = keys_in[base + i];
                 vals_out[base + i] = vals_in[base + i];
@@ -258,7 +264,7 @@ template <typename K>
 bool radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n, const int32_t* n_dev,
                      int begin_bit, int end_bit, int32_t* scratch, cudaStream_t stream) {
     if (n <= 1) return false;
-    const int n_blocks = static_cast<int>((n + kRadixTile - 1) / kRadixTile);
+    const int n_blocks = static_cast<int>((n + tile_of<K>() - 1) / tile_of<K>());
     const int passes = (end_bit - begin_bit + kRadixBits - 1) / kRadixBits;
     if (passes <= 0) return false;
     // tickets + histograms + status words start at zero
@@ -309,6 +315,11 @@ size_t radix_scratch_ints(int64_t n) {
     return static_cast<size_t>(kStatusOff + 2 * kMaxPasses * n_blocks * kRadixBuckets + 8);
 }
 
+size_t radix_scratch_ints64(int64_t n) {
+    const int64_t n_blocks = (n + kRadixTile64 - 1) / kRadixTile64;
+    return static_cast<size_t>(kStatusOff + 2 * kMaxPasses * n_blocks * kRadixBuckets + 8);
+}
+
 bool radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,
                           int64_t n, const int32_t* n_dev, int begin_bit, int end_bit, int32_t* scratch,
                           cudaStream_t stream) {
@@ -338,8 +349,9 @@ extern "C" int nx_debug_radix_sort(int key_bytes, void* keys, uint32_t* vals, in
     if (e == cudaSuccess) e = cudaMalloc(&k1, kb);
     if (e == cudaSuccess) e = cudaMalloc(&v0, vb);
     if (e == cudaSuccess) e = cudaMalloc(&v1, vb);
-    if (e == cudaSuccess) e = cudaMalloc(&sc, (nx::radix_scratch_ints(cap) + 1) * sizeof(int32_t));
-    int32_t* n_dev = sc ? sc + nx::radix_scratch_ints(cap) : nullptr;
+    const size_t sc_ints = std::max(nx::radix_scratch_ints(cap), nx::radix_scratch_ints64(cap));
+    if (e == cudaSuccess) e = cudaMalloc(&sc, (sc_ints + 1) * sizeof(int32_t));
+    int32_t* n_dev = sc ? sc + sc_ints : nullptr;
     const int32_t n32 = static_cast<int32_t>(n);
     if (e == cudaSuccess) e = cudaMemset(k0, 0xff, kb);  // past the count: garbage the sort must not read
     if (e == cudaSuccess) e = cudaMemcpy(k0, keys, static_cast<size_t>(n) * key_bytes, cudaMemcpyHostToDevice);

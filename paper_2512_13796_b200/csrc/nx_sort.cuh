@@ -17,6 +17,12 @@ constexpr int kRadixThreads = 256;
 #define NX_RADIX_TILE 2048
 #endif
 constexpr int kRadixTile = NX_RADIX_TILE;  // items per block per pass (look-back chains of n / tile blocks)
+// 64-bit (depth) sorts: ~180K keys at config 2, latency-bound; the tile is a separate
+// knob (smaller tiles = more blocks and shorter ranking chains, measured no faster)
+#ifndef NX_RADIX_TILE64
+#define NX_RADIX_TILE64 2048  // measured at config 2: 2048 473.3, 1024 471.2, 512 469.7, 256 462.8 frames/s
+#endif
+constexpr int kRadixTile64 = NX_RADIX_TILE64;
 constexpr int kRadixBits = 8;
 constexpr int kRadixBuckets = 1 << kRadixBits;
 
@@ -32,7 +38,8 @@ void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int32_t* total, 
 // sorted result ended in the *_alt buffers. Scratch: radix_scratch_ints(n) ints.
 // n is the host-side capacity (grid size); if n_dev != nullptr the actual count is
 // read on the device (no host round trip), capped by n.
-size_t radix_scratch_ints(int64_t n);
+size_t radix_scratch_ints(int64_t n);    // for radix_sort_pairs_u32
+size_t radix_scratch_ints64(int64_t n);  // for radix_sort_pairs_u64
 bool radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,
                           int64_t n, const int32_t* n_dev, int begin_bit, int end_bit, int32_t* scratch,
                           cudaStream_t stream);
