@@ -25,6 +25,8 @@
 #include "nx_composite.cuh"
 #include "nx_fastmath.cuh"
 
+#include <cuda_fp16.h>
+
 #include <algorithm>
 #include <type_traits>
 
@@ -67,19 +69,51 @@ struct PoolEntry {         // one evaluated (pixel, primitive) pair
     double t;              // plane crossing
     CT rgb[3];             // primitive colour along the ray
     int32_t id;
+    static constexpr bool kHasId = true;
+    __device__ __forceinline__ void set_id(int32_t i) { id = i; }
 };
 
 // Certified mode: alpha from the SFU with its error bound (cert_alpha), 1 - alpha and
 // the bounds travel with the entry so that B2 can certify T and the top-K order.
+#ifndef NX_POOL_PACKED
+#define NX_POOL_PACKED 1  // 32-byte certified entries: 18.4 KB of shared memory per CTA, 11 CTAs / SM
+#endif
+#if NX_POOL_PACKED
+// 32 bytes: the two bounds as fp16 scaled by 2^20 and rounded up (an overflow reads as
+// an infinite bound, i.e. a redo), no id: B2 recovers it from the lane's survivor mask
 struct PoolEntryCert {
+    static constexpr bool kHasId = false;
     double t;
-    float alpha;    // clamped kernel alpha (< 0: miss)
-    float oma;      // 1 - alpha
-    float eps;      // relative error bound of alpha
-    float eps_oma;  // relative error bound of oma
+    float alpha;  // clamped kernel alpha (< 0: miss)
+    float oma;    // 1 - alpha
+    __half2 eps2;
+    float rgb[3];
+    __device__ __forceinline__ void set_eps(float e, float eo) {
+        eps2 = __halves2half2(__float2half_ru(e * 1048576.f), __float2half_ru(eo * 1048576.f));
+    }
+    __device__ __forceinline__ float eps() const { return __low2float(eps2) * 9.5367431640625e-07f; }
+    __device__ __forceinline__ float eps_oma() const { return __high2float(eps2) * 9.5367431640625e-07f; }
+    __device__ __forceinline__ void set_id(int32_t) {}
+};
+#else
+struct PoolEntryCert {
+    static constexpr bool kHasId = true;
+    double t;
+    float alpha;     // clamped kernel alpha (< 0: miss)
+    float oma;       // 1 - alpha
+    float eps_;      // relative error bound of alpha
+    float eps_oma_;  // relative error bound of oma
     float rgb[3];
     int32_t id;
+    __device__ __forceinline__ void set_eps(float e, float eo) {
+        eps_ = e;
+        eps_oma_ = eo;
+    }
+    __device__ __forceinline__ float eps() const { return eps_; }
+    __device__ __forceinline__ float eps_oma() const { return eps_oma_; }
+    __device__ __forceinline__ void set_id(int32_t i) { id = i; }
 };
+#endif
 
 template <typename PE>
 struct alignas(16) WarpStage {  // one warp's private staging
@@ -141,9 +175,10 @@ __device__ __forceinline__ void eval_sh_smem(const float* sh, float x, float y, 
 
 template <int K, bool kDebug, typename CT, bool kCert>
 #ifndef NX_COMPOSITE_MINB
-#define NX_COMPOSITE_MINB 10
+#define NX_COMPOSITE_MINB 11  // certified pass, measured (packed entries): 10 1.076 ms, 11 1.059, 12 1.061
 #endif
-__global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(const CompositeArgs a) {
+// (the exact-path variants keep 10: their larger pool entries fit 10 CTAs of shared memory anyway)
+__global__ void __launch_bounds__(kThreads, kCert ? NX_COMPOSITE_MINB : 10) composite_kernel(const CompositeArgs a) {
     constexpr int KK = K > 0 ? K : 1;
     constexpr bool kKeepRgb = K <= 4;  // top-K slots remember their colour (else re-evaluated at the end)
     constexpr int KR = kKeepRgb ? KK : 1;
@@ -363,7 +398,8 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                     PE res;
                     res.alpha = -1.0;
                     res.t = 0.0;
-                    res.id = sm.id[ws.sel[g0 + b]];
+                    const int32_t pid = sm.id[ws.sel[g0 + b]];
+                    res.set_id(pid);
                     if constexpr (kCert) {
                         // intersect (intersect.hpp:23-42) in fp64 up to the plane offsets, then the
                         // kernel value on the SFU with its error bound; decisions the bound does
@@ -392,13 +428,11 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                                             if (lo > alpha_max) {  // clamped: alpha_max exactly
                                                 res.alpha = static_cast<float>(alpha_max);
                                                 res.oma = static_cast<float>(1.0 - alpha_max);
-                                                res.eps = 6e-8f;
-                                                res.eps_oma = 6e-8f;
+                                                res.set_eps(6e-8f, 6e-8f);
                                             } else {
                                                 res.alpha = c.alpha;
                                                 res.oma = c.oma;
-                                                res.eps = c.eps;
-                                                res.eps_oma = c.eps_oma;
+                                                res.set_eps(c.eps, c.eps_oma);
                                             }
                                         }
                                     } else {  // the exact routine decides (rare)
@@ -410,8 +444,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                                             res.t = h.t;
                                             res.alpha = static_cast<float>(ac);
                                             res.oma = static_cast<float>(1.0 - ac);
-                                            res.eps = 1.2e-7f;
-                                            res.eps_oma = 1.2e-7f;
+                                            res.set_eps(1.2e-7f, 1.2e-7f);
                                         }
                                     }
                                     if (res.alpha >= 0.f)
@@ -429,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                             res.t = h.t;
                             if constexpr (kF64) {
                                 const double dd3[3] = {d0, d1, d2};
-                                eval_sh_f64(a.sh64 + static_cast<int64_t>(res.id) * NX_SH_VALUES, dd3, a.sh_degree,
+                                eval_sh_f64(a.sh64 + static_cast<int64_t>(pid) * NX_SH_VALUES, dd3, a.sh_degree,
                                             res.rgb);
                             } else {
                                 eval_sh_smem(ws.sh[b], static_cast<float>(d0), static_cast<float>(d1),
@@ -441,16 +474,21 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                 }
                 __syncwarp();
                 // ---- B2. per-pixel compositing of this lane's hits, in list order (renderer.cpp:144-153)
+                uint32_t mrem = mask;  // this lane's survivors in group order (ids of packed entries)
                 for (int k = off; k < off + cnt && active; ++k) {
                     const PE& res = ws.res[k];
+                    const int bk = __ffs(mrem) - 1;
+                    mrem &= mrem - 1;
                     if (res.alpha < 0.0) continue;
-                    const int32_t id = res.id;
+                    int32_t id;
+                    if constexpr (PE::kHasId) id = res.id;
+                    else id = sm.id[ws.sel[g0 + bk]];
                     // (certified entries arrive clamped)
                     const TT alpha = kCert ? static_cast<TT>(res.alpha)
                                            : static_cast<TT>(alpha_max < res.alpha ? alpha_max : static_cast<double>(res.alpha));
                     const TT wgt = alpha * T;
                     float eps_a = 0.f;  // certified mode: alpha's relative error bound
-                    if constexpr (kCert) eps_a = res.eps;
+                    if constexpr (kCert) eps_a = res.eps();
                     acc[0] += wgt * res.rgb[0];
                     acc[1] += wgt * res.rgb[1];
                     acc[2] += wgt * res.rgb[2];
@@ -526,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, NX_COMPOSITE_MINB) composite_kernel(
                     }
                     if constexpr (kCert) {  // T *= 1 - alpha with 1 - alpha from the entry (no cancellation)
                         T *= res.oma;
-                        E_T += res.eps_oma + kCertRound;
+                        E_T += res.eps_oma() + kCertRound;
                         // T vs min_T uncertain (fp32 min_T and the subtraction: one more rounding each)
                         if (fabs(T - static_cast<TT>(min_T)) <= (E_T + 2.f * kCertRound) * fmax(T, static_cast<TT>(min_T)))
                             unsure = true;
