@@ -595,7 +595,10 @@ def run_ours(args):
         "base": torch.empty(npix * 3, dtype=torch.float32, pin_memory=True),
         "ids": torch.empty(npix * K, dtype=torch.int32, pin_memory=True),
         "depths": torch.empty(npix * K, dtype=torch.float64, pin_memory=True),
-        "weights": torch.empty(npix * K, dtype=torch.float64, pin_memory=True),
+        # display frames composite in fp32 (certified march): their weights are fp32 values,
+        # so they travel as fp32 (nx_host_frame.weights_f32; only the ~300 exactly redone
+        # pixels per frame round, 6e-8 relative)
+        "weights_f32": torch.empty(npix * K, dtype=torch.float32, pin_memory=True),
         "texture": torch.empty(npix * K * 3, dtype=torch.float32, pin_memory=True),
         "final_img": torch.empty(npix * 3, dtype=torch.float32, pin_memory=True),
         "residual": torch.empty(npix, dtype=torch.float32, pin_memory=True),
@@ -777,7 +780,7 @@ def run_config4(args):
     npix = W * rows
     host = {k: torch.empty(sz, dtype=dt, pin_memory=True) for k, sz, dt in (
         ("base", npix * 3, torch.float32), ("ids", npix * K, torch.int32), ("depths", npix * K, torch.float64),
-        ("weights", npix * K, torch.float64), ("texture", npix * K * 3, torch.float32),
+        ("weights_f32", npix * K, torch.float32), ("texture", npix * K * 3, torch.float32),
         ("final_img", npix * 3, torch.float32), ("residual", npix, torch.float32))}
     hf = _abi.nx_host_frame()
     for k, t in host.items():

@@ -126,6 +126,10 @@ typedef struct nx_host_frame {
                               FrameBuffers::residual at the reference's precision */
     double* texture_f64;   /* download only: fp64 texture / final of an NX_PRECISION_F64 render */
     double* final_f64;
+    float* weights_f32;    /* download only, pinned memory, exclusive with `weights`: the slot weights
+                              as fp32. Display frames composite in fp32 (certified march), so their
+                              weights are fp32 values and this halves their bytes losslessly (the few
+                              pixels the exact redo re-renders are rounded to fp32). */
 } nx_host_frame;
 
 /* Per-frame binning / work statistics (read back with nx_frame_stats). */

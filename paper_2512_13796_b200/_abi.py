@@ -115,6 +115,7 @@ class nx_host_frame(C.Structure):
         ("residual_f64", C.c_void_p),
         ("texture_f64", C.c_void_p),
         ("final_f64", C.c_void_p),
+        ("weights_f32", C.c_void_p),
     ]
 
 

@@ -1139,23 +1139,33 @@ int nx_frame_download(nx_ctx* c, const nx_frame* fc, const nx_host_frame* dst, v
         return e && std::strcmp(e, "memcpy") == 0;
     }();
     CopyJobs jobs{};
-    auto cp = [&](void* d, const DevBuf& b, size_t bytes) -> cudaError_t {
+    auto cp = [&](void* d, const DevBuf& b, size_t bytes, int narrow = 0) -> cudaError_t {
         if (!d || !bytes) return cudaSuccess;
-        if (!force_dma) {
+        if (!force_dma || narrow) {
             cudaPointerAttributes at{};
             if (cudaPointerGetAttributes(&at, d) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer &&
                 jobs.n < 8) {
-                jobs.j[jobs.n++] = {static_cast<const uint8_t*>(b.p), static_cast<uint8_t*>(at.devicePointer), bytes};
+                jobs.j[jobs.n++] = {static_cast<const uint8_t*>(b.p), static_cast<uint8_t*>(at.devicePointer), bytes,
+                                    narrow};
                 return cudaSuccess;
             }
             cudaGetLastError();  // unregistered host memory reports an error here: not fatal
         }
+        if (narrow) return cudaErrorInvalidValue;  // the narrowing copy needs pinned (mapped) memory
         return cudaMemcpyAsync(d, b.p, bytes, cudaMemcpyDeviceToHost, s);
     };
+    if (dst->weights_f32 && dst->weights)
+        return set_err(c, NX_INVALID_ARGUMENT, "weights and weights_f32 are exclusive");
     NX_CUDA(c, cp(dst->base, f->base, npix * 3 * sizeof(float)));
     NX_CUDA(c, cp(dst->ids, f->ids, ns * sizeof(int32_t)));
     NX_CUDA(c, cp(dst->depths, f->depths, ns * sizeof(double)));
     NX_CUDA(c, cp(dst->weights, f->weights, ns * sizeof(double)));
+    if (dst->weights_f32 && ns) {
+        const int st = cp(dst->weights_f32, f->weights, ns * sizeof(double), 1);
+        if (st == cudaErrorInvalidValue)
+            return set_err(c, NX_INVALID_ARGUMENT, "weights_f32 needs pinned (cudaHostAlloc / registered) memory");
+        NX_CUDA(c, static_cast<cudaError_t>(st));
+    }
     NX_CUDA(c, cp(dst->texture, f->texture, ns * 3 * sizeof(float)));
     NX_CUDA(c, cp(dst->final_img, f->final_img, npix * 3 * sizeof(float)));
     NX_CUDA(c, cp(dst->residual, f->residual, npix * sizeof(float)));

@@ -27,6 +27,23 @@ __global__ void __launch_bounds__(kCopyThreads) stream_copy_kernel(const CopyJob
         uint8_t* dst = jobs.j[k].dst;
         const int64_t bytes = static_cast<int64_t>(jobs.j[k].bytes);
         int64_t done = 0;
+        if (jobs.j[k].narrow) {  // fp64 -> fp32, two values per thread (16 B read, 8 B written)
+            const double* s8 = reinterpret_cast<const double*>(src);
+            float* d4 = reinterpret_cast<float*>(dst);
+            const int64_t nv = bytes / 8;
+            if (((reinterpret_cast<uintptr_t>(src) & 15) | (reinterpret_cast<uintptr_t>(dst) & 7)) == 0) {
+                const int64_t n2 = nv / 2;
+                const double2* s2 = reinterpret_cast<const double2*>(s8);
+                float2* d2 = reinterpret_cast<float2*>(d4);
+                for (int64_t i = tid; i < n2; i += nthreads) {
+                    const double2 v = __ldcs(s2 + i);
+                    __stcs(d2 + i, make_float2(static_cast<float>(v.x), static_cast<float>(v.y)));
+                }
+                done = n2 * 2;
+            }
+            for (int64_t i = done + tid; i < nv; i += nthreads) d4[i] = static_cast<float>(s8[i]);
+            continue;
+        }
         if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
             const int64_t n16 = bytes / 16;
             const int4* s4 = reinterpret_cast<const int4*>(src);

@@ -331,7 +331,8 @@ void launch_split_children(double* geom_new, int64_t n_new, const double* geom_o
 struct CopyJob {
     const uint8_t* src;  // device
     uint8_t* dst;        // device-mapped pinned host memory
-    size_t bytes;
+    size_t bytes;        // source bytes
+    int narrow;          // 1: src is fp64, dst receives it as fp32 (bytes / 2)
 };
 struct CopyJobs {
     CopyJob j[8];

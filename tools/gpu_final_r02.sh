@@ -17,3 +17,8 @@ timeout 600 ncu --set full --clock-control none --import-source on -k "regex:tex
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${T}_launches.csv \
   python bench.py --steps 5 --warmup 3 --no-cpu-baseline --train-steps 0 > gpurun_out/${T}_ncu_bench.log 2>&1
 tail -3 gpurun_out/${T}_tests.log; tail -c 400 gpurun_out/${T}_bench.log
+# summaries on the box (the full `others` report alone is ~48 MB: gpurun returns <= 64 MiB)
+python tools/ncu_table.py gpurun_out/${T}_others.ncu-rep > gpurun_out/${T}_others_table.txt 2>&1
+python tools/ncu_summary.py gpurun_out/${T}_composite.ncu-rep > gpurun_out/${T}_composite_summary.txt 2>&1
+python tools/ncu_lines.py gpurun_out/${T}_composite.ncu-rep 40 > gpurun_out/${T}_composite_lines.txt 2>&1
+rm -f gpurun_out/${T}_others.ncu-rep gpurun_out/${T}_tl1.json gpurun_out/${T}_tl2.json
