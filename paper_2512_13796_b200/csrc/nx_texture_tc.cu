@@ -1237,13 +1237,17 @@ __global__ void __launch_bounds__(kTcThreads, NX_B2_MINB) tex_mlp_bulk_kernel(co
 // layers 2 / 3 read their A operand from there: no shared-memory A buffer (~70 KB per
 // CTA, three CTAs per SM), no generic-to-async proxy fence. TMEM: accumulator columns
 // [0, 64), A hi [64, 96), A lo [96, 128).
-constexpr int kTsOffImg = kOffAh;                         // the weights, then two images
-constexpr int kTsOffRgb = kTsOffImg + 2 * kImgBytes;
+#ifndef NX_TS_SINGLE
+#define NX_TS_SINGLE 1  // one image buffer, refilled once layer 1 has read it (four CTAs per SM)
+#endif
+constexpr int kTsImgBufs = NX_TS_SINGLE ? 1 : 2;
+constexpr int kTsOffImg = kOffAh;                         // the weights, then the image buffer(s)
+constexpr int kTsOffRgb = kTsOffImg + kTsImgBufs * kImgBytes;
 constexpr int kTsOffBar = kTsOffRgb + kRows * 3 * 4;
 constexpr int kTsOffTmem = kTsOffBar + 3 * 8;
 constexpr int kTsSmem = kTsOffTmem + 8;
 constexpr uint32_t kTsTmemCols = 128;
-static_assert(kTsSmem <= 74 * 1024, "three CTAs per SM");
+static_assert(kTsSmem <= (NX_TS_SINGLE ? 56 : 74) * 1024, "four (three) CTAs per SM");
 
 __device__ __forceinline__ void ts_issue_layer(uint32_t dtm, uint32_t a_hi, uint32_t a_lo, uint8_t* smem, int off_bh,
                                                int off_bl, int K, uint32_t idesc, uint32_t bar) {
@@ -1259,7 +1263,7 @@ __device__ __forceinline__ void ts_issue_layer(uint32_t dtm, uint32_t a_hi, uint
 }
 
 #ifndef NX_TS_MINB
-#define NX_TS_MINB 3
+#define NX_TS_MINB (NX_TS_SINGLE ? 4 : 3)  // measured: single buffer x 4 CTAs 0.308 ms, two buffers x 3 0.354
 #endif
 __global__ void __launch_bounds__(kTcThreads, NX_TS_MINB) tex_mlp_ts_kernel(const TextureArgs a, int bw, int bh, int tiles_x,
                                                                    int64_t n_tiles) {
@@ -1323,9 +1327,9 @@ __global__ void __launch_bounds__(kTcThreads, NX_TS_MINB) tex_mlp_ts_kernel(cons
     int64_t k = 0;
     if (tid == 0 && blockIdx.x < n_tiles) load_tile(blockIdx.x, 0);
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
-        const int b = static_cast<int>(k & 1);
+        const int b = NX_TS_SINGLE ? 0 : static_cast<int>(k & 1);
         // the other buffer's last reader (the previous tile's layer 1) has completed
-        if (tid == 0 && tile + gridDim.x < n_tiles) load_tile(tile + gridDim.x, b ^ 1);
+        if (!NX_TS_SINGLE && tid == 0 && tile + gridDim.x < n_tiles) load_tile(tile + gridDim.x, b ^ 1);
         const WsTile wt = ws_tile(tile, row, K, bw, bh, tiles_x, W, H);
         const bool valid = wt.in_tile && a.fb.ids[wt.slot] >= 0;
         n_queries += valid;
@@ -1350,7 +1354,7 @@ __global__ void __launch_bounds__(kTcThreads, NX_TS_MINB) tex_mlp_ts_kernel(cons
                 }
             }
         }
-        mbar_wait(full(b), static_cast<uint32_t>((k >> 1) & 1));
+        mbar_wait(full(b), static_cast<uint32_t>(NX_TS_SINGLE ? (k & 1) : ((k >> 1) & 1)));
         tc_fence_after();
         const int ib = kTsOffImg + b * kImgBytes;
         if (tid == 0) b2_issue_layer(smem, tmem, ib, ib + kImgBytes / 2, kOffW1h, kOffW1l, kIn, kIdesc64, bar);
@@ -1379,6 +1383,9 @@ __global__ void __launch_bounds__(kTcThreads, NX_TS_MINB) tex_mlp_ts_kernel(cons
             tc_fence_before();
             __syncthreads();
             tc_fence_after();
+            // single buffer: layer 1 (its only reader) has completed and every thread is past
+            // this tile's wait on it (the barrier above), so the next tile's image can land
+            if (NX_TS_SINGLE && layer == 0 && tid == 0 && tile + gridDim.x < n_tiles) load_tile(tile + gridDim.x, 0);
             if (tid == 0) {
                 if (layer == 0) ts_issue_layer(tmem, tmem + 64, tmem + 96, smem, kOffW2h, kOffW2l, kHid, kIdesc64, bar);
                 else ts_issue_layer(tmem, tmem + 64, tmem + 96, smem, kOffW3h, kOffW3l, kHid, kIdesc48, bar);
@@ -1554,11 +1561,11 @@ int launch_texture_tc(const TextureArgs& a, cudaStream_t s) {
             cudaEventRecord(a.ev_mid, s);
             a.ev_mid_recorded = true;
         }
-        if (path == 5) {  // split2ts: activations in tensor memory, three CTAs per SM
+        if (path == 5) {  // split2ts: activations in tensor memory, four CTAs per SM
             cudaFuncSetAttribute(tex_mlp_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTsSmem);
             static const int per_sm = [] {  // resident decoder CTAs per SM (shared with the composite)
                 const char* e = getenv("NX_TS_CTAS_PER_SM");
-                return e ? std::max(1, atoi(e)) : 3;
+                return e ? std::max(1, atoi(e)) : NX_TS_MINB;
             }();
             const int64_t g3 = std::min<int64_t>(n_tiles, per_sm * static_cast<int64_t>(sms));
             tex_mlp_ts_kernel<<<static_cast<unsigned>(g3), kTcThreads, kTsSmem, s>>>(a, bw, bh, tiles_x, n_tiles);
