@@ -177,16 +177,54 @@ def traffic_of(stage: str):
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clocks and clock-event reasons sampled DURING the timed region. NVML is polled
+    from a host thread every 5 ms (a config-2 timed region of 20 frames lasts ~40 ms,
+    shorter than nvidia-smi's start-up, so an nvidia-smi loop would see none of it); the
+    thread is started and has taken a first sample before the region begins, and only
+    samples taken between mark() and stop() are reported. nvidia-smi is the fallback
+    when NVML is missing."""
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    PERIOD_S = 0.005
 
     def __init__(self, device: int):
-        self.device = device
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [x.strip() for x in vis.split(",") if x.strip()]
+        self.device = int(ids[device]) if device < len(ids) and ids[device].isdigit() else device
         self.proc = None
+        self.thread = None
         self.path = os.path.join("/tmp", f"nx_clocks_{os.getpid()}.csv")
 
     def start(self):
+        try:
+            import threading
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            self.samples, self.t_mark, self.done = [], None, threading.Event()
+            first = threading.Event()
+
+            def poll():
+                while not self.done.is_set():
+                    t = time.perf_counter()
+                    mhz = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((t, mhz, sorted(k for k, b in bits.items() if r & b)))
+                    first.set()
+                    self.done.wait(self.PERIOD_S)
+
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            first.wait(2.0)
+            return
+        except Exception:
+            self.thread = None
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -195,7 +233,26 @@ class ClockSampler:
         except (OSError, FileNotFoundError):
             self.proc = None
 
+    def mark(self):
+        """The timed region starts now."""
+        self.t_mark = time.perf_counter()
+
     def stop(self):
+        if self.thread is not None:
+            t_end = time.perf_counter()
+            self.done.set()
+            self.thread.join(timeout=2)
+            t0 = self.t_mark if self.t_mark is not None else 0.0
+            inside = [x for x in self.samples if t0 <= x[0] <= t_end]
+            if not inside:  # region shorter than one period: the samples either side of it
+                before = [x for x in self.samples if x[0] < t0][-1:]
+                after = [x for x in self.samples if x[0] > t_end][:1]
+                inside = before + after
+            if not inside:
+                return None
+            reasons = sorted({r for x in inside for r in x[2]})
+            return {"sm_mhz": statistics.median(x[1] for x in inside), "sm_max_mhz": self.max_mhz,
+                    "reasons": reasons, "samples": len(inside), "source": "NVML, 5 ms period, timed region only"}
         if not self.proc:
             return None
         self.proc.terminate()
@@ -221,7 +278,8 @@ class ClockSampler:
                         reasons.add(nm)
         if not sm:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvidia-smi -lms 20"}
 
 
 # ---------------------------------------------------------------- distributed plumbing
@@ -555,6 +613,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    clocks.mark()
     ev0.record(stream)
     if world > 1:
         # views dealt from one atomic counter shared by the ranks (views.DynamicDealer: the
@@ -765,6 +824,7 @@ def run_config4(args):
     barrier(dist)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.mark()
     e0.record(stream)
     for s in range(args.warmup, n_steps):
         r.render(ds, cams[s], frames[s % 2])
