@@ -67,16 +67,39 @@ __device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
 }
 
 // Exclusive prefix of `agg` over the blocks before `b` by decoupled look-back on
-// status[0..b) (stride `stride` between consecutive blocks' words). One thread.
+// status[0..b) (stride `stride` between consecutive blocks' words). One thread. The
+// words of kLookBatch predecessors are loaded together (independent loads in flight),
+// then consumed in order: a chain of b aggregates costs ~b / kLookBatch L2 round trips
+// instead of b (all blocks publish their aggregates at about the same time, so without
+// the batch the last block walks the whole chain one dependent load at a time).
+#ifndef NX_LOOK_BATCH
+#define NX_LOOK_BATCH 8
+#endif
+constexpr int kLookBatch = NX_LOOK_BATCH;
 __device__ __forceinline__ uint32_t look_back(const uint64_t* status, int64_t stride, int b) {
     uint32_t run = 0;
-    for (int p = b - 1; p >= 0;) {
-        const uint64_t w = ld_status(status + p * stride);
-        const uint32_t flag = static_cast<uint32_t>(w >> 32);
-        if (flag == 0) continue;  // predecessor not published yet (it is running: ticket order)
-        run += static_cast<uint32_t>(w);
-        if (flag == kFlagIncl) break;
-        --p;
+    int p = b - 1;
+    while (p >= 0) {
+        uint64_t w[kLookBatch];
+#pragma unroll
+        for (int i = 0; i < kLookBatch; ++i) w[i] = p - i >= 0 ? ld_status(status + (p - i) * stride) : 0ull;
+        int used = 0;
+        bool done = false;
+#pragma unroll
+        for (int i = 0; i < kLookBatch; ++i) {
+            if (done || used < i) continue;  // stopped at an earlier word
+            if (p - i < 0) {
+                done = true;
+                continue;
+            }
+            const uint32_t flag = static_cast<uint32_t>(w[i] >> 32);
+            if (flag == 0) continue;  // not published yet (it is running: ticket order): reload from here
+            run += static_cast<uint32_t>(w[i]);
+            used = i + 1;
+            if (flag == kFlagIncl) done = true;
+        }
+        if (done) break;
+        p -= used;
     }
     return run;
 }
