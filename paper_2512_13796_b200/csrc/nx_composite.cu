@@ -647,21 +647,27 @@ __global__ void __launch_bounds__(kThreads, kCert ? NX_COMPOSITE_MINB : 10) comp
 template <int K, bool kDebug>
 __global__ void __launch_bounds__(256) redo_pixels_kernel(const CompositeArgs a) {
     constexpr int KK = K > 0 ? K : 1;
+    // One CTA per redo pixel: the 256 threads intersect 256 list entries at a time (the
+    // exact fp64 hit, SH for the hits), the hits are compacted in list order into shared
+    // memory and thread 0 marches them exactly like the collection pass. The per-pixel
+    // chain is one L2 round trip per 256 entries instead of per 32 (a few hundred redo
+    // pixels per frame, each a dense tile's list of ~1000 entries).
     struct Hits {
-        double alpha[32], t[32];
-        float rgb[32][3];
-        int32_t id[32];
+        double alpha[256], t[256];
+        float rgb[256][3];
+        int32_t id[256];
     };
-    __shared__ Hits hs[8];
+    __shared__ Hits h;
+    __shared__ int s_wc[8];
+    __shared__ int s_active;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    Hits& h = hs[warp];
     const int n = *a.redo;
     if (blockIdx.x == 0 && threadIdx.x == 0) a.stats->redo_tiles = static_cast<unsigned long long>(n);
     const int W = a.cam.W;
     const double near_eps = a.st.near_eps, alpha_max = a.st.alpha_max, min_T = a.st.min_transmittance;
     const double2* rec2 = reinterpret_cast<const double2*>(a.rec);
     uint32_t n_near = 0;
-    for (int i = blockIdx.x * 8 + warp; i < n; i += gridDim.x * 8) {
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
         const int64_t pix = a.redo[1 + i];
         const int px = static_cast<int>(pix % W), py = static_cast<int>(pix / W);
         const int t = (py / kWorkTile) * a.fb.tiles_x + px / kWorkTile;
@@ -686,8 +692,8 @@ __global__ void __launch_bounds__(256) redo_pixels_kernel(const CompositeArgs a)
         bool active = true;
         const bool dbg_row = kDebug && py >= a.dbg_y0 && py < a.dbg_y1;
         const int64_t dbg_q = kDebug ? (static_cast<int64_t>(py - a.dbg_y0) * W + px) : 0;
-        for (int cb = list_begin; cb < list_end && active; cb += 32) {
-            const int e = cb + lane;
+        for (int cb = list_begin; cb < list_end && active; cb += 256) {
+            const int e = cb + static_cast<int>(threadIdx.x);
             bool hit = false;
             double al = 0.0, tt = 0.0;
             float rgb[3] = {0.f, 0.f, 0.f};
@@ -716,8 +722,17 @@ __global__ void __launch_bounds__(256) redo_pixels_kernel(const CompositeArgs a)
                 }
             }
             const uint32_t m = __ballot_sync(0xffffffffu, hit);
+            if (lane == 0) s_wc[warp] = __popc(m);
+            __syncthreads();
+            int off = 0, nh = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                const int c = s_wc[w];
+                off += w < warp ? c : 0;
+                nh += c;
+            }
             if (hit) {
-                const int k = __popc(m & ((1u << lane) - 1u));
+                const int k = off + __popc(m & ((1u << lane) - 1u));
                 h.alpha[k] = al;
                 h.t[k] = tt;
                 h.rgb[k][0] = rgb[0];
@@ -725,9 +740,8 @@ __global__ void __launch_bounds__(256) redo_pixels_kernel(const CompositeArgs a)
                 h.rgb[k][2] = rgb[2];
                 h.id[k] = id;
             }
-            __syncwarp();
-            if (lane == 0) {
-                const int nh = __popc(m);
+            __syncthreads();
+            if (threadIdx.x == 0) {
                 for (int k = 0; k < nh && active; ++k) {
                     const double alpha = alpha_max < h.alpha[k] ? alpha_max : h.alpha[k];
                     const double wgt = alpha * T;
@@ -770,11 +784,12 @@ __global__ void __launch_bounds__(256) redo_pixels_kernel(const CompositeArgs a)
                     if (T < min_T) active = false;
                     n_near += fabs(T - min_T) <= kNearRel * min_T ? (1u << 10) : 0u;
                 }
+                s_active = active;
             }
-            active = __shfl_sync(0xffffffffu, active, 0);
-            __syncwarp();
+            __syncthreads();
+            active = s_active;
         }
-        if (lane == 0) {  // the exact pass's epilogue (renderer.cpp:155-164, framebuffers.hpp:51-56)
+        if (threadIdx.x == 0) {  // the exact pass's epilogue (renderer.cpp:155-164, framebuffers.hpp:51-56)
             a.fb.residual[pix] = static_cast<float>(T);
             if (a.fb.residual64) a.fb.residual64[pix] = T;
             acc[0] += T * a.st.background[0];
@@ -832,7 +847,7 @@ __global__ void __launch_bounds__(256) redo_pixels_kernel(const CompositeArgs a)
                 for (int ii = dbg_n; ii < a.dbg_max; ++ii) a.dbg_hits[dbg_q * a.dbg_max + ii] = -1;
             }
         }
-        __syncwarp();
+        __syncthreads();
     }
     if (kNear && n_near) {
         if (n_near & 1023u) atomicAdd(&a.stats->near[NEAR_ALPHA], static_cast<unsigned long long>(n_near & 1023u));
@@ -861,7 +876,7 @@ void launch_one(const CompositeArgs& a, unsigned grid, cudaStream_t s) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t npix = static_cast<int64_t>(a.cam.W) * a.cam.H;
-        const unsigned rgrid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((npix + 7) / 8, sms * 4)));
+        const unsigned rgrid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(npix, sms * 4)));
         count_launch();
         redo_pixels_kernel<K, kDebug><<<rgrid, 256, 0, s>>>(a);  // the exact redo of those pixels
     } else {

@@ -21,6 +21,8 @@ constexpr int kRadixTile = NX_RADIX_TILE;  // items per block per pass (look-bac
 // knob (smaller tiles = more blocks and shorter ranking chains, measured no faster)
 #ifndef NX_RADIX_TILE64
 #define NX_RADIX_TILE64 2048  // measured at config 2: 2048 473.3, 1024 471.2, 512 469.7, 256 462.8 frames/s
+// (again with the batched look-back: 2048 488.5, 1024 485.3, 512 479.7; 32-bit tile
+// 4096 489.1, 1024 482.4; look-back batch 16 483.6 vs 8)
 #endif
 constexpr int kRadixTile64 = NX_RADIX_TILE64;
 constexpr int kRadixBits = 8;

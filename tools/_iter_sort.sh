@@ -1,7 +1,7 @@
 #!/bin/bash
 # binning parity + bench stage times after a sort change
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_binning.py tests/test_gpu_parity.py -m gpu -q -x 2>&1 | tail -3
+timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
 for rep in 1 2; do
   timeout 600 python bench.py --steps 200 --warmup 5 --no-cpu-baseline --train-steps 0 > /tmp/b.log 2>&1
   python -c "
