@@ -50,8 +50,17 @@ constexpr int kShPieces = NX_SH_VALUES * 4 / 16; // 16-byte pieces of the SH coe
 // Staged rows are padded by 16 bytes (208-byte stride): the B1 lanes of a warp read up
 // to kSub different rows at once, and at the unpadded 192-byte stride rows 0 / 2 and
 // 1 / 3 fall on the same banks (two-way conflicts on every record and SH load).
-constexpr int kRecStride = REC_FIELDS + 2;
-constexpr int kShStride = NX_SH_VALUES + 4;
+// Measured at config 2 (composite stage ms / frames/s): padded 1.036 / 488; no padding
+// (12 CTAs / SM fit) 1.123 / 469; no record padding with kSub 3 at 12 CTAs 1.107 / 481;
+// kSub 3 padded at 12 CTAs 1.055 / 486.
+#ifndef NX_REC_PAD
+#define NX_REC_PAD 2
+#endif
+#ifndef NX_SH_PAD
+#define NX_SH_PAD 4
+#endif
+constexpr int kRecStride = REC_FIELDS + NX_REC_PAD;
+constexpr int kShStride = NX_SH_VALUES + NX_SH_PAD;
 static_assert(kWorkTile == 8, "warp blocks are 8x4 pixels");
 #ifndef NX_NEAR_COUNTERS
 #define NX_NEAR_COUNTERS 1
