@@ -920,7 +920,7 @@ __global__ void __launch_bounds__(WsCfg<kMode>::kThreads, 1)
 // split into bf16 hi / lo and stored as the tile's K-major operand image (16 KB per
 // 128-row tile: hi then lo), at the (tile, row) texture_ws_kernel<kBulk> assigns the slot.
 #ifndef NX_FEAT_MINB
-#define NX_FEAT_MINB 6  // 80 registers, 6 CTAs per SM (measured: 2.257 -> 2.250 ms per frame)
+#define NX_FEAT_MINB 6  // 80 registers, 6 CTAs per SM (measured: 2.257 -> 2.250 ms per frame; final build: 5 481.8, 6 488.5, 8 470.5 frames/s)
 #endif
 #ifdef NX_FEAT_MINB
 #define NX_FEAT_BOUNDS __launch_bounds__(128, NX_FEAT_MINB)
@@ -1263,7 +1263,7 @@ __device__ __forceinline__ void ts_issue_layer(uint32_t dtm, uint32_t a_hi, uint
 }
 
 #ifndef NX_TS_MINB
-#define NX_TS_MINB (NX_TS_SINGLE ? 4 : 3)  // measured: single buffer x 4 CTAs 0.308 ms, two buffers x 3 0.354
+#define NX_TS_MINB (NX_TS_SINGLE ? 4 : 3)  // measured: single buffer x 4 CTAs 0.308 ms, two buffers x 3 0.354 (5: 0.46, 453 frames/s)
 #endif
 __global__ void __launch_bounds__(kTcThreads, NX_TS_MINB) tex_mlp_ts_kernel(const TextureArgs a, int bw, int bh, int tiles_x,
                                                                    int64_t n_tiles) {
