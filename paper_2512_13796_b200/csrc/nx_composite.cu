@@ -37,7 +37,10 @@ namespace {
 constexpr int kThreads = kWorkTile * kWorkTile;  // 64: one thread per pixel of the work tile
 constexpr int kWarps = kThreads / 32;
 #ifndef NX_COMPOSITE_CHUNK
-#define NX_COMPOSITE_CHUNK 64
+// 48: the certified CTA drops to ~17.4 KB of shared memory and 12 CTAs fit per SM (work
+// lists average ~63 primitives per 8x8 tile). Measured (frames/s, 200 frames): 32 at 12
+// CTAs 484.0, 48 at 12 CTAs 489.8, 64 at 11 CTAs 487.2, 96 at 10 CTAs 476.4.
+#define NX_COMPOSITE_CHUNK 48
 #endif
 #ifndef NX_COMPOSITE_SUB
 #define NX_COMPOSITE_SUB 4
@@ -184,7 +187,7 @@ __device__ __forceinline__ void eval_sh_smem(const float* sh, float x, float y, 
 
 template <int K, bool kDebug, typename CT, bool kCert>
 #ifndef NX_COMPOSITE_MINB
-#define NX_COMPOSITE_MINB 11  // certified pass, measured (packed entries): 10 1.076 ms, 11 1.059, 12 1.061
+#define NX_COMPOSITE_MINB 12  // certified pass, measured (packed entries, chunk 64): 10 1.076 ms, 11 1.059, 12 1.061; chunk 48: 12
 #endif
 // (the exact-path variants keep 10: their larger pool entries fit 10 CTAs of shared memory anyway)
 __global__ void __launch_bounds__(kThreads, kCert ? NX_COMPOSITE_MINB : 10) composite_kernel(const CompositeArgs a) {
