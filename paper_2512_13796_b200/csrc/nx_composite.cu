@@ -39,7 +39,8 @@ constexpr int kWarps = kThreads / 32;
 #ifndef NX_COMPOSITE_CHUNK
 // 48: the certified CTA drops to ~17.4 KB of shared memory and 12 CTAs fit per SM (work
 // lists average ~63 primitives per 8x8 tile). Measured (frames/s, 200 frames): 32 at 12
-// CTAs 484.0, 48 at 12 CTAs 489.8, 64 at 11 CTAs 487.2, 96 at 10 CTAs 476.4.
+// CTAs 484.0, 40 at 12 CTAs 486.0, 48 at 12 CTAs 489.8, 64 at 11 CTAs 487.2, 96 at 10 CTAs
+// 476.4; kSub 3 at 13 CTAs (78 registers) 468 with chunk 48, 478 with chunk 32.
 #define NX_COMPOSITE_CHUNK 48
 #endif
 #ifndef NX_COMPOSITE_SUB
