@@ -113,7 +113,7 @@ def composite_compute_roofline(comp_ms, sm_mhz):
     return {"bound": "issue", "kernel": "composite (certified fp32 alpha)", "achieved": ginst, "peak": peak,
             "unit": "G warp-instructions/s", "frac": ginst / peak, "warp_inst_per_launch": c["warp_inst"],
             "launch_ms": comp_ms, "fp64": fp64,
-            "note": "ncu: issue slots 64 % busy, 31 % occupancy (80 registers, 11 CTAs / SM, shared-memory bound); the HBM figure in "
+            "note": "ncu: issue slots 65 % busy, 33 % occupancy (80 registers, 12 CTAs / SM, register and shared-memory bound); the HBM figure in "
                     "`roofline` is kept for the contract"}
 
 
